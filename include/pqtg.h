@@ -1,0 +1,199 @@
+/*
+ * pqtg.h — C ABI of the B200 (sm_100a) query path for the Product Quantization Tree.
+ *
+ * This is the drop-in boundary. Plain pointers and sizes only; no C++ or torch types.
+ * Each entry point names the reference interface it replaces (paths relative to
+ * the reference checkout, proj/…):
+ *
+ *   pqtg_index_load          ← pqt::load_index            include/pqt/index_io.hpp:16, src/index_io.cpp:148-229
+ *   pqtg_index_create        ← constructing pqt::PqtIndex  include/pqt/search.hpp:34-47 (build_index /
+ *                              IndexBuilder::finalize output, src/search.cpp:93-124)
+ *   pqtg_search              ← pqt::knn_query_batch        include/pqt/search.hpp:83, src/search.cpp:262-274
+ *                              (each row = pqt::knn_query, src/search.cpp:126-260)
+ *   pqtg_search_device       ← same, device-resident inputs/outputs on a caller stream
+ *   pqtg_merge_topk_host     ← no reference counterpart: merges per-shard top-k lists by the
+ *                              reference's (dist, id) order (candidate_less, src/search.cpp:39-41)
+ *
+ * Errors: every int-returning call returns PQTG_OK (0) or a negative pqtg_status; the message
+ * is available from pqtg_last_error() (thread-local). The C++ drop-in (include/pqt/) maps
+ * PQTG_ERR_BAD_DIM / PQTG_ERR_CONFIG to std::invalid_argument and PQTG_ERR_FORMAT to
+ * pqt::FormatError, like the reference (src/search.cpp:264-266, src/codebook.cpp:15-35,
+ * src/index_io.cpp:28-42,155-165,211-213).
+ *
+ * There is no CPU fallback: configurations the GPU path does not implement (p_tree not in
+ * {1,2,4}, or slope tables missing so the reference would use its exact Dijkstra order,
+ * src/binorder.cpp:242-244) return PQTG_ERR_UNSUPPORTED.
+ */
+#ifndef PQTG_H
+#define PQTG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQTG_ABI_VERSION 1
+
+typedef enum pqtg_status {
+    PQTG_OK = 0,
+    PQTG_ERR_BAD_DIM = -1,      /* query dim != index dim (search.cpp:264-266) */
+    PQTG_ERR_CONFIG = -2,       /* PqtConfig::validate failure (codebook.cpp:15-35) */
+    PQTG_ERR_FORMAT = -3,       /* malformed PQTINDEX container (index_io.cpp) */
+    PQTG_ERR_UNSUPPORTED = -4,  /* valid for the reference, not implemented on the GPU path */
+    PQTG_ERR_OOM = -5,
+    PQTG_ERR_CUDA = -6,
+    PQTG_ERR_ARG = -7,          /* null pointer / bad size from the caller */
+    PQTG_ERR_NCCL = -8
+} pqtg_status;
+
+/* Mirrors pqt::PqtConfig (include/pqt/codebook.hpp:12-36) field for field.
+ * hash_size is the RESOLVED slot count H (search.cpp:106 stores it resolved). */
+typedef struct pqtg_config {
+    uint32_t dim;
+    uint32_t p_tree;
+    uint32_t k1;
+    uint32_t k2;
+    uint32_t w;
+    uint32_t p_line;
+    uint64_t hash_size;
+    uint32_t candidate_budget;
+    uint32_t rerank_exact;
+    uint32_t resort_bins;       /* bool in the reference; 0/1 here */
+    uint32_t train_iters;
+    uint64_t seed;
+} pqtg_config;
+
+/* Borrowed host view of everything pqt::PqtIndex holds that the query path reads
+ * (include/pqt/search.hpp:34-47). Array layouts are the reference's in-memory layouts:
+ *   level1      p_tree × k1 × m            (TreeCodebooks::level1[p].centroids, concatenated)
+ *   level2      p_tree × k1 × k2 × m       (TreeCodebooks::level2[p][i].centroids, concatenated)
+ *   d2          p_line × k1 × k1           (PairDistanceTable::d2 — as stored in the index file)
+ *   tables      table_count × table_len × (a, b)  plus one slope per table (OrderTable)
+ *   offsets     hash_size + 1              (InvertedLists::offsets)
+ *   ids         n                          (InvertedLists::ids)
+ *   lambda_q    n × p_line                 (LineCodes::lambda_q, vector-id order)
+ *   pair_id     n × p_line                 (LineCodes::pair_id, vector-id order)
+ * m = dim / p_tree.
+ *
+ * shard_lo/shard_hi select the range of inverted-list POSITIONS (indices into ids[]) whose
+ * line codes this device holds and re-ranks; 0/0 means all of [0, n). Traversal and bin
+ * selection always run over the full replicated offsets, so bins_visited / candidates stay
+ * global and per-shard top-k lists merge bit-exactly (pqtg_merge_topk_host). */
+typedef struct pqtg_index_view {
+    pqtg_config config;
+    uint64_t n;
+    const float* level1;
+    const float* level2;
+    const float* d2;
+    uint32_t table_count;
+    uint32_t table_len;
+    const double* table_slopes;
+    const uint32_t* table_entries;
+    const uint64_t* offsets;
+    const uint32_t* ids;
+    const uint8_t* lambda_q;
+    const uint16_t* pair_id;
+    uint64_t shard_lo;
+    uint64_t shard_hi;
+} pqtg_index_view;
+
+/* Per-query counters of pqt::QueryStats (include/pqt/search.hpp:15-23). The reference's
+ * *_us wall-clock timers have no per-query meaning on a batched GPU; per-stage batch times
+ * come from pqtg_workspace_stage_ms. exact_evals is 0 (no raw vectors on device, as for an
+ * index from load_index, search.cpp:229-238). */
+typedef struct pqtg_query_stats {
+    uint64_t bins_visited;
+    uint64_t candidates;
+    uint64_t exact_evals;
+} pqtg_query_stats;
+
+typedef struct pqtg_index_info {
+    pqtg_config config;
+    uint64_t n;
+    uint64_t shard_lo, shard_hi;
+    uint32_t list_len;          /* W = w * k2, entries per part in the level-2 list */
+    uint32_t pair_count;        /* k1(k1-1)/2, or 1 when k1 == 1 */
+    uint32_t pair_width;        /* 1 or 2 bytes per stored pair id (index_io.cpp:132) */
+    uint32_t code_row_bytes;    /* device bytes per line-code row (slot order) */
+    uint64_t device_bytes;      /* device memory owned by the index */
+    int device;
+} pqtg_index_info;
+
+typedef struct pqtg_index pqtg_index;
+typedef struct pqtg_workspace pqtg_workspace;
+
+/* ---- library ---------------------------------------------------------------------- */
+int pqtg_abi_version(void);
+const char* pqtg_last_error(void);
+/* 1 when a CUDA device with compute capability 10.x is usable, else 0. */
+int pqtg_device_ok(int device);
+
+/* ---- index ------------------------------------------------------------------------ */
+/* Copy a host index view to `device` (re-laid out for the kernels; the caller keeps
+ * ownership of the view arrays). Validates like PqtConfig::validate. */
+int pqtg_index_create(const pqtg_index_view* view, int device, pqtg_index** out);
+/* Parse a PQTINDEX v1 file (index_io.cpp:148-229 format) and upload it; shard_lo/hi as in
+ * the view (0/0 = whole index). */
+int pqtg_index_load(const char* path, int device, uint64_t shard_lo, uint64_t shard_hi,
+                    pqtg_index** out);
+int pqtg_index_info_get(const pqtg_index* index, pqtg_index_info* out);
+void pqtg_index_destroy(pqtg_index* index);
+
+/* ---- workspace (per stream; not shared by concurrent searches) -------------------- */
+int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_workspace** out);
+void pqtg_workspace_destroy(pqtg_workspace* ws);
+/* Device milliseconds of the last pqtg_search* call per stage: [0] traversal, [1] bin
+ * selection + gather, [2] re-rank + top-k, [3] whole search. Synchronises the last stream. */
+int pqtg_workspace_stage_ms(pqtg_workspace* ws, float* ms4);
+/* Copy per-query intermediates of the LAST sub-batch searched with `ws` to host buffers
+ * (any pointer may be NULL). Used by the per-stage parity tests.
+ *   fine         nq × p_line × k1              traversal fine_dists (pqtree.cpp:84-97)
+ *   l2_code      nq × p_tree × W  (parent << 16 | child)   sorted level-2 lists (pqtree.cpp:102-117)
+ *   l2_dist      nq × p_tree × W
+ *   slope        nq × 2           picked slope-table indices (binorder.cpp:52-65)
+ *   positions    nq × budget      gathered candidate positions (search.cpp:166-217), in order
+ *   ncand        nq               candidates gathered (global count)            */
+int pqtg_workspace_read(pqtg_workspace* ws, uint64_t nq, float* fine, uint32_t* l2_code,
+                        float* l2_dist, uint8_t* slope, uint32_t* positions, uint32_t* ncand);
+
+/* ---- search ----------------------------------------------------------------------- */
+/* Host buffers (copied in and out inside the call); synchronous. Outputs are nq × k
+ * row-major; counts[q] = min(k, candidates) valid entries (the reference's short results,
+ * search.cpp:251). stats may be NULL. dim must equal the index dim (else BAD_DIM). */
+int pqtg_search(pqtg_index* index, pqtg_workspace* ws, const float* queries, uint64_t nq,
+                uint32_t dim, uint32_t k, uint32_t* ids, float* dists, uint32_t* counts,
+                pqtg_query_stats* stats);
+/* Device pointers, asynchronous on `stream` (a cudaStream_t; NULL = legacy default).
+ * nq must be <= the workspace max_batch. */
+int pqtg_search_device(pqtg_index* index, pqtg_workspace* ws, const float* d_queries,
+                       uint64_t nq, uint32_t k, uint32_t* d_ids, float* d_dists,
+                       uint32_t* d_counts, pqtg_query_stats* d_stats, void* stream);
+
+/* Host twin of the kernels' bin-order addressing (test hook; needs no GPU). Materializes the
+ * static slope-table streams of `view` exactly as the device index does and writes the first
+ * max_tuples rank tuples (p_tree entries each) of the heuristic order for the sorted per-part
+ * lists `lists` (p_tree × w·k2) — BinStream (binorder.cpp:178-283). The slope pick here uses
+ * the host libm (the GPU uses CUDA's fp64 log). Returns the tuple count or a negative status. */
+int64_t pqtg_bin_stream_host(const pqtg_index_view* view, const float* lists, uint64_t max_tuples,
+                             uint32_t* out);
+
+/* ---- multi-GPU helpers ------------------------------------------------------------ */
+/* Merge G per-shard top-k lists (each nq × k, counts per query) into the global top-k by
+ * ascending (dist, id). Host-side; inputs laid out shard-major: ids[g][q][k]. */
+int pqtg_merge_topk_host(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids,
+                         const float* dists, const uint32_t* counts, uint32_t* out_ids,
+                         float* out_dists, uint32_t* out_counts);
+/* Same on device, asynchronous on `stream`. */
+int pqtg_merge_topk_device(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* d_ids,
+                           const float* d_dists, const uint32_t* d_counts, uint32_t* d_out_ids,
+                           float* d_out_dists, uint32_t* d_out_counts, void* stream);
+/* Even split of [0, n) into `shards` position ranges (the shard_lo/shard_hi to pass). */
+int pqtg_shard_range(uint64_t n, uint32_t shards, uint32_t rank, uint64_t* lo, uint64_t* hi);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PQTG_H */

@@ -1,0 +1,70 @@
+"""In-tree build of libpqtg.so for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_1702_05911_b200.build        # or __graft_entry__.build()
+
+Output: paper_1702_05911_b200/_build/libpqtg.so (git-ignored; travels to the GPU box).
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT = PKG / "_build"
+LIB = OUT / "libpqtg.so"
+REPO = PKG.parent
+
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# -fmad=false: belt and braces — every exact fp32 op is already an explicit __f*_rn intrinsic.
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
+              "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+CU_SOURCES = ["kernels.cu"]
+CXX_SOURCES = ["api.cpp", "index_prep.cpp", "pqt_dropin.cpp"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("build failed: " + " ".join(cmd))
+    return r.stdout + r.stderr
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    OUT.mkdir(exist_ok=True)
+    headers = list(CSRC.glob("*.h")) + list((REPO / "include").rglob("*.h*"))
+    objs = []
+    for src in CU_SOURCES + CXX_SOURCES:
+        path = CSRC / src
+        if not path.exists():
+            continue
+        obj = OUT / (src + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [path, *headers, Path(__file__)]):
+            cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-I", str(REPO / "include"), "-c", str(path), "-o", str(obj)]
+            if src.endswith(".cpp"):
+                cmd[1:1] = ["-x", "cu"] if False else []
+            out = _run(cmd)
+            if verbose and out.strip():
+                print(out)
+    if force or _stale(LIB, objs):
+        out = _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread"])
+        if verbose and out.strip():
+            print(out)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose=True, force="--force" in sys.argv))

@@ -1,0 +1,532 @@
+// api.cpp — the C ABI (include/pqtg.h): index lifecycle, PQTINDEX v1 loader, workspaces and
+// the search orchestration (K1 traverse → K3 bin selection/gather → K5 re-rank/top-k).
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pqtg_internal.h"
+
+namespace pqtg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+Workspace::~Workspace() {
+    if (index) cudaSetDevice(index->device);
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    if (own_stream) cudaStreamDestroy(own_stream);
+    for (void* p : allocations) cudaFree(p);
+}
+
+namespace {
+
+template <class F>
+int guarded(F&& fn) {
+    try {
+        return fn();
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_error("host out of memory");
+        return PQTG_ERR_OOM;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return PQTG_ERR_ARG;
+    }
+}
+
+// ---- PQTINDEX v1 (src/index_io.cpp:94-229). Fields are packed little-endian; every array
+// starts at an unaligned offset (73-byte header), so arrays are memcpy'd out of the map.
+struct MappedFile {
+    const uint8_t* base = nullptr;
+    size_t size = 0;
+    int fd = -1;
+    ~MappedFile() {
+        if (base) munmap(const_cast<uint8_t*>(base), size);
+        if (fd >= 0) close(fd);
+    }
+};
+
+struct Cursor {
+    const uint8_t* p;
+    size_t left;
+    std::string path;
+    const uint8_t* take(size_t n) {
+        if (n > left) throw Error{PQTG_ERR_FORMAT, path + ": truncated index file"};
+        const uint8_t* r = p;
+        p += n;
+        left -= n;
+        return r;
+    }
+    template <class T>
+    T pod() {
+        T v;
+        std::memcpy(&v, take(sizeof(T)), sizeof(T));
+        return v;
+    }
+    template <class T>
+    void vec(std::vector<T>& v, size_t count) {
+        v.resize(count);
+        if (count) std::memcpy(v.data(), take(count * sizeof(T)), count * sizeof(T));
+    }
+};
+
+struct LoadedFile {
+    MappedFile map;
+    Source src;
+    std::vector<float> level1, level2, d2;
+    std::vector<double> slopes;
+    std::vector<uint32_t> entries, ids;
+    std::vector<uint64_t> offsets;
+};
+
+void parse_index(const char* path, LoadedFile& lf) {
+    lf.map.fd = open(path, O_RDONLY);
+    if (lf.map.fd < 0) throw Error{PQTG_ERR_FORMAT, std::string("cannot open ") + path + " for reading"};
+    struct stat st {};
+    fstat(lf.map.fd, &st);
+    lf.map.size = (size_t)st.st_size;
+    if (lf.map.size > 0) {
+        void* m = mmap(nullptr, lf.map.size, PROT_READ, MAP_PRIVATE, lf.map.fd, 0);
+        if (m == MAP_FAILED) throw Error{PQTG_ERR_FORMAT, std::string("mmap failed for ") + path};
+        lf.map.base = static_cast<const uint8_t*>(m);
+        madvise(m, lf.map.size, MADV_SEQUENTIAL);
+    }
+    Cursor cur{lf.map.base, lf.map.size, path};
+    const uint8_t* magic = lf.map.size >= 8 ? cur.take(8) : nullptr;
+    if (!magic || std::memcmp(magic, "PQTINDEX", 8) != 0)
+        throw Error{PQTG_ERR_FORMAT, std::string(path) + ": bad index magic, expected \"PQTINDEX\""};
+    const uint32_t version = cur.pod<uint32_t>();
+    if (version != 1)
+        throw Error{PQTG_ERR_FORMAT, std::string(path) + ": unsupported index version " + std::to_string(version) +
+                                         ", expected 1"};
+    Source& s = lf.src;
+    pqtg_config& c = s.cfg;
+    c.dim = cur.pod<uint32_t>();
+    c.p_tree = cur.pod<uint32_t>();
+    c.k1 = cur.pod<uint32_t>();
+    c.k2 = cur.pod<uint32_t>();
+    c.w = cur.pod<uint32_t>();
+    c.p_line = cur.pod<uint32_t>();
+    c.hash_size = cur.pod<uint64_t>();
+    c.candidate_budget = cur.pod<uint32_t>();
+    c.rerank_exact = cur.pod<uint32_t>();
+    c.resort_bins = cur.pod<uint8_t>() ? 1u : 0u;
+    c.train_iters = cur.pod<uint32_t>();
+    c.seed = cur.pod<uint64_t>();
+    validate_config(c);
+    s.n = cur.pod<uint64_t>();
+    const uint32_t P = c.p_tree, k1 = c.k1, k2 = c.k2, m = c.dim / P;
+    lf.level1.resize((size_t)P * k1 * m);
+    lf.level2.resize((size_t)P * k1 * k2 * m);
+    for (uint32_t b = 0; b < P + P * k1; ++b) {
+        const uint32_t pd = cur.pod<uint32_t>(), kk = cur.pod<uint32_t>();
+        const bool lvl1 = b < P;
+        if (pd != m || kk != (lvl1 ? k1 : k2))
+            throw Error{PQTG_ERR_FORMAT, std::string(path) + ": codebook shape does not match config"};
+        float* dst = lvl1 ? lf.level1.data() + (size_t)b * k1 * m : lf.level2.data() + (size_t)(b - P) * k2 * m;
+        std::memcpy(dst, cur.take((size_t)pd * kk * 4), (size_t)pd * kk * 4);
+    }
+    cur.vec(lf.d2, (size_t)c.p_line * k1 * k1);
+    const uint32_t tc = cur.pod<uint32_t>(), tl = cur.pod<uint32_t>();
+    lf.slopes.resize(tc);
+    lf.entries.resize((size_t)tc * tl * 2);
+    for (uint32_t t = 0; t < tc; ++t) {
+        lf.slopes[t] = cur.pod<double>();
+        if (tl) std::memcpy(lf.entries.data() + (size_t)t * tl * 2, cur.take((size_t)tl * 8), (size_t)tl * 8);
+    }
+    cur.vec(lf.offsets, c.hash_size + 1);
+    cur.vec(lf.ids, s.n);
+    const uint8_t pw = cur.pod<uint8_t>();
+    if (pw != 1 && pw != 2)
+        throw Error{PQTG_ERR_FORMAT, std::string(path) + ": invalid line-code pair width " + std::to_string(pw)};
+    s.records = cur.take((size_t)s.n * c.p_line * (1 + pw));
+    s.record_pw = pw;
+    s.level1 = lf.level1.data();
+    s.level2 = lf.level2.data();
+    s.d2 = lf.d2.data();
+    s.table_count = tc;
+    s.table_len = tl;
+    s.slopes = lf.slopes.data();
+    s.entries = lf.entries.data();
+    s.offsets = lf.offsets.data();
+    s.ids = lf.ids.data();
+}
+
+void ensure_staging(Workspace& ws, uint64_t k) {
+    const DevParams& p = ws.index->prm;
+    if (!ws.d_queries) {
+        ws.d_queries = dev_alloc<float>(ws.allocations, ws.max_batch * p.D);
+        ws.d_counts = dev_alloc<uint32_t>(ws.allocations, ws.max_batch);
+        ws.d_stats = dev_alloc<pqtg_query_stats>(ws.allocations, ws.max_batch);
+    }
+    if (k > ws.stage_k) {
+        // grow: old buffers stay owned by the workspace until it is destroyed
+        ws.d_ids = dev_alloc<uint32_t>(ws.allocations, ws.max_batch * k);
+        ws.d_dists = dev_alloc<float>(ws.allocations, ws.max_batch * k);
+        ws.stage_k = k;
+    }
+}
+
+void run_search(const DevIndex& ix, Workspace& ws, const float* d_queries, uint64_t nq, uint32_t k,
+                uint32_t* d_ids, float* d_dists, uint32_t* d_counts, pqtg_query_stats* d_stats,
+                cudaStream_t s) {
+    const DevParams& p = ix.prm;
+    ws.last_stream = s;
+    ws.last_nq = nq;
+    PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[0], s));
+    if (nq == 0) {
+        for (int i = 1; i < 4; ++i) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[i], s));
+        return;
+    }
+    if (k == 0 || ix.n == 0) {  // search.cpp:130-132: empty results, zero stats
+        PQTG_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, nq * sizeof(uint32_t), s));
+        if (d_stats) PQTG_CUDA_CHECK(cudaMemsetAsync(d_stats, 0, nq * sizeof(pqtg_query_stats), s));
+        if (k && ix.n == 0) {
+            PQTG_CUDA_CHECK(cudaMemsetAsync(d_ids, 0xFF, nq * k * sizeof(uint32_t), s));
+            PQTG_CUDA_CHECK(cudaMemsetAsync(d_dists, 0x7F, nq * k * sizeof(float), s));
+        }
+        for (int i = 1; i < 4; ++i) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[i], s));
+        return;
+    }
+    launch_traverse(p, d_queries, nq, ws, s);
+    PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[1], s));
+    launch_binsel(p, nq, ws, d_stats, s);
+    PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[2], s));
+    launch_rerank(p, nq, k, ws, d_ids, d_dists, d_counts, s);
+    PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[3], s));
+}
+
+}  // namespace
+}  // namespace pqtg
+
+struct pqtg_index {
+    std::unique_ptr<pqtg::DevIndex> dev;
+};
+
+struct pqtg_workspace {
+    std::unique_ptr<pqtg::Workspace> ws;
+};
+
+using namespace pqtg;
+
+extern "C" {
+
+int pqtg_abi_version(void) { return PQTG_ABI_VERSION; }
+
+const char* pqtg_last_error(void) { return last_error(); }
+
+int pqtg_device_ok(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 0;
+    return prop.major == 10 ? 1 : 0;
+}
+
+int pqtg_index_create(const pqtg_index_view* v, int device, pqtg_index** out) {
+    return guarded([&] {
+        if (!v || !out) throw Error{PQTG_ERR_ARG, "null argument"};
+        *out = nullptr;
+        validate_config(v->config);
+        const uint64_t n = v->n;
+        if (!v->level1 || !v->level2 || !v->d2 || !v->offsets || (n && (!v->ids || !v->lambda_q || !v->pair_id)) ||
+            (v->table_count && (!v->table_entries || !v->table_slopes)))
+            throw Error{PQTG_ERR_ARG, "index view has null arrays"};
+        Source s;
+        s.cfg = v->config;
+        s.n = n;
+        s.level1 = v->level1;
+        s.level2 = v->level2;
+        s.d2 = v->d2;
+        s.table_count = v->table_count;
+        s.table_len = v->table_len;
+        s.slopes = v->table_slopes;
+        s.entries = v->table_entries;
+        s.offsets = v->offsets;
+        s.ids = v->ids;
+        s.lambda_q = v->lambda_q;
+        s.pair_id = v->pair_id;
+        auto* h = new pqtg_index;
+        h->dev.reset(build_device_index(s, device, v->shard_lo, v->shard_hi));
+        *out = h;
+        return PQTG_OK;
+    });
+}
+
+int pqtg_index_load(const char* path, int device, uint64_t shard_lo, uint64_t shard_hi, pqtg_index** out) {
+    return guarded([&] {
+        if (!path || !out) throw Error{PQTG_ERR_ARG, "null argument"};
+        *out = nullptr;
+        LoadedFile lf;
+        parse_index(path, lf);
+        auto* h = new pqtg_index;
+        h->dev.reset(build_device_index(lf.src, device, shard_lo, shard_hi));
+        *out = h;
+        return PQTG_OK;
+    });
+}
+
+int pqtg_index_info_get(const pqtg_index* index, pqtg_index_info* out) {
+    return guarded([&] {
+        if (!index || !out) throw Error{PQTG_ERR_ARG, "null argument"};
+        const DevIndex& d = *index->dev;
+        std::memset(out, 0, sizeof(*out));
+        out->config = d.cfg;
+        out->n = d.n;
+        out->shard_lo = d.prm.shard_lo;
+        out->shard_hi = d.prm.shard_hi;
+        out->list_len = d.prm.W;
+        out->pair_count = d.prm.npairs;
+        out->pair_width = d.prm.pw;
+        out->code_row_bytes = d.prm.row_bytes;
+        out->device_bytes = d.bytes;
+        out->device = d.device;
+        return PQTG_OK;
+    });
+}
+
+void pqtg_index_destroy(pqtg_index* index) { delete index; }
+
+int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_workspace** out) {
+    return guarded([&] {
+        if (!index || !out || max_batch == 0) throw Error{PQTG_ERR_ARG, "bad workspace arguments"};
+        *out = nullptr;
+        const DevIndex& d = *index->dev;
+        const DevParams& p = d.prm;
+        PQTG_CUDA_CHECK(cudaSetDevice(d.device));
+        auto ws = std::make_unique<Workspace>();
+        ws->index = &d;
+        ws->max_batch = max_batch;
+        PQTG_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->own_stream, cudaStreamNonBlocking));
+        for (auto& e : ws->ev) PQTG_CUDA_CHECK(cudaEventCreate(&e));
+        const uint64_t B = max_batch;
+        ws->fine = dev_alloc<float>(ws->allocations, B * p.L * p.k1);
+        ws->l2_dist = dev_alloc<float>(ws->allocations, B * p.P * p.W);
+        ws->l2_code = dev_alloc<uint32_t>(ws->allocations, B * p.P * p.W);
+        ws->slope = dev_alloc<uint8_t>(ws->allocations, B * 2);
+        ws->ranges = dev_alloc<uint2>(ws->allocations, B * std::max<uint64_t>(p.budget, 1));
+        ws->nranges = dev_alloc<uint32_t>(ws->allocations, B);
+        ws->ncand = dev_alloc<uint32_t>(ws->allocations, B);
+        auto* h = new pqtg_workspace;
+        h->ws = std::move(ws);
+        *out = h;
+        return PQTG_OK;
+    });
+}
+
+void pqtg_workspace_destroy(pqtg_workspace* ws) { delete ws; }
+
+int pqtg_workspace_stage_ms(pqtg_workspace* h, float* ms4) {
+    return guarded([&] {
+        if (!h || !ms4) throw Error{PQTG_ERR_ARG, "null argument"};
+        Workspace& ws = *h->ws;
+        PQTG_CUDA_CHECK(cudaEventSynchronize(ws.ev[3]));
+        for (int i = 0; i < 3; ++i) PQTG_CUDA_CHECK(cudaEventElapsedTime(&ms4[i], ws.ev[i], ws.ev[i + 1]));
+        PQTG_CUDA_CHECK(cudaEventElapsedTime(&ms4[3], ws.ev[0], ws.ev[3]));
+        return PQTG_OK;
+    });
+}
+
+int pqtg_workspace_read(pqtg_workspace* h, uint64_t nq, float* fine, uint32_t* l2_code, float* l2_dist,
+                        uint8_t* slope, uint32_t* positions, uint32_t* ncand) {
+    return guarded([&] {
+        if (!h) throw Error{PQTG_ERR_ARG, "null argument"};
+        Workspace& ws = *h->ws;
+        const DevParams& p = ws.index->prm;
+        if (nq > ws.last_nq) throw Error{PQTG_ERR_ARG, "nq exceeds the last searched batch"};
+        PQTG_CUDA_CHECK(cudaSetDevice(ws.index->device));
+        if (ws.last_stream || ws.own_stream) PQTG_CUDA_CHECK(cudaStreamSynchronize(ws.last_stream));
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            if (dst && bytes) PQTG_CUDA_CHECK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+        };
+        cp(fine, ws.fine, nq * p.L * p.k1 * sizeof(float));
+        cp(l2_code, ws.l2_code, nq * p.P * p.W * sizeof(uint32_t));
+        cp(l2_dist, ws.l2_dist, nq * p.P * p.W * sizeof(float));
+        cp(slope, ws.slope, nq * 2);
+        std::vector<uint32_t> nc(nq), nr(nq);
+        cp(nc.data(), ws.ncand, nq * 4);
+        cp(nr.data(), ws.nranges, nq * 4);
+        if (ncand) std::memcpy(ncand, nc.data(), nq * 4);
+        if (positions && p.budget) {
+            std::vector<uint2> rg(nq * p.budget);
+            cp(rg.data(), ws.ranges, rg.size() * sizeof(uint2));
+            for (uint64_t q = 0; q < nq; ++q) {
+                uint32_t* out = positions + q * p.budget;
+                const uint2* r = rg.data() + q * p.budget;
+                for (uint32_t b = 0; b < nr[q]; ++b) {
+                    const uint32_t end = b + 1 < nr[q] ? r[b + 1].y : nc[q];
+                    for (uint32_t j = r[b].y; j < end; ++j) out[j] = r[b].x + (j - r[b].y);
+                }
+            }
+        }
+        return PQTG_OK;
+    });
+}
+
+int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_queries, uint64_t nq, uint32_t k,
+                       uint32_t* d_ids, float* d_dists, uint32_t* d_counts, pqtg_query_stats* d_stats,
+                       void* stream) {
+    return guarded([&] {
+        if (!index || !wsh || (nq && (!d_queries || !d_counts || (k && (!d_ids || !d_dists)))))
+            throw Error{PQTG_ERR_ARG, "null argument"};
+        Workspace& ws = *wsh->ws;
+        if (ws.index != index->dev.get()) throw Error{PQTG_ERR_ARG, "workspace belongs to another index"};
+        if (nq > ws.max_batch) throw Error{PQTG_ERR_ARG, "nq exceeds the workspace max_batch"};
+        PQTG_CUDA_CHECK(cudaSetDevice(index->dev->device));
+        run_search(*index->dev, ws, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats,
+                   static_cast<cudaStream_t>(stream));
+        return PQTG_OK;
+    });
+}
+
+int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, uint64_t nq, uint32_t dim,
+                uint32_t k, uint32_t* ids, float* dists, uint32_t* counts, pqtg_query_stats* stats) {
+    return guarded([&] {
+        if (!index || !wsh) throw Error{PQTG_ERR_ARG, "null argument"};
+        const DevIndex& d = *index->dev;
+        if (nq > 0 && dim != d.prm.D)  // search.cpp:264-266
+            throw Error{PQTG_ERR_BAD_DIM, "knn_query_batch: query dimension mismatch"};
+        if (nq && (!queries || !counts || (k && (!ids || !dists)))) throw Error{PQTG_ERR_ARG, "null argument"};
+        Workspace& ws = *wsh->ws;
+        if (ws.index != &d) throw Error{PQTG_ERR_ARG, "workspace belongs to another index"};
+        std::lock_guard<std::mutex> lock(ws.mu);
+        PQTG_CUDA_CHECK(cudaSetDevice(d.device));
+        ensure_staging(ws, std::max<uint32_t>(k, 1));
+        cudaStream_t s = ws.own_stream;
+        const uint64_t D = d.prm.D;
+        for (uint64_t q0 = 0; q0 < nq || (nq == 0 && q0 == 0); q0 += ws.max_batch) {
+            const uint64_t b = std::min(ws.max_batch, nq - q0);
+            if (b == 0) {
+                run_search(d, ws, ws.d_queries, 0, k, ws.d_ids, ws.d_dists, ws.d_counts, ws.d_stats, s);
+                break;
+            }
+            PQTG_CUDA_CHECK(cudaMemcpyAsync(ws.d_queries, queries + q0 * D, b * D * sizeof(float),
+                                            cudaMemcpyHostToDevice, s));
+            run_search(d, ws, ws.d_queries, b, k, ws.d_ids, ws.d_dists, ws.d_counts, ws.d_stats, s);
+            if (k) {
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(ids + q0 * k, ws.d_ids, b * k * sizeof(uint32_t),
+                                                cudaMemcpyDeviceToHost, s));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(dists + q0 * k, ws.d_dists, b * k * sizeof(float),
+                                                cudaMemcpyDeviceToHost, s));
+            }
+            PQTG_CUDA_CHECK(cudaMemcpyAsync(counts + q0, ws.d_counts, b * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            if (stats)
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(stats + q0, ws.d_stats, b * sizeof(pqtg_query_stats),
+                                                cudaMemcpyDeviceToHost, s));
+            PQTG_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+        return PQTG_OK;
+    });
+}
+
+int64_t pqtg_bin_stream_host(const pqtg_index_view* v, const float* lists, uint64_t max_tuples, uint32_t* out) {
+    int64_t produced = 0;
+    const int rc = guarded([&] {
+        if (!v || !lists || (max_tuples && !out)) throw Error{PQTG_ERR_ARG, "null argument"};
+        validate_config(v->config);
+        const uint32_t P = v->config.p_tree;
+        if (!(P == 1 || P == 2 || P == 4)) unsupported("p_tree must be 1, 2 or 4");
+        if (P > 1 && v->table_count != kSlopeTables) unsupported("slope tables missing");
+        const uint64_t W64 = (uint64_t)v->config.w * v->config.k2;
+        if (W64 > 65535) unsupported("w*k2 must be < 65536");
+        const uint32_t W = (uint32_t)W64;
+        HostStreams hs = build_streams(v->table_entries, v->table_len, W, P);
+        // pick_slope_table (binorder.cpp:52-65), host libm
+        auto pick = [&](const float* a, const float* b) -> uint32_t {
+            if (W < 2) return kSlopeOne;
+            const double ga = (double)a[1] - a[0], gb = (double)b[1] - b[0];
+            if (!(ga > 0.0) || !(gb > 0.0)) return kSlopeOne;
+            long k = std::lround(std::log(gb / ga) / std::log(1.08));
+            k = std::clamp(k, -5L, 4L);
+            return (uint32_t)(k + 5);
+        };
+        const uint32_t ta = P >= 2 ? pick(lists, lists + W) : kSlopeOne;
+        const uint32_t tb = P == 4 ? pick(lists + 2 * W, lists + 3 * W) : kSlopeOne;
+        const uint64_t cnt = std::min<uint64_t>(max_tuples, hs.total);
+        for (uint64_t s = 0; s < cnt; ++s) hs.tuple_at(s, ta, tb, out + s * P);
+        produced = (int64_t)cnt;
+        return PQTG_OK;
+    });
+    return rc != PQTG_OK ? rc : produced;
+}
+
+int pqtg_merge_topk_host(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids, const float* dists,
+                         const uint32_t* counts, uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {
+    return guarded([&] {
+        if (shards == 0 || (nq && (!ids || !dists || !counts || !out_ids || !out_dists || !out_counts)))
+            throw Error{PQTG_ERR_ARG, "bad merge arguments"};
+        std::vector<uint32_t> cur(shards);
+        for (uint64_t q = 0; q < nq; ++q) {
+            std::fill(cur.begin(), cur.end(), 0u);
+            uint32_t out = 0;
+            while (out < k) {
+                int best = -1;
+                for (uint32_t g = 0; g < shards; ++g) {
+                    if (cur[g] >= counts[(uint64_t)g * nq + q]) continue;
+                    const uint64_t o = ((uint64_t)g * nq + q) * k + cur[g];
+                    if (best < 0) {
+                        best = (int)g;
+                        continue;
+                    }
+                    const uint64_t ob = ((uint64_t)best * nq + q) * k + cur[best];
+                    // candidate_less (search.cpp:39-41)
+                    const bool less = dists[o] != dists[ob] ? dists[o] < dists[ob] : ids[o] < ids[ob];
+                    if (less) best = (int)g;
+                }
+                if (best < 0) break;
+                const uint64_t o = ((uint64_t)best * nq + q) * k + cur[best];
+                out_ids[q * k + out] = ids[o];
+                out_dists[q * k + out] = dists[o];
+                ++cur[best];
+                ++out;
+            }
+            for (uint32_t i = out; i < k; ++i) {
+                out_ids[q * k + i] = 0xFFFFFFFFu;
+                out_dists[q * k + i] = __builtin_inff();
+            }
+            out_counts[q] = out;
+        }
+        return PQTG_OK;
+    });
+}
+
+int pqtg_merge_topk_device(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* d_ids, const float* d_dists,
+                           const uint32_t* d_counts, uint32_t* d_out_ids, float* d_out_dists, uint32_t* d_out_counts,
+                           void* stream) {
+    return guarded([&] {
+        if (shards == 0 || shards > 16) throw Error{PQTG_ERR_ARG, "shards must be in [1, 16]"};
+        launch_merge(shards, nq, k, d_ids, d_dists, d_counts, d_out_ids, d_out_dists, d_out_counts,
+                     static_cast<cudaStream_t>(stream));
+        return PQTG_OK;
+    });
+}
+
+int pqtg_shard_range(uint64_t n, uint32_t shards, uint32_t rank, uint64_t* lo, uint64_t* hi) {
+    return guarded([&] {
+        if (shards == 0 || rank >= shards || !lo || !hi) throw Error{PQTG_ERR_ARG, "bad shard arguments"};
+        const uint64_t per = n / shards, extra = n % shards;
+        *lo = rank * per + std::min<uint64_t>(rank, extra);
+        *hi = *lo + per + (rank < extra ? 1 : 0);
+        return PQTG_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,373 @@
+// index_prep.cpp — host side of the device index: validation, re-layout and upload.
+//
+// Inputs are the arrays of pqt::PqtIndex (include/pqt/search.hpp:34-47) — from a
+// pqtg_index_view or from a PQTINDEX v1 file (src/index_io.cpp:148-229). Outputs live in
+// HBM in kernel-friendly layouts:
+//   fine_t   [L][fd][k1]      level-1 centroid slices (build_fine_centroids, linequant.cpp:13-46)
+//   l2_t     [P][k1][m][k2]   level-2 codebooks, child-fastest for coalesced traversal loads
+//   pairs    [npairs]         lexicographic (i, j) pair enumeration (linequant.cpp:76-82)
+//   c2       [L][npairs]      the stored d2[f][i][j] per pair (index_io.cpp:188-190)
+//   streams  10 × W²          every slope table's full PairCursor order (binorder.cpp:69-110)
+//   merge    materialized prefix of the slope-1 merge over pair ranks (binorder.cpp:229-240)
+//   bitmap   H bits           non-empty slots
+//   offsets  H+1 u32          InvertedLists::offsets narrowed (n < 2^32)
+//   ids      positions        InvertedLists::ids of this shard
+//   codes    positions × row  line codes permuted into SLOT order: [λ_0..λ_{L-1}][pair ids]
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <functional>
+#include <memory>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <unordered_set>
+
+#include "pqtg_internal.h"
+
+namespace pqtg {
+
+DevIndex::~DevIndex() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (void* p : allocations) cudaFree(p);
+    cudaSetDevice(prev);
+}
+
+// PqtConfig::validate (src/codebook.cpp:15-35)
+void validate_config(const pqtg_config& c) {
+    auto fail = [](const char* m) { throw Error{PQTG_ERR_CONFIG, std::string("config: ") + m}; };
+    if (c.dim == 0 || c.p_tree == 0 || c.p_line == 0) fail("dim, p_tree and p_line must be positive");
+    if (c.dim % c.p_tree != 0) fail("dim must be divisible by p_tree");
+    if (c.p_line % c.p_tree != 0) fail("p_line must be a multiple of p_tree");
+    if (c.dim % c.p_line != 0) fail("dim must be divisible by p_line");
+    if (c.k1 < 1 || c.k2 < 1) fail("k1 and k2 must be at least 1");
+    if (c.w < 1 || c.w > c.k1) fail("w must be in [1, k1]");
+}
+
+[[noreturn]] void unsupported(const std::string& m) { throw Error{PQTG_ERR_UNSUPPORTED, m}; }
+[[noreturn]] void format(const std::string& m) { throw Error{PQTG_ERR_FORMAT, m}; }
+
+namespace {
+
+
+// PairCursor::next to exhaustion (binorder.cpp:80-110): table entries inside the grid in
+// table order, then a row-major sweep of every cell the table did not emit.
+std::vector<uint32_t> pair_stream(const uint32_t* entries, uint32_t tlen, uint32_t la, uint32_t lb) {
+    std::vector<uint32_t> out;
+    out.reserve((size_t)la * lb);
+    std::vector<uint8_t> emitted((size_t)la * lb, 0);
+    for (uint32_t e = 0; e < tlen; ++e) {
+        const uint32_t a = entries[2 * e], b = entries[2 * e + 1];
+        if (a < la && b < lb) {
+            // a table may repeat a cell; PairCursor re-emits it (the emitted set is only
+            // consulted by the sweep), so mirror that exactly
+            emitted[(size_t)a * lb + b] = 1;
+            out.push_back(a | (b << 16));
+        }
+    }
+    for (uint32_t a = 0; a < la; ++a) {
+        for (uint32_t b = 0; b < lb; ++b) {
+            if (!emitted[(size_t)a * lb + b]) out.push_back(a | (b << 16));
+        }
+    }
+    return out;
+}
+
+void parallel_rows(uint64_t n, const std::function<void(uint64_t, uint64_t)>& fn) {
+    unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (n < 65536 || hw == 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const uint64_t chunk = (n + hw - 1) / hw;
+    for (unsigned t = 0; t < hw; ++t) {
+        const uint64_t b = t * chunk, e = std::min(n, b + chunk);
+        if (b >= e) break;
+        th.emplace_back([&fn, b, e] { fn(b, e); });
+    }
+    for (auto& t : th) t.join();
+}
+
+template <class T>
+T* upload(DevIndex& ix, const T* host, uint64_t count) {
+    T* d = dev_alloc<T>(ix.allocations, count, &ix.bytes);
+    if (count) PQTG_CUDA_CHECK(cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+}
+
+}  // namespace
+
+HostStreams build_streams(const uint32_t* entries, uint32_t table_len, uint32_t W, uint32_t P) {
+    HostStreams hs;
+    hs.W = W;
+    hs.P = P;
+    hs.W2 = (uint64_t)W * W;
+    if (P == 1) {
+        hs.total = W;
+        return hs;
+    }
+    if (hs.W2 * kSlopeTables > (1ull << 28)) unsupported("w*k2 too large to materialize the slope streams");
+    hs.pair.reserve(hs.W2 * kSlopeTables);
+    for (uint32_t t = 0; t < kSlopeTables; ++t) {
+        auto s = pair_stream(entries + (size_t)t * table_len * 2, table_len, W, W);
+        // PairCursor re-emits a repeated in-bounds table cell; built tables never repeat one
+        // (binorder.cpp:30-47 sorts a duplicate-free grid), so require that here
+        if (s.size() != hs.W2) unsupported("slope table repeats grid cells");
+        hs.pair.insert(hs.pair.end(), s.begin(), s.end());
+    }
+    if (P == 2) {
+        hs.total = hs.W2;
+        return hs;
+    }
+    // merge cursor over (u, v) in [0, W²)² with the slope-1 table (binorder.cpp:229-240):
+    // its in-bounds prefix, then the sweep of the rows that prefix touched; every later row
+    // is swept whole and is addressed in closed form (row0 + j / W², j % W²).
+    const uint64_t len = hs.W2;
+    const uint32_t* e5 = entries + (size_t)kSlopeOne * table_len * 2;
+    std::unordered_set<uint64_t> emitted;
+    int64_t last_row = -1;
+    for (uint32_t e = 0; e < table_len; ++e) {
+        const uint64_t a = e5[2 * e], b = e5[2 * e + 1];
+        if (a < len && b < len) {
+            if (!emitted.insert((a << 32) | b).second) unsupported("slope table repeats grid cells");
+            hs.merge.push_back(make_uint2((uint32_t)a, (uint32_t)b));
+            last_row = std::max<int64_t>(last_row, (int64_t)a);
+        }
+    }
+    const uint64_t swept_rows = (uint64_t)(last_row + 1);
+    if (swept_rows * len > (1ull << 26)) unsupported("slope-1 table too deep to materialize its sweep");
+    for (uint64_t a = 0; a < swept_rows; ++a)
+        for (uint64_t b = 0; b < len; ++b)
+            if (!emitted.count((a << 32) | b)) hs.merge.push_back(make_uint2((uint32_t)a, (uint32_t)b));
+    hs.merge_row0 = swept_rows;
+    const long double tot = (long double)len * (long double)len;
+    hs.total = tot > 4294967294.0L ? 4294967294ull : len * len;
+    return hs;
+}
+
+// Host twin of the kernel's tuple addressing (kernels.cu tuple_slot): ranks of tuple s.
+void HostStreams::tuple_at(uint64_t s, uint32_t ta, uint32_t tb, uint32_t* r) const {
+    if (P == 1) {
+        r[0] = (uint32_t)s;
+        return;
+    }
+    if (P == 2) {
+        const uint32_t e = pair[(size_t)ta * W2 + s];
+        r[0] = e & 0xFFFF;
+        r[1] = e >> 16;
+        return;
+    }
+    uint64_t u, v;
+    if (s < merge.size()) {
+        u = merge[s].x;
+        v = merge[s].y;
+    } else {
+        const uint64_t j = s - merge.size();
+        u = merge_row0 + j / W2;
+        v = j % W2;
+    }
+    const uint32_t ea = pair[(size_t)ta * W2 + u], eb = pair[(size_t)tb * W2 + v];
+    r[0] = ea & 0xFFFF;
+    r[1] = ea >> 16;
+    r[2] = eb & 0xFFFF;
+    r[3] = eb >> 16;
+}
+
+DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, uint64_t shard_hi) {
+    const pqtg_config& c = src.cfg;
+    validate_config(c);
+    const uint64_t n = src.n;
+    const uint32_t P = c.p_tree, k1 = c.k1, k2 = c.k2, L = c.p_line;
+    const uint32_t m = c.dim / P, per_part = L / P, fd = m / per_part;
+    const uint64_t W64 = (uint64_t)c.w * k2;
+    const uint64_t H = c.hash_size;
+
+    // --- GPU-path limits (valid reference configs outside them are reported, not emulated)
+    if (!(P == 1 || P == 2 || P == 4)) unsupported("p_tree must be 1, 2 or 4 (other part counts use the exact order)");
+    if (P > 1 && src.table_count != kSlopeTables) unsupported("slope tables missing: the reference would use the exact order");
+    if (k1 > 65535 || k2 > 65535) unsupported("k1 and k2 must be < 65536");
+    if (W64 > 65535) unsupported("w*k2 must be < 65536");
+    if (n >= (1ull << 32)) unsupported("n must be < 2^32");
+    if (H == 0 || H >= 0xFFFFFFFFull) unsupported("hash_size must be in [1, 2^32-1)");
+    const uint32_t W = (uint32_t)W64;
+    const uint32_t npairs = k1 <= 1 ? 1u : k1 * (k1 - 1) / 2;
+    const uint32_t pw = npairs <= 256 ? 1u : 2u;  // index_io.cpp:132
+    if (npairs > 65536) unsupported("k1 too large for 16-bit pair ids");
+    if (c.resort_bins && std::min<uint64_t>(c.candidate_budget, n) > 4096)
+        unsupported("resort_bins with candidate budget > 4096");
+    const uint64_t budget = std::min<uint64_t>(c.candidate_budget, n);
+    if (budget > 16384) unsupported("candidate budget > 16384");
+    if (shard_hi == 0 && shard_lo == 0) shard_hi = n;
+    if (shard_lo > shard_hi || shard_hi > n) throw Error{PQTG_ERR_ARG, "bad shard range"};
+
+    // offsets sanity (InvertedLists invariants, pqtree.cpp:40-57)
+    if (src.offsets[0] != 0 || src.offsets[H] != n) format("inverted-list offsets do not cover [0, n)");
+
+    int ndev = 0;
+    PQTG_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Error{PQTG_ERR_ARG, "bad device ordinal"};
+    PQTG_CUDA_CHECK(cudaSetDevice(device));
+
+    auto ix = std::make_unique<DevIndex>();
+    ix->cfg = c;
+    ix->n = n;
+    ix->device = device;
+    DevParams& p = ix->prm;
+    p.D = c.dim;
+    p.P = P;
+    p.k1 = k1;
+    p.k2 = k2;
+    p.w = c.w;
+    p.L = L;
+    p.m = m;
+    p.fd = fd;
+    p.per_part = per_part;
+    p.W = W;
+    p.npairs = npairs;
+    p.pw = pw;
+    p.row_bytes = (L * (1 + pw) + 15) / 16 * 16;
+    p.budget = (uint32_t)budget;
+    p.resort = c.resort_bins ? 1u : 0u;
+    p.H = H;
+    p.n = n;
+    p.shard_lo = shard_lo;
+    p.shard_hi = shard_hi;
+    p.log108 = std::log(1.08);  // glibc, as in binorder.cpp:62
+    p.inv_log108 = 1.0 / p.log108;
+    p.h_pow2 = (H & (H - 1)) == 0;
+
+    // positional multipliers (pqtree.cpp:12-21) and whether the u64 code can wrap
+    const uint64_t base = (uint64_t)k1 * k2;
+    uint64_t mult = 1;
+    long double span = 1.0L;
+    for (uint32_t q = 0; q < P; ++q) {
+        p.mult[q] = mult;
+        mult *= base;
+        span *= (long double)base;
+    }
+    p.mod_fast = (span < 18446744073709551616.0L || p.h_pow2) ? 1u : 0u;
+
+    // --- level-1 slices [f][t][i] and level-2 codebooks [p][i][t][c]
+    {
+        std::vector<float> fine_t((size_t)L * fd * k1);
+        for (uint32_t f = 0; f < L; ++f) {
+            const uint32_t pp = f / per_part, within = f % per_part;
+            for (uint32_t i = 0; i < k1; ++i)
+                for (uint32_t t = 0; t < fd; ++t)
+                    fine_t[((size_t)f * fd + t) * k1 + i] =
+                        src.level1[((size_t)pp * k1 + i) * m + (size_t)within * fd + t];
+        }
+        p.fine_t = upload(*ix, fine_t.data(), fine_t.size());
+        std::vector<float> l2_t((size_t)P * k1 * m * k2);
+        for (uint32_t pp = 0; pp < P; ++pp)
+            for (uint32_t i = 0; i < k1; ++i)
+                for (uint32_t ch = 0; ch < k2; ++ch)
+                    for (uint32_t t = 0; t < m; ++t)
+                        l2_t[(((size_t)pp * k1 + i) * m + t) * k2 + ch] =
+                            src.level2[(((size_t)pp * k1 + i) * k2 + ch) * m + t];
+        p.l2_t = upload(*ix, l2_t.data(), l2_t.size());
+    }
+
+    // --- pair enumeration and per-pair d2
+    {
+        std::vector<uint32_t> pairs(npairs);
+        std::vector<float> c2((size_t)L * npairs);
+        if (k1 <= 1) {
+            pairs[0] = 0;
+        } else {
+            uint32_t q = 0;
+            for (uint32_t i = 0; i < k1; ++i)
+                for (uint32_t j = i + 1; j < k1; ++j) pairs[q++] = i | (j << 16);
+        }
+        for (uint32_t f = 0; f < L; ++f)
+            for (uint32_t q = 0; q < npairs; ++q) {
+                const uint32_t i = pairs[q] & 0xFFFF, j = pairs[q] >> 16;
+                c2[(size_t)f * npairs + q] = src.d2[((size_t)f * k1 + i) * k1 + j];
+            }
+        p.pairs = upload(*ix, pairs.data(), pairs.size());
+        p.c2 = upload(*ix, c2.data(), c2.size());
+    }
+
+    // --- static bin-order streams (binorder.cpp:178-283)
+    {
+        HostStreams hs = build_streams(src.entries, src.table_len, W, P);
+        p.W2 = hs.W2;
+        p.total_tuples = hs.total;
+        p.merge_count = hs.merge.size();
+        p.merge_row0 = hs.merge_row0;
+        if (!hs.pair.empty()) p.pair_streams = upload(*ix, hs.pair.data(), hs.pair.size());
+        if (!hs.merge.empty()) p.merge = upload(*ix, hs.merge.data(), hs.merge.size());
+    }
+
+    // --- inverted lists: bitmap of non-empty slots, u32 offsets
+    {
+        std::vector<uint32_t> bitmap((H + 31) / 32, 0u);
+        std::vector<uint32_t> off32(H + 1);
+        for (uint64_t s = 0; s <= H; ++s) {
+            if (s < H && src.offsets[s + 1] < src.offsets[s]) format("inverted-list offsets decrease");
+            off32[s] = (uint32_t)src.offsets[s];
+            if (s < H && src.offsets[s + 1] > src.offsets[s]) bitmap[s >> 5] |= 1u << (s & 31);
+        }
+        p.bitmap = upload(*ix, bitmap.data(), bitmap.size());
+        p.offsets = upload(*ix, off32.data(), off32.size());
+    }
+
+    // --- this shard's ids and line codes in slot order
+    const uint64_t npos = shard_hi - shard_lo;
+    p.ids = upload(*ix, src.ids + shard_lo, npos);
+    {
+        uint8_t* dcodes = dev_alloc<uint8_t>(ix->allocations, npos * p.row_bytes + 16, &ix->bytes);
+        p.codes = dcodes;
+        const uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / p.row_bytes);
+        std::vector<uint8_t> stage((size_t)std::min(chunk, std::max<uint64_t>(npos, 1)) * p.row_bytes);
+        std::atomic<bool> bad_pid{false}, bad_id{false};
+        for (uint64_t b = 0; b < npos; b += chunk) {
+            const uint64_t e = std::min(npos, b + chunk);
+            parallel_rows(e - b, [&](uint64_t lo, uint64_t hi) {
+                for (uint64_t r = lo; r < hi; ++r) {
+                    const uint64_t id = src.ids[shard_lo + b + r];
+                    uint8_t* row = stage.data() + r * p.row_bytes;
+                    std::memset(row, 0, p.row_bytes);
+                    if (id >= n) {
+                        bad_id = true;
+                        continue;
+                    }
+                    for (uint32_t f = 0; f < L; ++f) {
+                        uint32_t lq, pid;
+                        if (src.records) {
+                            const uint8_t* rec = src.records + (id * L + f) * (1 + src.record_pw);
+                            lq = rec[0];
+                            pid = src.record_pw == 1 ? rec[1] : (uint32_t)rec[1] | ((uint32_t)rec[2] << 8);
+                        } else {
+                            lq = src.lambda_q[id * L + f];
+                            pid = src.pair_id[id * L + f];
+                        }
+                        if (pid >= npairs) bad_pid = true;
+                        row[f] = (uint8_t)lq;
+                        if (pw == 1) {
+                            row[L + f] = (uint8_t)pid;
+                        } else {
+                            row[L + 2 * f] = (uint8_t)(pid & 0xFF);
+                            row[L + 2 * f + 1] = (uint8_t)(pid >> 8);
+                        }
+                    }
+                }
+            });
+            if (bad_pid) format("line code pair id out of range");
+            if (bad_id) format("inverted-list id out of range");
+            PQTG_CUDA_CHECK(cudaMemcpy(dcodes + b * p.row_bytes, stage.data(), (e - b) * p.row_bytes,
+                                       cudaMemcpyHostToDevice));
+        }
+    }
+    configure_kernels(p, 0);
+    return ix.release();
+}
+
+}  // namespace pqtg

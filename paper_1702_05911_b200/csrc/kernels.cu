@@ -1,0 +1,803 @@
+// kernels.cu — sm_100a kernels of the PQT online query path.
+//
+//   K1 traverse_kernel  (north-star kernels 1+2)  pqtree.cpp:74-120 + binorder.cpp:52-65
+//   K3 binsel_kernel    (north-star kernels 3+4)  binorder.cpp:69-283 + search.cpp:139-217
+//   K5 rerank_kernel    (north-star kernels 5+6)  linequant.cpp:169-182 + search.cpp:221-257
+//   merge_topk_kernel   per-shard top-k merge by (dist, id)  (search.cpp:39-41 order)
+//
+// Exactness contract: every fp32 op is an explicitly rounded
+// __fadd_rn/__fsub_rn/__fmul_rn (never contracted to FMA), reductions run in the reference's
+// sequential order, and every sort reproduces the reference's total order. Parallelism is
+// across (query, centroid, candidate), never inside one sum.
+#include <cub/block/block_radix_sort.cuh>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "pqtg_internal.h"
+
+namespace pqtg {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr uint64_t kSentinel = ~0ull;
+
+__device__ __forceinline__ float sq_step(float acc, float a, float b) {
+    const float d = __fsub_rn(a, b);
+    return __fadd_rn(acc, __fmul_rn(d, d));
+}
+
+// fp32 -> u32 preserving order (with -0.0 folded onto +0.0 so it ties like operator<).
+__device__ __forceinline__ uint32_t orderable(float x) {
+    uint32_t u = __float_as_uint(x);
+    if (u == 0x80000000u) u = 0u;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float unorderable(uint32_t o) {
+    uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+    return __uint_as_float(u);
+}
+
+// pick_slope_table (binorder.cpp:52-65): fp64 gaps, nearest slope 1.08^k in log space.
+__device__ uint32_t pick_slope(const float* a, const float* b, uint32_t len, double log108) {
+    if (len < 2) return kSlopeOne;
+    const double ga = (double)a[1] - (double)a[0];
+    const double gb = (double)b[1] - (double)b[0];
+    if (!(ga > 0.0) || !(gb > 0.0)) return kSlopeOne;
+    const double ratio = gb / ga;
+    long long k = llround(log(ratio) / log108);
+    k = k < -5 ? -5 : (k > 4 ? 4 : k);
+    return (uint32_t)(k + 5);
+}
+
+// ------------------------------------------------------------------ block scan helpers
+__device__ __forceinline__ uint64_t warp_incl_scan(uint64_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Exclusive block scan of one u64 per thread; returns the exclusive prefix, *total = sum.
+__device__ uint64_t block_excl_scan(uint64_t v, uint64_t* warp_sums, uint64_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    uint64_t incl = warp_incl_scan(v);
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t s = lane < nwarps ? warp_sums[lane] : 0;
+        s = warp_incl_scan(s);
+        if (lane < nwarps) warp_sums[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint64_t before = warp == 0 ? 0 : warp_sums[warp - 1];
+    *total = warp_sums[nwarps - 1];
+    __syncthreads();
+    return before + incl - v;
+}
+
+}  // namespace
+
+// =====================================================================================
+// K1 — traversal: exact fine-part LUT, level-1 sort, level-2 distances of the w best
+// parents, level-2 sort, slope pick. One CTA per query.
+// =====================================================================================
+__global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const float* __restrict__ Q,
+                                                            float* __restrict__ fine_out,
+                                                            float* __restrict__ l2d_out,
+                                                            uint32_t* __restrict__ l2c_out,
+                                                            uint8_t* __restrict__ slope_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t D = p.D, L = p.L, k1 = p.k1, P = p.P, W = p.W, k2 = p.k2, m = p.m, fd = p.fd;
+    float* y = reinterpret_cast<float*>(smem);
+    float* fine = y + D;
+    float* l1d = fine + L * k1;
+    uint32_t* l1o = reinterpret_cast<uint32_t*>(l1d + P * k1);
+    float* l2d = reinterpret_cast<float*>(l1o + P * k1);
+    uint32_t* l2c = reinterpret_cast<uint32_t*>(l2d + P * W);
+    float* sd = reinterpret_cast<float*>(l2c + P * W);
+    const uint64_t q = blockIdx.x;
+    const int tid = threadIdx.x;
+
+    for (uint32_t i = tid; i < D; i += blockDim.x) y[i] = Q[q * D + i];
+    __syncthreads();
+
+    // fine_dists[f][i] = l2_sq(y_f, slice(f, i), fd) sequentially (pqtree.cpp:90-93)
+    for (uint32_t idx = tid; idx < L * k1; idx += blockDim.x) {
+        const uint32_t f = idx / k1, i = idx - f * k1;
+        const float* c = p.fine_t + (size_t)f * fd * k1 + i;
+        const float* yf = y + f * fd;
+        float acc = 0.0f;
+        for (uint32_t t = 0; t < fd; ++t) acc = sq_step(acc, yf[t], c[(size_t)t * k1]);
+        fine[idx] = acc;
+        fine_out[q * L * k1 + idx] = acc;
+    }
+    __syncthreads();
+
+    // level-1 totals: fp32 sum of the part's fine partials in f order (pqtree.cpp:88-96)
+    for (uint32_t idx = tid; idx < P * k1; idx += blockDim.x) {
+        const uint32_t pp = idx / k1, i = idx - pp * k1;
+        float tot = 0.0f;
+        for (uint32_t f = pp * p.per_part; f < (pp + 1) * p.per_part; ++f) tot = __fadd_rn(tot, fine[f * k1 + i]);
+        l1d[idx] = tot;
+    }
+    __syncthreads();
+
+    // sort each part's k1 entries by (dist, id) (pqtree.cpp:98-100): rank = #smaller keys
+    for (uint32_t idx = tid; idx < P * k1; idx += blockDim.x) {
+        const uint32_t pp = idx / k1, i = idx - pp * k1;
+        const float d = l1d[idx];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < k1; ++j) {
+            const float dj = l1d[pp * k1 + j];
+            rank += (dj < d) || (dj == d && j < i);
+        }
+        l1o[pp * k1 + rank] = i;
+    }
+    __syncthreads();
+
+    // level-2: k2 children of each of the w best parents, l2_sq over m (pqtree.cpp:102-111)
+    const uint32_t per = p.w * k2;
+    for (uint32_t idx = tid; idx < P * per; idx += blockDim.x) {
+        const uint32_t pp = idx / per, rem = idx - pp * per, r = rem / k2, c = rem - r * k2;
+        const uint32_t parent = l1o[pp * k1 + r];
+        const float* yp = y + pp * m;
+        const float* cb = p.l2_t + ((size_t)(pp * k1 + parent) * m) * k2 + c;
+        float acc = 0.0f;
+        for (uint32_t t = 0; t < m; ++t) acc = sq_step(acc, yp[t], cb[(size_t)t * k2]);
+        l2d[idx] = acc;
+        l2c[idx] = (parent << 16) | c;
+    }
+    __syncthreads();
+
+    // sort each part's W entries by (dist, parent, child) (pqtree.cpp:112-117)
+    for (uint32_t idx = tid; idx < P * W; idx += blockDim.x) {
+        const uint32_t pp = idx / W;
+        const float d = l2d[idx];
+        const uint32_t code = l2c[idx];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < W; ++j) {
+            const float dj = l2d[pp * W + j];
+            const uint32_t cj = l2c[pp * W + j];
+            rank += (dj < d) || (dj == d && cj < code);
+        }
+        const size_t o = q * P * W + pp * W + rank;
+        l2d_out[o] = d;
+        l2c_out[o] = code;
+        sd[pp * W + rank] = d;
+    }
+    __syncthreads();
+
+    if (tid == 0) {
+        uint8_t s0 = kSlopeOne, s1 = kSlopeOne;
+        if (P >= 2) s0 = (uint8_t)pick_slope(sd, sd + W, W, p.log108);
+        if (P == 4) s1 = (uint8_t)pick_slope(sd + 2 * W, sd + 3 * W, W, p.log108);
+        slope_out[q * 2] = s0;
+        slope_out[q * 2 + 1] = s1;
+    }
+}
+
+size_t traverse_smem(const DevParams& p) {
+    return sizeof(float) * ((size_t)p.D + (size_t)p.L * p.k1 + 2ull * p.P * p.k1 + 3ull * p.P * p.W);
+}
+
+void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, Workspace& ws,
+                     cudaStream_t s) {
+    traverse_kernel<<<(unsigned)nq, kThreads, traverse_smem(p), s>>>(p, queries, ws.fine, ws.l2_dist,
+                                                                     ws.l2_code, ws.slope);
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+// =====================================================================================
+// K3 — bin selection + gather: walk the heuristic rank-tuple stream in chunks, hash each
+// tuple to its slot, drop empty slots with the bitmap, keep the first occurrence of every
+// non-empty slot (shared-memory hash set keyed by slot, atomicMin of processing rank), and
+// cut at the candidate budget with a block prefix sum. Emits one range per visited bin.
+// =====================================================================================
+namespace {
+
+struct BinselSmem {
+    uint32_t ts_mask;
+    uint32_t ts_shift;
+};
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t slot, uint32_t shift) {
+    return (slot * 0x9E3779B1u) >> shift;
+}
+
+// Stream tuple at position s -> the slot it addresses (binorder.cpp:251-283, pqtree.cpp:12-25).
+__device__ __forceinline__ uint64_t tuple_slot(const DevParams& p, uint64_t s, uint32_t ta, uint32_t tb,
+                                               const uint64_t* terms) {
+    uint32_t r0, r1 = 0, r2 = 0, r3 = 0;
+    if (p.P == 1) {
+        r0 = (uint32_t)s;
+    } else if (p.P == 2) {
+        const uint32_t e = __ldg(p.pair_streams + (size_t)ta * p.W2 + s);
+        r0 = e & 0xFFFFu;
+        r1 = e >> 16;
+    } else {
+        uint64_t u, v;
+        if (s < p.merge_count) {
+            const uint2 uv = __ldg(p.merge + s);
+            u = uv.x;
+            v = uv.y;
+        } else {
+            const uint64_t j = s - p.merge_count;
+            u = p.merge_row0 + j / p.W2;
+            v = j - (u - p.merge_row0) * p.W2;
+        }
+        const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + u);
+        const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + v);
+        r0 = ea & 0xFFFFu;
+        r1 = ea >> 16;
+        r2 = eb & 0xFFFFu;
+        r3 = eb >> 16;
+    }
+    const uint32_t W = p.W;
+    uint64_t code = terms[r0];
+    if (p.P >= 2) code += terms[W + r1];
+    if (p.P == 4) code += terms[2 * W + r2] + terms[3 * W + r3];
+    if (p.h_pow2) return code & (p.H - 1);
+    if (p.mod_fast) {  // terms already reduced mod H, sum < P*H
+        while (code >= p.H) code -= p.H;
+        return code;
+    }
+    return code % p.H;
+}
+
+}  // namespace
+
+template <int ITEMS, bool RESORT>
+__global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const float* __restrict__ l2d_in,
+                                                          const uint32_t* __restrict__ l2c_in,
+                                                          const uint8_t* __restrict__ slope_in,
+                                                          uint2* __restrict__ ranges,
+                                                          uint32_t* __restrict__ nranges,
+                                                          uint32_t* __restrict__ ncand,
+                                                          pqtg_query_stats* __restrict__ stats,
+                                                          uint32_t ts_log2) {
+    using Sort = cub::BlockRadixSort<uint32_t, kThreads, ITEMS, uint32_t>;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t PW_ = p.P * p.W;
+    const uint32_t TS = 1u << ts_log2;
+    const uint32_t shift = 32 - ts_log2;
+    uint64_t* terms = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* warp_sums = terms + PW_;
+    float* dl = reinterpret_cast<float*>(warp_sums + 32);
+    uint32_t* hkeys = reinterpret_cast<uint32_t*>(dl + PW_);
+    uint32_t* hvals = hkeys + TS;
+    __shared__ uint32_t s_emitted;
+    __shared__ typename Sort::TempStorage sort_tmp;
+
+    const uint64_t q = blockIdx.x;
+    const int tid = threadIdx.x;
+
+    for (uint32_t idx = tid; idx < PW_; idx += blockDim.x) {
+        const uint32_t code = l2c_in[q * PW_ + idx];
+        const uint32_t pp = idx / p.W;
+        const uint64_t flat = (uint64_t)(code >> 16) * p.k2 + (code & 0xFFFFu);  // flat_part_code
+        uint64_t t = flat * p.mult[pp];                                          // u64 wrap
+        if (p.mod_fast) t %= p.H;
+        terms[idx] = t;
+        dl[idx] = l2d_in[q * PW_ + idx];
+    }
+    for (uint32_t i = tid; i < TS; i += blockDim.x) {
+        hkeys[i] = kEmptyKey;
+        hvals[i] = 0xFFFFFFFFu;
+    }
+    const uint32_t ta = slope_in[q * 2], tb = slope_in[q * 2 + 1];
+    __syncthreads();
+
+    const uint32_t budget = p.budget;
+    const uint64_t total = p.total_tuples;
+    const uint32_t CH = kThreads * ITEMS;
+    uint2* qranges = ranges + q * (uint64_t)budget;
+    uint32_t C = 0, R = 0;
+    uint64_t base = 0;
+
+    while (C < budget && base < total) {
+        uint64_t spos[ITEMS];
+        bool inb[ITEMS];
+        uint64_t step;
+        if (RESORT) {
+            // one batch = the next `budget` tuples (search.cpp:153), stable-sorted by the
+            // fp32 sum of their part distances (search.cpp:179-190)
+            const uint64_t bs = min((uint64_t)budget, total - base);
+            uint32_t keys[ITEMS], vals[ITEMS];
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) {
+                const uint32_t o = tid * ITEMS + it;
+                vals[it] = o;
+                keys[it] = 0xFFFFFFFFu;
+                if (o < bs) {
+                    const uint64_t s = base + o;
+                    // ranks of tuple s (recomputed; resort batches are budget-sized)
+                    uint32_t r[4] = {0, 0, 0, 0};
+                    if (p.P == 1) {
+                        r[0] = (uint32_t)s;
+                    } else if (p.P == 2) {
+                        const uint32_t e = p.pair_streams[(size_t)ta * p.W2 + s];
+                        r[0] = e & 0xFFFFu;
+                        r[1] = e >> 16;
+                    } else {
+                        uint64_t u, v;
+                        if (s < p.merge_count) {
+                            u = p.merge[s].x;
+                            v = p.merge[s].y;
+                        } else {
+                            const uint64_t j = s - p.merge_count;
+                            u = p.merge_row0 + j / p.W2;
+                            v = j - (u - p.merge_row0) * p.W2;
+                        }
+                        const uint32_t ea = p.pair_streams[(size_t)ta * p.W2 + u];
+                        const uint32_t eb = p.pair_streams[(size_t)tb * p.W2 + v];
+                        r[0] = ea & 0xFFFFu;
+                        r[1] = ea >> 16;
+                        r[2] = eb & 0xFFFFu;
+                        r[3] = eb >> 16;
+                    }
+                    float agg = 0.0f;
+                    for (uint32_t pp = 0; pp < p.P; ++pp) agg = __fadd_rn(agg, dl[pp * p.W + r[pp]]);
+                    keys[it] = orderable(agg);
+                }
+            }
+            Sort(sort_tmp).Sort(keys, vals);  // stable LSD radix sort, blocked arrangement
+            __syncthreads();
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) {
+                const uint32_t o = tid * ITEMS + it;
+                inb[it] = o < bs;
+                spos[it] = base + vals[it];
+            }
+            step = bs;
+        } else {
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) {
+                spos[it] = base + (uint64_t)(tid * ITEMS + it);
+                inb[it] = spos[it] < total;
+            }
+            step = CH;
+        }
+
+        // slot, emptiness and first-occurrence bookkeeping
+        uint32_t slot[ITEMS], hidx[ITEMS];
+        bool ne[ITEMS];
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it) {
+            ne[it] = false;
+            hidx[it] = 0;
+            slot[it] = 0;
+            if (inb[it]) {
+                const uint64_t sl = tuple_slot(p, spos[it], ta, tb, terms);
+                slot[it] = (uint32_t)sl;
+                ne[it] = (__ldg(p.bitmap + (sl >> 5)) >> (sl & 31)) & 1u;
+            }
+            if (ne[it]) {
+                // Empty slots need no dedup: a repeat of an empty slot is empty again.
+                const uint32_t ord = (uint32_t)(base + tid * ITEMS + it);
+                uint32_t h = hash_slot(slot[it], shift);
+                for (;;) {
+                    const uint32_t prev = atomicCAS(hkeys + h, kEmptyKey, slot[it]);
+                    if (prev == kEmptyKey || prev == slot[it]) {
+                        atomicMin(hvals + h, ord);
+                        break;
+                    }
+                    h = (h + 1) & (TS - 1);
+                }
+                hidx[it] = h;
+            }
+        }
+        __syncthreads();
+
+        uint32_t cnt[ITEMS], start[ITEMS];
+        uint64_t local = 0;
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it) {
+            cnt[it] = 0;
+            start[it] = 0;
+            if (ne[it]) {
+                const uint32_t ord = (uint32_t)(base + tid * ITEMS + it);
+                if (hvals[hidx[it]] == ord) {  // first occurrence in processing order
+                    start[it] = __ldg(p.offsets + slot[it]);
+                    cnt[it] = __ldg(p.offsets + slot[it] + 1) - start[it];
+                }
+            }
+            local += ((uint64_t)cnt[it] << 32) | (cnt[it] ? 1u : 0u);
+        }
+        if (tid == 0) s_emitted = 0;
+        uint64_t tot;
+        uint64_t excl = block_excl_scan(local, warp_sums, &tot);
+        uint32_t emitted = 0;
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it) {
+            if (cnt[it]) {
+                const uint64_t before_c = (uint64_t)C + (excl >> 32);
+                if (before_c < budget) {
+                    const uint32_t r = R + (uint32_t)(excl & 0xFFFFFFFFu);
+                    qranges[r] = make_uint2(start[it], (uint32_t)before_c);
+                    ++emitted;
+                }
+                excl += ((uint64_t)cnt[it] << 32) | 1u;
+            }
+        }
+        if (emitted) atomicAdd(&s_emitted, emitted);
+        __syncthreads();
+        R += s_emitted;
+        const uint64_t newc = (uint64_t)C + (tot >> 32);
+        C = newc < budget ? (uint32_t)newc : budget;
+        base += step;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        nranges[q] = R;
+        ncand[q] = C;
+        if (stats) {
+            stats[q].bins_visited = R;
+            stats[q].candidates = C;
+            stats[q].exact_evals = 0;
+        }
+    }
+}
+
+namespace {
+uint32_t ts_log2_for(const DevParams& p) {
+    const uint64_t ch = p.resort ? 4096 : (uint64_t)kThreads * 4;
+    const uint64_t need = ((uint64_t)p.budget + ch) * 3 / 2 + 64;
+    uint32_t lg = 6;
+    while ((1ull << lg) < need) ++lg;
+    return lg;
+}
+}  // namespace
+
+size_t binsel_smem(const DevParams& p) {
+    const uint64_t TS = 1ull << ts_log2_for(p);
+    return (size_t)p.P * p.W * (8 + 4) + TS * 8 + 32 * 8;
+}
+
+void launch_binsel(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats,
+                   cudaStream_t s) {
+    const uint32_t lg = ts_log2_for(p);
+    if (p.resort) {
+        binsel_kernel<16, true><<<(unsigned)nq, kThreads, binsel_smem(p), s>>>(
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, stats, lg);
+    } else {
+        binsel_kernel<4, false><<<(unsigned)nq, kThreads, binsel_smem(p), s>>>(
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, stats, lg);
+    }
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+// =====================================================================================
+// K5 — line-quantized re-rank + top-k. One CTA per query; per-query LUT (fine dists) and
+// the pair tables in shared memory; one thread per candidate walks its code row; then an
+// 8-bit radix select finds the k-th (dist, id) key and a bitonic sort orders the top k.
+// =====================================================================================
+namespace {
+
+template <int LT, int PW>
+__device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ row, const float* fine,
+                                                   const float* c2, const uint32_t* pairs, uint32_t L,
+                                                   uint32_t k1, uint32_t npairs) {
+    const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
+    float total = 0.0f;
+    if constexpr (LT > 0) {
+        constexpr int kBytes = LT * (1 + PW);
+        constexpr int kVec = (kBytes + 15) / 16;
+        uint4 v[kVec];
+        const uint4* r4 = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+        for (int i = 0; i < kVec; ++i) v[i] = __ldg(r4 + i);
+        const uint32_t* wds = reinterpret_cast<const uint32_t*>(v);
+#pragma unroll
+        for (int f = 0; f < LT; ++f) {
+            const uint32_t lq = (wds[f >> 2] >> ((f & 3) * 8)) & 0xFFu;
+            uint32_t pid;
+            if constexpr (PW == 1) {
+                const int bi = LT + f;
+                pid = (wds[bi >> 2] >> ((bi & 3) * 8)) & 0xFFu;
+            } else {
+                const int b0 = LT + 2 * f, b1 = b0 + 1;
+                pid = ((wds[b0 >> 2] >> ((b0 & 3) * 8)) & 0xFFu) | (((wds[b1 >> 2] >> ((b1 & 3) * 8)) & 0xFFu) << 8);
+            }
+            const uint32_t pr = pairs[pid];
+            const float b2 = fine[f * k1 + (pr & 0xFFFFu)];
+            const float a2 = fine[f * k1 + (pr >> 16)];
+            const float cc = c2[f * npairs + pid];
+            const float lam = __fmul_rn((float)lq, inv255);
+            const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
+                                         __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
+            total = __fadd_rn(total, part);
+        }
+    } else {
+        for (uint32_t f = 0; f < L; ++f) {
+            const uint32_t lq = __ldg(row + f);
+            uint32_t pid;
+            if (PW == 1) {
+                pid = __ldg(row + L + f);
+            } else {
+                pid = (uint32_t)__ldg(row + L + 2 * f) | ((uint32_t)__ldg(row + L + 2 * f + 1) << 8);
+            }
+            const uint32_t pr = pairs[pid];
+            const float b2 = fine[f * k1 + (pr & 0xFFFFu)];
+            const float a2 = fine[f * k1 + (pr >> 16)];
+            const float cc = c2[f * npairs + pid];
+            const float lam = __fmul_rn((float)lq, inv255);
+            const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
+                                         __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
+            total = __fadd_rn(total, part);
+        }
+    }
+    return total;
+}
+
+uint32_t next_pow2(uint32_t x) {
+    uint32_t r = 1;
+    while (r < x) r <<= 1;
+    return r;
+}
+
+}  // namespace
+
+template <int LT, int PW>
+__global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t k, uint32_t sel_cap,
+                                                          const float* __restrict__ fine_in,
+                                                          const uint2* __restrict__ ranges,
+                                                          const uint32_t* __restrict__ nranges,
+                                                          const uint32_t* __restrict__ ncand,
+                                                          uint32_t* __restrict__ out_ids,
+                                                          float* __restrict__ out_dists,
+                                                          uint32_t* __restrict__ out_counts) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t L = p.L, k1 = p.k1, npairs = p.npairs, budget = p.budget;
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);          // budget
+    uint64_t* sel = keys + budget;                                // sel_cap
+    float* fine = reinterpret_cast<float*>(sel + sel_cap);        // L*k1
+    float* c2 = fine + L * k1;                                    // L*npairs
+    uint32_t* pairs = reinterpret_cast<uint32_t*>(c2 + L * npairs);  // npairs
+    uint32_t* coff = pairs + npairs;                              // budget
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t s_count, s_nsel, s_digit, s_before, s_bucket;
+
+    const uint64_t q = blockIdx.x;
+    const int tid = threadIdx.x;
+    const uint32_t R = nranges[q], C = ncand[q];
+    const uint2* qr = ranges + q * (uint64_t)budget;
+
+    for (uint32_t i = tid; i < L * k1; i += blockDim.x) fine[i] = fine_in[q * L * k1 + i];
+    for (uint32_t i = tid; i < L * npairs; i += blockDim.x) c2[i] = __ldg(p.c2 + i);
+    for (uint32_t i = tid; i < npairs; i += blockDim.x) pairs[i] = __ldg(p.pairs + i);
+    for (uint32_t r = tid; r < R; r += blockDim.x) coff[r] = qr[r].y;
+    if (tid == 0) {
+        s_count = 0;
+        s_nsel = 0;
+    }
+    __syncthreads();
+
+    const bool sharded = p.shard_hi > p.shard_lo;
+    uint32_t mine = 0;
+    for (uint32_t j = tid; j < C; j += blockDim.x) {
+        // range containing candidate j: last r with coff[r] <= j
+        uint32_t lo = 0, hi = R - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (coff[mid] <= j) lo = mid; else hi = mid - 1;
+        }
+        const uint64_t pos = (uint64_t)__ldg(&qr[lo].x) + (j - coff[lo]);
+        uint64_t key = kSentinel;
+        if (!sharded || (pos >= p.shard_lo && pos < p.shard_hi)) {
+            const uint64_t lp = pos - p.shard_lo;
+            const uint32_t id = __ldg(p.ids + lp);
+            const float d = line_distance_row<LT, PW>(p.codes + lp * p.row_bytes, fine, c2, pairs, L, k1, npairs);
+            key = ((uint64_t)orderable(d) << 32) | id;
+            ++mine;
+        }
+        keys[j] = key;
+    }
+    if (mine) atomicAdd(&s_count, mine);
+    __syncthreads();
+    const uint32_t nvalid = s_count;
+    const uint32_t kk = nvalid < k ? nvalid : k;
+
+    if (kk > 0) {
+        // ---- radix select of the kk-th smallest key (keys are distinct: ids are distinct)
+        uint64_t prefix = 0, mask = 0;
+        uint32_t need = kk;
+        int shift = 56;
+        for (;; shift -= 8) {
+            for (uint32_t i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+            __syncthreads();
+            for (uint32_t j = tid; j < C; j += blockDim.x) {
+                const uint64_t key = keys[j];
+                if (key != kSentinel && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1u);
+            }
+            __syncthreads();
+            if (tid < 32) {
+                uint32_t sum = 0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) sum += hist[tid * 8 + b];
+                uint32_t incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += t;
+                }
+                const uint32_t excl = incl - sum;
+                if (excl < need && need <= incl) {
+                    uint32_t acc = excl;
+                    for (int b = 0; b < 8; ++b) {
+                        const uint32_t h = hist[tid * 8 + b];
+                        if (acc + h >= need) {
+                            s_digit = tid * 8 + b;
+                            s_before = acc;
+                            s_bucket = h;
+                            break;
+                        }
+                        acc += h;
+                    }
+                }
+            }
+            __syncthreads();
+            prefix |= (uint64_t)s_digit << shift;
+            mask |= 0xFFull << shift;
+            need -= s_before;
+            if (s_bucket == need || shift == 0) break;
+            __syncthreads();
+        }
+        // ---- collect the kk smallest keys, then bitonic-sort them
+        const uint64_t top = prefix >> shift;
+        for (uint32_t j = tid; j < C; j += blockDim.x) {
+            const uint64_t key = keys[j];
+            if (key != kSentinel && (key >> shift) <= top) {
+                const uint32_t at = atomicAdd(&s_nsel, 1u);
+                if (at < sel_cap) sel[at] = key;
+            }
+        }
+        __syncthreads();
+        uint32_t n2 = 1;
+        while (n2 < kk) n2 <<= 1;
+        for (uint32_t i = kk + tid; i < n2; i += blockDim.x) sel[i] = kSentinel;
+        __syncthreads();
+        for (uint32_t size = 2; size <= n2; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = tid; i < n2 / 2; i += blockDim.x) {
+                    const uint32_t a = 2 * i - (i & (stride - 1));
+                    const uint32_t b = a + stride;
+                    const bool up = (a & size) == 0;
+                    const uint64_t x = sel[a], y = sel[b];
+                    if ((x > y) == up) {
+                        sel[a] = y;
+                        sel[b] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    for (uint32_t i = tid; i < k; i += blockDim.x) {
+        uint32_t id = 0xFFFFFFFFu;
+        float d = __uint_as_float(0x7F800000u);
+        if (i < kk) {
+            id = (uint32_t)(sel[i] & 0xFFFFFFFFu);
+            d = unorderable((uint32_t)(sel[i] >> 32));
+        }
+        out_ids[q * k + i] = id;
+        out_dists[q * k + i] = d;
+    }
+    if (tid == 0) out_counts[q] = kk;
+}
+
+namespace {
+uint32_t sel_cap_for(const DevParams& p, uint32_t k) {
+    const uint32_t kk = k < p.budget ? k : p.budget;
+    return next_pow2(kk > 0 ? kk : 1);
+}
+
+template <int LT, int PW>
+void set_rerank_attr() {
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_kernel<LT, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024));
+}
+}  // namespace
+
+size_t rerank_smem(const DevParams& p, uint32_t k) {
+    return 8ull * p.budget + 8ull * sel_cap_for(p, k) + 4ull * p.L * p.k1 + 4ull * p.L * p.npairs +
+           4ull * p.npairs + 4ull * p.budget;
+}
+
+void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
+                   float* dists, uint32_t* counts, cudaStream_t s) {
+    const size_t sm = rerank_smem(p, k);
+    const uint32_t cap = sel_cap_for(p, k);
+#define PQTG_RERANK(LT, PW)                                                                          \
+    rerank_kernel<LT, PW><<<(unsigned)nq, kThreads, sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \
+                                                             ws.ncand, ids, dists, counts)
+    if (p.pw == 1) {
+        switch (p.L) {
+        case 16: PQTG_RERANK(16, 1); break;
+        case 32: PQTG_RERANK(32, 1); break;
+        case 64: PQTG_RERANK(64, 1); break;
+        case 120: PQTG_RERANK(120, 1); break;
+        default: PQTG_RERANK(0, 1); break;
+        }
+    } else {
+        switch (p.L) {
+        case 32: PQTG_RERANK(32, 2); break;
+        default: PQTG_RERANK(0, 2); break;
+        }
+    }
+#undef PQTG_RERANK
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+void configure_kernels(const DevParams& p, uint32_t) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        PQTG_CUDA_CHECK(cudaFuncSetAttribute(traverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        set_rerank_attr<16, 1>();
+        set_rerank_attr<32, 1>();
+        set_rerank_attr<64, 1>();
+        set_rerank_attr<120, 1>();
+        set_rerank_attr<0, 1>();
+        set_rerank_attr<32, 2>();
+        set_rerank_attr<0, 2>();
+    });
+    (void)p;
+}
+
+// =====================================================================================
+// Per-shard top-k merge: G sorted lists per query -> global top-k by (dist, id).
+// =====================================================================================
+__global__ void merge_topk_kernel(uint32_t G, uint64_t nq, uint32_t k, const uint32_t* __restrict__ ids,
+                                  const float* __restrict__ dists, const uint32_t* __restrict__ counts,
+                                  uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
+                                  uint32_t* __restrict__ out_counts) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    uint32_t cur[16];
+    for (uint32_t g = 0; g < G; ++g) cur[g] = 0;
+    uint32_t out = 0;
+    while (out < k) {
+        int best = -1;
+        uint64_t bk = kSentinel;
+        for (uint32_t g = 0; g < G; ++g) {
+            if (cur[g] < counts[g * nq + q]) {
+                const uint64_t off = ((uint64_t)g * nq + q) * k + cur[g];
+                const uint64_t key = ((uint64_t)orderable(dists[off]) << 32) | ids[off];
+                if (best < 0 || key < bk) {
+                    best = (int)g;
+                    bk = key;
+                }
+            }
+        }
+        if (best < 0) break;
+        const uint64_t off = ((uint64_t)best * nq + q) * k + cur[best];
+        out_ids[q * k + out] = ids[off];
+        out_dists[q * k + out] = dists[off];
+        ++cur[best];
+        ++out;
+    }
+    for (uint32_t i = out; i < k; ++i) {
+        out_ids[q * k + i] = 0xFFFFFFFFu;
+        out_dists[q * k + i] = __uint_as_float(0x7F800000u);
+    }
+    out_counts[q] = out;
+}
+
+void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids, const float* dists,
+                  const uint32_t* counts, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
+                  cudaStream_t s) {
+    if (nq == 0) return;
+    const unsigned blocks = (unsigned)((nq + 127) / 128);
+    merge_topk_kernel<<<blocks, 128, 0, s>>>(shards, nq, k, ids, dists, counts, out_ids, out_dists, out_counts);
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace pqtg

@@ -1,0 +1,171 @@
+// pqtg_internal.h — device index layout, workspace and kernel launch interface.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pqtg.h"
+
+namespace pqtg {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+const char* last_error();
+
+struct Error {
+    int status;
+    std::string msg;
+};
+
+#define PQTG_CUDA_CHECK(expr)                                                              \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess) {                                                           \
+            throw ::pqtg::Error{PQTG_ERR_CUDA, std::string(#expr) + ": " +                 \
+                                                   cudaGetErrorString(_e)};                \
+        }                                                                                  \
+    } while (0)
+
+// ---------------------------------------------------------------- constants
+constexpr uint32_t kSlopeTables = 10;      // binorder.hpp:25
+constexpr uint32_t kSlopeOne = 5;          // slope 1.08^0 (binorder.cpp:59-64, :237)
+constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
+
+// Everything a kernel needs, passed by value (fits the parameter space).
+struct DevParams {
+    // config
+    uint32_t D, P, k1, k2, w, L, m, fd, per_part, W, npairs, pw, row_bytes;
+    uint32_t budget;            // min(candidate_budget, n) (search.cpp:148)
+    uint32_t resort;            // resort_bins
+    uint64_t H;                 // slots
+    uint64_t n;
+    uint64_t shard_lo, shard_hi;  // positions re-ranked here
+    uint64_t mult[4];           // (k1*k2)^p mod 2^64 (pqtree.cpp:12-21)
+    uint64_t total_tuples;      // W^P: stream length (BinStream::total)
+    double inv_log108;          // 1 / log(1.08), host glibc value
+    double log108;
+    uint32_t h_pow2;            // H is a power of two
+    uint32_t mod_fast;          // (k1k2)^P < 2^64 and H < 2^32: slot by sum of reduced terms
+    // static bin-order streams
+    const uint32_t* pair_streams;  // [10][W*W] (a | b << 16), PairCursor order per table
+    const uint2* merge;            // [merge_count] (u, v) for P == 4
+    uint64_t merge_count;
+    uint64_t merge_row0;           // first closed-form sweep row
+    uint64_t W2;
+    // arrays
+    const float* fine_t;        // [L][fd][k1]
+    const float* l2_t;          // [P][k1][m][k2]
+    const uint32_t* pairs;      // [npairs] (i | j << 16)
+    const float* c2;            // [L][npairs]  d2[f][i][j] per pair
+    const uint32_t* bitmap;     // [ceil(H / 32)] non-empty slots
+    const uint32_t* offsets;    // [H + 1] u32
+    const uint32_t* ids;        // [shard positions]
+    const uint8_t* codes;       // [shard positions][row_bytes]
+};
+
+struct DevIndex {
+    pqtg_config cfg{};
+    uint64_t n = 0;
+    int device = 0;
+    DevParams prm{};
+    uint64_t bytes = 0;
+    std::vector<void*> allocations;
+    ~DevIndex();
+};
+
+struct Workspace {
+    const DevIndex* index = nullptr;
+    uint64_t max_batch = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t last_stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t last_nq = 0;
+    // per-query intermediates
+    float* fine = nullptr;        // [B][L][k1]
+    float* l2_dist = nullptr;     // [B][P][W]
+    uint32_t* l2_code = nullptr;  // [B][P][W]
+    uint8_t* slope = nullptr;     // [B][2]
+    uint2* ranges = nullptr;      // [B][budget] (start position, candidate offset)
+    uint32_t* nranges = nullptr;  // [B]
+    uint32_t* ncand = nullptr;    // [B]
+    // host-call staging (grown on demand)
+    float* d_queries = nullptr;
+    uint32_t* d_ids = nullptr;
+    float* d_dists = nullptr;
+    uint32_t* d_counts = nullptr;
+    pqtg_query_stats* d_stats = nullptr;
+    uint64_t stage_k = 0;
+    std::mutex mu;
+    std::vector<void*> allocations;
+    ~Workspace();
+};
+
+// ---------------------------------------------------------------- host helpers
+template <class T>
+T* dev_alloc(std::vector<void*>& owner, uint64_t count, uint64_t* bytes = nullptr) {
+    void* p = nullptr;
+    size_t sz = count * sizeof(T);
+    if (sz == 0) sz = 16;
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e != cudaSuccess) {
+        throw Error{PQTG_ERR_OOM, "cudaMalloc(" + std::to_string(sz) + "): " + cudaGetErrorString(e)};
+    }
+    owner.push_back(p);
+    if (bytes) *bytes += sz;
+    return static_cast<T*>(p);
+}
+
+// Source arrays for building a device index (a view, or a parsed PQTINDEX file).
+struct Source {
+    pqtg_config cfg{};
+    uint64_t n = 0;
+    const float* level1 = nullptr;
+    const float* level2 = nullptr;
+    const float* d2 = nullptr;
+    uint32_t table_count = 0, table_len = 0;
+    const double* slopes = nullptr;
+    const uint32_t* entries = nullptr;
+    const uint64_t* offsets = nullptr;
+    const uint32_t* ids = nullptr;
+    // line codes: SoA (view) or interleaved records (file: (lambda, pair) per record)
+    const uint8_t* lambda_q = nullptr;
+    const uint16_t* pair_id = nullptr;
+    const uint8_t* records = nullptr;
+    uint32_t record_pw = 0;
+};
+
+// Static bin-order streams of one index (host copy; uploaded into DevParams).
+struct HostStreams {
+    uint32_t W = 0, P = 0;
+    uint64_t W2 = 0, total = 0, merge_row0 = 0;
+    std::vector<uint32_t> pair;  // [10][W2] (a | b << 16)
+    std::vector<uint2> merge;    // P == 4: materialized merge prefix
+    void tuple_at(uint64_t s, uint32_t ta, uint32_t tb, uint32_t* ranks) const;
+};
+HostStreams build_streams(const uint32_t* entries, uint32_t table_len, uint32_t W, uint32_t P);
+[[noreturn]] void unsupported(const std::string& m);
+[[noreturn]] void format(const std::string& m);
+
+DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, uint64_t shard_hi);
+void validate_config(const pqtg_config& c);
+
+// ---------------------------------------------------------------- kernels (kernels.cu)
+size_t traverse_smem(const DevParams& p);
+size_t binsel_smem(const DevParams& p);
+size_t rerank_smem(const DevParams& p, uint32_t k);
+void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, Workspace& ws,
+                     cudaStream_t s);
+void launch_binsel(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats,
+                   cudaStream_t s);
+void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
+                   float* dists, uint32_t* counts, cudaStream_t s);
+void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids,
+                  const float* dists, const uint32_t* counts, uint32_t* out_ids,
+                  float* out_dists, uint32_t* out_counts, cudaStream_t s);
+void configure_kernels(const DevParams& p, uint32_t k);
+
+}  // namespace pqtg

@@ -1,0 +1,216 @@
+"""Python mirror of the reference query API over the C-ABI (include/pqtg.h).
+
+    index = load_index(path)                       # pqt::load_index        (index_io.hpp:16)
+    results = knn_query_batch(index, queries, k)   # pqt::knn_query_batch   (search.hpp:83)
+    result = knn_query(index, y, k)                # pqt::knn_query         (search.hpp:80)
+
+Same names, argument meaning and error behaviour as the reference: a query-dimension
+mismatch raises ValueError (std::invalid_argument, search.cpp:264-266), a malformed
+container raises FormatError (index_io.cpp), k == 0 or an empty index gives empty results,
+and fewer than k candidates give short results. Everything runs in libpqtg.so on the GPU;
+there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import sys
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import PqtgError, PqtgIndexInfo, check, lib
+from .index import FormatError, HostIndex, PqtConfig
+
+
+@dataclass
+class QueryStats:
+    """pqt::QueryStats (search.hpp:15-23); *_us are per-query shares of the batch's stage times."""
+
+    bins_visited: int = 0
+    candidates: int = 0
+    exact_evals: int = 0
+    traversal_us: float = 0.0
+    bin_selection_us: float = 0.0
+    vector_proposal_us: float = 0.0
+    rerank_us: float = 0.0
+
+
+@dataclass
+class QueryResult:
+    ids: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    dists: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+    stats: QueryStats = field(default_factory=QueryStats)
+
+
+_warned_missing_db = False
+
+
+def _warn_missing_database():
+    # search.cpp:25-32: one-time warning when rerank_exact > 0 but no raw vectors are attached
+    global _warned_missing_db
+    if not _warned_missing_db:
+        _warned_missing_db = True
+        sys.stderr.write("pqt: rerank_exact > 0 but no raw vectors attached; exact re-ranking disabled\n")
+
+
+def _raise(e: PqtgError):
+    if e.status == -1 or e.status == -2:
+        raise ValueError(str(e)) from None
+    if e.status == -3:
+        raise FormatError(str(e)) from None
+    raise e
+
+
+class DeviceIndex:
+    """A PQT index resident in one GPU's HBM (pqtg_index), plus a workspace for searches."""
+
+    def __init__(self, source: "HostIndex | str", device: int = 0, shard: tuple[int, int] = (0, 0),
+                 max_batch: int = 16384):
+        L = lib()
+        h = C.c_void_p()
+        try:
+            if isinstance(source, HostIndex):
+                view = source.view(*shard)
+                check(L.pqtg_index_create(C.byref(view), device, C.byref(h)))
+            else:
+                check(L.pqtg_index_load(str(source).encode(), device, shard[0], shard[1], C.byref(h)))
+        except PqtgError as e:
+            _raise(e)
+        self._h = h
+        info = PqtgIndexInfo()
+        check(L.pqtg_index_info_get(h, C.byref(info)))
+        self.info = info
+        self.config = PqtConfig.from_c(info.config)
+        self.n = int(info.n)
+        self.device = device
+        self.max_batch = int(max_batch)
+        ws = C.c_void_p()
+        check(L.pqtg_workspace_create(h, self.max_batch, C.byref(ws)))
+        self._ws = ws
+
+    def close(self):
+        L = _abi._LIB
+        if L is not None:
+            if getattr(self, "_ws", None):
+                L.pqtg_workspace_destroy(self._ws)
+                self._ws = None
+            if getattr(self, "_h", None):
+                L.pqtg_index_destroy(self._h)
+                self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def size(self) -> int:
+        return self.n
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def workspace(self):
+        return self._ws
+
+    # ---- host-buffer search (pqtg_search) --------------------------------------------
+    def search(self, queries: np.ndarray, k: int):
+        """Returns (ids [nq,k] u32, dists [nq,k] f32, counts [nq] u32, stats [nq,3] u64)."""
+        q = np.ascontiguousarray(queries, np.float32)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        nq, dim = q.shape
+        kk = max(int(k), 1)
+        ids = np.empty((nq, kk), np.uint32)
+        dists = np.empty((nq, kk), np.float32)
+        counts = np.zeros(nq, np.uint32)
+        stats = np.zeros((nq, 3), np.uint64)
+        try:
+            check(lib().pqtg_search(self._h, self._ws, q.ctypes.data if nq else None, nq, dim, int(k),
+                                    ids.ctypes.data, dists.ctypes.data, counts.ctypes.data,
+                                    stats.ctypes.data))
+        except PqtgError as e:
+            _raise(e)
+        return ids[:, :k], dists[:, :k], counts, stats
+
+    # ---- device-buffer search (pqtg_search_device) -------------------------------------
+    def search_device(self, d_queries: int, nq: int, k: int, d_ids: int, d_dists: int, d_counts: int,
+                      d_stats: int | None = None, stream: int | None = None) -> None:
+        check(lib().pqtg_search_device(self._h, self._ws, d_queries, nq, k, d_ids, d_dists, d_counts,
+                                       d_stats, stream))
+
+    def stage_ms(self) -> list[float]:
+        ms = (C.c_float * 4)()
+        check(lib().pqtg_workspace_stage_ms(self._ws, ms))
+        return list(ms)
+
+    def intermediates(self, nq: int) -> dict:
+        """Per-query intermediates of the last searched sub-batch (for per-stage parity)."""
+        c = self.config
+        W = c.w * c.k2
+        budget = min(c.candidate_budget, self.n)
+        fine = np.zeros((nq, c.p_line, c.k1), np.float32)
+        l2c = np.zeros((nq, c.p_tree, W), np.uint32)
+        l2d = np.zeros((nq, c.p_tree, W), np.float32)
+        slope = np.zeros((nq, 2), np.uint8)
+        pos = np.zeros((nq, max(budget, 1)), np.uint32)
+        nc = np.zeros(nq, np.uint32)
+        check(lib().pqtg_workspace_read(self._ws, nq, fine.ctypes.data, l2c.ctypes.data, l2d.ctypes.data,
+                                        slope.ctypes.data, pos.ctypes.data, nc.ctypes.data))
+        return dict(fine=fine, l2_parent=l2c >> 16, l2_child=l2c & 0xFFFF, l2_dist=l2d, slope=slope,
+                    positions=[pos[i, : nc[i]] for i in range(nq)], ncand=nc)
+
+
+def load_index(path: str, device: int = 0, shard: tuple[int, int] = (0, 0)) -> DeviceIndex:
+    """pqt::load_index: read a PQTINDEX v1 file straight into GPU memory."""
+    return DeviceIndex(path, device=device, shard=shard)
+
+
+def knn_query_batch(index: DeviceIndex, queries: np.ndarray, k: int, threads: int = 0) -> list[QueryResult]:
+    """pqt::knn_query_batch (search.cpp:262-274). `threads` is accepted for API parity."""
+    q = np.asarray(queries, np.float32)
+    if q.ndim == 1:
+        q = q.reshape(1, -1)
+    if q.shape[0] > 0 and q.shape[1] != index.config.dim:
+        raise ValueError("knn_query_batch: query dimension mismatch")
+    if index.config.rerank_exact > 0 and k > 0 and index.n > 0 and q.shape[0] > 0:
+        _warn_missing_database()
+    ids, dists, counts, stats = index.search(q, k)
+    ms = index.stage_ms() if q.shape[0] else [0.0] * 4
+    per = 1000.0 / max(q.shape[0], 1)
+    out = []
+    for i in range(q.shape[0]):
+        c = int(counts[i])
+        st = QueryStats(int(stats[i, 0]), int(stats[i, 1]), int(stats[i, 2]),
+                        ms[0] * per, ms[1] * per * 0.5, ms[1] * per * 0.5, ms[2] * per)
+        out.append(QueryResult(ids[i, :c].copy(), dists[i, :c].copy(), st))
+    return out
+
+
+def knn_query(index: DeviceIndex, y: np.ndarray, k: int) -> QueryResult:
+    """pqt::knn_query (search.cpp:126-260) for one query vector."""
+    y = np.asarray(y, np.float32).reshape(1, -1)
+    return knn_query_batch(index, y, k)[0]
+
+
+def merge_topk_host(ids: np.ndarray, dists: np.ndarray, counts: np.ndarray):
+    """Merge per-shard top-k lists [G, nq, k] by (dist, id) via pqtg_merge_topk_host."""
+    ids = np.ascontiguousarray(ids, np.uint32)
+    dists = np.ascontiguousarray(dists, np.float32)
+    counts = np.ascontiguousarray(counts, np.uint32)
+    G, nq, k = ids.shape
+    oi = np.empty((nq, k), np.uint32)
+    od = np.empty((nq, k), np.float32)
+    oc = np.empty(nq, np.uint32)
+    check(lib().pqtg_merge_topk_host(G, nq, k, ids.ctypes.data, dists.ctypes.data, counts.ctypes.data,
+                                     oi.ctypes.data, od.ctypes.data, oc.ctypes.data))
+    return oi, od, oc
+
+
+def shard_range(n: int, shards: int, rank: int) -> tuple[int, int]:
+    lo, hi = C.c_uint64(), C.c_uint64()
+    check(lib().pqtg_shard_range(n, shards, rank, C.byref(lo), C.byref(hi)))
+    return int(lo.value), int(hi.value)

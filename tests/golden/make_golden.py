@@ -1,0 +1,76 @@
+"""Generate the golden fixtures under tests/golden/ from the REFERENCE ITSELF.
+
+Runs only in the build container (needs oracle/_ref/libpqtref.so, i.e. the reference sources
+compiled in place by oracle/Makefile). For each case it:
+  1. draws data with the reference's synth_clustered (bench.cpp:66-95),
+  2. builds the index with the reference's IndexBuilder (search.cpp:52-117),
+  3. saves it with the reference's save_index (index_io.cpp:94-146) -> <name>.pqt,
+  4. records the reference's knn_query_batch outputs (ids, dists, counts, stats), its
+     traverse() outputs for the first queries and heuristic_order() prefixes -> <name>.npz.
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parents[1]))
+
+from oracle.bindings import Ref  # noqa: E402
+from paper_1702_05911_b200.index import PqtConfig  # noqa: E402
+
+# name: (config, n, nq, k, blobs, seed)
+CASES = {
+    "p2_small": (dict(dim=32, p_tree=2, k1=8, k2=4, w=2, p_line=8, hash_size=2048, candidate_budget=256), 4000, 64, 20, 48, 11),
+    "p4_small": (dict(dim=32, p_tree=4, k1=8, k2=4, w=2, p_line=8, hash_size=4096, candidate_budget=256), 4000, 64, 20, 48, 12),
+    "p1_small": (dict(dim=16, p_tree=1, k1=16, k2=4, w=4, p_line=4, hash_size=1024, candidate_budget=200), 3000, 48, 10, 32, 13),
+    "p2_resort": (dict(dim=32, p_tree=2, k1=8, k2=4, w=3, p_line=8, hash_size=1500, candidate_budget=200, resort_bins=True), 4000, 64, 20, 48, 14),
+    "p2_wide": (dict(dim=32, p_tree=2, k1=24, k2=4, w=3, p_line=8, hash_size=4096, candidate_budget=256), 4000, 48, 20, 48, 15),
+    "p2_sift": (dict(dim=128, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=512), 5000, 48, 100, 64, 16),
+    "p4_gist": (dict(dim=96, p_tree=4, k1=16, k2=8, w=4, p_line=32, candidate_budget=512), 5000, 32, 50, 64, 17),
+}
+
+
+def make(name: str) -> None:
+    cfgd, n, nq, k, blobs, seed = CASES[name]
+    cfg = PqtConfig(train_iters=10, seed=seed, **cfgd)
+    X = Ref.synth(n + nq, cfg.dim, blobs, 20.0, seed)
+    db, Q = X[:n], X[n:]
+    ref = Ref.build(db, db, cfg, threads=8)
+    path = HERE / f"{name}.pqt"
+    ref.save(str(path))
+    ref = Ref.load(str(path))  # everything below runs on the loaded index, as in the GPU path
+    ids, dists, counts, stats = ref.knn(Q, k, threads=4)
+    ntrav = min(nq, 8)
+    trav = [ref.traverse(Q[i]) for i in range(ntrav)]
+    W = cfg.w * cfg.k2
+    orders = [ref.heuristic_order(t["l2_dist"], 4096) for t in trav]
+    np.savez_compressed(
+        HERE / f"{name}.npz",
+        queries=Q, k=np.array(k), ids=ids, dists=dists, counts=counts, stats=stats,
+        fine=np.stack([t["fine"] for t in trav]),
+        l1_id=np.stack([t["l1_id"] for t in trav]), l1_dist=np.stack([t["l1_dist"] for t in trav]),
+        l2_parent=np.stack([t["l2_parent"] for t in trav]), l2_child=np.stack([t["l2_child"] for t in trav]),
+        l2_dist=np.stack([t["l2_dist"] for t in trav]),
+        order_len=np.array([len(o) for o in orders]),
+        orders=np.concatenate(orders, axis=0) if orders else np.zeros((0, cfg.p_tree), np.uint32),
+        list_len=np.array(W),
+    )
+    print(name, "n", n, "bytes", path.stat().st_size, "mean C", stats[:, 1].mean(), "bins", stats[:, 0].mean())
+
+
+def main() -> None:
+    names = sys.argv[1:] or list(CASES)
+    for name in names:
+        make(name)
+    (HERE / "CASES.json").write_text(json.dumps({k: dict(config=v[0], n=v[1], nq=v[2], k=v[3], blobs=v[4], seed=v[5])
+                                                 for k, v in CASES.items()}, indent=1))
+
+
+if __name__ == "__main__":
+    main()

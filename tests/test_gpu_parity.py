@@ -1,0 +1,130 @@
+"""CUDA path vs the reference (golden fixtures) and vs the C oracle, through the C-ABI.
+
+Bar: candidate positions, bins_visited, candidates, neighbour ids and distances all
+bit-exact (the kernels follow the reference's fp32 operation order; the only documented
+near-tie class is pick_slope_table's fp64 log rounding, never hit at these shapes)."""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, GOLDEN_CASES, load_golden
+from oracle.bindings import Oracle
+from paper_1702_05911_b200 import DeviceIndex, HostIndex, knn_query_batch, merge_topk_host, shard_range
+
+pytestmark = pytest.mark.gpu
+
+
+def assert_same_results(a, b, ctx=""):
+    ids_a, d_a, c_a, s_a = a
+    ids_b, d_b, c_b, s_b = b
+    assert np.array_equal(c_a, c_b), ctx + " counts"
+    assert np.array_equal(s_a, s_b), ctx + " stats"
+    for q in range(len(c_a)):
+        c = c_a[q]
+        assert np.array_equal(ids_a[q, :c], ids_b[q, :c]), f"{ctx} ids q={q}"
+        assert np.array_equal(d_a[q, :c].view(np.uint32), d_b[q, :c].view(np.uint32)), f"{ctx} dists q={q}"
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+@pytest.mark.parametrize("source", ["file", "view"])
+def test_gpu_matches_reference_golden(name, source):
+    g = load_golden(name)
+    path = str(GOLDEN / f"{name}.pqt")
+    dev = DeviceIndex(path if source == "file" else HostIndex.load(path))
+    k = int(g["k"])
+    got = dev.search(g["queries"], k)
+    assert_same_results(got, (g["ids"], g["dists"], g["counts"], g["stats"]), name)
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_gpu_stages_match_reference(name):
+    """Per stage: traversal LUT + level-2 lists, slope pick, gathered candidate positions."""
+    g = load_golden(name)
+    path = str(GOLDEN / f"{name}.pqt")
+    dev = DeviceIndex(path)
+    o = Oracle(path)
+    Q = g["queries"]
+    dev.search(Q, int(g["k"]))
+    inter = dev.intermediates(len(Q))
+    ntrav = g["fine"].shape[0]
+    for i in range(ntrav):
+        assert np.array_equal(inter["fine"][i].view(np.uint32), g["fine"][i].view(np.uint32))
+        assert np.array_equal(inter["l2_parent"][i], g["l2_parent"][i])
+        assert np.array_equal(inter["l2_child"][i], g["l2_child"][i])
+        assert np.array_equal(inter["l2_dist"][i].view(np.uint32), g["l2_dist"][i].view(np.uint32))
+    for i in range(len(Q)):
+        pos, bins = o.candidates(Q[i])
+        assert np.array_equal(inter["positions"][i], pos), f"q={i}"
+        assert int(g["stats"][i, 0]) == bins
+
+
+@pytest.mark.parametrize("name", ["p2_sift", "p4_gist", "p2_wide"])
+@pytest.mark.parametrize("shards", [2, 3])
+def test_gpu_sharded_merge_equals_unsharded(name, shards):
+    g = load_golden(name)
+    path = str(GOLDEN / f"{name}.pqt")
+    k = int(g["k"])
+    n = HostIndex.load(path).n
+    parts = []
+    for r in range(shards):
+        lo, hi = shard_range(n, shards, r)
+        dev = DeviceIndex(path, shard=(lo, hi))
+        parts.append(dev.search(g["queries"], k))
+    ids = np.stack([p[0] for p in parts])
+    dists = np.stack([p[1] for p in parts])
+    counts = np.stack([p[2] for p in parts])
+    for p in parts:  # bin selection is global on every shard
+        assert np.array_equal(p[3], g["stats"])
+    mi, md, mc = merge_topk_host(ids, dists, counts)
+    assert_same_results((mi, md, mc, g["stats"]), (g["ids"], g["dists"], g["counts"], g["stats"]), name)
+
+
+def test_gpu_edge_cases():
+    path = str(GOLDEN / "p2_small.pqt")
+    g = load_golden("p2_small")
+    dev = DeviceIndex(path)
+    Q = g["queries"]
+    o = Oracle(path)
+    # k == 0 -> empty results and zero stats (search.cpp:130-132)
+    ids, d, c, s = dev.search(Q, 0)
+    assert (c == 0).all() and (s == 0).all()
+    # k larger than the candidate count -> short results (search.cpp:251)
+    got = dev.search(Q, 1000)
+    want = o.knn(Q, 1000)
+    assert_same_results(got, want, "k>C")
+    assert (got[2] <= got[3][:, 1]).all()
+    # dists non-decreasing
+    for q in range(len(Q)):
+        dd = got[1][q, : got[2][q]]
+        assert (np.diff(dd) >= 0).all()
+    # empty batch
+    ids, d, c, s = dev.search(Q[:0], 10)
+    assert c.shape == (0,)
+    # dimension mismatch -> ValueError (std::invalid_argument)
+    with pytest.raises(ValueError):
+        dev.search(np.zeros((2, 31), np.float32), 5)
+    # a query equal to a database vector: reference-identical answer
+    hix = HostIndex.load(path)
+    assert hix.n == 4000
+
+
+def test_gpu_knn_query_batch_api():
+    path = str(GOLDEN / "p4_small.pqt")
+    g = load_golden("p4_small")
+    dev = DeviceIndex(path)
+    res = knn_query_batch(dev, g["queries"], int(g["k"]))
+    for q, r in enumerate(res):
+        c = g["counts"][q]
+        assert np.array_equal(r.ids, g["ids"][q, :c])
+        assert r.stats.bins_visited == g["stats"][q, 0]
+        assert r.stats.candidates == g["stats"][q, 1]
+
+
+def test_gpu_batching_is_deterministic():
+    """Sub-batching (max_batch) and repeated runs give identical results."""
+    path = str(GOLDEN / "p4_gist.pqt")
+    g = load_golden("p4_gist")
+    Q = np.concatenate([g["queries"]] * 5)
+    a = DeviceIndex(path, max_batch=7).search(Q, 50)
+    b = DeviceIndex(path, max_batch=4096).search(Q, 50)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
