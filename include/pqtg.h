@@ -179,6 +179,20 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* ws, const float* d_que
 int64_t pqtg_bin_stream_host(const pqtg_index_view* view, const float* lists, uint64_t max_tuples,
                              uint32_t* out);
 
+/* ---- offline build on the GPU -------------------------------- */
+/* For n database vectors d_x (n × dim, device) compute, in the reference's exact fp32 order:
+ *   d_part_codes  n × p_tree   flat per-part bin code i1*k2+i2   (assign_bin, pqtree.cpp:27-38)
+ *   d_slots       n            global_code % hash_size (global_code when hash_size == 0)
+ *                                                                (pqtree.cpp:12-25)
+ *   d_lambda/d_pair n × p_line line codes                         (encode_line, linequant.cpp:84-152)
+ * Codebooks are device arrays in the view layouts (level1, level2); d_fine is the p_line × k1 ×
+ * fine_dim slice table, d_fine_sq its |slice|^2 (linequant.cpp:13-46), d_d2 the pair table
+ * (linequant.cpp:60-75). Asynchronous on `stream`. */
+int pqtg_build_codes(const pqtg_config* cfg, const float* d_level1, const float* d_level2,
+                     const float* d_fine, const float* d_fine_sq, const float* d_d2, const float* d_x,
+                     uint64_t n, uint32_t* d_part_codes, uint64_t* d_slots, uint8_t* d_lambda,
+                     uint16_t* d_pair, void* stream);
+
 /* ---- multi-GPU helpers ------------------------------------------------------------ */
 /* Merge G per-shard top-k lists (each nq × k, counts per query) into the global top-k by
  * ascending (dist, id). Host-side; inputs laid out shard-major: ids[g][q][k]. */

@@ -104,6 +104,7 @@ SIGNATURES = {
     "pqtg_workspace_read": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pqtg_search": (C.c_int, [_vp, _vp, _vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp]),
     "pqtg_search_device": (C.c_int, [_vp, _vp, _vp, _u64, _u32, _vp, _vp, _vp, _vp, _vp]),
+    "pqtg_build_codes": (C.c_int, [C.POINTER(PqtgConfig), _vp, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
     "pqtg_bin_stream_host": (C.c_int64, [C.POINTER(PqtgIndexView), _vp, _u64, _vp]),
     "pqtg_merge_topk_host": (C.c_int, [_u32, _u64, _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pqtg_merge_topk_device": (C.c_int, [_u32, _u64, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: belt and braces — every exact fp32 op is already an explicit __f*_rn intrinsic.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-CU_SOURCES = ["kernels.cu"]
+CU_SOURCES = ["kernels.cu", "build_kernels.cu"]
 CXX_SOURCES = ["api.cpp", "index_prep.cpp", "pqt_dropin.cpp"]
 
 
@@ -54,8 +54,6 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         objs.append(obj)
         if force or _stale(obj, [path, *headers, Path(__file__)]):
             cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-I", str(REPO / "include"), "-c", str(path), "-o", str(obj)]
-            if src.endswith(".cpp"):
-                cmd[1:1] = ["-x", "cu"] if False else []
             out = _run(cmd)
             if verbose and out.strip():
                 print(out)

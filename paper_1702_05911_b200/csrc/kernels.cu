@@ -698,10 +698,21 @@ uint32_t sel_cap_for(const DevParams& p, uint32_t k) {
     return next_pow2(kk > 0 ? kk : 1);
 }
 
+// Opt in to the largest dynamic shared memory the kernel can take next to its static part.
+template <class K>
+void allow_max_smem(K kernel) {
+    cudaFuncAttributes a{};
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, kernel));
+    int dev = 0, optin = 0;
+    PQTG_CUDA_CHECK(cudaGetDevice(&dev));
+    PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         optin - (int)a.sharedSizeBytes));
+}
+
 template <int LT, int PW>
 void set_rerank_attr() {
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_kernel<LT, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024));
+    allow_max_smem(rerank_kernel<LT, PW>);
 }
 }  // namespace
 
@@ -736,11 +747,14 @@ void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, u
 }
 
 void configure_kernels(const DevParams& p, uint32_t) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        PQTG_CUDA_CHECK(cudaFuncSetAttribute(traverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    // function attributes are per device: configure each device once
+    static std::once_flag once[64];
+    int dev = 0;
+    PQTG_CUDA_CHECK(cudaGetDevice(&dev));
+    std::call_once(once[dev & 63], [] {
+        allow_max_smem(traverse_kernel);
+        allow_max_smem(binsel_kernel<4, false>);
+        allow_max_smem(binsel_kernel<16, true>);
         set_rerank_attr<16, 1>();
         set_rerank_attr<32, 1>();
         set_rerank_attr<64, 1>();
