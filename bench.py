@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""bench.py — PQT online-query throughput on B200 (queries/s), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload gist1m|sift1m|deep10m]
+    python bench.py --impl reference ...      # the reference's own CPU path (oracle/_ref)
+
+A step = one pass of the hot path (traverse → bin selection/gather → line-quantized re-rank →
+top-k) over one query batch of the workload. Default workload = BASELINE.json configs[1]
+(GIST1M-shaped: 1M × 960-D, P=4, 1k queries, top-100). Data are synthetic clustered vectors
+(the reference's synth_clustered distribution) and an index trained/encoded on the GPU by
+paper_1702_05911_b200.builder (the reference's exact assign_bin / encode_line / inverted-list
+layout); the same index feeds every arm. The index (≈ 85 MB of HBM for gist1m) fits in L2,
+so L2 is flushed (256 MiB write) between timed steps, outside the timed intervals.
+
+  value        device-resident: queries already in HBM, pqtg_search_device on the current
+               stream, CUDA events around each step, summed over K steps, max over ranks.
+  e2e          pqtg_search with pinned host buffers: H2D of the queries, the three kernels,
+               D2H of ids/dists/counts/stats, all inside the (host-clocked) timed call.
+  roofline     the dominant kernel (largest mean event time): algorithmic bytes per launch
+                ÷ its mean launch time, against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline the reference compiled in place (oracle/_ref; else the C restatement) on this
+               host's cores over the same batch, with a parity check of the GPU results.
+Multi-GPU (torchrun): every rank holds a replica and processes its own batches (no data-path
+collective): "scaling": "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "queries/sec at fixed recall@1/@100 vs CPU oracle (1/2/4/8 B200); HBM GB/s"
+
+WORKLOADS = {
+    # BASELINE.json configs[1]
+    "gist1m": dict(config=dict(dim=960, p_tree=4, k1=16, k2=8, w=4, p_line=32, candidate_budget=4096),
+                   n=1_000_000, nq=1000, k=100, blobs=1024, sigma=20.0, ntrain=100_000),
+    # BASELINE.json configs[0]
+    "sift1m": dict(config=dict(dim=128, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=4096),
+                   n=1_000_000, nq=10000, k=100, blobs=1024, sigma=20.0, ntrain=100_000),
+    # a DEEP-shaped single-GPU config at 10M (configs[2] shape at 1/10 scale)
+    "deep10m": dict(config=dict(dim=96, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=4096),
+                    n=10_000_000, nq=10000, k=100, blobs=10_000, sigma=20.0, ntrain=100_000),
+}
+CACHE = Path(os.environ.get("PQTG_BENCH_CACHE", "/tmp/pqtg_bench"))
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- workload
+def workload_files(name: str, seed: int):
+    CACHE.mkdir(parents=True, exist_ok=True)
+    return CACHE / f"{name}_s{seed}.pqt", CACHE / f"{name}_s{seed}_queries.npy"
+
+
+def make_workload(name: str, seed: int, device: int, batches: int):
+    """Build (or load the cached) index + query pool for `name` on cuda:device."""
+    import torch
+
+    from paper_1702_05911_b200 import builder
+    from paper_1702_05911_b200.index import HostIndex, PqtConfig
+
+    wl = WORKLOADS[name]
+    ipath, qpath = workload_files(name, seed)
+    nq_pool = wl["nq"] * batches
+    if ipath.exists() and qpath.exists() and np.load(qpath, mmap_mode="r").shape[0] >= nq_pool:
+        log(f"[bench] loading cached {ipath}")
+        return HostIndex.load(str(ipath)), np.load(qpath)[:nq_pool]
+    t0 = time.time()
+    cfg = PqtConfig(train_iters=15, seed=seed, **wl["config"])
+    dev = torch.device("cuda", device)
+    X = builder.synth_clustered(wl["n"] + nq_pool, cfg.dim, wl["blobs"], wl["sigma"], seed, device=dev)
+    db, Q = X[: wl["n"]], X[wl["n"]:]
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed + 1)
+    train = db[torch.randperm(wl["n"], generator=g, device=dev)[: wl["ntrain"]]]
+    hix = builder.build_index(db, train, cfg)
+    q = Q.cpu().numpy()
+    del X, db, Q, train
+    torch.cuda.empty_cache()
+    tmp = ipath.with_suffix(".tmp")
+    hix.save(str(tmp))
+    os.replace(tmp, ipath)
+    np.save(qpath, q)
+    log(f"[bench] built {name} index in {time.time() - t0:.1f}s")
+    return hix, q
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clocks + throttle reasons during timing."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int, period: float = 0.02):
+        self.device, self.period = device, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            log(f"[bench] NVML unavailable: {e}")
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- algorithmic bytes
+def algorithmic_bytes(hix, counters, stats, k: int):
+    """Bytes each kernel's algorithm must move per batch."""
+    c = hix.config
+    nq = len(counters["ncand"])
+    W = c.w * c.k2
+    pw = hix.pair_width
+    C_q = counters["ncand"].astype(np.float64)
+    T_q = counters["ntuples"].astype(np.float64)
+    bins = stats[:, 0].astype(np.float64)
+    stream_entry = {1: 0, 2: 4, 4: 16}[c.p_tree]  # stream words read per probed tuple
+    trav = nq * (4 * c.dim + 4 * c.p_line * c.k1 + 8 * c.p_tree * W + 2) \
+        + 4 * (c.k1 * c.dim + c.p_tree * c.k1 * c.k2 * c.part_dim)
+    binsel = float(np.sum(8 * c.p_tree * W + T_q * (stream_entry + 4) + bins * (8 + 8) + 24))
+    rerank = float(np.sum(C_q * (c.p_line * (1 + pw) + 4) + bins * 8 + 4 * c.p_line * c.k1 + 8 * k + 4))
+    # SURVEY.md §8d whole-path model B_q = 4D + 16 T_q + 4 C_q + C_q L (1 + pw) + 8k
+    survey = float(np.sum(4 * c.dim + 16 * T_q + 4 * C_q + C_q * c.p_line * (1 + pw) + 8 * k))
+    return {"traverse": float(trav), "binsel": binsel, "rerank": rerank, "survey_Bq_total": survey,
+            "T_q": float(T_q.mean()), "C_q": float(C_q.mean()), "bins_q": float(bins.mean())}
+
+
+def peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_leg(hix, Q, k, min_seconds=10.0, max_reps=20):
+    """Time the reference (oracle/_ref) — else the C restatement — on this host's cores."""
+    from oracle.bindings import Oracle, Ref
+
+    threads = os.cpu_count() or 1
+    if Ref.available():
+        impl, kind = Ref.from_host(hix), "reference"
+    else:
+        impl, kind = Oracle(hix), "port"
+    impl.knn(Q[: min(len(Q), 16)], k, threads=threads)  # warm-up (page-in)
+    reps, t_total, out = 0, 0.0, None
+    while reps < max_reps and (t_total < min_seconds or reps == 0):
+        t0 = time.perf_counter()
+        res = impl.knn(Q, k, threads=threads)
+        t_total += time.perf_counter() - t0
+        out = out or res
+        reps += 1
+    return {"value": reps * len(Q) / t_total, "unit": "queries/s", "cores": threads, "kind": kind,
+            "sample": f"{reps} x {len(Q)} queries of the timed batch (k={k}), all host threads"}, out
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    wl = WORKLOADS[args.workload]
+    hix, Qpool = make_workload(args.workload, args.seed, 0, args.batches)
+    from oracle.bindings import Oracle, Ref
+
+    threads = os.cpu_count() or 1
+    impl, kind = (Ref.from_host(hix), "reference") if Ref.available() else (Oracle(hix), "port")
+    nq = wl["nq"]
+    Q = Qpool[:nq]
+    # bound each step to a few seconds of host work
+    t0 = time.perf_counter()
+    impl.knn(Q[:64], wl["k"], threads=threads)
+    per_q = (time.perf_counter() - t0) / 64
+    sample = int(max(16, min(nq, 3.0 / max(per_q, 1e-9))))
+    Qs = Q[:sample]
+    for _ in range(args.warmup):
+        impl.knn(Qs, wl["k"], threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        impl.knn(Qs, wl["k"], threads=threads)
+    dt = time.perf_counter() - t0
+    v = args.steps * sample / dt
+    line = {
+        "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (clustered blobs)",
+        "impl": "reference",
+        "config": {"workload": args.workload, **wl["config"], "n": wl["n"], "queries_per_step": sample, "k": wl["k"]},
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": threads, "kind": kind,
+                         "sample": f"{sample} queries per step of the {args.workload} batch"},
+        "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    del torch
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="gist1m", choices=sorted(WORKLOADS))
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--batches", type=int, default=4, help="distinct query batches cycled over steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1702_05911_b200 import DeviceIndex
+    from paper_1702_05911_b200._abi import lib
+
+    wl = WORKLOADS[args.workload]
+    nq, k = wl["nq"], wl["k"]
+    if rank == 0:
+        hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * max(world, 1))
+    if world > 1:
+        dist.barrier()
+        if rank != 0:
+            hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * world)
+    dev = DeviceIndex(hix, device=local, max_batch=nq)
+    batches = [Qpool[(rank * args.batches + b) * nq:(rank * args.batches + b + 1) * nq] for b in range(args.batches)]
+    d_q = [torch.from_numpy(b).cuda() for b in batches]
+    d_ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    d_dists = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    d_counts = torch.empty(nq, dtype=torch.int32, device="cuda")
+    d_stats = torch.empty((nq, 3), dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(b):
+        dev.search_device(d_q[b].data_ptr(), nq, k, d_ids.data_ptr(), d_dists.data_ptr(), d_counts.data_ptr(),
+                          d_stats.data_ptr(), stream.cuda_stream)
+
+    # per-batch counters for the algorithmic-bytes model + a correctness snapshot
+    counters, stats_all = [], []
+    for b in range(args.batches):
+        step(b)
+        torch.cuda.synchronize()
+        counters.append(dev.counters(nq))
+        stats_all.append(d_stats.cpu().numpy().astype(np.uint64))
+    for _ in range(args.warmup):
+        for b in range(args.batches):
+            step(b)
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stage_sum = np.zeros(4)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            if not args.no_flush:
+                flush.fill_(s & 0xFF)
+            evs[s][0].record(stream)
+            step(s % args.batches)
+            evs[s][1].record(stream)
+            stage_sum += np.array(dev.stage_ms())  # syncs this step; device time only is used
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * nq * args.steps / (ms_max / 1000.0)
+    stage_mean = stage_sum / args.steps
+
+    # ---- e2e through the public host API (pinned buffers, copies inside the timed call)
+    hq = [torch.from_numpy(b).pin_memory() for b in batches]
+    h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    h_dists = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    h_counts = torch.empty(nq, dtype=torch.int32).pin_memory()
+    h_stats = torch.empty((nq, 3), dtype=torch.int64).pin_memory()
+    L = lib()
+
+    def host_step(b):
+        rc = L.pqtg_search(dev.handle, dev.workspace, hq[b].data_ptr(), nq, hix.config.dim, k, h_ids.data_ptr(),
+                           h_dists.data_ptr(), h_counts.data_ptr(), h_stats.data_ptr())
+        assert rc == 0, L.pqtg_last_error()
+
+    for b in range(args.batches):
+        host_step(b)
+    e2e_steps = max(args.steps // 2, 10)
+    e2e_t = 0.0
+    for s in range(e2e_steps):
+        if not args.no_flush:
+            flush.fill_(s & 0xFF)
+            torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        host_step(s % args.batches)
+        e2e_t += time.perf_counter() - t0
+    tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_value = world * nq * e2e_steps / float(tt.item())
+    h2d = nq * hix.config.dim * 4
+    d2h = nq * k * 8 + nq * 4 + nq * 24
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel
+    names = ["traverse", "binsel", "rerank"]
+    abytes = [algorithmic_bytes(hix, counters[b], stats_all[b], k) for b in range(args.batches)]
+    ab = {kk: float(np.mean([a[kk] for a in abytes])) for kk in abytes[0]}
+    dom = int(np.argmax(stage_mean[:3]))
+    peak, peak_src = peaks()
+    achieved = ab[names[dom]] / (stage_mean[dom] / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "kernel": {"traverse": "traverse_kernel", "binsel": "binsel_kernel",
+                                           "rerank": "rerank_kernel"}[names[dom]],
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": peak_src, "traffic": None,
+                "algorithmic_bytes_per_launch": ab[names[dom]],
+                "stage_ms": {n: float(v) for n, v in zip(names, stage_mean[:3])},
+                "stage_share": {n: float(v / stage_mean[:3].sum()) for n, v in zip(names, stage_mean[:3])},
+                "per_kernel_gbs": {n: ab[n] / (stage_mean[i] / 1000.0) / 1e9 for i, n in enumerate(names)},
+                "T_q": ab["T_q"], "C_q": ab["C_q"], "bins_q": ab["bins_q"],
+                "survey_Bq_gbs": ab["survey_Bq_total"] / (ms_max / args.steps / 1000.0) / 1e9}
+
+    # ---- CPU baseline (rank 0, N=1) + parity of the timed batch
+    cpu = None
+    parity = None
+    if world == 1 and not args.no_cpu_baseline:
+        step(0)
+        torch.cuda.synchronize()
+        g_ids = d_ids.cpu().numpy().view(np.uint32)
+        g_d = d_dists.cpu().numpy()
+        g_c = d_counts.cpu().numpy().view(np.uint32)
+        g_s = d_stats.cpu().numpy().astype(np.uint64)
+        cpu, (r_ids, r_d, r_c, r_s) = cpu_leg(hix, batches[0], k)
+        same = np.array_equal(g_c, r_c) and np.array_equal(g_s, r_s)
+        for q in range(nq):
+            c = g_c[q]
+            same = same and np.array_equal(g_ids[q, :c], r_ids[q, :c]) and \
+                np.array_equal(g_d[q, :c].view(np.uint32), r_d[q, :c].view(np.uint32))
+        parity = {"queries": nq, "bit_exact_vs": cpu["kind"], "ok": bool(same)}
+
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic clustered blobs (synth_clustered distribution), GPU-built PQT index",
+        "config": {"workload": args.workload, **wl["config"], "n": wl["n"], "queries_per_step": nq, "k": k,
+                   "l2": "flushed between timed steps (256 MiB write)" if not args.no_flush else "not flushed",
+                   "parallelism": f"replicas x{world}"},
+        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": 3 * args.steps,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -154,9 +154,11 @@ int pqtg_workspace_stage_ms(pqtg_workspace* ws, float* ms4);
  *   l2_dist      nq × p_tree × W
  *   slope        nq × 2           picked slope-table indices (binorder.cpp:52-65)
  *   positions    nq × budget      gathered candidate positions (search.cpp:166-217), in order
- *   ncand        nq               candidates gathered (global count)            */
+ *   ncand        nq               candidates gathered (global count)
+ *   ntuples      nq               bin-order tuples the gather consumed (T_q) */
 int pqtg_workspace_read(pqtg_workspace* ws, uint64_t nq, float* fine, uint32_t* l2_code,
-                        float* l2_dist, uint8_t* slope, uint32_t* positions, uint32_t* ncand);
+                        float* l2_dist, uint8_t* slope, uint32_t* positions, uint32_t* ncand,
+                        uint32_t* ntuples);
 
 /* ---- search ----------------------------------------------------------------------- */
 /* Host buffers (copied in and out inside the call); synchronous. Outputs are nq × k

@@ -325,6 +325,7 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         ws->ranges = dev_alloc<uint2>(ws->allocations, B * std::max<uint64_t>(p.budget, 1));
         ws->nranges = dev_alloc<uint32_t>(ws->allocations, B);
         ws->ncand = dev_alloc<uint32_t>(ws->allocations, B);
+        ws->ntuples = dev_alloc<uint32_t>(ws->allocations, B);
         auto* h = new pqtg_workspace;
         h->ws = std::move(ws);
         *out = h;
@@ -346,7 +347,7 @@ int pqtg_workspace_stage_ms(pqtg_workspace* h, float* ms4) {
 }
 
 int pqtg_workspace_read(pqtg_workspace* h, uint64_t nq, float* fine, uint32_t* l2_code, float* l2_dist,
-                        uint8_t* slope, uint32_t* positions, uint32_t* ncand) {
+                        uint8_t* slope, uint32_t* positions, uint32_t* ncand, uint32_t* ntuples) {
     return guarded([&] {
         if (!h) throw Error{PQTG_ERR_ARG, "null argument"};
         Workspace& ws = *h->ws;
@@ -365,6 +366,7 @@ int pqtg_workspace_read(pqtg_workspace* h, uint64_t nq, float* fine, uint32_t* l
         cp(nc.data(), ws.ncand, nq * 4);
         cp(nr.data(), ws.nranges, nq * 4);
         if (ncand) std::memcpy(ncand, nc.data(), nq * 4);
+        cp(ntuples, ws.ntuples, nq * 4);
         if (positions && p.budget) {
             std::vector<uint2> rg(nq * p.budget);
             cp(rg.data(), ws.ranges, rg.size() * sizeof(uint2));

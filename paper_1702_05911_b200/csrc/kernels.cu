@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                                                           uint2* __restrict__ ranges,
                                                           uint32_t* __restrict__ nranges,
                                                           uint32_t* __restrict__ ncand,
+                                                          uint32_t* __restrict__ ntuples,
                                                           pqtg_query_stats* __restrict__ stats,
                                                           uint32_t ts_log2) {
     using Sort = cub::BlockRadixSort<uint32_t, kThreads, ITEMS, uint32_t>;
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
     float* dl = reinterpret_cast<float*>(warp_sums + 32);
     uint32_t* hkeys = reinterpret_cast<uint32_t*>(dl + PW_);
     uint32_t* hvals = hkeys + TS;
-    __shared__ uint32_t s_emitted;
+    __shared__ uint32_t s_emitted, s_maxord;
     __shared__ typename Sort::TempStorage sort_tmp;
 
     const uint64_t q = blockIdx.x;
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         hvals[i] = 0xFFFFFFFFu;
     }
     const uint32_t ta = slope_in[q * 2], tb = slope_in[q * 2 + 1];
+    if (tid == 0) s_maxord = 0;
     __syncthreads();
 
     const uint32_t budget = p.budget;
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         if (tid == 0) s_emitted = 0;
         uint64_t tot;
         uint64_t excl = block_excl_scan(local, warp_sums, &tot);
-        uint32_t emitted = 0;
+        uint32_t emitted = 0, maxord = 0;
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             if (cnt[it]) {
@@ -422,11 +424,15 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                     const uint32_t r = R + (uint32_t)(excl & 0xFFFFFFFFu);
                     qranges[r] = make_uint2(start[it], (uint32_t)before_c);
                     ++emitted;
+                    maxord = max(maxord, (uint32_t)(base + tid * ITEMS + it));
                 }
                 excl += ((uint64_t)cnt[it] << 32) | 1u;
             }
         }
-        if (emitted) atomicAdd(&s_emitted, emitted);
+        if (emitted) {
+            atomicAdd(&s_emitted, emitted);
+            atomicMax(&s_maxord, maxord);
+        }
         __syncthreads();
         R += s_emitted;
         const uint64_t newc = (uint64_t)C + (tot >> 32);
@@ -437,6 +443,9 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
     if (tid == 0) {
         nranges[q] = R;
         ncand[q] = C;
+        // tuples the reference's gather loop consumes: up to the one that filled the budget,
+        // or the whole stream (search.cpp:166-217)
+        ntuples[q] = C >= budget && budget > 0 ? s_maxord + 1 : (uint32_t)min(base, total);
         if (stats) {
             stats[q].bins_visited = R;
             stats[q].candidates = C;
@@ -465,10 +474,10 @@ void launch_binsel(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_st
     const uint32_t lg = ts_log2_for(p);
     if (p.resort) {
         binsel_kernel<16, true><<<(unsigned)nq, kThreads, binsel_smem(p), s>>>(
-            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, stats, lg);
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg);
     } else {
         binsel_kernel<4, false><<<(unsigned)nq, kThreads, binsel_smem(p), s>>>(
-            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, stats, lg);
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg);
     }
     PQTG_CUDA_CHECK(cudaGetLastError());
 }

@@ -92,6 +92,7 @@ struct Workspace {
     uint2* ranges = nullptr;      // [B][budget] (start position, candidate offset)
     uint32_t* nranges = nullptr;  // [B]
     uint32_t* ncand = nullptr;    // [B]
+    uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
     // host-call staging (grown on demand)
     float* d_queries = nullptr;
     uint32_t* d_ids = nullptr;

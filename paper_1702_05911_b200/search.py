@@ -158,10 +158,19 @@ class DeviceIndex:
         slope = np.zeros((nq, 2), np.uint8)
         pos = np.zeros((nq, max(budget, 1)), np.uint32)
         nc = np.zeros(nq, np.uint32)
+        nt = np.zeros(nq, np.uint32)
         check(lib().pqtg_workspace_read(self._ws, nq, fine.ctypes.data, l2c.ctypes.data, l2d.ctypes.data,
-                                        slope.ctypes.data, pos.ctypes.data, nc.ctypes.data))
+                                        slope.ctypes.data, pos.ctypes.data, nc.ctypes.data, nt.ctypes.data))
         return dict(fine=fine, l2_parent=l2c >> 16, l2_child=l2c & 0xFFFF, l2_dist=l2d, slope=slope,
-                    positions=[pos[i, : nc[i]] for i in range(nq)], ncand=nc)
+                    positions=[pos[i, : nc[i]] for i in range(nq)], ncand=nc, ntuples=nt)
+
+    def counters(self, nq: int) -> dict:
+        """Cheap per-query counters of the last sub-batch: candidates, tuples consumed."""
+        nc = np.zeros(nq, np.uint32)
+        nt = np.zeros(nq, np.uint32)
+        check(lib().pqtg_workspace_read(self._ws, nq, None, None, None, None, None, nc.ctypes.data,
+                                        nt.ctypes.data))
+        return dict(ncand=nc, ntuples=nt)
 
 
 def load_index(path: str, device: int = 0, shard: tuple[int, int] = (0, 0)) -> DeviceIndex:
