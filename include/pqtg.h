@@ -127,6 +127,9 @@ typedef struct pqtg_workspace pqtg_workspace;
 /* ---- library ---------------------------------------------------------------------- */
 int pqtg_abi_version(void);
 const char* pqtg_last_error(void);
+/* Kernel selection, process-wide: 0 = fastest kernel for each stage (default), 1 = the
+ * generic kernels only (used by the parity tests to cover both paths). */
+int pqtg_set_kernel_variant(int variant);
 /* 1 when a CUDA device with compute capability 10.x is usable, else 0. */
 int pqtg_device_ok(int device);
 

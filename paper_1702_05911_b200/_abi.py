@@ -94,6 +94,7 @@ SIGNATURES = {
     "pqtg_abi_version": (C.c_int, []),
     "pqtg_last_error": (C.c_char_p, []),
     "pqtg_device_ok": (C.c_int, [C.c_int]),
+    "pqtg_set_kernel_variant": (C.c_int, [C.c_int]),
     "pqtg_index_create": (C.c_int, [C.POINTER(PqtgIndexView), C.c_int, C.POINTER(_vp)]),
     "pqtg_index_load": (C.c_int, [C.c_char_p, C.c_int, _u64, _u64, C.POINTER(_vp)]),
     "pqtg_index_info_get": (C.c_int, [_vp, C.POINTER(PqtgIndexInfo)]),

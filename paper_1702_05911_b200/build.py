@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: belt and braces — every exact fp32 op is already an explicit __f*_rn intrinsic.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-CU_SOURCES = ["kernels.cu", "build_kernels.cu"]
+CU_SOURCES = ["kernels.cu", "rerank_fast.cu", "build_kernels.cu"]
 CXX_SOURCES = ["api.cpp", "index_prep.cpp", "pqt_dropin.cpp"]
 
 
@@ -44,7 +44,7 @@ def _stale(target: Path, deps) -> bool:
 
 def build(verbose: bool = False, force: bool = False) -> Path:
     OUT.mkdir(exist_ok=True)
-    headers = list(CSRC.glob("*.h")) + list((REPO / "include").rglob("*.h*"))
+    headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list((REPO / "include").rglob("*.h*"))
     objs = []
     for src in CU_SOURCES + CXX_SOURCES:
         path = CSRC / src

@@ -6,6 +6,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -21,6 +22,11 @@ thread_local std::string g_last_error;
 }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+std::atomic<int> g_variant{0};
+}
+int kernel_variant() { return g_variant.load(std::memory_order_relaxed); }
 const char* last_error() { return g_last_error.c_str(); }
 
 Workspace::~Workspace() {
@@ -227,6 +233,15 @@ using namespace pqtg;
 extern "C" {
 
 int pqtg_abi_version(void) { return PQTG_ABI_VERSION; }
+
+int pqtg_set_kernel_variant(int variant) {
+    if (variant != 0 && variant != 1) {
+        set_error("variant must be 0 (auto) or 1 (generic)");
+        return PQTG_ERR_ARG;
+    }
+    g_variant.store(variant);
+    return PQTG_OK;
+}
 
 const char* pqtg_last_error(void) { return last_error(); }
 

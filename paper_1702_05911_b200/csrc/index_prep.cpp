@@ -12,7 +12,8 @@
 //   bitmap   H bits           non-empty slots
 //   offsets  H+1 u32          InvertedLists::offsets narrowed (n < 2^32)
 //   ids      positions        InvertedLists::ids of this shard
-//   codes    positions × row  line codes permuted into SLOT order: [λ_0..λ_{L-1}][pair ids]
+//   codes    positions × row  line codes permuted into SLOT order; pair width 1: interleaved
+//                             (λ_f, pair_f) bytes; width 2: [λ_0..λ_{L-1}][u16 pair ids]
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -350,10 +351,11 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
                             pid = src.pair_id[id * L + f];
                         }
                         if (pid >= npairs) bad_pid = true;
-                        row[f] = (uint8_t)lq;
-                        if (pw == 1) {
-                            row[L + f] = (uint8_t)pid;
-                        } else {
+                        if (pw == 1) {  // interleaved (lambda, pair id) per part
+                            row[2 * f] = (uint8_t)lq;
+                            row[2 * f + 1] = (uint8_t)pid;
+                        } else {        // lambda block, then little-endian u16 pair ids
+                            row[f] = (uint8_t)lq;
                             row[L + 2 * f] = (uint8_t)(pid & 0xFF);
                             row[L + 2 * f + 1] = (uint8_t)(pid >> 8);
                         }

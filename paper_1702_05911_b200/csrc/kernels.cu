@@ -14,75 +14,14 @@
 #include <cfloat>
 #include <cstdint>
 
+#include "common.cuh"
 #include "pqtg_internal.h"
+#include "topk.cuh"
 
 namespace pqtg {
 
-namespace {
+using namespace dev;
 
-constexpr int kThreads = 256;
-constexpr uint64_t kSentinel = ~0ull;
-
-__device__ __forceinline__ float sq_step(float acc, float a, float b) {
-    const float d = __fsub_rn(a, b);
-    return __fadd_rn(acc, __fmul_rn(d, d));
-}
-
-// fp32 -> u32 preserving order (with -0.0 folded onto +0.0 so it ties like operator<).
-__device__ __forceinline__ uint32_t orderable(float x) {
-    uint32_t u = __float_as_uint(x);
-    if (u == 0x80000000u) u = 0u;
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-__device__ __forceinline__ float unorderable(uint32_t o) {
-    uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
-    return __uint_as_float(u);
-}
-
-// pick_slope_table (binorder.cpp:52-65): fp64 gaps, nearest slope 1.08^k in log space.
-__device__ uint32_t pick_slope(const float* a, const float* b, uint32_t len, double log108) {
-    if (len < 2) return kSlopeOne;
-    const double ga = (double)a[1] - (double)a[0];
-    const double gb = (double)b[1] - (double)b[0];
-    if (!(ga > 0.0) || !(gb > 0.0)) return kSlopeOne;
-    const double ratio = gb / ga;
-    long long k = llround(log(ratio) / log108);
-    k = k < -5 ? -5 : (k > 4 ? 4 : k);
-    return (uint32_t)(k + 5);
-}
-
-// ------------------------------------------------------------------ block scan helpers
-__device__ __forceinline__ uint64_t warp_incl_scan(uint64_t v) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint64_t t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-    }
-    return v;
-}
-
-// Exclusive block scan of one u64 per thread; returns the exclusive prefix, *total = sum.
-__device__ uint64_t block_excl_scan(uint64_t v, uint64_t* warp_sums, uint64_t* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nwarps = blockDim.x >> 5;
-    uint64_t incl = warp_incl_scan(v);
-    if (lane == 31) warp_sums[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        uint64_t s = lane < nwarps ? warp_sums[lane] : 0;
-        s = warp_incl_scan(s);
-        if (lane < nwarps) warp_sums[lane] = s;  // inclusive over warps
-    }
-    __syncthreads();
-    const uint64_t before = warp == 0 ? 0 : warp_sums[warp - 1];
-    *total = warp_sums[nwarps - 1];
-    __syncthreads();
-    return before + incl - v;
-}
-
-}  // namespace
 
 // =====================================================================================
 // K1 — traversal: exact fine-part LUT, level-1 sort, level-2 distances of the w best
@@ -505,12 +444,13 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
         const uint32_t* wds = reinterpret_cast<const uint32_t*>(v);
 #pragma unroll
         for (int f = 0; f < LT; ++f) {
-            const uint32_t lq = (wds[f >> 2] >> ((f & 3) * 8)) & 0xFFu;
-            uint32_t pid;
+            uint32_t lq, pid;
             if constexpr (PW == 1) {
-                const int bi = LT + f;
-                pid = (wds[bi >> 2] >> ((bi & 3) * 8)) & 0xFFu;
+                const int bl = 2 * f, bp = 2 * f + 1;
+                lq = (wds[bl >> 2] >> ((bl & 3) * 8)) & 0xFFu;
+                pid = (wds[bp >> 2] >> ((bp & 3) * 8)) & 0xFFu;
             } else {
+                lq = (wds[f >> 2] >> ((f & 3) * 8)) & 0xFFu;
                 const int b0 = LT + 2 * f, b1 = b0 + 1;
                 pid = ((wds[b0 >> 2] >> ((b0 & 3) * 8)) & 0xFFu) | (((wds[b1 >> 2] >> ((b1 & 3) * 8)) & 0xFFu) << 8);
             }
@@ -525,11 +465,12 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
         }
     } else {
         for (uint32_t f = 0; f < L; ++f) {
-            const uint32_t lq = __ldg(row + f);
-            uint32_t pid;
+            uint32_t lq, pid;
             if (PW == 1) {
-                pid = __ldg(row + L + f);
+                lq = __ldg(row + 2 * f);
+                pid = __ldg(row + 2 * f + 1);
             } else {
+                lq = __ldg(row + f);
                 pid = (uint32_t)__ldg(row + L + 2 * f) | ((uint32_t)__ldg(row + L + 2 * f + 1) << 8);
             }
             const uint32_t pr = pairs[pid];
@@ -571,7 +512,8 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     uint32_t* pairs = reinterpret_cast<uint32_t*>(c2 + L * npairs);  // npairs
     uint32_t* coff = pairs + npairs;                              // budget
     __shared__ uint32_t hist[256];
-    __shared__ uint32_t s_count, s_nsel, s_digit, s_before, s_bucket;
+    __shared__ uint32_t s_count;
+    __shared__ TopkShared s_sel;
 
     const uint64_t q = blockIdx.x;
     const int tid = threadIdx.x;
@@ -582,10 +524,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     for (uint32_t i = tid; i < L * npairs; i += blockDim.x) c2[i] = __ldg(p.c2 + i);
     for (uint32_t i = tid; i < npairs; i += blockDim.x) pairs[i] = __ldg(p.pairs + i);
     for (uint32_t r = tid; r < R; r += blockDim.x) coff[r] = qr[r].y;
-    if (tid == 0) {
-        s_count = 0;
-        s_nsel = 0;
-    }
+    if (tid == 0) s_count = 0;
     __syncthreads();
 
     const bool sharded = p.shard_hi > p.shard_lo;
@@ -613,92 +552,8 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     const uint32_t nvalid = s_count;
     const uint32_t kk = nvalid < k ? nvalid : k;
 
-    if (kk > 0) {
-        // ---- radix select of the kk-th smallest key (keys are distinct: ids are distinct)
-        uint64_t prefix = 0, mask = 0;
-        uint32_t need = kk;
-        int shift = 56;
-        for (;; shift -= 8) {
-            for (uint32_t i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-            __syncthreads();
-            for (uint32_t j = tid; j < C; j += blockDim.x) {
-                const uint64_t key = keys[j];
-                if (key != kSentinel && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1u);
-            }
-            __syncthreads();
-            if (tid < 32) {
-                uint32_t sum = 0;
-#pragma unroll
-                for (int b = 0; b < 8; ++b) sum += hist[tid * 8 + b];
-                uint32_t incl = sum;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (tid >= o) incl += t;
-                }
-                const uint32_t excl = incl - sum;
-                if (excl < need && need <= incl) {
-                    uint32_t acc = excl;
-                    for (int b = 0; b < 8; ++b) {
-                        const uint32_t h = hist[tid * 8 + b];
-                        if (acc + h >= need) {
-                            s_digit = tid * 8 + b;
-                            s_before = acc;
-                            s_bucket = h;
-                            break;
-                        }
-                        acc += h;
-                    }
-                }
-            }
-            __syncthreads();
-            prefix |= (uint64_t)s_digit << shift;
-            mask |= 0xFFull << shift;
-            need -= s_before;
-            if (s_bucket == need || shift == 0) break;
-            __syncthreads();
-        }
-        // ---- collect the kk smallest keys, then bitonic-sort them
-        const uint64_t top = prefix >> shift;
-        for (uint32_t j = tid; j < C; j += blockDim.x) {
-            const uint64_t key = keys[j];
-            if (key != kSentinel && (key >> shift) <= top) {
-                const uint32_t at = atomicAdd(&s_nsel, 1u);
-                if (at < sel_cap) sel[at] = key;
-            }
-        }
-        __syncthreads();
-        uint32_t n2 = 1;
-        while (n2 < kk) n2 <<= 1;
-        for (uint32_t i = kk + tid; i < n2; i += blockDim.x) sel[i] = kSentinel;
-        __syncthreads();
-        for (uint32_t size = 2; size <= n2; size <<= 1) {
-            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                for (uint32_t i = tid; i < n2 / 2; i += blockDim.x) {
-                    const uint32_t a = 2 * i - (i & (stride - 1));
-                    const uint32_t b = a + stride;
-                    const bool up = (a & size) == 0;
-                    const uint64_t x = sel[a], y = sel[b];
-                    if ((x > y) == up) {
-                        sel[a] = y;
-                        sel[b] = x;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-    }
-    for (uint32_t i = tid; i < k; i += blockDim.x) {
-        uint32_t id = 0xFFFFFFFFu;
-        float d = __uint_as_float(0x7F800000u);
-        if (i < kk) {
-            id = (uint32_t)(sel[i] & 0xFFFFFFFFu);
-            d = unorderable((uint32_t)(sel[i] >> 32));
-        }
-        out_ids[q * k + i] = id;
-        out_dists[q * k + i] = d;
-    }
-    if (tid == 0) out_counts[q] = kk;
+    block_topk(keys, C, kk, sel, sel_cap, hist, s_sel);
+    write_topk(sel, kk, k, q, out_ids, out_dists, out_counts);
 }
 
 namespace {
@@ -732,6 +587,10 @@ size_t rerank_smem(const DevParams& p, uint32_t k) {
 
 void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
                    float* dists, uint32_t* counts, cudaStream_t s) {
+    if (kernel_variant() == 0 && rerank_fast_ok(p, k)) {
+        launch_rerank_fast(p, nq, k, ws, ids, dists, counts, s);
+        return;
+    }
     const size_t sm = rerank_smem(p, k);
     const uint32_t cap = sel_cap_for(p, k);
 #define PQTG_RERANK(LT, PW)                                                                          \
@@ -771,6 +630,7 @@ void configure_kernels(const DevParams& p, uint32_t) {
         set_rerank_attr<0, 1>();
         set_rerank_attr<32, 2>();
         set_rerank_attr<0, 2>();
+        configure_rerank_fast();
     });
     (void)p;
 }

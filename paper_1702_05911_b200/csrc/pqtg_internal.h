@@ -168,5 +168,13 @@ void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids,
                   const float* dists, const uint32_t* counts, uint32_t* out_ids,
                   float* out_dists, uint32_t* out_counts, cudaStream_t s);
 void configure_kernels(const DevParams& p, uint32_t k);
+// rerank_fast.cu (p_line == 32, 1-byte pair ids)
+size_t rerank_fast_smem(const DevParams& p, uint32_t k);
+bool rerank_fast_ok(const DevParams& p, uint32_t k);
+void configure_rerank_fast();
+void launch_rerank_fast(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
+                        float* dists, uint32_t* counts, cudaStream_t s);
+// 0 = pick the fastest kernel per stage, 1 = force the generic kernels (parity tests)
+int kernel_variant();
 
 }  // namespace pqtg

@@ -13,6 +13,16 @@ from paper_1702_05911_b200 import DeviceIndex, HostIndex, knn_query_batch, merge
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["auto", "generic"], autouse=True)
+def kernel_variant(request):
+    """Run every GPU parity test through the fast kernels and through the generic ones."""
+    from paper_1702_05911_b200._abi import lib
+
+    lib().pqtg_set_kernel_variant(0 if request.param == "auto" else 1)
+    yield request.param
+    lib().pqtg_set_kernel_variant(0)
+
+
 def assert_same_results(a, b, ctx=""):
     ids_a, d_a, c_a, s_a = a
     ids_b, d_b, c_b, s_b = b
