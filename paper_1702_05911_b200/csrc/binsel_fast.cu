@@ -1,0 +1,313 @@
+// binsel_fast.cu — K3 fast path: bin selection + gather (binorder.cpp:178-283,
+// search.cpp:139-217) without resort_bins, for indexes whose slot arithmetic fits 32 bits.
+//
+// Per query (one CTA), the heuristic rank-tuple stream is walked in passes of growing size
+// (256, 512, ... tuples). Every thread turns its tuples into slots (per-part slot terms
+// pre-reduced mod H in shared memory; for P = 4 the two pair streams are folded into
+// per-pair-rank terms A[u], B[v] so a tuple costs one merge-entry load) and tests the
+// non-empty-slot bitmap. The few non-empty tuples are compacted IN STREAM ORDER into a
+// shared queue (ballot + a 1-warp scan of per-warp counts). Warp 0 then walks the queue in
+// order, 32 at a time: first occurrences by __match_any_sync within the batch plus a shared
+// hash set of visited slots across batches (only when two tuples can share a slot, i.e.
+// (k1·k2)^P > H), the offsets of first occurrences, a warp prefix sum of their sizes, and
+// the budget cut. Output: one (start position, candidate offset) range per visited bin —
+// exactly the reference's gather order.
+#include <cstdint>
+
+#include "common.cuh"
+#include "pqtg_internal.h"
+
+namespace pqtg {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kBsThreads = 256;
+constexpr int kBsWarps = kBsThreads / 32;
+constexpr int kMaxItems = 8;
+
+__device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t H) {
+    const uint64_t x = (uint64_t)a + b;
+    return (uint32_t)(x >= H ? x - H : x);
+}
+
+struct BsLayout {
+    size_t terms, ta, tb, queue, hash, total;
+};
+
+__host__ __device__ inline BsLayout bs_layout(uint32_t PW, uint32_t W2ab, uint32_t ts) {
+    BsLayout l{};
+    size_t o = 0;
+    l.terms = o;
+    o += ((size_t)PW * 4 + 15) & ~size_t(15);
+    l.ta = o;
+    o += (size_t)W2ab * 4;
+    l.tb = o;
+    o += (size_t)W2ab * 4;
+    l.queue = o;
+    o += (size_t)kBsThreads * kMaxItems * 8;
+    l.hash = o;
+    o += (size_t)ts * 4;
+    l.total = o;
+    return l;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kBsThreads, 4)
+    binsel_fast_kernel(DevParams p, const uint32_t* __restrict__ l2c_in, const uint8_t* __restrict__ slope_in,
+                       uint2* __restrict__ ranges, uint32_t* __restrict__ nranges, uint32_t* __restrict__ ncand,
+                       uint32_t* __restrict__ ntuples, pqtg_query_stats* __restrict__ stats, uint32_t ts_log2,
+                       uint32_t use_hash, uint32_t W2ab) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t P = p.P, W = p.W, PW = P * W;
+    const uint32_t H = (uint32_t)p.H;
+    const uint32_t TS = use_hash ? (1u << ts_log2) : 0u;
+    const BsLayout lay = bs_layout(PW, W2ab, TS);
+    uint32_t* terms = reinterpret_cast<uint32_t*>(smem + lay.terms);
+    uint32_t* tA = reinterpret_cast<uint32_t*>(smem + lay.ta);
+    uint32_t* tB = reinterpret_cast<uint32_t*>(smem + lay.tb);
+    uint2* queue = reinterpret_cast<uint2*>(smem + lay.queue);
+    uint32_t* hkeys = reinterpret_cast<uint32_t*>(smem + lay.hash);
+    __shared__ uint32_t wcnt[kMaxItems * kBsWarps];
+    __shared__ uint32_t s_nq, s_C, s_R, s_maxord;
+
+    const uint64_t q = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ta = slope_in[q * 2], tb = slope_in[q * 2 + 1];
+
+    // slot terms (flat_part_code · (k1k2)^p) mod H, pqtree.cpp:12-25
+    for (uint32_t idx = tid; idx < PW; idx += blockDim.x) {
+        const uint32_t code = l2c_in[q * PW + idx];
+        const uint64_t flat = (uint64_t)(code >> 16) * p.k2 + (code & 0xFFFFu);
+        terms[idx] = (uint32_t)((flat * p.mult[idx / W]) % p.H);
+    }
+    for (uint32_t i = tid; i < TS; i += blockDim.x) hkeys[i] = kEmptyKey;
+    if (tid == 0) {
+        s_C = 0;
+        s_R = 0;
+        s_maxord = 0;
+    }
+    __syncthreads();
+    if (W2ab) {  // P == 4: fold each pair stream into per-pair-rank slot terms
+        for (uint32_t u = tid; u < W2ab; u += blockDim.x) {
+            const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + u);
+            const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + u);
+            tA[u] = add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H);
+            tB[u] = add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H);
+        }
+        __syncthreads();
+    }
+
+    const uint32_t budget = p.budget;
+    const uint64_t total = p.total_tuples;
+    uint2* qranges = ranges + q * (uint64_t)budget;
+    uint32_t C = 0, R = 0;
+    uint64_t base = 0;
+    uint32_t nit = 1;
+    while (C < budget && base < total) {
+        // ---- filter: slot + non-empty test for 256·nit consecutive stream positions
+        uint32_t slot[kMaxItems];
+        uint32_t ball[kMaxItems];
+#pragma unroll
+        for (int it = 0; it < kMaxItems; ++it) {
+            slot[it] = 0;
+            ball[it] = 0;
+            if (it < (int)nit) {
+                const uint64_t s = base + (uint64_t)it * kBsThreads + tid;
+                bool ne = false;
+                if (s < total) {
+                    uint32_t sl;
+                    if (P == 1) {
+                        sl = terms[s];
+                    } else if (P == 2) {
+                        const uint32_t e = __ldg(p.pair_streams + (size_t)ta * p.W2 + s);
+                        sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
+                    } else {
+                        uint64_t u, v;
+                        if (s < p.merge_count) {
+                            const uint2 uv = __ldg(p.merge + s);
+                            u = uv.x;
+                            v = uv.y;
+                        } else {
+                            const uint64_t j = s - p.merge_count;
+                            u = p.merge_row0 + j / p.W2;
+                            v = j - (u - p.merge_row0) * p.W2;
+                        }
+                        if (W2ab) {
+                            sl = add_mod(tA[u], tB[v], H);
+                        } else {
+                            const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + u);
+                            const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + v);
+                            sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
+                                         add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
+                        }
+                    }
+                    slot[it] = sl;
+                    ne = (__ldg(p.bitmap + (sl >> 5)) >> (sl & 31)) & 1u;
+                }
+                ball[it] = __ballot_sync(0xffffffffu, ne);
+                if (lane == 0) wcnt[it * kBsWarps + warp] = __popc(ball[it]);
+            }
+        }
+        __syncthreads();
+        // ---- order-preserving compaction: scan per-(item, warp) counts in stream order
+        if (warp == 0) {
+            const uint32_t n = nit * kBsWarps;
+            const uint32_t v = lane < (int)n ? wcnt[lane] : 0;
+            uint32_t incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane < (int)n) wcnt[lane] = incl - v;
+            if (lane == 31) s_nq = incl;
+            // nit * 8 <= 64 > 32 when nit == 8: second half
+            if (n > 32) {
+                const uint32_t v2 = (uint32_t)(lane + 32) < n ? wcnt[lane + 32] : 0;
+                uint32_t incl2 = v2;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl2, o);
+                    if (lane >= o) incl2 += t;
+                }
+                const uint32_t carry = __shfl_sync(0xffffffffu, incl, 31);
+                if ((uint32_t)(lane + 32) < n) wcnt[lane + 32] = carry + incl2 - v2;
+                if (lane == 31) s_nq = carry + incl2;
+            }
+        }
+        __syncthreads();
+        const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int it = 0; it < kMaxItems; ++it) {
+            if (it < (int)nit && ((ball[it] >> lane) & 1u)) {
+                const uint32_t at = wcnt[it * kBsWarps + warp] + __popc(ball[it] & lt);
+                queue[at] = make_uint2((uint32_t)(base + (uint64_t)it * kBsThreads + tid), slot[it]);
+            }
+        }
+        __syncthreads();
+        // ---- warp 0: walk the non-empty tuples in stream order
+        const uint32_t nq = s_nq;
+        if (warp == 0 && nq > 0) {
+            uint32_t c = s_C, r = s_R, maxord = s_maxord;
+            for (uint32_t b0 = 0; b0 < nq && c < budget; b0 += 32) {
+                const uint32_t idx = b0 + lane;
+                const bool has = idx < nq;
+                const uint2 e = has ? queue[idx] : make_uint2(0, kEmptyKey);
+                bool first = has;
+                if (use_hash) {
+                    const uint32_t grp = __match_any_sync(0xffffffffu, e.y);
+                    if (has) {
+                        if ((uint32_t)(__ffs(grp) - 1) != (uint32_t)lane) {
+                            first = false;  // an earlier tuple of this batch has the slot
+                        } else {
+                            uint32_t h = (e.y * 0x9E3779B1u) >> (32 - ts_log2);
+                            for (;;) {
+                                const uint32_t prev = atomicCAS(hkeys + h, kEmptyKey, e.y);
+                                if (prev == kEmptyKey) break;
+                                if (prev == e.y) {
+                                    first = false;  // visited in an earlier batch
+                                    break;
+                                }
+                                h = (h + 1) & (TS - 1);
+                            }
+                        }
+                    }
+                }
+                uint32_t start = 0, cnt = 0;
+                if (first) {
+                    start = __ldg(p.offsets + e.y);
+                    cnt = __ldg(p.offsets + e.y + 1) - start;
+                }
+                uint32_t incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const uint32_t before = c + (incl - cnt);  // < 2^32: distinct bins hold <= n ids
+                const bool emit = first && before < budget;
+                const uint32_t em = __ballot_sync(0xffffffffu, emit);
+                if (emit) {
+                    qranges[r + __popc(em & lt)] = make_uint2(start, before);
+                    maxord = max(maxord, e.x);
+                }
+                maxord = __reduce_max_sync(0xffffffffu, maxord);
+                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                r += __popc(em);
+                c = (uint64_t)c + tot >= budget ? budget : c + tot;
+            }
+            if (lane == 0) {
+                s_C = c;
+                s_R = r;
+                s_maxord = maxord;
+            }
+        }
+        __syncthreads();
+        C = s_C;
+        R = s_R;
+        base += (uint64_t)nit * kBsThreads;
+        nit = nit * 2 < (uint32_t)kMaxItems ? nit * 2 : (uint32_t)kMaxItems;
+    }
+    if (tid == 0) {
+        nranges[q] = R;
+        ncand[q] = C;
+        ntuples[q] = C >= budget && budget > 0 ? s_maxord + 1 : (uint32_t)min(base, total);
+        if (stats) {
+            stats[q].bins_visited = R;
+            stats[q].candidates = C;
+            stats[q].exact_evals = 0;
+        }
+    }
+}
+
+namespace {
+
+struct BsConfig {
+    uint32_t ts_log2, use_hash, W2ab;
+    size_t smem;
+};
+
+BsConfig bs_config(const DevParams& p) {
+    BsConfig c{};
+    // two tuples can reach one slot only if the positional code space exceeds H
+    long double span = 1.0L;
+    for (uint32_t i = 0; i < p.P; ++i) span *= (long double)p.k1 * p.k2;
+    c.use_hash = span > (long double)p.H ? 1u : 0u;
+    c.ts_log2 = 6;
+    while ((1ull << c.ts_log2) < ((uint64_t)p.budget + 32) * 3 / 2) ++c.ts_log2;
+    c.W2ab = (p.P == 4 && p.W2 <= 4096) ? (uint32_t)p.W2 : 0u;
+    c.smem = bs_layout(p.P * p.W, c.W2ab, c.use_hash ? (1u << c.ts_log2) : 0u).total;
+    return c;
+}
+
+}  // namespace
+
+bool binsel_fast_ok(const DevParams& p) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return !p.resort && p.mod_fast && p.H < 0xFFFFFFFFull && bs_config(p).smem + 2048 <= (size_t)optin;
+}
+
+void configure_binsel_fast() {
+    int dev = 0, optin = 0;
+    PQTG_CUDA_CHECK(cudaGetDevice(&dev));
+    PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes a{};
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, binsel_fast_kernel));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         optin - (int)a.sharedSizeBytes));
+}
+
+void launch_binsel_fast(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats, cudaStream_t s) {
+    const BsConfig c = bs_config(p);
+    binsel_fast_kernel<<<(unsigned)nq, kBsThreads, c.smem, s>>>(p, ws.l2_code, ws.slope, ws.ranges, ws.nranges,
+                                                               ws.ncand, ws.ntuples, stats, c.ts_log2, c.use_hash,
+                                                               c.W2ab);
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace pqtg

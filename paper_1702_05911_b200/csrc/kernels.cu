@@ -410,6 +410,10 @@ size_t binsel_smem(const DevParams& p) {
 
 void launch_binsel(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats,
                    cudaStream_t s) {
+    if (kernel_variant() == 0 && binsel_fast_ok(p)) {
+        launch_binsel_fast(p, nq, ws, stats, s);
+        return;
+    }
     const uint32_t lg = ts_log2_for(p);
     if (p.resort) {
         binsel_kernel<16, true><<<(unsigned)nq, kThreads, binsel_smem(p), s>>>(
@@ -631,6 +635,7 @@ void configure_kernels(const DevParams& p, uint32_t) {
         set_rerank_attr<32, 2>();
         set_rerank_attr<0, 2>();
         configure_rerank_fast();
+        configure_binsel_fast();
     });
     (void)p;
 }

@@ -174,6 +174,10 @@ bool rerank_fast_ok(const DevParams& p, uint32_t k);
 void configure_rerank_fast();
 void launch_rerank_fast(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
                         float* dists, uint32_t* counts, cudaStream_t s);
+// binsel_fast.cu (no resort, 32-bit slot arithmetic)
+bool binsel_fast_ok(const DevParams& p);
+void configure_binsel_fast();
+void launch_binsel_fast(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats, cudaStream_t s);
 // 0 = pick the fastest kernel per stage, 1 = force the generic kernels (parity tests)
 int kernel_variant();
 
