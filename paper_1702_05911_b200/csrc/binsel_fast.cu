@@ -107,46 +107,59 @@ __global__ void __launch_bounds__(kBsThreads, 4)
     uint64_t base = 0;
     uint32_t nit = 1;
     while (C < budget && base < total) {
-        // ---- filter: slot + non-empty test for 256·nit consecutive stream positions
-        uint32_t slot[kMaxItems];
-        uint32_t ball[kMaxItems];
+        // ---- filter: slot + non-empty test for 256·nit consecutive stream positions.
+        // Three unrolled sweeps so each thread's loads are issued together: stream entries,
+        // then slots + bitmap words, then the ballots.
+        uint32_t slot[kMaxItems], word[kMaxItems], ball[kMaxItems];
+        uint2 ent[kMaxItems];
 #pragma unroll
         for (int it = 0; it < kMaxItems; ++it) {
+            const uint64_t s = base + (uint64_t)it * kBsThreads + tid;
+            ent[it] = make_uint2(0, 0);
+            if (it < (int)nit && s < total) {
+                if (P == 2) {
+                    ent[it].x = __ldg(p.pair_streams + (size_t)ta * p.W2 + s);
+                } else if (P == 4) {
+                    if (s < p.merge_count) {
+                        ent[it] = __ldg(p.merge + s);
+                    } else {
+                        const uint64_t j = s - p.merge_count;
+                        const uint64_t u = p.merge_row0 + j / p.W2;
+                        ent[it] = make_uint2((uint32_t)u, (uint32_t)(j - (u - p.merge_row0) * p.W2));
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < kMaxItems; ++it) {
+            const uint64_t s = base + (uint64_t)it * kBsThreads + tid;
             slot[it] = 0;
+            word[it] = 0;
+            if (it < (int)nit && s < total) {
+                uint32_t sl;
+                if (P == 1) {
+                    sl = terms[s];
+                } else if (P == 2) {
+                    const uint32_t e = ent[it].x;
+                    sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
+                } else if (W2ab) {
+                    sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
+                } else {
+                    const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + ent[it].x);
+                    const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + ent[it].y);
+                    sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
+                                 add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
+                }
+                slot[it] = sl;
+                word[it] = __ldg(p.bitmap + (sl >> 5));
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < kMaxItems; ++it) {
             ball[it] = 0;
             if (it < (int)nit) {
                 const uint64_t s = base + (uint64_t)it * kBsThreads + tid;
-                bool ne = false;
-                if (s < total) {
-                    uint32_t sl;
-                    if (P == 1) {
-                        sl = terms[s];
-                    } else if (P == 2) {
-                        const uint32_t e = __ldg(p.pair_streams + (size_t)ta * p.W2 + s);
-                        sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
-                    } else {
-                        uint64_t u, v;
-                        if (s < p.merge_count) {
-                            const uint2 uv = __ldg(p.merge + s);
-                            u = uv.x;
-                            v = uv.y;
-                        } else {
-                            const uint64_t j = s - p.merge_count;
-                            u = p.merge_row0 + j / p.W2;
-                            v = j - (u - p.merge_row0) * p.W2;
-                        }
-                        if (W2ab) {
-                            sl = add_mod(tA[u], tB[v], H);
-                        } else {
-                            const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + u);
-                            const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + v);
-                            sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
-                                         add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
-                        }
-                    }
-                    slot[it] = sl;
-                    ne = (__ldg(p.bitmap + (sl >> 5)) >> (sl & 31)) & 1u;
-                }
+                const bool ne = s < total && ((word[it] >> (slot[it] & 31)) & 1u);
                 ball[it] = __ballot_sync(0xffffffffu, ne);
                 if (lane == 0) wcnt[it * kBsWarps + warp] = __popc(ball[it]);
             }

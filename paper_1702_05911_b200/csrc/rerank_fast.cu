@@ -44,7 +44,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 struct FastLayout {
-    size_t ring, ids, lut, lc2, fine, ranges, keys, sel, total;
+    size_t ring, ids, lut, lc2, fine, pairs, ranges, keys, sel, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -62,6 +62,8 @@ __host__ __device__ inline FastLayout fast_layout(uint32_t npairs, uint32_t k1, 
     o += align16((size_t)npairs * 32 * 4);
     l.fine = o;
     o += align16((size_t)32 * k1 * 4);
+    l.pairs = o;
+    o += align16((size_t)npairs * 4);
     l.ranges = o;
     o += align16((size_t)budget * 8);
     l.keys = o;
@@ -101,6 +103,8 @@ __global__ void __launch_bounds__(kFastThreads, 1)
 
     for (uint32_t i = tid; i < 32 * k1; i += blockDim.x) fine[i] = fine_in[q * 32 * k1 + i];
     for (uint32_t r = tid; r < R; r += blockDim.x) rg[r] = qr[r];
+    uint32_t* spairs = reinterpret_cast<uint32_t*>(smem + lay.pairs);
+    for (uint32_t i = tid; i < npairs; i += blockDim.x) spairs[i] = __ldg(p.pairs + i);
     {
         uint4* z = reinterpret_cast<uint4*>(ring + (size_t)tid * kLaneBytes);
         for (int i = 0; i < kLaneBytes / 16; ++i) z[i] = make_uint4(0, 0, 0, 0);  // pid 0 in unused slots
@@ -108,9 +112,10 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     if (tid == 0) s_count = 0;
     __syncthreads();
     // per-query tables, [pid][f] so that lanes at distinct parts hit distinct banks
+#pragma unroll 4
     for (uint32_t idx = tid; idx < npairs * 32; idx += blockDim.x) {
         const uint32_t pid = idx >> 5, f = idx & 31;
-        const uint32_t pr = __ldg(p.pairs + pid);
+        const uint32_t pr = spairs[pid];
         const float b2 = fine[f * k1 + (pr & 0xFFFFu)];
         const float a2 = fine[f * k1 + (pr >> 16)];
         const float c2 = __ldg(p.c2 + (size_t)f * npairs + pid);
@@ -164,36 +169,50 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     const int32_t nparts = (int32_t)nround * 32;
     uint32_t mine = 0;
-    float acc = 0.0f;
+    float acc = 0.0f, done = 0.0f;
+    // One fine part of lane l's current candidate; g = lane's running part counter.
+    // Branch-free: the finished sum of a candidate (f == 31) is parked in `done` and the
+    // accumulator restarts, so the unrolled steps carry no control flow.
+    auto step = [&](int32_t g) {
+        const uint32_t f = (uint32_t)g & 31u;
+        const uint32_t code = *reinterpret_cast<const uint16_t*>(my + (((uint32_t)g & 127u) << 1));
+        const uint32_t li = ((code >> 8) << 5) | f;
+        const float2 be = lut[li];
+        const float c2 = lc2[li];
+        const float lam = __fmul_rn(__uint2float_rn(code & 0xFFu), inv255);
+        const float part = __fadd_rn(__fadd_rn(be.x, __fmul_rn(__fmul_rn(lam, lam), c2)), __fmul_rn(lam, be.y));
+        acc = __fadd_rn(acc, part);
+        const bool fin = f == 31u;
+        done = fin ? acc : done;
+        acc = fin ? 0.0f : acc;
+    };
     for (uint32_t m = 0; nround > 0 && m <= nround; ++m) {
         if (m > 0) stage(m + 2);
         cp_async_wait<2>();  // rounds <= m have landed (each lane reads only its own ring)
-#pragma unroll 8
-        for (uint32_t t = 0; t < 32; ++t) {
-            const int32_t g = (int32_t)(m * 32 + t) - lane;
-            if (g >= 0 && g < nparts) {
-                const uint32_t f = (uint32_t)g & 31u;
-                const uint32_t code = *reinterpret_cast<const uint16_t*>(my + (((uint32_t)g & 127u) << 1));
-                const uint32_t li = ((code >> 8) << 5) | f;
-                const float2 be = lut[li];
-                const float c2 = lc2[li];
-                const float lam = __fmul_rn(__uint2float_rn(code & 0xFFu), inv255);
-                const float part = __fadd_rn(__fadd_rn(be.x, __fmul_rn(__fmul_rn(lam, lam), c2)), __fmul_rn(lam, be.y));
-                acc = __fadd_rn(acc, part);
-                if (f == 31) {
-                    const uint32_t r = (uint32_t)g >> 5;
-                    const uint32_t c = aw + 32 * r + lane;
-                    const uint32_t id = myid[r & 3];
-                    if (c < bw) {
-                        uint64_t key = kSentinel;
-                        if (id != kInvalidId) {
-                            key = ((uint64_t)orderable(acc) << 32) | id;
-                            ++mine;
-                        }
-                        keys[c] = key;
-                    }
-                    acc = 0.0f;
+        const int32_t pb = (int32_t)(m * 32) - lane;
+        if (m >= 1 && m < nround) {  // every lane busy for all 32 steps
+#pragma unroll
+            for (int t = 0; t < 32; ++t) step(pb + t);
+        } else {                     // pipeline fill / drain
+#pragma unroll 4
+            for (int t = 0; t < 32; ++t) {
+                const int32_t g = pb + t;
+                if (g >= 0 && g < nparts) step(g);
+            }
+        }
+        // each lane finished exactly one candidate in this phase: lane 0 its round m,
+        // lanes l > 0 their round m - 1 (at t = l - 1)
+        const int32_t r = lane == 0 ? (int32_t)m : (int32_t)m - 1;
+        if (r >= 0 && r < (int32_t)nround) {
+            const uint32_t c = aw + 32 * (uint32_t)r + lane;
+            if (c < bw) {
+                const uint32_t id = myid[r & 3];
+                uint64_t key = kSentinel;
+                if (id != kInvalidId) {
+                    key = ((uint64_t)orderable(done) << 32) | id;
+                    ++mine;
                 }
+                keys[c] = key;
             }
         }
     }
