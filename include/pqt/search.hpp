@@ -1,0 +1,61 @@
+// pqt/search.hpp — drop-in replacement for the reference's query API
+// (proj/include/pqt/search.hpp:15-47, :80-83), served by the B200 kernels in libpqtg.so.
+//
+// Same types, same signatures, same exceptions. Differences a caller can observe:
+//  * queries run on a CUDA device (device 0 unless PQTG_DEVICE is set); the first query on
+//    an index uploads it and caches the device copy in PqtIndex::gpu;
+//  * exact re-ranking against attached raw vectors is not implemented on the GPU path: with
+//    a database attached and rerank_exact > 0 the calls throw std::runtime_error (without
+//    one they warn once and disable it, exactly as the reference does, search.cpp:25-32);
+//  * QueryStats *_us are the batch's per-stage device times divided evenly over its queries.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "pqt/binorder.hpp"
+#include "pqt/codebook.hpp"
+#include "pqt/linequant.hpp"
+#include "pqt/pqtree.hpp"
+#include "pqt/vecio.hpp"
+
+namespace pqt {
+
+struct QueryStats {
+    std::uint64_t bins_visited = 0;
+    std::uint64_t candidates = 0;
+    std::uint64_t exact_evals = 0;
+    double traversal_us = 0.0;
+    double bin_selection_us = 0.0;
+    double vector_proposal_us = 0.0;
+    double rerank_us = 0.0;
+};
+
+struct QueryResult {
+    std::vector<std::uint32_t> ids;
+    std::vector<float> dists;  // squared, non-decreasing
+    QueryStats stats;
+};
+
+struct PqtIndex {
+    PqtConfig config;  // hash_size resolved
+    TreeCodebooks tree;
+    FineCentroids fine;
+    PairDistanceTable pair_table;
+    std::vector<OrderTable> tables;
+    InvertedLists lists;
+    LineCodes codes;
+    std::shared_ptr<const VectorSet> database;  // optional
+    mutable std::shared_ptr<void> gpu;          // device copy (pqtg_index + workspace), lazily built
+
+    std::size_t size() const { return lists.ids.size(); }
+    void attach_database(std::shared_ptr<const VectorSet> db);
+};
+
+QueryResult knn_query(const PqtIndex& index, const float* y, std::uint32_t k);
+
+std::vector<QueryResult> knn_query_batch(const PqtIndex& index, const VectorSet& queries, std::uint32_t k,
+                                         int threads = 0);
+
+}  // namespace pqt

@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 CU_SOURCES = ["kernels.cu", "rerank_fast.cu", "binsel_fast.cu", "build_kernels.cu"]
-CXX_SOURCES = ["api.cpp", "index_prep.cpp", "pqt_dropin.cpp"]
+CXX_SOURCES = ["api.cpp", "index_file.cpp", "index_prep.cpp", "pqt_dropin.cpp"]
 
 
 def _run(cmd):
@@ -53,7 +53,10 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         obj = OUT / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path, *headers, Path(__file__)]):
-            cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-I", str(REPO / "include"), "-c", str(path), "-o", str(obj)]
+            flags = list(NVCC_FLAGS)
+            if src == "pqt_dropin.cpp":  # the reference API is C++20 (std::span)
+                flags[flags.index("-std=c++17")] = "-std=c++20"
+            cmd = [NVCC, *ARCH, *flags, "-I", str(REPO / "include"), "-c", str(path), "-o", str(obj)]
             out = _run(cmd)
             if verbose and out.strip():
                 print(out)

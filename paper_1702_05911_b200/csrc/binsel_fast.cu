@@ -55,21 +55,26 @@ __host__ __device__ inline BsLayout bs_layout(uint32_t PW, uint32_t W2ab, uint32
 
 }  // namespace
 
+// HASH: two tuples can reach one slot ((k1·k2)^P > H); first occurrences are then tracked in
+// a per-query region of a global, epoch-tagged open-addressing table (entries
+// epoch << 26 | slot, H <= 2^26), which needs no clearing between searches.
+template <int P, bool HASH>
 __global__ void __launch_bounds__(kBsThreads, 4)
     binsel_fast_kernel(DevParams p, const uint32_t* __restrict__ l2c_in, const uint8_t* __restrict__ slope_in,
                        uint2* __restrict__ ranges, uint32_t* __restrict__ nranges, uint32_t* __restrict__ ncand,
                        uint32_t* __restrict__ ntuples, pqtg_query_stats* __restrict__ stats, uint32_t ts_log2,
-                       uint32_t use_hash, uint32_t W2ab) {
+                       uint32_t* __restrict__ ghash, uint32_t epoch, uint32_t W2ab) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t P = p.P, W = p.W, PW = P * W;
+    const uint32_t W = p.W, PW = P * W;
     const uint32_t H = (uint32_t)p.H;
-    const uint32_t TS = use_hash ? (1u << ts_log2) : 0u;
-    const BsLayout lay = bs_layout(PW, W2ab, TS);
+    const BsLayout lay = bs_layout(PW, W2ab, 0);
     uint32_t* terms = reinterpret_cast<uint32_t*>(smem + lay.terms);
     uint32_t* tA = reinterpret_cast<uint32_t*>(smem + lay.ta);
     uint32_t* tB = reinterpret_cast<uint32_t*>(smem + lay.tb);
     uint2* queue = reinterpret_cast<uint2*>(smem + lay.queue);
-    uint32_t* hkeys = reinterpret_cast<uint32_t*>(smem + lay.hash);
+    const uint32_t TS = 1u << ts_log2;
+    uint32_t* hkeys = HASH ? ghash + ((uint64_t)blockIdx.x << ts_log2) : nullptr;
+    const uint32_t etag = epoch << 26;
     __shared__ uint32_t wcnt[kMaxItems * kBsWarps];
     __shared__ uint32_t s_nq, s_C, s_R, s_maxord;
 
@@ -83,14 +88,13 @@ __global__ void __launch_bounds__(kBsThreads, 4)
         const uint64_t flat = (uint64_t)(code >> 16) * p.k2 + (code & 0xFFFFu);
         terms[idx] = (uint32_t)((flat * p.mult[idx / W]) % p.H);
     }
-    for (uint32_t i = tid; i < TS; i += blockDim.x) hkeys[i] = kEmptyKey;
     if (tid == 0) {
         s_C = 0;
         s_R = 0;
         s_maxord = 0;
     }
     __syncthreads();
-    if (W2ab) {  // P == 4: fold each pair stream into per-pair-rank slot terms
+    if (P == 4 && W2ab) {  // fold each pair stream into per-pair-rank slot terms
         for (uint32_t u = tid; u < W2ab; u += blockDim.x) {
             const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + u);
             const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + u);
@@ -117,9 +121,9 @@ __global__ void __launch_bounds__(kBsThreads, 4)
             const uint64_t s = base + (uint64_t)it * kBsThreads + tid;
             ent[it] = make_uint2(0, 0);
             if (it < (int)nit && s < total) {
-                if (P == 2) {
+                if constexpr (P == 2) {
                     ent[it].x = __ldg(p.pair_streams + (size_t)ta * p.W2 + s);
-                } else if (P == 4) {
+                } else if constexpr (P == 4) {
                     if (s < p.merge_count) {
                         ent[it] = __ldg(p.merge + s);
                     } else {
@@ -137,9 +141,9 @@ __global__ void __launch_bounds__(kBsThreads, 4)
             word[it] = 0;
             if (it < (int)nit && s < total) {
                 uint32_t sl;
-                if (P == 1) {
+                if constexpr (P == 1) {
                     sl = terms[s];
-                } else if (P == 2) {
+                } else if constexpr (P == 2) {
                     const uint32_t e = ent[it].x;
                     sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
                 } else if (W2ab) {
@@ -210,17 +214,21 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                 const bool has = idx < nq;
                 const uint2 e = has ? queue[idx] : make_uint2(0, kEmptyKey);
                 bool first = has;
-                if (use_hash) {
+                if (HASH) {
                     const uint32_t grp = __match_any_sync(0xffffffffu, e.y);
                     if (has) {
                         if ((uint32_t)(__ffs(grp) - 1) != (uint32_t)lane) {
                             first = false;  // an earlier tuple of this batch has the slot
                         } else {
+                            const uint32_t key = etag | e.y;
                             uint32_t h = (e.y * 0x9E3779B1u) >> (32 - ts_log2);
                             for (;;) {
-                                const uint32_t prev = atomicCAS(hkeys + h, kEmptyKey, e.y);
-                                if (prev == kEmptyKey) break;
-                                if (prev == e.y) {
+                                const uint32_t cur = hkeys[h];
+                                if ((cur & 0xFC000000u) != etag) {  // stale epoch = empty
+                                    if (atomicCAS(hkeys + h, cur, key) == cur) break;
+                                    continue;  // lost a race on this entry; re-read it
+                                }
+                                if (cur == key) {
                                     first = false;  // visited in an earlier batch
                                     break;
                                 }
@@ -292,8 +300,19 @@ BsConfig bs_config(const DevParams& p) {
     c.ts_log2 = 6;
     while ((1ull << c.ts_log2) < ((uint64_t)p.budget + 32) * 3 / 2) ++c.ts_log2;
     c.W2ab = (p.P == 4 && p.W2 <= 4096) ? (uint32_t)p.W2 : 0u;
-    c.smem = bs_layout(p.P * p.W, c.W2ab, c.use_hash ? (1u << c.ts_log2) : 0u).total;
+    c.smem = bs_layout(p.P * p.W, c.W2ab, 0).total;
     return c;
+}
+
+template <int P, bool HASH>
+void configure_one() {
+    int dev = 0, optin = 0;
+    PQTG_CUDA_CHECK(cudaGetDevice(&dev));
+    PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes a{};
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, binsel_fast_kernel<P, HASH>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_fast_kernel<P, HASH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         optin - (int)a.sharedSizeBytes));
 }
 
 }  // namespace
@@ -302,24 +321,47 @@ bool binsel_fast_ok(const DevParams& p) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return !p.resort && p.mod_fast && p.H < 0xFFFFFFFFull && bs_config(p).smem + 2048 <= (size_t)optin;
+    const BsConfig c = bs_config(p);
+    return !p.resort && p.mod_fast && p.H < 0xFFFFFFFFull && (!c.use_hash || p.H <= (1ull << 26)) &&
+           c.smem + 2048 <= (size_t)optin;
+}
+
+uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch) {
+    const BsConfig c = bs_config(p);
+    return c.use_hash ? (max_batch << c.ts_log2) : 0;
 }
 
 void configure_binsel_fast() {
-    int dev = 0, optin = 0;
-    PQTG_CUDA_CHECK(cudaGetDevice(&dev));
-    PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cudaFuncAttributes a{};
-    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, binsel_fast_kernel));
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         optin - (int)a.sharedSizeBytes));
+    configure_one<1, false>();
+    configure_one<2, false>();
+    configure_one<2, true>();
+    configure_one<4, false>();
+    configure_one<4, true>();
 }
 
 void launch_binsel_fast(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats, cudaStream_t s) {
     const BsConfig c = bs_config(p);
-    binsel_fast_kernel<<<(unsigned)nq, kBsThreads, c.smem, s>>>(p, ws.l2_code, ws.slope, ws.ranges, ws.nranges,
-                                                               ws.ncand, ws.ntuples, stats, c.ts_log2, c.use_hash,
-                                                               c.W2ab);
+    uint32_t epoch = 0;
+    if (c.use_hash) {
+        // 6-bit epochs tag the entries of the global visited-slot table; clear it on wrap
+        if (ws.hash_epoch == 0 || ws.hash_epoch >= 63) {
+            PQTG_CUDA_CHECK(cudaMemsetAsync(ws.hash, 0, ws.hash_words * sizeof(uint32_t), s));
+            ws.hash_epoch = 0;
+        }
+        epoch = ++ws.hash_epoch;  // 1..63; 0 marks cleared entries
+    }
+#define PQTG_BS(PP, HH)                                                                                       \
+    binsel_fast_kernel<PP, HH><<<(unsigned)nq, kBsThreads, c.smem, s>>>(p, ws.l2_code, ws.slope, ws.ranges,     \
+                                                                       ws.nranges, ws.ncand, ws.ntuples, stats, \
+                                                                       c.ts_log2, ws.hash, epoch, c.W2ab)
+    if (p.P == 1) {
+        PQTG_BS(1, false);
+    } else if (p.P == 2) {
+        if (c.use_hash) PQTG_BS(2, true); else PQTG_BS(2, false);
+    } else {
+        if (c.use_hash) PQTG_BS(4, true); else PQTG_BS(4, false);
+    }
+#undef PQTG_BS
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -93,6 +93,9 @@ struct Workspace {
     uint32_t* nranges = nullptr;  // [B]
     uint32_t* ncand = nullptr;    // [B]
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
+    uint32_t* hash = nullptr;     // [B << ts_log2] epoch-tagged visited slots (binsel_fast.cu)
+    uint64_t hash_words = 0;
+    uint32_t hash_epoch = 0;
     // host-call staging (grown on demand)
     float* d_queries = nullptr;
     uint32_t* d_ids = nullptr;
@@ -151,6 +154,23 @@ HostStreams build_streams(const uint32_t* entries, uint32_t table_len, uint32_t 
 [[noreturn]] void unsupported(const std::string& m);
 [[noreturn]] void format(const std::string& m);
 
+// A PQTINDEX v1 file parsed into a Source (index_file.cpp).
+struct MappedFile {
+    const uint8_t* base = nullptr;
+    size_t size = 0;
+    int fd = -1;
+    ~MappedFile();
+};
+struct LoadedFile {
+    MappedFile map;
+    Source src;
+    std::vector<float> level1, level2, d2;
+    std::vector<double> slopes;
+    std::vector<uint32_t> entries, ids;
+    std::vector<uint64_t> offsets;
+};
+void parse_index(const char* path, LoadedFile& lf);
+
 DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, uint64_t shard_hi);
 void validate_config(const pqtg_config& c);
 
@@ -176,6 +196,7 @@ void launch_rerank_fast(const DevParams& p, uint64_t nq, uint32_t k, Workspace& 
                         float* dists, uint32_t* counts, cudaStream_t s);
 // binsel_fast.cu (no resort, 32-bit slot arithmetic)
 bool binsel_fast_ok(const DevParams& p);
+uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch);
 void configure_binsel_fast();
 void launch_binsel_fast(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats, cudaStream_t s);
 // 0 = pick the fastest kernel per stage, 1 = force the generic kernels (parity tests)

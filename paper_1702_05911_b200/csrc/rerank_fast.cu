@@ -1,18 +1,19 @@
 // rerank_fast.cu — K5 fast path: line-quantized re-rank (linequant.cpp:169-182) + top-k
 // (search.cpp:221-257) for p_line == 32 and 1-byte pair ids.
 //
-// Layout of the work: a CTA owns one query; its candidates are split into 8 contiguous
-// warp slices; lane l of a warp re-ranks candidates aw + 32r + l (round r). Each lane sums
+// Work layout: one CTA (16 warps) per query; the query's candidates are cut into 16
+// contiguous warp slices; lane l re-ranks candidates aw + 32r + l (round r). Each lane sums
 // its candidate's 32 fine parts in the reference's order, but lane l runs ONE PART BEHIND
 // lane l-1 (a skewed pipeline): at every step the 32 lanes touch 32 different fine parts,
-// so lookups into the per-query tables, laid out [pair][part], hit 32 different banks.
+// so lookups into the per-query table, laid out [pair][part], hit 32 different banks.
 //
-//   per-query tables   lut[pid][f] = (b2, (a2 - b2) - c2)   and   lc2[pid][f] = c2
-//                      (b2 = fine[f][i], a2 = fine[f][j], (i, j) = pairs[pid]); every value is
-//                      exactly the fp32 intermediate the reference computes, so
-//                      part = (b2 + (λ·λ)·c2) + λ·E  rounds identically.
-//   code staging       each lane prefetches its next rows with cp.async (16 B) into a private
-//                      4-round ring in shared memory, 2 rounds ahead of use.
+//   per-query table   row pid = 32 × (b2, E) then 32 × (c2, 0), E = (a2 - b2) - c2,
+//                     b2 = fine[f][i], a2 = fine[f][j], (i, j) = pairs[pid]: exactly the fp32
+//                     intermediates of the reference, so part = (b2 + (λ·λ)·c2) + λ·E rounds
+//                     identically. One address serves both loads.
+//   code staging      each lane prefetches its next row (64 B) with cp.async into a private
+//                     3-round ring in shared memory, one phase (32 steps) ahead of use.
+//   top-k             (dist, id) keys of all candidates in shared memory, block radix select.
 #include <cstdint>
 
 #include "common.cuh"
@@ -25,10 +26,11 @@ using namespace dev;
 
 namespace {
 
-constexpr int kFastWarps = 8;
+constexpr int kFastWarps = 16;
 constexpr int kFastThreads = kFastWarps * 32;
-constexpr int kSlotBytes = 64;                      // one row: 32 × (λ, pair) bytes
-constexpr int kLaneBytes = 4 * kSlotBytes + 16;     // 4-round ring + pad
+constexpr int kSlotBytes = 64;                   // one row: 32 × (λ, pair) bytes
+constexpr int kLaneBytes = 3 * kSlotBytes + 16;  // 3-round ring + pad
+constexpr uint32_t kRangeCache = 1024;           // ranges cached in shared memory
 constexpr uint32_t kInvalidId = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -44,7 +46,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 struct FastLayout {
-    size_t ring, ids, lut, lc2, fine, pairs, ranges, keys, sel, total;
+    size_t lut, ring, ids, fine, pairs, ranges, keys, sel, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -52,20 +54,18 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 __host__ __device__ inline FastLayout fast_layout(uint32_t npairs, uint32_t k1, uint32_t budget, uint32_t sel_cap) {
     FastLayout l{};
     size_t o = 0;
+    l.lut = o;  // offset 0: lookups use immediate offsets
+    o += (size_t)npairs * 512;
     l.ring = o;
     o += (size_t)kFastThreads * kLaneBytes;
     l.ids = o;
-    o += (size_t)kFastThreads * 4 * 4;
-    l.lut = o;
-    o += align16((size_t)npairs * 32 * 8);
-    l.lc2 = o;
-    o += align16((size_t)npairs * 32 * 4);
+    o += align16((size_t)kFastThreads * 3 * 4);
     l.fine = o;
     o += align16((size_t)32 * k1 * 4);
     l.pairs = o;
     o += align16((size_t)npairs * 4);
     l.ranges = o;
-    o += align16((size_t)budget * 8);
+    o += align16((size_t)(budget < kRangeCache ? budget : kRangeCache) * 8);
     l.keys = o;
     o += align16((size_t)budget * 8);
     l.sel = o;
@@ -84,12 +84,12 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t budget = p.budget, npairs = p.npairs, k1 = p.k1;
     const FastLayout lay = fast_layout(npairs, k1, budget, sel_cap);
+    unsigned char* lut = smem;  // [pid][64] float2
     uint8_t* ring = smem + lay.ring;
     uint32_t* ring_ids = reinterpret_cast<uint32_t*>(smem + lay.ids);
-    float2* lut = reinterpret_cast<float2*>(smem + lay.lut);
-    float* lc2 = reinterpret_cast<float*>(smem + lay.lc2);
     float* fine = reinterpret_cast<float*>(smem + lay.fine);
-    uint2* rg = reinterpret_cast<uint2*>(smem + lay.ranges);
+    uint32_t* spairs = reinterpret_cast<uint32_t*>(smem + lay.pairs);
+    uint2* rg_s = reinterpret_cast<uint2*>(smem + lay.ranges);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + lay.keys);
     uint64_t* sel = reinterpret_cast<uint64_t*>(smem + lay.sel);
     __shared__ uint32_t hist[256];
@@ -100,10 +100,12 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t R = nranges[q], C = ncand[q];
     const uint2* qr = ranges + q * (uint64_t)budget;
+    const bool cached = R <= kRangeCache;
+    const uint2* rg = cached ? rg_s : qr;
 
     for (uint32_t i = tid; i < 32 * k1; i += blockDim.x) fine[i] = fine_in[q * 32 * k1 + i];
-    for (uint32_t r = tid; r < R; r += blockDim.x) rg[r] = qr[r];
-    uint32_t* spairs = reinterpret_cast<uint32_t*>(smem + lay.pairs);
+    if (cached)
+        for (uint32_t r = tid; r < R; r += blockDim.x) rg_s[r] = qr[r];
     for (uint32_t i = tid; i < npairs; i += blockDim.x) spairs[i] = __ldg(p.pairs + i);
     {
         uint4* z = reinterpret_cast<uint4*>(ring + (size_t)tid * kLaneBytes);
@@ -111,7 +113,6 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     }
     if (tid == 0) s_count = 0;
     __syncthreads();
-    // per-query tables, [pid][f] so that lanes at distinct parts hit distinct banks
 #pragma unroll 4
     for (uint32_t idx = tid; idx < npairs * 32; idx += blockDim.x) {
         const uint32_t pid = idx >> 5, f = idx & 31;
@@ -119,8 +120,9 @@ __global__ void __launch_bounds__(kFastThreads, 1)
         const float b2 = fine[f * k1 + (pr & 0xFFFFu)];
         const float a2 = fine[f * k1 + (pr >> 16)];
         const float c2 = __ldg(p.c2 + (size_t)f * npairs + pid);
-        lut[idx] = make_float2(b2, __fsub_rn(__fsub_rn(a2, b2), c2));
-        lc2[idx] = c2;
+        float2* row = reinterpret_cast<float2*>(lut + (size_t)pid * 512);
+        row[f] = make_float2(b2, __fsub_rn(__fsub_rn(a2, b2), c2));
+        row[32 + f] = make_float2(c2, 0.0f);
     }
     __syncthreads();
 
@@ -129,17 +131,18 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     const uint32_t bw = (uint32_t)((uint64_t)C * (warp + 1) / kFastWarps);
     const uint32_t nround = (bw - aw + 31) >> 5;
     uint8_t* my = ring + (size_t)tid * kLaneBytes;
-    uint32_t* myid = ring_ids + tid * 4;
+    uint32_t* myid = ring_ids + tid * 3;
     const bool sharded = p.shard_hi > p.shard_lo;
     uint32_t cursor = 0;
     bool first = true;
 
     auto stage = [&](uint32_t r) {
         const uint32_t c = aw + 32 * r + lane;
-        const uint32_t slot = r & 3;
+        const uint32_t slot = r % 3;
         bool issued = false;
         if (r < nround && c < bw) {
-            // range holding candidate c: last rr with rg[rr].y <= c (candidate offsets ascend)
+            // range holding candidate c: last rr with rg[rr].y <= c (candidate offsets ascend);
+            // successive rounds move c by 32, so at most 32 ranges past the cursor
             uint32_t lo = first ? 0 : cursor;
             uint32_t hi = first ? R - 1 : min(R - 1, cursor + 32);
             first = false;
@@ -148,7 +151,8 @@ __global__ void __launch_bounds__(kFastThreads, 1)
                 if (rg[mid].y <= c) lo = mid; else hi = mid - 1;
             }
             cursor = lo;
-            const uint64_t pos = (uint64_t)rg[lo].x + (c - rg[lo].y);
+            const uint2 e = rg[lo];
+            const uint64_t pos = (uint64_t)e.x + (c - e.y);
             if (!sharded || (pos >= p.shard_lo && pos < p.shard_hi)) {
                 const uint64_t lp = pos - p.shard_lo;
                 const uint8_t* src = p.codes + lp * kSlotBytes;
@@ -163,50 +167,52 @@ __global__ void __launch_bounds__(kFastThreads, 1)
         cp_async_commit();
     };
 
-    stage(0);
-    stage(1);
-    stage(2);
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     const int32_t nparts = (int32_t)nround * 32;
     uint32_t mine = 0;
     float acc = 0.0f, done = 0.0f;
-    // One fine part of lane l's current candidate; g = lane's running part counter.
-    // Branch-free: the finished sum of a candidate (f == 31) is parked in `done` and the
-    // accumulator restarts, so the unrolled steps carry no control flow.
-    auto step = [&](int32_t g) {
-        const uint32_t f = (uint32_t)g & 31u;
-        const uint32_t code = *reinterpret_cast<const uint16_t*>(my + (((uint32_t)g & 127u) << 1));
-        const uint32_t li = ((code >> 8) << 5) | f;
-        const float2 be = lut[li];
-        const float c2 = lc2[li];
-        const float lam = __fmul_rn(__uint2float_rn(code & 0xFFu), inv255);
-        const float part = __fadd_rn(__fadd_rn(be.x, __fmul_rn(__fmul_rn(lam, lam), c2)), __fmul_rn(lam, be.y));
-        acc = __fadd_rn(acc, part);
-        const bool fin = f == 31u;
-        done = fin ? acc : done;
-        acc = fin ? 0.0f : acc;
-    };
+    stage(0);
+    stage(1);
     for (uint32_t m = 0; nround > 0 && m <= nround; ++m) {
-        if (m > 0) stage(m + 2);
-        cp_async_wait<2>();  // rounds <= m have landed (each lane reads only its own ring)
-        const int32_t pb = (int32_t)(m * 32) - lane;
+        if (m > 0) stage(m + 1);
+        cp_async_wait<1>();  // round m has landed (each lane reads only its own ring)
+        // byte offsets of lane l's current (round m) and previous (round m-1) rows, minus 2t
+        const int32_t off_cur = (int32_t)((m % 3) * kSlotBytes) - 2 * lane;
+        const int32_t off_prev = (int32_t)(((m + 2) % 3) * kSlotBytes + kSlotBytes) - 2 * lane;
+        const int32_t nl8 = -8 * lane;
+        // One fine part per lane per step, branch-free: the finished sum of a candidate
+        // (part 31, reached by lane (t + 1) & 31 at step t) is parked in `done`.
+        auto step = [&](int t) {
+            const int32_t off = (t >= lane ? off_cur : off_prev) + 2 * t;
+            const uint32_t code = *reinterpret_cast<const uint16_t*>(my + off);
+            const uint32_t f8 = (uint32_t)(nl8 + 8 * t) & 248u;
+            const uint32_t li8 = ((code << 1) & 0x1FE00u) | f8;  // pid * 512 + f * 8
+            const float2 be = *reinterpret_cast<const float2*>(lut + li8);
+            const float c2 = *reinterpret_cast<const float*>(lut + li8 + 256);
+            const float lam = __fmul_rn(__uint2float_rn(code & 0xFFu), inv255);
+            const float part = __fadd_rn(__fadd_rn(be.x, __fmul_rn(__fmul_rn(lam, lam), c2)), __fmul_rn(lam, be.y));
+            acc = __fadd_rn(acc, part);
+            const bool fin = lane == ((t + 1) & 31);
+            done = fin ? acc : done;
+            acc = fin ? 0.0f : acc;
+        };
         if (m >= 1 && m < nround) {  // every lane busy for all 32 steps
 #pragma unroll
-            for (int t = 0; t < 32; ++t) step(pb + t);
+            for (int t = 0; t < 32; ++t) step(t);
         } else {                     // pipeline fill / drain
 #pragma unroll 4
             for (int t = 0; t < 32; ++t) {
-                const int32_t g = pb + t;
-                if (g >= 0 && g < nparts) step(g);
+                const int32_t g = (int32_t)(m * 32) + t - lane;
+                if (g >= 0 && g < nparts) step(t);
             }
         }
-        // each lane finished exactly one candidate in this phase: lane 0 its round m,
-        // lanes l > 0 their round m - 1 (at t = l - 1)
+        // each lane finished one candidate this phase: lane 0 its round m, lanes l > 0 their
+        // round m - 1 (at step l - 1)
         const int32_t r = lane == 0 ? (int32_t)m : (int32_t)m - 1;
         if (r >= 0 && r < (int32_t)nround) {
             const uint32_t c = aw + 32 * (uint32_t)r + lane;
             if (c < bw) {
-                const uint32_t id = myid[r & 3];
+                const uint32_t id = myid[r % 3];
                 uint64_t key = kSentinel;
                 if (id != kInvalidId) {
                     key = ((uint64_t)orderable(done) << 32) | id;

@@ -66,7 +66,7 @@ class DeviceIndex:
     """A PQT index resident in one GPU's HBM (pqtg_index), plus a workspace for searches."""
 
     def __init__(self, source: "HostIndex | str", device: int = 0, shard: tuple[int, int] = (0, 0),
-                 max_batch: int = 16384):
+                 max_batch: int = 4096):
         L = lib()
         h = C.c_void_p()
         try:
