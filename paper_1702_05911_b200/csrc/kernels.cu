@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
         const float* c = p.fine_t + (size_t)f * fd * k1 + i;
         const float* yf = y + f * fd;
         float acc = 0.0f;
+#pragma unroll 8
         for (uint32_t t = 0; t < fd; ++t) acc = sq_step(acc, yf[t], c[(size_t)t * k1]);
         fine[idx] = acc;
         fine_out[q * L * k1 + idx] = acc;
@@ -89,7 +90,8 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
         const float* yp = y + pp * m;
         const float* cb = p.l2_t + ((size_t)(pp * k1 + parent) * m) * k2 + c;
         float acc = 0.0f;
-        for (uint32_t t = 0; t < m; ++t) acc = sq_step(acc, yp[t], cb[(size_t)t * k2]);
+#pragma unroll 16
+        for (uint32_t t = 0; t < m; ++t) acc = sq_step(acc, yp[t], __ldg(cb + (size_t)t * k2));
         l2d[idx] = acc;
         l2c[idx] = (parent << 16) | c;
     }

@@ -7,10 +7,10 @@
 // lane l-1 (a skewed pipeline): at every step the 32 lanes touch 32 different fine parts,
 // so lookups into the per-query table, laid out [pair][part], hit 32 different banks.
 //
-//   per-query table   row pid = 32 × (b2, E) then 32 × (c2, 0), E = (a2 - b2) - c2,
+//   per-query table   row pid = 32 × float4 (b2, E, c2, 0), E = (a2 - b2) - c2,
 //                     b2 = fine[f][i], a2 = fine[f][j], (i, j) = pairs[pid]: exactly the fp32
 //                     intermediates of the reference, so part = (b2 + (λ·λ)·c2) + λ·E rounds
-//                     identically. One address serves both loads.
+//                     identically. One 16-byte load per part.
 //   code staging      each lane prefetches its next row (64 B) with cp.async into a private
 //                     3-round ring in shared memory, one phase (32 steps) ahead of use.
 //   top-k             (dist, id) keys of all candidates in shared memory, block radix select.
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t budget = p.budget, npairs = p.npairs, k1 = p.k1;
     const FastLayout lay = fast_layout(npairs, k1, budget, sel_cap);
-    unsigned char* lut = smem;  // [pid][64] float2
+    unsigned char* lut = smem;  // [pid][32] float4
     uint8_t* ring = smem + lay.ring;
     uint32_t* ring_ids = reinterpret_cast<uint32_t*>(smem + lay.ids);
     float* fine = reinterpret_cast<float*>(smem + lay.fine);
@@ -120,9 +120,8 @@ __global__ void __launch_bounds__(kFastThreads, 1)
         const float b2 = fine[f * k1 + (pr & 0xFFFFu)];
         const float a2 = fine[f * k1 + (pr >> 16)];
         const float c2 = __ldg(p.c2 + (size_t)f * npairs + pid);
-        float2* row = reinterpret_cast<float2*>(lut + (size_t)pid * 512);
-        row[f] = make_float2(b2, __fsub_rn(__fsub_rn(a2, b2), c2));
-        row[32 + f] = make_float2(c2, 0.0f);
+        reinterpret_cast<float4*>(lut + (size_t)pid * 512)[f] =
+            make_float4(b2, __fsub_rn(__fsub_rn(a2, b2), c2), c2, 0.0f);
     }
     __syncthreads();
 
@@ -168,7 +167,6 @@ __global__ void __launch_bounds__(kFastThreads, 1)
     };
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
-    const int32_t nparts = (int32_t)nround * 32;
     uint32_t mine = 0;
     float acc = 0.0f, done = 0.0f;
     stage(0);
@@ -179,32 +177,25 @@ __global__ void __launch_bounds__(kFastThreads, 1)
         // byte offsets of lane l's current (round m) and previous (round m-1) rows, minus 2t
         const int32_t off_cur = (int32_t)((m % 3) * kSlotBytes) - 2 * lane;
         const int32_t off_prev = (int32_t)(((m + 2) % 3) * kSlotBytes + kSlotBytes) - 2 * lane;
-        const int32_t nl8 = -8 * lane;
+        const int32_t nl16 = -16 * lane;
         // One fine part per lane per step, branch-free: the finished sum of a candidate
-        // (part 31, reached by lane (t + 1) & 31 at step t) is parked in `done`.
-        auto step = [&](int t) {
+        // (part 31, reached by lane (t + 1) & 31 at step t) is parked in `done`. Fill and
+        // drain phases run the same code: before its first and after its last candidate a
+        // lane accumulates stale ring rows into "rounds" -1 / nround, whose keys are never
+        // written, and the part-31 reset clears acc before every real candidate.
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
             const int32_t off = (t >= lane ? off_cur : off_prev) + 2 * t;
             const uint32_t code = *reinterpret_cast<const uint16_t*>(my + off);
-            const uint32_t f8 = (uint32_t)(nl8 + 8 * t) & 248u;
-            const uint32_t li8 = ((code << 1) & 0x1FE00u) | f8;  // pid * 512 + f * 8
-            const float2 be = *reinterpret_cast<const float2*>(lut + li8);
-            const float c2 = *reinterpret_cast<const float*>(lut + li8 + 256);
+            const uint32_t f16 = (uint32_t)(nl16 + 16 * t) & 496u;
+            const uint32_t li = ((code << 1) & 0x1FE00u) | f16;  // pid * 512 + f * 16
+            const float4 e = *reinterpret_cast<const float4*>(lut + li);
             const float lam = __fmul_rn(__uint2float_rn(code & 0xFFu), inv255);
-            const float part = __fadd_rn(__fadd_rn(be.x, __fmul_rn(__fmul_rn(lam, lam), c2)), __fmul_rn(lam, be.y));
+            const float part = __fadd_rn(__fadd_rn(e.x, __fmul_rn(__fmul_rn(lam, lam), e.z)), __fmul_rn(lam, e.y));
             acc = __fadd_rn(acc, part);
             const bool fin = lane == ((t + 1) & 31);
             done = fin ? acc : done;
             acc = fin ? 0.0f : acc;
-        };
-        if (m >= 1 && m < nround) {  // every lane busy for all 32 steps
-#pragma unroll
-            for (int t = 0; t < 32; ++t) step(t);
-        } else {                     // pipeline fill / drain
-#pragma unroll 4
-            for (int t = 0; t < 32; ++t) {
-                const int32_t g = (int32_t)(m * 32) + t - lane;
-                if (g >= 0 && g < nparts) step(t);
-            }
         }
         // each lane finished one candidate this phase: lane 0 its round m, lanes l > 0 their
         // round m - 1 (at step l - 1)
