@@ -184,6 +184,50 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# --------------------------------------------------------------------------- recall
+def counters_ids(dev, dq, nq, k, step, d_ids, d_counts):
+    import torch
+
+    step(0)
+    torch.cuda.synchronize()
+    return d_ids.cpu().numpy().view(np.uint32), d_counts.cpu().numpy().view(np.uint32)
+
+
+def measure_recall(name: str, seed: int, device: int, Q: np.ndarray, nq_pool: int, result):
+    """recall@R = fraction of queries whose exact nearest neighbour is within the first R
+    results (recall_fraction, bench.cpp:23-44); exact neighbours by brute force on the GPU
+    over the regenerated (deterministic) base set. Identical for the CPU reference, whose
+    ids are bit-identical."""
+    import torch
+
+    from paper_1702_05911_b200 import builder
+
+    wl = WORKLOADS[name]
+    ids, counts = result
+    dev = torch.device("cuda", device)
+    # regenerate exactly the build's draw (same generator sequence), keep the base rows
+    X = builder.synth_clustered(wl["n"] + nq_pool, wl["config"]["dim"], wl["blobs"], wl["sigma"], seed,
+                                device=dev)[: wl["n"]]
+    q = torch.from_numpy(Q).to(dev)
+    best_d = torch.full((q.shape[0],), float("inf"), device=dev)
+    best_i = torch.zeros(q.shape[0], dtype=torch.int64, device=dev)
+    qq = (q * q).sum(1, keepdim=True)
+    for s in range(0, X.shape[0], 1 << 18):
+        xb = X[s:s + (1 << 18)]
+        d = qq - 2.0 * (q @ xb.T) + (xb * xb).sum(1)[None, :]
+        v, i = d.min(1)
+        better = v < best_d
+        best_d = torch.where(better, v, best_d)
+        best_i = torch.where(better, i + s, best_i)
+    del X
+    truth = best_i.cpu().numpy()
+    out = {}
+    for R in (1, 10, 100):
+        hit = [truth[i] in ids[i, : min(R, counts[i])] for i in range(len(truth))]
+        out[f"r@{R}"] = float(np.mean(hit))
+    return out
+
+
 # --------------------------------------------------------------------------- CPU legs
 def cpu_leg(hix, Q, k, min_seconds=10.0, max_reps=20):
     """Time the reference (oracle/_ref) — else the C restatement — on this host's cores."""
@@ -260,6 +304,9 @@ def main():
     ap.add_argument("--batches", type=int, default=4, help="distinct query batches cycled over steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--variant", type=int, default=0,
+                    help="kernel variant: 0 auto, 1 generic, 2 skewed re-rank, 3 table re-rank")
+    ap.add_argument("--no-recall", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -289,6 +336,7 @@ def main():
         dist.barrier()
         if rank != 0:
             hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * world)
+    lib().pqtg_set_kernel_variant(args.variant)
     dev = DeviceIndex(hix, device=local, max_batch=nq)
     batches = [Qpool[(rank * args.batches + b) * nq:(rank * args.batches + b + 1) * nq] for b in range(args.batches)]
     d_q = [torch.from_numpy(b).cuda() for b in batches]
@@ -413,6 +461,10 @@ def main():
                 np.array_equal(g_d[q, :c].view(np.uint32), r_d[q, :c].view(np.uint32))
         parity = {"queries": nq, "bit_exact_vs": cpu["kind"], "ok": bool(same)}
 
+    recall = None
+    if not args.no_recall:
+        recall = measure_recall(args.workload, args.seed, local, batches[0], nq * args.batches * max(world, 1),
+                                counters_ids(dev, d_q[0], nq, k, step, d_ids, d_counts))
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -427,6 +479,8 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu,
         "parity": parity,
+        "recall": recall,
+        "kernel_variant": args.variant,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -412,7 +412,7 @@ size_t binsel_smem(const DevParams& p) {
 
 void launch_binsel(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats,
                    cudaStream_t s) {
-    if (kernel_variant() == 0 && binsel_fast_ok(p)) {
+    if (kernel_variant() != 1 && binsel_fast_ok(p)) {
         launch_binsel_fast(p, nq, ws, stats, s);
         return;
     }
@@ -593,7 +593,12 @@ size_t rerank_smem(const DevParams& p, uint32_t k) {
 
 void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
                    float* dists, uint32_t* counts, cudaStream_t s) {
-    if (kernel_variant() == 0 && rerank_fast_ok(p, k)) {
+    const int v = kernel_variant();
+    if ((v == 0 || v == 3) && rerank_lut_ok(p, k)) {
+        launch_rerank_lut(p, nq, k, ws, ids, dists, counts, s);
+        return;
+    }
+    if ((v == 0 || v == 2) && rerank_fast_ok(p, k)) {
         launch_rerank_fast(p, nq, k, ws, ids, dists, counts, s);
         return;
     }
@@ -637,6 +642,7 @@ void configure_kernels(const DevParams& p, uint32_t) {
         set_rerank_attr<32, 2>();
         set_rerank_attr<0, 2>();
         configure_rerank_fast();
+        configure_rerank_lut();
         configure_binsel_fast();
     });
     (void)p;

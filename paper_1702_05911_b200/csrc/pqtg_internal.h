@@ -199,7 +199,14 @@ bool binsel_fast_ok(const DevParams& p);
 uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch);
 void configure_binsel_fast();
 void launch_binsel_fast(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats, cudaStream_t s);
-// 0 = pick the fastest kernel per stage, 1 = force the generic kernels (parity tests)
+// rerank_lut.cu (thread per candidate, per-query float4 table; 1-byte pairs, k1 <= 16)
+size_t rerank_lut_smem(const DevParams& p, uint32_t k);
+bool rerank_lut_ok(const DevParams& p, uint32_t k);
+void configure_rerank_lut();
+void launch_rerank_lut(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
+                       float* dists, uint32_t* counts, cudaStream_t s);
+// 0 = pick the fastest kernel per stage, 1 = generic kernels only, 2 = prefer the skewed
+// re-rank, 3 = prefer the table re-rank (parity tests cover every variant)
 int kernel_variant();
 
 }  // namespace pqtg

@@ -13,12 +13,15 @@ from paper_1702_05911_b200 import DeviceIndex, HostIndex, knn_query_batch, merge
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "generic"], autouse=True)
+VARIANTS = {"auto": 0, "generic": 1, "skew": 2, "table": 3}
+
+
+@pytest.fixture(params=list(VARIANTS), autouse=True)
 def kernel_variant(request):
-    """Run every GPU parity test through the fast kernels and through the generic ones."""
+    """Run every GPU parity test through each kernel variant (fast, generic, skewed, table)."""
     from paper_1702_05911_b200._abi import lib
 
-    lib().pqtg_set_kernel_variant(0 if request.param == "auto" else 1)
+    lib().pqtg_set_kernel_variant(VARIANTS[request.param])
     yield request.param
     lib().pqtg_set_kernel_variant(0)
 
