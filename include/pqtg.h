@@ -128,8 +128,7 @@ typedef struct pqtg_workspace pqtg_workspace;
 int pqtg_abi_version(void);
 const char* pqtg_last_error(void);
 /* Kernel selection, process-wide: 0 = fastest kernel for each stage (default), 1 = the
- * generic kernels only, 2 = prefer the skewed re-rank, 3 = prefer the table re-rank. The
- * parity tests run every variant; results are identical by construction. */
+ * generic kernels only. The parity tests run both; results are identical by construction. */
 int pqtg_set_kernel_variant(int variant);
 /* 1 when a CUDA device with compute capability 10.x is usable, else 0. */
 int pqtg_device_ok(int device);

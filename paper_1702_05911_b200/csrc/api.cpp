@@ -117,8 +117,8 @@ extern "C" {
 int pqtg_abi_version(void) { return PQTG_ABI_VERSION; }
 
 int pqtg_set_kernel_variant(int variant) {
-    if (variant < 0 || variant > 3) {
-        set_error("variant must be 0 (auto), 1 (generic), 2 (skewed re-rank) or 3 (table re-rank)");
+    if (variant != 0 && variant != 1) {
+        set_error("variant must be 0 (auto) or 1 (generic)");
         return PQTG_ERR_ARG;
     }
     g_variant.store(variant);

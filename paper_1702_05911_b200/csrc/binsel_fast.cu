@@ -24,8 +24,10 @@ using namespace dev;
 namespace {
 
 constexpr int kBsThreads = 256;
-constexpr int kBsWarps = kBsThreads / 32;
+constexpr int kFilterWarps = kBsThreads / 32 - 1;  // warp 0 walks the queue
+constexpr int kFilterThreads = kFilterWarps * 32;
 constexpr int kMaxItems = 8;
+constexpr uint32_t kQueueCap = kFilterThreads * kMaxItems;
 
 __device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t H) {
     const uint64_t x = (uint64_t)a + b;
@@ -46,7 +48,7 @@ __host__ __device__ inline BsLayout bs_layout(uint32_t PW, uint32_t W2ab, uint32
     l.tb = o;
     o += (size_t)W2ab * 4;
     l.queue = o;
-    o += (size_t)kBsThreads * kMaxItems * 8;
+    o += (size_t)2 * kQueueCap * 8;  // double-buffered
     l.hash = o;
     o += (size_t)ts * 4;
     l.total = o;
@@ -75,8 +77,8 @@ __global__ void __launch_bounds__(kBsThreads, 4)
     const uint32_t TS = 1u << ts_log2;
     uint32_t* hkeys = HASH ? ghash + ((uint64_t)blockIdx.x << ts_log2) : nullptr;
     const uint32_t etag = epoch << 26;
-    __shared__ uint32_t wcnt[kMaxItems * kBsWarps];
-    __shared__ uint32_t s_nq, s_C, s_R, s_maxord;
+    __shared__ uint32_t wcnt[2][64];
+    __shared__ uint32_t s_nq[2], s_C, s_R, s_maxord;
 
     const uint64_t q = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -107,172 +109,184 @@ __global__ void __launch_bounds__(kBsThreads, 4)
     const uint32_t budget = p.budget;
     const uint64_t total = p.total_tuples;
     uint2* qranges = ranges + q * (uint64_t)budget;
-    uint32_t C = 0, R = 0;
-    uint64_t base = 0;
+    // Warp 0 walks the queue of pass i-1 while warps 1..7 filter pass i (warp
+    // specialization): per pass two barriers, and the queue's dependent loads (hash probe,
+    // offsets) overlap the next pass's stream/bitmap loads.
+    const int fw = warp - 1;                // filter warp index, -1 for warp 0
+    const int ft = tid - 32;                // filter thread index
+    uint64_t base = 0;                      // first stream position of the pass being filtered
     uint32_t nit = 1;
-    while (C < budget && base < total) {
-        // ---- filter: slot + non-empty test for 256·nit consecutive stream positions.
-        // Three unrolled sweeps so each thread's loads are issued together: stream entries,
-        // then slots + bitmap words, then the ballots.
-        uint32_t slot[kMaxItems], word[kMaxItems], ball[kMaxItems];
-        uint2 ent[kMaxItems];
-#pragma unroll
-        for (int it = 0; it < kMaxItems; ++it) {
-            const uint64_t s = base + (uint64_t)it * kBsThreads + tid;
-            ent[it] = make_uint2(0, 0);
-            if (it < (int)nit && s < total) {
-                if constexpr (P == 2) {
-                    ent[it].x = __ldg(p.pair_streams + (size_t)ta * p.W2 + s);
-                } else if constexpr (P == 4) {
-                    if (s < p.merge_count) {
-                        ent[it] = __ldg(p.merge + s);
-                    } else {
-                        const uint64_t j = s - p.merge_count;
-                        const uint64_t u = p.merge_row0 + j / p.W2;
-                        ent[it] = make_uint2((uint32_t)u, (uint32_t)(j - (u - p.merge_row0) * p.W2));
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int it = 0; it < kMaxItems; ++it) {
-            const uint64_t s = base + (uint64_t)it * kBsThreads + tid;
-            slot[it] = 0;
-            word[it] = 0;
-            if (it < (int)nit && s < total) {
-                uint32_t sl;
-                if constexpr (P == 1) {
-                    sl = terms[s];
-                } else if constexpr (P == 2) {
-                    const uint32_t e = ent[it].x;
-                    sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
-                } else if (W2ab) {
-                    sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
-                } else {
-                    const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + ent[it].x);
-                    const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + ent[it].y);
-                    sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
-                                 add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
-                }
-                slot[it] = sl;
-                word[it] = __ldg(p.bitmap + (sl >> 5));
-            }
-        }
-#pragma unroll
-        for (int it = 0; it < kMaxItems; ++it) {
-            ball[it] = 0;
-            if (it < (int)nit) {
-                const uint64_t s = base + (uint64_t)it * kBsThreads + tid;
-                const bool ne = s < total && ((word[it] >> (slot[it] & 31)) & 1u);
-                ball[it] = __ballot_sync(0xffffffffu, ne);
-                if (lane == 0) wcnt[it * kBsWarps + warp] = __popc(ball[it]);
-            }
-        }
-        __syncthreads();
-        // ---- order-preserving compaction: scan per-(item, warp) counts in stream order
+    uint32_t prev_n = 0;                    // queued tuples of the previous pass
+    for (uint32_t pass = 0;; ++pass) {
+        const uint32_t buf = pass & 1u;
+        uint2* qb = queue + (size_t)buf * kQueueCap;
+        uint32_t slot[kMaxItems], ball[kMaxItems];
         if (warp == 0) {
-            const uint32_t n = nit * kBsWarps;
-            const uint32_t v = lane < (int)n ? wcnt[lane] : 0;
-            uint32_t incl = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            if (lane < (int)n) wcnt[lane] = incl - v;
-            if (lane == 31) s_nq = incl;
-            // nit * 8 <= 64 > 32 when nit == 8: second half
-            if (n > 32) {
-                const uint32_t v2 = (uint32_t)(lane + 32) < n ? wcnt[lane + 32] : 0;
-                uint32_t incl2 = v2;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl2, o);
-                    if (lane >= o) incl2 += t;
-                }
-                const uint32_t carry = __shfl_sync(0xffffffffu, incl, 31);
-                if ((uint32_t)(lane + 32) < n) wcnt[lane + 32] = carry + incl2 - v2;
-                if (lane == 31) s_nq = carry + incl2;
-            }
-        }
-        __syncthreads();
-        const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-        for (int it = 0; it < kMaxItems; ++it) {
-            if (it < (int)nit && ((ball[it] >> lane) & 1u)) {
-                const uint32_t at = wcnt[it * kBsWarps + warp] + __popc(ball[it] & lt);
-                queue[at] = make_uint2((uint32_t)(base + (uint64_t)it * kBsThreads + tid), slot[it]);
-            }
-        }
-        __syncthreads();
-        // ---- warp 0: walk the non-empty tuples in stream order
-        const uint32_t nq = s_nq;
-        if (warp == 0 && nq > 0) {
-            uint32_t c = s_C, r = s_R, maxord = s_maxord;
-            for (uint32_t b0 = 0; b0 < nq && c < budget; b0 += 32) {
-                const uint32_t idx = b0 + lane;
-                const bool has = idx < nq;
-                const uint2 e = has ? queue[idx] : make_uint2(0, kEmptyKey);
-                bool first = has;
-                if (HASH) {
-                    const uint32_t grp = __match_any_sync(0xffffffffu, e.y);
-                    if (has) {
-                        if ((uint32_t)(__ffs(grp) - 1) != (uint32_t)lane) {
-                            first = false;  // an earlier tuple of this batch has the slot
-                        } else {
-                            const uint32_t key = etag | e.y;
-                            uint32_t h = (e.y * 0x9E3779B1u) >> (32 - ts_log2);
-                            for (;;) {
-                                const uint32_t cur = hkeys[h];
-                                if ((cur & 0xFC000000u) != etag) {  // stale epoch = empty
-                                    if (atomicCAS(hkeys + h, cur, key) == cur) break;
-                                    continue;  // lost a race on this entry; re-read it
+            // ---- queue of the previous pass, in stream order, 32 tuples at a time
+            if (pass > 0 && prev_n > 0) {
+                const uint2* qp = queue + (size_t)(buf ^ 1u) * kQueueCap;
+                uint32_t c = s_C, r = s_R, maxord = s_maxord;
+                const uint32_t lt = (1u << lane) - 1u;
+                for (uint32_t b0 = 0; b0 < prev_n && c < budget; b0 += 32) {
+                    const uint32_t idx = b0 + lane;
+                    const bool has = idx < prev_n;
+                    const uint2 e = has ? qp[idx] : make_uint2(0, kEmptyKey);
+                    bool first = has;
+                    if (HASH) {
+                        const uint32_t grp = __match_any_sync(0xffffffffu, e.y);
+                        if (has) {
+                            if ((uint32_t)(__ffs(grp) - 1) != (uint32_t)lane) {
+                                first = false;  // an earlier tuple of this batch has the slot
+                            } else {
+                                const uint32_t key = etag | e.y;
+                                uint32_t h = (e.y * 0x9E3779B1u) >> (32 - ts_log2);
+                                for (;;) {
+                                    const uint32_t cur = hkeys[h];
+                                    if ((cur & 0xFC000000u) != etag) {  // stale epoch = empty
+                                        if (atomicCAS(hkeys + h, cur, key) == cur) break;
+                                        continue;  // lost a race on this entry; re-read it
+                                    }
+                                    if (cur == key) {
+                                        first = false;  // visited in an earlier batch
+                                        break;
+                                    }
+                                    h = (h + 1) & (TS - 1);
                                 }
-                                if (cur == key) {
-                                    first = false;  // visited in an earlier batch
-                                    break;
-                                }
-                                h = (h + 1) & (TS - 1);
                             }
                         }
                     }
-                }
-                uint32_t start = 0, cnt = 0;
-                if (first) {
-                    start = __ldg(p.offsets + e.y);
-                    cnt = __ldg(p.offsets + e.y + 1) - start;
-                }
-                uint32_t incl = cnt;
+                    uint32_t start = 0, cnt = 0;
+                    if (first) {
+                        start = __ldg(p.offsets + e.y);
+                        cnt = __ldg(p.offsets + e.y + 1) - start;
+                    }
+                    uint32_t incl = cnt;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    const uint32_t before = c + (incl - cnt);  // < 2^32: distinct bins hold <= n ids
+                    const bool emit = first && before < budget;
+                    const uint32_t em = __ballot_sync(0xffffffffu, emit);
+                    if (emit) {
+                        qranges[r + __popc(em & lt)] = make_uint2(start, before);
+                        maxord = max(maxord, e.x);
+                    }
+                    maxord = __reduce_max_sync(0xffffffffu, maxord);
+                    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                    r += __popc(em);
+                    c = (uint64_t)c + tot >= budget ? budget : c + tot;
                 }
-                const uint32_t before = c + (incl - cnt);  // < 2^32: distinct bins hold <= n ids
-                const bool emit = first && before < budget;
-                const uint32_t em = __ballot_sync(0xffffffffu, emit);
-                if (emit) {
-                    qranges[r + __popc(em & lt)] = make_uint2(start, before);
-                    maxord = max(maxord, e.x);
+                if (lane == 0) {
+                    s_C = c;
+                    s_R = r;
+                    s_maxord = maxord;
                 }
-                maxord = __reduce_max_sync(0xffffffffu, maxord);
-                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-                r += __popc(em);
-                c = (uint64_t)c + tot >= budget ? budget : c + tot;
             }
-            if (lane == 0) {
-                s_C = c;
-                s_R = r;
-                s_maxord = maxord;
+        } else if (base < total) {
+            // ---- filter: slot + non-empty test for kFilterThreads·nit stream positions;
+            // three unrolled sweeps so each thread's loads are issued together
+            uint32_t word[kMaxItems];
+            uint2 ent[kMaxItems];
+#pragma unroll
+            for (int it = 0; it < kMaxItems; ++it) {
+                const uint64_t s = base + (uint64_t)it * kFilterThreads + ft;
+                ent[it] = make_uint2(0, 0);
+                if (it < (int)nit && s < total) {
+                    if constexpr (P == 2) {
+                        ent[it].x = __ldg(p.pair_streams + (size_t)ta * p.W2 + s);
+                    } else if constexpr (P == 4) {
+                        if (s < p.merge_count) {
+                            ent[it] = __ldg(p.merge + s);
+                        } else {
+                            const uint64_t j = s - p.merge_count;
+                            const uint64_t u = p.merge_row0 + j / p.W2;
+                            ent[it] = make_uint2((uint32_t)u, (uint32_t)(j - (u - p.merge_row0) * p.W2));
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int it = 0; it < kMaxItems; ++it) {
+                const uint64_t s = base + (uint64_t)it * kFilterThreads + ft;
+                slot[it] = 0;
+                word[it] = 0;
+                if (it < (int)nit && s < total) {
+                    uint32_t sl;
+                    if constexpr (P == 1) {
+                        sl = terms[s];
+                    } else if constexpr (P == 2) {
+                        const uint32_t e = ent[it].x;
+                        sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
+                    } else if (W2ab) {
+                        sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
+                    } else {
+                        const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + ent[it].x);
+                        const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + ent[it].y);
+                        sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
+                                     add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
+                    }
+                    slot[it] = sl;
+                    word[it] = __ldg(p.bitmap + (sl >> 5));
+                }
+            }
+#pragma unroll
+            for (int it = 0; it < kMaxItems; ++it) {
+                ball[it] = 0;
+                if (it < (int)nit) {
+                    const uint64_t s = base + (uint64_t)it * kFilterThreads + ft;
+                    const bool ne = s < total && ((word[it] >> (slot[it] & 31)) & 1u);
+                    ball[it] = __ballot_sync(0xffffffffu, ne);
+                    if (lane == 0) wcnt[buf][it * kFilterWarps + fw] = __popc(ball[it]);
+                }
             }
         }
-        __syncthreads();
-        C = s_C;
-        R = s_R;
-        base += (uint64_t)nit * kBsThreads;
+        __syncthreads();  // B1: counts of pass `pass`; C / R after the previous pass's queue
+        // done: budget reached, or the stream ended and its last queue was just walked
+        if (s_C >= budget || base >= total) break;
+        // ---- order-preserving compaction (every filter warp scans the counts itself)
+        if (warp > 0) {
+            const uint32_t n = nit * kFilterWarps;
+            const uint32_t v0 = lane < (int)n ? wcnt[buf][lane] : 0;
+            const uint32_t v1 = (uint32_t)(lane + 32) < n ? wcnt[buf][lane + 32] : 0;
+            uint32_t i0 = v0, i1 = v1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t0 = __shfl_up_sync(0xffffffffu, i0, o);
+                const uint32_t t1 = __shfl_up_sync(0xffffffffu, i1, o);
+                if (lane >= o) {
+                    i0 += t0;
+                    i1 += t1;
+                }
+            }
+            const uint32_t carry = __shfl_sync(0xffffffffu, i0, 31);
+            const uint32_t ntot = carry + __shfl_sync(0xffffffffu, i1, 31);
+            const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+            for (int it = 0; it < kMaxItems; ++it) {
+                if (it < (int)nit) {
+                    // exclusive prefix of entry e = (item, filter warp) in stream order
+                    const uint32_t e = it * kFilterWarps + fw;
+                    const uint32_t src = e & 31u;
+                    const uint32_t a0 = __shfl_sync(0xffffffffu, i0, src) - __shfl_sync(0xffffffffu, v0, src);
+                    const uint32_t a1 = __shfl_sync(0xffffffffu, i1, src) - __shfl_sync(0xffffffffu, v1, src);
+                    const uint32_t excl = e < 32 ? a0 : carry + a1;
+                    if ((ball[it] >> lane) & 1u) {
+                        qb[excl + __popc(ball[it] & lt)] =
+                            make_uint2((uint32_t)(base + (uint64_t)it * kFilterThreads + ft), slot[it]);
+                    }
+                }
+            }
+            if (warp == 1 && lane == 0) s_nq[buf] = ntot;
+        }
+        __syncthreads();  // B2: queue of pass `pass` complete
+        prev_n = s_nq[buf];
+        base += (uint64_t)nit * kFilterThreads;
         nit = nit * 2 < (uint32_t)kMaxItems ? nit * 2 : (uint32_t)kMaxItems;
     }
     if (tid == 0) {
+        const uint32_t C = s_C, R = s_R;
         nranges[q] = R;
         ncand[q] = C;
         ntuples[q] = C >= budget && budget > 0 ? s_maxord + 1 : (uint32_t)min(base, total);

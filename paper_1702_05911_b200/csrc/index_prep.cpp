@@ -320,6 +320,22 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
         p.offsets = upload(*ix, off32.data(), off32.size());
     }
 
+    // --- k1 <= 16 with 1-byte pairs: codes carry (i << 4 | j); c2 by that byte
+    p.code_ij = (pw == 1 && k1 <= 16) ? 1u : 0u;
+    std::vector<uint8_t> ij_of(npairs, 0);
+    if (p.code_ij) {
+        std::vector<float> c2ij((size_t)L * 256, 0.0f);
+        uint32_t q = 0;
+        if (k1 > 1) {
+            for (uint32_t i = 0; i < k1; ++i)
+                for (uint32_t j = i + 1; j < k1; ++j) ij_of[q++] = (uint8_t)((i << 4) | j);
+        }
+        for (uint32_t f = 0; f < L; ++f)
+            for (uint32_t i = 0; i < k1; ++i)
+                for (uint32_t j = 0; j < k1; ++j) c2ij[(size_t)f * 256 + (i << 4) + j] = src.d2[((size_t)f * k1 + i) * k1 + j];
+        p.c2ij = upload(*ix, c2ij.data(), c2ij.size());
+    }
+
     // --- this shard's ids and line codes in slot order
     const uint64_t npos = shard_hi - shard_lo;
     p.ids = upload(*ix, src.ids + shard_lo, npos);
@@ -351,9 +367,11 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
                             pid = src.pair_id[id * L + f];
                         }
                         if (pid >= npairs) bad_pid = true;
-                        if (pw == 1) {  // interleaved (lambda, pair id) per part
+                        if (pw == 1) {  // interleaved (lambda, pair) per part
                             row[2 * f] = (uint8_t)lq;
-                            row[2 * f + 1] = (uint8_t)pid;
+                            // k1 <= 16: store the pair as its centroids (i << 4 | j), so the
+                            // re-rank indexes the fine row and c2[f][i][j] directly
+                            row[2 * f + 1] = (uint8_t)(p.code_ij && pid < npairs ? ij_of[pid] : pid);
                         } else {        // lambda block, then little-endian u16 pair ids
                             row[f] = (uint8_t)lq;
                             row[L + 2 * f] = (uint8_t)(pid & 0xFF);

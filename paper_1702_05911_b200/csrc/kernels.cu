@@ -130,7 +130,11 @@ size_t traverse_smem(const DevParams& p) {
 
 void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, Workspace& ws,
                      cudaStream_t s) {
-    traverse_kernel<<<(unsigned)nq, kThreads, traverse_smem(p), s>>>(p, queries, ws.fine, ws.l2_dist,
+    // one thread per level-2 distance (P·w·k2 of them) keeps every thread busy in the long
+    // sequential m-loop; 64..256 threads
+    const uint32_t jobs = p.P * p.w * p.k2;
+    const unsigned bs = jobs >= 256 ? 256u : (jobs <= 64 ? 64u : (unsigned)((jobs + 31) / 32 * 32));
+    traverse_kernel<<<(unsigned)nq, bs, traverse_smem(p), s>>>(p, queries, ws.fine, ws.l2_dist,
                                                                      ws.l2_code, ws.slope);
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
@@ -434,10 +438,28 @@ void launch_binsel(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_st
 // =====================================================================================
 namespace {
 
+// part contribution (linequant.hpp:83-85 in linequant.cpp:171-181's order) for stored byte
+// `b` (a pair id, or i << 4 | j when the index re-encoded pairs); c2 rows are [f][npairs] or,
+// for (i, j) codes, [f][256].
+__device__ __forceinline__ void pair_terms(uint32_t b, uint32_t f, bool ij, const float* fine, const float* c2,
+                                           const uint32_t* pairs, uint32_t k1, uint32_t npairs, float& b2,
+                                           float& a2, float& cc) {
+    if (ij) {
+        b2 = fine[f * k1 + (b >> 4)];
+        a2 = fine[f * k1 + (b & 15u)];
+        cc = c2[f * 256 + b];
+    } else {
+        const uint32_t pr = pairs[b];
+        b2 = fine[f * k1 + (pr & 0xFFFFu)];
+        a2 = fine[f * k1 + (pr >> 16)];
+        cc = c2[f * npairs + b];
+    }
+}
+
 template <int LT, int PW>
 __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ row, const float* fine,
                                                    const float* c2, const uint32_t* pairs, uint32_t L,
-                                                   uint32_t k1, uint32_t npairs) {
+                                                   uint32_t k1, uint32_t npairs, bool ij) {
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     float total = 0.0f;
     if constexpr (LT > 0) {
@@ -460,10 +482,8 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
                 const int b0 = LT + 2 * f, b1 = b0 + 1;
                 pid = ((wds[b0 >> 2] >> ((b0 & 3) * 8)) & 0xFFu) | (((wds[b1 >> 2] >> ((b1 & 3) * 8)) & 0xFFu) << 8);
             }
-            const uint32_t pr = pairs[pid];
-            const float b2 = fine[f * k1 + (pr & 0xFFFFu)];
-            const float a2 = fine[f * k1 + (pr >> 16)];
-            const float cc = c2[f * npairs + pid];
+            float b2, a2, cc;
+            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc);
             const float lam = __fmul_rn((float)lq, inv255);
             const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
                                          __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
@@ -479,10 +499,8 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
                 lq = __ldg(row + f);
                 pid = (uint32_t)__ldg(row + L + 2 * f) | ((uint32_t)__ldg(row + L + 2 * f + 1) << 8);
             }
-            const uint32_t pr = pairs[pid];
-            const float b2 = fine[f * k1 + (pr & 0xFFFFu)];
-            const float a2 = fine[f * k1 + (pr >> 16)];
-            const float cc = c2[f * npairs + pid];
+            float b2, a2, cc;
+            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc);
             const float lam = __fmul_rn((float)lq, inv255);
             const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
                                          __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
@@ -515,7 +533,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     uint64_t* sel = keys + budget;                                // sel_cap
     float* fine = reinterpret_cast<float*>(sel + sel_cap);        // L*k1
     float* c2 = fine + L * k1;                                    // L*npairs
-    uint32_t* pairs = reinterpret_cast<uint32_t*>(c2 + L * npairs);  // npairs
+    uint32_t* pairs = reinterpret_cast<uint32_t*>(c2 + L * (p.code_ij ? 256u : npairs));  // npairs
     uint32_t* coff = pairs + npairs;                              // budget
     __shared__ uint32_t hist[256];
     __shared__ uint32_t s_count;
@@ -527,7 +545,9 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     const uint2* qr = ranges + q * (uint64_t)budget;
 
     for (uint32_t i = tid; i < L * k1; i += blockDim.x) fine[i] = fine_in[q * L * k1 + i];
-    for (uint32_t i = tid; i < L * npairs; i += blockDim.x) c2[i] = __ldg(p.c2 + i);
+    const bool ij = p.code_ij != 0;
+    const uint32_t c2n = ij ? L * 256 : L * npairs;
+    for (uint32_t i = tid; i < c2n; i += blockDim.x) c2[i] = __ldg((ij ? p.c2ij : p.c2) + i);
     for (uint32_t i = tid; i < npairs; i += blockDim.x) pairs[i] = __ldg(p.pairs + i);
     for (uint32_t r = tid; r < R; r += blockDim.x) coff[r] = qr[r].y;
     if (tid == 0) s_count = 0;
@@ -547,7 +567,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
         if (!sharded || (pos >= p.shard_lo && pos < p.shard_hi)) {
             const uint64_t lp = pos - p.shard_lo;
             const uint32_t id = __ldg(p.ids + lp);
-            const float d = line_distance_row<LT, PW>(p.codes + lp * p.row_bytes, fine, c2, pairs, L, k1, npairs);
+            const float d = line_distance_row<LT, PW>(p.codes + lp * p.row_bytes, fine, c2, pairs, L, k1, npairs, ij);
             key = ((uint64_t)orderable(d) << 32) | id;
             ++mine;
         }
@@ -587,19 +607,14 @@ void set_rerank_attr() {
 }  // namespace
 
 size_t rerank_smem(const DevParams& p, uint32_t k) {
-    return 8ull * p.budget + 8ull * sel_cap_for(p, k) + 4ull * p.L * p.k1 + 4ull * p.L * p.npairs +
-           4ull * p.npairs + 4ull * p.budget;
+    return 8ull * p.budget + 8ull * sel_cap_for(p, k) + 4ull * p.L * p.k1 +
+           4ull * p.L * (p.code_ij ? 256u : p.npairs) + 4ull * p.npairs + 4ull * p.budget;
 }
 
 void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
                    float* dists, uint32_t* counts, cudaStream_t s) {
-    const int v = kernel_variant();
-    if ((v == 0 || v == 3) && rerank_lut_ok(p, k)) {
-        launch_rerank_lut(p, nq, k, ws, ids, dists, counts, s);
-        return;
-    }
-    if ((v == 0 || v == 2) && rerank_fast_ok(p, k)) {
-        launch_rerank_fast(p, nq, k, ws, ids, dists, counts, s);
+    if (kernel_variant() == 0 && rerank_ij_ok(p, k)) {
+        launch_rerank_ij(p, nq, k, ws, ids, dists, counts, s);
         return;
     }
     const size_t sm = rerank_smem(p, k);
@@ -641,8 +656,7 @@ void configure_kernels(const DevParams& p, uint32_t) {
         set_rerank_attr<0, 1>();
         set_rerank_attr<32, 2>();
         set_rerank_attr<0, 2>();
-        configure_rerank_fast();
-        configure_rerank_lut();
+        configure_rerank_ij();
         configure_binsel_fast();
     });
     (void)p;

@@ -65,6 +65,8 @@ struct DevParams {
     const uint32_t* offsets;    // [H + 1] u32
     const uint32_t* ids;        // [shard positions]
     const uint8_t* codes;       // [shard positions][row_bytes]
+    uint32_t code_ij;           // 1-byte codes hold (i << 4 | j) instead of the pair id (k1 <= 16)
+    const float* c2ij;          // [L][256] d2[f][i][j] at i << 4 | j (code_ij only)
 };
 
 struct DevIndex {
@@ -188,25 +190,17 @@ void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids,
                   const float* dists, const uint32_t* counts, uint32_t* out_ids,
                   float* out_dists, uint32_t* out_counts, cudaStream_t s);
 void configure_kernels(const DevParams& p, uint32_t k);
-// rerank_fast.cu (p_line == 32, 1-byte pair ids)
-size_t rerank_fast_smem(const DevParams& p, uint32_t k);
-bool rerank_fast_ok(const DevParams& p, uint32_t k);
-void configure_rerank_fast();
-void launch_rerank_fast(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
-                        float* dists, uint32_t* counts, cudaStream_t s);
+// rerank_ij.cu (1-byte (i, j) pair codes, k1 <= 16, p_line in {16, 32, 64})
+bool rerank_ij_ok(const DevParams& p, uint32_t k);
+void configure_rerank_ij();
+void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
+                      float* dists, uint32_t* counts, cudaStream_t s);
 // binsel_fast.cu (no resort, 32-bit slot arithmetic)
 bool binsel_fast_ok(const DevParams& p);
 uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch);
 void configure_binsel_fast();
 void launch_binsel_fast(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats, cudaStream_t s);
-// rerank_lut.cu (thread per candidate, per-query float4 table; 1-byte pairs, k1 <= 16)
-size_t rerank_lut_smem(const DevParams& p, uint32_t k);
-bool rerank_lut_ok(const DevParams& p, uint32_t k);
-void configure_rerank_lut();
-void launch_rerank_lut(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
-                       float* dists, uint32_t* counts, cudaStream_t s);
-// 0 = pick the fastest kernel per stage, 1 = generic kernels only, 2 = prefer the skewed
-// re-rank, 3 = prefer the table re-rank (parity tests cover every variant)
+// 0 = pick the fastest kernel per stage, 1 = generic kernels only (parity tests run both)
 int kernel_variant();
 
 }  // namespace pqtg

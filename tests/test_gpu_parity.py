@@ -13,12 +13,12 @@ from paper_1702_05911_b200 import DeviceIndex, HostIndex, knn_query_batch, merge
 pytestmark = pytest.mark.gpu
 
 
-VARIANTS = {"auto": 0, "generic": 1, "skew": 2, "table": 3}
+VARIANTS = {"auto": 0, "generic": 1}
 
 
 @pytest.fixture(params=list(VARIANTS), autouse=True)
 def kernel_variant(request):
-    """Run every GPU parity test through each kernel variant (fast, generic, skewed, table)."""
+    """Run every GPU parity test through the fast kernels and through the generic ones."""
     from paper_1702_05911_b200._abi import lib
 
     lib().pqtg_set_kernel_variant(VARIANTS[request.param])
