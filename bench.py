@@ -108,7 +108,7 @@ class ClockSampler:
         0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, device: int, period: float = 0.02):
+    def __init__(self, device: int, period: float = 0.002):
         self.device, self.period = device, period
         self.samples, self.reasons = [], set()
         self._stop = threading.Event()

@@ -57,6 +57,67 @@ __host__ __device__ inline BsLayout bs_layout(uint32_t PW, uint32_t W2ab, uint32
 
 }  // namespace
 
+// One filter pass for one thread: NIT stream positions base + it·224 + ft. Slot = the sum of
+// pre-reduced per-part terms mod H (pqtree.cpp:12-25); non-empty = the slot's bitmap bit.
+// Loads of all items are issued before any is consumed; positions are 32-bit.
+template <int P, int NIT>
+__device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32_t total, int ft, int lane, int fw,
+                                       uint32_t ta, uint32_t tb, uint32_t W, uint32_t H, const uint32_t* terms,
+                                       const uint32_t* tA, const uint32_t* tB, uint32_t W2ab, uint32_t* slot,
+                                       uint32_t* ball, uint32_t* wcnt) {
+    const uint32_t W2 = (uint32_t)p.W2;
+    uint2 ent[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const uint32_t s = base + it * kFilterThreads + ft;
+        ent[it] = make_uint2(0, 0);
+        if (s < total) {
+            if constexpr (P == 2) {
+                ent[it].x = __ldg(p.pair_streams + (size_t)ta * W2 + s);
+            } else if constexpr (P == 4) {
+                if (s < (uint32_t)p.merge_count) {
+                    ent[it] = __ldg(p.merge + s);
+                } else {  // closed-form sweep rows past the slope-1 table (binorder.cpp:96-108)
+                    const uint32_t j = s - (uint32_t)p.merge_count;
+                    const uint32_t u = j / W2;
+                    ent[it] = make_uint2((uint32_t)p.merge_row0 + u, j - u * W2);
+                }
+            }
+        }
+    }
+    uint32_t word[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const uint32_t s = base + it * kFilterThreads + ft;
+        uint32_t sl = 0;
+        if constexpr (P == 1) {
+            sl = terms[s < total ? s : 0];
+        } else if constexpr (P == 2) {
+            const uint32_t e = ent[it].x;
+            sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
+        } else {
+            if (W2ab) {
+                sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
+            } else {
+                const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * W2 + ent[it].x);
+                const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * W2 + ent[it].y);
+                sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
+                             add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
+            }
+        }
+        slot[it] = sl;
+        word[it] = __ldg(p.bitmap + (sl >> 5));
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const uint32_t s = base + it * kFilterThreads + ft;
+        ball[it] = __ballot_sync(0xffffffffu, s < total && ((word[it] >> (slot[it] & 31)) & 1u));
+        if (lane == 0) wcnt[it * kFilterWarps + fw] = __popc(ball[it]);
+    }
+#pragma unroll
+    for (int it = NIT; it < kMaxItems; ++it) ball[it] = 0;
+}
+
 // HASH: two tuples can reach one slot ((k1·k2)^P > H); first occurrences are then tracked in
 // a per-query region of a global, epoch-tagged open-addressing table (entries
 // epoch << 26 | slot, H <= 2^26), which needs no clearing between searches.
@@ -114,8 +175,10 @@ __global__ void __launch_bounds__(kBsThreads, 4)
     // offsets) overlap the next pass's stream/bitmap loads.
     const int fw = warp - 1;                // filter warp index, -1 for warp 0
     const int ft = tid - 32;                // filter thread index
-    uint64_t base = 0;                      // first stream position of the pass being filtered
-    uint32_t nit = 1;
+    // stream positions fit 32 bits (BinStream::total is capped at 2^32 - 2 at index build)
+    const uint32_t total32 = (uint32_t)total;
+    uint32_t base = 0;                      // first stream position of the pass being filtered
+    uint32_t nit = 1;                       // items per filter thread: 1 on the first pass, then 8
     uint32_t prev_n = 0;                    // queued tuples of the previous pass
     for (uint32_t pass = 0;; ++pass) {
         const uint32_t buf = pass & 1u;
@@ -185,62 +248,9 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                 }
             }
         } else if (base < total) {
-            // ---- filter: slot + non-empty test for kFilterThreads·nit stream positions;
-            // three unrolled sweeps so each thread's loads are issued together
-            uint32_t word[kMaxItems];
-            uint2 ent[kMaxItems];
-#pragma unroll
-            for (int it = 0; it < kMaxItems; ++it) {
-                const uint64_t s = base + (uint64_t)it * kFilterThreads + ft;
-                ent[it] = make_uint2(0, 0);
-                if (it < (int)nit && s < total) {
-                    if constexpr (P == 2) {
-                        ent[it].x = __ldg(p.pair_streams + (size_t)ta * p.W2 + s);
-                    } else if constexpr (P == 4) {
-                        if (s < p.merge_count) {
-                            ent[it] = __ldg(p.merge + s);
-                        } else {
-                            const uint64_t j = s - p.merge_count;
-                            const uint64_t u = p.merge_row0 + j / p.W2;
-                            ent[it] = make_uint2((uint32_t)u, (uint32_t)(j - (u - p.merge_row0) * p.W2));
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int it = 0; it < kMaxItems; ++it) {
-                const uint64_t s = base + (uint64_t)it * kFilterThreads + ft;
-                slot[it] = 0;
-                word[it] = 0;
-                if (it < (int)nit && s < total) {
-                    uint32_t sl;
-                    if constexpr (P == 1) {
-                        sl = terms[s];
-                    } else if constexpr (P == 2) {
-                        const uint32_t e = ent[it].x;
-                        sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
-                    } else if (W2ab) {
-                        sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
-                    } else {
-                        const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + ent[it].x);
-                        const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * p.W2 + ent[it].y);
-                        sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
-                                     add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
-                    }
-                    slot[it] = sl;
-                    word[it] = __ldg(p.bitmap + (sl >> 5));
-                }
-            }
-#pragma unroll
-            for (int it = 0; it < kMaxItems; ++it) {
-                ball[it] = 0;
-                if (it < (int)nit) {
-                    const uint64_t s = base + (uint64_t)it * kFilterThreads + ft;
-                    const bool ne = s < total && ((word[it] >> (slot[it] & 31)) & 1u);
-                    ball[it] = __ballot_sync(0xffffffffu, ne);
-                    if (lane == 0) wcnt[buf][it * kFilterWarps + fw] = __popc(ball[it]);
-                }
-            }
+            // ---- filter: slot + non-empty test of this pass's stream positions
+            if (nit == 1) filter<P, 1>(p, base, total32, ft, lane, fw, ta, tb, W, H, terms, tA, tB, W2ab, slot, ball, wcnt[buf]);
+            else filter<P, kMaxItems>(p, base, total32, ft, lane, fw, ta, tb, W, H, terms, tA, tB, W2ab, slot, ball, wcnt[buf]);
         }
         __syncthreads();  // B1: counts of pass `pass`; C / R after the previous pass's queue
         // done: budget reached, or the stream ended and its last queue was just walked
@@ -274,7 +284,7 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                     const uint32_t excl = e < 32 ? a0 : carry + a1;
                     if ((ball[it] >> lane) & 1u) {
                         qb[excl + __popc(ball[it] & lt)] =
-                            make_uint2((uint32_t)(base + (uint64_t)it * kFilterThreads + ft), slot[it]);
+                            make_uint2(base + it * kFilterThreads + ft, slot[it]);
                     }
                 }
             }
@@ -282,14 +292,14 @@ __global__ void __launch_bounds__(kBsThreads, 4)
         }
         __syncthreads();  // B2: queue of pass `pass` complete
         prev_n = s_nq[buf];
-        base += (uint64_t)nit * kFilterThreads;
-        nit = nit * 2 < (uint32_t)kMaxItems ? nit * 2 : (uint32_t)kMaxItems;
+        base += nit * kFilterThreads;
+        nit = kMaxItems;
     }
     if (tid == 0) {
         const uint32_t C = s_C, R = s_R;
         nranges[q] = R;
         ncand[q] = C;
-        ntuples[q] = C >= budget && budget > 0 ? s_maxord + 1 : (uint32_t)min(base, total);
+        ntuples[q] = C >= budget && budget > 0 ? s_maxord + 1 : min(base, total32);
         if (stats) {
             stats[q].bins_visited = R;
             stats[q].candidates = C;
