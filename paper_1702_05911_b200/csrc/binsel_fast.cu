@@ -60,59 +60,98 @@ __host__ __device__ inline BsLayout bs_layout(uint32_t PW, uint32_t W2ab, uint32
 // One filter pass for one thread: NIT stream positions base + it·224 + ft. Slot = the sum of
 // pre-reduced per-part terms mod H (pqtree.cpp:12-25); non-empty = the slot's bitmap bit.
 // Loads of all items are issued before any is consumed; positions are 32-bit.
+__device__ __forceinline__ uint32_t add_mod_fast(uint32_t a, uint32_t b, uint32_t H) {
+    const uint32_t x = a + b;  // a, b < H < 2^31
+    return min(x, x - H);      // x - H wraps above x when x < H
+}
+
 template <int P, int NIT>
 __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32_t total, int ft, int lane, int fw,
                                        uint32_t ta, uint32_t tb, uint32_t W, uint32_t H, const uint32_t* terms,
                                        const uint32_t* tA, const uint32_t* tB, uint32_t W2ab, uint32_t* slot,
                                        uint32_t* ball, uint32_t* wcnt) {
     const uint32_t W2 = (uint32_t)p.W2;
-    uint2 ent[NIT];
+    const uint32_t mcount = (uint32_t)p.merge_count;
+    const uint32_t end = base + NIT * kFilterThreads;  // positions of this pass: [base, end)
+    // uniform fast path: the whole pass lies inside the stream and (P = 4) inside the
+    // materialized merge prefix, so no item needs a bounds or closed-form check
+    const bool fast = end <= total && (P != 4 || (end <= mcount && W2ab && H < 0x80000000u)) &&
+                      (P != 2 || H < 0x80000000u);
+    uint32_t word[NIT];
+    if (fast) {
+        if constexpr (P == 4) {
+            const uint2* mp = p.merge + base + ft;
+            uint2 e[NIT];
 #pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const uint32_t s = base + it * kFilterThreads + ft;
-        ent[it] = make_uint2(0, 0);
-        if (s < total) {
-            if constexpr (P == 2) {
-                ent[it].x = __ldg(p.pair_streams + (size_t)ta * W2 + s);
-            } else if constexpr (P == 4) {
-                if (s < (uint32_t)p.merge_count) {
-                    ent[it] = __ldg(p.merge + s);
-                } else {  // closed-form sweep rows past the slope-1 table (binorder.cpp:96-108)
-                    const uint32_t j = s - (uint32_t)p.merge_count;
-                    const uint32_t u = j / W2;
-                    ent[it] = make_uint2((uint32_t)p.merge_row0 + u, j - u * W2);
+            for (int it = 0; it < NIT; ++it) e[it] = __ldg(mp + it * kFilterThreads);
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) slot[it] = add_mod_fast(tA[e[it].x], tB[e[it].y], H);
+        } else if constexpr (P == 2) {
+            const uint32_t* sp = p.pair_streams + (size_t)ta * W2 + base + ft;
+            uint32_t e[NIT];
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) e[it] = __ldg(sp + it * kFilterThreads);
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) slot[it] = add_mod_fast(terms[e[it] & 0xFFFFu], terms[W + (e[it] >> 16)], H);
+        } else {
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) slot[it] = terms[base + it * kFilterThreads + ft];
+        }
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) word[it] = __ldg(p.bitmap + (slot[it] >> 5));
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            ball[it] = __ballot_sync(0xffffffffu, (word[it] >> (slot[it] & 31)) & 1u);
+            if (lane == 0) wcnt[it * kFilterWarps + fw] = __popc(ball[it]);
+        }
+    } else {
+        uint2 ent[NIT];
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const uint32_t s = base + it * kFilterThreads + ft;
+            ent[it] = make_uint2(0, 0);
+            if (s < total) {
+                if constexpr (P == 2) {
+                    ent[it].x = __ldg(p.pair_streams + (size_t)ta * W2 + s);
+                } else if constexpr (P == 4) {
+                    if (s < mcount) {
+                        ent[it] = __ldg(p.merge + s);
+                    } else {  // closed-form sweep rows past the slope-1 table (binorder.cpp:96-108)
+                        const uint32_t j = s - mcount;
+                        const uint32_t u = j / W2;
+                        ent[it] = make_uint2((uint32_t)p.merge_row0 + u, j - u * W2);
+                    }
                 }
             }
         }
-    }
-    uint32_t word[NIT];
 #pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const uint32_t s = base + it * kFilterThreads + ft;
-        uint32_t sl = 0;
-        if constexpr (P == 1) {
-            sl = terms[s < total ? s : 0];
-        } else if constexpr (P == 2) {
-            const uint32_t e = ent[it].x;
-            sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
-        } else {
-            if (W2ab) {
-                sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
+        for (int it = 0; it < NIT; ++it) {
+            const uint32_t s = base + it * kFilterThreads + ft;
+            uint32_t sl = 0;
+            if constexpr (P == 1) {
+                sl = terms[s < total ? s : 0];
+            } else if constexpr (P == 2) {
+                const uint32_t e = ent[it].x;
+                sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
             } else {
-                const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * W2 + ent[it].x);
-                const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * W2 + ent[it].y);
-                sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
-                             add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
+                if (W2ab) {
+                    sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
+                } else {
+                    const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * W2 + ent[it].x);
+                    const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * W2 + ent[it].y);
+                    sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
+                                 add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
+                }
             }
+            slot[it] = sl;
+            word[it] = __ldg(p.bitmap + (sl >> 5));
         }
-        slot[it] = sl;
-        word[it] = __ldg(p.bitmap + (sl >> 5));
-    }
 #pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const uint32_t s = base + it * kFilterThreads + ft;
-        ball[it] = __ballot_sync(0xffffffffu, s < total && ((word[it] >> (slot[it] & 31)) & 1u));
-        if (lane == 0) wcnt[it * kFilterWarps + fw] = __popc(ball[it]);
+        for (int it = 0; it < NIT; ++it) {
+            const uint32_t s = base + it * kFilterThreads + ft;
+            ball[it] = __ballot_sync(0xffffffffu, s < total && ((word[it] >> (slot[it] & 31)) & 1u));
+            if (lane == 0) wcnt[it * kFilterWarps + fw] = __popc(ball[it]);
+        }
     }
 #pragma unroll
     for (int it = NIT; it < kMaxItems; ++it) ball[it] = 0;

@@ -27,13 +27,15 @@ using namespace dev;
 // K1 — traversal: exact fine-part LUT, level-1 sort, level-2 distances of the w best
 // parents, level-2 sort, slope pick. One CTA per query.
 // =====================================================================================
+template <int K1T, int K2T>  // compile-time k1 / k2 (0 = runtime): strided loads become immediates
 __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const float* __restrict__ Q,
                                                             float* __restrict__ fine_out,
                                                             float* __restrict__ l2d_out,
                                                             uint32_t* __restrict__ l2c_out,
                                                             uint8_t* __restrict__ slope_out) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t D = p.D, L = p.L, k1 = p.k1, P = p.P, W = p.W, k2 = p.k2, m = p.m, fd = p.fd;
+    const uint32_t D = p.D, L = p.L, P = p.P, W = p.W, m = p.m, fd = p.fd;
+    const uint32_t k1 = K1T ? (uint32_t)K1T : p.k1, k2 = K2T ? (uint32_t)K2T : p.k2;
     float* y = reinterpret_cast<float*>(smem);
     float* fine = y + D;
     float* l1d = fine + L * k1;
@@ -53,8 +55,12 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
         const float* c = p.fine_t + (size_t)f * fd * k1 + i;
         const float* yf = y + f * fd;
         float acc = 0.0f;
-#pragma unroll 8
-        for (uint32_t t = 0; t < fd; ++t) acc = sq_step(acc, yf[t], c[(size_t)t * k1]);
+        uint32_t t = 0;
+        for (; t + 8 <= fd; t += 8, c += 8 * k1) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = sq_step(acc, yf[t + u], __ldg(c + u * k1));
+        }
+        for (; t < fd; ++t, c += k1) acc = sq_step(acc, yf[t], __ldg(c));
         fine[idx] = acc;
         fine_out[q * L * k1 + idx] = acc;
     }
@@ -90,8 +96,15 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
         const float* yp = y + pp * m;
         const float* cb = p.l2_t + ((size_t)(pp * k1 + parent) * m) * k2 + c;
         float acc = 0.0f;
-#pragma unroll 16
-        for (uint32_t t = 0; t < m; ++t) acc = sq_step(acc, yp[t], __ldg(cb + (size_t)t * k2));
+        uint32_t t = 0;
+        for (; t + 16 <= m; t += 16, cb += 16 * k2) {
+            float cv[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) cv[u] = __ldg(cb + u * k2);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) acc = sq_step(acc, yp[t + u], cv[u]);
+        }
+        for (; t < m; ++t, cb += k2) acc = sq_step(acc, yp[t], __ldg(cb));
         l2d[idx] = acc;
         l2c[idx] = (parent << 16) | c;
     }
@@ -134,8 +147,14 @@ void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, Work
     // sequential m-loop; 64..256 threads
     const uint32_t jobs = p.P * p.w * p.k2;
     const unsigned bs = jobs >= 256 ? 256u : (jobs <= 64 ? 64u : (unsigned)((jobs + 31) / 32 * 32));
-    traverse_kernel<<<(unsigned)nq, bs, traverse_smem(p), s>>>(p, queries, ws.fine, ws.l2_dist,
-                                                                     ws.l2_code, ws.slope);
+#define PQTG_TRAV(A, B)                                                                       \
+    traverse_kernel<A, B><<<(unsigned)nq, bs, traverse_smem(p), s>>>(p, queries, ws.fine, ws.l2_dist, \
+                                                                     ws.l2_code, ws.slope)
+    if (p.k1 == 16 && p.k2 == 8) PQTG_TRAV(16, 8);
+    else if (p.k1 == 32 && p.k2 == 16) PQTG_TRAV(32, 16);
+    else if (p.k1 == 16 && p.k2 == 16) PQTG_TRAV(16, 16);
+    else PQTG_TRAV(0, 0);
+#undef PQTG_TRAV
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -646,7 +665,10 @@ void configure_kernels(const DevParams& p, uint32_t) {
     int dev = 0;
     PQTG_CUDA_CHECK(cudaGetDevice(&dev));
     std::call_once(once[dev & 63], [] {
-        allow_max_smem(traverse_kernel);
+        allow_max_smem(traverse_kernel<16, 8>);
+        allow_max_smem(traverse_kernel<32, 16>);
+        allow_max_smem(traverse_kernel<16, 16>);
+        allow_max_smem(traverse_kernel<0, 0>);
         allow_max_smem(binsel_kernel<4, false>);
         allow_max_smem(binsel_kernel<16, true>);
         set_rerank_attr<16, 1>();

@@ -4,12 +4,15 @@
 //
 // One thread per candidate; the code row (L × (λ, ij) bytes, slot order) is read with 16-byte
 // loads into registers and its parts are summed in the reference's order. Per part:
-//     b2 = fine[f][i], a2 = fine[f][j]      a 16-float row per part: the 32 lanes of a warp
-//                                           touch at most 16 addresses, all in distinct banks
-//                                           (duplicates broadcast) — conflict-free;
-//     c2 = c2ij[f][i << 4 | j]              query-independent, the one random lookup;
-//     part = (b2 + (λ·λ)·c2) + λ·((a2 − b2) − c2)   exactly linequant.hpp:83-85's rounding.
-// Shared memory: c2ij (L × 1 KB), fine (L × 64 B), candidate keys, range offsets.
+//     b2 = fine[f][i]                   a 16-float row per part: the 32 lanes of a warp touch
+//                                       at most 16 addresses, all in distinct banks
+//                                       (duplicates broadcast) — conflict-free;
+//     (E, c2) = T[f][i << 4 | j]        per-query table, E = (a2 − b2) − c2 with a2 = fine[f][j]
+//                                       and c2 = d2[f][i][j]: the reference's own intermediate
+//                                       (linequant.hpp:85), built once per query;
+//     part = (b2 + (λ·λ)·c2) + λ·E      exactly linequant.hpp:83-85's rounding.
+// Shared memory: T (L × 2 KB), fine (L × 64 B), candidate keys, range offsets (cached up to
+// kRangeCache, else read from global memory); 512 threads per CTA, two CTAs per SM.
 #include <cstdint>
 
 #include "common.cuh"
@@ -22,10 +25,11 @@ using namespace dev;
 
 namespace {
 
-constexpr int kIjThreads = 256;
+constexpr int kIjThreads = 512;
+constexpr uint32_t kRangeCache = 1024;
 
 struct IjLayout {
-    size_t c2, fine, keys, sel, coff, total;
+    size_t t, fine, keys, sel, coff, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -33,8 +37,8 @@ __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15)
 __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint32_t sel_cap) {
     IjLayout l{};
     size_t o = 0;
-    l.c2 = o;  // offset 0: compile-time part offsets become load immediates
-    o += (size_t)L * 256 * 4;
+    l.t = o;  // offset 0: compile-time part offsets become load immediates
+    o += (size_t)L * 256 * 8;
     l.fine = o;
     o += (size_t)L * 16 * 4;
     l.keys = o;
@@ -42,7 +46,7 @@ __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint3
     l.sel = o;
     o += al16((size_t)sel_cap * 8);
     l.coff = o;
-    o += al16((size_t)budget * 4);
+    o += al16((size_t)(budget < kRangeCache ? budget : kRangeCache) * 4);
     l.total = o;
     return l;
 }
@@ -58,7 +62,7 @@ __global__ void __launch_bounds__(kIjThreads)
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k1 = p.k1, budget = p.budget;
     const IjLayout lay = ij_layout(LT, budget, sel_cap);
-    const float* c2 = reinterpret_cast<const float*>(smem);
+    float2* T = reinterpret_cast<float2*>(smem);
     float* fine = reinterpret_cast<float*>(smem + lay.fine);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + lay.keys);
     uint64_t* sel = reinterpret_cast<uint64_t*>(smem + lay.sel);
@@ -72,17 +76,24 @@ __global__ void __launch_bounds__(kIjThreads)
     const uint32_t R = nranges[q], C = ncand[q];
     const uint2* qr = ranges + q * (uint64_t)budget;
 
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(p.c2ij);
-        uint4* dst = reinterpret_cast<uint4*>(smem);
-        for (uint32_t i = tid; i < LT * 64; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
     for (uint32_t i = tid; i < LT * 16; i += blockDim.x) {
         const uint32_t f = i >> 4, c = i & 15;
         fine[i] = c < k1 ? fine_in[q * LT * k1 + f * k1 + c] : 0.0f;
     }
-    for (uint32_t r = tid; r < R; r += blockDim.x) coff[r] = qr[r].y;
+    const bool cached = R <= kRangeCache;
+    if (cached)
+        for (uint32_t r = tid; r < R; r += blockDim.x) coff[r] = qr[r].y;
     if (tid == 0) s_count = 0;
+    __syncthreads();
+    // T[f][i << 4 | j] = (E, c2) for every pair; entries with i >= j are never referenced
+    for (uint32_t idx = tid; idx < LT * 256; idx += blockDim.x) {
+        const uint32_t f = idx >> 8, i = (idx >> 4) & 15u, j = idx & 15u;
+        if (i < k1 && j < k1) {
+            const float c2 = __ldg(p.c2ij + idx);
+            const float b2 = fine[f * 16 + i], a2 = fine[f * 16 + j];
+            T[idx] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2), c2);
+        }
+    }
     __syncthreads();
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
@@ -93,9 +104,11 @@ __global__ void __launch_bounds__(kIjThreads)
         uint32_t lo = 0, hi = R - 1;  // range holding candidate j
         while (lo < hi) {
             const uint32_t mid = (lo + hi + 1) >> 1;
-            if (coff[mid] <= j) lo = mid; else hi = mid - 1;
+            const uint32_t cm = cached ? coff[mid] : __ldg(&qr[mid].y);
+            if (cm <= j) lo = mid; else hi = mid - 1;
         }
-        const uint64_t pos = (uint64_t)__ldg(&qr[lo].x) + (j - coff[lo]);
+        const uint2 rl = __ldg(qr + lo);
+        const uint64_t pos = (uint64_t)rl.x + (j - rl.y);
         uint64_t key = kSentinel;
         if (!sharded || (pos >= p.shard_lo && pos < p.shard_hi)) {
             const uint64_t lp = pos - p.shard_lo;
@@ -111,11 +124,9 @@ __global__ void __launch_bounds__(kIjThreads)
                 const uint32_t half = w[f >> 1] >> ((f & 1) * 16);  // λ | (i << 4 | j) << 8
                 const uint32_t ij = (half >> 8) & 0xFFu;
                 const float b2 = fine[f * 16 + (ij >> 4)];
-                const float a2 = fine[f * 16 + (ij & 15u)];
-                const float cc = c2[f * 256 + ij];
+                const float2 ec = T[f * 256 + ij];
                 const float lam = __fmul_rn(__uint2float_rn(half & 0xFFu), inv255);
-                const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
-                                             __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
+                const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), ec.y)), __fmul_rn(lam, ec.x));
                 total = __fadd_rn(total, part);
             }
             key = ((uint64_t)orderable(total) << 32) | id;
