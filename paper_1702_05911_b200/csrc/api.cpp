@@ -33,8 +33,26 @@ Workspace::~Workspace() {
     if (index) cudaSetDevice(index->device);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
+    if (join) cudaEventDestroy(join);
     if (own_stream) cudaStreamDestroy(own_stream);
+    if (aux_stream) cudaStreamDestroy(aux_stream);
     for (void* p : allocations) cudaFree(p);
+}
+
+WsSlice Workspace::slice(uint64_t q0) const {
+    const DevParams& p = index->prm;
+    WsSlice s;
+    s.fine = fine + q0 * p.L * p.k1;
+    s.l2_dist = l2_dist + q0 * p.P * p.W;
+    s.l2_code = l2_code + q0 * p.P * p.W;
+    s.slope = slope + q0 * 2;
+    s.ranges = ranges + q0 * std::max<uint64_t>(p.budget, 1);
+    s.nranges = nranges + q0;
+    s.ncand = ncand + q0;
+    s.ntuples = ntuples + q0;
+    s.hash = hash ? hash + q0 * hash_stride : nullptr;
+    s.epoch = hash_epoch;
+    return s;
 }
 
 namespace {
@@ -70,33 +88,45 @@ void ensure_staging(Workspace& ws, uint64_t k) {
     }
 }
 
-void run_search(const DevIndex& ix, Workspace& ws, const float* d_queries, uint64_t nq, uint32_t k,
-                uint32_t* d_ids, float* d_dists, uint32_t* d_counts, pqtg_query_stats* d_stats,
-                cudaStream_t s) {
+// A fresh epoch for the workspace's visited-slot table before its regions are reused. On wrap
+// the table is cleared; `streams` are drained first so no in-flight chunk still uses it.
+void next_epoch(Workspace& ws, cudaStream_t s, cudaStream_t other) {
+    if (!ws.hash) return;
+    if (ws.hash_epoch == 0 || ws.hash_epoch >= 63) {
+        if (other) PQTG_CUDA_CHECK(cudaStreamSynchronize(other));
+        PQTG_CUDA_CHECK(cudaMemsetAsync(ws.hash, 0, ws.hash_words * sizeof(uint32_t), s));
+        ws.hash_epoch = 0;
+    }
+    ++ws.hash_epoch;  // 1..63; 0 marks cleared entries
+}
+
+// The three stages for queries [q0, q0 + nq) of the current sub-batch on stream s. Events
+// ev[0..3] bracket the stages when `timed` (the first chunk of a call).
+void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_queries, uint64_t nq, uint32_t k,
+               uint32_t* d_ids, float* d_dists, uint32_t* d_counts, pqtg_query_stats* d_stats, cudaStream_t s,
+               bool timed) {
     const DevParams& p = ix.prm;
-    ws.last_stream = s;
-    ws.last_nq = nq;
-    PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[0], s));
-    if (nq == 0) {
-        for (int i = 1; i < 4; ++i) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[i], s));
-        return;
-    }
-    if (k == 0 || ix.n == 0) {  // search.cpp:130-132: empty results, zero stats
-        PQTG_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, nq * sizeof(uint32_t), s));
-        if (d_stats) PQTG_CUDA_CHECK(cudaMemsetAsync(d_stats, 0, nq * sizeof(pqtg_query_stats), s));
-        if (k && ix.n == 0) {
-            PQTG_CUDA_CHECK(cudaMemsetAsync(d_ids, 0xFF, nq * k * sizeof(uint32_t), s));
-            PQTG_CUDA_CHECK(cudaMemsetAsync(d_dists, 0x7F, nq * k * sizeof(float), s));
+    if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[0], s));
+    if (nq == 0 || k == 0 || ix.n == 0) {  // search.cpp:130-132: empty results, zero stats
+        if (nq) {
+            PQTG_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, nq * sizeof(uint32_t), s));
+            if (d_stats) PQTG_CUDA_CHECK(cudaMemsetAsync(d_stats, 0, nq * sizeof(pqtg_query_stats), s));
+            if (k && ix.n == 0) {
+                PQTG_CUDA_CHECK(cudaMemsetAsync(d_ids, 0xFF, nq * k * sizeof(uint32_t), s));
+                PQTG_CUDA_CHECK(cudaMemsetAsync(d_dists, 0x7F, nq * k * sizeof(float), s));
+            }
         }
-        for (int i = 1; i < 4; ++i) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[i], s));
+        if (timed)
+            for (int i = 1; i < 4; ++i) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[i], s));
         return;
     }
-    launch_traverse(p, d_queries, nq, ws, s);
-    PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[1], s));
-    launch_binsel(p, nq, ws, d_stats, s);
-    PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[2], s));
-    launch_rerank(p, nq, k, ws, d_ids, d_dists, d_counts, s);
-    PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[3], s));
+    const WsSlice sl = ws.slice(q0);
+    launch_traverse(p, d_queries, nq, sl, s);
+    if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[1], s));
+    launch_binsel(p, nq, sl, d_stats, s);
+    if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[2], s));
+    launch_rerank(p, nq, k, sl, d_ids, d_dists, d_counts, s);
+    if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[3], s));
 }
 
 }  // namespace
@@ -213,6 +243,8 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         ws->index = &d;
         ws->max_batch = max_batch;
         PQTG_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->own_stream, cudaStreamNonBlocking));
+        PQTG_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->aux_stream, cudaStreamNonBlocking));
+        PQTG_CUDA_CHECK(cudaEventCreateWithFlags(&ws->join, cudaEventDisableTiming));
         for (auto& e : ws->ev) PQTG_CUDA_CHECK(cudaEventCreate(&e));
         const uint64_t B = max_batch;
         ws->fine = dev_alloc<float>(ws->allocations, B * p.L * p.k1);
@@ -224,6 +256,7 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         ws->ncand = dev_alloc<uint32_t>(ws->allocations, B);
         ws->ntuples = dev_alloc<uint32_t>(ws->allocations, B);
         ws->hash_words = binsel_fast_ok(p) ? binsel_hash_words(p, B) : 0;
+        ws->hash_stride = ws->hash_words ? binsel_hash_stride(p) : 0;
         if (ws->hash_words) ws->hash = dev_alloc<uint32_t>(ws->allocations, ws->hash_words);
         auto* h = new pqtg_workspace;
         h->ws = std::move(ws);
@@ -292,8 +325,11 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         if (ws.index != index->dev.get()) throw Error{PQTG_ERR_ARG, "workspace belongs to another index"};
         if (nq > ws.max_batch) throw Error{PQTG_ERR_ARG, "nq exceeds the workspace max_batch"};
         PQTG_CUDA_CHECK(cudaSetDevice(index->dev->device));
-        run_search(*index->dev, ws, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats,
-                   static_cast<cudaStream_t>(stream));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        next_epoch(ws, s, nullptr);
+        ws.last_stream = s;
+        ws.last_nq = nq;
+        run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, s, true);
         return PQTG_OK;
     });
 }
@@ -311,29 +347,49 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         std::lock_guard<std::mutex> lock(ws.mu);
         PQTG_CUDA_CHECK(cudaSetDevice(d.device));
         ensure_staging(ws, std::max<uint32_t>(k, 1));
-        cudaStream_t s = ws.own_stream;
         const uint64_t D = d.prm.D;
+        cudaStream_t st[2] = {ws.own_stream, ws.aux_stream};
+        ws.last_stream = ws.own_stream;
+        // Sub-batches of <= max_batch queries; each is cut into chunks that alternate between
+        // two streams, so chunk c's kernels overlap chunk c+1's H2D and chunk c-1's D2H.
         for (uint64_t q0 = 0; q0 < nq || (nq == 0 && q0 == 0); q0 += ws.max_batch) {
             const uint64_t b = std::min(ws.max_batch, nq - q0);
             if (b == 0) {
-                run_search(d, ws, ws.d_queries, 0, k, ws.d_ids, ws.d_dists, ws.d_counts, ws.d_stats, s);
+                run_chunk(d, ws, 0, ws.d_queries, 0, k, ws.d_ids, ws.d_dists, ws.d_counts, ws.d_stats, st[0], true);
+                ws.last_nq = 0;
                 break;
             }
-            PQTG_CUDA_CHECK(cudaMemcpyAsync(ws.d_queries, queries + q0 * D, b * D * sizeof(float),
-                                            cudaMemcpyHostToDevice, s));
-            run_search(d, ws, ws.d_queries, b, k, ws.d_ids, ws.d_dists, ws.d_counts, ws.d_stats, s);
-            if (k) {
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(ids + q0 * k, ws.d_ids, b * k * sizeof(uint32_t),
+            // reusing the slices: the other stream's chunks of the previous sub-batch must be done
+            PQTG_CUDA_CHECK(cudaEventRecord(ws.join, st[1]));
+            PQTG_CUDA_CHECK(cudaStreamWaitEvent(st[0], ws.join, 0));
+            next_epoch(ws, st[0], st[1]);
+            const uint64_t nch = b >= 1024 ? 4 : (b >= 256 ? 2 : 1);
+            const uint64_t per = (b + nch - 1) / nch;
+            for (uint64_t c = 0; c * per < b; ++c) {
+                const uint64_t c0 = c * per, cn = std::min(per, b - c0);
+                cudaStream_t s = st[c & 1];
+                if (c == 1) PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));  // after the epoch bump
+                if (c == 0) PQTG_CUDA_CHECK(cudaEventRecord(ws.join, s));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(ws.d_queries + c0 * D, queries + (q0 + c0) * D, cn * D * sizeof(float),
+                                                cudaMemcpyHostToDevice, s));
+                run_chunk(d, ws, c0, ws.d_queries + c0 * D, cn, k, ws.d_ids + c0 * std::max<uint32_t>(k, 1),
+                          ws.d_dists + c0 * std::max<uint32_t>(k, 1), ws.d_counts + c0, ws.d_stats + c0, s, c == 0);
+                if (k) {
+                    PQTG_CUDA_CHECK(cudaMemcpyAsync(ids + (q0 + c0) * k, ws.d_ids + c0 * k, cn * k * sizeof(uint32_t),
+                                                    cudaMemcpyDeviceToHost, s));
+                    PQTG_CUDA_CHECK(cudaMemcpyAsync(dists + (q0 + c0) * k, ws.d_dists + c0 * k, cn * k * sizeof(float),
+                                                    cudaMemcpyDeviceToHost, s));
+                }
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(counts + q0 + c0, ws.d_counts + c0, cn * sizeof(uint32_t),
                                                 cudaMemcpyDeviceToHost, s));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(dists + q0 * k, ws.d_dists, b * k * sizeof(float),
-                                                cudaMemcpyDeviceToHost, s));
+                if (stats)
+                    PQTG_CUDA_CHECK(cudaMemcpyAsync(stats + q0 + c0, ws.d_stats + c0, cn * sizeof(pqtg_query_stats),
+                                                    cudaMemcpyDeviceToHost, s));
             }
-            PQTG_CUDA_CHECK(cudaMemcpyAsync(counts + q0, ws.d_counts, b * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            if (stats)
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(stats + q0, ws.d_stats, b * sizeof(pqtg_query_stats),
-                                                cudaMemcpyDeviceToHost, s));
-            PQTG_CUDA_CHECK(cudaStreamSynchronize(s));
+            ws.last_nq = b;
         }
+        PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
+        PQTG_CUDA_CHECK(cudaStreamSynchronize(st[1]));
         return PQTG_OK;
     });
 }

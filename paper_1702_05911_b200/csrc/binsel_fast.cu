@@ -394,6 +394,11 @@ uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch) {
     return c.use_hash ? (max_batch << c.ts_log2) : 0;
 }
 
+uint64_t binsel_hash_stride(const DevParams& p) {
+    const BsConfig c = bs_config(p);
+    return c.use_hash ? (1ull << c.ts_log2) : 0;
+}
+
 void configure_binsel_fast() {
     configure_one<1, false>();
     configure_one<2, false>();
@@ -402,17 +407,9 @@ void configure_binsel_fast() {
     configure_one<4, true>();
 }
 
-void launch_binsel_fast(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats, cudaStream_t s) {
+void launch_binsel_fast(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats, cudaStream_t s) {
     const BsConfig c = bs_config(p);
-    uint32_t epoch = 0;
-    if (c.use_hash) {
-        // 6-bit epochs tag the entries of the global visited-slot table; clear it on wrap
-        if (ws.hash_epoch == 0 || ws.hash_epoch >= 63) {
-            PQTG_CUDA_CHECK(cudaMemsetAsync(ws.hash, 0, ws.hash_words * sizeof(uint32_t), s));
-            ws.hash_epoch = 0;
-        }
-        epoch = ++ws.hash_epoch;  // 1..63; 0 marks cleared entries
-    }
+    const uint32_t epoch = ws.epoch;  // bumped per search by the caller (api.cpp)
 #define PQTG_BS(PP, HH)                                                                                       \
     binsel_fast_kernel<PP, HH><<<(unsigned)nq, kBsThreads, c.smem, s>>>(p, ws.l2_code, ws.slope, ws.ranges,     \
                                                                        ws.nranges, ws.ncand, ws.ntuples, stats, \

@@ -141,7 +141,7 @@ size_t traverse_smem(const DevParams& p) {
     return sizeof(float) * ((size_t)p.D + (size_t)p.L * p.k1 + 2ull * p.P * p.k1 + 3ull * p.P * p.W);
 }
 
-void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, Workspace& ws,
+void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                      cudaStream_t s) {
     // one thread per level-2 distance (P·w·k2 of them) keeps every thread busy in the long
     // sequential m-loop; 64..256 threads
@@ -433,7 +433,7 @@ size_t binsel_smem(const DevParams& p) {
     return (size_t)p.P * p.W * (8 + 4) + TS * 8 + 32 * 8;
 }
 
-void launch_binsel(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats,
+void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats,
                    cudaStream_t s) {
     if (kernel_variant() != 1 && binsel_fast_ok(p)) {
         launch_binsel_fast(p, nq, ws, stats, s);
@@ -630,7 +630,7 @@ size_t rerank_smem(const DevParams& p, uint32_t k) {
            4ull * p.L * (p.code_ij ? 256u : p.npairs) + 4ull * p.npairs + 4ull * p.budget;
 }
 
-void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
+void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids,
                    float* dists, uint32_t* counts, cudaStream_t s) {
     if (kernel_variant() == 0 && rerank_ij_ok(p, k)) {
         launch_rerank_ij(p, nq, k, ws, ids, dists, counts, s);

@@ -79,6 +79,20 @@ struct DevIndex {
     ~DevIndex();
 };
 
+// Per-query intermediate buffers of one contiguous group of queries (a workspace slice).
+struct WsSlice {
+    float* fine = nullptr;        // [q][L][k1]
+    float* l2_dist = nullptr;     // [q][P][W]
+    uint32_t* l2_code = nullptr;  // [q][P][W]
+    uint8_t* slope = nullptr;     // [q][2]
+    uint2* ranges = nullptr;      // [q][budget]
+    uint32_t* nranges = nullptr;
+    uint32_t* ncand = nullptr;
+    uint32_t* ntuples = nullptr;
+    uint32_t* hash = nullptr;     // [q][hash_stride] visited-slot table (binsel_fast.cu)
+    uint32_t epoch = 0;
+};
+
 struct Workspace {
     const DevIndex* index = nullptr;
     uint64_t max_batch = 0;
@@ -97,7 +111,11 @@ struct Workspace {
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
     uint32_t* hash = nullptr;     // [B << ts_log2] epoch-tagged visited slots (binsel_fast.cu)
     uint64_t hash_words = 0;
+    uint64_t hash_stride = 0;     // words per query
     uint32_t hash_epoch = 0;
+    cudaStream_t aux_stream = nullptr;  // second stream of the pipelined host search
+    cudaEvent_t join = nullptr;
+    WsSlice slice(uint64_t q0) const;
     // host-call staging (grown on demand)
     float* d_queries = nullptr;
     uint32_t* d_ids = nullptr;
@@ -180,11 +198,11 @@ void validate_config(const pqtg_config& c);
 size_t traverse_smem(const DevParams& p);
 size_t binsel_smem(const DevParams& p);
 size_t rerank_smem(const DevParams& p, uint32_t k);
-void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, Workspace& ws,
+void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                      cudaStream_t s);
-void launch_binsel(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats,
+void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats,
                    cudaStream_t s);
-void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
+void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids,
                    float* dists, uint32_t* counts, cudaStream_t s);
 void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids,
                   const float* dists, const uint32_t* counts, uint32_t* out_ids,
@@ -193,13 +211,14 @@ void configure_kernels(const DevParams& p, uint32_t k);
 // rerank_ij.cu (1-byte (i, j) pair codes, k1 <= 16, p_line in {16, 32, 64})
 bool rerank_ij_ok(const DevParams& p, uint32_t k);
 void configure_rerank_ij();
-void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids,
+void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids,
                       float* dists, uint32_t* counts, cudaStream_t s);
 // binsel_fast.cu (no resort, 32-bit slot arithmetic)
 bool binsel_fast_ok(const DevParams& p);
 uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch);
+uint64_t binsel_hash_stride(const DevParams& p);
 void configure_binsel_fast();
-void launch_binsel_fast(const DevParams& p, uint64_t nq, Workspace& ws, pqtg_query_stats* stats, cudaStream_t s);
+void launch_binsel_fast(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats, cudaStream_t s);
 // 0 = pick the fastest kernel per stage, 1 = generic kernels only (parity tests run both)
 int kernel_variant();
 

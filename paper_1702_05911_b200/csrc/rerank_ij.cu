@@ -26,6 +26,7 @@ using namespace dev;
 namespace {
 
 constexpr int kIjThreads = 512;
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // no id: the candidate belongs to another shard
 constexpr uint32_t kRangeCache = 1024;
 
 struct IjLayout {
@@ -54,7 +55,7 @@ __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint3
 }  // namespace
 
 template <int LT>
-__global__ void __launch_bounds__(kIjThreads)
+__global__ void __launch_bounds__(kIjThreads, 2)
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
@@ -100,7 +101,8 @@ __global__ void __launch_bounds__(kIjThreads)
     const bool sharded = p.shard_hi > p.shard_lo;
     constexpr int kVec = (2 * LT + 15) / 16;
     uint32_t mine = 0;
-    for (uint32_t j = tid; j < C; j += blockDim.x) {
+    // candidate j's code row and id, fetched one iteration ahead (software pipelining)
+    auto fetch = [&](uint32_t j, uint4* v, uint32_t& id) {
         uint32_t lo = 0, hi = R - 1;  // range holding candidate j
         while (lo < hi) {
             const uint32_t mid = (lo + hi + 1) >> 1;
@@ -109,14 +111,26 @@ __global__ void __launch_bounds__(kIjThreads)
         }
         const uint2 rl = __ldg(qr + lo);
         const uint64_t pos = (uint64_t)rl.x + (j - rl.y);
-        uint64_t key = kSentinel;
+        id = kInvalid;
         if (!sharded || (pos >= p.shard_lo && pos < p.shard_hi)) {
             const uint64_t lp = pos - p.shard_lo;
-            const uint32_t id = __ldg(p.ids + lp);
-            uint4 v[kVec];
+            id = __ldg(p.ids + lp);
             const uint4* r4 = reinterpret_cast<const uint4*>(p.codes + lp * p.row_bytes);
 #pragma unroll
             for (int i = 0; i < kVec; ++i) v[i] = __ldg(r4 + i);
+        }
+    };
+    uint4 vn[kVec];
+    uint32_t idn = kInvalid;
+    if (tid < C) fetch(tid, vn, idn);
+    for (uint32_t j = tid; j < C; j += blockDim.x) {
+        uint4 v[kVec];
+#pragma unroll
+        for (int i = 0; i < kVec; ++i) v[i] = vn[i];
+        const uint32_t id = idn;
+        if (j + blockDim.x < C) fetch(j + blockDim.x, vn, idn);
+        uint64_t key = kSentinel;
+        if (id != kInvalid) {
             const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
             float total = 0.0f;
 #pragma unroll
@@ -181,7 +195,7 @@ void configure_rerank_ij() {
     allow<64>(optin);
 }
 
-void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, Workspace& ws, uint32_t* ids, float* dists,
+void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids, float* dists,
                       uint32_t* counts, cudaStream_t s) {
     const uint32_t kk = k < p.budget ? k : p.budget;
     const uint32_t cap = np2(kk > 0 ? kk : 1);

@@ -12,6 +12,7 @@ namespace dev {
 
 struct TopkShared {
     uint32_t nsel, digit, before, bucket;
+    unsigned long long kand, kor;
 };
 
 // All threads of the block call this; keys[0..C) in smem; result: sel[0..kk) ascending.
@@ -19,11 +20,40 @@ __device__ inline void block_topk(const uint64_t* keys, uint32_t C, uint32_t kk,
                                   uint32_t sel_cap, uint32_t* hist, TopkShared& sh) {
     const int tid = threadIdx.x;
     if (kk == 0) return;
-    if (tid == 0) sh.nsel = 0;
-    uint64_t prefix = 0, mask = 0;
+    if (tid == 0) {
+        sh.nsel = 0;
+        sh.kand = ~0ull;
+        sh.kor = 0ull;
+    }
+    __syncthreads();
+    // bits shared by every key need no radix pass: start below the highest differing bit
+    {
+        uint64_t a = ~0ull, o = 0ull;
+        for (uint32_t j = tid; j < C; j += blockDim.x) {
+            const uint64_t key = keys[j];
+            if (key != kSentinel) {
+                a &= key;
+                o |= key;
+            }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            a &= __shfl_xor_sync(0xffffffffu, a, d);
+            o |= __shfl_xor_sync(0xffffffffu, o, d);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAnd(&sh.kand, (unsigned long long)a);
+            atomicOr(&sh.kor, (unsigned long long)o);
+        }
+    }
+    __syncthreads();
+    const uint64_t diff = sh.kand ^ sh.kor;
+    const int hb = diff ? 63 - __clzll((long long)diff) : 0;  // highest differing bit
+    uint64_t mask = hb >= 63 ? 0ull : (~0ull << (hb + 1));
+    uint64_t prefix = sh.kand & mask;
     uint32_t need = kk;
-    int shift = 56;
-    for (;; shift -= 8) {
+    int shift = hb >= 7 ? hb - 7 : 0;
+    for (;;) {
         for (uint32_t i = tid; i < 256; i += blockDim.x) hist[i] = 0;
         __syncthreads();
         for (uint32_t j = tid; j < C; j += blockDim.x) {
@@ -63,6 +93,9 @@ __device__ inline void block_topk(const uint64_t* keys, uint32_t C, uint32_t kk,
         const bool done = sh.bucket == need || shift == 0;
         __syncthreads();
         if (done) break;
+        // next 8-bit window; the last one may overlap bits already fixed in the prefix,
+        // which only narrows its histogram
+        shift = shift >= 8 ? shift - 8 : 0;
     }
     const uint64_t top = prefix >> shift;
     for (uint32_t j = tid; j < C; j += blockDim.x) {
