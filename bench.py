@@ -184,6 +184,12 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def gpu_launches(hix, nq: int, chunks: int) -> int:
+    """Kernels launched per step: traverse, bin selection, re-rank per chunk (api.cpp)."""
+    n = chunks if chunks else (4 if nq >= 2048 else (2 if nq >= 256 else 1))
+    return 3 * (n if nq >= n else 1)
+
+
 # --------------------------------------------------------------------------- recall
 def counters_ids(dev, dq, nq, k, step, d_ids, d_counts):
     import torch
@@ -307,6 +313,8 @@ def main():
     ap.add_argument("--variant", type=int, default=0,
                     help="kernel variant: 0 auto, 1 generic, 2 skewed re-rank, 3 table re-rank")
     ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="pieces per batch overlapped on two streams (0 auto, 1 off)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -338,6 +346,7 @@ def main():
             hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * world)
     lib().pqtg_set_kernel_variant(args.variant)
     dev = DeviceIndex(hix, device=local, max_batch=nq)
+    dev.set_chunks(args.chunks)
     batches = [Qpool[(rank * args.batches + b) * nq:(rank * args.batches + b + 1) * nq] for b in range(args.batches)]
     d_q = [torch.from_numpy(b).cuda() for b in batches]
     d_ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
@@ -365,7 +374,6 @@ def main():
 
     # ---- timed: device-resident
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stage_sum = np.zeros(4)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -376,7 +384,6 @@ def main():
             evs[s][0].record(stream)
             step(s % args.batches)
             evs[s][1].record(stream)
-            stage_sum += np.array(dev.stage_ms())  # syncs this step; device time only is used
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -386,7 +393,18 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * nq * args.steps / (ms_max / 1000.0)
-    stage_mean = stage_sum / args.steps
+
+    # ---- per-kernel times (unchunked launches: one launch per stage per step)
+    dev.set_chunks(1)
+    stage_sum = np.zeros(4)
+    kstep = min(args.steps, 50)
+    for s in range(kstep):
+        if not args.no_flush:
+            flush.fill_(s & 0xFF)
+        step(s % args.batches)
+        stage_sum += np.array(dev.stage_ms())
+    stage_mean = stage_sum / kstep
+    dev.set_chunks(args.chunks)
 
     # ---- e2e through the public host API (pinned buffers, copies inside the timed call)
     hq = [torch.from_numpy(b).pin_memory() for b in batches]
@@ -475,12 +493,13 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write)" if not args.no_flush else "not flushed",
                    "parallelism": f"replicas x{world}"},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": gpu_launches(hix, nq, args.chunks) * args.steps,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "parity": parity,
         "recall": recall,
         "kernel_variant": args.variant,
+        "chunks": args.chunks,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -147,8 +147,13 @@ void pqtg_index_destroy(pqtg_index* index);
 /* ---- workspace (per stream; not shared by concurrent searches) -------------------- */
 int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_workspace** out);
 void pqtg_workspace_destroy(pqtg_workspace* ws);
+/* Split each (sub-)batch into `chunks` pieces that alternate between two streams so one
+ * piece's re-rank overlaps the next piece's traversal / bin selection (and, in pqtg_search, the
+ * copies). 0 = automatic (1, 2 or 4 by batch size), 1 = no overlap. Results are identical. */
+int pqtg_workspace_set_chunks(pqtg_workspace* ws, uint32_t chunks);
 /* Device milliseconds of the last pqtg_search* call per stage: [0] traversal, [1] bin
- * selection + gather, [2] re-rank + top-k, [3] whole search. Synchronises the last stream. */
+ * selection + gather, [2] re-rank + top-k, [3] whole search — of the call's first chunk (see
+ * pqtg_workspace_set_chunks). Synchronises the last stream. */
 int pqtg_workspace_stage_ms(pqtg_workspace* ws, float* ms4);
 /* Copy per-query intermediates of the LAST sub-batch searched with `ws` to host buffers
  * (any pointer may be NULL). Used by the per-stage parity tests.

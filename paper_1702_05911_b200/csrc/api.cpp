@@ -267,6 +267,14 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
 
 void pqtg_workspace_destroy(pqtg_workspace* ws) { delete ws; }
 
+int pqtg_workspace_set_chunks(pqtg_workspace* h, uint32_t chunks) {
+    return guarded([&] {
+        if (!h) throw Error{PQTG_ERR_ARG, "null argument"};
+        h->ws->chunks = chunks;
+        return PQTG_OK;
+    });
+}
+
 int pqtg_workspace_stage_ms(pqtg_workspace* h, float* ms4) {
     return guarded([&] {
         if (!h || !ms4) throw Error{PQTG_ERR_ARG, "null argument"};
@@ -326,10 +334,32 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         if (nq > ws.max_batch) throw Error{PQTG_ERR_ARG, "nq exceeds the workspace max_batch"};
         PQTG_CUDA_CHECK(cudaSetDevice(index->dev->device));
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        next_epoch(ws, s, nullptr);
+        // the workspace's aux stream may still run a previous call's chunks on these slices
+        PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
+        PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));
+        next_epoch(ws, s, ws.aux_stream);
         ws.last_stream = s;
         ws.last_nq = nq;
-        run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, s, true);
+        const uint64_t nch = ws.chunks ? ws.chunks : (nq >= 2048 ? 4 : (nq >= 256 ? 2 : 1));
+        if (nch <= 1 || nq < nch) {
+            run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, s, true);
+            return PQTG_OK;
+        }
+        // chunks alternate between the caller's stream and the workspace's aux stream (forked
+        // from and joined back into the caller's), so one chunk's re-rank overlaps the next
+        // chunk's traversal / bin selection
+        PQTG_CUDA_CHECK(cudaEventRecord(ws.join, s));
+        PQTG_CUDA_CHECK(cudaStreamWaitEvent(ws.aux_stream, ws.join, 0));
+        const uint64_t per = (nq + nch - 1) / nch;
+        const uint64_t kk = std::max<uint32_t>(k, 1);
+        for (uint64_t c = 0; c * per < nq; ++c) {
+            const uint64_t c0 = c * per, cn = std::min(per, nq - c0);
+            run_chunk(*index->dev, ws, c0, d_queries + c0 * index->dev->prm.D, cn, k, d_ids ? d_ids + c0 * kk : nullptr,
+                      d_dists ? d_dists + c0 * kk : nullptr, d_counts + c0, d_stats ? d_stats + c0 : nullptr,
+                      (c & 1) ? ws.aux_stream : s, c == 0);
+        }
+        PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
+        PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));
         return PQTG_OK;
     });
 }
@@ -363,7 +393,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
             PQTG_CUDA_CHECK(cudaEventRecord(ws.join, st[1]));
             PQTG_CUDA_CHECK(cudaStreamWaitEvent(st[0], ws.join, 0));
             next_epoch(ws, st[0], st[1]);
-            const uint64_t nch = b >= 1024 ? 4 : (b >= 256 ? 2 : 1);
+            const uint64_t nch = ws.chunks ? ws.chunks : (b >= 1024 ? 4 : (b >= 256 ? 2 : 1));
             const uint64_t per = (b + nch - 1) / nch;
             for (uint64_t c = 0; c * per < b; ++c) {
                 const uint64_t c0 = c * per, cn = std::min(per, b - c0);

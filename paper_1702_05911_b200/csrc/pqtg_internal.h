@@ -113,7 +113,8 @@ struct Workspace {
     uint64_t hash_words = 0;
     uint64_t hash_stride = 0;     // words per query
     uint32_t hash_epoch = 0;
-    cudaStream_t aux_stream = nullptr;  // second stream of the pipelined host search
+    cudaStream_t aux_stream = nullptr;  // second stream of the pipelined searches
+    uint32_t chunks = 0;                // sub-batch chunks per search (0 = automatic)
     cudaEvent_t join = nullptr;
     WsSlice slice(uint64_t q0) const;
     // host-call staging (grown on demand)

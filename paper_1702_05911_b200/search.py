@@ -142,6 +142,10 @@ class DeviceIndex:
         check(lib().pqtg_search_device(self._h, self._ws, d_queries, nq, k, d_ids, d_dists, d_counts,
                                        d_stats, stream))
 
+    def set_chunks(self, chunks: int) -> None:
+        """Overlap stages across `chunks` pieces of each batch on two streams (0 = auto, 1 = off)."""
+        check(lib().pqtg_workspace_set_chunks(self._ws, int(chunks)))
+
     def stage_ms(self) -> list[float]:
         ms = (C.c_float * 4)()
         check(lib().pqtg_workspace_stage_ms(self._ws, ms))
