@@ -141,3 +141,33 @@ def test_gpu_batching_is_deterministic():
     b = DeviceIndex(path, max_batch=4096).search(Q, 50)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("chunks", [1, 2, 3, 0])
+def test_gpu_chunked_searches_identical(chunks):
+    """Chunked two-stream searches (host and device entry points) return the reference's results."""
+    import torch
+
+    g = load_golden("p4_gist")
+    Q = np.concatenate([g["queries"]] * 9)  # 288 queries -> auto picks 2 chunks
+    k = int(g["k"])
+    dev = DeviceIndex(str(GOLDEN / "p4_gist.pqt"), max_batch=300)
+    dev.set_chunks(chunks)
+    host = dev.search(Q, k)
+    n = len(g["queries"])
+    for r in range(9):
+        sl = slice(r * n, (r + 1) * n)
+        assert_same_results(tuple(x[sl] for x in host), (g["ids"], g["dists"], g["counts"], g["stats"]), "host")
+    dq = torch.from_numpy(Q).cuda()
+    d_ids = torch.empty((len(Q), k), dtype=torch.int32, device="cuda")
+    d_d = torch.empty((len(Q), k), dtype=torch.float32, device="cuda")
+    d_c = torch.empty(len(Q), dtype=torch.int32, device="cuda")
+    d_s = torch.empty((len(Q), 3), dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+    dev.search_device(dq.data_ptr(), len(Q), k, d_ids.data_ptr(), d_d.data_ptr(), d_c.data_ptr(), d_s.data_ptr(),
+                      stream.cuda_stream)
+    torch.cuda.synchronize()
+    got = (d_ids.cpu().numpy().view(np.uint32), d_d.cpu().numpy(), d_c.cpu().numpy().view(np.uint32),
+           d_s.cpu().numpy().view(np.uint64))
+    for x, y in zip(got, host):
+        assert np.array_equal(x, y)
