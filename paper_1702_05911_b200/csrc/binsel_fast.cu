@@ -28,6 +28,10 @@ constexpr int kFilterWarps = kBsThreads / 32 - 1;  // warp 0 walks the queue
 constexpr int kFilterThreads = kFilterWarps * 32;
 constexpr int kMaxItems = 8;
 constexpr uint32_t kQueueCap = kFilterThreads * kMaxItems;
+// the walker's visited set: a shared open-addressing table of slot + 1 (0 = free); past half
+// full it moves to the query's global table, which is sized for the whole budget
+constexpr uint32_t kVisLog2 = 10;
+constexpr uint32_t kVis = 1u << kVisLog2;
 
 __device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t H) {
     const uint64_t x = (uint64_t)a + b;
@@ -178,6 +182,7 @@ __global__ void __launch_bounds__(kBsThreads, 4)
     uint32_t* hkeys = HASH ? ghash + ((uint64_t)blockIdx.x << ts_log2) : nullptr;
     const uint32_t etag = epoch << 26;
     __shared__ uint32_t wcnt[2][64];
+    __shared__ uint32_t svis[HASH ? kVis : 1];
     __shared__ uint32_t s_nq[2], s_C, s_R, s_maxord;
 
     const uint64_t q = blockIdx.x;
@@ -190,6 +195,8 @@ __global__ void __launch_bounds__(kBsThreads, 4)
         const uint64_t flat = (uint64_t)(code >> 16) * p.k2 + (code & 0xFFFFu);
         terms[idx] = (uint32_t)((flat * p.mult[idx / W]) % p.H);
     }
+    if (HASH)
+        for (uint32_t i = tid; i < kVis; i += blockDim.x) svis[i] = 0u;
     if (tid == 0) {
         s_C = 0;
         s_R = 0;
@@ -219,6 +226,8 @@ __global__ void __launch_bounds__(kBsThreads, 4)
     uint32_t base = 0;                      // first stream position of the pass being filtered
     uint32_t nit = 1;                       // items per filter thread: 1 on the first pass, then 8
     uint32_t prev_n = 0;                    // queued tuples of the previous pass
+    uint32_t nvis = 0;                      // walker: slots inserted in the visited set
+    bool spilled = false;                   // walker: visited set moved to global memory
     for (uint32_t pass = 0;; ++pass) {
         const uint32_t buf = pass & 1u;
         uint2* qb = queue + (size_t)buf * kQueueCap;
@@ -233,12 +242,37 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                     const uint32_t idx = b0 + lane;
                     const bool has = idx < prev_n;
                     const uint2 e = has ? qp[idx] : make_uint2(0, kEmptyKey);
+                    // the bin's extent, loaded before the visited test so the two overlap
+                    uint32_t start = 0, cnt = 0;
+                    if (has) {
+                        start = __ldg(p.offsets + e.y);
+                        cnt = __ldg(p.offsets + e.y + 1) - start;
+                    }
                     bool first = has;
                     if (HASH) {
                         const uint32_t grp = __match_any_sync(0xffffffffu, e.y);
-                        if (has) {
-                            if ((uint32_t)(__ffs(grp) - 1) != (uint32_t)lane) {
-                                first = false;  // an earlier tuple of this batch has the slot
+                        if (has && (uint32_t)(__ffs(grp) - 1) != (uint32_t)lane) first = false;  // earlier in batch
+                        bool fresh = false;
+                        if (first) {
+                            if (!spilled) {
+                                // shared visited set: keys slot + 1, 0 = free
+                                const uint32_t key = e.y + 1u;
+                                uint32_t h = (e.y * 0x9E3779B1u) >> (32 - kVisLog2);
+                                for (;;) {
+                                    const uint32_t cur = svis[h];
+                                    if (cur == 0u) {
+                                        if (atomicCAS(svis + h, 0u, key) == 0u) {
+                                            fresh = true;
+                                            break;
+                                        }
+                                        continue;
+                                    }
+                                    if (cur == key) {
+                                        first = false;  // visited in an earlier batch
+                                        break;
+                                    }
+                                    h = (h + 1) & (kVis - 1);
+                                }
                             } else {
                                 const uint32_t key = etag | e.y;
                                 uint32_t h = (e.y * 0x9E3779B1u) >> (32 - ts_log2);
@@ -256,12 +290,30 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                                 }
                             }
                         }
+                        nvis += __popc(__ballot_sync(0xffffffffu, fresh));
+                        if (!spilled && nvis > kVis / 2) {
+                            // the shared set is half full: move it to the per-query global
+                            // table (sized for the whole budget) and continue there
+                            __syncwarp();
+                            for (uint32_t i = lane; i < kVis; i += 32) {
+                                const uint32_t v = svis[i];
+                                if (v == 0u) continue;
+                                const uint32_t sl = v - 1u, key = etag | sl;
+                                uint32_t h = (sl * 0x9E3779B1u) >> (32 - ts_log2);
+                                for (;;) {
+                                    const uint32_t cur = hkeys[h];
+                                    if ((cur & 0xFC000000u) != etag) {
+                                        if (atomicCAS(hkeys + h, cur, key) == cur) break;
+                                        continue;
+                                    }
+                                    h = (h + 1) & (TS - 1);
+                                }
+                            }
+                            __syncwarp();
+                            spilled = true;
+                        }
                     }
-                    uint32_t start = 0, cnt = 0;
-                    if (first) {
-                        start = __ldg(p.offsets + e.y);
-                        cnt = __ldg(p.offsets + e.y + 1) - start;
-                    }
+                    if (!first) cnt = 0;
                     uint32_t incl = cnt;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {

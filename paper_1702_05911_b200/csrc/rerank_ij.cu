@@ -27,35 +27,89 @@ namespace {
 
 constexpr int kIjThreads = 512;
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // no id: the candidate belongs to another shard
-constexpr uint32_t kRangeCache = 1024;
+constexpr uint32_t kRangeCache = 512;       // ranges whose (start − offset) is kept in smem
 
 struct IjLayout {
-    size_t t, fine, keys, sel, coff, total;
+    size_t t, fine, keys, sel, rid, delta, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
+constexpr int kSelBits = 10;                 // wide radix-select digit (block_select_wide)
+constexpr uint32_t kSelMin = 512;           // sel capacity for the wide select's bin
+
+// sel capacity: a power of two >= max(kk, kSelMin)
+__host__ __device__ inline uint32_t ij_sel_cap(uint32_t kk) {
+    uint32_t c = kSelMin;
+    while (c < kk) c <<= 1;
+    return c;
+}
+
 __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint32_t sel_cap) {
     IjLayout l{};
     size_t o = 0;
-    l.t = o;  // offset 0: compile-time part offsets become load immediates
+    l.t = o;  // T, fine, delta and rid sit at compile-time offsets (load immediates)
     o += (size_t)L * 256 * 8;
     l.fine = o;
     o += (size_t)L * 16 * 4;
+    l.delta = o;
+    o += (size_t)kRangeCache * 4;
+    // rid: u16 range index per candidate, padded to whole 4096-candidate scan tiles; after
+    // the candidate loop the same bytes hold the select histogram and sel
+    l.rid = o;
+    const size_t rid_bytes = al16((size_t)((budget + 4095) / 4096) * 4096 * 2);
+    const size_t sel_bytes = ((size_t)4 << kSelBits) + (size_t)sel_cap * 8;
+    l.sel = o + ((size_t)4 << kSelBits);
+    o += rid_bytes > sel_bytes ? rid_bytes : sel_bytes;
     l.keys = o;
     o += al16((size_t)budget * 8);
-    l.sel = o;
-    o += al16((size_t)sel_cap * 8);
-    l.coff = o;
-    o += al16((size_t)(budget < kRangeCache ? budget : kRangeCache) * 4);
     l.total = o;
     return l;
+}
+
+// rid[j] = index of the range holding candidate j, for j < C: rid is zero except
+// rid[offset of range r] = r, so an inclusive max-scan gives it (range offsets increase
+// with r). 512 threads × 8 consecutive u16 per 4096-candidate tile.
+__device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wmax) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < C; base += 8 * kIjThreads) {
+        uint4* v4 = reinterpret_cast<uint4*>(rid + base) + tid;
+        uint4 v = *v4;
+        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        uint32_t run = 0, e[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            run = max(run, w[i] & 0xFFFFu);
+            e[2 * i] = run;
+            run = max(run, w[i] >> 16);
+            e[2 * i + 1] = run;
+        }
+        uint32_t incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl = max(incl, t);
+        }
+        if (lane == 31) wmax[warp] = incl;
+        __syncthreads();
+        uint32_t before = carry;
+        for (uint32_t i = 0; i < warp; ++i) before = max(before, wmax[i]);
+        const uint32_t up = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane > 0) before = max(before, up);
+        uint32_t r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = max(before, e[i]);
+        *v4 = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), r[4] | (r[5] << 16), r[6] | (r[7] << 16));
+        for (uint32_t i = 0; i < kIjThreads / 32; ++i) carry = max(carry, wmax[i]);
+        __syncthreads();
+    }
 }
 
 }  // namespace
 
 template <int LT>
-__global__ void __launch_bounds__(kIjThreads, 2)
+__global__ void __launch_bounds__(kIjThreads, LT >= 64 ? 1 : 2)
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
@@ -64,53 +118,89 @@ __global__ void __launch_bounds__(kIjThreads, 2)
     const uint32_t k1 = p.k1, budget = p.budget;
     const IjLayout lay = ij_layout(LT, budget, sel_cap);
     float2* T = reinterpret_cast<float2*>(smem);
-    float* fine = reinterpret_cast<float*>(smem + lay.fine);
+    float* fine = reinterpret_cast<float*>(smem + ij_layout(LT, 0, 0).fine);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + lay.keys);
     uint64_t* sel = reinterpret_cast<uint64_t*>(smem + lay.sel);
-    uint32_t* coff = reinterpret_cast<uint32_t*>(smem + lay.coff);
-    __shared__ uint32_t hist[256];
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0).rid);  // aliases rid
+    uint16_t* rid = reinterpret_cast<uint16_t*>(smem + ij_layout(LT, 0, 0).rid);
+    uint32_t* delta = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0).delta);
+    __shared__ uint32_t wmax[kIjThreads / 32];
     __shared__ uint32_t s_count;
     __shared__ TopkShared s_sel;
 
     const uint64_t q = blockIdx.x;
-    const int tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x;
     const uint32_t R = nranges[q], C = ncand[q];
     const uint2* qr = ranges + q * (uint64_t)budget;
 
+    // every global load of the prologue is issued before the first barrier: the query's fine
+    // LUT, the first kIjThreads ranges and this thread's column of d2 (T build below)
+    constexpr uint32_t kPairLanes = 128;
+    constexpr uint32_t kFPer = (LT + kIjThreads / kPairLanes - 1) / (kIjThreads / kPairLanes);
+    const uint32_t pi = tid & (kPairLanes - 1), f0 = tid / kPairLanes;
+    const bool pair_lane = pi < p.npairs;
+    uint32_t pi_i = 0, pi_j = 0;
+    float c2v[kFPer];
+    if (pair_lane) {
+        const uint32_t pr = __ldg(p.pairs + pi);
+        pi_i = pr & 0xFFFFu;
+        pi_j = pr >> 16;
+#pragma unroll
+        for (uint32_t u = 0; u < kFPer; ++u) {
+            const uint32_t f = f0 + u * (kIjThreads / kPairLanes);
+            c2v[u] = f < LT ? __ldg(p.c2ij + f * 256 + (pi_i << 4 | pi_j)) : 0.0f;
+        }
+    }
+    const uint2 rg0 = tid < R ? __ldg(qr + tid) : make_uint2(0, 0);
     for (uint32_t i = tid; i < LT * 16; i += blockDim.x) {
         const uint32_t f = i >> 4, c = i & 15;
         fine[i] = c < k1 ? fine_in[q * LT * k1 + f * k1 + c] : 0.0f;
     }
+    const uint32_t Cpad = (C + 8 * kIjThreads - 1) / (8 * kIjThreads) * (8 * kIjThreads);
+    for (uint32_t i = tid; i < Cpad / 2; i += blockDim.x) reinterpret_cast<uint32_t*>(rid)[i] = 0;
     const bool cached = R <= kRangeCache;
-    if (cached)
-        for (uint32_t r = tid; r < R; r += blockDim.x) coff[r] = qr[r].y;
-    if (tid == 0) s_count = 0;
+    if (tid == 0) {
+        s_count = 0;
+        s_sel.kand = ~0ull;
+        s_sel.kor = 0ull;
+    }
     __syncthreads();
-    // T[f][i << 4 | j] = (E, c2) for every pair; entries with i >= j are never referenced
-    for (uint32_t idx = tid; idx < LT * 256; idx += blockDim.x) {
-        const uint32_t f = idx >> 8, i = (idx >> 4) & 15u, j = idx & 15u;
-        if (i < k1 && j < k1) {
-            const float c2 = __ldg(p.c2ij + idx);
-            const float b2 = fine[f * 16 + i], a2 = fine[f * 16 + j];
-            T[idx] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2), c2);
+    for (uint32_t r = tid; r < R; r += blockDim.x) {
+        const uint2 rg = r == tid ? rg0 : __ldg(qr + r);
+        rid[rg.y] = (uint16_t)r;
+        if (cached) delta[r] = rg.x - rg.y;
+    }
+    // T[f][i << 4 | j] = (E, c2) for every pair i < j (linequant.cpp:76-82); other entries
+    // are never referenced. Thread: one pair, every (blockDim / 128)-th part.
+    if (pair_lane) {
+        const uint32_t ij = pi_i << 4 | pi_j;
+#pragma unroll
+        for (uint32_t u = 0; u < kFPer; ++u) {
+            const uint32_t f = f0 + u * (kIjThreads / kPairLanes);
+            if (f < LT) {
+                const float b2 = fine[f * 16 + pi_i], a2 = fine[f * 16 + pi_j];
+                T[f * 256 + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
+            }
         }
     }
     __syncthreads();
+    range_index_scan(rid, C, wmax);
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     const bool sharded = p.shard_hi > p.shard_lo;
     constexpr int kVec = (2 * LT + 15) / 16;
     uint32_t mine = 0;
+    uint32_t kand = ~0u, kor = 0u;  // AND / OR of this thread's orderable distances
     // candidate j's code row and id, fetched one iteration ahead (software pipelining)
     auto fetch = [&](uint32_t j, uint4* v, uint32_t& id) {
-        uint32_t lo = 0, hi = R - 1;  // range holding candidate j
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            const uint32_t cm = cached ? coff[mid] : __ldg(&qr[mid].y);
-            if (cm <= j) lo = mid; else hi = mid - 1;
+        const uint32_t r = rid[j];
+        uint64_t pos;
+        if (cached) {
+            pos = (uint32_t)(delta[r] + j);
+        } else {
+            const uint2 rl = __ldg(qr + r);
+            pos = (uint64_t)rl.x + (j - rl.y);
         }
-        const uint2 rl = __ldg(qr + lo);
-        const uint64_t pos = (uint64_t)rl.x + (j - rl.y);
         id = kInvalid;
         if (!sharded || (pos >= p.shard_lo && pos < p.shard_hi)) {
             const uint64_t lp = pos - p.shard_lo;
@@ -143,26 +233,39 @@ __global__ void __launch_bounds__(kIjThreads, 2)
                 const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), ec.y)), __fmul_rn(lam, ec.x));
                 total = __fadd_rn(total, part);
             }
-            key = ((uint64_t)orderable(total) << 32) | id;
+            const uint32_t od = orderable(total);
+            key = ((uint64_t)od << 32) | id;
+            kand &= od;
+            kor |= od;
             ++mine;
         }
         keys[j] = key;
     }
-    if (mine) atomicAdd(&s_count, mine);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        kand &= __shfl_xor_sync(0xffffffffu, kand, d);
+        kor |= __shfl_xor_sync(0xffffffffu, kor, d);
+        mine += __shfl_xor_sync(0xffffffffu, mine, d);
+    }
+    if ((tid & 31) == 0 && mine) {
+        atomicAdd(&s_count, mine);
+        // ids are taken as all-different: only the distance bits' common prefix is skipped
+        atomicAnd(&s_sel.kand, ((unsigned long long)kand << 32));
+        atomicOr(&s_sel.kor, ((unsigned long long)kor << 32) | 0xFFFFFFFFull);
+    }
     __syncthreads();
     const uint32_t nvalid = s_count;
     const uint32_t kk = nvalid < k ? nvalid : k;
-    block_topk(keys, C, kk, sel, sel_cap, hist, s_sel);
-    write_topk(sel, kk, k, q, out_ids, out_dists, out_counts);
+    uint32_t m = 0;
+    if (kk) {
+        for (uint32_t i = tid; i < (1u << kSelBits); i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        m = block_select_wide<kSelBits, kIjThreads>(keys, C, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap, wmax, s_sel);
+    }
+    block_sort_write(sel, m, kk, k, q, out_ids, out_dists, out_counts);
 }
 
 namespace {
-
-uint32_t np2(uint32_t x) {
-    uint32_t r = 1;
-    while (r < x) r <<= 1;
-    return r;
-}
 
 template <int LT>
 void allow(int optin) {
@@ -174,7 +277,7 @@ void allow(int optin) {
 
 size_t ij_smem(const DevParams& p, uint32_t k) {
     const uint32_t kk = k < p.budget ? k : p.budget;
-    return ij_layout(p.L, p.budget, np2(kk > 0 ? kk : 1)).total;
+    return ij_layout(p.L, p.budget, ij_sel_cap(kk)).total;
 }
 
 }  // namespace
@@ -183,7 +286,8 @@ bool rerank_ij_ok(const DevParams& p, uint32_t k) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return p.code_ij && (p.L == 16 || p.L == 32 || p.L == 64) && ij_smem(p, k) + 4096 <= (size_t)optin;
+    return p.code_ij && p.budget <= 65535 && p.npairs <= 128 &&
+           (p.L == 16 || p.L == 32 || p.L == 64) && ij_smem(p, k) + 4096 <= (size_t)optin;
 }
 
 void configure_rerank_ij() {
@@ -198,7 +302,7 @@ void configure_rerank_ij() {
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids, float* dists,
                       uint32_t* counts, cudaStream_t s) {
     const uint32_t kk = k < p.budget ? k : p.budget;
-    const uint32_t cap = np2(kk > 0 ? kk : 1);
+    const uint32_t cap = ij_sel_cap(kk);
     const size_t sm = ij_smem(p, k);
 #define PQTG_IJ(LT)                                                                                         \
     rerank_ij_kernel<LT><<<(unsigned)nq, kIjThreads, sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \

@@ -1,0 +1,69 @@
+"""Top-k selection edge cases of the re-rank kernels (search.cpp:229-257) against the C oracle.
+
+* k from 1 to beyond the 512-key wide-select capacity and beyond the block size (bitonic
+  fallback), on the golden indexes whose shapes take the fast (i, j)-code re-rank;
+* a database of repeated vectors, so thousands of candidates share one distance and the
+  wide select's bin overflows (exact 8-bit select fallback); ties resolve by id.
+"""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden
+from oracle.bindings import Oracle
+from paper_1702_05911_b200 import DeviceIndex, PqtConfig, builder
+from test_gpu_parity import VARIANTS, assert_same_results
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=list(VARIANTS), autouse=True)
+def kernel_variant(request):
+    from paper_1702_05911_b200._abi import lib
+
+    lib().pqtg_set_kernel_variant(VARIANTS[request.param])
+    yield request.param
+    lib().pqtg_set_kernel_variant(0)
+
+
+@pytest.mark.parametrize("name", ["p2_sift", "p4_gist"])
+@pytest.mark.parametrize("k", [1, 3, 511, 1500])
+def test_gpu_topk_sizes(name, k):
+    path = str(GOLDEN / f"{name}.pqt")
+    Q = load_golden(name)["queries"][:24]
+    got = DeviceIndex(path).search(Q, k)
+    want = Oracle(path).knn(Q, k)
+    assert_same_results(got, want, f"{name} k={k}")
+
+
+def test_gpu_topk_repeated_vectors():
+    import torch
+
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=128, p_tree=2, k1=16, k2=8, w=4, p_line=32, train_iters=4, seed=9,
+                    candidate_budget=4096)
+    base = builder.synth_clustered(300, cfg.dim, 8, 20.0, 9, device=dev)
+    db = base.repeat(100, 1).contiguous()  # every vector 100 times: equal codes, equal distances
+    hix = builder.build_index(db, db[:3000], cfg)
+    Q = builder.synth_clustered(16, cfg.dim, 8, 20.0, 10, device=dev).cpu().numpy()
+    o = Oracle(hix)
+    for k in (100, 700):
+        got = DeviceIndex(hix).search(Q, k)
+        want = o.knn(Q, k)
+        assert_same_results(got, want, f"repeated k={k}")
+
+
+def test_gpu_many_small_bins():
+    """P = 4 with (k1·k2)^4 > H (the walker's visited set is needed) and bins of about one
+    vector: ~2000 bins per query overflow the shared visited set into the global table."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=64, p_tree=4, k1=8, k2=8, w=4, p_line=16, train_iters=4, seed=12,
+                    hash_size=1 << 17, candidate_budget=2048)
+    db = builder.synth_clustered(60_000, cfg.dim, 60_000, 20.0, 12, device=dev)  # ~uniform
+    hix = builder.build_index(db, db[:20_000], cfg)
+    Q = builder.synth_clustered(24, cfg.dim, 64, 20.0, 13, device=dev).cpu().numpy()
+    got = DeviceIndex(hix).search(Q, 50)
+    want = Oracle(hix).knn(Q, 50)
+    assert_same_results(got, want, "small bins")
+    assert (got[3][:, 0] > 600).any()  # bins_visited: past the shared set's 512
