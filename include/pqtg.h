@@ -11,6 +11,8 @@
  *   pqtg_search              ← pqt::knn_query_batch        include/pqt/search.hpp:83, src/search.cpp:262-274
  *                              (each row = pqt::knn_query, src/search.cpp:126-260)
  *   pqtg_search_device       ← same, device-resident inputs/outputs on a caller stream
+ *   pqtg_index_attach_database ← pqt::PqtIndex::attach_database  include/pqt/search.hpp:53,
+ *                              src/search.cpp:44-49 (enables the exact re-rank, :229-249)
  *   pqtg_merge_topk_host     ← no reference counterpart: merges per-shard top-k lists by the
  *                              reference's (dist, id) order (candidate_less, src/search.cpp:39-41)
  *
@@ -101,8 +103,9 @@ typedef struct pqtg_index_view {
 
 /* Per-query counters of pqt::QueryStats (include/pqt/search.hpp:15-23). The reference's
  * *_us wall-clock timers have no per-query meaning on a batched GPU; per-stage batch times
- * come from pqtg_workspace_stage_ms. exact_evals is 0 (no raw vectors on device, as for an
- * index from load_index, search.cpp:229-238). */
+ * come from pqtg_workspace_stage_ms. exact_evals = min(max(rerank_exact, k), C) when raw vectors
+ * are attached (pqtg_index_attach_database) and rerank_exact > 0, else 0 (as for an index from
+ * load_index, search.cpp:229-238). */
 typedef struct pqtg_query_stats {
     uint64_t bins_visited;
     uint64_t candidates;
@@ -142,6 +145,14 @@ int pqtg_index_create(const pqtg_index_view* view, int device, pqtg_index** out)
 int pqtg_index_load(const char* path, int device, uint64_t shard_lo, uint64_t shard_hi,
                     pqtg_index** out);
 int pqtg_index_info_get(const pqtg_index* index, pqtg_index_info* out);
+/* pqt::PqtIndex::attach_database (src/search.cpp:44-49): copy n × dim float32 raw vectors
+ * (vector-id order, row-major) to the index's device. Searches then run the exact re-rank
+ * stage when config.rerank_exact > 0 (src/search.cpp:229-249): the min(max(rerank_exact, k), C)
+ * best candidates by line distance get l2_sq(row, y) distances in the reference's fp32 order
+ * and are re-sorted by (dist, id). rows == NULL detaches. A mismatched n or dim returns
+ * PQTG_ERR_BAD_DIM (std::invalid_argument in the reference); a sharded index returns
+ * PQTG_ERR_UNSUPPORTED. Not safe to call concurrently with a search on the same index. */
+int pqtg_index_attach_database(pqtg_index* index, const float* rows, uint64_t n, uint32_t dim);
 void pqtg_index_destroy(pqtg_index* index);
 
 /* ---- workspace (per stream; not shared by concurrent searches) -------------------- */

@@ -77,6 +77,7 @@ class Oracle(_Lib):
         "pqto_line_distance": (C.c_float, [_vp, _vp, _vp, _vp]),
         "pqto_candidates": (C.c_int64, [_vp, _vp, _vp, _u64, C.POINTER(_u64)]),
         "pqto_knn_batch": (C.c_int, [_vp, _vp, _u64, _u32, _u32, C.c_int, _u64, _u64, _vp, _vp, _vp, _vp]),
+        "pqto_attach_database": (None, [_vp, _vp]),
     }
 
     def __init__(self, index: HostIndex | str):
@@ -107,6 +108,18 @@ class Oracle(_Lib):
     def save(self, path: str) -> None:
         if self.so().pqto_save(self.h, str(path).encode()) != 0:
             raise RuntimeError(self.so().pqto_last_error().decode())
+
+    def attach_database(self, rows: np.ndarray | None) -> None:
+        """PqtIndex::attach_database (search.cpp:44-49); the array is kept alive here."""
+        if rows is None:
+            self._db = None
+            self.so().pqto_attach_database(self.h, None)
+            return
+        rows = np.ascontiguousarray(rows, np.float32)
+        if rows.shape != (self.n, self.config.dim):
+            raise ValueError("attach_database: vector set does not match index")
+        self._db = rows
+        self.so().pqto_attach_database(self.h, _p(rows))
 
     def knn(self, queries: np.ndarray, k: int, threads: int = 0, shard=(0, 0)):
         q = np.ascontiguousarray(queries, np.float32)

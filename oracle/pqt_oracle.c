@@ -43,6 +43,7 @@ struct pqto_index {
     float* fine;            /* L × k1 × fd: FineCentroids::slices (linequant.cpp:13-46) */
     uint16_t* pairs;        /* npairs × 2: PairDistanceTable::pairs (linequant.cpp:76-82) */
     uint32_t npairs;
+    const float* db;        /* borrowed raw vectors n × dim (PqtIndex::database), or NULL */
 };
 
 /* ---------------------------------------------------------------- small containers */
@@ -783,7 +784,8 @@ static int cmp_cand(const void* x, const void* y) {  /* candidate_less, search.c
     return a->id < b->id ? -1 : (a->id > b->id);
 }
 
-/* knn_query (src/search.cpp:126-260) with rerank = 0 (no raw vectors attached). */
+/* knn_query (src/search.cpp:126-260). The exact re-rank (:229-249) runs when raw vectors
+ * are attached (pqto_attach_database) and rerank_exact > 0, on unsharded searches only. */
 static int knn_one(const pqto_index* ix, const float* y, uint32_t k, uint64_t lo, uint64_t hi,
                    uint32_t* ids, float* dists, uint32_t* count, uint64_t* stats) {
     const pqtg_config* c = &ix->cfg;
@@ -813,7 +815,18 @@ static int knn_one(const pqto_index* ix, const float* y, uint32_t k, uint64_t lo
                                              ix->pair_id + (size_t)id * c->p_line, fine);
         ++nr;
     }
+    /* rerank = min(max(rerank_exact, k), C) with raw vectors attached (search.cpp:229-238) */
+    uint64_t rerank = 0;
+    if (c->rerank_exact > 0 && ix->db && !(hi > lo)) {
+        uint64_t r = c->rerank_exact > k ? c->rerank_exact : k;
+        rerank = r < nr ? r : nr;
+    }
     qsort(ranked, nr, sizeof(cand), cmp_cand);  /* partial_sort prefix == full sort prefix */
+    if (rerank > 0) {  /* search.cpp:242-249: exact l2_sq(db.row(id), y), then re-sort */
+        for (uint64_t i = 0; i < rerank; ++i)
+            ranked[i].dist = l2_sq(ix->db + (size_t)ranked[i].id * c->dim, y, c->dim);
+        qsort(ranked, rerank, sizeof(cand), cmp_cand);
+    }
     uint64_t out = k < nr ? k : nr;
     for (uint64_t i = 0; i < out; ++i) {
         ids[i] = ranked[i].id;
@@ -823,11 +836,13 @@ static int knn_one(const pqto_index* ix, const float* y, uint32_t k, uint64_t lo
     if (stats) {
         stats[0] = bins;
         stats[1] = (uint64_t)C;
-        stats[2] = 0;
+        stats[2] = rerank;
     }
     free(fine); free(l1); free(l2); free(pos); free(ranked);
     return 0;
 }
+
+void pqto_attach_database(pqto_index* ix, const float* rows) { ix->db = rows; }
 
 typedef struct {
     const pqto_index* ix;

@@ -61,8 +61,12 @@ float pqto_line_distance(const pqto_index* index, const uint8_t* lambda_q,
 int64_t pqto_candidates(const pqto_index* index, const float* y, uint32_t* positions,
                         uint64_t cap, uint64_t* bins_visited);
 
-/* knn_query_batch (src/search.cpp:262-274) with exact re-rank disabled (loaded index:
- * no raw vectors). Outputs nq × k; counts[q] valid entries; stats nq × 3
+/* PqtIndex::attach_database (src/search.cpp:44-49): borrow n × dim raw vectors (id order) for
+ * the exact re-rank stage; NULL detaches. */
+void pqto_attach_database(pqto_index* index, const float* rows);
+
+/* knn_query_batch (src/search.cpp:262-274); the exact re-rank runs only with raw vectors
+ * attached (else as for a loaded index). Outputs nq × k; counts[q] valid entries; stats nq × 3
  * (bins_visited, candidates, exact_evals) may be NULL. shard_lo/hi restrict re-ranking to
  * positions in [lo, hi) (0/0 = all) and return that shard's local top-k. threads <= 0 means
  * all hardware threads. Returns 0 or a negative status. */

@@ -99,6 +99,7 @@ SIGNATURES = {
     "pqtg_index_load": (C.c_int, [C.c_char_p, C.c_int, _u64, _u64, C.POINTER(_vp)]),
     "pqtg_index_info_get": (C.c_int, [_vp, C.POINTER(PqtgIndexInfo)]),
     "pqtg_index_destroy": (None, [_vp]),
+    "pqtg_index_attach_database": (C.c_int, [_vp, _vp, _u64, _u32]),
     "pqtg_workspace_create": (C.c_int, [_vp, _u64, C.POINTER(_vp)]),
     "pqtg_workspace_destroy": (None, [_vp]),
     "pqtg_workspace_set_chunks": (C.c_int, [_vp, _u32]),

@@ -88,6 +88,27 @@ void ensure_staging(Workspace& ws, uint64_t k) {
     }
 }
 
+// k' of the line-ranked prefix the exact stage re-ranks: max(k, rerank_exact), at most the
+// candidate budget (C <= budget).
+uint32_t exact_prefix(const DevParams& p, uint32_t k) {
+    const uint32_t kp = std::max(k, p.rerank_exact);
+    return std::min(kp, std::max<uint32_t>(p.budget, 1));
+}
+
+// Buffers of the line-ranked prefix for the exact stage (only with raw vectors attached).
+void ensure_exact(Workspace& ws, uint32_t k) {
+    const DevParams& p = ws.index->prm;
+    if (!p.db || p.rerank_exact == 0 || k == 0) return;
+    const uint32_t kp = exact_prefix(p, k);
+    if (!ws.ex_counts) ws.ex_counts = dev_alloc<uint32_t>(ws.allocations, ws.max_batch);
+    if (kp > ws.ex_cap) {  // grow: old buffers stay owned by the workspace
+        ws.ex_ids = dev_alloc<uint32_t>(ws.allocations, ws.max_batch * kp);
+        ws.ex_dists = dev_alloc<float>(ws.allocations, ws.max_batch * kp);
+        ws.ex_cap = kp;
+    }
+    ws.ex_k = kp;
+}
+
 // A fresh epoch for the workspace's visited-slot table before its regions are reused. On wrap
 // the table is cleared; `streams` are drained first so no in-flight chunk still uses it.
 void next_epoch(Workspace& ws, cudaStream_t s, cudaStream_t other) {
@@ -125,7 +146,17 @@ void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_qu
     if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[1], s));
     launch_binsel(p, nq, sl, d_stats, s);
     if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[2], s));
-    launch_rerank(p, nq, k, sl, d_ids, d_dists, d_counts, s);
+    if (p.db && p.rerank_exact > 0) {
+        // exact re-rank (search.cpp:229-249): K5 keeps the k' = max(k, rerank_exact) best by
+        // line distance (the reference's partial_sort prefix, :239-240), K6 replaces their
+        // distances by exact ones and returns the first min(k, C)
+        const uint32_t kp = exact_prefix(p, k);
+        launch_rerank(p, nq, kp, sl, ws.ex_ids + q0 * ws.ex_k, ws.ex_dists + q0 * ws.ex_k, ws.ex_counts + q0, s);
+        launch_exact(p, d_queries, nq, (uint32_t)ws.ex_k, ws.ex_ids + q0 * ws.ex_k, ws.ex_counts + q0, k, d_ids,
+                     d_dists, d_counts, d_stats, s);
+    } else {
+        launch_rerank(p, nq, k, sl, d_ids, d_dists, d_counts, s);
+    }
     if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[3], s));
 }
 
@@ -226,6 +257,44 @@ int pqtg_index_info_get(const pqtg_index* index, pqtg_index_info* out) {
         out->code_row_bytes = d.prm.row_bytes;
         out->device_bytes = d.bytes;
         out->device = d.device;
+        return PQTG_OK;
+    });
+}
+
+int pqtg_index_attach_database(pqtg_index* index, const float* rows, uint64_t n, uint32_t dim) {
+    return guarded([&] {
+        if (!index) throw Error{PQTG_ERR_ARG, "null argument"};
+        DevIndex& d = *index->dev;
+        PQTG_CUDA_CHECK(cudaSetDevice(d.device));
+        if (!rows) {  // detach
+            if (d.db) {
+                PQTG_CUDA_CHECK(cudaDeviceSynchronize());
+                PQTG_CUDA_CHECK(cudaFree(d.db));
+            }
+            d.db = nullptr;
+            d.prm.db = nullptr;
+            return PQTG_OK;
+        }
+        // search.cpp:44-49: the vector set must match the index
+        if (n != d.n || dim != d.prm.D)
+            throw Error{PQTG_ERR_BAD_DIM, "attach_database: vector set does not match index"};
+        if (d.prm.shard_hi > d.prm.shard_lo && (d.prm.shard_lo != 0 || d.prm.shard_hi != d.n))
+            unsupported("exact re-ranking on a sharded index");
+        float* buf = nullptr;
+        const size_t bytes = (size_t)n * dim * sizeof(float);
+        cudaError_t e = cudaMalloc(&buf, bytes ? bytes : 16);
+        if (e != cudaSuccess) throw Error{PQTG_ERR_OOM, std::string("attach_database: ") + cudaGetErrorString(e)};
+        e = cudaMemcpy(buf, rows, bytes, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(buf);
+            throw Error{PQTG_ERR_CUDA, std::string("attach_database: ") + cudaGetErrorString(e)};
+        }
+        if (d.db) {
+            PQTG_CUDA_CHECK(cudaDeviceSynchronize());
+            cudaFree(d.db);
+        }
+        d.db = buf;
+        d.prm.db = buf;
         return PQTG_OK;
     });
 }
@@ -333,6 +402,7 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         if (ws.index != index->dev.get()) throw Error{PQTG_ERR_ARG, "workspace belongs to another index"};
         if (nq > ws.max_batch) throw Error{PQTG_ERR_ARG, "nq exceeds the workspace max_batch"};
         PQTG_CUDA_CHECK(cudaSetDevice(index->dev->device));
+        ensure_exact(ws, k);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         // the workspace's aux stream may still run a previous call's chunks on these slices
         PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
@@ -377,6 +447,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         std::lock_guard<std::mutex> lock(ws.mu);
         PQTG_CUDA_CHECK(cudaSetDevice(d.device));
         ensure_staging(ws, std::max<uint32_t>(k, 1));
+        ensure_exact(ws, k);
         const uint64_t D = d.prm.D;
         cudaStream_t st[2] = {ws.own_stream, ws.aux_stream};
         ws.last_stream = ws.own_stream;

@@ -166,7 +166,8 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
 // epoch << 26 | slot, H <= 2^26), which needs no clearing between searches.
 template <int P, bool HASH>
 __global__ void __launch_bounds__(kBsThreads, 4)
-    binsel_fast_kernel(DevParams p, const uint32_t* __restrict__ l2c_in, const uint8_t* __restrict__ slope_in,
+    binsel_fast_kernel(DevParams p, const uint32_t* __restrict__ l2c_in, const float* __restrict__ l2d_in,
+                       uint8_t* __restrict__ slope_out,
                        uint2* __restrict__ ranges, uint32_t* __restrict__ nranges, uint32_t* __restrict__ ncand,
                        uint32_t* __restrict__ ntuples, pqtg_query_stats* __restrict__ stats, uint32_t ts_log2,
                        uint32_t* __restrict__ ghash, uint32_t epoch, uint32_t W2ab) {
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(kBsThreads, 4)
 
     const uint64_t q = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t ta = slope_in[q * 2], tb = slope_in[q * 2 + 1];
+    __shared__ uint32_t s_slope[2];
 
     // slot terms (flat_part_code · (k1k2)^p) mod H, pqtree.cpp:12-25
     for (uint32_t idx = tid; idx < PW; idx += blockDim.x) {
@@ -201,8 +202,15 @@ __global__ void __launch_bounds__(kBsThreads, 4)
         s_C = 0;
         s_R = 0;
         s_maxord = 0;
+        uint32_t a, b;
+        query_slopes(p, l2d_in + q * PW, a, b);  // pick_slope_table (binorder.cpp:52-65)
+        s_slope[0] = a;
+        s_slope[1] = b;
+        slope_out[q * 2] = (uint8_t)a;
+        slope_out[q * 2 + 1] = (uint8_t)b;
     }
     __syncthreads();
+    const uint32_t ta = s_slope[0], tb = s_slope[1];
     if (P == 4 && W2ab) {  // fold each pair stream into per-pair-rank slot terms
         for (uint32_t u = tid; u < W2ab; u += blockDim.x) {
             const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * p.W2 + u);
@@ -347,7 +355,10 @@ __global__ void __launch_bounds__(kBsThreads, 4)
         // done: budget reached, or the stream ended and its last queue was just walked
         if (s_C >= budget || base >= total) break;
         // ---- order-preserving compaction (every filter warp scans the counts itself)
-        if (warp > 0) {
+        uint32_t anyhit = 0;
+#pragma unroll
+        for (int it = 0; it < kMaxItems; ++it) anyhit |= ball[it];
+        if (warp > 0 && (anyhit || warp == 1)) {  // a warp without hits has nothing to place
             const uint32_t n = nit * kFilterWarps;
             const uint32_t v0 = lane < (int)n ? wcnt[buf][lane] : 0;
             const uint32_t v1 = (uint32_t)(lane + 32) < n ? wcnt[buf][lane + 32] : 0;
@@ -366,7 +377,7 @@ __global__ void __launch_bounds__(kBsThreads, 4)
             const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
             for (int it = 0; it < kMaxItems; ++it) {
-                if (it < (int)nit) {
+                if (it < (int)nit && ball[it]) {  // warp-uniform: most items hold no hit
                     // exclusive prefix of entry e = (item, filter warp) in stream order
                     const uint32_t e = it * kFilterWarps + fw;
                     const uint32_t src = e & 31u;
@@ -463,7 +474,7 @@ void launch_binsel_fast(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg
     const BsConfig c = bs_config(p);
     const uint32_t epoch = ws.epoch;  // bumped per search by the caller (api.cpp)
 #define PQTG_BS(PP, HH)                                                                                       \
-    binsel_fast_kernel<PP, HH><<<(unsigned)nq, kBsThreads, c.smem, s>>>(p, ws.l2_code, ws.slope, ws.ranges,     \
+    binsel_fast_kernel<PP, HH><<<(unsigned)nq, kBsThreads, c.smem, s>>>(p, ws.l2_code, ws.l2_dist, ws.slope, ws.ranges,     \
                                                                        ws.nranges, ws.ncand, ws.ntuples, stats, \
                                                                        c.ts_log2, ws.hash, epoch, c.W2ab)
     if (p.P == 1) {

@@ -40,6 +40,65 @@ __device__ inline uint32_t pick_slope(const float* a, const float* b, uint32_t l
     return (uint32_t)(k + 5);
 }
 
+// pick_slope_table for a query's pair streams from its sorted level-2 lists l2d[P][W] in
+// global memory: (lists 0,1) and, for P = 4, (lists 2,3) (binorder.cpp:52-65, :237).
+__device__ inline void query_slopes(const DevParams& p, const float* l2d, uint32_t& ta, uint32_t& tb) {
+    ta = kSlopeOne;
+    tb = kSlopeOne;
+    const uint32_t W = p.W;
+    if (p.P < 2 || W < 2) return;
+    float a[2], b[2];
+    a[0] = l2d[0];
+    a[1] = l2d[1];
+    b[0] = l2d[W];
+    b[1] = l2d[W + 1];
+    ta = pick_slope(a, b, W, p.log108);
+    if (p.P == 4) {
+        a[0] = l2d[2 * W];
+        a[1] = l2d[2 * W + 1];
+        b[0] = l2d[3 * W];
+        b[1] = l2d[3 * W + 1];
+        tb = pick_slope(a, b, W, p.log108);
+    }
+}
+
+// ------------------------------------------------------------------ bulk async copies
+__device__ __forceinline__ uint32_t smem_addr(const void* ptr) {
+    return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// TMA 1-D bulk copy global -> shared (SASS UBLKCP); completes `bytes` on the mbarrier.
+// dst, src 16-byte aligned; bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred done;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        "@!done bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+
 // ------------------------------------------------------------------ block scan helpers
 __device__ __forceinline__ uint64_t warp_incl_scan(uint64_t v) {
     const int lane = threadIdx.x & 31;

@@ -37,6 +37,7 @@ DevIndex::~DevIndex() {
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     for (void* p : allocations) cudaFree(p);
+    if (db) cudaFree(db);
     cudaSetDevice(prev);
 }
 
@@ -236,6 +237,8 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     p.row_bytes = (L * (1 + pw) + 15) / 16 * 16;
     p.budget = (uint32_t)budget;
     p.resort = c.resort_bins ? 1u : 0u;
+    p.rerank_exact = c.rerank_exact;
+    p.db = nullptr;
     p.H = H;
     p.n = n;
     p.shard_lo = shard_lo;

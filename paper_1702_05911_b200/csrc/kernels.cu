@@ -31,8 +31,7 @@ template <int K1T, int K2T>  // compile-time k1 / k2 (0 = runtime): strided load
 __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const float* __restrict__ Q,
                                                             float* __restrict__ fine_out,
                                                             float* __restrict__ l2d_out,
-                                                            uint32_t* __restrict__ l2c_out,
-                                                            uint8_t* __restrict__ slope_out) {
+                                                            uint32_t* __restrict__ l2c_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t D = p.D, L = p.L, P = p.P, W = p.W, m = p.m, fd = p.fd;
     const uint32_t k1 = K1T ? (uint32_t)K1T : p.k1, k2 = K2T ? (uint32_t)K2T : p.k2;
@@ -42,7 +41,6 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
     uint32_t* l1o = reinterpret_cast<uint32_t*>(l1d + P * k1);
     float* l2d = reinterpret_cast<float*>(l1o + P * k1);
     uint32_t* l2c = reinterpret_cast<uint32_t*>(l2d + P * W);
-    float* sd = reinterpret_cast<float*>(l2c + P * W);
     const uint64_t q = blockIdx.x;
     const int tid = threadIdx.x;
 
@@ -124,32 +122,26 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
         const size_t o = q * P * W + pp * W + rank;
         l2d_out[o] = d;
         l2c_out[o] = code;
-        sd[pp * W + rank] = d;
-    }
-    __syncthreads();
-
-    if (tid == 0) {
-        uint8_t s0 = kSlopeOne, s1 = kSlopeOne;
-        if (P >= 2) s0 = (uint8_t)pick_slope(sd, sd + W, W, p.log108);
-        if (P == 4) s1 = (uint8_t)pick_slope(sd + 2 * W, sd + 3 * W, W, p.log108);
-        slope_out[q * 2] = s0;
-        slope_out[q * 2 + 1] = s1;
     }
 }
 
 size_t traverse_smem(const DevParams& p) {
-    return sizeof(float) * ((size_t)p.D + (size_t)p.L * p.k1 + 2ull * p.P * p.k1 + 3ull * p.P * p.W);
+    return sizeof(float) * ((size_t)p.D + (size_t)p.L * p.k1 + 2ull * p.P * p.k1 + 2ull * p.P * p.W);
 }
 
 void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                      cudaStream_t s) {
+    if (kernel_variant() != 1 && traverse_part_ok(p)) {
+        launch_traverse_part(p, queries, nq, ws, s);
+        return;
+    }
     // one thread per level-2 distance (P·w·k2 of them) keeps every thread busy in the long
     // sequential m-loop; 64..256 threads
     const uint32_t jobs = p.P * p.w * p.k2;
     const unsigned bs = jobs >= 256 ? 256u : (jobs <= 64 ? 64u : (unsigned)((jobs + 31) / 32 * 32));
 #define PQTG_TRAV(A, B)                                                                       \
     traverse_kernel<A, B><<<(unsigned)nq, bs, traverse_smem(p), s>>>(p, queries, ws.fine, ws.l2_dist, \
-                                                                     ws.l2_code, ws.slope)
+                                                                     ws.l2_code)
     if (p.k1 == 16 && p.k2 == 8) PQTG_TRAV(16, 8);
     else if (p.k1 == 32 && p.k2 == 16) PQTG_TRAV(32, 16);
     else if (p.k1 == 16 && p.k2 == 16) PQTG_TRAV(16, 16);
@@ -220,7 +212,7 @@ __device__ __forceinline__ uint64_t tuple_slot(const DevParams& p, uint64_t s, u
 template <int ITEMS, bool RESORT>
 __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const float* __restrict__ l2d_in,
                                                           const uint32_t* __restrict__ l2c_in,
-                                                          const uint8_t* __restrict__ slope_in,
+                                                          uint8_t* __restrict__ slope_out,
                                                           uint2* __restrict__ ranges,
                                                           uint32_t* __restrict__ nranges,
                                                           uint32_t* __restrict__ ncand,
@@ -256,9 +248,18 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         hkeys[i] = kEmptyKey;
         hvals[i] = 0xFFFFFFFFu;
     }
-    const uint32_t ta = slope_in[q * 2], tb = slope_in[q * 2 + 1];
-    if (tid == 0) s_maxord = 0;
+    __shared__ uint32_t s_slope[2];
+    if (tid == 0) {
+        s_maxord = 0;
+        uint32_t a, b;
+        query_slopes(p, l2d_in + q * PW_, a, b);  // pick_slope_table (binorder.cpp:52-65)
+        s_slope[0] = a;
+        s_slope[1] = b;
+        slope_out[q * 2] = (uint8_t)a;
+        slope_out[q * 2 + 1] = (uint8_t)b;
+    }
     __syncthreads();
+    const uint32_t ta = s_slope[0], tb = s_slope[1];
 
     const uint32_t budget = p.budget;
     const uint64_t total = p.total_tuples;
@@ -680,6 +681,8 @@ void configure_kernels(const DevParams& p, uint32_t) {
         set_rerank_attr<0, 2>();
         configure_rerank_ij();
         configure_binsel_fast();
+        configure_traverse_part();
+        configure_exact();
     });
     (void)p;
 }

@@ -242,6 +242,7 @@ namespace {
 struct DeviceCopy {
     pqtg_index* ix = nullptr;
     pqtg_workspace* ws = nullptr;
+    const VectorSet* db = nullptr;  // raw vectors currently on the device (exact re-rank)
     ~DeviceCopy() {
         pqtg_workspace_destroy(ws);
         pqtg_index_destroy(ix);
@@ -306,12 +307,18 @@ std::vector<QueryResult> knn_query_batch(const PqtIndex& index, const VectorSet&
     const std::size_t nq = queries.count();
     std::vector<QueryResult> results(nq);
     if (nq == 0 || k == 0 || index.size() == 0) return results;  // search.cpp:130-132
-    if (index.config.rerank_exact > 0) {
-        if (index.database)
-            throw std::runtime_error("pqt (GPU): exact re-ranking of attached raw vectors is not implemented");
-        warn_missing_database();
-    }
+    if (index.config.rerank_exact > 0 && !index.database) warn_missing_database();  // search.cpp:229-238
     DeviceCopy& d = device_copy(index);
+    {
+        // mirror PqtIndex::database on the device: the exact re-rank stage (search.cpp:229-249)
+        std::lock_guard<std::mutex> lock(g_upload_mu);
+        const VectorSet* want = index.config.rerank_exact > 0 ? index.database.get() : nullptr;
+        if (d.db != want) {
+            check(pqtg_index_attach_database(d.ix, want ? want->data.data() : nullptr, want ? want->count() : 0,
+                                             want ? want->dim : 0));
+            d.db = want;
+        }
+    }
     std::vector<std::uint32_t> ids(nq * k), counts(nq);
     std::vector<float> dists(nq * k);
     std::vector<pqtg_query_stats> stats(nq);

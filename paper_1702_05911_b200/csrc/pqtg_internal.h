@@ -67,6 +67,9 @@ struct DevParams {
     const uint8_t* codes;       // [shard positions][row_bytes]
     uint32_t code_ij;           // 1-byte codes hold (i << 4 | j) instead of the pair id (k1 <= 16)
     const float* c2ij;          // [L][256] d2[f][i][j] at i << 4 | j (code_ij only)
+    // exact re-rank (search.cpp:229-249): raw vectors n × D f32 in id order, or null
+    const float* db;
+    uint32_t rerank_exact;
 };
 
 struct DevIndex {
@@ -76,6 +79,7 @@ struct DevIndex {
     DevParams prm{};
     uint64_t bytes = 0;
     std::vector<void*> allocations;
+    float* db = nullptr;  // attached raw vectors (pqtg_index_attach_database)
     ~DevIndex();
 };
 
@@ -124,6 +128,12 @@ struct Workspace {
     uint32_t* d_counts = nullptr;
     pqtg_query_stats* d_stats = nullptr;
     uint64_t stage_k = 0;
+    // line-ranked prefix feeding the exact re-rank (grown on demand): [max_batch][ex_k]
+    uint32_t* ex_ids = nullptr;
+    float* ex_dists = nullptr;
+    uint32_t* ex_counts = nullptr;
+    uint64_t ex_k = 0;    // row stride (k') of the current search
+    uint64_t ex_cap = 0;  // rows' capacity in entries per query
     std::mutex mu;
     std::vector<void*> allocations;
     ~Workspace();
@@ -220,6 +230,16 @@ uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch);
 uint64_t binsel_hash_stride(const DevParams& p);
 void configure_binsel_fast();
 void launch_binsel_fast(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats, cudaStream_t s);
+// traverse.cu (one CTA per (query, part), TMA-staged level-2 blocks)
+bool traverse_part_ok(const DevParams& p);
+void configure_traverse_part();
+void launch_traverse_part(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
+                          cudaStream_t s);
+// exact.cu (exact re-rank of the line-ranked prefix with attached raw vectors)
+void configure_exact();
+void launch_exact(const DevParams& p, const float* queries, uint64_t nq, uint32_t kp, const uint32_t* line_ids,
+                  const uint32_t* line_counts, uint32_t k, uint32_t* ids, float* dists, uint32_t* counts,
+                  pqtg_query_stats* stats, cudaStream_t s);
 // 0 = pick the fastest kernel per stage, 1 = generic kernels only (parity tests run both)
 int kernel_variant();
 

@@ -112,6 +112,22 @@ class DeviceIndex:
     def handle(self):
         return self._h
 
+    def attach_database(self, rows: "np.ndarray | None") -> None:
+        """PqtIndex::attach_database (search.cpp:44-49): n × dim raw vectors (id order) for the
+        exact re-rank stage (search.cpp:229-249, when rerank_exact > 0); None detaches."""
+        if rows is None:
+            check(lib().pqtg_index_attach_database(self._h, None, 0, 0))
+            return
+        r = np.ascontiguousarray(rows, np.float32)
+        if r.ndim != 2:
+            raise ValueError("attach_database: vector set does not match index")
+        try:
+            check(lib().pqtg_index_attach_database(self._h, r.ctypes.data, r.shape[0], r.shape[1]))
+        except _abi.PqtgError as e:
+            if e.status == -1:  # BAD_DIM: std::invalid_argument in the reference
+                raise ValueError(str(e)) from None
+            raise
+
     @property
     def workspace(self):
         return self._ws

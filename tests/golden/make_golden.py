@@ -34,6 +34,12 @@ CASES = {
     "p2_sift": (dict(dim=128, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=512), 5000, 48, 100, 64, 16),
     "p4_gist": (dict(dim=96, p_tree=4, k1=16, k2=8, w=4, p_line=32, candidate_budget=512), 5000, 32, 50, 64, 17),
 }
+# raw vectors attached (keep_raw build): the exact re-rank stage (search.cpp:229-249) for two k,
+# one below rerank_exact and one above it
+EXACT_CASES = {
+    "p2_exact": (dict(dim=128, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=512, rerank_exact=48),
+                 5000, 40, (20, 80), 64, 18),
+}
 
 
 def make(name: str) -> None:
@@ -64,12 +70,29 @@ def make(name: str) -> None:
     print(name, "n", n, "bytes", path.stat().st_size, "mean C", stats[:, 1].mean(), "bins", stats[:, 0].mean())
 
 
+def make_exact(name: str) -> None:
+    cfgd, n, nq, ks, blobs, seed = EXACT_CASES[name]
+    cfg = PqtConfig(train_iters=10, seed=seed, **cfgd)
+    X = Ref.synth(n + nq, cfg.dim, blobs, 20.0, seed)
+    db, Q = X[:n], X[n:]
+    ref = Ref.build(db, db, cfg, threads=8, keep_raw=True)
+    path = HERE / f"{name}.pqt"
+    ref.save(str(path))  # the container never holds raw vectors (index_io.hpp:9-11)
+    out = dict(queries=Q, db=db, ks=np.array(ks))
+    for k in ks:
+        ids, dists, counts, stats = ref.knn(Q, k, threads=4)
+        assert (stats[:, 2] > 0).all(), "exact re-rank did not run"
+        out.update({f"ids_k{k}": ids, f"dists_k{k}": dists, f"counts_k{k}": counts, f"stats_k{k}": stats})
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, "n", n, "exact_evals", [int(out[f"stats_k{k}"][0, 2]) for k in ks])
+
+
 def main() -> None:
-    names = sys.argv[1:] or list(CASES)
+    names = sys.argv[1:] or list(CASES) + list(EXACT_CASES)
     for name in names:
-        make(name)
+        (make_exact if name in EXACT_CASES else make)(name)
     (HERE / "CASES.json").write_text(json.dumps({k: dict(config=v[0], n=v[1], nq=v[2], k=v[3], blobs=v[4], seed=v[5])
-                                                 for k, v in CASES.items()}, indent=1))
+                                                 for k, v in {**CASES, **EXACT_CASES}.items()}, indent=1))
 
 
 if __name__ == "__main__":

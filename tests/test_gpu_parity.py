@@ -171,3 +171,23 @@ def test_gpu_chunked_searches_identical(chunks):
            d_s.cpu().numpy().view(np.uint64))
     for x, y in zip(got, host):
         assert np.array_equal(x, y)
+
+
+def test_gpu_exact_rerank_matches_reference_golden():
+    """Raw vectors attached (pqtg_index_attach_database): K5 keeps the max(k, rerank_exact)
+    line-ranked prefix, K6 re-ranks it by exact l2_sq — bit-exact against the reference's
+    keep_raw build (search.cpp:229-249), for k below and above rerank_exact."""
+    from test_oracle_golden import _check_exact
+
+    g = load_golden("p2_exact")
+    dev = DeviceIndex(str(GOLDEN / "p2_exact.pqt"))
+    dev.attach_database(g["db"])
+    for k in g["ks"]:
+        _check_exact(dev.search(g["queries"], int(k)), g, int(k), f"k={k}")
+    with pytest.raises(ValueError):
+        dev.attach_database(g["db"][:, :-1])
+    dev.attach_database(None)
+    ids, d, c, s = dev.search(g["queries"], 20)
+    assert (s[:, 2] == 0).all()
+    want = Oracle(str(GOLDEN / "p2_exact.pqt")).knn(g["queries"], 20)
+    assert_same_results((ids, d, c, s), want, "detached")

@@ -67,3 +67,26 @@ def test_gpu_many_small_bins():
     want = Oracle(hix).knn(Q, 50)
     assert_same_results(got, want, "small bins")
     assert (got[3][:, 0] > 600).any()  # bins_visited: past the shared set's 512
+
+
+@pytest.mark.parametrize("k", [10, 100])
+def test_gpu_exact_rerank_built_index(k):
+    """A GPU-built 200k × 128 index with its raw vectors attached, rerank_exact = 64: the
+    exact stage against the C oracle with the same vectors attached."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=128, p_tree=2, k1=16, k2=8, w=4, p_line=32, train_iters=6, seed=21,
+                    candidate_budget=2048, rerank_exact=64)
+    X = builder.synth_clustered(200_000 + 64, cfg.dim, 256, 20.0, 21, device=dev)
+    db, Q = X[:200_000], X[200_000:].cpu().numpy()
+    hix = builder.build_index(db, db[:40_000], cfg)
+    rows = db.cpu().numpy()
+    g = DeviceIndex(hix)
+    g.attach_database(rows)
+    got = g.search(Q, k)
+    o = Oracle(hix)
+    o.attach_database(rows)
+    want = o.knn(Q, k)
+    assert_same_results(got, want, f"exact k={k}")
+    assert (got[3][:, 2] == np.minimum(max(64, k), got[3][:, 1])).all()

@@ -63,3 +63,30 @@ def test_truncated_container_is_rejected(tmp_path):
     (tmp_path / "m.pqt").write_bytes(bytes(bad))
     with pytest.raises(RuntimeError, match="magic"):
         Oracle(str(tmp_path / "m.pqt"))
+
+
+def _check_exact(got, g, k, ctx):
+    ids, dists, counts, stats = got
+    assert np.array_equal(counts, g[f"counts_k{k}"]), ctx
+    assert np.array_equal(stats, g[f"stats_k{k}"]), ctx  # exact_evals = min(max(rerank_exact, k), C)
+    for q in range(len(counts)):
+        c = counts[q]
+        assert np.array_equal(ids[q, :c], g[f"ids_k{k}"][q, :c]), f"{ctx} q={q}"
+        assert np.array_equal(dists[q, :c].view(np.uint32), g[f"dists_k{k}"][q, :c].view(np.uint32)), f"{ctx} q={q}"
+
+
+def test_oracle_exact_rerank_matches_golden():
+    """Raw vectors attached: the exact re-rank stage (search.cpp:229-249), k below and above
+    rerank_exact, against the reference's outputs on its keep_raw build."""
+    g = load_golden("p2_exact")
+    o = Oracle(str(GOLDEN / "p2_exact.pqt"))
+    assert o.config.rerank_exact == 48
+    o.attach_database(g["db"])
+    for k in g["ks"]:
+        _check_exact(o.knn(g["queries"], int(k), threads=4), g, int(k), f"k={k}")
+    # detached: the loaded-index path (no exact stage, exact_evals 0)
+    o.attach_database(None)
+    ids, dists, counts, stats = o.knn(g["queries"], 20, threads=4)
+    assert (stats[:, 2] == 0).all()
+    with pytest.raises(ValueError):
+        o.attach_database(g["db"][:-1])
