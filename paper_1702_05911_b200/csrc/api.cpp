@@ -8,7 +8,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -34,6 +36,8 @@ Workspace::~Workspace() {
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
     if (join) cudaEventDestroy(join);
+    if (fork) cudaEventDestroy(fork);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (aux_stream) cudaStreamDestroy(aux_stream);
     for (void* p : allocations) cudaFree(p);
@@ -51,7 +55,6 @@ WsSlice Workspace::slice(uint64_t q0) const {
     s.ncand = ncand + q0;
     s.ntuples = ntuples + q0;
     s.hash = hash ? hash + q0 * hash_stride : nullptr;
-    s.epoch = hash_epoch;
     return s;
 }
 
@@ -85,7 +88,42 @@ void ensure_staging(Workspace& ws, uint64_t k) {
         ws.d_ids = dev_alloc<uint32_t>(ws.allocations, ws.max_batch * k);
         ws.d_dists = dev_alloc<float>(ws.allocations, ws.max_batch * k);
         ws.stage_k = k;
+        ++ws.gen;
     }
+}
+
+// Chunk boundaries of a host-buffer sub-batch of b queries: chunk c+1's H2D copy hides under
+// chunk c's kernels. Two equal chunks measured best on B200 (tools/e2e_probe.py: growing
+// plans such as 1:3:4 expose less of the first copy but pay the latency-bound traversal and
+// bin-selection kernels once more). ws.chunks > 0 forces that many equal chunks;
+// PQTG_CHUNK_PLAN="w1,w2,..." sets relative chunk sizes (experiments).
+std::vector<uint64_t> host_chunks(const Workspace& ws, uint64_t b) {
+    std::vector<uint64_t> w;
+    if (ws.chunks) {
+        w.assign(ws.chunks, 1);
+    } else if (const char* env = std::getenv("PQTG_CHUNK_PLAN")) {
+        for (const char* c = env; *c;) {
+            char* end = nullptr;
+            const unsigned long v = std::strtoul(c, &end, 10);
+            if (end == c) break;
+            if (v) w.push_back(v);
+            c = *end ? end + 1 : end;
+        }
+    } else if (b >= 256) {
+        w = {1, 1};
+    }
+    if (w.empty()) w = {1};
+    uint64_t tot = 0;
+    for (uint64_t x : w) tot += x;
+    std::vector<uint64_t> bounds{0};
+    uint64_t acc = 0;
+    for (uint64_t x : w) {
+        acc += x;
+        const uint64_t e = b * acc / tot;
+        if (e > bounds.back()) bounds.push_back(e);
+    }
+    if (bounds.back() != b) bounds.push_back(b);
+    return bounds;
 }
 
 // k' of the line-ranked prefix the exact stage re-ranks: max(k, rerank_exact), at most the
@@ -105,21 +143,11 @@ void ensure_exact(Workspace& ws, uint32_t k) {
         ws.ex_ids = dev_alloc<uint32_t>(ws.allocations, ws.max_batch * kp);
         ws.ex_dists = dev_alloc<float>(ws.allocations, ws.max_batch * kp);
         ws.ex_cap = kp;
+        ++ws.gen;
     }
     ws.ex_k = kp;
 }
 
-// A fresh epoch for the workspace's visited-slot table before its regions are reused. On wrap
-// the table is cleared; `streams` are drained first so no in-flight chunk still uses it.
-void next_epoch(Workspace& ws, cudaStream_t s, cudaStream_t other) {
-    if (!ws.hash) return;
-    if (ws.hash_epoch == 0 || ws.hash_epoch >= 63) {
-        if (other) PQTG_CUDA_CHECK(cudaStreamSynchronize(other));
-        PQTG_CUDA_CHECK(cudaMemsetAsync(ws.hash, 0, ws.hash_words * sizeof(uint32_t), s));
-        ws.hash_epoch = 0;
-    }
-    ++ws.hash_epoch;  // 1..63; 0 marks cleared entries
-}
 
 // The three stages for queries [q0, q0 + nq) of the current sub-batch on stream s. Events
 // ev[0..3] bracket the stages when `timed` (the first chunk of a call).
@@ -314,6 +342,7 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         PQTG_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->own_stream, cudaStreamNonBlocking));
         PQTG_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->aux_stream, cudaStreamNonBlocking));
         PQTG_CUDA_CHECK(cudaEventCreateWithFlags(&ws->join, cudaEventDisableTiming));
+        PQTG_CUDA_CHECK(cudaEventCreateWithFlags(&ws->fork, cudaEventDisableTiming));
         for (auto& e : ws->ev) PQTG_CUDA_CHECK(cudaEventCreate(&e));
         const uint64_t B = max_batch;
         ws->fine = dev_alloc<float>(ws->allocations, B * p.L * p.k1);
@@ -340,6 +369,7 @@ int pqtg_workspace_set_chunks(pqtg_workspace* h, uint32_t chunks) {
     return guarded([&] {
         if (!h) throw Error{PQTG_ERR_ARG, "null argument"};
         h->ws->chunks = chunks;
+        ++h->ws->gen;
         return PQTG_OK;
     });
 }
@@ -407,7 +437,6 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         // the workspace's aux stream may still run a previous call's chunks on these slices
         PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
         PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));
-        next_epoch(ws, s, ws.aux_stream);
         ws.last_stream = s;
         ws.last_nq = nq;
         const uint64_t nch = ws.chunks ? ws.chunks : (nq >= 2048 ? 4 : (nq >= 256 ? 2 : 1));
@@ -451,46 +480,108 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         const uint64_t D = d.prm.D;
         cudaStream_t st[2] = {ws.own_stream, ws.aux_stream};
         ws.last_stream = ws.own_stream;
-        // Sub-batches of <= max_batch queries; each is cut into chunks that alternate between
-        // two streams, so chunk c's kernels overlap chunk c+1's H2D and chunk c-1's D2H.
-        for (uint64_t q0 = 0; q0 < nq || (nq == 0 && q0 == 0); q0 += ws.max_batch) {
-            const uint64_t b = std::min(ws.max_batch, nq - q0);
-            if (b == 0) {
-                run_chunk(d, ws, 0, ws.d_queries, 0, k, ws.d_ids, ws.d_dists, ws.d_counts, ws.d_stats, st[0], true);
-                ws.last_nq = 0;
-                break;
-            }
-            // reusing the slices: the other stream's chunks of the previous sub-batch must be done
-            PQTG_CUDA_CHECK(cudaEventRecord(ws.join, st[1]));
-            PQTG_CUDA_CHECK(cudaStreamWaitEvent(st[0], ws.join, 0));
-            next_epoch(ws, st[0], st[1]);
-            const uint64_t nch = ws.chunks ? ws.chunks : (b >= 1024 ? 4 : (b >= 256 ? 2 : 1));
-            const uint64_t per = (b + nch - 1) / nch;
-            for (uint64_t c = 0; c * per < b; ++c) {
-                const uint64_t c0 = c * per, cn = std::min(per, b - c0);
-                cudaStream_t s = st[c & 1];
-                if (c == 1) PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));  // after the epoch bump
-                if (c == 0) PQTG_CUDA_CHECK(cudaEventRecord(ws.join, s));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(ws.d_queries + c0 * D, queries + (q0 + c0) * D, cn * D * sizeof(float),
-                                                cudaMemcpyHostToDevice, s));
-                run_chunk(d, ws, c0, ws.d_queries + c0 * D, cn, k, ws.d_ids + c0 * std::max<uint32_t>(k, 1),
-                          ws.d_dists + c0 * std::max<uint32_t>(k, 1), ws.d_counts + c0, ws.d_stats + c0, s, c == 0);
-                if (k) {
-                    PQTG_CUDA_CHECK(cudaMemcpyAsync(ids + (q0 + c0) * k, ws.d_ids + c0 * k, cn * k * sizeof(uint32_t),
-                                                    cudaMemcpyDeviceToHost, s));
-                    PQTG_CUDA_CHECK(cudaMemcpyAsync(dists + (q0 + c0) * k, ws.d_dists + c0 * k, cn * k * sizeof(float),
-                                                    cudaMemcpyDeviceToHost, s));
+        auto enqueue = [&] {
+            // Sub-batches of <= max_batch queries; each is cut into chunks that alternate between
+            // two streams, so chunk c's kernels overlap chunk c+1's H2D and chunk c-1's D2H.
+            for (uint64_t q0 = 0; q0 < nq || (nq == 0 && q0 == 0); q0 += ws.max_batch) {
+                const uint64_t b = std::min(ws.max_batch, nq - q0);
+                if (b == 0) {
+                    run_chunk(d, ws, 0, ws.d_queries, 0, k, ws.d_ids, ws.d_dists, ws.d_counts, ws.d_stats, st[0], true);
+                    ws.last_nq = 0;
+                    break;
                 }
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(counts + q0 + c0, ws.d_counts + c0, cn * sizeof(uint32_t),
-                                                cudaMemcpyDeviceToHost, s));
-                if (stats)
-                    PQTG_CUDA_CHECK(cudaMemcpyAsync(stats + q0 + c0, ws.d_stats + c0, cn * sizeof(pqtg_query_stats),
+                // reusing the slices: the other stream's chunks of the previous sub-batch must be done
+                PQTG_CUDA_CHECK(cudaEventRecord(ws.join, st[1]));
+                PQTG_CUDA_CHECK(cudaStreamWaitEvent(st[0], ws.join, 0));
+                const std::vector<uint64_t> bounds = host_chunks(ws, b);
+                for (uint64_t c = 0; c + 1 < bounds.size(); ++c) {
+                    const uint64_t c0 = bounds[c], cn = bounds[c + 1] - c0;
+                    cudaStream_t s = st[c & 1];
+                    if (c == 1) PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));  // after the epoch bump
+                    if (c == 0) PQTG_CUDA_CHECK(cudaEventRecord(ws.join, s));
+                    PQTG_CUDA_CHECK(cudaMemcpyAsync(ws.d_queries + c0 * D, queries + (q0 + c0) * D, cn * D * sizeof(float),
+                                                    cudaMemcpyHostToDevice, s));
+                    run_chunk(d, ws, c0, ws.d_queries + c0 * D, cn, k, ws.d_ids + c0 * std::max<uint32_t>(k, 1),
+                              ws.d_dists + c0 * std::max<uint32_t>(k, 1), ws.d_counts + c0, ws.d_stats + c0, s, c == 0);
+                    if (k) {
+                        PQTG_CUDA_CHECK(cudaMemcpyAsync(ids + (q0 + c0) * k, ws.d_ids + c0 * k, cn * k * sizeof(uint32_t),
+                                                        cudaMemcpyDeviceToHost, s));
+                        PQTG_CUDA_CHECK(cudaMemcpyAsync(dists + (q0 + c0) * k, ws.d_dists + c0 * k, cn * k * sizeof(float),
+                                                        cudaMemcpyDeviceToHost, s));
+                    }
+                    PQTG_CUDA_CHECK(cudaMemcpyAsync(counts + q0 + c0, ws.d_counts + c0, cn * sizeof(uint32_t),
                                                     cudaMemcpyDeviceToHost, s));
+                    if (stats)
+                        PQTG_CUDA_CHECK(cudaMemcpyAsync(stats + q0 + c0, ws.d_stats + c0, cn * sizeof(pqtg_query_stats),
+                                                        cudaMemcpyDeviceToHost, s));
+                }
+                ws.last_nq = b;
             }
-            ws.last_nq = b;
+        };
+        // The whole search is one CUDA graph, replayed when the same arguments come back: one
+        // launch instead of ~10 API calls per chunk (PQTG_NO_GRAPH=1 disables).
+        static const bool no_graph = std::getenv("PQTG_NO_GRAPH") != nullptr;
+        auto pinned = [](const void* ptr) {  // graph memcpy nodes want page-locked host memory
+            if (!ptr) return true;
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            return a.type == cudaMemoryTypeHost;
+        };
+        if (no_graph || nq == 0 || !pinned(queries) || !pinned(ids) || !pinned(dists) || !pinned(counts) ||
+            !pinned(stats)) {
+            enqueue();
+            PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
+            PQTG_CUDA_CHECK(cudaStreamSynchronize(st[1]));
+            return PQTG_OK;
         }
+        const uint64_t key[12] = {(uint64_t)(uintptr_t)queries, nq, k, (uint64_t)(uintptr_t)ids,
+                                  (uint64_t)(uintptr_t)dists, (uint64_t)(uintptr_t)counts,
+                                  (uint64_t)(uintptr_t)stats, ws.gen, (uint64_t)kernel_variant(),
+                                  (uint64_t)(uintptr_t)d.db, d.prm.rerank_exact,
+                                  (uint64_t)std::hash<std::string>{}(std::getenv("PQTG_CHUNK_PLAN") ? std::getenv("PQTG_CHUNK_PLAN") : "")};
+        Workspace::GraphEntry* hit = nullptr;
+        for (auto& g : ws.graphs)
+            if (std::memcmp(g.key, key, sizeof(key)) == 0) hit = &g;
+        if (!hit) {
+            cudaGraph_t graph = nullptr;
+            PQTG_CUDA_CHECK(cudaStreamBeginCapture(st[0], cudaStreamCaptureModeThreadLocal));
+            try {
+                PQTG_CUDA_CHECK(cudaEventRecord(ws.fork, st[0]));
+                PQTG_CUDA_CHECK(cudaStreamWaitEvent(st[1], ws.fork, 0));
+                enqueue();
+                PQTG_CUDA_CHECK(cudaEventRecord(ws.fork, st[1]));
+                PQTG_CUDA_CHECK(cudaStreamWaitEvent(st[0], ws.fork, 0));
+            } catch (...) {
+                cudaStreamEndCapture(st[0], &graph);
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();
+                throw;
+            }
+            PQTG_CUDA_CHECK(cudaStreamEndCapture(st[0], &graph));
+            cudaGraphExec_t exec = nullptr;
+            const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+            cudaGraphDestroy(graph);
+            PQTG_CUDA_CHECK(e);
+            if (ws.graphs.size() >= 8) {  // evict the least recently used
+                auto lru = std::min_element(ws.graphs.begin(), ws.graphs.end(),
+                                            [](const auto& x, const auto& y) { return x.used < y.used; });
+                cudaGraphExecDestroy(lru->exec);
+                ws.graphs.erase(lru);
+            }
+            Workspace::GraphEntry g{};
+            std::memcpy(g.key, key, sizeof(key));
+            g.exec = exec;
+            ws.graphs.push_back(g);
+            hit = &ws.graphs.back();
+        } else {
+            ws.last_nq = nq - (nq - 1) / ws.max_batch * ws.max_batch;  // the last sub-batch
+        }
+        hit->used = ++ws.graph_clock;
+        PQTG_CUDA_CHECK(cudaGraphLaunch(hit->exec, st[0]));
         PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
-        PQTG_CUDA_CHECK(cudaStreamSynchronize(st[1]));
         return PQTG_OK;
     });
 }

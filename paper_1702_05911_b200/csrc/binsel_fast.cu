@@ -162,15 +162,15 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
 }
 
 // HASH: two tuples can reach one slot ((k1·k2)^P > H); first occurrences are then tracked in
-// a per-query region of a global, epoch-tagged open-addressing table (entries
-// epoch << 26 | slot, H <= 2^26), which needs no clearing between searches.
+// a shared open-addressing set (slot + 1, 0 = free); past half full the walker clears its
+// query's region of a global table sized for the whole budget and moves the set there.
 template <int P, bool HASH>
 __global__ void __launch_bounds__(kBsThreads, 4)
     binsel_fast_kernel(DevParams p, const uint32_t* __restrict__ l2c_in, const float* __restrict__ l2d_in,
                        uint8_t* __restrict__ slope_out,
                        uint2* __restrict__ ranges, uint32_t* __restrict__ nranges, uint32_t* __restrict__ ncand,
                        uint32_t* __restrict__ ntuples, pqtg_query_stats* __restrict__ stats, uint32_t ts_log2,
-                       uint32_t* __restrict__ ghash, uint32_t epoch, uint32_t W2ab) {
+                       uint32_t* __restrict__ ghash, uint32_t W2ab) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t W = p.W, PW = P * W;
     const uint32_t H = (uint32_t)p.H;
@@ -181,7 +181,6 @@ __global__ void __launch_bounds__(kBsThreads, 4)
     uint2* queue = reinterpret_cast<uint2*>(smem + lay.queue);
     const uint32_t TS = 1u << ts_log2;
     uint32_t* hkeys = HASH ? ghash + ((uint64_t)blockIdx.x << ts_log2) : nullptr;
-    const uint32_t etag = epoch << 26;
     __shared__ uint32_t wcnt[2][64];
     __shared__ uint32_t svis[HASH ? kVis : 1];
     __shared__ uint32_t s_nq[2], s_C, s_R, s_maxord;
@@ -282,12 +281,12 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                                     h = (h + 1) & (kVis - 1);
                                 }
                             } else {
-                                const uint32_t key = etag | e.y;
+                                const uint32_t key = e.y + 1u;
                                 uint32_t h = (e.y * 0x9E3779B1u) >> (32 - ts_log2);
                                 for (;;) {
                                     const uint32_t cur = hkeys[h];
-                                    if ((cur & 0xFC000000u) != etag) {  // stale epoch = empty
-                                        if (atomicCAS(hkeys + h, cur, key) == cur) break;
+                                    if (cur == 0u) {
+                                        if (atomicCAS(hkeys + h, 0u, key) == 0u) break;
                                         continue;  // lost a race on this entry; re-read it
                                     }
                                     if (cur == key) {
@@ -302,20 +301,13 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                         if (!spilled && nvis > kVis / 2) {
                             // the shared set is half full: move it to the per-query global
                             // table (sized for the whole budget) and continue there
+                            for (uint32_t i = lane; i < TS; i += 32) hkeys[i] = 0u;
                             __syncwarp();
                             for (uint32_t i = lane; i < kVis; i += 32) {
                                 const uint32_t v = svis[i];
                                 if (v == 0u) continue;
-                                const uint32_t sl = v - 1u, key = etag | sl;
-                                uint32_t h = (sl * 0x9E3779B1u) >> (32 - ts_log2);
-                                for (;;) {
-                                    const uint32_t cur = hkeys[h];
-                                    if ((cur & 0xFC000000u) != etag) {
-                                        if (atomicCAS(hkeys + h, cur, key) == cur) break;
-                                        continue;
-                                    }
-                                    h = (h + 1) & (TS - 1);
-                                }
+                                uint32_t h = ((v - 1u) * 0x9E3779B1u) >> (32 - ts_log2);
+                                while (atomicCAS(hkeys + h, 0u, v) != 0u) h = (h + 1) & (TS - 1);
                             }
                             __syncwarp();
                             spilled = true;
@@ -472,11 +464,10 @@ void configure_binsel_fast() {
 
 void launch_binsel_fast(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats, cudaStream_t s) {
     const BsConfig c = bs_config(p);
-    const uint32_t epoch = ws.epoch;  // bumped per search by the caller (api.cpp)
 #define PQTG_BS(PP, HH)                                                                                       \
     binsel_fast_kernel<PP, HH><<<(unsigned)nq, kBsThreads, c.smem, s>>>(p, ws.l2_code, ws.l2_dist, ws.slope, ws.ranges,     \
                                                                        ws.nranges, ws.ncand, ws.ntuples, stats, \
-                                                                       c.ts_log2, ws.hash, epoch, c.W2ab)
+                                                                       c.ts_log2, ws.hash, c.W2ab)
     if (p.P == 1) {
         PQTG_BS(1, false);
     } else if (p.P == 2) {

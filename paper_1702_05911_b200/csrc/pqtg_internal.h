@@ -94,7 +94,6 @@ struct WsSlice {
     uint32_t* ncand = nullptr;
     uint32_t* ntuples = nullptr;
     uint32_t* hash = nullptr;     // [q][hash_stride] visited-slot table (binsel_fast.cu)
-    uint32_t epoch = 0;
 };
 
 struct Workspace {
@@ -113,13 +112,22 @@ struct Workspace {
     uint32_t* nranges = nullptr;  // [B]
     uint32_t* ncand = nullptr;    // [B]
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
-    uint32_t* hash = nullptr;     // [B << ts_log2] epoch-tagged visited slots (binsel_fast.cu)
+    uint32_t* hash = nullptr;     // [B << ts_log2] visited slots, cleared on use (binsel_fast.cu)
     uint64_t hash_words = 0;
     uint64_t hash_stride = 0;     // words per query
-    uint32_t hash_epoch = 0;
     cudaStream_t aux_stream = nullptr;  // second stream of the pipelined searches
     uint32_t chunks = 0;                // sub-batch chunks per search (0 = automatic)
     cudaEvent_t join = nullptr;
+    cudaEvent_t fork = nullptr;         // graph capture: brings aux_stream into the capture
+    // pqtg_search replays: CUDA graphs of whole host-buffer searches, keyed by their arguments
+    struct GraphEntry {
+        uint64_t key[12];
+        cudaGraphExec_t exec;
+        uint64_t used;
+    };
+    std::vector<GraphEntry> graphs;
+    uint64_t graph_clock = 0;
+    uint64_t gen = 0;                   // bumped when buffers / settings a graph bakes in change
     WsSlice slice(uint64_t q0) const;
     // host-call staging (grown on demand)
     float* d_queries = nullptr;

@@ -191,3 +191,36 @@ def test_gpu_exact_rerank_matches_reference_golden():
     assert (s[:, 2] == 0).all()
     want = Oracle(str(GOLDEN / "p2_exact.pqt")).knn(g["queries"], 20)
     assert_same_results((ids, d, c, s), want, "detached")
+
+
+def test_gpu_pinned_search_graph_replays():
+    """pqtg_search on page-locked buffers runs as a replayed CUDA graph: same results as the
+    direct path, also when the buffers' contents change between replays."""
+    import torch
+
+    from paper_1702_05911_b200._abi import check, lib
+
+    path = str(GOLDEN / "p4_gist.pqt")
+    g = load_golden("p4_gist")
+    Q = g["queries"]
+    k = int(g["k"])
+    dev = DeviceIndex(path)
+    nq, dim = Q.shape
+    hq = torch.from_numpy(Q.copy()).pin_memory()
+    h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    h_d = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    h_c = torch.empty(nq, dtype=torch.int32).pin_memory()
+    h_s = torch.empty((nq, 3), dtype=torch.int64).pin_memory()
+
+    def run():
+        check(lib().pqtg_search(dev.handle, dev.workspace, hq.data_ptr(), nq, dim, k, h_ids.data_ptr(),
+                                h_d.data_ptr(), h_c.data_ptr(), h_s.data_ptr()))
+        return (h_ids.numpy().view(np.uint32).copy(), h_d.numpy().copy(), h_c.numpy().view(np.uint32).copy(),
+                h_s.numpy().view(np.uint64).copy())
+
+    want = Oracle(path).knn(Q, k)
+    for _ in range(3):  # capture, then replays
+        assert_same_results(run(), want, "pinned")
+    Q2 = Q[::-1].copy()
+    hq.copy_(torch.from_numpy(Q2))
+    assert_same_results(run(), Oracle(path).knn(Q2, k), "pinned, new contents")

@@ -60,7 +60,13 @@ def main():
         torch.cuda.synchronize()
         print(f"{name}: {t[0].elapsed_time(t[1]) / a.reps * 1000:.1f} us/step")
 
-    for chunks in (1, 2, 4, 8, 0):
+    import os
+
+    plans = [(c, "") for c in (1, 2, 4, 0)] + [(0, p) for p in ("1,1", "1,3", "1,3,4", "1,2,5", "1,1,2", "1,2,3,6")]
+    for chunks, plan in plans:
+        os.environ["PQTG_CHUNK_PLAN"] = plan
+        if not plan:
+            del os.environ["PQTG_CHUNK_PLAN"]
         dev.set_chunks(chunks)
         for b in range(4):
             dev.search_device(d_q[b].data_ptr(), nq, k, d_ids.data_ptr(), d_d.data_ptr(), d_c.data_ptr(),
@@ -91,7 +97,7 @@ def main():
         for r in range(a.reps):
             host(r % 4)
         bb = (time.perf_counter() - t0) / a.reps
-        print(f"chunks={chunks}: device {dms * 1000:.1f} us/step ({nq / dms * 1000 / 1e6:.2f} Mq/s); "
+        print(f"chunks={chunks} plan={plan or '-'}: device {dms * 1000:.1f} us/step ({nq / dms * 1000 / 1e6:.2f} Mq/s); "
               f"host call median {np.median(ts) * 1e6:.1f} us min {np.min(ts) * 1e6:.1f} us "
               f"({nq / np.median(ts) / 1e6:.2f} Mq/s); back-to-back {bb * 1e6:.1f} us")
 
