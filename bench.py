@@ -51,6 +51,10 @@ WORKLOADS = {
     # a DEEP-shaped single-GPU config at 10M (configs[2] shape at 1/10 scale)
     "deep10m": dict(config=dict(dim=96, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=4096),
                     n=10_000_000, nq=10000, k=100, blobs=10_000, sigma=20.0, ntrain=100_000),
+    # BASELINE.json configs[2]: DEEP1B-shaped 100M x 96-D, HBM-resident on one B200 (H = 2^26);
+    # built in memory on the GPU (not cached: the container would be ~7 GB)
+    "deep100m": dict(config=dict(dim=96, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=4096),
+                     n=100_000_000, nq=10000, k=100, blobs=100_000, sigma=20.0, ntrain=100_000, cache=False),
 }
 CACHE = Path(os.environ.get("PQTG_BENCH_CACHE", "/tmp/pqtg_bench"))
 
@@ -75,7 +79,8 @@ def make_workload(name: str, seed: int, device: int, batches: int):
     wl = WORKLOADS[name]
     ipath, qpath = workload_files(name, seed)
     nq_pool = wl["nq"] * batches
-    if ipath.exists() and qpath.exists() and np.load(qpath, mmap_mode="r").shape[0] >= nq_pool:
+    cache = wl.get("cache", True)
+    if cache and ipath.exists() and qpath.exists() and np.load(qpath, mmap_mode="r").shape[0] >= nq_pool:
         log(f"[bench] loading cached {ipath}")
         return HostIndex.load(str(ipath)), np.load(qpath)[:nq_pool]
     t0 = time.time()
@@ -90,10 +95,11 @@ def make_workload(name: str, seed: int, device: int, batches: int):
     q = Q.cpu().numpy()
     del X, db, Q, train
     torch.cuda.empty_cache()
-    tmp = ipath.with_suffix(".tmp")
-    hix.save(str(tmp))
-    os.replace(tmp, ipath)
-    np.save(qpath, q)
+    if cache:
+        tmp = ipath.with_suffix(".tmp")
+        hix.save(str(tmp))
+        os.replace(tmp, ipath)
+        np.save(qpath, q)
     log(f"[bench] built {name} index in {time.time() - t0:.1f}s")
     return hix, q
 
@@ -174,6 +180,19 @@ def algorithmic_bytes(hix, counters, stats, k: int):
     survey = float(np.sum(4 * c.dim + 16 * T_q + 4 * C_q + C_q * c.p_line * (1 + pw) + 8 * k))
     return {"traverse": float(trav), "binsel": binsel, "rerank": rerank, "survey_Bq_total": survey,
             "T_q": float(T_q.mean()), "C_q": float(C_q.mean()), "bins_q": float(bins.mean())}
+
+
+def measured_traffic(workload: str, stage: str, nq: int):
+    """DRAM bytes per launch of `stage` from the committed ncu capture (profiles/traffic.json,
+    tools/ncu_traffic.py), scaled to this run's queries per launch; None if not captured."""
+    p = REPO / "profiles" / "traffic.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text())
+    k = d.get("kernels", {}).get(stage)
+    if d.get("workload") != workload or not k:
+        return None, None
+    return k["dram_bytes_per_launch"] * nq / d["queries_per_launch"], f"profiles/traffic.json ({d['report']})"
 
 
 def peaks():
@@ -315,6 +334,9 @@ def main():
     ap.add_argument("--no-recall", action="store_true")
     ap.add_argument("--chunks", type=int, default=0,
                     help="pieces per batch overlapped on two streams (0 auto, 1 off)")
+    ap.add_argument("--shard", action="store_true",
+                    help="shard the index's positions over the ranks (NCCL broadcast + all-gather + "
+                         "merge; sharded.py) instead of one replica per rank")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -345,9 +367,18 @@ def main():
         if rank != 0:
             hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * world)
     lib().pqtg_set_kernel_variant(args.variant)
-    dev = DeviceIndex(hix, device=local, max_batch=nq)
+    if args.shard:
+        from paper_1702_05911_b200.sharded import ShardedIndex
+
+        sh = ShardedIndex(hix, device=local, max_batch=nq)
+        dev = sh.local
+        # every rank searches the same batches (rank 0's, broadcast inside the timed step)
+        batches = [Qpool[b * nq:(b + 1) * nq] for b in range(args.batches)]
+    else:
+        dev = DeviceIndex(hix, device=local, max_batch=nq)
+        batches = [Qpool[(rank * args.batches + b) * nq:(rank * args.batches + b + 1) * nq]
+                   for b in range(args.batches)]
     dev.set_chunks(args.chunks)
-    batches = [Qpool[(rank * args.batches + b) * nq:(rank * args.batches + b + 1) * nq] for b in range(args.batches)]
     d_q = [torch.from_numpy(b).cuda() for b in batches]
     d_ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
     d_dists = torch.empty((nq, k), dtype=torch.float32, device="cuda")
@@ -357,6 +388,9 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(b):
+        if args.shard:
+            sh.search(d_q[b], k, d_ids, d_dists, d_counts, d_stats)
+            return
         dev.search_device(d_q[b].data_ptr(), nq, k, d_ids.data_ptr(), d_dists.data_ptr(), d_counts.data_ptr(),
                           d_stats.data_ptr(), stream.cuda_stream)
 
@@ -392,7 +426,8 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * nq * args.steps / (ms_max / 1000.0)
+    jobs = 1 if args.shard else world  # sharded: all ranks share each batch
+    value = jobs * nq * args.steps / (ms_max / 1000.0)
 
     # ---- per-kernel times (unchunked launches: one launch per stage per step)
     dev.set_chunks(1)
@@ -415,6 +450,15 @@ def main():
     L = lib()
 
     def host_step(b):
+        if args.shard:  # H2D of the batch, sharded search, D2H of the merged top-k
+            d_q[b].copy_(hq[b], non_blocking=True)
+            sh.search(d_q[b], k, d_ids, d_dists, d_counts, d_stats)
+            h_ids.copy_(d_ids, non_blocking=True)
+            h_dists.copy_(d_dists, non_blocking=True)
+            h_counts.copy_(d_counts, non_blocking=True)
+            h_stats.copy_(d_stats, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return
         rc = L.pqtg_search(dev.handle, dev.workspace, hq[b].data_ptr(), nq, hix.config.dim, k, h_ids.data_ptr(),
                            h_dists.data_ptr(), h_counts.data_ptr(), h_stats.data_ptr())
         assert rc == 0, L.pqtg_last_error()
@@ -433,7 +477,7 @@ def main():
     tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    e2e_value = world * nq * e2e_steps / float(tt.item())
+    e2e_value = jobs * nq * e2e_steps / float(tt.item())
     h2d = nq * hix.config.dim * 4
     d2h = nq * k * 8 + nq * 4 + nq * 24
 
@@ -449,11 +493,12 @@ def main():
     ab = {kk: float(np.mean([a[kk] for a in abytes])) for kk in abytes[0]}
     dom = int(np.argmax(stage_mean[:3]))
     peak, peak_src = peaks()
+    traffic, traffic_src = measured_traffic(args.workload, names[dom], nq)
     achieved = ab[names[dom]] / (stage_mean[dom] / 1000.0) / 1e9
     roofline = {"bound": "hbm", "kernel": {"traverse": "traverse_kernel", "binsel": "binsel_kernel",
                                            "rerank": "rerank_kernel"}[names[dom]],
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_source": peak_src, "traffic": None,
+                "peak_source": peak_src, "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": ab[names[dom]],
                 "stage_ms": {n: float(v) for n, v in zip(names, stage_mean[:3])},
                 "stage_share": {n: float(v / stage_mean[:3].sum()) for n, v in zip(names, stage_mean[:3])},
@@ -487,11 +532,12 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic clustered blobs (synth_clustered distribution), GPU-built PQT index",
         "config": {"workload": args.workload, **wl["config"], "n": wl["n"], "queries_per_step": nq, "k": k,
                    "l2": "flushed between timed steps (256 MiB write)" if not args.no_flush else "not flushed",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": (f"position shards x{world} (NCCL broadcast + all-gather + merge)"
+                                   if args.shard else f"replicas x{world}")},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": gpu_launches(hix, nq, args.chunks) * args.steps,
         "roofline": roofline,
