@@ -55,6 +55,7 @@ WsSlice Workspace::slice(uint64_t q0) const {
     s.ncand = ncand + q0;
     s.ntuples = ntuples + q0;
     s.hash = hash ? hash + q0 * hash_stride : nullptr;
+    s.scr = scr ? scr + q0 * p.P * p.scr_nj : nullptr;
     return s;
 }
 
@@ -206,8 +207,8 @@ extern "C" {
 int pqtg_abi_version(void) { return PQTG_ABI_VERSION; }
 
 int pqtg_set_kernel_variant(int variant) {
-    if (variant != 0 && variant != 1) {
-        set_error("variant must be 0 (auto) or 1 (generic)");
+    if (variant < 0 || variant > 2) {
+        set_error("variant must be 0 (auto), 1 (generic) or 2 (auto with the tensor-core level-2 screen)");
         return PQTG_ERR_ARG;
     }
     g_variant.store(variant);
@@ -356,6 +357,9 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         ws->hash_words = binsel_fast_ok(p) ? binsel_hash_words(p, B) : 0;
         ws->hash_stride = ws->hash_words ? binsel_hash_stride(p) : 0;
         if (ws->hash_words) ws->hash = dev_alloc<uint32_t>(ws->allocations, ws->hash_words);
+        if (screen_ok(p)) {
+            ws->scr = dev_alloc<float>(ws->allocations, B * p.P * p.scr_nj);
+        }
         auto* h = new pqtg_workspace;
         h->ws = std::move(ws);
         *out = h;

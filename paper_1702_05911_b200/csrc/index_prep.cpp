@@ -279,6 +279,47 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
         p.l2_t = upload(*ix, l2_t.data(), l2_t.size());
     }
 
+    // --- tensor-core level-2 screen (screen.cu). Per part p: mu_p = the mean child; each child
+    // c of parent i as c'' = c - mu_i (mu_i = the level-1 centroid), K-major rows [P][nj][kpad]
+    // zero-padded; kc = (mu_i - mu_p) . c'' and |c''|^2 (fp64 sums). The screen then uses
+    // |y - c|^2 = |y - mu_i|^2 - 2 ((y - mu_p) . c'' - kc) + |c''|^2 with small operands.
+    {
+        const uint32_t nj0 = k1 * k2;
+        const uint32_t nt = nj0 >= 256 ? 256u : 64u;  // screen.cu's N tile
+        const uint32_t nj = (nj0 + nt - 1) / nt * nt;
+        const uint32_t kpad = (m + 15) / 16 * 16;
+        p.scr_nj = nj;
+        p.scr_kpad = kpad;
+        std::vector<float> crow((size_t)P * nj * kpad, 0.0f), mu((size_t)P * kpad, 0.0f), cn((size_t)P * nj, 0.0f),
+            kc((size_t)P * nj, 0.0f);
+        for (uint32_t pp = 0; pp < P; ++pp) {
+            const float* l2 = src.level2 + (size_t)pp * nj0 * m;  // [k1][k2][m] = [nj0][m]
+            const float* l1 = src.level1 + (size_t)pp * k1 * m;   // [k1][m]
+            std::vector<double> mup(m, 0.0);
+            for (uint32_t t = 0; t < m; ++t) {
+                for (uint32_t j = 0; j < nj0; ++j) mup[t] += l2[(size_t)j * m + t];
+                mup[t] /= nj0;
+                mu[(size_t)pp * kpad + t] = (float)mup[t];
+            }
+            for (uint32_t j = 0; j < nj0; ++j) {
+                const float* par = l1 + (size_t)(j / k2) * m;
+                double nrm = 0.0, kk = 0.0;
+                for (uint32_t t = 0; t < m; ++t) {
+                    const float v = (float)((double)l2[(size_t)j * m + t] - (double)par[t]);
+                    crow[((size_t)pp * nj + j) * kpad + t] = v;
+                    nrm += (double)v * v;
+                    kk += ((double)par[t] - (double)mu[(size_t)pp * kpad + t]) * v;
+                }
+                cn[(size_t)pp * nj + j] = (float)nrm;
+                kc[(size_t)pp * nj + j] = (float)kk;
+            }
+        }
+        p.scr_c = upload(*ix, crow.data(), crow.size());
+        p.scr_mu = upload(*ix, mu.data(), mu.size());
+        p.scr_cn = upload(*ix, cn.data(), cn.size());
+        p.scr_kc = upload(*ix, kc.data(), kc.size());
+    }
+
     // --- pair enumeration and per-pair d2
     {
         std::vector<uint32_t> pairs(npairs);

@@ -131,6 +131,13 @@ size_t traverse_smem(const DevParams& p) {
 
 void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                      cudaStream_t s) {
+    if (kernel_variant() == 2 && ws.scr && screen_ok(p)) {
+        // north-star kernel (1): tcgen05 screen of every child, exact residual check per part
+        // (opt-in: at the benchmark shapes the all-exact per-part traversal is faster)
+        launch_screen_gemm(p, queries, nq, ws.scr, s);
+        launch_traverse_screen(p, queries, nq, ws.scr, ws, s);
+        return;
+    }
     if (kernel_variant() != 1 && traverse_part_ok(p)) {
         launch_traverse_part(p, queries, nq, ws, s);
         return;
@@ -633,7 +640,7 @@ size_t rerank_smem(const DevParams& p, uint32_t k) {
 
 void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids,
                    float* dists, uint32_t* counts, cudaStream_t s) {
-    if (kernel_variant() == 0 && rerank_ij_ok(p, k)) {
+    if (kernel_variant() != 1 && rerank_ij_ok(p, k)) {
         launch_rerank_ij(p, nq, k, ws, ids, dists, counts, s);
         return;
     }
@@ -683,6 +690,7 @@ void configure_kernels(const DevParams& p, uint32_t) {
         configure_binsel_fast();
         configure_traverse_part();
         configure_exact();
+        configure_screen();
     });
     (void)p;
 }

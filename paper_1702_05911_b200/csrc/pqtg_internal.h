@@ -70,6 +70,12 @@ struct DevParams {
     // exact re-rank (search.cpp:229-249): raw vectors n × D f32 in id order, or null
     const float* db;
     uint32_t rerank_exact;
+    // tensor-core level-2 screen (screen.cu)
+    const float* scr_c;         // [P][scr_nj][scr_kpad] children minus their parent: c'' = c - mu_i
+    const float* scr_mu;        // [P][scr_kpad] the part's mean child mu_p (query centring)
+    const float* scr_cn;        // [P][scr_nj] |c''|^2
+    const float* scr_kc;        // [P][scr_nj] (mu_i - mu_p) . c''
+    uint32_t scr_nj, scr_kpad;  // k1·k2 padded to the N tile; m padded to 16
 };
 
 struct DevIndex {
@@ -94,6 +100,7 @@ struct WsSlice {
     uint32_t* ncand = nullptr;
     uint32_t* ntuples = nullptr;
     uint32_t* hash = nullptr;     // [q][hash_stride] visited-slot table (binsel_fast.cu)
+    float* scr = nullptr;         // [q][P][scr_nj] tensor-core dot products (screen.cu)
 };
 
 struct Workspace {
@@ -112,6 +119,7 @@ struct Workspace {
     uint32_t* nranges = nullptr;  // [B]
     uint32_t* ncand = nullptr;    // [B]
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
+    float* scr = nullptr;         // [B][P][scr_nj] (y - mu_p) . c'' on the tensor cores (screen.cu)
     uint32_t* hash = nullptr;     // [B << ts_log2] visited slots, cleared on use (binsel_fast.cu)
     uint64_t hash_words = 0;
     uint64_t hash_stride = 0;     // words per query
@@ -248,6 +256,12 @@ void configure_exact();
 void launch_exact(const DevParams& p, const float* queries, uint64_t nq, uint32_t kp, const uint32_t* line_ids,
                   const uint32_t* line_counts, uint32_t k, uint32_t* ids, float* dists, uint32_t* counts,
                   pqtg_query_stats* stats, cudaStream_t s);
+// screen.cu (tcgen05 level-2 screen + certified exact residual check)
+bool screen_ok(const DevParams& p);
+void configure_screen();
+void launch_screen_gemm(const DevParams& p, const float* queries, uint64_t nq, float* out, cudaStream_t s);
+void launch_traverse_screen(const DevParams& p, const float* queries, uint64_t nq, const float* scr,
+                            const WsSlice& ws, cudaStream_t s);
 // 0 = pick the fastest kernel per stage, 1 = generic kernels only (parity tests run both)
 int kernel_variant();
 
