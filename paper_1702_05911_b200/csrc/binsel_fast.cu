@@ -201,12 +201,11 @@ __global__ void __launch_bounds__(kBsThreads, 4)
         s_C = 0;
         s_R = 0;
         s_maxord = 0;
-        uint32_t a, b;
-        query_slopes(p, l2d_in + q * PW, a, b);  // pick_slope_table (binorder.cpp:52-65)
-        s_slope[0] = a;
-        s_slope[1] = b;
-        slope_out[q * 2] = (uint8_t)a;
-        slope_out[q * 2 + 1] = (uint8_t)b;
+    }
+    if ((tid & 31) == 0 && tid < 64) {  // pick_slope_table (binorder.cpp:52-65), one pair per warp
+        const uint32_t pr = tid >> 5, t = query_slope(p, l2d_in + q * PW, pr);
+        s_slope[pr] = t;
+        slope_out[q * 2 + pr] = (uint8_t)t;
     }
     __syncthreads();
     const uint32_t ta = s_slope[0], tb = s_slope[1];
@@ -231,7 +230,9 @@ __global__ void __launch_bounds__(kBsThreads, 4)
     // stream positions fit 32 bits (BinStream::total is capped at 2^32 - 2 at index build)
     const uint32_t total32 = (uint32_t)total;
     uint32_t base = 0;                      // first stream position of the pass being filtered
-    uint32_t nit = 1;                       // items per filter thread: 1 on the first pass, then 8
+    // items per filter thread: 1 on the first pass, then 8; P = 4 streams reach thousands of
+    // tuples per query, so they start with full passes
+    uint32_t nit = P == 4 ? kMaxItems : 1;
     uint32_t prev_n = 0;                    // queued tuples of the previous pass
     uint32_t nvis = 0;                      // walker: slots inserted in the visited set
     bool spilled = false;                   // walker: visited set moved to global memory

@@ -28,38 +28,46 @@ __device__ __forceinline__ float unorderable(uint32_t o) {
     return __uint_as_float(u);
 }
 
-// pick_slope_table (binorder.cpp:52-65): fp64 gaps, nearest slope 1.08^k in log space.
+// pick_slope_table (binorder.cpp:52-65): fp64 gaps, nearest slope 1.08^k in log space,
+// k = clamp(lround(log(gb / ga) / log(1.08)), -5, 4). The fp64 log is a long dependent
+// sequence on one thread, so a fp32 estimate decides whenever it is provably on the same side
+// of every rounding boundary: its error (fp32 logf <= 2 ulp plus the ratio's rounding) is
+// below 2e-4 for |log ratio| <= 64, and the estimate must be >= 1e-3 from a half-integer or
+// beyond the clamp; otherwise the reference's fp64 formula runs.
 __device__ inline uint32_t pick_slope(const float* a, const float* b, uint32_t len, double log108) {
     if (len < 2) return kSlopeOne;
     const double ga = (double)a[1] - (double)a[0];
     const double gb = (double)b[1] - (double)b[0];
     if (!(ga > 0.0) || !(gb > 0.0)) return kSlopeOne;
     const double ratio = gb / ga;
-    long long k = llround(log(ratio) / log108);
+    const float rf = (float)ratio;
+    const float lf = logf(rf);
+    long long k;
+    if (rf > 0.0f && rf < 3.0e38f && fabsf(lf) <= 64.0f) {
+        const float kf = lf * (float)(1.0 / log108);
+        const float frac = fabsf(kf - truncf(kf));  // distance pattern to the .5 boundary
+        if (kf <= -6.0f || kf >= 5.0f) return kf < 0.0f ? 0u : 9u;  // clamped either way
+        if (fabsf(frac - 0.5f) >= 1e-3f) {
+            k = (long long)roundf(kf);  // round half away from zero, as lround
+            k = k < -5 ? -5 : (k > 4 ? 4 : k);
+            return (uint32_t)(k + 5);
+        }
+    }
+    k = llround(log(ratio) / log108);
     k = k < -5 ? -5 : (k > 4 ? 4 : k);
     return (uint32_t)(k + 5);
 }
 
-// pick_slope_table for a query's pair streams from its sorted level-2 lists l2d[P][W] in
-// global memory: (lists 0,1) and, for P = 4, (lists 2,3) (binorder.cpp:52-65, :237).
-__device__ inline void query_slopes(const DevParams& p, const float* l2d, uint32_t& ta, uint32_t& tb) {
-    ta = kSlopeOne;
-    tb = kSlopeOne;
+// pick_slope_table for one of a query's pair streams from its sorted level-2 lists l2d[P][W]
+// in global memory: pair 0 = lists (0,1), pair 1 = lists (2,3) when P = 4 (binorder.cpp:52-65,
+// :237); kSlopeOne for the streams a query does not have.
+__device__ inline uint32_t query_slope(const DevParams& p, const float* l2d, uint32_t pair) {
     const uint32_t W = p.W;
-    if (p.P < 2 || W < 2) return;
-    float a[2], b[2];
-    a[0] = l2d[0];
-    a[1] = l2d[1];
-    b[0] = l2d[W];
-    b[1] = l2d[W + 1];
-    ta = pick_slope(a, b, W, p.log108);
-    if (p.P == 4) {
-        a[0] = l2d[2 * W];
-        a[1] = l2d[2 * W + 1];
-        b[0] = l2d[3 * W];
-        b[1] = l2d[3 * W + 1];
-        tb = pick_slope(a, b, W, p.log108);
-    }
+    if (p.P < 2 || W < 2 || (pair == 1 && p.P != 4)) return kSlopeOne;
+    const float* la = l2d + (size_t)(2 * pair) * W;
+    const float* lb = la + W;
+    const float a[2] = {la[0], la[1]}, b[2] = {lb[0], lb[1]};
+    return pick_slope(a, b, W, p.log108);
 }
 
 // ------------------------------------------------------------------ bulk async copies

@@ -256,14 +256,11 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         hvals[i] = 0xFFFFFFFFu;
     }
     __shared__ uint32_t s_slope[2];
-    if (tid == 0) {
-        s_maxord = 0;
-        uint32_t a, b;
-        query_slopes(p, l2d_in + q * PW_, a, b);  // pick_slope_table (binorder.cpp:52-65)
-        s_slope[0] = a;
-        s_slope[1] = b;
-        slope_out[q * 2] = (uint8_t)a;
-        slope_out[q * 2 + 1] = (uint8_t)b;
+    if (tid == 0) s_maxord = 0;
+    if ((tid & 31) == 0 && tid < 64) {  // pick_slope_table (binorder.cpp:52-65), one pair per warp
+        const uint32_t pr = tid >> 5, t = query_slope(p, l2d_in + q * PW_, pr);
+        s_slope[pr] = t;
+        slope_out[q * 2 + pr] = (uint8_t)t;
     }
     __syncthreads();
     const uint32_t ta = s_slope[0], tb = s_slope[1];
