@@ -12,7 +12,7 @@
 //                                       (linequant.hpp:85), built once per query;
 //     part = (b2 + (λ·λ)·c2) + λ·E      exactly linequant.hpp:83-85's rounding.
 // Shared memory: T (L × 2 KB), fine (L × 64 B), candidate keys, range offsets (cached up to
-// kRangeCache, else read from global memory); 512 threads per CTA, two CTAs per SM.
+// kRangeCache, else read from global memory); ij_threads(L) threads per CTA.
 #include <cstdint>
 
 #include "common.cuh"
@@ -25,7 +25,10 @@ using namespace dev;
 
 namespace {
 
-constexpr int kIjThreads = 512;
+// threads per CTA: 512, two CTAs (queries) per SM. (1024-thread CTAs, one query per SM, cut the
+// last wave's idle time but measured 20% slower on B200: MIO-queue stalls.)
+__host__ __device__ constexpr int ij_threads(int L) { return L >= 64 ? 512 : 512; }
+constexpr int kScanItems = 8;  // rid entries per thread per scan tile
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // no id: the candidate belongs to another shard
 constexpr uint32_t kRangeCache = 512;       // ranges whose (start − offset) is kept in smem
 
@@ -57,7 +60,8 @@ __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint3
     // rid: u16 range index per candidate, padded to whole 4096-candidate scan tiles; after
     // the candidate loop the same bytes hold the select histogram and sel
     l.rid = o;
-    const size_t rid_bytes = al16((size_t)((budget + 4095) / 4096) * 4096 * 2);
+    const size_t tile = (size_t)kScanItems * ij_threads((int)L);
+    const size_t rid_bytes = al16((budget + tile - 1) / tile * tile * 2);
     const size_t sel_bytes = ((size_t)4 << kSelBits) + (size_t)sel_cap * 8;
     l.sel = o + ((size_t)4 << kSelBits);
     o += rid_bytes > sel_bytes ? rid_bytes : sel_bytes;
@@ -69,11 +73,12 @@ __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint3
 
 // rid[j] = index of the range holding candidate j, for j < C: rid is zero except
 // rid[offset of range r] = r, so an inclusive max-scan gives it (range offsets increase
-// with r). 512 threads × 8 consecutive u16 per 4096-candidate tile.
+// with r). TH threads × 8 consecutive u16 per scan tile.
+template <int TH>
 __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wmax) {
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t carry = 0;
-    for (uint32_t base = 0; base < C; base += 8 * kIjThreads) {
+    for (uint32_t base = 0; base < C; base += kScanItems * TH) {
         uint4* v4 = reinterpret_cast<uint4*>(rid + base) + tid;
         uint4 v = *v4;
         uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -101,7 +106,7 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 #pragma unroll
         for (int i = 0; i < 8; ++i) r[i] = max(before, e[i]);
         *v4 = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), r[4] | (r[5] << 16), r[6] | (r[7] << 16));
-        for (uint32_t i = 0; i < kIjThreads / 32; ++i) carry = max(carry, wmax[i]);
+        for (uint32_t i = 0; i < TH / 32; ++i) carry = max(carry, wmax[i]);
         __syncthreads();
     }
 }
@@ -109,7 +114,7 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 }  // namespace
 
 template <int LT>
-__global__ void __launch_bounds__(kIjThreads, LT >= 64 ? 1 : 2)
+__global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
@@ -124,6 +129,7 @@ __global__ void __launch_bounds__(kIjThreads, LT >= 64 ? 1 : 2)
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0).rid);  // aliases rid
     uint16_t* rid = reinterpret_cast<uint16_t*>(smem + ij_layout(LT, 0, 0).rid);
     uint32_t* delta = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0).delta);
+    constexpr int kIjThreads = ij_threads(LT);
     __shared__ uint32_t wmax[kIjThreads / 32];
     __shared__ uint32_t s_count;
     __shared__ TopkShared s_sel;
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(kIjThreads, LT >= 64 ? 1 : 2)
         const uint32_t f = i >> 4, c = i & 15;
         fine[i] = c < k1 ? fine_in[q * LT * k1 + f * k1 + c] : 0.0f;
     }
-    const uint32_t Cpad = (C + 8 * kIjThreads - 1) / (8 * kIjThreads) * (8 * kIjThreads);
+    const uint32_t Cpad = (C + kScanItems * kIjThreads - 1) / (kScanItems * kIjThreads) * (kScanItems * kIjThreads);
     for (uint32_t i = tid; i < Cpad / 2; i += blockDim.x) reinterpret_cast<uint32_t*>(rid)[i] = 0;
     const bool cached = R <= kRangeCache;
     if (tid == 0) {
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kIjThreads, LT >= 64 ? 1 : 2)
         }
     }
     __syncthreads();
-    range_index_scan(rid, C, wmax);
+    range_index_scan<kIjThreads>(rid, C, wmax);
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     const bool sharded = p.shard_hi > p.shard_lo;
@@ -305,7 +311,7 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     const uint32_t cap = ij_sel_cap(kk);
     const size_t sm = ij_smem(p, k);
 #define PQTG_IJ(LT)                                                                                         \
-    rerank_ij_kernel<LT><<<(unsigned)nq, kIjThreads, sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \
+    rerank_ij_kernel<LT><<<(unsigned)nq, ij_threads(LT), sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \
                                                              ws.ncand, ids, dists, counts)
     switch (p.L) {
     case 16: PQTG_IJ(16); break;
