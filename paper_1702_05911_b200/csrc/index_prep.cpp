@@ -364,19 +364,22 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
         p.offsets = upload(*ix, off32.data(), off32.size());
     }
 
-    // --- k1 <= 16 with 1-byte pairs: codes carry (i << 4 | j); c2 by that byte
+    // --- k1 <= 16 with 1-byte pairs: codes carry the pair's centroids as t = i << 4 | ((i + j) & 15)
+    // (rerank_ij.cu: the low nibble picks the shared-memory bank pair of the per-query table, and
+    // i + j spreads the lines of a part over the banks better than j alone); c2 by that byte
     p.code_ij = (pw == 1 && k1 <= 16) ? 1u : 0u;
     std::vector<uint8_t> ij_of(npairs, 0);
+    auto tcode = [](uint32_t i, uint32_t j) { return (uint8_t)((i << 4) | ((i + j) & 15u)); };
     if (p.code_ij) {
         std::vector<float> c2ij((size_t)L * 256, 0.0f);
         uint32_t q = 0;
         if (k1 > 1) {
             for (uint32_t i = 0; i < k1; ++i)
-                for (uint32_t j = i + 1; j < k1; ++j) ij_of[q++] = (uint8_t)((i << 4) | j);
+                for (uint32_t j = i + 1; j < k1; ++j) ij_of[q++] = tcode(i, j);
         }
         for (uint32_t f = 0; f < L; ++f)
             for (uint32_t i = 0; i < k1; ++i)
-                for (uint32_t j = 0; j < k1; ++j) c2ij[(size_t)f * 256 + (i << 4) + j] = src.d2[((size_t)f * k1 + i) * k1 + j];
+                for (uint32_t j = 0; j < k1; ++j) c2ij[(size_t)f * 256 + tcode(i, j)] = src.d2[((size_t)f * k1 + i) * k1 + j];
         p.c2ij = upload(*ix, c2ij.data(), c2ij.size());
     }
 

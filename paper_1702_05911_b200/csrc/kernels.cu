@@ -463,14 +463,14 @@ void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_quer
 namespace {
 
 // part contribution (linequant.hpp:83-85 in linequant.cpp:171-181's order) for stored byte
-// `b` (a pair id, or i << 4 | j when the index re-encoded pairs); c2 rows are [f][npairs] or,
+// `b` (a pair id, or i << 4 | ((i + j) & 15) when the index re-encoded pairs); c2 rows are [f][npairs] or,
 // for (i, j) codes, [f][256].
 __device__ __forceinline__ void pair_terms(uint32_t b, uint32_t f, bool ij, const float* fine, const float* c2,
                                            const uint32_t* pairs, uint32_t k1, uint32_t npairs, float& b2,
                                            float& a2, float& cc) {
-    if (ij) {
+    if (ij) {  // b = i << 4 | ((i + j) & 15) (index_prep.cpp)
         b2 = fine[f * k1 + (b >> 4)];
-        a2 = fine[f * k1 + (b & 15u)];
+        a2 = fine[f * k1 + (((b & 15u) - (b >> 4)) & 15u)];
         cc = c2[f * 256 + b];
     } else {
         const uint32_t pr = pairs[b];

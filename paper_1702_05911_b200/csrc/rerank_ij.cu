@@ -1,13 +1,13 @@
 // rerank_ij.cu — K5 fast path: line-quantized re-rank (linequant.cpp:169-182) + top-k
 // (search.cpp:221-257) for indexes with k1 <= 16 and 1-byte pairs, whose device codes store
-// each part's centroid pair as (i << 4 | j) instead of the pair id (index_prep.cpp).
+// each part's centroid pair as t = i << 4 | ((i + j) & 15) instead of the pair id (index_prep.cpp).
 //
 // One thread per candidate; the code row (L × (λ, ij) bytes, slot order) is read with 16-byte
 // loads into registers and its parts are summed in the reference's order. Per part:
 //     b2 = fine[f][i]                   a 16-float row per part: the 32 lanes of a warp touch
 //                                       at most 16 addresses, all in distinct banks
 //                                       (duplicates broadcast) — conflict-free;
-//     (E, c2) = T[f][i << 4 | j]        per-query table, E = (a2 − b2) − c2 with a2 = fine[f][j]
+//     (E, c2) = T[f][t]                 per-query table, E = (a2 − b2) − c2 with a2 = fine[f][j]
 //                                       and c2 = d2[f][i][j]: the reference's own intermediate
 //                                       (linequant.hpp:85), built once per query;
 //     part = (b2 + (λ·λ)·c2) + λ·E      exactly linequant.hpp:83-85's rounding.
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
             const uint32_t f = f0 + u * (kIjThreads / kPairLanes);
-            c2v[u] = f < LT ? __ldg(p.c2ij + f * 256 + (pi_i << 4 | pi_j)) : 0.0f;
+            c2v[u] = f < LT ? __ldg(p.c2ij + f * 256 + (pi_i << 4 | ((pi_i + pi_j) & 15u))) : 0.0f;
         }
     }
     const uint2 rg0 = tid < R ? __ldg(qr + tid) : make_uint2(0, 0);
@@ -176,10 +176,10 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
         rid[rg.y] = (uint16_t)r;
         if (cached) delta[r] = rg.x - rg.y;
     }
-    // T[f][i << 4 | j] = (E, c2) for every pair i < j (linequant.cpp:76-82); other entries
+    // T[f][t(i, j)] = (E, c2) for every pair i < j (linequant.cpp:76-82); other entries
     // are never referenced. Thread: one pair, every (blockDim / 128)-th part.
     if (pair_lane) {
-        const uint32_t ij = pi_i << 4 | pi_j;
+        const uint32_t ij = pi_i << 4 | ((pi_i + pi_j) & 15u);  // the device code of the pair
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
             const uint32_t f = f0 + u * (kIjThreads / kPairLanes);
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
             float total = 0.0f;
 #pragma unroll
             for (int f = 0; f < LT; ++f) {
-                const uint32_t half = w[f >> 1] >> ((f & 1) * 16);  // λ | (i << 4 | j) << 8
+                const uint32_t half = w[f >> 1] >> ((f & 1) * 16);  // λ | t << 8, t = i << 4 | ((i + j) & 15)
                 const uint32_t ij = (half >> 8) & 0xFFu;
                 const float b2 = fine[f * 16 + (ij >> 4)];
                 const float2 ec = T[f * 256 + ij];

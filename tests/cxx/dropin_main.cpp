@@ -2,10 +2,12 @@
 // against the reference's proj/include/pqt would call it. Used by tests/test_dropin_cxx.py.
 //
 //   dropin_main io    <index.pqt> <copy.pqt>                         load + save (no GPU)
-//   dropin_main query <index.pqt> <queries.f32> <dim> <k> <out.bin>  load + knn_query_batch
+//   dropin_main query <index.pqt> <queries.f32> <dim> <k> <out.bin> [db.f32]
+//                                                      load (+ attach_database) + knn_query_batch
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -43,6 +45,16 @@ int main(int argc, char** argv) {
         threw = true;
     }
     if (!threw) return 3;
+    if (argc > 7) {  // raw vectors for the exact re-rank stage (PqtIndex::attach_database)
+        auto db = std::make_shared<pqt::VectorSet>();
+        db->dim = dim;
+        std::ifstream in(argv[7], std::ios::binary | std::ios::ate);
+        const auto bytes = static_cast<std::size_t>(in.tellg());
+        db->data.resize(bytes / sizeof(float));
+        in.seekg(0);
+        in.read(reinterpret_cast<char*>(db->data.data()), bytes);
+        index.attach_database(db);
+    }
     std::vector<pqt::QueryResult> res = pqt::knn_query_batch(index, q, k);
     pqt::QueryResult one = pqt::knn_query(index, q.row(0), k);
     if (one.ids != res[0].ids) return 4;

@@ -49,3 +49,29 @@ def test_cxx_knn_query_batch_matches_reference(dropin_bin, name, tmp_path):
         assert np.array_equal(st, g["stats"][q])
         assert np.array_equal(ids, g["ids"][q, :c])
         assert np.array_equal(d.view(np.uint32), g["dists"][q, :c].view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [20, 80])
+def test_cxx_attach_database_exact_rerank(dropin_bin, k, tmp_path):
+    """PqtIndex::attach_database through the C++ drop-in: the exact re-rank stage on the GPU,
+    bit-exact against the reference's keep_raw build (golden p2_exact)."""
+    g = load_golden("p2_exact")
+    qf, dbf, out = tmp_path / "q.f32", tmp_path / "db.f32", tmp_path / "out.bin"
+    g["queries"].astype(np.float32).tofile(qf)
+    g["db"].astype(np.float32).tofile(dbf)
+    r = subprocess.run([str(dropin_bin), "query", str(GOLDEN / "p2_exact.pqt"), str(qf), str(g["queries"].shape[1]),
+                        str(k), str(out), str(dbf)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    buf = out.read_bytes()
+    pos = 0
+    for q in range(g["queries"].shape[0]):
+        c = int(np.frombuffer(buf, np.uint32, 1, pos)[0])
+        st = np.frombuffer(buf, np.uint64, 3, pos + 4)
+        ids = np.frombuffer(buf, np.uint32, c, pos + 28)
+        d = np.frombuffer(buf, np.float32, c, pos + 28 + 4 * c)
+        pos += 28 + 8 * c
+        assert c == g[f"counts_k{k}"][q]
+        assert np.array_equal(st, g[f"stats_k{k}"][q])
+        assert np.array_equal(ids, g[f"ids_k{k}"][q, :c])
+        assert np.array_equal(d.view(np.uint32), g[f"dists_k{k}"][q, :c].view(np.uint32))
