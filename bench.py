@@ -55,6 +55,14 @@ WORKLOADS = {
     # built in memory on the GPU (not cached: the container would be ~7 GB)
     "deep100m": dict(config=dict(dim=96, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=4096),
                      n=100_000_000, nq=10000, k=100, blobs=100_000, sigma=20.0, ntrain=100_000, cache=False),
+    # BASELINE.json configs[3]'s tree (SIFT1B: P=4, k1=32, k2=16, w=8, L=32, 496 pairs -> 2-byte pair
+    # ids, H = 2^26) at one GPU's share of 1B over 8 GPUs (125M), and a 10M variant for quick runs
+    "sift1b_shard": dict(config=dict(dim=128, p_tree=4, k1=32, k2=16, w=8, p_line=32, candidate_budget=4096,
+                                     hash_size=1 << 26),
+                         n=125_000_000, nq=10000, k=100, blobs=125_000, sigma=20.0, ntrain=200_000, cache=False),
+    "sift1b10m": dict(config=dict(dim=128, p_tree=4, k1=32, k2=16, w=8, p_line=32, candidate_budget=4096,
+                                  hash_size=1 << 26),
+                      n=10_000_000, nq=10000, k=100, blobs=10_000, sigma=20.0, ntrain=200_000),
 }
 CACHE = Path(os.environ.get("PQTG_BENCH_CACHE", "/tmp/pqtg_bench"))
 
@@ -205,7 +213,7 @@ def peaks():
 
 def gpu_launches(hix, nq: int, chunks: int) -> int:
     """Kernels launched per step: traverse, bin selection, re-rank per chunk (api.cpp)."""
-    n = chunks if chunks else (4 if nq >= 2048 else (2 if nq >= 256 else 1))
+    n = chunks if chunks else (2 if nq >= 4096 else 1)  # pqtg_search_device's default (api.cpp)
     return 3 * (n if nq >= n else 1)
 
 
