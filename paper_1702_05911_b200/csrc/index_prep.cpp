@@ -368,6 +368,15 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     // (rerank_ij.cu: the low nibble picks the shared-memory bank pair of the per-query table, and
     // i + j spreads the lines of a part over the banks better than j alone); c2 by that byte
     p.code_ij = (pw == 1 && k1 <= 16) ? 1u : 0u;
+    // 16 < k1 <= 32 (2-byte pair ids, <= 496 pairs): the stored u16 also carries the pair's
+    // first centroid, v = pid | i << 9, so the re-rank reads fine[f][i] without the pair table
+    p.code_pi = (pw == 2 && k1 <= 32 && npairs <= 512) ? 1u : 0u;
+    std::vector<uint16_t> pi_of(p.code_pi ? npairs : 0);
+    if (p.code_pi) {
+        uint32_t q = 0;
+        for (uint32_t i = 0; i < k1; ++i)
+            for (uint32_t j = i + 1; j < k1; ++j, ++q) pi_of[q] = (uint16_t)(q | (i << 9));
+    }
     std::vector<uint8_t> ij_of(npairs, 0);
     auto tcode = [](uint32_t i, uint32_t j) { return (uint8_t)((i << 4) | ((i + j) & 15u)); };
     if (p.code_ij) {
@@ -419,10 +428,11 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
                             // k1 <= 16: store the pair as its centroids (i << 4 | j), so the
                             // re-rank indexes the fine row and c2[f][i][j] directly
                             row[2 * f + 1] = (uint8_t)(p.code_ij && pid < npairs ? ij_of[pid] : pid);
-                        } else {        // lambda block, then little-endian u16 pair ids
+                        } else {        // lambda block, then little-endian u16 pair ids (| i << 9)
+                            const uint32_t v = p.code_pi && pid < npairs ? pi_of[pid] : pid;
                             row[f] = (uint8_t)lq;
-                            row[L + 2 * f] = (uint8_t)(pid & 0xFF);
-                            row[L + 2 * f + 1] = (uint8_t)(pid >> 8);
+                            row[L + 2 * f] = (uint8_t)(v & 0xFF);
+                            row[L + 2 * f + 1] = (uint8_t)(v >> 8);
                         }
                     }
                 }

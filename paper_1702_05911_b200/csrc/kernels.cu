@@ -483,7 +483,7 @@ __device__ __forceinline__ void pair_terms(uint32_t b, uint32_t f, bool ij, cons
 template <int LT, int PW>
 __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ row, const float* fine,
                                                    const float* c2, const uint32_t* pairs, uint32_t L,
-                                                   uint32_t k1, uint32_t npairs, bool ij) {
+                                                   uint32_t k1, uint32_t npairs, bool ij, uint32_t pid_mask) {
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     float total = 0.0f;
     if constexpr (LT > 0) {
@@ -505,6 +505,7 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
                 lq = (wds[f >> 2] >> ((f & 3) * 8)) & 0xFFu;
                 const int b0 = LT + 2 * f, b1 = b0 + 1;
                 pid = ((wds[b0 >> 2] >> ((b0 & 3) * 8)) & 0xFFu) | (((wds[b1 >> 2] >> ((b1 & 3) * 8)) & 0xFFu) << 8);
+                pid &= pid_mask;  // code_pi rows carry the first centroid in bits 9..13
             }
             float b2, a2, cc;
             pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc);
@@ -521,7 +522,7 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
                 pid = __ldg(row + 2 * f + 1);
             } else {
                 lq = __ldg(row + f);
-                pid = (uint32_t)__ldg(row + L + 2 * f) | ((uint32_t)__ldg(row + L + 2 * f + 1) << 8);
+                pid = ((uint32_t)__ldg(row + L + 2 * f) | ((uint32_t)__ldg(row + L + 2 * f + 1) << 8)) & pid_mask;
             }
             float b2, a2, cc;
             pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc);
@@ -591,7 +592,8 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
         if (!sharded || (pos >= p.shard_lo && pos < p.shard_hi)) {
             const uint64_t lp = pos - p.shard_lo;
             const uint32_t id = __ldg(p.ids + lp);
-            const float d = line_distance_row<LT, PW>(p.codes + lp * p.row_bytes, fine, c2, pairs, L, k1, npairs, ij);
+            const float d = line_distance_row<LT, PW>(p.codes + lp * p.row_bytes, fine, c2, pairs, L, k1, npairs, ij,
+                                                      p.code_pi ? 0x1FFu : 0xFFFFu);
             key = ((uint64_t)orderable(d) << 32) | id;
             ++mine;
         }

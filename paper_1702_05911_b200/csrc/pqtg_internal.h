@@ -65,7 +65,8 @@ struct DevParams {
     const uint32_t* offsets;    // [H + 1] u32
     const uint32_t* ids;        // [shard positions]
     const uint8_t* codes;       // [shard positions][row_bytes]
-    uint32_t code_ij;           // 1-byte codes hold (i << 4 | j) instead of the pair id (k1 <= 16)
+    uint32_t code_ij;           // 1-byte codes hold i << 4 | ((i + j) & 15) instead of the pair id (k1 <= 16)
+    uint32_t code_pi;           // 2-byte codes hold pid | i << 9 (16 < k1 <= 32)
     const float* c2ij;          // [L][256] d2[f][i][j] at i << 4 | j (code_ij only)
     // exact re-rank (search.cpp:229-249): raw vectors n × D f32 in id order, or null
     const float* db;

@@ -48,13 +48,18 @@ __host__ __device__ inline uint32_t ij_sel_cap(uint32_t kk) {
     return c;
 }
 
-__host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint32_t sel_cap) {
+// K1M = 16: 1-byte codes t = i << 4 | ((i + j) & 15), T[f] has 256 entries, fine rows 16 floats.
+// K1M = 32: 2-byte codes v = pid | i << 9 (k1 <= 32, 496 pairs), T[f] has 512 entries by pair id,
+// fine rows 32 floats.
+__host__ __device__ constexpr uint32_t t_entries(int K1M) { return K1M == 16 ? 256u : 512u; }
+
+__host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint32_t sel_cap, int K1M = 16) {
     IjLayout l{};
     size_t o = 0;
     l.t = o;  // T, fine, delta and rid sit at compile-time offsets (load immediates)
-    o += (size_t)L * 256 * 8;
+    o += (size_t)L * t_entries(K1M) * 8;
     l.fine = o;
-    o += (size_t)L * 16 * 4;
+    o += (size_t)L * K1M * 4;
     l.delta = o;
     o += (size_t)kRangeCache * 4;
     // rid: u16 range index per candidate, padded to whole 4096-candidate scan tiles; after
@@ -113,22 +118,23 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 
 }  // namespace
 
-template <int LT>
-__global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
+template <int LT, int K1M>
+__global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 2)
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
                      float* __restrict__ out_dists, uint32_t* __restrict__ out_counts) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k1 = p.k1, budget = p.budget;
-    const IjLayout lay = ij_layout(LT, budget, sel_cap);
+    constexpr uint32_t TE = t_entries(K1M);
+    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M);
     float2* T = reinterpret_cast<float2*>(smem);
-    float* fine = reinterpret_cast<float*>(smem + ij_layout(LT, 0, 0).fine);
+    float* fine = reinterpret_cast<float*>(smem + ij_layout(LT, 0, 0, K1M).fine);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + lay.keys);
     uint64_t* sel = reinterpret_cast<uint64_t*>(smem + lay.sel);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0).rid);  // aliases rid
-    uint16_t* rid = reinterpret_cast<uint16_t*>(smem + ij_layout(LT, 0, 0).rid);
-    uint32_t* delta = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0).delta);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0, K1M).rid);  // aliases rid
+    uint16_t* rid = reinterpret_cast<uint16_t*>(smem + ij_layout(LT, 0, 0, K1M).rid);
+    uint32_t* delta = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0, K1M).delta);
     constexpr int kIjThreads = ij_threads(LT);
     __shared__ uint32_t wmax[kIjThreads / 32];
     __shared__ uint32_t s_count;
@@ -141,8 +147,9 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
 
     // every global load of the prologue is issued before the first barrier: the query's fine
     // LUT, the first kIjThreads ranges and this thread's column of d2 (T build below)
-    constexpr uint32_t kPairLanes = 128;
-    constexpr uint32_t kFPer = (LT + kIjThreads / kPairLanes - 1) / (kIjThreads / kPairLanes);
+    constexpr uint32_t kPairLanes = K1M == 16 ? 128 : 512;  // >= the pair count
+    constexpr uint32_t kFLanes = kIjThreads / kPairLanes;
+    constexpr uint32_t kFPer = (LT + kFLanes - 1) / kFLanes;
     const uint32_t pi = tid & (kPairLanes - 1), f0 = tid / kPairLanes;
     const bool pair_lane = pi < p.npairs;
     uint32_t pi_i = 0, pi_j = 0;
@@ -153,13 +160,16 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
         pi_j = pr >> 16;
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
-            const uint32_t f = f0 + u * (kIjThreads / kPairLanes);
-            c2v[u] = f < LT ? __ldg(p.c2ij + f * 256 + (pi_i << 4 | ((pi_i + pi_j) & 15u))) : 0.0f;
+            const uint32_t f = f0 + u * kFLanes;
+            if constexpr (K1M == 16)
+                c2v[u] = f < LT ? __ldg(p.c2ij + f * 256 + (pi_i << 4 | ((pi_i + pi_j) & 15u))) : 0.0f;
+            else
+                c2v[u] = f < LT ? __ldg(p.c2 + f * p.npairs + pi) : 0.0f;
         }
     }
     const uint2 rg0 = tid < R ? __ldg(qr + tid) : make_uint2(0, 0);
-    for (uint32_t i = tid; i < LT * 16; i += blockDim.x) {
-        const uint32_t f = i >> 4, c = i & 15;
+    for (uint32_t i = tid; i < LT * K1M; i += blockDim.x) {
+        const uint32_t f = i / K1M, c = i % K1M;
         fine[i] = c < k1 ? fine_in[q * LT * k1 + f * k1 + c] : 0.0f;
     }
     const uint32_t Cpad = (C + kScanItems * kIjThreads - 1) / (kScanItems * kIjThreads) * (kScanItems * kIjThreads);
@@ -179,13 +189,14 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
     // T[f][t(i, j)] = (E, c2) for every pair i < j (linequant.cpp:76-82); other entries
     // are never referenced. Thread: one pair, every (blockDim / 128)-th part.
     if (pair_lane) {
-        const uint32_t ij = pi_i << 4 | ((pi_i + pi_j) & 15u);  // the device code of the pair
+        // the pair's T slot: its device code (K1M = 16) or its pair id (K1M = 32)
+        const uint32_t ij = K1M == 16 ? (pi_i << 4 | ((pi_i + pi_j) & 15u)) : pi;
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
-            const uint32_t f = f0 + u * (kIjThreads / kPairLanes);
+            const uint32_t f = f0 + u * kFLanes;
             if (f < LT) {
-                const float b2 = fine[f * 16 + pi_i], a2 = fine[f * 16 + pi_j];
-                T[f * 256 + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
+                const float b2 = fine[f * K1M + pi_i], a2 = fine[f * K1M + pi_j];
+                T[f * TE + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
             }
         }
     }
@@ -194,7 +205,7 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     const bool sharded = p.shard_hi > p.shard_lo;
-    constexpr int kVec = (2 * LT + 15) / 16;
+    constexpr int kVec = ((K1M == 16 ? 2 : 3) * LT + 15) / 16;
     uint32_t mine = 0;
     uint32_t kand = ~0u, kor = 0u;  // AND / OR of this thread's orderable distances
     // candidate j's code row and id, fetched one iteration ahead (software pipelining)
@@ -231,11 +242,21 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
             float total = 0.0f;
 #pragma unroll
             for (int f = 0; f < LT; ++f) {
-                const uint32_t half = w[f >> 1] >> ((f & 1) * 16);  // λ | t << 8, t = i << 4 | ((i + j) & 15)
-                const uint32_t ij = (half >> 8) & 0xFFu;
-                const float b2 = fine[f * 16 + (ij >> 4)];
-                const float2 ec = T[f * 256 + ij];
-                const float lam = __fmul_rn(__uint2float_rn(half & 0xFFu), inv255);
+                uint32_t lq, ti, fi;  // λq, T slot, fine index
+                if constexpr (K1M == 16) {
+                    const uint32_t half = w[f >> 1] >> ((f & 1) * 16);  // λ | t << 8, t = i << 4 | ((i + j) & 15)
+                    ti = (half >> 8) & 0xFFu;
+                    fi = ti >> 4;
+                    lq = half & 0xFFu;
+                } else {
+                    lq = (w[f >> 2] >> ((f & 3) * 8)) & 0xFFu;                 // λ block
+                    const uint32_t v = (w[LT / 4 + (f >> 1)] >> ((f & 1) * 16)) & 0xFFFFu;  // pid | i << 9
+                    ti = v & 0x1FFu;
+                    fi = v >> 9;
+                }
+                const float b2 = fine[f * K1M + fi];
+                const float2 ec = T[f * TE + ti];
+                const float lam = __fmul_rn(__uint2float_rn(lq), inv255);
                 const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), ec.y)), __fmul_rn(lam, ec.x));
                 total = __fadd_rn(total, part);
             }
@@ -273,17 +294,19 @@ __global__ void __launch_bounds__(ij_threads(LT), LT >= 64 ? 1 : 2)
 
 namespace {
 
-template <int LT>
+template <int LT, int K1M>
 void allow(int optin) {
     cudaFuncAttributes a{};
-    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, rerank_ij_kernel<LT>));
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_ij_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, rerank_ij_kernel<LT, K1M>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_ij_kernel<LT, K1M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          optin - (int)a.sharedSizeBytes));
 }
 
+int code_k1m(const DevParams& p) { return p.code_ij ? 16 : (p.code_pi ? 32 : 0); }
+
 size_t ij_smem(const DevParams& p, uint32_t k) {
     const uint32_t kk = k < p.budget ? k : p.budget;
-    return ij_layout(p.L, p.budget, ij_sel_cap(kk)).total;
+    return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16).total;
 }
 
 }  // namespace
@@ -292,17 +315,21 @@ bool rerank_ij_ok(const DevParams& p, uint32_t k) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return p.code_ij && p.budget <= 65535 && p.npairs <= 128 &&
-           (p.L == 16 || p.L == 32 || p.L == 64) && ij_smem(p, k) + 4096 <= (size_t)optin;
+    const int k1m = code_k1m(p);
+    const bool shape = k1m == 16 ? (p.L == 16 || p.L == 32 || p.L == 64) : (k1m == 32 && (p.L == 16 || p.L == 32));
+    return shape && p.budget <= 65535 && p.npairs <= (k1m == 16 ? 128u : 512u) &&
+           ij_smem(p, k) + 4096 <= (size_t)optin;
 }
 
 void configure_rerank_ij() {
     int dev = 0, optin = 0;
     PQTG_CUDA_CHECK(cudaGetDevice(&dev));
     PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    allow<16>(optin);
-    allow<32>(optin);
-    allow<64>(optin);
+    allow<16, 16>(optin);
+    allow<32, 16>(optin);
+    allow<64, 16>(optin);
+    allow<16, 32>(optin);
+    allow<32, 32>(optin);
 }
 
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids, float* dists,
@@ -310,13 +337,18 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     const uint32_t kk = k < p.budget ? k : p.budget;
     const uint32_t cap = ij_sel_cap(kk);
     const size_t sm = ij_smem(p, k);
-#define PQTG_IJ(LT)                                                                                         \
-    rerank_ij_kernel<LT><<<(unsigned)nq, ij_threads(LT), sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \
-                                                             ws.ncand, ids, dists, counts)
-    switch (p.L) {
-    case 16: PQTG_IJ(16); break;
-    case 32: PQTG_IJ(32); break;
-    default: PQTG_IJ(64); break;
+#define PQTG_IJ(LT, K)                                                                                        \
+    rerank_ij_kernel<LT, K><<<(unsigned)nq, ij_threads(LT), sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \
+                                                                   ws.ncand, ids, dists, counts)
+    if (code_k1m(p) == 32) {
+        if (p.L == 16) PQTG_IJ(16, 32);
+        else PQTG_IJ(32, 32);
+    } else {
+        switch (p.L) {
+        case 16: PQTG_IJ(16, 16); break;
+        case 32: PQTG_IJ(32, 16); break;
+        default: PQTG_IJ(64, 16); break;
+        }
     }
 #undef PQTG_IJ
     PQTG_CUDA_CHECK(cudaGetLastError());

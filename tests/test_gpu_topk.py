@@ -90,3 +90,22 @@ def test_gpu_exact_rerank_built_index(k):
     want = o.knn(Q, k)
     assert_same_results(got, want, f"exact k={k}")
     assert (got[3][:, 2] == np.minimum(max(64, k), got[3][:, 1])).all()
+
+
+@pytest.mark.parametrize("k1,p_tree,p_line", [(24, 2, 16), (32, 4, 32)])
+def test_gpu_two_byte_pair_codes(k1, p_tree, p_line):
+    """16 < k1 <= 32: 2-byte pair ids whose device codes also carry the first centroid
+    (v = pid | i << 9, index_prep.cpp) — the fast re-rank (K1M = 32) and the generic one
+    against the C oracle on a GPU-built index."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=128, p_tree=p_tree, k1=k1, k2=8, w=4, p_line=p_line, train_iters=4, seed=31 + k1,
+                    candidate_budget=1024)
+    X = builder.synth_clustered(80_000 + 48, cfg.dim, 128, 20.0, 31, device=dev)
+    db, Q = X[:80_000], X[80_000:].cpu().numpy()
+    hix = builder.build_index(db, db[:20_000], cfg)
+    assert hix.pair_width == 2
+    got = DeviceIndex(hix).search(Q, 100)
+    want = Oracle(hix).knn(Q, 100)
+    assert_same_results(got, want, f"k1={k1}")
