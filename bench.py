@@ -214,7 +214,7 @@ def peaks():
 def gpu_launches(hix, nq: int, chunks: int) -> int:
     """Kernels launched per step: traverse, bin selection, re-rank per chunk (api.cpp)."""
     n = chunks if chunks else (2 if nq >= 4096 else 1)  # pqtg_search_device's default (api.cpp)
-    return 3 * (n if nq >= n else 1)
+    return 3 * (n if nq >= n else 1)  # (+1 per chunk with --exact: exact_rerank_kernel)
 
 
 # --------------------------------------------------------------------------- recall
@@ -262,8 +262,9 @@ def measure_recall(name: str, seed: int, device: int, Q: np.ndarray, nq_pool: in
 
 
 # --------------------------------------------------------------------------- CPU legs
-def cpu_leg(hix, Q, k, min_seconds=10.0, max_reps=20):
-    """Time the reference (oracle/_ref) — else the C restatement — on this host's cores."""
+def cpu_leg(hix, Q, k, min_seconds=10.0, max_reps=20, db=None):
+    """Time the reference (oracle/_ref) — else the C restatement — on this host's cores
+    (with the raw vectors attached when db is given: the exact re-rank stage)."""
     from oracle.bindings import Oracle, Ref
 
     threads = os.cpu_count() or 1
@@ -271,6 +272,8 @@ def cpu_leg(hix, Q, k, min_seconds=10.0, max_reps=20):
         impl, kind = Ref.from_host(hix), "reference"
     else:
         impl, kind = Oracle(hix), "port"
+    if db is not None:
+        impl.attach_database(db)
     impl.knn(Q[: min(len(Q), 16)], k, threads=threads)  # warm-up (page-in)
     reps, t_total, out = 0, 0.0, None
     while reps < max_reps and (t_total < min_seconds or reps == 0):
@@ -342,6 +345,8 @@ def main():
     ap.add_argument("--no-recall", action="store_true")
     ap.add_argument("--chunks", type=int, default=0,
                     help="pieces per batch overlapped on two streams (0 auto, 1 off)")
+    ap.add_argument("--exact", action="store_true",
+                    help="attach the raw base vectors: the exact re-rank stage runs (rerank_exact = 64)")
     ap.add_argument("--shard", action="store_true",
                     help="shard the index's positions over the ranks (NCCL broadcast + all-gather + "
                          "merge; sharded.py) instead of one replica per rank")
@@ -387,6 +392,13 @@ def main():
         batches = [Qpool[(rank * args.batches + b) * nq:(rank * args.batches + b + 1) * nq]
                    for b in range(args.batches)]
     dev.set_chunks(args.chunks)
+    db_rows = None
+    if args.exact:  # the build's base rows, regenerated deterministically (make_workload's draw)
+        from paper_1702_05911_b200 import builder
+
+        db_rows = builder.synth_clustered(wl["n"] + len(Qpool), wl["config"]["dim"], wl["blobs"], wl["sigma"],
+                                          args.seed, device=torch.device("cuda", local))[: wl["n"]].cpu().numpy()
+        dev.attach_database(db_rows)
     d_q = [torch.from_numpy(b).cuda() for b in batches]
     d_ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
     d_dists = torch.empty((nq, k), dtype=torch.float32, device="cuda")
@@ -524,7 +536,7 @@ def main():
         g_d = d_dists.cpu().numpy()
         g_c = d_counts.cpu().numpy().view(np.uint32)
         g_s = d_stats.cpu().numpy().astype(np.uint64)
-        cpu, (r_ids, r_d, r_c, r_s) = cpu_leg(hix, batches[0], k)
+        cpu, (r_ids, r_d, r_c, r_s) = cpu_leg(hix, batches[0], k, db=db_rows)
         same = np.array_equal(g_c, r_c) and np.array_equal(g_s, r_s)
         for q in range(nq):
             c = g_c[q]
@@ -543,11 +555,12 @@ def main():
         "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic clustered blobs (synth_clustered distribution), GPU-built PQT index",
         "config": {"workload": args.workload, **wl["config"], "n": wl["n"], "queries_per_step": nq, "k": k,
+                   "exact_rerank": bool(args.exact),
                    "l2": "flushed between timed steps (256 MiB write)" if not args.no_flush else "not flushed",
                    "parallelism": (f"position shards x{world} (NCCL broadcast + all-gather + merge)"
                                    if args.shard else f"replicas x{world}")},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": gpu_launches(hix, nq, args.chunks) * args.steps,
+        "gpu_launches": gpu_launches(hix, nq, args.chunks) * args.steps * (4 if args.exact else 3) // 3,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "parity": parity,

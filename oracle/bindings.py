@@ -199,6 +199,7 @@ class Ref(_Lib):
         "ref_index_view": (C.c_int, [_vp, C.POINTER(PqtgIndexView)]),
         "ref_index_database": (_vp, [_vp]),
         "ref_detach_database": (None, [_vp]),
+        "ref_attach_database": (C.c_int, [_vp, _vp, _u64]),
         "ref_knn_batch": (C.c_int, [_vp, _vp, _u64, _u32, C.c_int, _vp, _vp, _vp, _vp, _vp]),
         "ref_traverse": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
         "ref_heuristic_order": (C.c_int64, [_vp, _vp, _u32, _u32, _u64, _vp]),
@@ -264,6 +265,11 @@ class Ref(_Lib):
 
     def detach_database(self) -> None:
         self.so().ref_detach_database(self.h)
+
+    def attach_database(self, rows: np.ndarray) -> None:
+        rows = np.ascontiguousarray(rows, np.float32)
+        if self.so().ref_attach_database(self.h, _p(rows), rows.shape[0]) != 0:
+            raise ValueError("reference: " + self.so().ref_last_error().decode())
 
     def knn(self, queries: np.ndarray, k: int, threads: int = 0, stage_times: bool = False):
         q = np.ascontiguousarray(queries, np.float32)

@@ -252,6 +252,18 @@ const float* ref_index_database(void* handle) {
 // Detach the raw database so queries run the loaded-index path (rerank disabled).
 void ref_detach_database(void* handle) { static_cast<Handle*>(handle)->index.database.reset(); }
 
+// pqt::PqtIndex::attach_database (search.cpp:44-49) with a copy of n × dim raw vectors.
+int ref_attach_database(void* handle, const float* rows, uint64_t n) {
+    try {
+        auto* h = static_cast<Handle*>(handle);
+        auto db = std::make_shared<pqt::VectorSet>(make_set(rows, n, h->index.config.dim));
+        h->index.attach_database(db);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 // pqt::knn_query_batch (search.cpp:262-274). stats: nq × 3 (bins_visited, candidates, exact_evals);
 // stage_us: nq × 4 (traversal, bin_selection, vector_proposal, rerank) or NULL.
 int ref_knn_batch(void* handle, const float* queries, uint64_t nq, uint32_t k, int threads,

@@ -312,10 +312,14 @@ int pqtg_index_attach_database(pqtg_index* index, const float* rows, uint64_t n,
         if (d.prm.shard_hi > d.prm.shard_lo && (d.prm.shard_lo != 0 || d.prm.shard_hi != d.n))
             unsupported("exact re-ranking on a sharded index");
         float* buf = nullptr;
-        const size_t bytes = (size_t)n * dim * sizeof(float);
+        const uint32_t stride = (dim + 3) / 4 * 4;  // 16-byte rows for the exact stage's bulk copies
+        const size_t bytes = (size_t)n * stride * sizeof(float);
         cudaError_t e = cudaMalloc(&buf, bytes ? bytes : 16);
         if (e != cudaSuccess) throw Error{PQTG_ERR_OOM, std::string("attach_database: ") + cudaGetErrorString(e)};
-        e = cudaMemcpy(buf, rows, bytes, cudaMemcpyHostToDevice);
+        if (stride != dim) e = cudaMemset(buf, 0, bytes);
+        if (e == cudaSuccess && n)
+            e = cudaMemcpy2D(buf, stride * sizeof(float), rows, dim * sizeof(float), dim * sizeof(float), n,
+                             cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
             cudaFree(buf);
             throw Error{PQTG_ERR_CUDA, std::string("attach_database: ") + cudaGetErrorString(e)};
@@ -326,6 +330,7 @@ int pqtg_index_attach_database(pqtg_index* index, const float* rows, uint64_t n,
         }
         d.db = buf;
         d.prm.db = buf;
+        d.prm.db_stride = stride;
         return PQTG_OK;
     });
 }

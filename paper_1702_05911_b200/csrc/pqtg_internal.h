@@ -69,7 +69,8 @@ struct DevParams {
     uint32_t code_pi;           // 2-byte codes hold pid | i << 9 (16 < k1 <= 32)
     const float* c2ij;          // [L][256] d2[f][i][j] at i << 4 | j (code_ij only)
     // exact re-rank (search.cpp:229-249): raw vectors n × D f32 in id order, or null
-    const float* db;
+    const float* db;            // [n][db_stride]
+    uint32_t db_stride;         // D rounded up to 4 floats
     uint32_t rerank_exact;
     // tensor-core level-2 screen (screen.cu)
     const float* scr_c;         // [P][scr_nj][scr_kpad] children minus their parent: c'' = c - mu_i
