@@ -95,12 +95,9 @@ __global__ void __launch_bounds__(kScThreads) tc_screen_kernel(DevParams p, cons
                                                                float* __restrict__ out) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr uint32_t A_BYTES = kScM * kScKC * 2, B_BYTES = NT * kScKC * 2;
-    unsigned char* a_hi = smem;
-    unsigned char* a_lo = smem + A_BYTES;
-    unsigned char* b_hi = smem + 2 * A_BYTES;
-    unsigned char* b_lo = smem + 2 * A_BYTES + B_BYTES;
+    constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;  // hi/lo A, hi/lo B of one K chunk
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ __align__(8) uint64_t s_bar[2];
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const uint32_t part = blockIdx.y, m = p.m, kpad = p.scr_kpad, nj = p.scr_nj, D = p.D;
@@ -115,7 +112,10 @@ __global__ void __launch_bounds__(kScThreads) tc_screen_kernel(DevParams p, cons
                      "r"((uint32_t)NT));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) mbar_init(&s_bar, 1);
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+    }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -123,14 +123,12 @@ __global__ void __launch_bounds__(kScThreads) tc_screen_kernel(DevParams p, cons
     // idesc: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1, K-major A/B, N>>3 [17,23), M>>4 [24,29)
     constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
                                ((uint32_t)(kScM >> 4) << 24);
-    uint32_t phase = 0;
-    for (uint32_t k0 = 0; k0 < kpad; k0 += kScKC) {
-        const uint32_t kc = kpad - k0 < (uint32_t)kScKC ? kpad - k0 : (uint32_t)kScKC;  // multiple of 16
-        const uint32_t c4n = kc / 4;
-        // A: 128 query rows × kc, consecutive threads on consecutive 16-byte pieces of a row; all
-        // of a thread's loads are issued before any is converted
-        constexpr uint32_t kAIt = kScM * (kScKC / 4) / kScThreads;
-        float4 av[kAIt];
+    constexpr uint32_t kAIt = kScM * (kScKC / 4) / kScThreads;
+    constexpr uint32_t kBIt = NT * (kScKC / 4) / kScThreads;
+    float4 av[kAIt], bv[kBIt];
+    // global -> registers for chunk k0: consecutive threads on consecutive 16-byte pieces of a row
+    auto load = [&](uint32_t k0) {
+        const uint32_t kc = kpad - k0 < (uint32_t)kScKC ? kpad - k0 : (uint32_t)kScKC, c4n = kc / 4;
 #pragma unroll
         for (uint32_t it = 0; it < kAIt; ++it) {
             const uint32_t idx = it * kScThreads + tid, r = idx / c4n, k = (idx - r * c4n) * 4;
@@ -148,23 +146,25 @@ __global__ void __launch_bounds__(kScThreads) tc_screen_kernel(DevParams p, cons
                 }
             }
         }
-        constexpr uint32_t kBIt = NT * (kScKC / 4) / kScThreads;
-        float4 bv[kBIt];
 #pragma unroll
         for (uint32_t it = 0; it < kBIt; ++it) {
             const uint32_t idx = it * kScThreads + tid, r = idx / c4n, k = (idx - r * c4n) * 4;
             bv[it] = idx < NT * c4n ? __ldg(reinterpret_cast<const float4*>(crow + (size_t)r * kpad + k0 + k))
                                     : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         }
+    };
+    // registers -> bf16 hi/lo core-matrix tiles of a stage (A centred on the part's mean child)
+    auto stage_store = [&](uint32_t k0, unsigned char* st) {
+        const uint32_t kc = kpad - k0 < (uint32_t)kScKC ? kpad - k0 : (uint32_t)kScKC, c4n = kc / 4;
 #pragma unroll
         for (uint32_t it = 0; it < kAIt; ++it) {
             const uint32_t idx = it * kScThreads + tid, r = idx / c4n, k = (idx - r * c4n) * 4;
             if (idx < kScM * c4n) {
                 const bool live = q0 + r < nq;
                 float x[4] = {av[it].x, av[it].y, av[it].z, av[it].w};
-                for (uint32_t i = 0; i < 4; ++i)  // centre on the part's mean child
+                for (uint32_t i = 0; i < 4; ++i)
                     x[i] = (live && k0 + k + i < m) ? x[i] - __ldg(mu + k0 + k + i) : 0.0f;
-                stage4(a_hi, a_lo, kScM, r, k, x);
+                stage4(st, st + A_BYTES, kScM, r, k, x);
             }
         }
 #pragma unroll
@@ -172,27 +172,46 @@ __global__ void __launch_bounds__(kScThreads) tc_screen_kernel(DevParams p, cons
             const uint32_t idx = it * kScThreads + tid, r = idx / c4n, k = (idx - r * c4n) * 4;
             if (idx < NT * c4n) {
                 const float x[4] = {bv[it].x, bv[it].y, bv[it].z, bv[it].w};
-                stage4(b_hi, b_lo, NT, r, k, x);
+                stage4(st + 2 * A_BYTES, st + 2 * A_BYTES + B_BYTES, NT, r, k, x);
             }
         }
+    };
+    // two-stage pipeline: chunk c's global loads are in flight while the tensor core multiplies
+    // chunk c − 1; a stage is rewritten only after the MMAs that read it have committed
+    const uint32_t nchunk = (kpad + kScKC - 1) / kScKC;
+    uint32_t phase[2] = {0u, 0u};
+    load(0);
+    for (uint32_t c = 0; c < nchunk; ++c) {
+        const uint32_t k0 = c * kScKC, st = c & 1u;
+        unsigned char* sb = smem + (size_t)st * STAGE;
+        if (c >= 2) {  // the MMAs of chunk c − 2 read this stage
+            mbar_wait(&s_bar[st], phase[st]);
+            phase[st] ^= 1u;
+        }
+        stage_store(k0, sb);
+        if (c + 1 < nchunk) load(k0 + kScKC);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
         __syncthreads();
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t kc = kpad - k0 < (uint32_t)kScKC ? kpad - k0 : (uint32_t)kScKC;
             for (uint32_t s = 0; s < kc / 16; ++s) {
                 const uint32_t aoff = 2 * s * (kScM / 8) * 128, boff = 2 * s * (NT / 8) * 128;
-                const uint64_t ah = umma_desc(smem_addr(a_hi + aoff), kScM * 16, 128);
-                const uint64_t al = umma_desc(smem_addr(a_lo + aoff), kScM * 16, 128);
-                const uint64_t bh = umma_desc(smem_addr(b_hi + boff), NT * 16, 128);
-                const uint64_t bl = umma_desc(smem_addr(b_lo + boff), NT * 16, 128);
+                const uint64_t ah = umma_desc(smem_addr(sb + aoff), kScM * 16, 128);
+                const uint64_t al = umma_desc(smem_addr(sb + A_BYTES + aoff), kScM * 16, 128);
+                const uint64_t bh = umma_desc(smem_addr(sb + 2 * A_BYTES + boff), NT * 16, 128);
+                const uint64_t bl = umma_desc(smem_addr(sb + 2 * A_BYTES + B_BYTES + boff), NT * 16, 128);
                 umma_bf16(tmem, ah, bh, idesc, (k0 | s) != 0);
                 umma_bf16(tmem, ah, bl, idesc, 1u);
                 umma_bf16(tmem, al, bh, idesc, 1u);
             }
-            umma_commit(&s_bar);  // arrives when the MMAs above (and their smem reads) are done
+            umma_commit(&s_bar[st]);  // arrives when these MMAs (and their smem reads) are done
         }
-        mbar_wait(&s_bar, phase);
-        phase ^= 1u;
+    }
+    // the last chunk's commit covers every earlier MMA (tcgen05 ops complete in issue order)
+    {
+        const uint32_t st = (nchunk - 1) & 1u;
+        mbar_wait(&s_bar[st], phase[st]);
     }
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
@@ -238,12 +257,15 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
                                                               uint32_t* __restrict__ l2c_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k1 = K1T ? (uint32_t)K1T : p.k1, k2 = K2T ? (uint32_t)K2T : p.k2;
-    const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W;
+    const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W, nj0 = k1 * k2;
     float* y = reinterpret_cast<float*>(smem);                     // m
     float* fine = y + m;                                           // pp · k1
     float* l1d = fine + pp * k1;                                   // k1
     uint32_t* l1o = reinterpret_cast<uint32_t*>(l1d + k1);         // k1
-    float* dt = reinterpret_cast<float*>(l1o + k1);                // W screened
+    float* sg = reinterpret_cast<float*>(l1o + k1);                // nj0: G of every child
+    float* skc = sg + nj0;                                         // nj0: kc
+    float* scn = skc + nj0;                                        // nj0: |c''|^2
+    float* dt = scn + nj0;                                         // W screened
     float* lo = dt + W;                                            // W lower bounds
     float* hi = lo + W;                                            // W upper bounds
     float* dx = hi + W;                                            // W exact distances
@@ -261,6 +283,15 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
     const uint32_t jobs = pp * k1, f0 = part * pp;
     const float* yq = Q + q * p.D + (uint64_t)part * m;
     const float* mu = p.scr_mu + (size_t)part * p.scr_kpad;
+    // every global load that does not depend on the level-1 order is issued first: the query
+    // part, the tensor-core dot products and constants of all k1·k2 children
+    const float* grow = scr + (q * P + part) * (uint64_t)p.scr_nj;
+    const size_t cbase = (size_t)part * p.scr_nj;
+    for (uint32_t j = tid; j < nj0; j += blockDim.x) {
+        sg[j] = __ldg(grow + j);
+        skc[j] = __ldg(p.scr_kc + cbase + j);
+        scn[j] = __ldg(p.scr_cn + cbase + j);
+    }
     float ynp = 0.0f;  // |y − μ_p|² (for the radius only)
     for (uint32_t t = tid; t < m; t += blockDim.x) {
         const float v = __ldg(yq + t);
@@ -312,11 +343,9 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
 
     // screened distances of the W children, |y − c|² = l1(i) − 2 (G − kc) + |c''|², with radii
     const float yn = s_yn[0] + s_yn[1] + s_yn[2] + s_yn[3];
-    const float* grow = scr + (q * P + part) * (uint64_t)p.scr_nj;
-    const size_t cbase = (size_t)part * p.scr_nj;
     for (uint32_t j = tid; j < W; j += blockDim.x) {
         const uint32_t r = j / k2, c = j - r * k2, parent = l1o[r], child = parent * k2 + c;
-        const float g = __ldg(grow + child), kc = __ldg(p.scr_kc + cbase + child), cn = __ldg(p.scr_cn + cbase + child);
+        const float g = sg[child], kc = skc[child], cn = scn[child];
         const float l1 = l1d[parent];
         const float d = __fadd_rn(__fsub_rn(l1, __fmul_rn(2.0f, __fsub_rn(g, kc))), cn);
         const float rad = screen_radius(d, l1, g, kc, yn, cn, m);
@@ -324,7 +353,6 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
         lo[j] = d - rad;
         hi[j] = d + rad;
         code[j] = (parent << 16) | c;
-        need[j] = 0;
     }
     __syncthreads();
     // order by lower bound (ties by code): ord[rank] = entry
@@ -335,37 +363,60 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
         ord[rank] = j;
     }
     __syncthreads();
-    // groups: sweep in lower-bound order; an entry joins the current group while its lower
-    // bound is <= the group's running max upper bound (their exact order is then uncertain)
-    if (tid == 0) {
-        uint32_t g = 0, gstart = 0, first_size = 0;
-        float run = hi[ord[0]];
-        grp[ord[0]] = 0;
-        for (uint32_t r = 1; r < W; ++r) {
-            const uint32_t e = ord[r];
-            if (lo[e] <= run) {
-                run = fmaxf(run, hi[e]);
-            } else {
-                if (g == 0) first_size = r;
-                if (r - gstart > 1)
-                    for (uint32_t x = gstart; x < r; ++x) need[ord[x]] = 1;
-                ++g;
-                gstart = r;
-                run = hi[e];
+    // groups, one warp: in lower-bound order an entry starts a new group when its lower bound
+    // exceeds every earlier upper bound (a running max: a warp max-scan with a carry per 32)
+    if (warp == 0) {
+        float carry_hi = -__int_as_float(0x7f800000);
+        uint32_t carry_g = 0;
+        for (uint32_t b = 0; b < W; b += 32) {
+            const uint32_t r = b + lane;
+            const bool live = r < W;
+            const uint32_t e = live ? ord[r] : 0u;
+            const float h = live ? hi[e] : -__int_as_float(0x7f800000);
+            float incl = h;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl = fmaxf(incl, t);
             }
-            grp[e] = g;
+            float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            excl = lane == 0 ? carry_hi : fmaxf(excl, carry_hi);
+            const bool start = live && r > 0 && lo[e] > excl;
+            uint32_t nstart = start ? 1u : 0u;  // inclusive count of group starts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, nstart, o);
+                if (lane >= (uint32_t)o) nstart += t;
+            }
+            if (live) grp[e] = carry_g + nstart;
+            carry_g += __shfl_sync(0xffffffffu, nstart, 31);
+            carry_hi = fmaxf(carry_hi, __shfl_sync(0xffffffffu, incl, 31));
         }
-        if (g == 0) first_size = W;
-        if (W - gstart > 1)
-            for (uint32_t x = gstart; x < W; ++x) need[ord[x]] = 1;
-        // ranks 0 and 1 are exact (pick_slope_table): the first group, and the second one when
-        // the first is a single entry
-        const uint32_t last = first_size >= 2 ? 0u : 1u;
-        for (uint32_t x = 0; x < W && grp[ord[x]] <= last; ++x) need[ord[x]] = 1;
+    }
+    __syncthreads();
+    // exact for members of groups of two or more, and for ranks 0 and 1 (pick_slope_table): the
+    // first group, and the second when the first is a single entry
+    {
+        const bool first_single = W < 2 || grp[ord[1]] != 0u;
+        for (uint32_t r = tid; r < W; r += blockDim.x) {
+            const uint32_t e = ord[r], g = grp[e];
+            const bool shared = (r > 0 && grp[ord[r - 1]] == g) || (r + 1 < W && grp[ord[r + 1]] == g);
+            need[e] = (shared || g == 0u || (first_single && g == 1u)) ? 1u : 0u;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {  // compact the marked entries
         uint32_t n = 0;
-        for (uint32_t j = 0; j < W; ++j)
-            if (need[j]) s_ex[n++ & 127] = j;
-        s_nex = n;
+        for (uint32_t b = 0; b < W; b += 32) {
+            const bool mk = b + lane < W && need[b + lane];
+            const uint32_t bal = __ballot_sync(0xffffffffu, mk);
+            if (mk) {
+                const uint32_t at = n + __popc(bal & ((1u << lane) - 1u));
+                if (at < 128) s_ex[at] = b + lane;
+            }
+            n += __popc(bal);
+        }
+        if (lane == 0) s_nex = n;
     }
     __syncthreads();
     const uint32_t nex = s_nex;
@@ -422,10 +473,11 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
 
 namespace {
 
-size_t screen_smem(uint32_t nt) { return (size_t)2 * kScM * kScKC * 2 + (size_t)2 * nt * kScKC * 2; }
+size_t screen_smem(uint32_t nt) { return 2 * ((size_t)2 * kScM * kScKC * 2 + (size_t)2 * nt * kScKC * 2); }
 
 size_t ts_smem(const DevParams& p) {
-    return 4ull * ((size_t)p.m + (size_t)p.per_part * p.k1 + 2ull * p.k1 + 8ull * p.W + 4ull * p.m) + 16;
+    return 4ull * ((size_t)p.m + (size_t)p.per_part * p.k1 + 2ull * p.k1 + 3ull * p.k1 * p.k2 + 8ull * p.W +
+                   4ull * p.m) + 16;
 }
 
 uint32_t screen_nt(const DevParams& p) { return p.scr_nj >= 256 ? 256u : 64u; }
