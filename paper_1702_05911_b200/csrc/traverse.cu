@@ -4,10 +4,11 @@
 // A part's work is independent of the other parts' until bin selection: its fine-part LUT
 // entries (pqtree.cpp:84-93), its level-1 totals and order (:88-100), and the level-2
 // distances of its w best parents' children (:102-117). Splitting a query over P CTAs gives
-// P times the parallelism of the latency-bound chains, and each CTA stages its w parents'
+// P times the parallelism of the latency-bound chains, and each CTA streams its w parents'
 // level-2 codebook blocks ([m][k2] f32, contiguous) into shared memory with TMA bulk copies
-// (cp.async.bulk → UBLKCP) on one mbarrier, so the whole working set is in flight at once
-// instead of 16 registers' worth per thread. The level-2 chains then read shared memory.
+// (cp.async.bulk → UBLKCP) in t-chunks through two mbarrier-tracked buffers, so the next chunk
+// is in flight while the chains run over the current one and a CTA needs only ~18 KB of shared
+// memory (about 12 resident per SM). The level-2 chains read shared memory.
 // pick_slope_table (binorder.cpp:52-65) needs two parts' lists; bin selection computes it.
 //
 // Exactness: every sum is the reference's sequential fp32 chain (common.cuh sq_step,
@@ -28,13 +29,22 @@ constexpr int kFineBatch = 32;  // fine-part codebook values loaded per thread p
 
 struct TpLayout {
     size_t blk, y, fine, l1d, l1o, l2d, l2c, total;
-    uint32_t blk_stride;  // floats per staged parent block (padded; 16-byte multiple)
+    uint32_t rows;        // t-rows of the parent blocks staged per chunk (multiple of 4)
+    uint32_t blk_stride;  // floats per staged parent piece (padded; 16-byte multiple)
 };
 
+// The w best parents' blocks L2[part][parent][m][k2] are staged in chunks of `rows` t-rows
+// through two buffers (~16 KB together), so a CTA needs little shared memory and many CTAs
+// (query parts) are resident per SM.
 __host__ __device__ inline TpLayout tp_layout(const DevParams& p) {
     TpLayout l{};
-    const uint32_t mk = p.m * p.k2;
-    // pad so consecutive parents' blocks start k2 banks apart: the lanes (parent r, child c)
+    uint32_t rows = (16u * 1024u) / (2u * p.w * p.k2 * 4u);
+    rows = rows / 4 * 4;
+    if (rows < 4) rows = 4;
+    if (rows > (p.m + 3) / 4 * 4) rows = (p.m + 3) / 4 * 4;
+    l.rows = rows;
+    const uint32_t mk = rows * p.k2;
+    // pad so consecutive parents' pieces start k2 banks apart: the lanes (parent r, child c)
     // of a warp then read distinct banks at every t
     uint32_t pad = 0;
     while (((mk + pad) % 32 != p.k2 % 32 || pad % 4) && pad < 128) ++pad;
@@ -42,7 +52,7 @@ __host__ __device__ inline TpLayout tp_layout(const DevParams& p) {
     l.blk_stride = mk + pad;
     size_t o = 0;
     l.blk = o;
-    o += (size_t)p.w * l.blk_stride * 4;
+    o += 2ull * p.w * l.blk_stride * 4;
     l.y = o;
     o += (size_t)p.m * 4;
     l.fine = o;
@@ -67,7 +77,7 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
                                                                    float* __restrict__ l2d_out,
                                                                    uint32_t* __restrict__ l2c_out, uint32_t bulk) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(8) uint64_t mbar;
+    __shared__ __align__(8) uint64_t mbar[2];
     const uint32_t k1 = K1T ? (uint32_t)K1T : p.k1, k2 = K2T ? (uint32_t)K2T : p.k2;
     const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W, w = p.w;
     const TpLayout lay = tp_layout(p);
@@ -85,7 +95,10 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     const uint32_t jobs = pp * k1;  // this part's fine LUT entries (f, i)
     const uint32_t f0 = part * pp;
 
-    if (tid == 0) mbar_init(&mbar, 1);
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+    }
     const float* yq = Q + q * p.D + (uint64_t)part * m;
     for (uint32_t t = tid; t < m; t += blockDim.x) y[t] = __ldg(yq + t);
     // first batch of this thread's first fine job, in flight across the barrier
@@ -137,43 +150,65 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     }
     __syncthreads();
 
-    // stage the w best parents' level-2 blocks L2[part][parent][m][k2]
-    const uint32_t mk = m * k2, bs = lay.blk_stride;
-    if (bulk) {
-        if (tid == 0) {
-            mbar_expect_tx(&mbar, w * mk * 4);
-            for (uint32_t r = 0; r < w; ++r)
-                bulk_g2s(blk + r * bs, p.l2_t + ((size_t)part * k1 + l1o[r]) * mk, mk * 4, &mbar);
+    // level-2: l2_sq(y_p, L2[part][parent][c], m) sequentially over m (pqtree.cpp:102-111), the
+    // parents' blocks streamed in t-chunks through two buffers (TMA bulk copies on one mbarrier
+    // per buffer; chunk c + 2 is issued as soon as chunk c's buffer is free)
+    const uint32_t mk = m * k2, bs = lay.blk_stride, rows = lay.rows;
+    const uint32_t nch = (m + rows - 1) / rows;
+    auto stage = [&](uint32_t c) {  // thread 0 (bulk) / every thread (plain loads)
+        const uint32_t t0 = c * rows, nr = m - t0 < rows ? m - t0 : rows, b = c & 1u;
+        float* dst = blk + (size_t)b * w * bs;
+        if (bulk) {
+            if (tid == 0) {
+                mbar_expect_tx(&mbar[b], w * nr * k2 * 4);
+                for (uint32_t r = 0; r < w; ++r)
+                    bulk_g2s(dst + r * bs, p.l2_t + ((size_t)part * k1 + l1o[r]) * mk + (size_t)t0 * k2, nr * k2 * 4,
+                             &mbar[b]);
+            }
+        } else {
+            for (uint32_t e = tid; e < w * nr * k2; e += blockDim.x) {
+                const uint32_t r = e / (nr * k2), o = e - r * nr * k2;
+                dst[r * bs + o] = __ldg(p.l2_t + ((size_t)part * k1 + l1o[r]) * mk + (size_t)t0 * k2 + o);
+            }
         }
-        mbar_wait(&mbar, 0);
-    } else {
-        for (uint32_t e = tid; e < w * mk; e += blockDim.x) {
-            const uint32_t r = e / mk, o = e - r * mk;
-            blk[r * bs + o] = __ldg(p.l2_t + ((size_t)part * k1 + l1o[r]) * mk + o);
+    };
+    stage(0);
+    if (nch > 1) stage(1);
+    const uint32_t j = tid;  // W <= blockDim (traverse_part_ok)
+    const uint32_t r = j / k2, c = j - r * k2;
+    float acc = 0.0f;
+    uint32_t phase[2] = {0u, 0u};
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+        const uint32_t b = ch & 1u, t0 = ch * rows, nr = m - t0 < rows ? m - t0 : rows;
+        if (bulk) {
+            mbar_wait(&mbar[b], phase[b]);
+            phase[b] ^= 1u;
+        } else {
+            __syncthreads();
         }
-        __syncthreads();
-    }
-
-    // level-2: l2_sq(y_p, L2[part][parent][c], m) sequentially over m (pqtree.cpp:102-111)
-    for (uint32_t j = tid; j < W; j += blockDim.x) {
-        const uint32_t r = j / k2, c = j - r * k2;
-        const float* b = blk + r * bs + c;
-        float acc = 0.0f;
-        uint32_t t = 0;
-        for (; t + 16 <= m; t += 16) {
+        if (j < W) {
+            const float* bp = blk + (size_t)b * w * bs + r * bs + c;
+            const float* yt = y + t0;
+            uint32_t t = 0;
+            for (; t + 16 <= nr; t += 16) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u) acc = sq_step(acc, y[t + u], b[(t + u) * k2]);
+                for (int u = 0; u < 16; ++u) acc = sq_step(acc, yt[t + u], bp[(t + u) * k2]);
+            }
+            for (; t < nr; ++t) acc = sq_step(acc, yt[t], bp[t * k2]);
         }
-        for (; t < m; ++t) acc = sq_step(acc, y[t], b[t * k2]);
+        __syncthreads();  // buffer b is free
+        if (ch + 2 < nch) stage(ch + 2);
+    }
+    if (j < W) {
         l2d[j] = acc;
         l2c[j] = (l1o[r] << 16) | c;
     }
     __syncthreads();
 
     // rank by (dist, parent, child) (pqtree.cpp:112-117)
-    for (uint32_t j = tid; j < W; j += blockDim.x) {
-        const float d = l2d[j];
-        const uint32_t code = l2c[j];
+    for (uint32_t jj = tid; jj < W; jj += blockDim.x) {
+        const float d = l2d[jj];
+        const uint32_t code = l2c[jj];
         uint32_t rank = 0;
         for (uint32_t o = 0; o < W; ++o) {
             const float dj = l2d[o];
@@ -199,8 +234,8 @@ void tp_allow(int optin) {
 }  // namespace
 
 bool traverse_part_ok(const DevParams& p) {
-    // the staged parent blocks should leave room for several CTAs per SM
-    return tp_layout(p).total <= 64 * 1024 && p.W < 65536;
+    // one level-2 chain per thread; the staged chunks leave room for many CTAs per SM
+    return p.W <= (uint32_t)kTpThreads && tp_layout(p).total <= 48 * 1024;
 }
 
 void configure_traverse_part() {
@@ -216,8 +251,8 @@ void configure_traverse_part() {
 void launch_traverse_part(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                           cudaStream_t s) {
     const TpLayout lay = tp_layout(p);
-    const uint64_t mk_bytes = (uint64_t)p.m * p.k2 * 4;
-    const uint32_t bulk = (mk_bytes % 16 == 0 && (lay.blk_stride * 4) % 16 == 0 &&
+    const uint64_t mk_bytes = (uint64_t)p.m * p.k2 * 4, row_bytes = (uint64_t)lay.rows * p.k2 * 4;
+    const uint32_t bulk = (mk_bytes % 16 == 0 && row_bytes % 16 == 0 && (lay.blk_stride * 4) % 16 == 0 &&
                            (reinterpret_cast<uintptr_t>(p.l2_t) & 15) == 0)
                               ? 1u
                               : 0u;
