@@ -153,6 +153,118 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
     for (int it = NIT; it < kMaxItems; ++it) ball[it] = 0;
 }
 
+// The walker (one warp): the next n queued non-empty tuples (stream position, slot) in stream
+// order, 32 at a time — first occurrences by __match_any_sync within the batch plus the visited
+// set across batches (HASH), the bins' extents, a warp prefix sum of their sizes and the budget
+// cut (search.cpp:194-214). Emits (start position, candidate offset) ranges; c / r / maxord
+// (candidates, ranges, last stream position used) carry across calls.
+struct WalkState {
+    uint32_t c, r, maxord, nvis;
+    bool spilled;
+};
+
+template <bool HASH>
+__device__ __forceinline__ void walk_queue(const DevParams& p, const uint2* qp, uint32_t n, WalkState& st,
+                                           uint32_t budget, uint2* qranges, uint32_t* svis, uint32_t* hkeys,
+                                           uint32_t ts_log2, int lane) {
+    const uint32_t TS = 1u << ts_log2;
+    uint32_t c = st.c, r = st.r, maxord = st.maxord, nvis = st.nvis;
+    bool spilled = st.spilled;
+        const uint32_t lt = (1u << lane) - 1u;
+        for (uint32_t b0 = 0; b0 < n && c < budget; b0 += 32) {
+            const uint32_t idx = b0 + lane;
+            const bool has = idx < n;
+            const uint2 e = has ? qp[idx] : make_uint2(0, kEmptyKey);
+            // the bin's extent, loaded before the visited test so the two overlap
+            uint32_t start = 0, cnt = 0;
+            if (has) {
+                start = __ldg(p.offsets + e.y);
+                cnt = __ldg(p.offsets + e.y + 1) - start;
+            }
+            bool first = has;
+            if (HASH) {
+                const uint32_t grp = __match_any_sync(0xffffffffu, e.y);
+                if (has && (uint32_t)(__ffs(grp) - 1) != (uint32_t)lane) first = false;  // earlier in batch
+                bool fresh = false;
+                if (first) {
+                    if (!spilled) {
+                        // shared visited set: keys slot + 1, 0 = free
+                        const uint32_t key = e.y + 1u;
+                        uint32_t h = (e.y * 0x9E3779B1u) >> (32 - kVisLog2);
+                        for (;;) {
+                            const uint32_t cur = svis[h];
+                            if (cur == 0u) {
+                                if (atomicCAS(svis + h, 0u, key) == 0u) {
+                                    fresh = true;
+                                    break;
+                                }
+                                continue;
+                            }
+                            if (cur == key) {
+                                first = false;  // visited in an earlier batch
+                                break;
+                            }
+                            h = (h + 1) & (kVis - 1);
+                        }
+                    } else {
+                        const uint32_t key = e.y + 1u;
+                        uint32_t h = (e.y * 0x9E3779B1u) >> (32 - ts_log2);
+                        for (;;) {
+                            const uint32_t cur = hkeys[h];
+                            if (cur == 0u) {
+                                if (atomicCAS(hkeys + h, 0u, key) == 0u) break;
+                                continue;  // lost a race on this entry; re-read it
+                            }
+                            if (cur == key) {
+                                first = false;  // visited in an earlier batch
+                                break;
+                            }
+                            h = (h + 1) & (TS - 1);
+                        }
+                    }
+                }
+                nvis += __popc(__ballot_sync(0xffffffffu, fresh));
+                if (!spilled && nvis > kVis / 2) {
+                    // the shared set is half full: move it to the per-query global
+                    // table (sized for the whole budget) and continue there
+                    for (uint32_t i = lane; i < TS; i += 32) hkeys[i] = 0u;
+                    __syncwarp();
+                    for (uint32_t i = lane; i < kVis; i += 32) {
+                        const uint32_t v = svis[i];
+                        if (v == 0u) continue;
+                        uint32_t h = ((v - 1u) * 0x9E3779B1u) >> (32 - ts_log2);
+                        while (atomicCAS(hkeys + h, 0u, v) != 0u) h = (h + 1) & (TS - 1);
+                    }
+                    __syncwarp();
+                    spilled = true;
+                }
+            }
+            if (!first) cnt = 0;
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const uint32_t before = c + (incl - cnt);  // < 2^32: distinct bins hold <= n ids
+            const bool emit = first && before < budget;
+            const uint32_t em = __ballot_sync(0xffffffffu, emit);
+            if (emit) {
+                qranges[r + __popc(em & lt)] = make_uint2(start, before);
+                maxord = max(maxord, e.x);
+            }
+            maxord = __reduce_max_sync(0xffffffffu, maxord);
+            const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+            r += __popc(em);
+            c = (uint64_t)c + tot >= budget ? budget : c + tot;
+        }
+    st.c = c;
+    st.r = r;
+    st.maxord = maxord;
+    st.nvis = nvis;
+    st.spilled = spilled;
+}
+
 template <int P, bool HASH, class SYNC>
 __device__ __forceinline__ void binsel_fast_body(const DevParams& p, uint64_t q, const uint32_t* __restrict__ l2c_in,
                                                  const float* __restrict__ l2d_in, uint8_t* __restrict__ slope_out,
@@ -231,95 +343,11 @@ __device__ __forceinline__ void binsel_fast_body(const DevParams& p, uint64_t q,
             // ---- queue of the previous pass, in stream order, 32 tuples at a time
             if (pass > 0 && prev_n > 0) {
                 const uint2* qp = queue + (size_t)(buf ^ 1u) * kQueueCap;
-                uint32_t c = s_C, r = s_R, maxord = s_maxord;
-                const uint32_t lt = (1u << lane) - 1u;
-                for (uint32_t b0 = 0; b0 < prev_n && c < budget; b0 += 32) {
-                    const uint32_t idx = b0 + lane;
-                    const bool has = idx < prev_n;
-                    const uint2 e = has ? qp[idx] : make_uint2(0, kEmptyKey);
-                    // the bin's extent, loaded before the visited test so the two overlap
-                    uint32_t start = 0, cnt = 0;
-                    if (has) {
-                        start = __ldg(p.offsets + e.y);
-                        cnt = __ldg(p.offsets + e.y + 1) - start;
-                    }
-                    bool first = has;
-                    if (HASH) {
-                        const uint32_t grp = __match_any_sync(0xffffffffu, e.y);
-                        if (has && (uint32_t)(__ffs(grp) - 1) != (uint32_t)lane) first = false;  // earlier in batch
-                        bool fresh = false;
-                        if (first) {
-                            if (!spilled) {
-                                // shared visited set: keys slot + 1, 0 = free
-                                const uint32_t key = e.y + 1u;
-                                uint32_t h = (e.y * 0x9E3779B1u) >> (32 - kVisLog2);
-                                for (;;) {
-                                    const uint32_t cur = svis[h];
-                                    if (cur == 0u) {
-                                        if (atomicCAS(svis + h, 0u, key) == 0u) {
-                                            fresh = true;
-                                            break;
-                                        }
-                                        continue;
-                                    }
-                                    if (cur == key) {
-                                        first = false;  // visited in an earlier batch
-                                        break;
-                                    }
-                                    h = (h + 1) & (kVis - 1);
-                                }
-                            } else {
-                                const uint32_t key = e.y + 1u;
-                                uint32_t h = (e.y * 0x9E3779B1u) >> (32 - ts_log2);
-                                for (;;) {
-                                    const uint32_t cur = hkeys[h];
-                                    if (cur == 0u) {
-                                        if (atomicCAS(hkeys + h, 0u, key) == 0u) break;
-                                        continue;  // lost a race on this entry; re-read it
-                                    }
-                                    if (cur == key) {
-                                        first = false;  // visited in an earlier batch
-                                        break;
-                                    }
-                                    h = (h + 1) & (TS - 1);
-                                }
-                            }
-                        }
-                        nvis += __popc(__ballot_sync(0xffffffffu, fresh));
-                        if (!spilled && nvis > kVis / 2) {
-                            // the shared set is half full: move it to the per-query global
-                            // table (sized for the whole budget) and continue there
-                            for (uint32_t i = lane; i < TS; i += 32) hkeys[i] = 0u;
-                            __syncwarp();
-                            for (uint32_t i = lane; i < kVis; i += 32) {
-                                const uint32_t v = svis[i];
-                                if (v == 0u) continue;
-                                uint32_t h = ((v - 1u) * 0x9E3779B1u) >> (32 - ts_log2);
-                                while (atomicCAS(hkeys + h, 0u, v) != 0u) h = (h + 1) & (TS - 1);
-                            }
-                            __syncwarp();
-                            spilled = true;
-                        }
-                    }
-                    if (!first) cnt = 0;
-                    uint32_t incl = cnt;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += t;
-                    }
-                    const uint32_t before = c + (incl - cnt);  // < 2^32: distinct bins hold <= n ids
-                    const bool emit = first && before < budget;
-                    const uint32_t em = __ballot_sync(0xffffffffu, emit);
-                    if (emit) {
-                        qranges[r + __popc(em & lt)] = make_uint2(start, before);
-                        maxord = max(maxord, e.x);
-                    }
-                    maxord = __reduce_max_sync(0xffffffffu, maxord);
-                    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-                    r += __popc(em);
-                    c = (uint64_t)c + tot >= budget ? budget : c + tot;
-                }
+                WalkState st{s_C, s_R, s_maxord, nvis, spilled};
+                walk_queue<HASH>(p, qp, prev_n, st, budget, qranges, svis, hkeys, ts_log2, lane);
+                nvis = st.nvis;
+                spilled = st.spilled;
+                const uint32_t c = st.c, r = st.r, maxord = st.maxord;
                 if (lane == 0) {
                     s_C = c;
                     s_R = r;
