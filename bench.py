@@ -213,7 +213,7 @@ def peaks():
 
 def gpu_launches(hix, nq: int, chunks: int) -> int:
     """Kernels launched per step: traverse, bin selection, re-rank per chunk (api.cpp)."""
-    n = chunks if chunks else (2 if nq >= 4096 else 1)  # pqtg_search_device's default (api.cpp)
+    n = chunks if chunks else (2 if nq >= 256 else 1)  # pqtg_search_device's default (api.cpp)
     return 3 * (n if nq >= n else 1)  # (+1 per chunk with --exact: exact_rerank_kernel)
 
 

@@ -450,11 +450,10 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));
         ws.last_stream = s;
         ws.last_nq = nq;
-        // device-resident batches: chunks on two streams overlap one chunk's re-rank with the
-        // next chunk's traversal / bin selection, but pay the latency-bound kernels' fixed cost
-        // once more per chunk — a loss for 1000 GIST queries (1 chunk 247 us, 2 chunks 260 us,
-        // tools/e2e_probe.py), a small gain from ~10k queries (SIFT1M: 7.47 -> 7.56 M q/s)
-        const uint64_t nch = ws.chunks ? ws.chunks : (nq >= 4096 ? 2 : 1);
+        // device-resident batches: two chunks on two streams, so the next chunk's traversal and bin
+        // selection fill the SMs the re-rank's last wave leaves idle (tools/e2e_probe.py on B200,
+        // 1000 GIST queries: 1 chunk 234 us, 2 chunks 207 us, 4 chunks 261 us)
+        const uint64_t nch = ws.chunks ? ws.chunks : (nq >= 256 ? 2 : 1);
         if (nch <= 1 || nq < nch) {
             run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, s, true);
             return PQTG_OK;
