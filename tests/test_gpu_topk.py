@@ -109,3 +109,32 @@ def test_gpu_two_byte_pair_codes(k1, p_tree, p_line):
     got = DeviceIndex(hix).search(Q, 100)
     want = Oracle(hix).knn(Q, 100)
     assert_same_results(got, want, f"k1={k1}")
+
+
+@pytest.mark.parametrize("p_line", [16, 64])
+def test_gpu_line_counts(p_line):
+    """The (i, j)-code re-rank at L = 16 and L = 64 (L = 32 is covered by the golden cases)."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=128, p_tree=2, k1=16, k2=8, w=4, p_line=p_line, train_iters=4, seed=40 + p_line,
+                    candidate_budget=1500)
+    X = builder.synth_clustered(60_000 + 40, cfg.dim, 96, 20.0, 41, device=dev)
+    db, Q = X[:60_000], X[60_000:].cpu().numpy()
+    hix = builder.build_index(db, db[:20_000], cfg)
+    got = DeviceIndex(hix).search(Q, 64)
+    want = Oracle(hix).knn(Q, 64)
+    assert_same_results(got, want, f"L={p_line}")
+
+
+def test_gpu_sharded_index_refuses_raw_vectors():
+    """Exact re-rank needs every candidate's row: a position shard refuses attach_database."""
+    from paper_1702_05911_b200 import HostIndex
+    from paper_1702_05911_b200._abi import PqtgError
+
+    path = str(GOLDEN / "p2_exact.pqt")
+    g = load_golden("p2_exact")
+    hix = HostIndex.load(path)
+    shard = DeviceIndex(hix, shard=(0, hix.n // 2))
+    with pytest.raises(PqtgError):
+        shard.attach_database(g["db"])
