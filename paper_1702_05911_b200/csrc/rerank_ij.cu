@@ -227,15 +227,8 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
             for (int i = 0; i < kVec; ++i) v[i] = __ldg(r4 + i);
         }
     };
-    uint4 vn[kVec];
-    uint32_t idn = kInvalid;
-    if (tid < C) fetch(tid, vn, idn);
-    for (uint32_t j = tid; j < C; j += blockDim.x) {
-        uint4 v[kVec];
-#pragma unroll
-        for (int i = 0; i < kVec; ++i) v[i] = vn[i];
-        const uint32_t id = idn;
-        if (j + blockDim.x < C) fetch(j + blockDim.x, vn, idn);
+    // one candidate's line distance -> its (dist, id) key
+    auto score = [&](uint32_t j, const uint4* v, uint32_t id) {
         uint64_t key = kSentinel;
         if (id != kInvalid) {
             const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
@@ -250,9 +243,9 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
                     lq = half & 0xFFu;
                 } else {
                     lq = (w[f >> 2] >> ((f & 3) * 8)) & 0xFFu;                 // λ block
-                    const uint32_t v = (w[LT / 4 + (f >> 1)] >> ((f & 1) * 16)) & 0xFFFFu;  // pid | i << 9
-                    ti = v & 0x1FFu;
-                    fi = v >> 9;
+                    const uint32_t v2 = (w[LT / 4 + (f >> 1)] >> ((f & 1) * 16)) & 0xFFFFu;  // pid | i << 9
+                    ti = v2 & 0x1FFu;
+                    fi = v2 >> 9;
                 }
                 const float b2 = fine[f * K1M + fi];
                 const float2 ec = T[f * TE + ti];
@@ -267,6 +260,20 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
             ++mine;
         }
         keys[j] = key;
+    };
+    // two row buffers in turn: the next candidate's row is in flight while this one is scored,
+    // with no register copies between iterations
+    uint4 va[kVec], vb[kVec];
+    uint32_t ida = kInvalid, idb = kInvalid;
+    const uint32_t step = blockDim.x;
+    if (tid < C) fetch(tid, va, ida);
+    for (uint32_t j = tid; j < C; j += 2 * step) {
+        const uint32_t j2 = j + step;
+        if (j2 < C) fetch(j2, vb, idb);
+        score(j, va, ida);
+        if (j2 >= C) break;
+        if (j2 + step < C) fetch(j2 + step, va, ida);
+        score(j2, vb, idb);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {

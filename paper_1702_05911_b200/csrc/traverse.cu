@@ -190,9 +190,17 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
             const float* bp = blk + (size_t)b * w * bs + r * bs + c;
             const float* yt = y + t0;
             uint32_t t = 0;
+            // y four at a time (16-byte aligned: t0 and the y block are multiples of 4 floats)
+            const float4* y4 = reinterpret_cast<const float4*>(yt);
             for (; t + 16 <= nr; t += 16) {
 #pragma unroll
-                for (int u = 0; u < 16; ++u) acc = sq_step(acc, yt[t + u], bp[(t + u) * k2]);
+                for (int u = 0; u < 16; u += 4) {
+                    const float4 yv = y4[(t + u) >> 2];
+                    acc = sq_step(acc, yv.x, bp[(t + u + 0) * k2]);
+                    acc = sq_step(acc, yv.y, bp[(t + u + 1) * k2]);
+                    acc = sq_step(acc, yv.z, bp[(t + u + 2) * k2]);
+                    acc = sq_step(acc, yv.w, bp[(t + u + 3) * k2]);
+                }
             }
             for (; t < nr; ++t) acc = sq_step(acc, yt[t], bp[t * k2]);
         }
