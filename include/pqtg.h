@@ -162,7 +162,9 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
 void pqtg_workspace_destroy(pqtg_workspace* ws);
 /* Split each (sub-)batch into `chunks` pieces that alternate between two streams so one
  * piece's re-rank overlaps the next piece's traversal / bin selection (and, in pqtg_search, the
- * copies). 0 = automatic (1, 2 or 4 by batch size), 1 = no overlap. Results are identical. */
+ * copies). 0 = automatic (2 from 256 queries; 4 for host batches from 4096), 1 = no overlap.
+ * Results are identical. Calls on one workspace serialise on its lock; use one workspace per
+ * concurrent caller. */
 int pqtg_workspace_set_chunks(pqtg_workspace* ws, uint32_t chunks);
 /* Device milliseconds of the last pqtg_search* call per stage: [0] traversal, [1] bin
  * selection + gather, [2] re-rank + top-k, [3] whole search — of the call's first chunk (see
@@ -184,7 +186,9 @@ int pqtg_workspace_read(pqtg_workspace* ws, uint64_t nq, float* fine, uint32_t* 
 /* ---- search ----------------------------------------------------------------------- */
 /* Host buffers (copied in and out inside the call); synchronous. Outputs are nq × k
  * row-major; counts[q] = min(k, candidates) valid entries (the reference's short results,
- * search.cpp:251). stats may be NULL. dim must equal the index dim (else BAD_DIM). */
+ * search.cpp:251). stats may be NULL. dim must equal the index dim (else BAD_DIM). With
+ * page-locked host buffers the whole chunked copy/kernel sequence is recorded once per argument
+ * set as a CUDA graph and replayed (PQTG_NO_GRAPH=1 disables). */
 int pqtg_search(pqtg_index* index, pqtg_workspace* ws, const float* queries, uint64_t nq,
                 uint32_t dim, uint32_t k, uint32_t* ids, float* dists, uint32_t* counts,
                 pqtg_query_stats* stats);

@@ -442,6 +442,7 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         Workspace& ws = *wsh->ws;
         if (ws.index != index->dev.get()) throw Error{PQTG_ERR_ARG, "workspace belongs to another index"};
         if (nq > ws.max_batch) throw Error{PQTG_ERR_ARG, "nq exceeds the workspace max_batch"};
+        std::lock_guard<std::mutex> lock(ws.mu);  // the workspace's host state (buffers, chunking)
         PQTG_CUDA_CHECK(cudaSetDevice(index->dev->device));
         ensure_exact(ws, k);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
