@@ -147,6 +147,14 @@ int pqtg_index_create(const pqtg_index_view* view, int device, pqtg_index** out)
 int pqtg_index_load(const char* path, int device, uint64_t shard_lo, uint64_t shard_hi,
                     pqtg_index** out);
 int pqtg_index_info_get(const pqtg_index* index, pqtg_index_info* out);
+/* One position shard [view->shard_lo, view->shard_hi) of an index whose ids and line codes were
+ * never gathered on one host (a sharded billion-scale build): view->ids points to the SHARD's ids
+ * (positions shard_lo..shard_hi-1, in order), view->lambda_q / pair_id are not read, and the
+ * shard's codes come in position order (shard_lambda_q, shard_pair_id: (shard_hi - shard_lo) ×
+ * p_line each). offsets and the codebooks are the whole index's.
+ * The device index is identical to pqtg_index_create on the full view with the same range. */
+int pqtg_index_create_shard(const pqtg_index_view* view, const uint8_t* shard_lambda_q,
+                            const uint16_t* shard_pair_id, int device, pqtg_index** out);
 /* pqt::PqtIndex::attach_database (src/search.cpp:44-49): copy n × dim float32 raw vectors
  * (vector-id order, row-major) to the index's device. Searches then run the exact re-rank
  * stage when config.rerank_exact > 0 (src/search.cpp:229-249): the min(max(rerank_exact, k), C)
@@ -215,6 +223,7 @@ int64_t pqtg_bin_stream_host(const pqtg_index_view* view, const float* lists, ui
  * Codebooks are device arrays in the view layouts (level1, level2); d_fine is the p_line × k1 ×
  * fine_dim slice table, d_fine_sq its |slice|^2 (linequant.cpp:13-46), d_d2 the pair table
  * (linequant.cpp:60-75). Asynchronous on `stream`. */
+/* (d_part_codes, d_slots) NULL: skip the bins; (d_lambda, d_pair) NULL: skip the line codes. */
 int pqtg_build_codes(const pqtg_config* cfg, const float* d_level1, const float* d_level2,
                      const float* d_fine, const float* d_fine_sq, const float* d_d2, const float* d_x,
                      uint64_t n, uint32_t* d_part_codes, uint64_t* d_slots, uint8_t* d_lambda,

@@ -97,6 +97,7 @@ SIGNATURES = {
     "pqtg_set_kernel_variant": (C.c_int, [C.c_int]),
     "pqtg_index_create": (C.c_int, [C.POINTER(PqtgIndexView), C.c_int, C.POINTER(_vp)]),
     "pqtg_index_load": (C.c_int, [C.c_char_p, C.c_int, _u64, _u64, C.POINTER(_vp)]),
+    "pqtg_index_create_shard": (C.c_int, [C.POINTER(PqtgIndexView), _vp, _vp, C.c_int, C.POINTER(_vp)]),
     "pqtg_index_info_get": (C.c_int, [_vp, C.POINTER(PqtgIndexInfo)]),
     "pqtg_index_destroy": (None, [_vp]),
     "pqtg_index_attach_database": (C.c_int, [_vp, _vp, _u64, _u32]),

@@ -212,3 +212,151 @@ def build_index(db, train, cfg: PqtConfig, iters: int | None = None) -> HostInde
         offsets=offsets.cpu().numpy().astype(np.uint64), ids=order.to(torch.int32).cpu().numpy().view(np.uint32),
         lambda_q=lam.cpu().numpy(), pair_id=pid.cpu().numpy().view(np.uint16),
     )
+
+
+# ------------------------------------------------------------------------ sharded billion-scale build
+def synth_chunks(n: int, dim: int, blobs: int, sigma: float, seed: int, device="cuda", chunk=1 << 20):
+    """The synth_clustered stream chunk by chunk: yields (start, chunk tensor); the same call
+    yields the same data again (one generator, consumed in the same order)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    means = torch.rand((blobs, dim), generator=g, device=device) * 255.0
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        pick = torch.randint(0, blobs, (e - s,), generator=g, device=device)
+        yield s, means[pick] + sigma * torch.randn((e - s, dim), generator=g, device=device)
+
+
+def synth_queries(nq: int, dim: int, blobs: int, sigma: float, seed: int, query_seed: int, device="cuda"):
+    """Queries from the same blobs as synth_chunks(seed) but an independent sample stream."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    means = torch.rand((blobs, dim), generator=g, device=device) * 255.0
+    gq = torch.Generator(device=device)
+    gq.manual_seed(query_seed)
+    pick = torch.randint(0, blobs, (nq,), generator=gq, device=device)
+    return means[pick] + sigma * torch.randn((nq, dim), generator=gq, device=device)
+
+
+class ShardIndex:
+    """One inverted-list position shard [shard_lo, shard_hi) of an index over n vectors, as a
+    sharded deployment holds it: the whole index's codebooks, tables and offsets, and only this
+    shard's ids and line codes, in position order (pqtg_index_create_shard)."""
+
+    def __init__(self, config, n, level1, level2, d2, slopes, entries, offsets, shard_lo, shard_hi, ids,
+                 lambda_q, pair_id):
+        self.config, self.n = config, n
+        self.level1, self.level2, self.d2 = level1, level2, d2
+        self.slopes, self.entries, self.offsets = slopes, entries, offsets
+        self.shard_lo, self.shard_hi = shard_lo, shard_hi
+        self.ids, self.lambda_q, self.pair_id = ids, lambda_q, pair_id
+
+    def view(self):
+        from .index import PqtgIndexView, _ptr
+
+        v = PqtgIndexView()
+        v.config = self.config.to_c()
+        v.n = self.n
+        v.level1 = _ptr(self.level1)
+        v.level2 = _ptr(self.level2)
+        v.d2 = _ptr(self.d2)
+        v.table_count = len(self.slopes)
+        v.table_len = self.entries.shape[1]
+        v.table_slopes = _ptr(self.slopes)
+        v.table_entries = _ptr(self.entries)
+        v.offsets = _ptr(self.offsets)
+        v.ids = _ptr(self.ids)  # the shard's ids (positions shard_lo ..)
+        v.shard_lo = self.shard_lo
+        v.shard_hi = self.shard_hi
+        return v
+
+
+def build_index_sharded(n: int, blobs: int, sigma: float, seed: int, cfg: PqtConfig, shards: int, rank: int,
+                        ntrain: int, device="cuda", chunk=1 << 20, iters: int | None = None,
+                        tree=None) -> ShardIndex:
+    """Build shard `rank` of `shards` of the index over synth_chunks(n, ...) on one GPU without
+    holding the whole index: pass 1 assigns every vector's bin (exact assign_bin/global_code),
+    a stable sort gives the inverted lists; pass 2 regenerates the stream and encodes only the
+    vectors whose list positions fall in this shard (exact encode_line). With the same trained
+    codebooks (`tree` = (level1, level2); k-means on the GPU is not bit-reproducible), identical
+    for the shard to build_index over all n vectors (tests/test_gpu_topk.py)."""
+    import torch
+
+    from .search import shard_range
+
+    cfg.validate()
+    dev = torch.device(device)
+    H = cfg.resolved_hash_size(n)
+    if tree is None:  # training sample: the stream's first ntrain vectors
+        parts = []
+        got = 0
+        for s, x in synth_chunks(n, cfg.dim, blobs, sigma, seed, dev, chunk):
+            parts.append(x[: ntrain - got])
+            got += parts[-1].shape[0]
+            if got >= ntrain:
+                break
+        train = torch.cat(parts)
+        del parts
+        level1, level2 = train_tree(train, cfg, iters)
+        del train
+    else:
+        level1, level2 = tree
+    sl = fine_slices(level1, cfg.p_line)
+    sq = seq_sqnorm(sl)
+    d2 = pair_d2(sl)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    l1, l2, tsl, tsq, td2 = t(level1), t(level2), t(sl), t(sq), t(d2)
+    c = cfg.to_c()
+    c.hash_size = H
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    L = cfg.p_line
+    # pass 1: bins of all n vectors
+    slots = torch.empty(n, dtype=torch.int32, device=dev)
+    pc = torch.empty((chunk, cfg.p_tree), dtype=torch.int32, device=dev)
+    sl64 = torch.empty(chunk, dtype=torch.int64, device=dev)
+    for s, x in synth_chunks(n, cfg.dim, blobs, sigma, seed, dev, chunk):
+        m = x.shape[0]
+        check(lib().pqtg_build_codes(C.byref(c), l1.data_ptr(), l2.data_ptr(), tsl.data_ptr(), tsq.data_ptr(),
+                                     td2.data_ptr(), x.data_ptr(), m, pc.data_ptr(), sl64.data_ptr(), None, None,
+                                     stream))
+        slots[s:s + m] = sl64[:m].to(torch.int32)
+    counts = torch.bincount(slots, minlength=H)
+    offsets = torch.zeros(H + 1, dtype=torch.int64, device=dev)
+    offsets[1:] = torch.cumsum(counts, 0)
+    del counts
+    order = torch.sort(slots, stable=True).indices  # ascending ids within a slot (pqtree.cpp:40-57)
+    del slots
+    lo, hi = shard_range(n, shards, rank)
+    ids = order[lo:hi].to(torch.int32)
+    del order
+    inv = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    inv[ids.long()] = torch.arange(hi - lo, dtype=torch.int32, device=dev)
+    # pass 2: line codes of this shard's vectors, written at their positions
+    lam = torch.zeros((hi - lo, L), dtype=torch.uint8, device=dev)
+    pid = torch.zeros((hi - lo, L), dtype=torch.int16, device=dev)
+    for s, x in synth_chunks(n, cfg.dim, blobs, sigma, seed, dev, chunk):
+        pos = inv[s:s + x.shape[0]]
+        keep = pos >= 0
+        if not bool(keep.any()):
+            continue
+        xs = x[keep].contiguous()
+        m = xs.shape[0]
+        lc = torch.empty((m, L), dtype=torch.uint8, device=dev)
+        pcd = torch.empty((m, L), dtype=torch.int16, device=dev)
+        check(lib().pqtg_build_codes(C.byref(c), l1.data_ptr(), l2.data_ptr(), tsl.data_ptr(), tsq.data_ptr(),
+                                     td2.data_ptr(), xs.data_ptr(), m, None, None, lc.data_ptr(), pcd.data_ptr(),
+                                     stream))
+        p = pos[keep].long()
+        lam[p] = lc
+        pid[p] = pcd
+    torch.cuda.synchronize(dev)
+    del inv
+    slopes, entries = slope_tables(4096)
+    out_cfg = PqtConfig(**{**cfg.__dict__})
+    out_cfg.hash_size = H
+    return ShardIndex(out_cfg, n, level1, level2, d2, slopes, entries, offsets.cpu().numpy().astype(np.uint64),
+                      lo, hi, ids.cpu().numpy().view(np.uint32), lam.cpu().numpy(), pid.cpu().numpy().view(np.uint16))

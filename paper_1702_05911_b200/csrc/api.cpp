@@ -260,6 +260,38 @@ int pqtg_index_create(const pqtg_index_view* v, int device, pqtg_index** out) {
     });
 }
 
+int pqtg_index_create_shard(const pqtg_index_view* v, const uint8_t* shard_lambda_q, const uint16_t* shard_pair_id,
+                            int device, pqtg_index** out) {
+    return guarded([&] {
+        if (!v || !out) throw Error{PQTG_ERR_ARG, "null argument"};
+        *out = nullptr;
+        validate_config(v->config);
+        const uint64_t n = v->n;
+        if (v->shard_hi <= v->shard_lo || v->shard_hi > n) throw Error{PQTG_ERR_ARG, "bad shard range"};
+        if (!v->level1 || !v->level2 || !v->d2 || !v->offsets || !v->ids || !shard_lambda_q || !shard_pair_id ||
+            (v->table_count && (!v->table_entries || !v->table_slopes)))
+            throw Error{PQTG_ERR_ARG, "index view has null arrays"};
+        Source s;
+        s.cfg = v->config;
+        s.n = n;
+        s.level1 = v->level1;
+        s.level2 = v->level2;
+        s.d2 = v->d2;
+        s.table_count = v->table_count;
+        s.table_len = v->table_len;
+        s.slopes = v->table_slopes;
+        s.entries = v->table_entries;
+        s.offsets = v->offsets;
+        s.ids = v->ids;
+        s.pos_lambda_q = shard_lambda_q;
+        s.pos_pair_id = shard_pair_id;
+        auto* h = new pqtg_index;
+        h->dev.reset(build_device_index(s, device, v->shard_lo, v->shard_hi));
+        *out = h;
+        return PQTG_OK;
+    });
+}
+
 int pqtg_index_load(const char* path, int device, uint64_t shard_lo, uint64_t shard_hi, pqtg_index** out) {
     return guarded([&] {
         if (!path || !out) throw Error{PQTG_ERR_ARG, "null argument"};

@@ -159,15 +159,19 @@ extern "C" int pqtg_build_codes(const pqtg_config* cfg, const float* d_level1, c
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const uint32_t P = cfg->p_tree, L = cfg->p_line;
         const unsigned tb = 128;
-        assign_kernel<<<(unsigned)((n * P + tb - 1) / tb), tb, 0, s>>>(cfg->dim, P, cfg->k1, cfg->k2, d_level1,
-                                                                       d_level2, d_x, n, d_part_codes);
-        PQTG_CUDA_CHECK(cudaGetLastError());
-        global_code_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, (uint64_t)cfg->k1 * cfg->k2, d_part_codes,
-                                                                       n, cfg->hash_size, d_slots);
-        PQTG_CUDA_CHECK(cudaGetLastError());
-        encode_kernel<<<(unsigned)((n * L + tb - 1) / tb), tb, 0, s>>>(cfg->dim, L, cfg->k1, d_fine, d_fine_sq, d_d2,
-                                                                       d_x, n, d_lambda, d_pair);
-        PQTG_CUDA_CHECK(cudaGetLastError());
+        if (d_part_codes && d_slots) {  // bins (NULL: line codes only)
+            assign_kernel<<<(unsigned)((n * P + tb - 1) / tb), tb, 0, s>>>(cfg->dim, P, cfg->k1, cfg->k2, d_level1,
+                                                                           d_level2, d_x, n, d_part_codes);
+            PQTG_CUDA_CHECK(cudaGetLastError());
+            global_code_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+                P, (uint64_t)cfg->k1 * cfg->k2, d_part_codes, n, cfg->hash_size, d_slots);
+            PQTG_CUDA_CHECK(cudaGetLastError());
+        }
+        if (d_lambda && d_pair) {  // line codes (NULL: bins only)
+            encode_kernel<<<(unsigned)((n * L + tb - 1) / tb), tb, 0, s>>>(cfg->dim, L, cfg->k1, d_fine, d_fine_sq,
+                                                                           d_d2, d_x, n, d_lambda, d_pair);
+            PQTG_CUDA_CHECK(cudaGetLastError());
+        }
         return PQTG_OK;
     } catch (const Error& e) {
         set_error(e.msg);

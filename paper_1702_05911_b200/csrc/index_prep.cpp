@@ -394,7 +394,8 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
 
     // --- this shard's ids and line codes in slot order
     const uint64_t npos = shard_hi - shard_lo;
-    p.ids = upload(*ix, src.ids + shard_lo, npos);
+    const uint32_t* shard_ids = src.pos_lambda_q ? src.ids : src.ids + shard_lo;  // shard-only ids: from 0
+    p.ids = upload(*ix, shard_ids, npos);
     {
         uint8_t* dcodes = dev_alloc<uint8_t>(ix->allocations, npos * p.row_bytes + 16, &ix->bytes);
         p.codes = dcodes;
@@ -405,7 +406,7 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
             const uint64_t e = std::min(npos, b + chunk);
             parallel_rows(e - b, [&](uint64_t lo, uint64_t hi) {
                 for (uint64_t r = lo; r < hi; ++r) {
-                    const uint64_t id = src.ids[shard_lo + b + r];
+                    const uint64_t id = shard_ids[b + r];
                     uint8_t* row = stage.data() + r * p.row_bytes;
                     std::memset(row, 0, p.row_bytes);
                     if (id >= n) {
@@ -414,7 +415,10 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
                     }
                     for (uint32_t f = 0; f < L; ++f) {
                         uint32_t lq, pid;
-                        if (src.records) {
+                        if (src.pos_lambda_q) {  // position-ordered shard codes
+                            lq = src.pos_lambda_q[(b + r) * L + f];
+                            pid = src.pos_pair_id[(b + r) * L + f];
+                        } else if (src.records) {
                             const uint8_t* rec = src.records + (id * L + f) * (1 + src.record_pw);
                             lq = rec[0];
                             pid = src.record_pw == 1 ? rec[1] : (uint32_t)rec[1] | ((uint32_t)rec[2] << 8);

@@ -188,6 +188,9 @@ struct Source {
     const uint8_t* lambda_q = nullptr;
     const uint16_t* pair_id = nullptr;
     const uint8_t* records = nullptr;
+    // or the shard's codes in position order (pqtg_index_create_shard)
+    const uint8_t* pos_lambda_q = nullptr;
+    const uint16_t* pos_pair_id = nullptr;
     uint32_t record_pw = 0;
 };
 

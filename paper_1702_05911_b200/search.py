@@ -73,6 +73,10 @@ class DeviceIndex:
             if isinstance(source, HostIndex):
                 view = source.view(*shard)
                 check(L.pqtg_index_create(C.byref(view), device, C.byref(h)))
+            elif hasattr(source, "shard_lo"):  # builder.ShardIndex: one shard, codes by position
+                view = source.view()
+                check(L.pqtg_index_create_shard(C.byref(view), source.lambda_q.ctypes.data,
+                                                source.pair_id.ctypes.data, device, C.byref(h)))
             else:
                 check(L.pqtg_index_load(str(source).encode(), device, shard[0], shard[1], C.byref(h)))
         except PqtgError as e:

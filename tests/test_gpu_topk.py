@@ -138,3 +138,33 @@ def test_gpu_sharded_index_refuses_raw_vectors():
     shard = DeviceIndex(hix, shard=(0, hix.n // 2))
     with pytest.raises(PqtgError):
         shard.attach_database(g["db"])
+
+
+def test_gpu_sharded_build_equals_full_build():
+    """builder.build_index_sharded (two streaming passes, only one shard's ids and codes kept)
+    gives, shard by shard, exactly the device index of the full build restricted to the same
+    position range; the shards' merged top-k equals the unsharded search."""
+    import torch
+
+    from paper_1702_05911_b200 import merge_topk_host
+
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=128, p_tree=4, k1=32, k2=16, w=8, p_line=32, train_iters=4, seed=51,
+                    candidate_budget=2048, hash_size=1 << 20)
+    n, blobs, ntrain, chunk = 300_000, 300, 50_000, 1 << 16
+    X = builder.synth_clustered(n, cfg.dim, blobs, 20.0, 51, device=dev, chunk=chunk)
+    full = builder.build_index(X, X[:ntrain], cfg)
+    Q = builder.synth_queries(40, cfg.dim, blobs, 20.0, 51, 52, device=dev).cpu().numpy()
+    k = 50
+    want = DeviceIndex(full).search(Q, k)
+    parts = []
+    for rank in range(3):
+        sh = builder.build_index_sharded(n, blobs, 20.0, 51, cfg, 3, rank, ntrain, device=dev, chunk=chunk,
+                                         tree=(full.level1, full.level2))
+        got = DeviceIndex(sh).search(Q, k)
+        ref = DeviceIndex(full, shard=(sh.shard_lo, sh.shard_hi)).search(Q, k)
+        assert_same_results(got, ref, f"shard {rank}")
+        parts.append(got)
+    mi, md, mc = merge_topk_host(np.stack([p[0] for p in parts]), np.stack([p[1] for p in parts]),
+                                 np.stack([p[2] for p in parts]))
+    assert_same_results((mi, md, mc, want[3]), want, "merged")
