@@ -60,6 +60,15 @@ WORKLOADS = {
     "sift1b_shard": dict(config=dict(dim=128, p_tree=4, k1=32, k2=16, w=8, p_line=32, candidate_budget=4096,
                                      hash_size=1 << 26),
                          n=125_000_000, nq=10000, k=100, blobs=125_000, sigma=20.0, ntrain=200_000, cache=False),
+    # BASELINE.json configs[3] itself: SIFT1B-shaped 1B x 128-D over 8 GPUs by inverted-list
+    # position (search.cpp's shard_range); this process builds and serves shard (rank % 8) --
+    # codebooks trained on the stream's first 200k vectors, all 1B vectors binned, only the
+    # shard's 125M encoded (builder.build_index_sharded). Each query is searched by every shard,
+    # so one shard's queries/s is the 8-GPU deployment's rate before the merge.
+    "sift1b": dict(config=dict(dim=128, p_tree=4, k1=32, k2=16, w=8, p_line=32, candidate_budget=4096,
+                               hash_size=1 << 26),
+                   n=1_000_000_000, nq=10000, k=100, blobs=1_000_000, sigma=20.0, ntrain=200_000, cache=False,
+                   shards=8),
     "sift1b10m": dict(config=dict(dim=128, p_tree=4, k1=32, k2=16, w=8, p_line=32, candidate_budget=4096,
                                   hash_size=1 << 26),
                       n=10_000_000, nq=10000, k=100, blobs=10_000, sigma=20.0, ntrain=200_000),
@@ -77,7 +86,7 @@ def workload_files(name: str, seed: int):
     return CACHE / f"{name}_s{seed}.pqt", CACHE / f"{name}_s{seed}_queries.npy"
 
 
-def make_workload(name: str, seed: int, device: int, batches: int):
+def make_workload(name: str, seed: int, device: int, batches: int, shards: int | None = None):
     """Build (or load the cached) index + query pool for `name` on cuda:device."""
     import torch
 
@@ -94,6 +103,25 @@ def make_workload(name: str, seed: int, device: int, batches: int):
     t0 = time.time()
     cfg = PqtConfig(train_iters=15, seed=seed, **wl["config"])
     dev = torch.device("cuda", device)
+    if "shards" in wl:  # one position shard of a larger-than-HBM index, built streaming
+        shards = shards or wl["shards"]
+        shard = int(os.environ.get("RANK", "0")) % shards
+        import torch.distributed as dist
+
+        tree = None
+        if dist.is_initialized() and dist.get_world_size() > 1:  # one training, broadcast
+            box = [builder.train_stream_tree(wl["n"], wl["blobs"], wl["sigma"], seed, cfg, wl["ntrain"], dev)
+                   if dist.get_rank() == 0 else None]
+            dist.broadcast_object_list(box, src=0, device=dev)
+            tree = box[0]
+        six = builder.build_index_sharded(wl["n"], wl["blobs"], wl["sigma"], seed, cfg, shards, shard,
+                                          wl["ntrain"], device=dev, tree=tree)
+        q = builder.synth_queries(nq_pool, cfg.dim, wl["blobs"], wl["sigma"], seed, seed + 1000,
+                                  device=dev).cpu().numpy()
+        torch.cuda.empty_cache()
+        log(f"[bench] built {name} shard {shard}/{shards} "
+            f"(positions {six.shard_lo}..{six.shard_hi}) in {time.time() - t0:.1f}s")
+        return six, q
     X = builder.synth_clustered(wl["n"] + nq_pool, cfg.dim, wl["blobs"], wl["sigma"], seed, device=dev)
     db, Q = X[: wl["n"]], X[wl["n"]:]
     g = torch.Generator(device=dev)
@@ -176,7 +204,7 @@ def algorithmic_bytes(hix, counters, stats, k: int):
     nq = len(counters["ncand"])
     W = c.w * c.k2
     pw = hix.pair_width
-    C_q = counters["ncand"].astype(np.float64)
+    C_q = counters["nlocal"].astype(np.float64)  # candidates this index's re-rank scores
     T_q = counters["ntuples"].astype(np.float64)
     bins = stats[:, 0].astype(np.float64)
     stream_entry = {1: 0, 2: 4, 4: 16}[c.p_tree]  # stream words read per probed tuple
@@ -294,6 +322,10 @@ def run_reference(args):
     import torch
 
     wl = WORKLOADS[args.workload]
+    if "shards" in wl:
+        print(json.dumps({"impl": "reference", "unavailable": f"{args.workload} is one shard of a "
+                          "larger-than-HBM index; the reference's CPU path has no shard build"}), flush=True)
+        return
     hix, Qpool = make_workload(args.workload, args.seed, 0, args.batches)
     from oracle.bindings import Oracle, Ref
 
@@ -373,12 +405,16 @@ def main():
 
     wl = WORKLOADS[args.workload]
     nq, k = wl["nq"], wl["k"]
-    if rank == 0:
-        hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * max(world, 1))
-    if world > 1:
+    # a sharded workload under --shard splits its index over the ranks (else: shard rank % 8)
+    shards = world if (args.shard and world > 1) else None
+    if "shards" in wl:  # every rank builds its shard at once (codebooks trained on rank 0)
+        hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * max(world, 1), shards)
+    elif rank == 0:
+        hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * max(world, 1), shards)
+    if world > 1 and "shards" not in wl:
         dist.barrier()
         if rank != 0:
-            hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * world)
+            hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * world, shards)
     lib().pqtg_set_kernel_variant(args.variant)
     if args.shard:
         from paper_1702_05911_b200.sharded import ShardedIndex
@@ -529,7 +565,12 @@ def main():
     # ---- CPU baseline (rank 0, N=1) + parity of the timed batch
     cpu = None
     parity = None
-    if world == 1 and not args.no_cpu_baseline:
+    sharded_wl = "shards" in wl
+    if sharded_wl:
+        cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "port",
+               "sample": "none: the CPU restatement needs the whole index; shard parity is "
+                         "tests/test_gpu_topk.py::test_gpu_sharded_build_equals_full_build"}
+    if world == 1 and not args.no_cpu_baseline and not sharded_wl:
         step(0)
         torch.cuda.synchronize()
         g_ids = d_ids.cpu().numpy().view(np.uint32)
@@ -545,7 +586,7 @@ def main():
         parity = {"queries": nq, "bit_exact_vs": cpu["kind"], "ok": bool(same)}
 
     recall = None
-    if not args.no_recall:
+    if not args.no_recall and not sharded_wl:
         recall = measure_recall(args.workload, args.seed, local, batches[0], nq * args.batches * max(world, 1),
                                 counters_ids(dev, d_q[0], nq, k, step, d_ids, d_counts))
     clocks = clk.summary()

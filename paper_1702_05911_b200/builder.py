@@ -255,6 +255,10 @@ class ShardIndex:
         self.shard_lo, self.shard_hi = shard_lo, shard_hi
         self.ids, self.lambda_q, self.pair_id = ids, lambda_q, pair_id
 
+    @property
+    def pair_width(self) -> int:
+        return 1 if self.config.pair_count <= 256 else 2
+
     def view(self):
         from .index import PqtgIndexView, _ptr
 
@@ -275,6 +279,25 @@ class ShardIndex:
         return v
 
 
+def train_stream_tree(n: int, blobs: int, sigma: float, seed: int, cfg: PqtConfig, ntrain: int, device="cuda",
+                      chunk=1 << 20, iters: int | None = None):
+    """Codebooks (level1, level2) trained on the first ntrain vectors of synth_chunks(n, ...).
+    GPU k-means is not bit-reproducible: a multi-process shard build trains once and
+    broadcasts (bench.py)."""
+    import torch
+
+    parts = []
+    got = 0
+    for _, x in synth_chunks(n, cfg.dim, blobs, sigma, seed, device, chunk):
+        parts.append(x[: ntrain - got])
+        got += parts[-1].shape[0]
+        if got >= ntrain:
+            break
+    train = torch.cat(parts)
+    del parts
+    return train_tree(train, cfg, iters)
+
+
 def build_index_sharded(n: int, blobs: int, sigma: float, seed: int, cfg: PqtConfig, shards: int, rank: int,
                         ntrain: int, device="cuda", chunk=1 << 20, iters: int | None = None,
                         tree=None) -> ShardIndex:
@@ -291,20 +314,8 @@ def build_index_sharded(n: int, blobs: int, sigma: float, seed: int, cfg: PqtCon
     cfg.validate()
     dev = torch.device(device)
     H = cfg.resolved_hash_size(n)
-    if tree is None:  # training sample: the stream's first ntrain vectors
-        parts = []
-        got = 0
-        for s, x in synth_chunks(n, cfg.dim, blobs, sigma, seed, dev, chunk):
-            parts.append(x[: ntrain - got])
-            got += parts[-1].shape[0]
-            if got >= ntrain:
-                break
-        train = torch.cat(parts)
-        del parts
-        level1, level2 = train_tree(train, cfg, iters)
-        del train
-    else:
-        level1, level2 = tree
+    level1, level2 = tree if tree is not None else train_stream_tree(n, blobs, sigma, seed, cfg, ntrain, dev, chunk,
+                                                                     iters)
     sl = fine_slices(level1, cfg.p_line)
     sq = seq_sqnorm(sl)
     d2 = pair_d2(sl)

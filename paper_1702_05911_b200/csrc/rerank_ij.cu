@@ -168,23 +168,64 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
         }
     }
     const uint2 rg0 = tid < R ? __ldg(qr + tid) : make_uint2(0, 0);
+    const bool sharded = p.shard_hi > p.shard_lo;
+    const bool cached = R <= kRangeCache;
+    // a position shard with cached ranges re-ranks only its own candidates: the ranges are
+    // clipped to [shard_lo, shard_hi) and renumbered densely (thread r = range r), so the loop,
+    // the scan and the select run over this shard's candidates only
+    const bool clip = sharded && cached;
+    const uint32_t y1 = clip && tid < R ? (tid + 1 < R ? __ldg(&qr[tid + 1].y) : C) : 0u;
     for (uint32_t i = tid; i < LT * K1M; i += blockDim.x) {
         const uint32_t f = i / K1M, c = i % K1M;
         fine[i] = c < k1 ? fine_in[q * LT * k1 + f * k1 + c] : 0.0f;
     }
     const uint32_t Cpad = (C + kScanItems * kIjThreads - 1) / (kScanItems * kIjThreads) * (kScanItems * kIjThreads);
     for (uint32_t i = tid; i < Cpad / 2; i += blockDim.x) reinterpret_cast<uint32_t*>(rid)[i] = 0;
-    const bool cached = R <= kRangeCache;
     if (tid == 0) {
         s_count = 0;
         s_sel.kand = ~0ull;
         s_sel.kor = 0ull;
     }
     __syncthreads();
-    for (uint32_t r = tid; r < R; r += blockDim.x) {
-        const uint2 rg = r == tid ? rg0 : __ldg(qr + r);
-        rid[rg.y] = (uint16_t)r;
-        if (cached) delta[r] = rg.x - rg.y;
+    uint32_t Cn = C;  // candidates scored by this CTA
+    if (clip) {
+        __shared__ uint32_t wsum[kIjThreads / 32];
+        uint64_t a = 0;
+        uint32_t len = 0;
+        if (tid < R) {
+            const uint64_t x = rg0.x, e = x + (y1 - rg0.y);
+            a = x > p.shard_lo ? x : p.shard_lo;
+            const uint64_t b = e < p.shard_hi ? e : p.shard_hi;
+            len = b > a ? (uint32_t)(b - a) : 0u;
+        }
+        const uint32_t lane = tid & 31, warp = tid >> 5;
+        uint32_t incl = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= (uint32_t)d) incl += v;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        uint32_t off = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kIjThreads / 32; ++w) {
+            const uint32_t v = wsum[w];
+            off += (uint32_t)w < warp ? v : 0u;
+            tot += v;
+        }
+        if (len) {
+            const uint32_t y = off + incl - len;
+            rid[y] = (uint16_t)tid;
+            delta[tid] = (uint32_t)a - y;
+        }
+        Cn = tot;
+    } else {
+        for (uint32_t r = tid; r < R; r += blockDim.x) {
+            const uint2 rg = r == tid ? rg0 : __ldg(qr + r);
+            rid[rg.y] = (uint16_t)r;
+            if (cached) delta[r] = rg.x - rg.y;
+        }
     }
     // T[f][t(i, j)] = (E, c2) for every pair i < j (linequant.cpp:76-82); other entries
     // are never referenced. Thread: one pair, every (blockDim / 128)-th part.
@@ -201,10 +242,9 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
         }
     }
     __syncthreads();
-    range_index_scan<kIjThreads>(rid, C, wmax);
+    range_index_scan<kIjThreads>(rid, Cn, wmax);
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
-    const bool sharded = p.shard_hi > p.shard_lo;
     constexpr int kVec = ((K1M == 16 ? 2 : 3) * LT + 15) / 16;
     uint32_t mine = 0;
     uint32_t kand = ~0u, kor = 0u;  // AND / OR of this thread's orderable distances
@@ -219,7 +259,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
             pos = (uint64_t)rl.x + (j - rl.y);
         }
         id = kInvalid;
-        if (!sharded || (pos >= p.shard_lo && pos < p.shard_hi)) {
+        if (!sharded || clip || (pos >= p.shard_lo && pos < p.shard_hi)) {
             const uint64_t lp = pos - p.shard_lo;
             id = __ldg(p.ids + lp);
             const uint4* r4 = reinterpret_cast<const uint4*>(p.codes + lp * p.row_bytes);
@@ -266,13 +306,13 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
     uint4 va[kVec], vb[kVec];
     uint32_t ida = kInvalid, idb = kInvalid;
     const uint32_t step = blockDim.x;
-    if (tid < C) fetch(tid, va, ida);
-    for (uint32_t j = tid; j < C; j += 2 * step) {
+    if (tid < Cn) fetch(tid, va, ida);
+    for (uint32_t j = tid; j < Cn; j += 2 * step) {
         const uint32_t j2 = j + step;
-        if (j2 < C) fetch(j2, vb, idb);
+        if (j2 < Cn) fetch(j2, vb, idb);
         score(j, va, ida);
-        if (j2 >= C) break;
-        if (j2 + step < C) fetch(j2 + step, va, ida);
+        if (j2 >= Cn) break;
+        if (j2 + step < Cn) fetch(j2 + step, va, ida);
         score(j2, vb, idb);
     }
 #pragma unroll
@@ -294,7 +334,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
     if (kk) {
         for (uint32_t i = tid; i < (1u << kSelBits); i += blockDim.x) hist[i] = 0;
         __syncthreads();
-        m = block_select_wide<kSelBits, kIjThreads>(keys, C, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap, wmax, s_sel);
+        m = block_select_wide<kSelBits, kIjThreads>(keys, Cn, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap, wmax, s_sel);
     }
     block_sort_write(sel, m, kk, k, q, out_ids, out_dists, out_counts);
 }

@@ -189,12 +189,23 @@ class DeviceIndex:
                     positions=[pos[i, : nc[i]] for i in range(nq)], ncand=nc, ntuples=nt)
 
     def counters(self, nq: int) -> dict:
-        """Cheap per-query counters of the last sub-batch: candidates, tuples consumed."""
+        """Cheap per-query counters of the last sub-batch: candidates, tuples consumed, and
+        (`nlocal`) the candidates inside this index's position shard, which are the ones its
+        re-rank scores (all of them when unsharded)."""
         nc = np.zeros(nq, np.uint32)
         nt = np.zeros(nq, np.uint32)
-        check(lib().pqtg_workspace_read(self._ws, nq, None, None, None, None, None, nc.ctypes.data,
-                                        nt.ctypes.data))
-        return dict(ncand=nc, ntuples=nt)
+        lo, hi = int(self.info.shard_lo), int(self.info.shard_hi)
+        if hi > lo and self.config.candidate_budget:
+            pos = np.zeros((nq, self.config.candidate_budget), np.uint32)
+            check(lib().pqtg_workspace_read(self._ws, nq, None, None, None, None, pos.ctypes.data,
+                                            nc.ctypes.data, nt.ctypes.data))
+            valid = np.arange(pos.shape[1])[None, :] < nc[:, None]
+            nl = np.count_nonzero(valid & (pos >= lo) & (pos < hi), axis=1).astype(np.uint32)
+        else:
+            check(lib().pqtg_workspace_read(self._ws, nq, None, None, None, None, None, nc.ctypes.data,
+                                            nt.ctypes.data))
+            nl = nc
+        return dict(ncand=nc, ntuples=nt, nlocal=nl)
 
 
 def load_index(path: str, device: int = 0, shard: tuple[int, int] = (0, 0)) -> DeviceIndex:

@@ -25,15 +25,22 @@ from .search import DeviceIndex, shard_range
 
 
 class ShardedIndex:
-    def __init__(self, hix: HostIndex, group=None, device: int | None = None, max_batch: int = 4096):
+    def __init__(self, hix: "HostIndex | builder.ShardIndex", group=None, device: int | None = None, max_batch: int = 4096):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = torch.cuda.current_device() if device is None else device
-        lo, hi = shard_range(hix.n, self.world, self.rank)
+        if hasattr(hix, "shard_lo"):  # builder.ShardIndex: this rank's shard, built in place
+            lo, hi = shard_range(hix.n, self.world, self.rank)
+            if (lo, hi) != (hix.shard_lo, hix.shard_hi):
+                raise ValueError(f"rank {self.rank} of {self.world} owns positions {lo}..{hi}, "
+                                 f"the shard index holds {hix.shard_lo}..{hix.shard_hi}")
+            self.local = DeviceIndex(hix, device=self.device, max_batch=max_batch)
+        else:
+            lo, hi = shard_range(hix.n, self.world, self.rank)
+            self.local = DeviceIndex(hix, device=self.device, shard=(lo, hi) if self.world > 1 else (0, 0),
+                                     max_batch=max_batch)
         self.shard = (lo, hi)
-        self.local = DeviceIndex(hix, device=self.device, shard=(lo, hi) if self.world > 1 else (0, 0),
-                                 max_batch=max_batch)
         self.n = hix.n
         self.dim = hix.config.dim
         self._bufs = {}
