@@ -373,7 +373,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--variant", type=int, default=0,
-                    help="kernel variant: 0 auto, 1 generic, 2 auto + tensor-core level-2 screen")
+                    help="kernel variant: 0 auto, 1 generic, 2 auto + tensor-core level-2 screen, 3 / 4 auto with the walker-warp / all-warp bin selection forced")
     ap.add_argument("--no-recall", action="store_true")
     ap.add_argument("--chunks", type=int, default=0,
                     help="pieces per batch overlapped on two streams (0 auto, 1 off)")

@@ -132,8 +132,9 @@ int pqtg_abi_version(void);
 const char* pqtg_last_error(void);
 /* Kernel selection, process-wide: 0 = fastest kernel for each stage (default), 1 = the generic
  * kernels only, 2 = the fast kernels with the level-2 distances screened on the tensor cores
- * (tcgen05) and an exact fp32 residual check (screen.cu). The parity tests run all three;
- * search results are identical by construction. */
+ * (tcgen05) and an exact fp32 residual check (screen.cu), 3 / 4 = the fast kernels with the
+ * walker-warp bin selection (binsel_fast.cu) / the all-warp one (binsel_par.cu) forced (0 picks
+ * per index). The parity tests run all five; search results are identical by construction. */
 int pqtg_set_kernel_variant(int variant);
 /* 1 when a CUDA device with compute capability 10.x is usable, else 0. */
 int pqtg_device_ok(int device);

@@ -209,8 +209,9 @@ extern "C" {
 int pqtg_abi_version(void) { return PQTG_ABI_VERSION; }
 
 int pqtg_set_kernel_variant(int variant) {
-    if (variant < 0 || variant > 2) {
-        set_error("variant must be 0 (auto), 1 (generic) or 2 (auto with the tensor-core level-2 screen)");
+    if (variant < 0 || variant > 4) {
+        set_error("variant must be 0 (auto), 1 (generic), 2 (auto with the tensor-core level-2 screen), 3 "
+                  "(auto with the walker-warp bin selection) or 4 (auto with the all-warp bin selection)");
         return PQTG_ERR_ARG;
     }
     g_variant.store(variant);
@@ -394,7 +395,8 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         ws->ncand = dev_alloc<uint32_t>(ws->allocations, B);
         ws->ntuples = dev_alloc<uint32_t>(ws->allocations, B);
         ws->hash_words = binsel_fast_ok(p) ? binsel_hash_words(p, B) : 0;
-        ws->hash_stride = ws->hash_words ? binsel_hash_stride(p) : 0;
+        ws->hash_stride = ws->hash_words ? std::max(binsel_hash_stride(p), binsel_par_hash_stride(p)) : 0;
+        ws->hash_words = ws->hash_stride * B;
         if (ws->hash_words) ws->hash = dev_alloc<uint32_t>(ws->allocations, ws->hash_words);
         if (screen_ok(p)) {
             ws->scr = dev_alloc<float>(ws->allocations, B * p.P * p.scr_nj);

@@ -58,6 +58,10 @@ bool binsel_fast_ok(const DevParams& p) {
            c.smem + 2048 <= (size_t)optin;
 }
 
+bool binsel_prefers_walker(const DevParams& p) {
+    return p.P == 4 && bs_config(p).W2ab > 0;
+}
+
 uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch) {
     const BsConfig c = bs_config(p);
     return c.use_hash ? (max_batch << c.ts_log2) : 0;

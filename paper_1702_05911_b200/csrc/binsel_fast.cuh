@@ -20,6 +20,7 @@ constexpr int kFilterWarps = kBsThreads / 32 - 1;  // warp 0 walks the queue
 constexpr int kFilterThreads = kFilterWarps * 32;
 constexpr int kMaxItems = 8;
 constexpr uint32_t kQueueCap = kFilterThreads * kMaxItems;
+constexpr int kWalkAhead = 4;  // walker batches whose bin extents are in flight
 // the walker's visited set: a shared open-addressing table of slot + 1 (0 = free); past half
 // full it moves to the query's global table, which is sized for the whole budget
 constexpr uint32_t kVisLog2 = 10;
@@ -53,7 +54,7 @@ __host__ __device__ inline BsLayout bs_layout(uint32_t PW, uint32_t W2ab, uint32
     return l;
 }
 
-// One filter pass for one thread: NIT stream positions base + it·224 + ft. Slot = the sum of
+// One filter pass for one thread: NIT stream positions base + it·NT + ft (NT filter threads). Slot = the sum of
 // pre-reduced per-part terms mod H (pqtree.cpp:12-25); non-empty = the slot's bitmap bit.
 // Loads of all items are issued before any is consumed; positions are 32-bit.
 __device__ __forceinline__ uint32_t add_mod_fast(uint32_t a, uint32_t b, uint32_t H) {
@@ -61,14 +62,14 @@ __device__ __forceinline__ uint32_t add_mod_fast(uint32_t a, uint32_t b, uint32_
     return min(x, x - H);      // x - H wraps above x when x < H
 }
 
-template <int P, int NIT>
+template <int P, int NIT, int NT = kFilterThreads>
 __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32_t total, int ft, int lane, int fw,
                                        uint32_t ta, uint32_t tb, uint32_t W, uint32_t H, const uint32_t* terms,
                                        const uint32_t* tA, const uint32_t* tB, uint32_t W2ab, uint32_t* slot,
                                        uint32_t* ball, uint32_t* wcnt) {
     const uint32_t W2 = (uint32_t)p.W2;
     const uint32_t mcount = (uint32_t)p.merge_count;
-    const uint32_t end = base + NIT * kFilterThreads;  // positions of this pass: [base, end)
+    const uint32_t end = base + NIT * NT;  // positions of this pass: [base, end)
     // uniform fast path: the whole pass lies inside the stream and (P = 4) inside the
     // materialized merge prefix, so no item needs a bounds or closed-form check
     const bool fast = end <= total && (P != 4 || (end <= mcount && W2ab && H < 0x80000000u)) &&
@@ -79,32 +80,32 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
             const uint2* mp = p.merge + base + ft;
             uint2 e[NIT];
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) e[it] = __ldg(mp + it * kFilterThreads);
+            for (int it = 0; it < NIT; ++it) e[it] = __ldg(mp + it * NT);
 #pragma unroll
             for (int it = 0; it < NIT; ++it) slot[it] = add_mod_fast(tA[e[it].x], tB[e[it].y], H);
         } else if constexpr (P == 2) {
             const uint32_t* sp = p.pair_streams + (size_t)ta * W2 + base + ft;
             uint32_t e[NIT];
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) e[it] = __ldg(sp + it * kFilterThreads);
+            for (int it = 0; it < NIT; ++it) e[it] = __ldg(sp + it * NT);
 #pragma unroll
             for (int it = 0; it < NIT; ++it) slot[it] = add_mod_fast(terms[e[it] & 0xFFFFu], terms[W + (e[it] >> 16)], H);
         } else {
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) slot[it] = terms[base + it * kFilterThreads + ft];
+            for (int it = 0; it < NIT; ++it) slot[it] = terms[base + it * NT + ft];
         }
 #pragma unroll
         for (int it = 0; it < NIT; ++it) word[it] = __ldg(p.bitmap + (slot[it] >> 5));
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
             ball[it] = __ballot_sync(0xffffffffu, (word[it] >> (slot[it] & 31)) & 1u);
-            if (lane == 0) wcnt[it * kFilterWarps + fw] = __popc(ball[it]);
+            if (lane == 0) wcnt[it * (NT / 32) + fw] = __popc(ball[it]);
         }
     } else {
         uint2 ent[NIT];
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
-            const uint32_t s = base + it * kFilterThreads + ft;
+            const uint32_t s = base + it * NT + ft;
             ent[it] = make_uint2(0, 0);
             if (s < total) {
                 if constexpr (P == 2) {
@@ -122,7 +123,7 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
         }
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
-            const uint32_t s = base + it * kFilterThreads + ft;
+            const uint32_t s = base + it * NT + ft;
             uint32_t sl = 0;
             if constexpr (P == 1) {
                 sl = terms[s < total ? s : 0];
@@ -144,9 +145,9 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
         }
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
-            const uint32_t s = base + it * kFilterThreads + ft;
+            const uint32_t s = base + it * NT + ft;
             ball[it] = __ballot_sync(0xffffffffu, s < total && ((word[it] >> (slot[it] & 31)) & 1u));
-            if (lane == 0) wcnt[it * kFilterWarps + fw] = __popc(ball[it]);
+            if (lane == 0) wcnt[it * (NT / 32) + fw] = __popc(ball[it]);
         }
     }
 #pragma unroll
@@ -170,17 +171,34 @@ __device__ __forceinline__ void walk_queue(const DevParams& p, const uint2* qp, 
     const uint32_t TS = 1u << ts_log2;
     uint32_t c = st.c, r = st.r, maxord = st.maxord, nvis = st.nvis;
     bool spilled = st.spilled;
-        const uint32_t lt = (1u << lane) - 1u;
-        for (uint32_t b0 = 0; b0 < n && c < budget; b0 += 32) {
+    const uint32_t lt = (1u << lane) - 1u;
+    // the bins' extents are loaded kWalkAhead batches ahead: with offsets larger than L2
+    // (H = 2^26) each batch's extents are a DRAM round trip, the walker's critical path
+    uint32_t pf_lo[kWalkAhead], pf_hi[kWalkAhead];
+    auto prefetch = [&](uint32_t b0, int k) {
+        const uint32_t idx = b0 + lane;
+        if (idx < n) {
+            const uint32_t sl = qp[idx].y;
+            pf_lo[k] = __ldg(p.offsets + sl);
+            pf_hi[k] = __ldg(p.offsets + sl + 1);
+        }
+    };
+#pragma unroll
+    for (int k = 0; k < kWalkAhead; ++k) prefetch(k * 32u, k);
+    for (uint32_t g0 = 0; g0 < n && c < budget; g0 += 32u * kWalkAhead) {
+#pragma unroll
+        for (int k = 0; k < kWalkAhead; ++k) {
+            const uint32_t b0 = g0 + 32u * k;
+            if (b0 >= n || c >= budget) break;
             const uint32_t idx = b0 + lane;
             const bool has = idx < n;
             const uint2 e = has ? qp[idx] : make_uint2(0, kEmptyKey);
-            // the bin's extent, loaded before the visited test so the two overlap
             uint32_t start = 0, cnt = 0;
             if (has) {
-                start = __ldg(p.offsets + e.y);
-                cnt = __ldg(p.offsets + e.y + 1) - start;
+                start = pf_lo[k];
+                cnt = pf_hi[k] - start;
             }
+            prefetch(b0 + 32u * kWalkAhead, k);
             bool first = has;
             if (HASH) {
                 const uint32_t grp = __match_any_sync(0xffffffffu, e.y);
@@ -258,6 +276,7 @@ __device__ __forceinline__ void walk_queue(const DevParams& p, const uint2* qp, 
             r += __popc(em);
             c = (uint64_t)c + tot >= budget ? budget : c + tot;
         }
+    }
     st.c = c;
     st.r = r;
     st.maxord = maxord;

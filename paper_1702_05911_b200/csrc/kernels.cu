@@ -441,7 +441,13 @@ size_t binsel_smem(const DevParams& p) {
 void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats,
                    cudaStream_t s) {
     if (kernel_variant() != 1 && binsel_fast_ok(p)) {
-        launch_binsel_fast(p, nq, ws, stats, s);
+        // all-warp passes (binsel_par) unless the stream is the folded P = 4 one (W·W <= 4096,
+        // e.g. GIST1M), whose sparse hits favour overlapping the filter with a walker warp
+        // (measured); variants 3 / 4 force either design
+        const int v = kernel_variant();
+        const bool walker = v == 3 || (v != 4 && binsel_prefers_walker(p));
+        if (walker) launch_binsel_fast(p, nq, ws, stats, s);
+        else launch_binsel_par(p, nq, ws, stats, s);
         return;
     }
     const uint32_t lg = ts_log2_for(p);
@@ -687,6 +693,7 @@ void configure_kernels(const DevParams& p, uint32_t) {
         set_rerank_attr<0, 2>();
         configure_rerank_ij();
         configure_binsel_fast();
+        configure_binsel_par();
         configure_traverse_part();
         configure_exact();
         configure_screen();

@@ -250,6 +250,11 @@ bool binsel_fast_ok(const DevParams& p);
 uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch);
 uint64_t binsel_hash_stride(const DevParams& p);
 void configure_binsel_fast();
+// binsel_par.cu (same contract; all warps finish each pass together, no walker warp)
+void launch_binsel_par(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats, cudaStream_t s);
+uint64_t binsel_par_hash_stride(const DevParams& p);
+bool binsel_prefers_walker(const DevParams& p);  // the auto choice between the two
+void configure_binsel_par();
 void launch_binsel_fast(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats, cudaStream_t s);
 // traverse.cu (one CTA per (query, part), TMA-staged level-2 blocks)
 bool traverse_part_ok(const DevParams& p);

@@ -25,10 +25,9 @@ using namespace dev;
 namespace {
 
 constexpr int kTpThreads = 128;
-constexpr int kFineBatch = 32;  // fine-part codebook values loaded per thread per batch
 
 struct TpLayout {
-    size_t blk, y, fine, l1d, l1o, l2d, l2c, total;
+    size_t blk, y, fine, l1d, l1o, keys, total;
     uint32_t rows;        // t-rows of the parent blocks staged per chunk (multiple of 4)
     uint32_t blk_stride;  // floats per staged parent piece (padded; 16-byte multiple)
 };
@@ -61,17 +60,18 @@ __host__ __device__ inline TpLayout tp_layout(const DevParams& p) {
     o += (size_t)p.k1 * 4;
     l.l1o = o;
     o += (size_t)p.k1 * 4;
-    l.l2d = o;
-    o += (size_t)p.W * 4;
-    l.l2c = o;
-    o += (size_t)p.W * 4;
+    l.keys = (o + 7) & ~size_t(7);  // level-2 sort exchange: one u64 per power-of-two slot
+    uint32_t n2 = 1;
+    while (n2 < p.W) n2 <<= 1;
+    o = l.keys + (size_t)n2 * 8;
     l.total = (o + 15) & ~size_t(15);
     return l;
 }
 
 }  // namespace
 
-template <int K1T, int K2T>
+// FB: fine-part codebook values loaded per thread per batch (8 when fd <= 8, else 32)
+template <int K1T, int K2T, int FB>
 __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, const float* __restrict__ Q,
                                                                    float* __restrict__ fine_out,
                                                                    float* __restrict__ l2d_out,
@@ -86,8 +86,6 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     float* fine = reinterpret_cast<float*>(smem + lay.fine);
     float* l1d = reinterpret_cast<float*>(smem + lay.l1d);
     uint32_t* l1o = reinterpret_cast<uint32_t*>(smem + lay.l1o);
-    float* l2d = reinterpret_cast<float*>(smem + lay.l2d);
-    uint32_t* l2c = reinterpret_cast<uint32_t*>(smem + lay.l2c);
 
     const uint64_t q = blockIdx.x / P;
     const uint32_t part = blockIdx.x - (uint32_t)q * P;
@@ -102,12 +100,12 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     const float* yq = Q + q * p.D + (uint64_t)part * m;
     for (uint32_t t = tid; t < m; t += blockDim.x) y[t] = __ldg(yq + t);
     // first batch of this thread's first fine job, in flight across the barrier
-    float cv[kFineBatch];
+    float cv[FB];
     auto load_batch = [&](uint32_t idx, uint32_t t0) {
         const uint32_t f = f0 + idx / k1, i = idx - (idx / k1) * k1;
         const float* c = p.fine_t + ((size_t)f * fd + t0) * k1 + i;
 #pragma unroll
-        for (int u = 0; u < kFineBatch; ++u) cv[u] = t0 + u < fd ? __ldg(c + (size_t)u * k1) : 0.0f;
+        for (int u = 0; u < FB; ++u) cv[u] = t0 + u < fd ? __ldg(c + (size_t)u * k1) : 0.0f;
     };
     if (tid < jobs) load_batch(tid, 0);
     __syncthreads();
@@ -119,9 +117,9 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
         float acc = 0.0f;
         for (uint32_t t0 = 0;;) {
 #pragma unroll
-            for (int u = 0; u < kFineBatch; ++u)
+            for (int u = 0; u < FB; ++u)
                 if (t0 + u < fd) acc = sq_step(acc, yf[t0 + u], cv[u]);
-            t0 += kFineBatch;
+            t0 += FB;
             if (t0 >= fd) break;
             load_batch(idx, t0);
         }
@@ -177,12 +175,12 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     const uint32_t j = tid;  // W <= blockDim (traverse_part_ok)
     const uint32_t r = j / k2, c = j - r * k2;
     float acc = 0.0f;
-    uint32_t phase[2] = {0u, 0u};
+    uint32_t phases = 0u;  // bit b: buffer b's mbarrier parity
     for (uint32_t ch = 0; ch < nch; ++ch) {
         const uint32_t b = ch & 1u, t0 = ch * rows, nr = m - t0 < rows ? m - t0 : rows;
         if (bulk) {
-            mbar_wait(&mbar[b], phase[b]);
-            phase[b] ^= 1u;
+            mbar_wait(&mbar[b], (phases >> b) & 1u);
+            phases ^= 1u << b;
         } else {
             __syncthreads();
         }
@@ -207,36 +205,52 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
         __syncthreads();  // buffer b is free
         if (ch + 2 < nch) stage(ch + 2);
     }
-    if (j < W) {
-        l2d[j] = acc;
-        l2c[j] = (l1o[r] << 16) | c;
-    }
-    __syncthreads();
-
-    // rank by (dist, parent, child) (pqtree.cpp:112-117)
-    for (uint32_t jj = tid; jj < W; jj += blockDim.x) {
-        const float d = l2d[jj];
-        const uint32_t code = l2c[jj];
-        uint32_t rank = 0;
-        for (uint32_t o = 0; o < W; ++o) {
-            const float dj = l2d[o];
-            const uint32_t cj = l2c[o];
-            rank += (dj < d) || (dj == d && cj < code);
+    // order by (dist, parent, child) (pqtree.cpp:112-117): the keys (orderable(dist) << 32 |
+    // parent << 16 | child) -- distances are sums of squares, never -0 or NaN, so the u64 order
+    // is the reference's -- bitonic-sorted across the block (shuffles below 32, shared memory
+    // above), thread t ends holding rank t
+    uint32_t n2 = 1;
+    while (n2 < W) n2 <<= 1;
+    uint64_t key = ~0ull;
+    if (j < W) key = ((uint64_t)orderable(acc) << 32) | ((l1o[r] << 16) | c);
+    uint64_t* kbuf = reinterpret_cast<uint64_t*>(smem + lay.keys);  // used when n2 > 32
+    for (uint32_t kk = 2; kk <= n2; kk <<= 1) {
+        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+            uint64_t other;
+            if (jj >= 32) {
+                __syncthreads();
+                if (tid < n2) kbuf[tid] = key;
+                __syncthreads();
+                other = tid < n2 ? kbuf[tid ^ jj] : ~0ull;
+            } else {
+                other = __shfl_xor_sync(0xffffffffu, key, jj);
+            }
+            const bool up = (tid & kk) == 0, lower = (tid & jj) == 0;
+            const bool take_min = lower == up;
+            key = (take_min ? (other < key) : (other > key)) ? other : key;
         }
-        const size_t out = (q * P + part) * W + rank;
-        l2d_out[out] = d;
-        l2c_out[out] = code;
+    }
+    if (j < W) {
+        const size_t out = (q * P + part) * W + j;
+        l2d_out[out] = unorderable((uint32_t)(key >> 32));
+        l2c_out[out] = (uint32_t)key;
     }
 }
 
 namespace {
 
+template <int A, int B, int FB>
+void tp_allow1(int optin) {
+    cudaFuncAttributes a{};
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, traverse_part_kernel<A, B, FB>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(traverse_part_kernel<A, B, FB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes));
+}
+
 template <int A, int B>
 void tp_allow(int optin) {
-    cudaFuncAttributes a{};
-    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, traverse_part_kernel<A, B>));
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(traverse_part_kernel<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         optin - (int)a.sharedSizeBytes));
+    tp_allow1<A, B, 8>(optin);
+    tp_allow1<A, B, 32>(optin);
 }
 
 }  // namespace
@@ -265,9 +279,11 @@ void launch_traverse_part(const DevParams& p, const float* queries, uint64_t nq,
                               ? 1u
                               : 0u;
     const unsigned grid = (unsigned)(nq * p.P);
-#define PQTG_TP(A, B)                                                                                   \
-    traverse_part_kernel<A, B><<<grid, kTpThreads, lay.total, s>>>(p, queries, ws.fine, ws.l2_dist, \
-                                                                   ws.l2_code, bulk)
+#define PQTG_TP(A, B)                                                                                         \
+    (p.fd <= 8 ? traverse_part_kernel<A, B, 8><<<grid, kTpThreads, lay.total, s>>>(p, queries, ws.fine, ws.l2_dist, \
+                                                                                   ws.l2_code, bulk)               \
+               : traverse_part_kernel<A, B, 32><<<grid, kTpThreads, lay.total, s>>>(p, queries, ws.fine,          \
+                                                                                    ws.l2_dist, ws.l2_code, bulk))
     if (p.k1 == 16 && p.k2 == 8) PQTG_TP(16, 8);
     else if (p.k1 == 32 && p.k2 == 16) PQTG_TP(32, 16);
     else if (p.k1 == 16 && p.k2 == 16) PQTG_TP(16, 16);

@@ -13,7 +13,7 @@ from paper_1702_05911_b200 import DeviceIndex, HostIndex, knn_query_batch, merge
 pytestmark = pytest.mark.gpu
 
 
-VARIANTS = {"auto": 0, "generic": 1, "tc_screen": 2}
+VARIANTS = {"auto": 0, "generic": 1, "tc_screen": 2, "walker_binsel": 3, "allwarp_binsel": 4}
 
 
 @pytest.fixture(params=list(VARIANTS), autouse=True)

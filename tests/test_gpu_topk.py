@@ -52,21 +52,23 @@ def test_gpu_topk_repeated_vectors():
         assert_same_results(got, want, f"repeated k={k}")
 
 
-def test_gpu_many_small_bins():
-    """P = 4 with (k1·k2)^4 > H (the walker's visited set is needed) and bins of about one
-    vector: ~2000 bins per query overflow the shared visited set into the global table."""
+@pytest.mark.parametrize("budget", [2048, 4096])
+def test_gpu_many_small_bins(budget):
+    """P = 4 with (k1·k2)^4 > H (the visited set is needed) and bins of about one vector:
+    ~2000 / ~4000 bins per query overflow the shared visited sets (binsel_fast: 512 slots,
+    binsel_par: 1536) into the global tables."""
     import torch
 
     dev = torch.device("cuda", 0)
     cfg = PqtConfig(dim=64, p_tree=4, k1=8, k2=8, w=4, p_line=16, train_iters=4, seed=12,
-                    hash_size=1 << 17, candidate_budget=2048)
+                    hash_size=1 << 17, candidate_budget=budget)
     db = builder.synth_clustered(60_000, cfg.dim, 60_000, 20.0, 12, device=dev)  # ~uniform
     hix = builder.build_index(db, db[:20_000], cfg)
     Q = builder.synth_clustered(24, cfg.dim, 64, 20.0, 13, device=dev).cpu().numpy()
     got = DeviceIndex(hix).search(Q, 50)
     want = Oracle(hix).knn(Q, 50)
     assert_same_results(got, want, "small bins")
-    assert (got[3][:, 0] > 600).any()  # bins_visited: past the shared set's 512
+    assert (got[3][:, 0] > (600 if budget == 2048 else 1600)).any()  # bins_visited past the shared sets
 
 
 @pytest.mark.parametrize("k", [10, 100])
