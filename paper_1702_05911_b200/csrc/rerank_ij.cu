@@ -13,6 +13,12 @@
 //     part = (b2 + (λ·λ)·c2) + λ·E      exactly linequant.hpp:83-85's rounding.
 // Shared memory: T (L × 2 KB), fine (L × 64 B), candidate keys, range offsets (cached up to
 // kRangeCache, else read from global memory); ij_threads(L) threads per CTA.
+//
+// DIRECT (k1 <= 32 two-byte codes only): no T. Building T costs L × 496 entries per query, as
+// much as scoring ~500 candidates — the share of a 4096-candidate budget that one of eight
+// position shards re-ranks. DIRECT computes E per part from fine[f][i], fine[f][j] (j from a
+// per-pair table) and c2 = d2[f][pair] (read through L1), the same three roundings, and leaves
+// the shared memory small enough for two CTAs per SM.
 #include <cstdint>
 
 #include "common.cuh"
@@ -53,11 +59,12 @@ __host__ __device__ inline uint32_t ij_sel_cap(uint32_t kk) {
 // fine rows 32 floats.
 __host__ __device__ constexpr uint32_t t_entries(int K1M) { return K1M == 16 ? 256u : 512u; }
 
-__host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint32_t sel_cap, int K1M = 16) {
+__host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint32_t sel_cap, int K1M = 16,
+                                              bool direct = false) {
     IjLayout l{};
     size_t o = 0;
-    l.t = o;  // T, fine, delta and rid sit at compile-time offsets (load immediates)
-    o += (size_t)L * t_entries(K1M) * 8;
+    l.t = o;  // T (DIRECT: the pairs' j, u16), fine, delta and rid sit at compile-time offsets
+    o += direct ? (size_t)t_entries(K1M) * 2 : (size_t)L * t_entries(K1M) * 8;
     l.fine = o;
     o += (size_t)L * K1M * 4;
     l.delta = o;
@@ -118,8 +125,8 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 
 }  // namespace
 
-template <int LT, int K1M>
-__global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 2)
+template <int LT, int K1M, bool DIRECT>
+__global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DIRECT)) ? 1 : 2)
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
@@ -127,14 +134,16 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k1 = p.k1, budget = p.budget;
     constexpr uint32_t TE = t_entries(K1M);
-    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M);
+    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT);
+    const IjLayout fix = ij_layout(LT, 0, 0, K1M, DIRECT);
     float2* T = reinterpret_cast<float2*>(smem);
-    float* fine = reinterpret_cast<float*>(smem + ij_layout(LT, 0, 0, K1M).fine);
+    uint16_t* jt = reinterpret_cast<uint16_t*>(smem);  // DIRECT: j of pair id
+    float* fine = reinterpret_cast<float*>(smem + fix.fine);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + lay.keys);
     uint64_t* sel = reinterpret_cast<uint64_t*>(smem + lay.sel);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0, K1M).rid);  // aliases rid
-    uint16_t* rid = reinterpret_cast<uint16_t*>(smem + ij_layout(LT, 0, 0, K1M).rid);
-    uint32_t* delta = reinterpret_cast<uint32_t*>(smem + ij_layout(LT, 0, 0, K1M).delta);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + fix.rid);  // aliases rid
+    uint16_t* rid = reinterpret_cast<uint16_t*>(smem + fix.rid);
+    uint32_t* delta = reinterpret_cast<uint32_t*>(smem + fix.delta);
     constexpr int kIjThreads = ij_threads(LT);
     __shared__ uint32_t wmax[kIjThreads / 32];
     __shared__ uint32_t s_count;
@@ -158,6 +167,9 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
         const uint32_t pr = __ldg(p.pairs + pi);
         pi_i = pr & 0xFFFFu;
         pi_j = pr >> 16;
+        if constexpr (DIRECT) {
+            if (f0 == 0) jt[pi] = (uint16_t)pi_j;
+        } else
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
             const uint32_t f = f0 + u * kFLanes;
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
     }
     // T[f][t(i, j)] = (E, c2) for every pair i < j (linequant.cpp:76-82); other entries
     // are never referenced. Thread: one pair, every (blockDim / 128)-th part.
-    if (pair_lane) {
+    if (!DIRECT && pair_lane) {
         // the pair's T slot: its device code (K1M = 16) or its pair id (K1M = 32)
         const uint32_t ij = K1M == 16 ? (pi_i << 4 | ((pi_i + pi_j) & 15u)) : pi;
 #pragma unroll
@@ -288,7 +300,14 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
                     fi = v2 >> 9;
                 }
                 const float b2 = fine[f * K1M + fi];
-                const float2 ec = T[f * TE + ti];
+                float2 ec;
+                if constexpr (DIRECT) {  // E and c2 of this part, in T's roundings
+                    const float a2 = fine[f * K1M + jt[ti]];
+                    ec.y = __ldg(p.c2 + f * p.npairs + ti);
+                    ec.x = __fsub_rn(__fsub_rn(a2, b2), ec.y);
+                } else {
+                    ec = T[f * TE + ti];
+                }
                 const float lam = __fmul_rn(__uint2float_rn(lq), inv255);
                 const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), ec.y)), __fmul_rn(lam, ec.x));
                 total = __fadd_rn(total, part);
@@ -341,19 +360,25 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || K1M == 32) ? 1 : 
 
 namespace {
 
-template <int LT, int K1M>
+template <int LT, int K1M, bool DIRECT = false>
 void allow(int optin) {
     cudaFuncAttributes a{};
-    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, rerank_ij_kernel<LT, K1M>));
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_ij_kernel<LT, K1M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         optin - (int)a.sharedSizeBytes));
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, rerank_ij_kernel<LT, K1M, DIRECT>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_ij_kernel<LT, K1M, DIRECT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes));
 }
 
 int code_k1m(const DevParams& p) { return p.code_ij ? 16 : (p.code_pi ? 32 : 0); }
 
+// DIRECT when this index re-ranks a small share of each query's candidates: a position shard
+// holding at most a quarter of the lists (about budget / 4 candidates per query)
+bool ij_direct(const DevParams& p) {
+    return code_k1m(p) == 32 && p.shard_hi > p.shard_lo && (p.shard_hi - p.shard_lo) * 4 <= p.n;
+}
+
 size_t ij_smem(const DevParams& p, uint32_t k) {
     const uint32_t kk = k < p.budget ? k : p.budget;
-    return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16).total;
+    return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16, ij_direct(p)).total;
 }
 
 }  // namespace
@@ -377,6 +402,8 @@ void configure_rerank_ij() {
     allow<64, 16>(optin);
     allow<16, 32>(optin);
     allow<32, 32>(optin);
+    allow<16, 32, true>(optin);
+    allow<32, 32, true>(optin);
 }
 
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids, float* dists,
@@ -384,17 +411,21 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     const uint32_t kk = k < p.budget ? k : p.budget;
     const uint32_t cap = ij_sel_cap(kk);
     const size_t sm = ij_smem(p, k);
-#define PQTG_IJ(LT, K)                                                                                        \
-    rerank_ij_kernel<LT, K><<<(unsigned)nq, ij_threads(LT), sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \
-                                                                   ws.ncand, ids, dists, counts)
+#define PQTG_IJ(LT, K, D)                                                                                     \
+    rerank_ij_kernel<LT, K, D><<<(unsigned)nq, ij_threads(LT), sm, s>>>(p, k, cap, ws.fine, ws.ranges,         \
+                                                                      ws.nranges, ws.ncand, ids, dists, counts)
     if (code_k1m(p) == 32) {
-        if (p.L == 16) PQTG_IJ(16, 32);
-        else PQTG_IJ(32, 32);
+        const bool direct = ij_direct(p);
+        if (p.L == 16) {
+            if (direct) PQTG_IJ(16, 32, true); else PQTG_IJ(16, 32, false);
+        } else {
+            if (direct) PQTG_IJ(32, 32, true); else PQTG_IJ(32, 32, false);
+        }
     } else {
         switch (p.L) {
-        case 16: PQTG_IJ(16, 16); break;
-        case 32: PQTG_IJ(32, 16); break;
-        default: PQTG_IJ(64, 16); break;
+        case 16: PQTG_IJ(16, 16, false); break;
+        case 32: PQTG_IJ(32, 16, false); break;
+        default: PQTG_IJ(64, 16, false); break;
         }
     }
 #undef PQTG_IJ

@@ -214,20 +214,22 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     uint64_t key = ~0ull;
     if (j < W) key = ((uint64_t)orderable(acc) << 32) | ((l1o[r] << 16) | c);
     uint64_t* kbuf = reinterpret_cast<uint64_t*>(smem + lay.keys);  // used when n2 > 32
-    for (uint32_t kk = 2; kk <= n2; kk <<= 1) {
-        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
-            uint64_t other;
-            if (jj >= 32) {
-                __syncthreads();
-                if (tid < n2) kbuf[tid] = key;
-                __syncthreads();
-                other = tid < n2 ? kbuf[tid ^ jj] : ~0ull;
-            } else {
-                other = __shfl_xor_sync(0xffffffffu, key, jj);
+    if (n2 > 32 || tid < 32) {  // W <= 32: warp 0 alone, shuffles only
+        for (uint32_t kk = 2; kk <= n2; kk <<= 1) {
+            for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+                uint64_t other;
+                if (jj >= 32) {  // n2 > 32: every thread of the block is here
+                    __syncthreads();
+                    if (tid < n2) kbuf[tid] = key;
+                    __syncthreads();
+                    other = tid < n2 ? kbuf[tid ^ jj] : ~0ull;
+                } else {
+                    other = __shfl_xor_sync(0xffffffffu, key, jj);
+                }
+                const bool up = (tid & kk) == 0, lower = (tid & jj) == 0;
+                const bool take_min = lower == up;
+                key = (take_min ? (other < key) : (other > key)) ? other : key;
             }
-            const bool up = (tid & kk) == 0, lower = (tid & jj) == 0;
-            const bool take_min = lower == up;
-            key = (take_min ? (other < key) : (other > key)) ? other : key;
         }
     }
     if (j < W) {

@@ -113,6 +113,30 @@ def test_gpu_two_byte_pair_codes(k1, p_tree, p_line):
     assert_same_results(got, want, f"k1={k1}")
 
 
+@pytest.mark.parametrize("k1,p_tree,p_line,shards", [(24, 2, 16, 4), (32, 4, 32, 8), (32, 4, 32, 3)])
+def test_gpu_two_byte_pair_codes_sharded(k1, p_tree, p_line, shards):
+    """Position shards of a 2-byte-pair index: with at most a quarter of the lists per shard
+    the re-rank computes E per part (rerank_ij DIRECT, no per-query table); merged, the shards
+    equal the oracle's unsharded search."""
+    import torch
+
+    from paper_1702_05911_b200 import merge_topk_host, shard_range
+
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=128, p_tree=p_tree, k1=k1, k2=8, w=4, p_line=p_line, train_iters=4, seed=61 + k1,
+                    candidate_budget=2048)
+    X = builder.synth_clustered(90_000 + 40, cfg.dim, 160, 20.0, 61, device=dev)
+    db, Q = X[:90_000], X[90_000:].cpu().numpy()
+    hix = builder.build_index(db, db[:20_000], cfg)
+    want = Oracle(hix).knn(Q, 100)
+    parts = [DeviceIndex(hix, shard=shard_range(hix.n, shards, r)).search(Q, 100) for r in range(shards)]
+    for part in parts:
+        assert np.array_equal(part[3], want[3])
+    mi, md, mc = merge_topk_host(np.stack([x[0] for x in parts]), np.stack([x[1] for x in parts]),
+                                 np.stack([x[2] for x in parts]))
+    assert_same_results((mi, md, mc, want[3]), want, f"k1={k1} shards={shards}")
+
+
 @pytest.mark.parametrize("p_line", [16, 64])
 def test_gpu_line_counts(p_line):
     """The (i, j)-code re-rank at L = 16 and L = 64 (L = 32 is covered by the golden cases)."""
