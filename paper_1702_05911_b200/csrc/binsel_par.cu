@@ -85,7 +85,7 @@ __device__ __forceinline__ uint32_t vis_shared(uint32_t* vkey, uint32_t* vpos, u
         }
         h = (h + 1) & (kPVis - 1);
     }
-    atomicMin(vpos + h, pos);
+    if (*reinterpret_cast<volatile uint32_t*>(vpos + h) > pos) atomicMin(vpos + h, pos);  // only ever lowers
     return h;
 }
 
@@ -102,7 +102,7 @@ __device__ __forceinline__ uint32_t vis_global(uint32_t* gkey, uint32_t* gpos, u
         }
         h = (h + 1) & mask;
     }
-    atomicMin(gpos + h, pos);
+    if (*reinterpret_cast<volatile uint32_t*>(gpos + h) > pos) atomicMin(gpos + h, pos);
     return h;
 }
 

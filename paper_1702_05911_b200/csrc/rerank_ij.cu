@@ -322,17 +322,28 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     };
     // two row buffers in turn: the next candidate's row is in flight while this one is scored,
     // with no register copies between iterations
-    uint4 va[kVec], vb[kVec];
-    uint32_t ida = kInvalid, idb = kInvalid;
     const uint32_t step = blockDim.x;
-    if (tid < Cn) fetch(tid, va, ida);
-    for (uint32_t j = tid; j < Cn; j += 2 * step) {
-        const uint32_t j2 = j + step;
-        if (j2 < Cn) fetch(j2, vb, idb);
-        score(j, va, ida);
-        if (j2 >= Cn) break;
-        if (j2 + step < Cn) fetch(j2 + step, va, ida);
-        score(j2, vb, idb);
+    if constexpr (DIRECT) {
+        // a shard's share of the candidates is about one per thread: one row buffer (the
+        // 64-register budget of two CTAs per SM has no room for a second)
+        uint4 va[kVec];
+        uint32_t ida = kInvalid;
+        for (uint32_t j = tid; j < Cn; j += step) {
+            fetch(j, va, ida);
+            score(j, va, ida);
+        }
+    } else {
+        uint4 va[kVec], vb[kVec];
+        uint32_t ida = kInvalid, idb = kInvalid;
+        if (tid < Cn) fetch(tid, va, ida);
+        for (uint32_t j = tid; j < Cn; j += 2 * step) {
+            const uint32_t j2 = j + step;
+            if (j2 < Cn) fetch(j2, vb, idb);
+            score(j, va, ida);
+            if (j2 >= Cn) break;
+            if (j2 + step < Cn) fetch(j2 + step, va, ida);
+            score(j2, vb, idb);
+        }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {

@@ -68,6 +68,31 @@ __host__ __device__ inline TpLayout tp_layout(const DevParams& p) {
     return l;
 }
 
+// Ascending bitonic sort of N u64 keys, thread t holding key t (t < N; N <= blockDim): the
+// network fully unrolled, partner exchange by shuffle within a warp and through `buf` (N
+// slots) across warps. Every thread of the block calls it when N > 32.
+template <int N>
+__device__ __forceinline__ uint64_t bitonic_block(uint64_t key, uint32_t tid, uint64_t* buf) {
+#pragma unroll
+    for (uint32_t kk = 2; kk <= (uint32_t)N; kk <<= 1) {
+#pragma unroll
+        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+            uint64_t other;
+            if (jj >= 32) {
+                __syncthreads();
+                if (tid < (uint32_t)N) buf[tid] = key;
+                __syncthreads();
+                other = tid < (uint32_t)N ? buf[tid ^ jj] : ~0ull;
+            } else {
+                other = __shfl_xor_sync(0xffffffffu, key, jj);
+            }
+            const bool take_min = ((tid & kk) == 0) == ((tid & jj) == 0);
+            key = (take_min ? (other < key) : (other > key)) ? other : key;
+        }
+    }
+    return key;
+}
+
 }  // namespace
 
 // FB: fine-part codebook values loaded per thread per batch (8 when fd <= 8, else 32)
@@ -209,28 +234,15 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     // parent << 16 | child) -- distances are sums of squares, never -0 or NaN, so the u64 order
     // is the reference's -- bitonic-sorted across the block (shuffles below 32, shared memory
     // above), thread t ends holding rank t
-    uint32_t n2 = 1;
-    while (n2 < W) n2 <<= 1;
     uint64_t key = ~0ull;
     if (j < W) key = ((uint64_t)orderable(acc) << 32) | ((l1o[r] << 16) | c);
-    uint64_t* kbuf = reinterpret_cast<uint64_t*>(smem + lay.keys);  // used when n2 > 32
-    if (n2 > 32 || tid < 32) {  // W <= 32: warp 0 alone, shuffles only
-        for (uint32_t kk = 2; kk <= n2; kk <<= 1) {
-            for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
-                uint64_t other;
-                if (jj >= 32) {  // n2 > 32: every thread of the block is here
-                    __syncthreads();
-                    if (tid < n2) kbuf[tid] = key;
-                    __syncthreads();
-                    other = tid < n2 ? kbuf[tid ^ jj] : ~0ull;
-                } else {
-                    other = __shfl_xor_sync(0xffffffffu, key, jj);
-                }
-                const bool up = (tid & kk) == 0, lower = (tid & jj) == 0;
-                const bool take_min = lower == up;
-                key = (take_min ? (other < key) : (other > key)) ? other : key;
-            }
-        }
+    uint64_t* kbuf = reinterpret_cast<uint64_t*>(smem + lay.keys);  // used when W > 32
+    if (W <= 32) {
+        if (tid < 32) key = bitonic_block<32>(key, tid, kbuf);  // warp 0 alone, shuffles only
+    } else if (W <= 64) {
+        key = bitonic_block<64>(key, tid, kbuf);
+    } else {
+        key = bitonic_block<128>(key, tid, kbuf);
     }
     if (j < W) {
         const size_t out = (q * P + part) * W + j;
