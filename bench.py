@@ -189,6 +189,7 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+            self.nv.nvmlShutdown()
 
     def summary(self):
         if not self.samples:
@@ -245,6 +246,50 @@ def gpu_launches(hix, nq: int, chunks: int) -> int:
     return 3 * (n if nq >= n else 1)  # (+1 per chunk with --exact: exact_rerank_kernel)
 
 
+_ALL_CPUS = None  # the process's CPUs before pin_to_gpu_numa (the CPU legs use all of them)
+
+
+def pin_to_gpu_numa(device: int):
+    """Restrict this process to the CPUs NVML reports as local to the GPU, so pinned host
+    buffers (first-touched here) live on the GPU's NUMA node. Returns the CPU count, or None."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        global _ALL_CPUS
+        _ALL_CPUS = set(os.sched_getaffinity(0))
+        cpus &= _ALL_CPUS
+        pynvml.nvmlShutdown()
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception as e:  # pragma: no cover
+        log(f"[bench] NUMA pinning skipped: {e}")
+    return None
+
+
+def link_bandwidth(h_src, d_dst, h_dst, d_src, reps: int = 20):
+    """Pinned host<->device copy bandwidth of this box (GB/s) at the step's own buffer sizes:
+    the ceiling the e2e number is held against."""
+    import torch
+
+    out = {}
+    for name, dst, src in (("h2d", d_dst, h_src), ("d2h", h_dst, d_src)):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        out[name] = src.numel() * src.element_size() * reps / (a.elapsed_time(b) / 1000.0) / 1e9
+    return out
+
+
 # --------------------------------------------------------------------------- recall
 def counters_ids(dev, dq, nq, k, step, d_ids, d_counts):
     import torch
@@ -295,6 +340,8 @@ def cpu_leg(hix, Q, k, min_seconds=10.0, max_reps=20, db=None):
     (with the raw vectors attached when db is given: the exact re-rank stage)."""
     from oracle.bindings import Oracle, Ref
 
+    if _ALL_CPUS:  # undo the GPU-side NUMA pinning: the reference gets every host core
+        os.sched_setaffinity(0, _ALL_CPUS)
     threads = os.cpu_count() or 1
     if Ref.available():
         impl, kind = Ref.from_host(hix), "reference"
@@ -396,6 +443,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    affinity = pin_to_gpu_numa(local)  # host buffers on the GPU's NUMA node (H2D varies 2x otherwise)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -467,6 +515,8 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # (NVML is shut down again on exit: while initialised it slows the host-side CUDA calls of
+    # the e2e loop by ~40%, 300 -> 420 us per GIST1M step, measured)
     with ClockSampler(local) as clk:
         for s in range(args.steps):
             if not args.no_flush:
@@ -523,19 +573,24 @@ def main():
         host_step(b)
     e2e_steps = max(args.steps // 2, 10)
     e2e_t = 0.0
+    e2e_each = []
     for s in range(e2e_steps):
         if not args.no_flush:
             flush.fill_(s & 0xFF)
             torch.cuda.synchronize()
         t0 = time.perf_counter()
         host_step(s % args.batches)
-        e2e_t += time.perf_counter() - t0
+        e2e_each.append(time.perf_counter() - t0)
+        e2e_t += e2e_each[-1]
+    log(f"[bench] e2e step us: median {np.median(e2e_each) * 1e6:.1f} mean {np.mean(e2e_each) * 1e6:.1f} "
+        f"p90 {np.percentile(e2e_each, 90) * 1e6:.1f} max {np.max(e2e_each) * 1e6:.1f}")
     tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_value = jobs * nq * e2e_steps / float(tt.item())
     h2d = nq * hix.config.dim * 4
     d2h = nq * k * 8 + nq * 4 + nq * 24
+    link = link_bandwidth(hq[0], d_q[0], h_ids, d_ids)
 
     if rank != 0:
         if world > 1:
@@ -600,7 +655,9 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write)" if not args.no_flush else "not flushed",
                    "parallelism": (f"position shards x{world} (NCCL broadcast + all-gather + merge)"
                                    if args.shard else f"replicas x{world}")},
-        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "link_gbs": link, "host_cpus": affinity,
+                "transfer_bound_qps": nq / (h2d / (link["h2d"] * 1e9) + d2h / (link["d2h"] * 1e9))},
         "gpu_launches": gpu_launches(hix, nq, args.chunks) * args.steps * (4 if args.exact else 3) // 3,
         "roofline": roofline,
         "cpu_baseline": cpu,
