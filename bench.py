@@ -455,6 +455,9 @@ def main():
     nq, k = wl["nq"], wl["k"]
     # a sharded workload under --shard splits its index over the ranks (else: shard rank % 8)
     shards = world if (args.shard and world > 1) else None
+    if args.shard and "shards" in wl and world == 1:
+        raise SystemExit(f"--shard on {args.workload} splits the index over the ranks: run it under torchrun with "
+                         f">= 2 ranks (without --shard one process serves shard 0 of {wl['shards']})")
     if "shards" in wl:  # every rank builds its shard at once (codebooks trained on rank 0)
         hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * max(world, 1), shards)
     elif rank == 0:
