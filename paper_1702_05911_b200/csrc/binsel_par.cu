@@ -28,10 +28,8 @@ using namespace bsf;
 
 namespace bsp {
 
-constexpr int kPThreads = 256;
-constexpr int kPWarps = kPThreads / 32;
 constexpr int kPItems = 8;
-constexpr uint32_t kPass = kPThreads * kPItems;       // stream positions per full pass
+constexpr uint32_t kPassMax = 256 * kPItems;         // stream positions per full pass
 constexpr uint32_t kPVisLog2 = 11;
 constexpr uint32_t kPVis = 1u << kPVisLog2;          // shared visited-set entries
 constexpr uint32_t kPVisMax = kPVis * 3 / 4;         // distinct slots before the set moves to global
@@ -62,7 +60,7 @@ __host__ __device__ inline Layout layout(uint32_t PW, uint32_t W2ab, bool hash) 
 // distinct non-empty slot seen before the budget is reached (<= budget) plus one pass
 __host__ __device__ inline uint32_t ts_log2_for(uint32_t budget) {
     uint32_t lg = 6;
-    while ((1ull << lg) < ((uint64_t)budget + kPass + 32) * 3 / 2) ++lg;
+    while ((1ull << lg) < ((uint64_t)budget + kPassMax + 32) * 3 / 2) ++lg;
     return lg;
 }
 
@@ -108,14 +106,18 @@ __device__ __forceinline__ uint32_t vis_global(uint32_t* gkey, uint32_t* gpos, u
 
 }  // namespace bsp
 
-template <int P, bool HASH>
-__global__ void __launch_bounds__(bsp::kPThreads, 4)
+// NT threads per CTA: 256, four CTAs per SM. (512-thread CTAs, passes twice as long at two CTAs
+// per SM, measured slower on every workload: GIST1M 77 -> 82 us, SIFT1M 63 -> 133 us, SIFT1B
+// 332 -> 737 us per batch -- most queries need one or two passes, so the longer pass is wasted.)
+template <int P, bool HASH, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT)
     binsel_par_kernel(DevParams p, const uint32_t* __restrict__ l2c_in, const float* __restrict__ l2d_in,
                       uint8_t* __restrict__ slope_out, uint2* __restrict__ ranges, uint32_t* __restrict__ nranges,
                       uint32_t* __restrict__ ncand, uint32_t* __restrict__ ntuples,
                       pqtg_query_stats* __restrict__ stats, uint32_t ts_log2, uint32_t* __restrict__ ghash,
                       uint32_t W2ab) {
     using namespace bsp;
+    constexpr int kPThreads = NT, kPWarps = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t q = blockIdx.x;
@@ -268,38 +270,48 @@ __global__ void __launch_bounds__(bsp::kPThreads, 4)
             }
         }
         __syncthreads();
-        // every warp scans the <= 64 (item, warp) totals itself
+        // every warp scans the <= kPItems·kPWarps (item, warp) totals itself: entry r·32 + lane
+        // of row r, rows in stream order; xc / xf = exclusive prefixes over all rows
+        constexpr int kRows = kPItems * kPWarps / 32;
         const uint32_t ne = nit * kPWarps;
-        const uint32_t c0 = lane < ne ? s_cnt[pb][lane] : 0u, c1 = lane + 32 < ne ? s_cnt[pb][lane + 32] : 0u;
-        const uint32_t f0 = lane < ne ? s_fst[pb][lane] : 0u, f1 = lane + 32 < ne ? s_fst[pb][lane + 32] : 0u;
-        uint32_t ic0 = c0, ic1 = c1, if0 = f0, if1 = f1;
+        uint32_t xcr[kRows], xfr[kRows];
+        uint32_t ccarry = 0, fcarry = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t a = __shfl_up_sync(0xffffffffu, ic0, o), b = __shfl_up_sync(0xffffffffu, ic1, o);
-            const uint32_t c = __shfl_up_sync(0xffffffffu, if0, o), d = __shfl_up_sync(0xffffffffu, if1, o);
-            if (lane >= (uint32_t)o) {
-                ic0 += a;
-                ic1 += b;
-                if0 += c;
-                if1 += d;
+        for (int r = 0; r < kRows; ++r) {
+            const uint32_t e = r * 32 + lane;
+            const uint32_t cv = e < ne ? s_cnt[pb][e] : 0u, fv = e < ne ? s_fst[pb][e] : 0u;
+            uint32_t ic = cv, iff = fv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t a = __shfl_up_sync(0xffffffffu, ic, o), b = __shfl_up_sync(0xffffffffu, iff, o);
+                if (lane >= (uint32_t)o) {
+                    ic += a;
+                    iff += b;
+                }
             }
+            xcr[r] = ccarry + ic - cv;
+            xfr[r] = fcarry + iff - fv;
+            ccarry += __shfl_sync(0xffffffffu, ic, 31);  // bins of one pass hold < 2^32 ids
+            fcarry += __shfl_sync(0xffffffffu, iff, 31);
         }
-        const uint32_t ccarry = __shfl_sync(0xffffffffu, ic0, 31), fcarry = __shfl_sync(0xffffffffu, if0, 31);
-        const uint64_t ctot = (uint64_t)ccarry + __shfl_sync(0xffffffffu, ic1, 31);
-        const uint32_t ftot = fcarry + __shfl_sync(0xffffffffu, if1, 31);
+        const uint64_t ctot = ccarry;
+        const uint32_t ftot = fcarry;
         done = (uint64_t)C + ctot >= budget;
 #pragma unroll
         for (int it = 0; it < kPItems; ++it) {
             const bool fst = (first >> it) & 1u;
             const uint32_t fb = __ballot_sync(0xffffffffu, fst);
             if (it < (int)nit && fb) {
-                const uint32_t e = it * kPWarps + warp, src = e & 31u;
-                const uint32_t xc0 = __shfl_sync(0xffffffffu, ic0 - c0, src);
-                const uint32_t xc1 = __shfl_sync(0xffffffffu, ic1 - c1, src);
-                const uint32_t xf0 = __shfl_sync(0xffffffffu, if0 - f0, src);
-                const uint32_t xf1 = __shfl_sync(0xffffffffu, if1 - f1, src);
-                const uint64_t ec = e < 32 ? xc0 : (uint64_t)ccarry + xc1;
-                const uint32_t ef = e < 32 ? xf0 : fcarry + xf1;
+                const uint32_t e = it * kPWarps + warp, src = e & 31u, row = e >> 5;  // warp-uniform
+                uint32_t sc = 0, sf = 0;
+#pragma unroll
+                for (int r = 0; r < kRows; ++r)
+                    if ((uint32_t)r == row) {
+                        sc = xcr[r];
+                        sf = xfr[r];
+                    }
+                const uint64_t ec = __shfl_sync(0xffffffffu, sc, src);
+                const uint32_t ef = __shfl_sync(0xffffffffu, sf, src);
                 const uint64_t before = (uint64_t)C + ec + (inc[it] - cn[it]);
                 const bool emit = fst && before < budget;
                 if (emit) qranges[R + ef + __popc(fb & lt)] = make_uint2(st[it], (uint32_t)before);
@@ -339,15 +351,20 @@ __global__ void __launch_bounds__(bsp::kPThreads, 4)
 
 namespace {
 
-template <int P, bool HASH>
-void configure_par_one() {
+template <int P, bool HASH, int NT>
+void configure_par_nt() {
     int dev = 0, optin = 0;
     PQTG_CUDA_CHECK(cudaGetDevice(&dev));
     PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes a{};
-    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, binsel_par_kernel<P, HASH>));
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_par_kernel<P, HASH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         optin - (int)a.sharedSizeBytes));
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, binsel_par_kernel<P, HASH, NT>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(binsel_par_kernel<P, HASH, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes));
+}
+
+template <int P, bool HASH>
+void configure_par_one() {
+    configure_par_nt<P, HASH, 256>();
 }
 
 }  // namespace
@@ -368,10 +385,10 @@ void launch_binsel_par(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_
     const BsConfig c = bs_config(p);
     const uint32_t lg = bsp::ts_log2_for(p.budget);
     const size_t smem = bsp::layout(p.P * p.W, c.W2ab, c.use_hash).total;
-#define PQTG_BP(PP, HH)                                                                                       \
-    binsel_par_kernel<PP, HH><<<(unsigned)nq, bsp::kPThreads, smem, s>>>(p, ws.l2_code, ws.l2_dist, ws.slope,     \
-                                                                        ws.ranges, ws.nranges, ws.ncand,         \
-                                                                        ws.ntuples, stats, lg, ws.hash, c.W2ab)
+#define PQTG_BP(PP, HH)                                                                                      \
+    binsel_par_kernel<PP, HH, 256><<<(unsigned)nq, 256, smem, s>>>(p, ws.l2_code, ws.l2_dist, ws.slope, ws.ranges, \
+                                                                  ws.nranges, ws.ncand, ws.ntuples, stats, lg,   \
+                                                                  ws.hash, c.W2ab)
     if (p.P == 1) {
         PQTG_BP(1, false);
     } else if (p.P == 2) {
