@@ -22,9 +22,10 @@
  * pqt::FormatError, like the reference (src/search.cpp:264-266, src/codebook.cpp:15-35,
  * src/index_io.cpp:28-42,155-165,211-213).
  *
- * There is no CPU fallback: configurations the GPU path does not implement (p_tree not in
- * {1,2,4}, or slope tables missing so the reference would use its exact Dijkstra order,
- * src/binorder.cpp:242-244) return PQTG_ERR_UNSUPPORTED.
+ * There is no CPU fallback: configurations the GPU path does not implement (p_tree > 8; an
+ * exact-order tuple wider than 64 bits; an exact Dijkstra-order frontier larger than the
+ * shared-memory heap -- src/binorder.cpp:114-167, used for p_tree not in {1,2,4} or without
+ * slope tables) return PQTG_ERR_UNSUPPORTED.
  */
 #ifndef PQTG_H
 #define PQTG_H

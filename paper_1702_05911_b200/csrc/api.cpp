@@ -579,11 +579,22 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
             }
             return a.type == cudaMemoryTypeHost;
         };
+        // exact bin order: a query whose heap outgrew shared memory reports ntuples = ~0
+        // (kernels.cu exact_fill); checked on the last sub-batch
+        auto check_exact = [&] {
+            if (!d.prm.exact_order || ws.last_nq == 0) return;
+            std::vector<uint32_t> nt(ws.last_nq);
+            PQTG_CUDA_CHECK(cudaMemcpy(nt.data(), ws.ntuples, nt.size() * 4, cudaMemcpyDeviceToHost));
+            for (uint32_t v : nt)
+                if (v == 0xFFFFFFFFu)
+                    throw Error{PQTG_ERR_UNSUPPORTED, "exact bin order: the tuple heap outgrew shared memory"};
+        };
         if (no_graph || nq == 0 || !pinned(queries) || !pinned(ids) || !pinned(dists) || !pinned(counts) ||
             !pinned(stats)) {
             enqueue();
             PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
             PQTG_CUDA_CHECK(cudaStreamSynchronize(st[1]));
+            check_exact();
             return PQTG_OK;
         }
         const uint64_t key[12] = {(uint64_t)(uintptr_t)queries, nq, k, (uint64_t)(uintptr_t)ids,
@@ -631,6 +642,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         hit->used = ++ws.graph_clock;
         PQTG_CUDA_CHECK(cudaGraphLaunch(hit->exec, st[0]));
         PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
+        check_exact();
         return PQTG_OK;
     });
 }

@@ -54,7 +54,7 @@ bool binsel_fast_ok(const DevParams& p) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const BsConfig c = bs_config(p);
-    return !p.resort && p.mod_fast && p.H < 0xFFFFFFFFull && (!c.use_hash || p.H <= (1ull << 26)) &&
+    return !p.resort && !p.exact_order && p.mod_fast && p.H < 0xFFFFFFFFull && (!c.use_hash || p.H <= (1ull << 26)) &&
            c.smem + 2048 <= (size_t)optin;
 }
 

@@ -192,13 +192,18 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     const uint64_t H = c.hash_size;
 
     // --- GPU-path limits (valid reference configs outside them are reported, not emulated)
-    if (!(P == 1 || P == 2 || P == 4)) unsupported("p_tree must be 1, 2 or 4 (other part counts use the exact order)");
-    if (P > 1 && src.table_count != kSlopeTables) unsupported("slope tables missing: the reference would use the exact order");
+    // part counts without a precomputed heuristic, or an index without its slope tables, use
+    // the exact order (binorder.cpp:242-244)
+    const bool exact_order = !(P == 1 || P == 2 || P == 4) || (P > 1 && src.table_count != kSlopeTables);
+    if (P > 8) unsupported("p_tree must be <= 8");
     if (k1 > 65535 || k2 > 65535) unsupported("k1 and k2 must be < 65536");
     if (W64 > 65535) unsupported("w*k2 must be < 65536");
     if (n >= (1ull << 32)) unsupported("n must be < 2^32");
     if (H == 0 || H >= 0xFFFFFFFFull) unsupported("hash_size must be in [1, 2^32-1)");
     const uint32_t W = (uint32_t)W64;
+    uint32_t tuple_bits = 1;
+    while ((1ull << tuple_bits) < W) ++tuple_bits;
+    if (exact_order && (uint64_t)tuple_bits * P > 64) unsupported("exact bin order: P * ceil(log2(w*k2)) > 64");
     const uint32_t npairs = k1 <= 1 ? 1u : k1 * (k1 - 1) / 2;
     const uint32_t pw = npairs <= 256 ? 1u : 2u;  // index_io.cpp:132
     if (npairs > 65536) unsupported("k1 too large for 16-bit pair ids");
@@ -246,6 +251,8 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     p.log108 = std::log(1.08);  // glibc, as in binorder.cpp:62
     p.inv_log108 = 1.0 / p.log108;
     p.h_pow2 = (H & (H - 1)) == 0;
+    p.exact_order = exact_order ? 1u : 0u;
+    p.tuple_bits = tuple_bits;
 
     // positional multipliers (pqtree.cpp:12-21) and whether the u64 code can wrap
     const uint64_t base = (uint64_t)k1 * k2;
@@ -341,7 +348,12 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     }
 
     // --- static bin-order streams (binorder.cpp:178-283)
-    {
+    if (exact_order) {  // BinStream::total = the saturating product of the list lengths
+        p.W2 = (uint64_t)W * W;
+        uint64_t t = 1;
+        for (uint32_t q = 0; q < P; ++q) t = t > (1ull << 62) / W ? (1ull << 62) : t * W;
+        p.total_tuples = t;
+    } else {
         HostStreams hs = build_streams(src.entries, src.table_len, W, P);
         p.W2 = hs.W2;
         p.total_tuples = hs.total;

@@ -174,6 +174,115 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t slot, uint32_t shift) {
     return (slot * 0x9E3779B1u) >> shift;
 }
 
+// The slot of a rank tuple (pqtree.cpp:12-25): the positional code sum (u64 wrap) mod H, from
+// the per-part terms (flat code · (k1k2)^p, reduced mod H when mod_fast).
+__device__ __forceinline__ uint64_t slot_of_ranks(const DevParams& p, const uint32_t* r, const uint64_t* terms) {
+    uint64_t code = 0;
+    for (uint32_t q = 0; q < p.P; ++q) code += terms[q * p.W + r[q]];
+    if (p.h_pow2) return code & (p.H - 1);
+    if (p.mod_fast) {  // terms already reduced mod H, sum < P*H
+        while (code >= p.H) code -= p.H;
+        return code;
+    }
+    return code % p.H;
+}
+
+// ---- exact order (binorder.cpp:114-167): every tuple in ascending (fp64 sum of its list
+// distances, tuple) order. A min-heap in shared memory on one thread; each tuple is pushed once,
+// by its canonical parent (the tuple minus one at its last non-zero rank: its sum is not larger
+// and it is lexicographically smaller, so it pops first), which emits the reference's sequence
+// without its visited set. Tuples are packed big-endian, tuple_bits per rank, so u64 order is
+// the lexicographic order.
+struct ExactHeap {
+    double* sum;
+    uint64_t* tup;
+    uint32_t cap;
+};
+
+__device__ __forceinline__ bool exact_less(const ExactHeap& h, uint32_t a, uint32_t b) {
+    return h.sum[a] < h.sum[b] || (h.sum[a] == h.sum[b] && h.tup[a] < h.tup[b]);
+}
+
+__device__ __forceinline__ double exact_sum(const DevParams& p, uint64_t t, const float* dl) {
+    const uint32_t B = p.tuple_bits, mask = (1u << B) - 1u;
+    double s = 0.0;  // BinStream's sum_of: fp64, parts in order
+    for (uint32_t q = 0; q < p.P; ++q) {
+        const uint32_t r = (uint32_t)(t >> ((p.P - 1 - q) * B)) & mask;
+        s = __dadd_rn(s, (double)dl[q * p.W + r]);
+    }
+    return s;
+}
+
+// push; false when the heap is full
+__device__ __forceinline__ bool exact_push(ExactHeap& h, uint32_t& n, double sum, uint64_t t) {
+    if (n >= h.cap) return false;
+    uint32_t i = n++;
+    h.sum[i] = sum;
+    h.tup[i] = t;
+    while (i > 0) {
+        const uint32_t par = (i - 1) >> 1;
+        if (!exact_less(h, i, par)) break;
+        const double ds = h.sum[i];
+        const uint64_t dt = h.tup[i];
+        h.sum[i] = h.sum[par];
+        h.tup[i] = h.tup[par];
+        h.sum[par] = ds;
+        h.tup[par] = dt;
+        i = par;
+    }
+    return true;
+}
+
+// the next `want` tuples of the exact order into out; returns how many (fewer at the end of the
+// stream or, with *overflow set, when the heap is full)
+__device__ uint32_t exact_fill(const DevParams& p, ExactHeap& h, uint32_t& n, const float* dl, uint64_t* out,
+                               uint32_t want, uint32_t* overflow) {
+    const uint32_t B = p.tuple_bits, mask = (1u << B) - 1u, P = p.P;
+    uint32_t got = 0;
+    while (got < want && n > 0) {
+        const uint64_t t = h.tup[0];
+        out[got++] = t;
+        // pop
+        --n;
+        h.sum[0] = h.sum[n];
+        h.tup[0] = h.tup[n];
+        for (uint32_t i = 0;;) {
+            const uint32_t l = 2 * i + 1, r = l + 1;
+            uint32_t m = i;
+            if (l < n && exact_less(h, l, m)) m = l;
+            if (r < n && exact_less(h, r, m)) m = r;
+            if (m == i) break;
+            const double ds = h.sum[i];
+            const uint64_t dt = h.tup[i];
+            h.sum[i] = h.sum[m];
+            h.tup[i] = h.tup[m];
+            h.sum[m] = ds;
+            h.tup[m] = dt;
+            i = m;
+        }
+        // children: +1 at every part from the last non-zero rank on
+        uint32_t j = 0;
+        for (uint32_t q = 0; q < P; ++q)
+            if ((t >> ((P - 1 - q) * B)) & mask) j = q;
+        for (uint32_t q = j; q < P; ++q) {
+            const uint32_t sh = (P - 1 - q) * B;
+            if (((t >> sh) & mask) + 1 < p.W) {
+                const uint64_t c = t + (1ull << sh);
+                if (!exact_push(h, n, exact_sum(p, c, dl), c)) {
+                    *overflow = 1;
+                    return got;
+                }
+            }
+        }
+    }
+    return got;
+}
+
+__device__ __forceinline__ void exact_ranks(const DevParams& p, uint64_t t, uint32_t* r) {
+    const uint32_t B = p.tuple_bits, mask = (1u << B) - 1u;
+    for (uint32_t q = 0; q < p.P; ++q) r[q] = (uint32_t)(t >> ((p.P - 1 - q) * B)) & mask;
+}
+
 // Stream tuple at position s -> the slot it addresses (binorder.cpp:251-283, pqtree.cpp:12-25).
 __device__ __forceinline__ uint64_t tuple_slot(const DevParams& p, uint64_t s, uint32_t ta, uint32_t tb,
                                                const uint64_t* terms) {
@@ -216,7 +325,7 @@ __device__ __forceinline__ uint64_t tuple_slot(const DevParams& p, uint64_t s, u
 
 }  // namespace
 
-template <int ITEMS, bool RESORT>
+template <int ITEMS, bool RESORT, bool EXACT>
 __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const float* __restrict__ l2d_in,
                                                           const uint32_t* __restrict__ l2c_in,
                                                           uint8_t* __restrict__ slope_out,
@@ -225,7 +334,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                                                           uint32_t* __restrict__ ncand,
                                                           uint32_t* __restrict__ ntuples,
                                                           pqtg_query_stats* __restrict__ stats,
-                                                          uint32_t ts_log2) {
+                                                          uint32_t ts_log2, uint32_t heap_cap) {
     using Sort = cub::BlockRadixSort<uint32_t, kThreads, ITEMS, uint32_t>;
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t PW_ = p.P * p.W;
@@ -236,7 +345,12 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
     float* dl = reinterpret_cast<float*>(warp_sums + 32);
     uint32_t* hkeys = reinterpret_cast<uint32_t*>(dl + PW_);
     uint32_t* hvals = hkeys + TS;
-    __shared__ uint32_t s_emitted, s_maxord;
+    // EXACT: this chunk's tuples, then the heap (8-byte aligned after the u32 tables)
+    uint64_t* tbuf = reinterpret_cast<uint64_t*>(
+        smem + (((size_t)(reinterpret_cast<unsigned char*>(hvals + TS) - smem) + 7) & ~size_t(7)));
+    ExactHeap heap{reinterpret_cast<double*>(tbuf + kThreads * ITEMS), nullptr, heap_cap};
+    heap.tup = reinterpret_cast<uint64_t*>(heap.sum + heap_cap);
+    __shared__ uint32_t s_emitted, s_maxord, s_got, s_overflow, s_heap_n;
     __shared__ typename Sort::TempStorage sort_tmp;
 
     const uint64_t q = blockIdx.x;
@@ -256,7 +370,11 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         hvals[i] = 0xFFFFFFFFu;
     }
     __shared__ uint32_t s_slope[2];
-    if (tid == 0) s_maxord = 0;
+    if (tid == 0) {
+        s_maxord = 0;
+        s_overflow = 0;
+        s_heap_n = 0;
+    }
     if ((tid & 31) == 0 && tid < 64) {  // pick_slope_table (binorder.cpp:52-65), one pair per warp
         const uint32_t pr = tid >> 5, t = query_slope(p, l2d_in + q * PW_, pr);
         s_slope[pr] = t;
@@ -266,13 +384,31 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
     const uint32_t ta = s_slope[0], tb = s_slope[1];
 
     const uint32_t budget = p.budget;
-    const uint64_t total = p.total_tuples;
+    uint64_t total = p.total_tuples;
     const uint32_t CH = kThreads * ITEMS;
     uint2* qranges = ranges + q * (uint64_t)budget;
     uint32_t C = 0, R = 0;
     uint64_t base = 0;
+    if (EXACT && tid == 0) {  // the all-zero tuple starts the exact order
+        uint32_t n0 = 0;
+        exact_push(heap, n0, exact_sum(p, 0, dl), 0);
+        s_heap_n = n0;
+    }
 
     while (C < budget && base < total) {
+        if constexpr (EXACT) {
+            // this chunk's (or resort batch's) tuples, in order, from the heap
+            const uint32_t want = RESORT ? (uint32_t)min((uint64_t)budget, total - base) : CH;
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t n = s_heap_n;
+                s_got = exact_fill(p, heap, n, dl, tbuf, want, &s_overflow);
+                s_heap_n = n;
+            }
+            __syncthreads();
+            if (s_got < want) total = base + s_got;  // the stream (or the heap) ends in this chunk
+            if (s_got == 0) break;
+        }
         uint64_t spos[ITEMS];
         bool inb[ITEMS];
         uint64_t step;
@@ -289,8 +425,10 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                 if (o < bs) {
                     const uint64_t s = base + o;
                     // ranks of tuple s (recomputed; resort batches are budget-sized)
-                    uint32_t r[4] = {0, 0, 0, 0};
-                    if (p.P == 1) {
+                    uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    if (EXACT) {
+                        exact_ranks(p, tbuf[o], r);
+                    } else if (p.P == 1) {
                         r[0] = (uint32_t)s;
                     } else if (p.P == 2) {
                         const uint32_t e = p.pair_streams[(size_t)ta * p.W2 + s];
@@ -345,7 +483,14 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
             hidx[it] = 0;
             slot[it] = 0;
             if (inb[it]) {
-                const uint64_t sl = tuple_slot(p, spos[it], ta, tb, terms);
+                uint64_t sl;
+                if constexpr (EXACT) {
+                    uint32_t r[8];
+                    exact_ranks(p, tbuf[spos[it] - base], r);
+                    sl = slot_of_ranks(p, r, terms);
+                } else {
+                    sl = tuple_slot(p, spos[it], ta, tb, terms);
+                }
                 slot[it] = (uint32_t)sl;
                 ne[it] = (__ldg(p.bitmap + (sl >> 5)) >> (sl & 31)) & 1u;
             }
@@ -415,6 +560,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         // tuples the reference's gather loop consumes: up to the one that filled the budget,
         // or the whole stream (search.cpp:166-217)
         ntuples[q] = C >= budget && budget > 0 ? s_maxord + 1 : (uint32_t)min(base, total);
+        if (EXACT && s_overflow) ntuples[q] = 0xFFFFFFFFu;  // the heap overflowed: reported by the host API
         if (stats) {
             stats[q].bins_visited = R;
             stats[q].candidates = C;
@@ -451,12 +597,33 @@ void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_quer
         return;
     }
     const uint32_t lg = ts_log2_for(p);
-    if (p.resort) {
-        binsel_kernel<16, true><<<(unsigned)nq, kThreads, binsel_smem(p), s>>>(
-            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg);
+    const size_t sm = binsel_smem(p);
+    if (p.exact_order) {
+        // the exact order's heap takes the rest of the opt-in shared memory (<= 64 Ki entries)
+        const uint32_t ch = (p.resort ? 16u : 4u) * kThreads;
+        const size_t fixed = ((sm + 7) & ~size_t(7)) + (size_t)ch * 8;
+        int dev = 0, optin = 0;
+        PQTG_CUDA_CHECK(cudaGetDevice(&dev));
+        PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        cudaFuncAttributes a{};
+        if (p.resort) PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, binsel_kernel<16, true, true>));
+        else PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, binsel_kernel<4, false, true>));
+        const size_t avail = (size_t)optin - a.sharedSizeBytes;
+        if (avail < fixed + 64 * 16) throw Error{PQTG_ERR_UNSUPPORTED, "exact bin order: no shared memory for its heap"};
+        const uint32_t cap = (uint32_t)std::min<size_t>((avail - fixed) / 16, 65536);
+        const size_t smx = fixed + (size_t)cap * 16;
+        if (p.resort)
+            binsel_kernel<16, true, true><<<(unsigned)nq, kThreads, smx, s>>>(
+                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap);
+        else
+            binsel_kernel<4, false, true><<<(unsigned)nq, kThreads, smx, s>>>(
+                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap);
+    } else if (p.resort) {
+        binsel_kernel<16, true, false><<<(unsigned)nq, kThreads, sm, s>>>(
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0);
     } else {
-        binsel_kernel<4, false><<<(unsigned)nq, kThreads, binsel_smem(p), s>>>(
-            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg);
+        binsel_kernel<4, false, false><<<(unsigned)nq, kThreads, sm, s>>>(
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0);
     }
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
@@ -682,8 +849,10 @@ void configure_kernels(const DevParams& p, uint32_t) {
         allow_max_smem(traverse_kernel<32, 16>);
         allow_max_smem(traverse_kernel<16, 16>);
         allow_max_smem(traverse_kernel<0, 0>);
-        allow_max_smem(binsel_kernel<4, false>);
-        allow_max_smem(binsel_kernel<16, true>);
+        allow_max_smem(binsel_kernel<4, false, false>);
+        allow_max_smem(binsel_kernel<16, true, false>);
+        allow_max_smem(binsel_kernel<4, false, true>);
+        allow_max_smem(binsel_kernel<16, true, true>);
         set_rerank_attr<16, 1>();
         set_rerank_attr<32, 1>();
         set_rerank_attr<64, 1>();

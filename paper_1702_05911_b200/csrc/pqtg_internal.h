@@ -44,7 +44,9 @@ struct DevParams {
     uint64_t H;                 // slots
     uint64_t n;
     uint64_t shard_lo, shard_hi;  // positions re-ranked here
-    uint64_t mult[4];           // (k1*k2)^p mod 2^64 (pqtree.cpp:12-21)
+    uint64_t mult[8];           // (k1*k2)^p mod 2^64 (pqtree.cpp:12-21), p < P <= 8
+    uint32_t exact_order;       // no slope tables for this P: exact (Dijkstra) order (binorder.cpp:114-167)
+    uint32_t tuple_bits;        // exact order: bits per rank in a packed tuple (P · bits <= 64)
     uint64_t total_tuples;      // W^P: stream length (BinStream::total)
     double inv_log108;          // 1 / log(1.08), host glibc value
     double log108;

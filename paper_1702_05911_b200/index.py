@@ -120,7 +120,8 @@ class HostIndex:
         self.level2 = np.ascontiguousarray(self.level2, np.float32).reshape(P, k1, k2, m)
         self.d2 = np.ascontiguousarray(self.d2, np.float32).reshape(L, k1, k1)
         self.slopes = np.ascontiguousarray(self.slopes, np.float64).reshape(-1)
-        self.entries = np.ascontiguousarray(self.entries, np.uint32).reshape(len(self.slopes), -1, 2)
+        self.entries = (np.ascontiguousarray(self.entries, np.uint32).reshape(len(self.slopes), -1, 2)
+                        if len(self.slopes) else np.zeros((0, 0, 2), np.uint32))
         self.offsets = np.ascontiguousarray(self.offsets, np.uint64).reshape(-1)
         self.ids = np.ascontiguousarray(self.ids, np.uint32).reshape(-1)
         self.lambda_q = np.ascontiguousarray(self.lambda_q, np.uint8).reshape(self.n, L)

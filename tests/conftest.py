@@ -10,6 +10,8 @@ REPO = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(REPO))
 GOLDEN = REPO / "tests" / "golden"
 GOLDEN_CASES = ["p2_small", "p4_small", "p1_small", "p2_resort", "p2_wide", "p2_sift", "p4_gist"]
+# the reference's exact (Dijkstra) bin order: P = 3, and P = 2 without slope tables
+ORDER_CASES = ["p3_order", "p3_order_resort", "p2_notables"]
 
 
 def pytest_configure(config):

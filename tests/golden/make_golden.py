@@ -70,6 +70,39 @@ def make(name: str) -> None:
     print(name, "n", n, "bytes", path.stat().st_size, "mean C", stats[:, 1].mean(), "bins", stats[:, 0].mean())
 
 
+# part counts without a precomputed heuristic (P = 3), or an index stripped of its slope
+# tables (P = 2): the reference's exact Dijkstra bin order (binorder.cpp:114-167, :242-244)
+ORDER_CASES = {
+    "p3_order": (dict(dim=96, p_tree=3, k1=16, k2=8, w=4, p_line=24, hash_size=20000, candidate_budget=512,
+                      rerank_exact=0), 6000, 40, 50, 48, 19),
+    "p3_order_resort": (dict(dim=48, p_tree=3, k1=8, k2=4, w=3, p_line=12, hash_size=4000, candidate_budget=300,
+                             rerank_exact=0, resort_bins=True), 4000, 40, 20, 48, 20),
+    "p2_notables": (dict(dim=32, p_tree=2, k1=8, k2=4, w=3, p_line=8, hash_size=2048, candidate_budget=256,
+                         rerank_exact=0), 4000, 48, 20, 48, 22),
+}
+
+
+def make_order(name: str) -> None:
+    cfgd, n, nq, k, blobs, seed = ORDER_CASES[name]
+    cfg = PqtConfig(train_iters=10, seed=seed, **cfgd)
+    X = Ref.synth(n + nq, cfg.dim, blobs, 20.0, seed)
+    db, Q = X[:n], X[n:]
+    ref = Ref.build(db, db, cfg, threads=8)
+    if name.endswith("notables"):  # no slope tables in the container: BinStream falls back to exact
+        hix = ref.host_index()
+        hix.slopes = np.zeros(0, np.float64)
+        hix.entries = np.zeros((0, 0, 2), np.uint32)
+        hix.__post_init__()
+        ref = Ref.from_host(hix)
+    path = HERE / f"{name}.pqt"
+    ref.save(str(path))
+    ref = Ref.load(str(path))
+    ids, dists, counts, stats = ref.knn(Q, k, threads=4)
+    np.savez_compressed(HERE / f"{name}.npz", queries=Q, k=np.array(k), ids=ids, dists=dists, counts=counts,
+                        stats=stats)
+    print(name, "n", n, "bytes", path.stat().st_size, "mean C", stats[:, 1].mean(), "bins", stats[:, 0].mean())
+
+
 def make_exact(name: str) -> None:
     cfgd, n, nq, ks, blobs, seed = EXACT_CASES[name]
     cfg = PqtConfig(train_iters=10, seed=seed, **cfgd)
@@ -88,11 +121,12 @@ def make_exact(name: str) -> None:
 
 
 def main() -> None:
-    names = sys.argv[1:] or list(CASES) + list(EXACT_CASES)
+    names = sys.argv[1:] or list(CASES) + list(EXACT_CASES) + list(ORDER_CASES)
     for name in names:
-        (make_exact if name in EXACT_CASES else make)(name)
+        (make_exact if name in EXACT_CASES else make_order if name in ORDER_CASES else make)(name)
     (HERE / "CASES.json").write_text(json.dumps({k: dict(config=v[0], n=v[1], nq=v[2], k=v[3], blobs=v[4], seed=v[5])
-                                                 for k, v in {**CASES, **EXACT_CASES}.items()}, indent=1))
+                                                 for k, v in {**CASES, **EXACT_CASES, **ORDER_CASES}.items()},
+                                                indent=1))
 
 
 if __name__ == "__main__":

@@ -8,7 +8,7 @@
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, load_golden
+from conftest import GOLDEN, ORDER_CASES, load_golden
 from oracle.bindings import Oracle
 from paper_1702_05911_b200 import DeviceIndex, PqtConfig, builder
 from test_gpu_parity import VARIANTS, assert_same_results
@@ -194,3 +194,35 @@ def test_gpu_sharded_build_equals_full_build():
     mi, md, mc = merge_topk_host(np.stack([p[0] for p in parts]), np.stack([p[1] for p in parts]),
                                  np.stack([p[2] for p in parts]))
     assert_same_results((mi, md, mc, want[3]), want, "merged")
+
+
+@pytest.mark.parametrize("name", ORDER_CASES)
+def test_gpu_exact_bin_order_golden(name):
+    """Indexes the reference walks in its exact Dijkstra order (binorder.cpp:114-167): P = 3
+    (with and without resort_bins) and a P = 2 container without slope tables. The GPU's heap
+    of canonical-parent pushes (kernels.cu exact_fill) against the reference's own outputs."""
+    g = load_golden(name)
+    dev = DeviceIndex(str(GOLDEN / f"{name}.pqt"))
+    got = dev.search(g["queries"], int(g["k"]))
+    assert_same_results(got, (g["ids"], g["dists"], g["counts"], g["stats"]), name)
+
+
+def test_gpu_exact_bin_order_built_index():
+    """A GPU-built P = 3 index at budget 4096 (a deep heap) against the reference compiled in
+    place, run on the same index."""
+    import torch
+
+    from oracle.bindings import Ref
+
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=96, p_tree=3, k1=16, k2=8, w=4, p_line=24, train_iters=4, seed=71, candidate_budget=4096,
+                    rerank_exact=0)
+    X = builder.synth_clustered(60_000 + 64, cfg.dim, 256, 20.0, 71, device=dev)
+    db, Q = X[:60_000], X[60_000:].cpu().numpy()
+    hix = builder.build_index(db, db[:20_000], cfg)
+    got = DeviceIndex(hix).search(Q, 100)
+    want = Ref.from_host(hix).knn(Q, 100)
+    assert_same_results(got, want, "p3 built")
+    assert (got[3][:, 1] == 4096).all()

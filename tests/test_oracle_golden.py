@@ -2,7 +2,7 @@
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, GOLDEN_CASES, load_golden
+from conftest import GOLDEN, GOLDEN_CASES, ORDER_CASES, load_golden
 from oracle.bindings import Oracle
 from paper_1702_05911_b200.index import HostIndex
 
@@ -35,7 +35,7 @@ def test_oracle_traverse_and_order_match_golden(name):
         off += n
 
 
-@pytest.mark.parametrize("name", GOLDEN_CASES)
+@pytest.mark.parametrize("name", GOLDEN_CASES + ORDER_CASES)
 def test_container_roundtrip_is_byte_identical(name, tmp_path):
     """PQTINDEX v1 reader/writer (index.py) reproduce the reference's save_index bytes."""
     src = GOLDEN / f"{name}.pqt"
@@ -90,3 +90,21 @@ def test_oracle_exact_rerank_matches_golden():
     assert (stats[:, 2] == 0).all()
     with pytest.raises(ValueError):
         o.attach_database(g["db"][:-1])
+
+
+@pytest.mark.parametrize("name", ORDER_CASES)
+def test_exact_order_golden_is_the_reference(name):
+    """The exact-order fixtures (P = 3; P = 2 without slope tables) replay on the reference
+    compiled in place: its knn_query_batch reproduces them (the C restatement has no exact order,
+    so these are pinned by the reference alone)."""
+    from oracle.bindings import Ref
+
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    g = load_golden(name)
+    ids, dists, counts, stats = Ref.load(str(GOLDEN / f"{name}.pqt")).knn(g["queries"], int(g["k"]), threads=4)
+    assert np.array_equal(counts, g["counts"]) and np.array_equal(stats, g["stats"])
+    for q in range(len(counts)):
+        c = counts[q]
+        assert np.array_equal(ids[q, :c], g["ids"][q, :c])
+        assert np.array_equal(dists[q, :c].view(np.uint32), g["dists"][q, :c].view(np.uint32))
