@@ -242,7 +242,8 @@ def peaks():
 
 def gpu_launches(hix, nq: int, chunks: int) -> int:
     """Kernels launched per step: traverse, bin selection, re-rank per chunk (api.cpp)."""
-    n = chunks if chunks else (2 if nq >= 256 else 1)  # pqtg_search_device's default (api.cpp)
+    shard = hasattr(hix, "shard_lo") and (hix.shard_lo > 0 or hix.shard_hi < hix.n)
+    n = chunks if chunks else (2 if nq >= 256 and (nq < 4096 or not shard) else 1)  # api.cpp's default
     return 3 * (n if nq >= n else 1)  # (+1 per chunk with --exact: exact_rerank_kernel)
 
 

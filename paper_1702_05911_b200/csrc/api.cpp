@@ -487,8 +487,12 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         ws.last_nq = nq;
         // device-resident batches: two chunks on two streams, so the next chunk's traversal and bin
         // selection fill the SMs the re-rank's last wave leaves idle (tools/e2e_probe.py on B200,
-        // 1000 GIST queries: 1 chunk 234 us, 2 chunks 207 us, 4 chunks 261 us)
-        const uint64_t nch = ws.chunks ? ws.chunks : (nq >= 256 ? 2 : 1);
+        // 1000 GIST queries: 1 chunk 234 us, 2 chunks 207 us, 4 chunks 261 us). A position shard's
+        // short re-rank gains nothing from the overlap once every stage runs many waves (SIFT1B
+        // shard, 10k queries: 0.97 ms unchunked vs 1.13 ms; SIFT1M, unsharded: 1.26 vs 1.24 ms).
+        const DevParams& pp = index->dev->prm;
+        const bool shard = pp.shard_hi > pp.shard_lo && (pp.shard_lo > 0 || pp.shard_hi < pp.n);
+        const uint64_t nch = ws.chunks ? ws.chunks : (nq >= 256 && (nq < 4096 || !shard) ? 2 : 1);
         if (nch <= 1 || nq < nch) {
             run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, s, true);
             return PQTG_OK;

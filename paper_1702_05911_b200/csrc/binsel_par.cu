@@ -177,7 +177,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t C = 0, R = 0, base = 0;
     bool done = budget == 0, spilled = false;
-    // P = 4 streams run to thousands of tuples: full passes from the start
+    // P = 4 streams run to thousands of tuples: full passes from the start (a first
+    // pass of 1024 measured slower even at SIFT1B, whose queries need ~930 tuples: 333 -> 354 us,
+    // the pass is latency-bound and the queries past 1024 pay a second one)
     uint32_t nit = P == 4 ? kPItems : 1;
     for (uint32_t pass = 0; !done && base < total32; ++pass) {
         const uint32_t pb = pass & 1u;
