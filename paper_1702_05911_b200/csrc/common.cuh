@@ -100,10 +100,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "{\n"
         ".reg .pred done;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n"
         "@!done bra WAIT_%=;\n"
         "}\n" ::"r"(smem_addr(bar)),
-        "r"(phase)
+        "r"(phase), "r"(0x989680u)  // suspend hint: sleep until the phase flips, not spin
         : "memory");
 }
 

@@ -388,6 +388,15 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
         uint32_t q = 0;
         for (uint32_t i = 0; i < k1; ++i)
             for (uint32_t j = i + 1; j < k1; ++j, ++q) pi_of[q] = (uint16_t)(q | (i << 9));
+        // c2 rows padded to 512 pairs: the DIRECT re-rank's loads use compile-time row offsets
+        std::vector<float> c2p((size_t)L * 512, 0.0f);
+        for (uint32_t f = 0; f < L; ++f) {
+            uint32_t pq = 0;
+            for (uint32_t i = 0; i < k1; ++i)
+                for (uint32_t j = i + 1; j < k1; ++j, ++pq)
+                    c2p[(size_t)f * 512 + pq] = src.d2[((size_t)f * k1 + i) * k1 + j];
+        }
+        p.c2p = upload(*ix, c2p.data(), c2p.size());
     }
     std::vector<uint8_t> ij_of(npairs, 0);
     auto tcode = [](uint32_t i, uint32_t j) { return (uint8_t)((i << 4) | ((i + j) & 15u)); };

@@ -70,6 +70,7 @@ struct DevParams {
     uint32_t code_ij;           // 1-byte codes hold i << 4 | ((i + j) & 15) instead of the pair id (k1 <= 16)
     uint32_t code_pi;           // 2-byte codes hold pid | i << 9 (16 < k1 <= 32)
     const float* c2ij;          // [L][256] d2[f][i][j] at i << 4 | j (code_ij only)
+    const float* c2p;           // [L][512] d2[f][pair] (code_pi only)
     // exact re-rank (search.cpp:229-249): raw vectors n × D f32 in id order, or null
     const float* db;            // [n][db_stride]
     uint32_t db_stride;         // D rounded up to 4 floats

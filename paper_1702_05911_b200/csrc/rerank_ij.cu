@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
                 float2 ec;
                 if constexpr (DIRECT) {  // E and c2 of this part, in T's roundings
                     const float a2 = fine[f * K1M + jt[ti]];
-                    ec.y = __ldg(p.c2 + f * p.npairs + ti);
+                    ec.y = __ldg(p.c2p + f * 512 + ti);
                     ec.x = __fsub_rn(__fsub_rn(a2, b2), ec.y);
                 } else {
                     ec = T[f * TE + ti];

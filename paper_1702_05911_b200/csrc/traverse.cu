@@ -100,12 +100,12 @@ template <int K1T, int K2T, int FB>
 __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, const float* __restrict__ Q,
                                                                    float* __restrict__ fine_out,
                                                                    float* __restrict__ l2d_out,
-                                                                   uint32_t* __restrict__ l2c_out, uint32_t bulk) {
+                                                                   uint32_t* __restrict__ l2c_out, uint32_t bulk,
+                                                                   const TpLayout lay) {  // tp_layout(p), host-made
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar[2];
     const uint32_t k1 = K1T ? (uint32_t)K1T : p.k1, k2 = K2T ? (uint32_t)K2T : p.k2;
     const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W, w = p.w;
-    const TpLayout lay = tp_layout(p);
     float* blk = reinterpret_cast<float*>(smem + lay.blk);
     float* y = reinterpret_cast<float*>(smem + lay.y);
     float* fine = reinterpret_cast<float*>(smem + lay.fine);
@@ -295,9 +295,9 @@ void launch_traverse_part(const DevParams& p, const float* queries, uint64_t nq,
     const unsigned grid = (unsigned)(nq * p.P);
 #define PQTG_TP(A, B)                                                                                         \
     (p.fd <= 8 ? traverse_part_kernel<A, B, 8><<<grid, kTpThreads, lay.total, s>>>(p, queries, ws.fine, ws.l2_dist, \
-                                                                                   ws.l2_code, bulk)               \
+                                                                                   ws.l2_code, bulk, lay)          \
                : traverse_part_kernel<A, B, 32><<<grid, kTpThreads, lay.total, s>>>(p, queries, ws.fine,          \
-                                                                                    ws.l2_dist, ws.l2_code, bulk))
+                                                                                    ws.l2_dist, ws.l2_code, bulk, lay))
     if (p.k1 == 16 && p.k2 == 8) PQTG_TP(16, 8);
     else if (p.k1 == 32 && p.k2 == 16) PQTG_TP(32, 16);
     else if (p.k1 == 16 && p.k2 == 16) PQTG_TP(16, 16);
