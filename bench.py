@@ -444,7 +444,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    affinity = pin_to_gpu_numa(local)  # host buffers on the GPU's NUMA node (H2D varies 2x otherwise)
+    affinity = pin_to_gpu_numa(local)  # host buffers on the GPU's NUMA node
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -514,13 +514,60 @@ def main():
             step(b)
     torch.cuda.synchronize()
 
+    jobs = 1 if args.shard else world  # sharded: all ranks share each batch
+    # ---- e2e through the public host API (pinned buffers, copies inside the timed call)
+    def run_e2e():
+        hq = [torch.from_numpy(b).pin_memory() for b in batches]
+        h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+        h_dists = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+        h_counts = torch.empty(nq, dtype=torch.int32).pin_memory()
+        h_stats = torch.empty((nq, 3), dtype=torch.int64).pin_memory()
+        L = lib()
+
+        def host_step(b):
+            if args.shard:  # H2D of the batch, sharded search, D2H of the merged top-k
+                d_q[b].copy_(hq[b], non_blocking=True)
+                sh.search(d_q[b], k, d_ids, d_dists, d_counts, d_stats)
+                h_ids.copy_(d_ids, non_blocking=True)
+                h_dists.copy_(d_dists, non_blocking=True)
+                h_counts.copy_(d_counts, non_blocking=True)
+                h_stats.copy_(d_stats, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return
+            rc = L.pqtg_search(dev.handle, dev.workspace, hq[b].data_ptr(), nq, hix.config.dim, k, h_ids.data_ptr(),
+                               h_dists.data_ptr(), h_counts.data_ptr(), h_stats.data_ptr())
+            assert rc == 0, L.pqtg_last_error()
+
+        for b in range(args.batches):
+            host_step(b)
+        e2e_steps = max(args.steps // 2, 10)
+        e2e_t = 0.0
+        e2e_each = []
+        for s in range(e2e_steps):
+            if not args.no_flush:
+                flush.fill_(s & 0xFF)
+                torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            host_step(s % args.batches)
+            e2e_each.append(time.perf_counter() - t0)
+            e2e_t += e2e_each[-1]
+        log(f"[bench] e2e step us: median {np.median(e2e_each) * 1e6:.1f} mean {np.mean(e2e_each) * 1e6:.1f} "
+            f"p90 {np.percentile(e2e_each, 90) * 1e6:.1f} max {np.max(e2e_each) * 1e6:.1f}")
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_value = jobs * nq * e2e_steps / float(tt.item())
+        h2d = nq * hix.config.dim * 4
+        d2h = nq * k * 8 + nq * 4 + nq * 24
+        link = link_bandwidth(hq[0], d_q[0], h_ids, d_ids)
+
+        return e2e_value, h2d, d2h, link
+
     # ---- timed: device-resident
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    # (NVML is shut down again on exit: while initialised it slows the host-side CUDA calls of
-    # the e2e loop by ~40%, 300 -> 420 us per GIST1M step, measured)
     with ClockSampler(local) as clk:
         for s in range(args.steps):
             if not args.no_flush:
@@ -536,7 +583,6 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    jobs = 1 if args.shard else world  # sharded: all ranks share each batch
     value = jobs * nq * args.steps / (ms_max / 1000.0)
 
     # ---- per-kernel times (unchunked launches: one launch per stage per step)
@@ -551,50 +597,7 @@ def main():
     stage_mean = stage_sum / kstep
     dev.set_chunks(args.chunks)
 
-    # ---- e2e through the public host API (pinned buffers, copies inside the timed call)
-    hq = [torch.from_numpy(b).pin_memory() for b in batches]
-    h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory()
-    h_dists = torch.empty((nq, k), dtype=torch.float32).pin_memory()
-    h_counts = torch.empty(nq, dtype=torch.int32).pin_memory()
-    h_stats = torch.empty((nq, 3), dtype=torch.int64).pin_memory()
-    L = lib()
-
-    def host_step(b):
-        if args.shard:  # H2D of the batch, sharded search, D2H of the merged top-k
-            d_q[b].copy_(hq[b], non_blocking=True)
-            sh.search(d_q[b], k, d_ids, d_dists, d_counts, d_stats)
-            h_ids.copy_(d_ids, non_blocking=True)
-            h_dists.copy_(d_dists, non_blocking=True)
-            h_counts.copy_(d_counts, non_blocking=True)
-            h_stats.copy_(d_stats, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            return
-        rc = L.pqtg_search(dev.handle, dev.workspace, hq[b].data_ptr(), nq, hix.config.dim, k, h_ids.data_ptr(),
-                           h_dists.data_ptr(), h_counts.data_ptr(), h_stats.data_ptr())
-        assert rc == 0, L.pqtg_last_error()
-
-    for b in range(args.batches):
-        host_step(b)
-    e2e_steps = max(args.steps // 2, 10)
-    e2e_t = 0.0
-    e2e_each = []
-    for s in range(e2e_steps):
-        if not args.no_flush:
-            flush.fill_(s & 0xFF)
-            torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        host_step(s % args.batches)
-        e2e_each.append(time.perf_counter() - t0)
-        e2e_t += e2e_each[-1]
-    log(f"[bench] e2e step us: median {np.median(e2e_each) * 1e6:.1f} mean {np.mean(e2e_each) * 1e6:.1f} "
-        f"p90 {np.percentile(e2e_each, 90) * 1e6:.1f} max {np.max(e2e_each) * 1e6:.1f}")
-    tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    e2e_value = jobs * nq * e2e_steps / float(tt.item())
-    h2d = nq * hix.config.dim * 4
-    d2h = nq * k * 8 + nq * 4 + nq * 24
-    link = link_bandwidth(hq[0], d_q[0], h_ids, d_ids)
+    e2e_value, h2d, d2h, link = run_e2e()
 
     if rank != 0:
         if world > 1:
