@@ -77,12 +77,12 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
     uint32_t word[NIT];
     if (fast) {
         if constexpr (P == 4) {
-            const uint2* mp = p.merge + base + ft;
-            uint2 e[NIT];
+            const uint32_t* mp = p.merge16 + base + ft;  // fast path: W2ab > 0, so W2 <= 4096
+            uint32_t e[NIT];
 #pragma unroll
             for (int it = 0; it < NIT; ++it) e[it] = __ldg(mp + it * NT);
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) slot[it] = add_mod_fast(tA[e[it].x], tB[e[it].y], H);
+            for (int it = 0; it < NIT; ++it) slot[it] = add_mod_fast(tA[e[it] & 0xFFFFu], tB[e[it] >> 16], H);
         } else if constexpr (P == 2) {
             const uint32_t* sp = p.pair_streams + (size_t)ta * W2 + base + ft;
             uint32_t e[NIT];

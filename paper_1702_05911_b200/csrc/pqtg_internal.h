@@ -55,6 +55,7 @@ struct DevParams {
     // static bin-order streams
     const uint32_t* pair_streams;  // [10][W*W] (a | b << 16), PairCursor order per table
     const uint2* merge;            // [merge_count] (u, v) for P == 4
+    const uint32_t* merge16;       // [merge_count] u | v << 16 (W2 <= 65536), or null
     uint64_t merge_count;
     uint64_t merge_row0;           // first closed-form sweep row
     uint64_t W2;
