@@ -302,9 +302,9 @@ def counters_ids(dev, dq, nq, k, step, d_ids, d_counts):
 
 def measure_recall(name: str, seed: int, device: int, Q: np.ndarray, nq_pool: int, result):
     """recall@R = fraction of queries whose exact nearest neighbour is within the first R
-    results (recall_fraction, bench.cpp:23-44); exact neighbours by brute force on the GPU
-    over the regenerated (deterministic) base set. Identical for the CPU reference, whose
-    ids are bit-identical."""
+    results (recall_fraction, bench.cpp:23-44); exact neighbours by the GPU brute force
+    (brute.cu, the reference's brute_force_knn) over the regenerated (deterministic) base set.
+    Identical for the CPU reference, whose ids are bit-identical."""
     import torch
 
     from paper_1702_05911_b200 import builder
@@ -316,18 +316,32 @@ def measure_recall(name: str, seed: int, device: int, Q: np.ndarray, nq_pool: in
     X = builder.synth_clustered(wl["n"] + nq_pool, wl["config"]["dim"], wl["blobs"], wl["sigma"], seed,
                                 device=dev)[: wl["n"]]
     q = torch.from_numpy(Q).to(dev)
-    best_d = torch.full((q.shape[0],), float("inf"), device=dev)
-    best_i = torch.zeros(q.shape[0], dtype=torch.int64, device=dev)
-    qq = (q * q).sum(1, keepdim=True)
-    for s in range(0, X.shape[0], 1 << 18):
-        xb = X[s:s + (1 << 18)]
-        d = qq - 2.0 * (q @ xb.T) + (xb * xb).sum(1)[None, :]
-        v, i = d.min(1)
-        better = v < best_d
-        best_d = torch.where(better, v, best_d)
-        best_i = torch.where(better, i + s, best_i)
+    if X.shape[0] <= 20_000_000:
+        # the exact nearest neighbour as the reference defines it (brute_force_knn, sequential fp32
+        # l2_sq, (dist, id) order: search.cpp:276-299), on the GPU (pqtg_brute_force_knn_device)
+        from paper_1702_05911_b200._abi import check, lib
+
+        X = X.contiguous()
+        gt_i = torch.empty(q.shape[0], dtype=torch.int32, device=dev)
+        gt_d = torch.empty(q.shape[0], dtype=torch.float32, device=dev)
+        gt_c = torch.empty(q.shape[0], dtype=torch.int32, device=dev)
+        check(lib().pqtg_brute_force_knn_device(X.data_ptr(), X.shape[0], X.shape[1], q.data_ptr(), q.shape[0], 1,
+                                                gt_i.data_ptr(), gt_d.data_ptr(), gt_c.data_ptr(),
+                                                torch.cuda.current_stream(dev).cuda_stream))
+        truth = gt_i.cpu().numpy().view(np.uint32).astype(np.int64)
+    else:  # 100M+ rows: the torch matmul form (exact up to fp32 rounding of the expansion)
+        best_d = torch.full((q.shape[0],), float("inf"), device=dev)
+        best_i = torch.zeros(q.shape[0], dtype=torch.int64, device=dev)
+        qq = (q * q).sum(1, keepdim=True)
+        for s in range(0, X.shape[0], 1 << 18):
+            xb = X[s:s + (1 << 18)]
+            d = qq - 2.0 * (q @ xb.T) + (xb * xb).sum(1)[None, :]
+            v, i = d.min(1)
+            better = v < best_d
+            best_d = torch.where(better, v, best_d)
+            best_i = torch.where(better, i + s, best_i)
+        truth = best_i.cpu().numpy()
     del X
-    truth = best_i.cpu().numpy()
     out = {}
     for R in (1, 10, 100):
         hit = [truth[i] in ids[i, : min(R, counts[i])] for i in range(len(truth))]

@@ -4,9 +4,9 @@
 // Same types, same signatures, same exceptions. Differences a caller can observe:
 //  * queries run on a CUDA device (device 0 unless PQTG_DEVICE is set); the first query on
 //    an index uploads it and caches the device copy in PqtIndex::gpu;
-//  * exact re-ranking against attached raw vectors is not implemented on the GPU path: with
-//    a database attached and rerank_exact > 0 the calls throw std::runtime_error (without
-//    one they warn once and disable it, exactly as the reference does, search.cpp:25-32);
+//  * exact re-ranking against attached raw vectors runs on the GPU (the database is copied to
+//    the device on the first query after attach_database); without one the calls warn once and
+//    disable it, exactly as the reference does (search.cpp:25-32);
 //  * QueryStats *_us are the batch's per-stage device times divided evenly over its queries.
 #pragma once
 
@@ -57,5 +57,8 @@ QueryResult knn_query(const PqtIndex& index, const float* y, std::uint32_t k);
 
 std::vector<QueryResult> knn_query_batch(const PqtIndex& index, const VectorSet& queries, std::uint32_t k,
                                          int threads = 0);
+
+// Exact k-NN by brute force over db (search.cpp:276-299), computed on the GPU.
+QueryResult brute_force_knn(const VectorSet& db, const float* y, std::uint32_t k);
 
 }  // namespace pqt

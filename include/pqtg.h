@@ -244,6 +244,20 @@ int pqtg_merge_topk_device(uint32_t shards, uint64_t nq, uint32_t k, const uint3
 /* Even split of [0, n) into `shards` position ranges (the shard_lo/shard_hi to pass). */
 int pqtg_shard_range(uint64_t n, uint32_t shards, uint32_t rank, uint64_t* lo, uint64_t* hi);
 
+/* ---- exact ground truth ---------------------------------------------------------- */
+/* pqt::brute_force_knn (src/search.cpp:276-299) for a batch: for every query the min(k, n)
+ * rows of db (n × dim float32, row-major, vector id = row) nearest by l2_sq (distance.hpp:11-18,
+ * sequential fp32), ordered by (dist, id); ids/dists are nq × k (padded with UINT32_MAX / +inf),
+ * counts[q] = min(k, n); stats (optional) = {0, n, n} as the reference reports. n < 2^32,
+ * k <= 4096. Host buffers, copied to and from `device` inside the call. */
+int pqtg_brute_force_knn(const float* db, uint64_t n, uint32_t dim, const float* queries, uint64_t nq,
+                         uint32_t k, int device, uint32_t* ids, float* dists, uint32_t* counts,
+                         pqtg_query_stats* stats);
+/* Same with device buffers, asynchronous on `stream` (no stats). */
+int pqtg_brute_force_knn_device(const float* d_db, uint64_t n, uint32_t dim, const float* d_queries,
+                                uint64_t nq, uint32_t k, uint32_t* d_ids, float* d_dists,
+                                uint32_t* d_counts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

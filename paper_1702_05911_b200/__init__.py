@@ -5,5 +5,5 @@ hand-written CUDA kernels in libpqtg.so behind the C-ABI in include/pqtg.h; this
 the host-side mirror of the reference's query API (proj/include/pqt/search.hpp).
 """
 from .index import FormatError, HostIndex, PqtConfig  # noqa: F401
-from .search import (DeviceIndex, QueryResult, QueryStats, knn_query, knn_query_batch,  # noqa: F401
-                     load_index, merge_topk_host, shard_range)
+from .search import (DeviceIndex, QueryResult, QueryStats, brute_force_knn, knn_query,  # noqa: F401
+                     knn_query_batch, load_index, merge_topk_host, shard_range)

@@ -113,6 +113,8 @@ SIGNATURES = {
     "pqtg_merge_topk_host": (C.c_int, [_u32, _u64, _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pqtg_merge_topk_device": (C.c_int, [_u32, _u64, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pqtg_shard_range": (C.c_int, [_u64, _u32, _u32, C.POINTER(_u64), C.POINTER(_u64)]),
+    "pqtg_brute_force_knn": (C.c_int, [_vp, _u64, _u32, _vp, _u64, _u32, C.c_int, _vp, _vp, _vp, _vp]),
+    "pqtg_brute_force_knn_device": (C.c_int, [_vp, _u64, _u32, _vp, _u64, _u32, _vp, _vp, _vp, _vp]),
 }
 
 _LIB = None

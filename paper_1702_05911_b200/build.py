@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: belt and braces — every exact fp32 op is already an explicit __f*_rn intrinsic.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-CU_SOURCES = ["kernels.cu", "traverse.cu", "rerank_ij.cu", "binsel_fast.cu", "binsel_par.cu", "build_kernels.cu", "exact.cu", "screen.cu"]
+CU_SOURCES = ["kernels.cu", "traverse.cu", "rerank_ij.cu", "binsel_fast.cu", "binsel_par.cu", "build_kernels.cu", "exact.cu", "screen.cu", "brute.cu"]
 CXX_SOURCES = ["api.cpp", "index_file.cpp", "index_prep.cpp", "pqt_dropin.cpp"]
 
 

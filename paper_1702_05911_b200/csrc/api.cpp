@@ -733,6 +733,64 @@ int pqtg_merge_topk_device(uint32_t shards, uint64_t nq, uint32_t k, const uint3
     });
 }
 
+int pqtg_brute_force_knn_device(const float* d_db, uint64_t n, uint32_t dim, const float* d_queries, uint64_t nq,
+                                uint32_t k, uint32_t* d_ids, float* d_dists, uint32_t* d_counts, void* stream) {
+    return guarded([&] {
+        if (nq && (!d_queries || !d_counts || (k && (!d_ids || !d_dists)) || (n && !d_db)))
+            throw Error{PQTG_ERR_ARG, "null argument"};
+        if (dim == 0) throw Error{PQTG_ERR_BAD_DIM, "brute_force_knn: dim must be positive"};
+        if (n >= (1ull << 32)) throw Error{PQTG_ERR_UNSUPPORTED, "brute_force_knn: n must be < 2^32"};
+        if (!brute_force_ok(dim, k)) throw Error{PQTG_ERR_UNSUPPORTED, "brute_force_knn: k or dim too large"};
+        launch_brute_force(d_db, n, dim, d_queries, nq, k, d_ids, d_dists, d_counts, static_cast<cudaStream_t>(stream));
+        return PQTG_OK;
+    });
+}
+
+int pqtg_brute_force_knn(const float* db, uint64_t n, uint32_t dim, const float* queries, uint64_t nq, uint32_t k,
+                         int device, uint32_t* ids, float* dists, uint32_t* counts, pqtg_query_stats* stats) {
+    return guarded([&] {
+        if (nq && (!queries || !counts || (k && (!ids || !dists)) || (n && !db))) throw Error{PQTG_ERR_ARG, "null argument"};
+        if (dim == 0) throw Error{PQTG_ERR_BAD_DIM, "brute_force_knn: dim must be positive"};
+        if (n >= (1ull << 32)) throw Error{PQTG_ERR_UNSUPPORTED, "brute_force_knn: n must be < 2^32"};
+        PQTG_CUDA_CHECK(cudaSetDevice(device));
+        if (!brute_force_ok(dim, k)) throw Error{PQTG_ERR_UNSUPPORTED, "brute_force_knn: k or dim too large"};
+        if (nq == 0) return PQTG_OK;
+        std::vector<void*> held;
+        auto alloc = [&](size_t bytes) {
+            void* p = nullptr;
+            PQTG_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+            held.push_back(p);
+            return p;
+        };
+        try {
+            float* d_db = static_cast<float*>(alloc(n * dim * 4));
+            float* d_q = static_cast<float*>(alloc(nq * dim * 4));
+            uint32_t* d_ids = static_cast<uint32_t*>(alloc(nq * std::max<uint32_t>(k, 1) * 4));
+            float* d_d = static_cast<float*>(alloc(nq * std::max<uint32_t>(k, 1) * 4));
+            uint32_t* d_c = static_cast<uint32_t*>(alloc(nq * 4));
+            if (n) PQTG_CUDA_CHECK(cudaMemcpy(d_db, db, n * dim * 4, cudaMemcpyHostToDevice));
+            PQTG_CUDA_CHECK(cudaMemcpy(d_q, queries, nq * dim * 4, cudaMemcpyHostToDevice));
+            launch_brute_force(d_db, n, dim, d_q, nq, k, d_ids, d_d, d_c, nullptr);
+            if (k) {
+                PQTG_CUDA_CHECK(cudaMemcpy(ids, d_ids, nq * k * 4, cudaMemcpyDeviceToHost));
+                PQTG_CUDA_CHECK(cudaMemcpy(dists, d_d, nq * k * 4, cudaMemcpyDeviceToHost));
+            }
+            PQTG_CUDA_CHECK(cudaMemcpy(counts, d_c, nq * 4, cudaMemcpyDeviceToHost));
+        } catch (...) {
+            for (void* p : held) cudaFree(p);
+            throw;
+        }
+        for (void* p : held) cudaFree(p);
+        if (stats)
+            for (uint64_t q = 0; q < nq; ++q) {
+                stats[q].bins_visited = 0;
+                stats[q].candidates = k && n ? n : 0;  // search.cpp:279-296: empty result when min(k, n) == 0
+                stats[q].exact_evals = k && n ? n : 0;
+            }
+        return PQTG_OK;
+    });
+}
+
 int pqtg_shard_range(uint64_t n, uint32_t shards, uint32_t rank, uint64_t* lo, uint64_t* hi) {
     return guarded([&] {
         if (shards == 0 || rank >= shards || !lo || !hi) throw Error{PQTG_ERR_ARG, "bad shard arguments"};

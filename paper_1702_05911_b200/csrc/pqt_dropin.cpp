@@ -6,6 +6,7 @@
 //   pqt::knn_query_batch   ← search.cpp:262-274     → pqtg_search on the cached device index
 //   pqt::knn_query         ← search.cpp:126-260     → a batch of one
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -347,6 +348,30 @@ QueryResult knn_query(const PqtIndex& index, const float* y, std::uint32_t k) {
     one.dim = index.config.dim;
     one.data.assign(y, y + index.config.dim);
     return knn_query_batch(index, one, k).front();
+}
+
+// brute_force_knn (search.cpp:276-299): exact l2_sq to every row of db on the GPU
+// (pqtg_brute_force_knn, brute.cu), (dist, id) order, min(k, n) results.
+QueryResult brute_force_knn(const VectorSet& db, const float* y, std::uint32_t k) {
+    QueryResult result;
+    const std::size_t n = db.count();
+    const std::size_t out = std::min<std::size_t>(k, n);
+    if (out == 0) return result;
+    const char* dev_env = std::getenv("PQTG_DEVICE");
+    const int device = dev_env ? std::atoi(dev_env) : 0;
+    std::vector<std::uint32_t> ids(k);
+    std::vector<float> dists(k);
+    std::uint32_t count = 0;
+    pqtg_query_stats st{};
+    const auto t0 = std::chrono::steady_clock::now();
+    check(pqtg_brute_force_knn(db.data.data(), n, db.dim, y, 1, k, device, ids.data(), dists.data(), &count, &st));
+    result.ids.assign(ids.begin(), ids.begin() + count);
+    result.dists.assign(dists.begin(), dists.begin() + count);
+    result.stats.candidates = n;
+    result.stats.exact_evals = n;
+    result.stats.rerank_us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    return result;
 }
 
 }  // namespace pqt

@@ -254,6 +254,10 @@ bool binsel_fast_ok(const DevParams& p);
 uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch);
 uint64_t binsel_hash_stride(const DevParams& p);
 void configure_binsel_fast();
+// brute.cu (exact brute-force k-NN, search.cpp:276-299)
+bool brute_force_ok(uint32_t dim, uint32_t k);
+void launch_brute_force(const float* d_db, uint64_t n, uint32_t dim, const float* d_queries, uint64_t nq, uint32_t k,
+                        uint32_t* d_ids, float* d_dists, uint32_t* d_counts, cudaStream_t s);
 // binsel_par.cu (same contract; all warps finish each pass together, no walker warp)
 void launch_binsel_par(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats, cudaStream_t s);
 uint64_t binsel_par_hash_stride(const DevParams& p);

@@ -208,6 +208,26 @@ class DeviceIndex:
         return dict(ncand=nc, ntuples=nt, nlocal=nl)
 
 
+def brute_force_knn(db: np.ndarray, queries: np.ndarray, k: int, device: int = 0):
+    """pqt::brute_force_knn (search.cpp:276-299) for a batch, on the GPU: exact sequential-fp32
+    l2_sq to every row, (dist, id) order. Returns (ids, dists, counts, stats) like
+    DeviceIndex.search; stats rows are (bins_visited, candidates, exact_evals) = (0, n, n)."""
+    x = np.ascontiguousarray(db, np.float32)
+    q = np.ascontiguousarray(queries, np.float32)
+    if q.ndim == 1:
+        q = q.reshape(1, -1)
+    if x.ndim != 2 or q.shape[1] != x.shape[1]:
+        raise ValueError("brute_force_knn: query dimension mismatch")
+    nq = q.shape[0]
+    ids = np.zeros((nq, max(k, 1)), np.uint32)
+    dists = np.zeros((nq, max(k, 1)), np.float32)
+    counts = np.zeros(nq, np.uint32)
+    stats = np.zeros((nq, 3), np.uint64)
+    check(lib().pqtg_brute_force_knn(x.ctypes.data, x.shape[0], x.shape[1], q.ctypes.data, nq, k, device,
+                                     ids.ctypes.data, dists.ctypes.data, counts.ctypes.data, stats.ctypes.data))
+    return ids[:, :k], dists[:, :k], counts, stats
+
+
 def load_index(path: str, device: int = 0, shard: tuple[int, int] = (0, 0)) -> DeviceIndex:
     """pqt::load_index: read a PQTINDEX v1 file straight into GPU memory."""
     return DeviceIndex(path, device=device, shard=shard)

@@ -226,3 +226,29 @@ def test_gpu_exact_bin_order_built_index():
     want = Ref.from_host(hix).knn(Q, 100)
     assert_same_results(got, want, "p3 built")
     assert (got[3][:, 1] == 4096).all()
+
+
+@pytest.mark.parametrize("n,dim,k", [(5000, 128, 100), (3000, 30, 20), (50, 16, 100), (4000, 96, 0)])
+def test_gpu_brute_force_knn(n, dim, k):
+    """pqt::brute_force_knn (search.cpp:276-299) on the GPU against the reference's own, bit for
+    bit: unaligned dim, n < k, k = 0, and repeated rows (ties broken by id)."""
+    from oracle.bindings import Ref
+
+    from paper_1702_05911_b200 import brute_force_knn
+
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(n + dim)
+    db = (rng.standard_normal((n, dim)) * 10).astype(np.float32)
+    db[n // 2:n // 2 + 7] = db[3]  # duplicates: equal distances, order by id
+    Q = (rng.standard_normal((24, dim)) * 10).astype(np.float32)
+    Q[0] = db[3]
+    ids, dists, counts, stats = brute_force_knn(db, Q, k)
+    assert (counts == min(k, n)).all()
+    if k and n:
+        assert (stats[:, 1] == n).all() and (stats[:, 2] == n).all()
+        r_ids, r_d = Ref.brute_force(db, Q, k)
+        c = min(k, n)
+        assert np.array_equal(ids[:, :c], r_ids[:, :c])
+        assert np.array_equal(dists[:, :c].view(np.uint32), r_d[:, :c].view(np.uint32))
+        assert ids[0, 0] == 3 and dists[0, 0] == 0.0
