@@ -59,7 +59,7 @@ bool binsel_fast_ok(const DevParams& p) {
 }
 
 bool binsel_prefers_walker(const DevParams& p) {
-    return p.P == 4 && bs_config(p).W2ab > 0;
+    return p.P == 4 && p.W2 <= 4096;  // the whole pair-stream grid folded (GIST1M-shaped)
 }
 
 uint64_t binsel_hash_words(const DevParams& p, uint64_t max_batch) {

@@ -72,12 +72,12 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
     const uint32_t end = base + NIT * NT;  // positions of this pass: [base, end)
     // uniform fast path: the whole pass lies inside the stream and (P = 4) inside the
     // materialized merge prefix, so no item needs a bounds or closed-form check
-    const bool fast = end <= total && (P != 4 || (end <= mcount && W2ab && H < 0x80000000u)) &&
+    const bool fast = end <= total && (P != 4 || (end <= mcount && W2ab == W2 && H < 0x80000000u)) &&
                       (P != 2 || H < 0x80000000u);
     uint32_t word[NIT];
     if (fast) {
         if constexpr (P == 4) {
-            const uint32_t* mp = p.merge16 + base + ft;  // fast path: W2ab > 0, so W2 <= 4096
+            const uint32_t* mp = p.merge16 + base + ft;  // fast path: the whole stream folded, W2 <= 4096
             uint32_t e[NIT];
 #pragma unroll
             for (int it = 0; it < NIT; ++it) e[it] = __ldg(mp + it * NT);
@@ -131,7 +131,7 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
                 const uint32_t e = ent[it].x;
                 sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
             } else {
-                if (W2ab) {
+                if (ent[it].x < W2ab && ent[it].y < W2ab) {  // both pair ranks inside the folded prefix
                     sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
                 } else {
                     const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * W2 + ent[it].x);
@@ -451,7 +451,10 @@ inline BsConfig bs_config(const DevParams& p) {
     c.use_hash = span > (long double)p.H ? 1u : 0u;
     c.ts_log2 = 6;
     while ((1ull << c.ts_log2) < ((uint64_t)p.budget + 32) * 3 / 2) ++c.ts_log2;
-    c.W2ab = (p.P == 4 && p.W2 <= 4096) ? (uint32_t)p.W2 : 0u;
+    // P = 4: the pair streams folded into per-pair-rank slot terms -- whole when W² <= 4096
+    // (GIST1M), else their first 256 ranks (SIFT1B's W² = 16384: the merge stream's first few
+    // thousand tuples stay below pair rank ~64), past which a tuple loads its pair-stream entries
+    c.W2ab = p.P == 4 ? (uint32_t)(p.W2 <= 4096 ? p.W2 : 256) : 0u;
     c.smem = bs_layout(p.P * p.W, c.W2ab, 0).total;
     return c;
 }
