@@ -1,3 +1,6 @@
+#!/bin/bash
+# Parity subset + GIST1M/SIFT1M (and SIFT1B with SIFT1B=1) bench lines per kernel variant.
+# usage: VARS="0 3 4" SIFT1B=1 bash tools/cmp_variants.sh
 mkdir -p gpurun_out
 python -m pytest tests -x -q -m gpu -k "parity or topk" 2>&1 | tail -2
 for v in ${VARS:-0}; do
