@@ -30,6 +30,7 @@ namespace bsp {
 
 constexpr int kPItems = 8;
 constexpr uint32_t kPassMax = 256 * kPItems;         // stream positions per full pass
+constexpr uint32_t kPThreadsMax = 256;                // threads per CTA (filter_blocked's pass width)
 constexpr uint32_t kPVisLog2 = 11;
 constexpr uint32_t kPVis = 1u << kPVisLog2;          // shared visited-set entries
 constexpr uint32_t kPVisMax = kPVis * 3 / 4;         // distinct slots before the set moves to global
@@ -104,6 +105,100 @@ __device__ __forceinline__ uint32_t vis_global(uint32_t* gkey, uint32_t* gpos, u
     return h;
 }
 
+// One filter pass in the blocked arrangement: thread t tests stream positions base + t·NIT + i
+// (i < NIT), consecutive in stream order, so a thread's merge / pair-stream entries are one
+// contiguous run (16-byte loads on the fast path). Returns the non-empty bits.
+template <int P, int NIT>
+__device__ __forceinline__ uint32_t filter_blocked(const DevParams& p, uint32_t base, uint32_t total, uint32_t tid,
+                                                   uint32_t ta, uint32_t tb, uint32_t W, uint32_t H,
+                                                   const uint32_t* terms, const uint32_t* tA, const uint32_t* tB,
+                                                   uint32_t W2ab, uint32_t* slot) {
+    const uint32_t W2 = (uint32_t)p.W2;
+    const uint32_t mcount = (uint32_t)p.merge_count;
+    const uint32_t s0 = base + tid * NIT;
+    const uint32_t end = base + NIT * kPThreadsMax;
+    const bool fast = end <= total && (P != 4 || (end <= mcount && W2ab == W2 && H < 0x80000000u)) &&
+                      (P != 2 || H < 0x80000000u);
+    uint32_t word[NIT];
+    if (fast) {
+        uint32_t e[NIT];
+        if constexpr (P == 4 || P == 2) {
+            const uint32_t* src = P == 4 ? p.merge16 + s0 : p.pair_streams + (size_t)ta * W2 + s0;
+            if (NIT % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+                for (int v = 0; v < NIT / 4; ++v) {
+                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(src) + v);
+                    e[4 * v] = x.x;
+                    e[4 * v + 1] = x.y;
+                    e[4 * v + 2] = x.z;
+                    e[4 * v + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) e[it] = __ldg(src + it);
+            }
+#pragma unroll
+            for (int it = 0; it < NIT; ++it)
+                slot[it] = P == 4 ? add_mod_fast(tA[e[it] & 0xFFFFu], tB[e[it] >> 16], H)
+                                  : add_mod_fast(terms[e[it] & 0xFFFFu], terms[W + (e[it] >> 16)], H);
+        } else {
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) slot[it] = terms[s0 + it];
+        }
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) word[it] = __ldg(p.bitmap + (slot[it] >> 5));
+        uint32_t hit = 0;
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) hit |= ((word[it] >> (slot[it] & 31)) & 1u) << it;
+        return hit;
+    }
+    uint2 ent[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const uint32_t s = s0 + it;
+        ent[it] = make_uint2(0, 0);
+        if (s < total) {
+            if constexpr (P == 2) {
+                ent[it].x = __ldg(p.pair_streams + (size_t)ta * W2 + s);
+            } else if constexpr (P == 4) {
+                if (s < mcount) {
+                    ent[it] = __ldg(p.merge + s);
+                } else {  // closed-form sweep rows past the slope-1 table (binorder.cpp:96-108)
+                    const uint32_t j = s - mcount;
+                    const uint32_t u = j / W2;
+                    ent[it] = make_uint2((uint32_t)p.merge_row0 + u, j - u * W2);
+                }
+            }
+        }
+    }
+    uint32_t hit = 0;
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const uint32_t s = s0 + it;
+        uint32_t sl = 0;
+        if constexpr (P == 1) {
+            sl = terms[s < total ? s : 0];
+        } else if constexpr (P == 2) {
+            const uint32_t e = ent[it].x;
+            sl = add_mod(terms[e & 0xFFFFu], terms[W + (e >> 16)], H);
+        } else {
+            if (ent[it].x < W2ab && ent[it].y < W2ab) {  // both pair ranks inside the folded prefix
+                sl = add_mod(tA[ent[it].x], tB[ent[it].y], H);
+            } else {
+                const uint32_t ea = __ldg(p.pair_streams + (size_t)ta * W2 + ent[it].x);
+                const uint32_t eb = __ldg(p.pair_streams + (size_t)tb * W2 + ent[it].y);
+                sl = add_mod(add_mod(terms[ea & 0xFFFFu], terms[W + (ea >> 16)], H),
+                             add_mod(terms[2 * W + (eb & 0xFFFFu)], terms[3 * W + (eb >> 16)], H), H);
+            }
+        }
+        slot[it] = sl;
+        word[it] = __ldg(p.bitmap + (sl >> 5));
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) hit |= (uint32_t)(s0 + it < total && ((word[it] >> (slot[it] & 31)) & 1u)) << it;
+    return hit;
+}
+
 }  // namespace bsp
 
 // NT threads per CTA: 256, four CTAs per SM. (512-thread CTAs, passes twice as long at two CTAs
@@ -130,8 +225,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     uint32_t* vkey = reinterpret_cast<uint32_t*>(smem + lay.vkey);
     uint32_t* vpos = reinterpret_cast<uint32_t*>(smem + lay.vpos);
     __shared__ uint32_t s_slope[2];
-    __shared__ uint32_t s_wc[2][kPItems * kPWarps];                   // hits per (item, warp) (filter)
-    __shared__ uint32_t s_cnt[2][kPItems * kPWarps], s_fst[2][kPItems * kPWarps];  // scan partials
     __shared__ uint32_t s_nvis, s_over, s_emit, s_maxord;
 
     // ---- prologue: slot terms (flat_part_code · (k1k2)^p) mod H (pqtree.cpp:12-25), the slope
@@ -174,39 +267,34 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     uint2* qranges = ranges + q * (uint64_t)budget;
     uint32_t* gkey = HASH ? ghash + (q << (ts_log2 + 1)) : nullptr;
     uint32_t* gpos = HASH ? gkey + (1u << ts_log2) : nullptr;
-    const uint32_t lt = (1u << lane) - 1u;
     uint32_t C = 0, R = 0, base = 0;
     bool done = budget == 0, spilled = false;
     // P = 4 streams run to thousands of tuples: full passes from the start (a first
     // pass of 1024 measured slower even at SIFT1B, whose queries need ~930 tuples: 333 -> 354 us,
     // the pass is latency-bound and the queries past 1024 pay a second one)
     uint32_t nit = P == 4 ? kPItems : 1;
+    __shared__ uint32_t s_wtc[2][kPWarps], s_wtf[2][kPWarps];  // per-warp totals (bin sizes, first flags)
     for (uint32_t pass = 0; !done && base < total32; ++pass) {
         const uint32_t pb = pass & 1u;
-        uint32_t slot[kPItems], ball[kPItems];
-        if (nit == 1)
-            filter<P, 1, kPThreads>(p, base, total32, tid, lane, warp, ta, tb, W, H, terms, tA, tB, W2ab, slot, ball,
-                                   s_wc[pb]);
-        else
-            filter<P, kPItems, kPThreads>(p, base, total32, tid, lane, warp, ta, tb, W, H, terms, tA, tB, W2ab, slot,
-                                        ball, s_wc[pb]);
-        uint32_t first = 0;  // bit it: position base + it·256 + tid is its slot's first occurrence
+        // blocked arrangement: thread t owns stream positions base + t·nit .. + nit − 1, so its
+        // items are consecutive in stream order and one block scan orders the whole pass
+        uint32_t slot[kPItems];
+        const uint32_t hit = nit == 1
+                                 ? filter_blocked<P, 1>(p, base, total32, tid, ta, tb, W, H, terms, tA, tB, W2ab, slot)
+                                 : filter_blocked<P, kPItems>(p, base, total32, tid, ta, tb, W, H, terms, tA, tB, W2ab,
+                                                              slot);
+        uint32_t first = 0;  // bit i: position base + tid·nit + i is its slot's first occurrence
         if constexpr (HASH) {
             uint32_t hidx[kPItems];
 #pragma unroll
             for (int it = 0; it < kPItems; ++it) {
                 hidx[it] = kPNone;
-                if ((ball[it] >> lane) & 1u) {
-                    const uint32_t pos = base + it * kPThreads + tid;
-                    hidx[it] = spilled ? vis_global(gkey, gpos, slot[it] + 1u, pos, ts_log2)
-                                       : vis_shared(vkey, vpos, slot[it] + 1u, pos, &s_nvis, &s_over);
-                }
+                if ((hit >> it) & 1u)
+                    hidx[it] = spilled ? vis_global(gkey, gpos, slot[it] + 1u, base + tid * nit + it, ts_log2)
+                                       : vis_shared(vkey, vpos, slot[it] + 1u, base + tid * nit + it, &s_nvis, &s_over);
             }
-            __syncthreads();
             // a pass without a single non-empty position (most of a sparse stream) ends here
-            uint32_t hits = 0;
-            for (uint32_t e = lane; e < nit * kPWarps; e += 32) hits += s_wc[pb][e];
-            if (__any_sync(0xffffffffu, hits != 0) == 0) {
+            if (!__syncthreads_or(hit != 0)) {
                 base += nit * kPThreads;
                 nit = kPItems;
                 continue;
@@ -215,27 +303,31 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
                 // the shared set is 3/4 full: move it to this query's global table and redo
                 // this pass's positions there (insert + atomicMin commute, so repeats are harmless)
                 const uint32_t TS = 1u << ts_log2;
-                for (uint32_t i = tid; i < TS; i += kPThreads) {
-                    gkey[i] = 0u;
-                    gpos[i] = 0xFFFFFFFFu;
+                for (uint32_t x = tid; x < TS; x += kPThreads) {
+                    gkey[x] = 0u;
+                    gpos[x] = 0xFFFFFFFFu;
                 }
                 __syncthreads();
-                for (uint32_t i = tid; i < kPVis; i += kPThreads)
-                    if (vkey[i]) vis_global(gkey, gpos, vkey[i], vpos[i], ts_log2);
+                for (uint32_t x = tid; x < kPVis; x += kPThreads)
+                    if (vkey[x]) vis_global(gkey, gpos, vkey[x], vpos[x], ts_log2);
 #pragma unroll
                 for (int it = 0; it < kPItems; ++it)
-                    if ((ball[it] >> lane) & 1u)
-                        hidx[it] = vis_global(gkey, gpos, slot[it] + 1u, base + it * kPThreads + tid, ts_log2);
+                    if ((hit >> it) & 1u)
+                        hidx[it] = vis_global(gkey, gpos, slot[it] + 1u, base + tid * nit + it, ts_log2);
                 __syncthreads();
                 spilled = true;
             }
             const uint32_t* vp = spilled ? gpos : vpos;
 #pragma unroll
             for (int it = 0; it < kPItems; ++it)
-                if (hidx[it] != kPNone && vp[hidx[it]] == base + it * kPThreads + tid) first |= 1u << it;
+                if (hidx[it] != kPNone && vp[hidx[it]] == base + tid * nit + it) first |= 1u << it;
         } else {
-#pragma unroll
-            for (int it = 0; it < kPItems; ++it) first |= ((ball[it] >> lane) & 1u) << it;
+            if (!__syncthreads_or(hit != 0)) {
+                base += nit * kPThreads;
+                nit = kPItems;
+                continue;
+            }
+            first = hit;
         }
         // extents of the first occurrences, all loads in flight together
         uint32_t st[kPItems], cn[kPItems];
@@ -248,87 +340,66 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
                 cn[it] = __ldg(p.offsets + slot[it] + 1);
             }
         }
-        // warp-level inclusive scans of bin sizes per item; the (item, warp) totals in stream order
-        uint32_t inc[kPItems];
+        uint32_t tc = 0;
 #pragma unroll
         for (int it = 0; it < kPItems; ++it) {
             cn[it] -= st[it];
-            if (it < (int)nit) {
-                const uint32_t fb = __ballot_sync(0xffffffffu, (first >> it) & 1u);
-                uint32_t x = 0;
-                if (fb) {  // warp-uniform: most (item, warp) groups hold no first occurrence
-                    x = cn[it];
+            tc += cn[it];  // a pass's bins hold < 2^32 ids
+        }
+        const uint32_t tf = __popc(first);
+        // one block scan of (bin sizes, first flags) over threads = stream order
+        uint32_t ic = tc, iff = tf;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-                        if (lane >= (uint32_t)o) x += t;
-                    }
-                }
-                inc[it] = x;
-                if (lane == 31) {
-                    s_cnt[pb][it * kPWarps + warp] = x;
-                    s_fst[pb][it * kPWarps + warp] = __popc(fb);
-                }
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, ic, o), b = __shfl_up_sync(0xffffffffu, iff, o);
+            if (lane >= (uint32_t)o) {
+                ic += a;
+                iff += b;
             }
+        }
+        if (lane == 31) {
+            s_wtc[pb][warp] = ic;
+            s_wtf[pb][warp] = iff;
         }
         __syncthreads();
-        // every warp scans the <= kPItems·kPWarps (item, warp) totals itself: entry r·32 + lane
-        // of row r, rows in stream order; xc / xf = exclusive prefixes over all rows
-        constexpr int kRows = kPItems * kPWarps / 32;
-        const uint32_t ne = nit * kPWarps;
-        uint32_t xcr[kRows], xfr[kRows];
-        uint32_t ccarry = 0, fcarry = 0;
+        uint32_t wc = 0, wf = 0, ctot = 0, ftot = 0;
 #pragma unroll
-        for (int r = 0; r < kRows; ++r) {
-            const uint32_t e = r * 32 + lane;
-            const uint32_t cv = e < ne ? s_cnt[pb][e] : 0u, fv = e < ne ? s_fst[pb][e] : 0u;
-            uint32_t ic = cv, iff = fv;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t a = __shfl_up_sync(0xffffffffu, ic, o), b = __shfl_up_sync(0xffffffffu, iff, o);
-                if (lane >= (uint32_t)o) {
-                    ic += a;
-                    iff += b;
-                }
+        for (int w = 0; w < kPWarps; ++w) {
+            const uint32_t a = s_wtc[pb][w], b = s_wtf[pb][w];
+            if ((uint32_t)w < warp) {
+                wc += a;
+                wf += b;
             }
-            xcr[r] = ccarry + ic - cv;
-            xfr[r] = fcarry + iff - fv;
-            ccarry += __shfl_sync(0xffffffffu, ic, 31);  // bins of one pass hold < 2^32 ids
-            fcarry += __shfl_sync(0xffffffffu, iff, 31);
+            ctot += a;
+            ftot += b;
         }
-        const uint64_t ctot = ccarry;
-        const uint32_t ftot = fcarry;
         done = (uint64_t)C + ctot >= budget;
+        uint64_t before = (uint64_t)C + wc + (ic - tc);
+        uint32_t rank = R + wf + (iff - tf), emitted = 0, maxo = 0;
 #pragma unroll
         for (int it = 0; it < kPItems; ++it) {
-            const bool fst = (first >> it) & 1u;
-            const uint32_t fb = __ballot_sync(0xffffffffu, fst);
-            if (it < (int)nit && fb) {
-                const uint32_t e = it * kPWarps + warp, src = e & 31u, row = e >> 5;  // warp-uniform
-                uint32_t sc = 0, sf = 0;
-#pragma unroll
-                for (int r = 0; r < kRows; ++r)
-                    if ((uint32_t)r == row) {
-                        sc = xcr[r];
-                        sf = xfr[r];
-                    }
-                const uint64_t ec = __shfl_sync(0xffffffffu, sc, src);
-                const uint32_t ef = __shfl_sync(0xffffffffu, sf, src);
-                const uint64_t before = (uint64_t)C + ec + (inc[it] - cn[it]);
-                const bool emit = fst && before < budget;
-                if (emit) qranges[R + ef + __popc(fb & lt)] = make_uint2(st[it], (uint32_t)before);
-                if (done) {
-                    const uint32_t eb = __ballot_sync(0xffffffffu, emit);
-                    const uint32_t mo = __reduce_max_sync(0xffffffffu, emit ? base + it * kPThreads + tid + 1u : 0u);
-                    if (lane == 0 && eb) {
-                        atomicAdd(&s_emit, __popc(eb));
-                        atomicMax(&s_maxord, mo);
-                    }
+            if ((first >> it) & 1u) {
+                if (before < budget) {
+                    qranges[rank] = make_uint2(st[it], (uint32_t)before);
+                    ++emitted;
+                    maxo = base + tid * nit + it + 1u;
                 }
+                before += cn[it];
+                ++rank;
             }
         }
-        if (!done) {
-            C += (uint32_t)ctot;
+        if (done) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                emitted += __shfl_xor_sync(0xffffffffu, emitted, o);
+                maxo = max(maxo, __shfl_xor_sync(0xffffffffu, maxo, o));
+            }
+            if (lane == 0 && emitted) {
+                atomicAdd(&s_emit, emitted);
+                atomicMax(&s_maxord, maxo);
+            }
+        } else {
+            C += ctot;
             R += ftot;
         }
         base += nit * kPThreads;
