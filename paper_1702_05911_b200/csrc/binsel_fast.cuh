@@ -72,12 +72,14 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
     const uint32_t end = base + NIT * NT;  // positions of this pass: [base, end)
     // uniform fast path: the whole pass lies inside the stream and (P = 4) inside the
     // materialized merge prefix, so no item needs a bounds or closed-form check
-    const bool fast = end <= total && (P != 4 || (end <= mcount && W2ab == W2 && H < 0x80000000u)) &&
+    const bool fast = end <= total &&
+                      (P != 4 || (end <= mcount && p.merge16 && (W2ab == W2 || end <= p.merge_fold_end) &&
+                                  H < 0x80000000u)) &&
                       (P != 2 || H < 0x80000000u);
     uint32_t word[NIT];
     if (fast) {
         if constexpr (P == 4) {
-            const uint32_t* mp = p.merge16 + base + ft;  // fast path: the whole stream folded, W2 <= 4096
+            const uint32_t* mp = p.merge16 + base + ft;  // fast path: every (u, v) of the pass is folded
             uint32_t e[NIT];
 #pragma unroll
             for (int it = 0; it < NIT; ++it) e[it] = __ldg(mp + it * NT);
@@ -454,7 +456,7 @@ inline BsConfig bs_config(const DevParams& p) {
     // P = 4: the pair streams folded into per-pair-rank slot terms -- whole when W² <= 4096
     // (GIST1M), else their first 256 ranks (SIFT1B's W² = 16384: the merge stream's first few
     // thousand tuples stay below pair rank ~64), past which a tuple loads its pair-stream entries
-    c.W2ab = p.P == 4 ? (uint32_t)(p.W2 <= 4096 ? p.W2 : 256) : 0u;
+    c.W2ab = p.P == 4 ? (uint32_t)(p.W2 <= 4096 ? p.W2 : kPartialFold) : 0u;
     c.smem = bs_layout(p.P * p.W, c.W2ab, 0).total;
     return c;
 }

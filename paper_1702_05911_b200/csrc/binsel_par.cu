@@ -117,7 +117,9 @@ __device__ __forceinline__ uint32_t filter_blocked(const DevParams& p, uint32_t 
     const uint32_t mcount = (uint32_t)p.merge_count;
     const uint32_t s0 = base + tid * NIT;
     const uint32_t end = base + NIT * kPThreadsMax;
-    const bool fast = end <= total && (P != 4 || (end <= mcount && W2ab == W2 && H < 0x80000000u)) &&
+    const bool fast = end <= total &&
+                      (P != 4 || (end <= mcount && p.merge16 && (W2ab == W2 || end <= p.merge_fold_end) &&
+                                  H < 0x80000000u)) &&
                       (P != 2 || H < 0x80000000u);
     uint32_t word[NIT];
     if (fast) {

@@ -361,6 +361,10 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
         p.merge_row0 = hs.merge_row0;
         if (!hs.pair.empty()) p.pair_streams = upload(*ix, hs.pair.data(), hs.pair.size());
         if (!hs.merge.empty()) p.merge = upload(*ix, hs.merge.data(), hs.merge.size());
+        p.merge_fold_end = 0;
+        while (p.merge_fold_end < hs.merge.size() && hs.merge[p.merge_fold_end].x < kPartialFold &&
+               hs.merge[p.merge_fold_end].y < kPartialFold)
+            ++p.merge_fold_end;
         if (!hs.merge.empty() && hs.W2 <= 65536) {  // the same (u, v) as u | v << 16: half the bytes per probe
             std::vector<uint32_t> m16(hs.merge.size());
             for (size_t i = 0; i < m16.size(); ++i) m16[i] = hs.merge[i].x | (hs.merge[i].y << 16);

@@ -34,6 +34,7 @@ struct Error {
 constexpr uint32_t kSlopeTables = 10;      // binorder.hpp:25
 constexpr uint32_t kSlopeOne = 5;          // slope 1.08^0 (binorder.cpp:59-64, :237)
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
+constexpr uint32_t kPartialFold = 256;    // pair ranks folded when W² > 4096 (binsel_fast.cuh bs_config)
 
 // Everything a kernel needs, passed by value (fits the parameter space).
 struct DevParams {
@@ -56,6 +57,7 @@ struct DevParams {
     const uint32_t* pair_streams;  // [10][W*W] (a | b << 16), PairCursor order per table
     const uint2* merge;            // [merge_count] (u, v) for P == 4
     const uint32_t* merge16;       // [merge_count] u | v << 16 (W2 <= 65536), or null
+    uint64_t merge_fold_end;       // merge entries [0, this) have u, v < kPartialFold
     uint64_t merge_count;
     uint64_t merge_row0;           // first closed-form sweep row
     uint64_t W2;
