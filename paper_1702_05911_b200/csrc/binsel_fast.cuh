@@ -302,7 +302,6 @@ __device__ __forceinline__ void binsel_fast_body(const DevParams& p, uint64_t q,
     uint32_t* tB = reinterpret_cast<uint32_t*>(smem + lay.tb);
     uint2* queue = reinterpret_cast<uint2*>(smem + lay.queue);
     uint32_t* svis = reinterpret_cast<uint32_t*>(smem + lay.svis);
-    const uint32_t TS = 1u << ts_log2;
     uint32_t* hkeys = HASH ? ghash + (q << ts_log2) : nullptr;
     __shared__ uint32_t wcnt[2][64];
     __shared__ uint32_t s_nq[2], s_C, s_R, s_maxord;

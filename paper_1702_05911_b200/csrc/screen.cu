@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
                                                               float* __restrict__ fine_out,
                                                               float* __restrict__ l2d_out,
                                                               uint32_t* __restrict__ l2c_out) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t k1 = K1T ? (uint32_t)K1T : p.k1, k2 = K2T ? (uint32_t)K2T : p.k2;
     const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W, nj0 = k1 * k2;
     float* y = reinterpret_cast<float*>(smem);                     // m
