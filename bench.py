@@ -636,7 +636,12 @@ def main():
                 "stage_share": {n: float(v / stage_mean[:3].sum()) for n, v in zip(names, stage_mean[:3])},
                 "per_kernel_gbs": {n: ab[n] / (stage_mean[i] / 1000.0) / 1e9 for i, n in enumerate(names)},
                 "T_q": ab["T_q"], "C_q": ab["C_q"], "bins_q": ab["bins_q"],
-                "survey_Bq_gbs": ab["survey_Bq_total"] / (ms_max / args.steps / 1000.0) / 1e9}
+                "survey_Bq_gbs": ab["survey_Bq_total"] / (ms_max / args.steps / 1000.0) / 1e9,
+                # what bounds each kernel instead of HBM (ncu, profiles/r01h/ncu_full_summary_*.txt)
+                "limiter": {"traverse": "issue (IPC ~3.5, sequential fp32 chains + level-2 sort)",
+                            "binsel": "latency / L2-probe throughput per pass (issue active ~22-60%)",
+                            "rerank": "issue + shared-memory pipe (~14 SASS and 2 LDS per part, issue "
+                                      "active ~64%; real DRAM traffic ~1/4 of the algorithmic bytes)"}}
 
     # ---- CPU baseline (rank 0, N=1) + parity of the timed batch
     cpu = None
