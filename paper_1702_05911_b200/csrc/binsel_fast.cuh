@@ -62,6 +62,23 @@ __device__ __forceinline__ uint32_t add_mod_fast(uint32_t a, uint32_t b, uint32_
     return min(x, x - H);      // x - H wraps above x when x < H
 }
 
+// The non-empty bits of NIT slots: the fine bitmap word of each, looked up only when the coarse
+// bitmap (1 bit per 2^coarse_shift slots, L1-resident, built for sparse indexes) has the group.
+template <int NIT>
+__device__ __forceinline__ void probe_bitmap(const DevParams& p, const uint32_t* slot, uint32_t* word) {
+    if (p.bitmap_coarse) {
+        uint32_t cw[NIT];
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) cw[it] = __ldg(p.bitmap_coarse + ((slot[it] >> p.coarse_shift) >> 5));
+#pragma unroll
+        for (int it = 0; it < NIT; ++it)
+            word[it] = ((cw[it] >> ((slot[it] >> p.coarse_shift) & 31u)) & 1u) ? __ldg(p.bitmap + (slot[it] >> 5)) : 0u;
+    } else {
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) word[it] = __ldg(p.bitmap + (slot[it] >> 5));
+    }
+}
+
 template <int P, int NIT, int NT = kFilterThreads>
 __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32_t total, int ft, int lane, int fw,
                                        uint32_t ta, uint32_t tb, uint32_t W, uint32_t H, const uint32_t* terms,
@@ -96,8 +113,7 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
 #pragma unroll
             for (int it = 0; it < NIT; ++it) slot[it] = terms[base + it * NT + ft];
         }
-#pragma unroll
-        for (int it = 0; it < NIT; ++it) word[it] = __ldg(p.bitmap + (slot[it] >> 5));
+        probe_bitmap<NIT>(p, slot, word);
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
             ball[it] = __ballot_sync(0xffffffffu, (word[it] >> (slot[it] & 31)) & 1u);
@@ -143,8 +159,8 @@ __device__ __forceinline__ void filter(const DevParams& p, uint32_t base, uint32
                 }
             }
             slot[it] = sl;
-            word[it] = __ldg(p.bitmap + (sl >> 5));
         }
+        probe_bitmap<NIT>(p, slot, word);
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
             const uint32_t s = base + it * NT + ft;

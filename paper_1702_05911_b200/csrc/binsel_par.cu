@@ -147,8 +147,7 @@ __device__ __forceinline__ uint32_t filter_blocked(const DevParams& p, uint32_t 
 #pragma unroll
             for (int it = 0; it < NIT; ++it) slot[it] = terms[s0 + it];
         }
-#pragma unroll
-        for (int it = 0; it < NIT; ++it) word[it] = __ldg(p.bitmap + (slot[it] >> 5));
+        probe_bitmap<NIT>(p, slot, word);
         uint32_t hit = 0;
 #pragma unroll
         for (int it = 0; it < NIT; ++it) hit |= ((word[it] >> (slot[it] & 31)) & 1u) << it;
@@ -194,8 +193,8 @@ __device__ __forceinline__ uint32_t filter_blocked(const DevParams& p, uint32_t 
             }
         }
         slot[it] = sl;
-        word[it] = __ldg(p.bitmap + (sl >> 5));
     }
+    probe_bitmap<NIT>(p, slot, word);
 #pragma unroll
     for (int it = 0; it < NIT; ++it) hit |= (uint32_t)(s0 + it < total && ((word[it] >> (slot[it] & 31)) & 1u)) << it;
     return hit;

@@ -383,6 +383,29 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
         }
         p.bitmap = upload(*ix, bitmap.data(), bitmap.size());
         p.offsets = upload(*ix, off32.data(), off32.size());
+        // a coarse bitmap (1 bit per 2^coarse_shift slots, <= 32 KB, L1-resident) in front of
+        // the fine one when the slots are sparse: most empty probes then never reach L2
+        uint64_t occupied = 0;
+        for (uint32_t w : bitmap) occupied += (uint64_t)__builtin_popcount(w);
+        uint32_t g = 4;
+        while ((H >> g) > 32 * 1024 * 8) ++g;
+        const double occ = H ? (double)occupied / (double)H : 1.0;
+        const double density = 1.0 - std::pow(1.0 - occ, (double)(1u << g));
+        p.coarse_shift = 0;
+        p.bitmap_coarse = nullptr;
+        if (density < 0.25) {
+            std::vector<uint32_t> coarse(((H >> g) + 32) / 32 + 1, 0u);
+            for (uint64_t w = 0; w < bitmap.size(); ++w) {
+                uint32_t bits = bitmap[w];
+                while (bits) {
+                    const uint64_t s = w * 32 + (uint64_t)__builtin_ctz(bits);
+                    bits &= bits - 1;
+                    coarse[(s >> g) >> 5] |= 1u << ((s >> g) & 31);
+                }
+            }
+            p.coarse_shift = g;
+            p.bitmap_coarse = upload(*ix, coarse.data(), coarse.size());
+        }
     }
 
     // --- k1 <= 16 with 1-byte pairs: codes carry the pair's centroids as t = i << 4 | ((i + j) & 15)

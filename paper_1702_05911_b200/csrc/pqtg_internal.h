@@ -67,6 +67,8 @@ struct DevParams {
     const uint32_t* pairs;      // [npairs] (i | j << 16)
     const float* c2;            // [L][npairs]  d2[f][i][j] per pair
     const uint32_t* bitmap;     // [ceil(H / 32)] non-empty slots
+    const uint32_t* bitmap_coarse;  // 1 bit per 2^coarse_shift slots (sparse slots only), or null
+    uint32_t coarse_shift;
     const uint32_t* offsets;    // [H + 1] u32
     const uint32_t* ids;        // [shard positions]
     const uint8_t* codes;       // [shard positions][row_bytes]
