@@ -385,7 +385,7 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
         p.bitmap = upload(*ix, bitmap.data(), bitmap.size());
         p.offsets = upload(*ix, off32.data(), off32.size());
         // a coarse bitmap (1 bit per 2^coarse_shift slots, 2 KB, L1-resident) in front of the
-        // fine one when the slots are sparse (< 1.8% occupied): most empty probes then never
+        // fine one when the slots are sparse (< 1.8% occupied, P = 4): most empty probes never
         // reach L2. GIST1M (0.24% occupied) bins: 72 -> 51 us; the table size was swept
         // 128 KB .. 2 KB (71, 60, 54, 53, 52, 51, 51 us) -- a query's probes cluster, so a tiny
         // table stays in L1 and still filters
@@ -396,7 +396,9 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
         const double occ = H ? (double)occupied / (double)H : 1.0;
         p.coarse_shift = 0;
         p.bitmap_coarse = nullptr;
-        if (occ < 0.018) {
+        // P = 4 only: its streams run thousands of mostly empty probes per query; P <= 2
+        // queries probe a few dozen mostly non-empty slots (SIFT1M bins: 58.4 -> 60.6 us with it)
+        if (occ < 0.018 && P == 4) {
             std::vector<uint32_t> coarse(((H >> g) + 32) / 32 + 1, 0u);
             for (uint64_t w = 0; w < bitmap.size(); ++w) {
                 uint32_t bits = bitmap[w];
