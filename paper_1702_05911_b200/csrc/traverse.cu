@@ -14,6 +14,7 @@
 // Exactness: every sum is the reference's sequential fp32 chain (common.cuh sq_step,
 // explicit __f*_rn), every sort reproduces its total order.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "pqtg_internal.h"
@@ -251,6 +252,89 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     }
 }
 
+// Small trees (W = w·k2 <= 32, k1 <= 32, P <= 4): one CTA per query, one warp per part, no
+// block barrier after the query is staged. In traverse_part_kernel three of its four warps wait
+// at a barrier while one warp runs the W level-2 chains; here every warp runs its own part's
+// chains, reading the parents' [m][k2] blocks straight from L2 (the level-2 codebooks are
+// shared by all queries) with eight loads in flight, and sorts them with a one-warp network.
+template <int K1T, int K2T, int FB>
+__global__ void __launch_bounds__(128) traverse_warp_kernel(DevParams p, const float* __restrict__ Q,
+                                                            float* __restrict__ fine_out, float* __restrict__ l2d_out,
+                                                            uint32_t* __restrict__ l2c_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t k1 = K1T ? (uint32_t)K1T : p.k1, k2 = K2T ? (uint32_t)K2T : p.k2;
+    const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W;
+    const uint64_t q = blockIdx.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, part = tid >> 5;
+    float* y = reinterpret_cast<float*>(smem);                        // [D]
+    float* fine = y + ((p.D + 3) & ~3u) + part * pp * 32;             // [P][pp][<= 32]
+    float* l1d = y + ((p.D + 3) & ~3u) + P * pp * 32 + part * 32;     // [P][32]
+    uint32_t* l1o = reinterpret_cast<uint32_t*>(y + ((p.D + 3) & ~3u) + P * pp * 32 + P * 32) + part * 32;
+    for (uint32_t t = tid; t < p.D; t += blockDim.x) y[t] = __ldg(Q + q * p.D + t);
+    __syncthreads();
+    if (part >= P) return;
+    const uint32_t f0 = part * pp, jobs = pp * k1;
+    // fine_dists[f][i] = l2_sq(y_f, slice(f, i), fd), sequential (pqtree.cpp:90-93)
+    for (uint32_t idx = lane; idx < jobs; idx += 32) {
+        const uint32_t lf = idx / k1, i = idx - lf * k1;
+        const float* yf = y + (f0 + lf) * fd;
+        const float* c = p.fine_t + (size_t)(f0 + lf) * fd * k1 + i;
+        float acc = 0.0f;
+        for (uint32_t t0 = 0; t0 < fd; t0 += FB) {
+            float cv[FB];
+#pragma unroll
+            for (int u = 0; u < FB; ++u) cv[u] = t0 + u < fd ? __ldg(c + (size_t)(t0 + u) * k1) : 0.0f;
+#pragma unroll
+            for (int u = 0; u < FB; ++u)
+                if (t0 + u < fd) acc = sq_step(acc, yf[t0 + u], cv[u]);
+        }
+        fine[lf * k1 + i] = acc;
+        fine_out[(q * p.L + f0 + lf) * k1 + i] = acc;
+    }
+    __syncwarp();
+    // level-1 totals in f order (pqtree.cpp:88-96), ranked by (dist, id) (:98-100)
+    if (lane < k1) {
+        float tot = 0.0f;
+        for (uint32_t lf = 0; lf < pp; ++lf) tot = __fadd_rn(tot, fine[lf * k1 + lane]);
+        l1d[lane] = tot;
+    }
+    __syncwarp();
+    if (lane < k1) {
+        const float d = l1d[lane];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < k1; ++j) {
+            const float dj = l1d[j];
+            rank += (dj < d) || (dj == d && j < lane);
+        }
+        l1o[rank] = lane;
+    }
+    __syncwarp();
+    // level-2: l2_sq(y_p, L2[part][parent][c], m), sequential over m (pqtree.cpp:102-111)
+    uint64_t key = ~0ull;
+    if (lane < W) {
+        const uint32_t r = lane / k2, c = lane - r * k2, parent = l1o[r];
+        const float* cb = p.l2_t + ((size_t)part * k1 + parent) * m * k2 + c;
+        const float* yp = y + part * m;
+        float acc = 0.0f;
+        uint32_t t = 0;
+        for (; t + 8 <= m; t += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(cb + (size_t)(t + u) * k2);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = sq_step(acc, yp[t + u], v[u]);
+        }
+        for (; t < m; ++t) acc = sq_step(acc, yp[t], __ldg(cb + (size_t)t * k2));
+        key = ((uint64_t)orderable(acc) << 32) | ((parent << 16) | c);
+    }
+    key = bitonic_block<32>(key, lane, nullptr);  // (dist, parent, child) (pqtree.cpp:112-117)
+    if (lane < W) {
+        const size_t out = (q * P + part) * W + lane;
+        l2d_out[out] = unorderable((uint32_t)(key >> 32));
+        l2c_out[out] = (uint32_t)key;
+    }
+}
+
 namespace {
 
 template <int A, int B, int FB>
@@ -284,8 +368,34 @@ void configure_traverse_part() {
     tp_allow<0, 0>(optin);
 }
 
+size_t tw_smem(const DevParams& p) {
+    return ((size_t)((p.D + 3) & ~3u) + (size_t)p.P * p.per_part * 32 + (size_t)p.P * 32 * 2) * 4;
+}
+
+bool traverse_warp_ok(const DevParams& p) {
+    static const bool off = std::getenv("PQTG_NO_TRAVERSE_WARP") != nullptr;
+    // short level-2 chains only: SIFT1M (m = 64) 59 -> 51 us, DEEP (m = 48) 54 -> 45 us; GIST1M
+    // (m = 240) is faster with its blocks staged in shared memory (33 vs 37 us)
+    return !off && p.W <= 32 && p.k1 <= 32 && p.P <= 4 && p.m <= 128 && tw_smem(p) <= 48 * 1024;
+}
+
 void launch_traverse_part(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                           cudaStream_t s) {
+    if (traverse_warp_ok(p)) {
+        const size_t sm = tw_smem(p);
+        const unsigned th = 32 * p.P;
+#define PQTG_TW(A, B)                                                                                           \
+    (p.fd <= 8 ? traverse_warp_kernel<A, B, 8><<<(unsigned)nq, th, sm, s>>>(p, queries, ws.fine, ws.l2_dist,     \
+                                                                            ws.l2_code)                          \
+               : traverse_warp_kernel<A, B, 32><<<(unsigned)nq, th, sm, s>>>(p, queries, ws.fine, ws.l2_dist,    \
+                                                                             ws.l2_code))
+        if (p.k1 == 16 && p.k2 == 8) PQTG_TW(16, 8);
+        else if (p.k1 == 16 && p.k2 == 16) PQTG_TW(16, 16);
+        else PQTG_TW(0, 0);
+#undef PQTG_TW
+        PQTG_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     const TpLayout lay = tp_layout(p);
     const uint64_t mk_bytes = (uint64_t)p.m * p.k2 * 4, row_bytes = (uint64_t)lay.rows * p.k2 * 4;
     const uint32_t bulk = (mk_bytes % 16 == 0 && row_bytes % 16 == 0 && (lay.blk_stride * 4) % 16 == 0 &&
