@@ -125,3 +125,33 @@ def test_errors_without_gpu_are_reported_not_crashes():
     bad.config.w = 100
     assert lib().pqtg_index_create(C.byref(bad), 0, C.byref(h)) == -2
     assert b"w must be in" in lib().pqtg_last_error()
+
+
+def test_kernel_variant_selector_range():
+    """pqtg_set_kernel_variant: 0 auto, 1 generic, 2 tensor-core screen, 3 / 4 walker / all-warp
+    bin selection (include/pqtg.h); anything else is an argument error."""
+    L = lib()
+    try:
+        for v in range(5):
+            assert L.pqtg_set_kernel_variant(v) == 0
+        assert L.pqtg_set_kernel_variant(5) == -7  # PQTG_ERR_ARG
+        assert L.pqtg_set_kernel_variant(-1) == -7
+        assert b"variant must be" in L.pqtg_last_error()
+    finally:
+        L.pqtg_set_kernel_variant(0)
+
+
+def test_brute_force_argument_errors_without_device_work():
+    """pqtg_brute_force_knn rejects bad arguments before touching a device."""
+    import numpy as np
+
+    L = lib()
+    q = np.zeros((2, 8), np.float32)
+    out_i = np.zeros((2, 4), np.uint32)
+    out_d = np.zeros((2, 4), np.float32)
+    out_c = np.zeros(2, np.uint32)
+    assert L.pqtg_brute_force_knn(None, 10, 8, q.ctypes.data, 2, 4, 0, out_i.ctypes.data, out_d.ctypes.data,
+                                  out_c.ctypes.data, None) == -7  # PQTG_ERR_ARG: null db with n > 0
+    db = np.zeros((10, 8), np.float32)
+    assert L.pqtg_brute_force_knn(db.ctypes.data, 10, 0, q.ctypes.data, 2, 4, 0, out_i.ctypes.data,
+                                  out_d.ctypes.data, out_c.ctypes.data, None) < 0  # dim 0
