@@ -252,3 +252,28 @@ def test_gpu_brute_force_knn(n, dim, k):
         assert np.array_equal(ids[:, :c], r_ids[:, :c])
         assert np.array_equal(dists[:, :c].view(np.uint32), r_d[:, :c].view(np.uint32))
         assert ids[0, 0] == 3 and dists[0, 0] == 0.0
+
+
+def test_gpu_brute_force_device_entry_point():
+    """pqtg_brute_force_knn_device (device buffers, caller stream; what bench.py's recall uses)
+    equals the host entry point."""
+    import torch
+
+    from paper_1702_05911_b200 import brute_force_knn
+    from paper_1702_05911_b200._abi import check, lib
+
+    rng = np.random.default_rng(5)
+    db = rng.standard_normal((7000, 96)).astype(np.float32)
+    Q = rng.standard_normal((33, 96)).astype(np.float32)
+    k = 17
+    ids, dists, counts, _ = brute_force_knn(db, Q, k)
+    d_db, d_q = torch.from_numpy(db).cuda(), torch.from_numpy(Q).cuda()
+    d_i = torch.empty((33, k), dtype=torch.int32, device="cuda")
+    d_d = torch.empty((33, k), dtype=torch.float32, device="cuda")
+    d_c = torch.empty(33, dtype=torch.int32, device="cuda")
+    check(lib().pqtg_brute_force_knn_device(d_db.data_ptr(), 7000, 96, d_q.data_ptr(), 33, k, d_i.data_ptr(),
+                                            d_d.data_ptr(), d_c.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert np.array_equal(d_i.cpu().numpy().view(np.uint32), ids)
+    assert np.array_equal(d_d.cpu().numpy().view(np.uint32), dists.view(np.uint32))
+    assert np.array_equal(d_c.cpu().numpy().view(np.uint32), counts)
