@@ -335,6 +335,134 @@ __global__ void __launch_bounds__(128) traverse_warp_kernel(DevParams p, const f
     }
 }
 
+// Ascending bitonic sort of 32·EPT u64 keys held by one warp in registers, lane l holding keys
+// l·EPT + i: exchanges below distance EPT stay in the lane (one thread does both sides), the
+// others go through shuffles.
+template <int EPT>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&e)[EPT], uint32_t lane) {
+    constexpr uint32_t N = 32 * EPT;
+#pragma unroll
+    for (uint32_t kk = 2; kk <= N; kk <<= 1) {
+#pragma unroll
+        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+            if (jj < (uint32_t)EPT) {
+#pragma unroll
+                for (uint32_t i = 0; i < (uint32_t)EPT; ++i) {
+                    if (i & jj) continue;
+                    const uint32_t n = lane * EPT + i;
+                    const uint64_t a = e[i], b = e[i ^ jj];
+                    const bool sw = ((n & kk) == 0) ? (b < a) : (a < b);
+                    e[i] = sw ? b : a;
+                    e[i ^ jj] = sw ? a : b;
+                }
+            } else {
+#pragma unroll
+                for (uint32_t i = 0; i < (uint32_t)EPT; ++i) {
+                    const uint32_t n = lane * EPT + i;
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, e[i], jj / EPT);
+                    const bool take_min = ((n & kk) == 0) == ((n & jj) == 0);
+                    e[i] = (take_min ? (o < e[i]) : (o > e[i])) ? o : e[i];
+                }
+            }
+        }
+    }
+}
+
+// The warp-per-part traversal for W = 32·EPT > 32 (the SIFT1B tree: W = 128, k2 = 16): lane l
+// owns children l·EPT .. l·EPT + EPT − 1 — consecutive children of one parent when k2 % EPT == 0,
+// read as one 16-byte load per t — and sorts the part's W keys held in registers.
+template <int K1T, int K2T, int EPT>
+__global__ void __launch_bounds__(128) traverse_warp_wide_kernel(DevParams p, const float* __restrict__ Q,
+                                                                 float* __restrict__ fine_out,
+                                                                 float* __restrict__ l2d_out,
+                                                                 uint32_t* __restrict__ l2c_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr uint32_t k1 = K1T, k2 = K2T;
+    const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W;
+    const uint64_t q = blockIdx.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, part = tid >> 5;
+    float* y = reinterpret_cast<float*>(smem);
+    float* fine = y + ((p.D + 3) & ~3u) + part * pp * 32;
+    float* l1d = y + ((p.D + 3) & ~3u) + P * pp * 32 + part * 32;
+    uint32_t* l1o = reinterpret_cast<uint32_t*>(y + ((p.D + 3) & ~3u) + P * pp * 32 + P * 32) + part * 32;
+    for (uint32_t t = tid; t < p.D; t += blockDim.x) y[t] = __ldg(Q + q * p.D + t);
+    __syncthreads();
+    if (part >= P) return;
+    const uint32_t f0 = part * pp, jobs = pp * k1;
+    // fine LUT (pqtree.cpp:90-93): jobs / 32 independent sequential chains per lane
+    for (uint32_t idx = lane; idx < jobs; idx += 32) {
+        const uint32_t lf = idx / k1, i = idx - lf * k1;
+        const float* yf = y + (f0 + lf) * fd;
+        const float* c = p.fine_t + (size_t)(f0 + lf) * fd * k1 + i;
+        float acc = 0.0f;
+        for (uint32_t t = 0; t < fd; ++t) acc = sq_step(acc, yf[t], __ldg(c + (size_t)t * k1));
+        fine[lf * k1 + i] = acc;
+        fine_out[(q * p.L + f0 + lf) * k1 + i] = acc;
+    }
+    __syncwarp();
+    if (lane < k1) {
+        float tot = 0.0f;
+        for (uint32_t lf = 0; lf < pp; ++lf) tot = __fadd_rn(tot, fine[lf * k1 + lane]);
+        l1d[lane] = tot;
+    }
+    __syncwarp();
+    if (lane < k1) {
+        const float d = l1d[lane];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < k1; ++j) {
+            const float dj = l1d[j];
+            rank += (dj < d) || (dj == d && j < lane);
+        }
+        l1o[rank] = lane;
+    }
+    __syncwarp();
+    // level-2 chains (pqtree.cpp:102-111): EPT children of one parent per lane
+    uint64_t key[EPT];
+    const uint32_t j0 = lane * EPT, r = j0 / k2, c0 = j0 - r * k2;
+    const bool live = j0 < W;
+    const uint32_t parent = live ? l1o[r] : 0u;
+    const float* cb = p.l2_t + ((size_t)part * k1 + parent) * m * k2 + c0;
+    const float* yp = y + part * m;
+    float acc[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) acc[e] = 0.0f;
+    if (live) {
+        for (uint32_t t = 0; t < m; t += 4) {
+            float4 v[4][EPT / 4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int e4 = 0; e4 < EPT / 4; ++e4)
+                    v[u][e4] = t + u < m ? __ldg(reinterpret_cast<const float4*>(cb + (size_t)(t + u) * k2) + e4)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (t + u >= m) break;
+                const float yv = yp[t + u];
+#pragma unroll
+                for (int e4 = 0; e4 < EPT / 4; ++e4) {
+                    acc[4 * e4 + 0] = sq_step(acc[4 * e4 + 0], yv, v[u][e4].x);
+                    acc[4 * e4 + 1] = sq_step(acc[4 * e4 + 1], yv, v[u][e4].y);
+                    acc[4 * e4 + 2] = sq_step(acc[4 * e4 + 2], yv, v[u][e4].z);
+                    acc[4 * e4 + 3] = sq_step(acc[4 * e4 + 3], yv, v[u][e4].w);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+        key[e] = live ? ((uint64_t)orderable(acc[e]) << 32) | ((parent << 16) | (c0 + e)) : ~0ull;
+    warp_sort_regs<EPT>(key, lane);  // (dist, parent, child) (pqtree.cpp:112-117)
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        const uint32_t o = lane * EPT + e;
+        if (o < W) {
+            l2d_out[(q * P + part) * W + o] = unorderable((uint32_t)(key[e] >> 32));
+            l2c_out[(q * P + part) * W + o] = (uint32_t)key[e];
+        }
+    }
+}
+
 namespace {
 
 template <int A, int B, int FB>
@@ -379,8 +507,20 @@ bool traverse_warp_ok(const DevParams& p) {
     return !off && p.W <= 32 && p.k1 <= 32 && p.P <= 4 && p.m <= 128 && tw_smem(p) <= 48 * 1024;
 }
 
+bool traverse_warp_wide_ok(const DevParams& p) {
+    static const bool off = std::getenv("PQTG_NO_TRAVERSE_WARP") != nullptr;
+    return !off && p.W == 128 && p.k1 == 32 && p.k2 == 16 && p.P <= 4 && p.m <= 128 && tw_smem(p) <= 48 * 1024 &&
+           (reinterpret_cast<uintptr_t>(p.l2_t) & 15) == 0;
+}
+
 void launch_traverse_part(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                           cudaStream_t s) {
+    if (traverse_warp_wide_ok(p)) {
+        traverse_warp_wide_kernel<32, 16, 4><<<(unsigned)nq, 32 * p.P, tw_smem(p), s>>>(p, queries, ws.fine,
+                                                                                      ws.l2_dist, ws.l2_code);
+        PQTG_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     if (traverse_warp_ok(p)) {
         const size_t sm = tw_smem(p);
         const unsigned th = 32 * p.P;

@@ -277,3 +277,25 @@ def test_gpu_brute_force_device_entry_point():
     assert np.array_equal(d_i.cpu().numpy().view(np.uint32), ids)
     assert np.array_equal(d_d.cpu().numpy().view(np.uint32), dists.view(np.uint32))
     assert np.array_equal(d_c.cpu().numpy().view(np.uint32), counts)
+
+
+def test_gpu_sift1b_tree_small():
+    """The SIFT1B tree (P = 4, k1 = 32, k2 = 16, w = 8: W = 128, 2-byte pair codes, H = 2^20) on a
+    GPU-built 80k index: the wide warp-per-part traversal, the partial pair-stream fold and the
+    K1M = 32 re-rank against the C oracle, unsharded and as 8 position shards merged."""
+    import torch
+
+    from paper_1702_05911_b200 import merge_topk_host, shard_range
+
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=128, p_tree=4, k1=32, k2=16, w=8, p_line=32, train_iters=4, seed=81, candidate_budget=2048,
+                    hash_size=1 << 20, rerank_exact=0)
+    X = builder.synth_clustered(80_000 + 40, cfg.dim, 400, 20.0, 81, device=dev)
+    db, Q = X[:80_000], X[80_000:].cpu().numpy()
+    hix = builder.build_index(db, db[:30_000], cfg)
+    want = Oracle(hix).knn(Q, 100)
+    assert_same_results(DeviceIndex(hix).search(Q, 100), want, "sift1b tree")
+    parts = [DeviceIndex(hix, shard=shard_range(hix.n, 8, r)).search(Q, 100) for r in range(8)]
+    mi, md, mc = merge_topk_host(np.stack([x[0] for x in parts]), np.stack([x[1] for x in parts]),
+                                 np.stack([x[2] for x in parts]))
+    assert_same_results((mi, md, mc, want[3]), want, "sift1b tree, 8 shards")
