@@ -51,10 +51,13 @@ WORKLOADS = {
     # a DEEP-shaped single-GPU config at 10M (configs[2] shape at 1/10 scale)
     "deep10m": dict(config=dict(dim=96, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=4096),
                     n=10_000_000, nq=10000, k=100, blobs=10_000, sigma=20.0, ntrain=100_000),
-    # BASELINE.json configs[2]: DEEP1B-shaped 100M x 96-D, HBM-resident on one B200 (H = 2^26);
-    # built in memory on the GPU (not cached: the container would be ~7 GB)
+    # BASELINE.json configs[2]: DEEP1B-shaped 100M x 96-D, HBM-resident on one B200 (H = 2^26) -- the
+    # N=1 default. The index is built by the REFERENCE (pqtref IndexBuilder waves, keep_raw=false,
+    # search.cpp:52-117) from a chunked synthetic stream, written with pqtref save_index, and read by
+    # the GPU path through pqtg_index_load (index="reference"; --index gpu builds it on the GPU).
     "deep100m": dict(config=dict(dim=96, p_tree=2, k1=16, k2=8, w=4, p_line=32, candidate_budget=4096),
-                     n=100_000_000, nq=10000, k=100, blobs=100_000, sigma=20.0, ntrain=100_000, cache=False),
+                     n=100_000_000, nq=10000, k=100, blobs=100_000, sigma=20.0, ntrain=100_000, cache=False,
+                     index="reference"),
     # BASELINE.json configs[3]'s tree (SIFT1B: P=4, k1=32, k2=16, w=8, L=32, 496 pairs -> 2-byte pair
     # ids, H = 2^26) at one GPU's share of 1B over 8 GPUs (125M), and a 10M variant for quick runs
     "sift1b_shard": dict(config=dict(dim=128, p_tree=4, k1=32, k2=16, w=8, p_line=32, candidate_budget=4096,
@@ -84,6 +87,130 @@ def log(*a):
 def workload_files(name: str, seed: int):
     CACHE.mkdir(parents=True, exist_ok=True)
     return CACHE / f"{name}_s{seed}.pqt", CACHE / f"{name}_s{seed}_queries.npy"
+
+
+def _gen_device():
+    import torch
+
+    return torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+
+
+def synth_stream(n: int, dim: int, blobs: int, sigma: float, seed: int, device, chunk: int = 1 << 22):
+    """The synthetic base set as a chunk stream (the reference's synth_clustered distribution,
+    bench.cpp:66-95: uniform [0,255) blob means, isotropic sigma noise), pure torch so the
+    reference arm never imports the product package. The same call yields the same rows."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    means = torch.rand((blobs, dim), generator=g, device=device) * 255.0
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        pick = torch.randint(0, blobs, (e - s,), generator=g, device=device)
+        yield s, means[pick] + sigma * torch.randn((e - s, dim), generator=g, device=device)
+
+
+def synth_query_pool(batches: int, nq: int, dim: int, blobs: int, sigma: float, seed: int, device):
+    """Query batches from the base stream's blobs; batch b is an independent sample stream
+    (seed + 1000 + b), so a longer pool keeps the same first batches."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    means = torch.rand((blobs, dim), generator=g, device=device) * 255.0
+    out = []
+    for b in range(batches):
+        gq = torch.Generator(device=device)
+        gq.manual_seed(seed + 1000 + b)
+        pick = torch.randint(0, blobs, (nq,), generator=gq, device=device)
+        out.append((means[pick] + sigma * torch.randn((nq, dim), generator=gq, device=device)).cpu().numpy())
+    return np.concatenate(out)
+
+
+def ref_index_files(name: str, seed: int):
+    CACHE.mkdir(parents=True, exist_ok=True)
+    stem = CACHE / f"{name}_s{seed}_ref"
+    return (stem.with_suffix(".pqt"), Path(f"{stem}_queries.npy"), Path(f"{stem}.json"),
+            Path(f"{stem}_results.npz"))
+
+
+def build_reference_index(name: str, seed: int, batches: int, threads: int):
+    """The reference builds the workload's index on the CPU: pqtref IndexBuilder(train,
+    keep_raw=false), add() per chunk of the synthetic stream, finalize() (search.cpp:52-117),
+    save_index (index_io.cpp:94-146). Runs in a process that never loads libpqtg.so. Returns
+    the in-memory pqtref index (the caller may time it) -- the file is the shared artifact."""
+    import torch
+
+    from oracle.bindings import Ref
+    from paper_1702_05911_b200.index import PqtConfig  # a plain dataclass (no native code)
+
+    wl = WORKLOADS[name]
+    ipath, qpath, mpath, rpath = ref_index_files(name, seed)
+    for p in (ipath, qpath, mpath, rpath):
+        p.unlink(missing_ok=True)
+    cfg = PqtConfig(train_iters=15, seed=seed, **wl["config"])
+    dev = _gen_device()
+    t0 = time.time()
+    stream = synth_stream(wl["n"], cfg.dim, wl["blobs"], wl["sigma"], seed, dev)
+    first = next(stream)
+    train = first[1][: wl["ntrain"]].cpu().numpy()  # the first ntrain base rows (bench.cpp's train split)
+
+    def chunks():
+        yield first[1].cpu().numpy()
+        for _, x in stream:
+            yield x.cpu().numpy()
+            done = _ + x.shape[0]
+            if done % (1 << 25) == 0:
+                log(f"[bench] reference build: {done / 1e6:.0f}M of {wl['n'] / 1e6:.0f}M vectors "
+                    f"({time.time() - t0:.0f}s)")
+
+    ref = Ref.build_streamed(train, chunks(), cfg, threads=threads)
+    t_build = time.time() - t0
+    tmp = ipath.with_suffix(".tmp")
+    ref.save(str(tmp))
+    os.replace(tmp, ipath)
+    np.save(qpath, synth_query_pool(batches, wl["nq"], cfg.dim, wl["blobs"], wl["sigma"], seed, dev))
+    mpath.write_text(json.dumps({"workload": name, "seed": seed, "n": wl["n"], "config": wl["config"],
+                                 "generator_device": dev.type, "builder": "pqtref IndexBuilder (keep_raw=false)",
+                                 "threads": threads, "build_s": t_build, "total_s": time.time() - t0}))
+    log(f"[bench] reference-built {name} index ({wl['n']} vectors) in {t_build:.0f}s, "
+        f"saved {ipath} ({ipath.stat().st_size / 1e9:.2f} GB) in {time.time() - t0 - t_build:.0f}s")
+    del torch
+    return ref
+
+
+def reference_index(name: str, seed: int, batches: int):
+    """Path, query pool and build record of the reference-built index, building it in a separate
+    process (the reference arm's own code path) if this box has none yet."""
+    wl = WORKLOADS[name]
+    ipath, qpath, mpath, _ = ref_index_files(name, seed)
+    if not (ipath.exists() and qpath.exists() and mpath.exists()):
+        import subprocess
+
+        log(f"[bench] no reference-built {name} index on this box: building it (reference code, CPU)")
+        subprocess.run([sys.executable, str(REPO / "bench.py"), "--impl", "reference", "--build-index-only",
+                        "--workload", name, "--seed", str(seed), "--batches", str(batches)], check=True)
+    else:
+        log(f"[bench] using the reference-built {ipath}")
+    meta = json.loads(mpath.read_text())
+    Q = np.load(qpath)
+    if Q.shape[0] < wl["nq"] * batches:  # more batches than the build saved: same generator, longer pool
+        import torch
+
+        gen = torch.device("cuda", 0) if meta["generator_device"] == "cuda" else torch.device("cpu")
+        Q2 = synth_query_pool(batches, wl["nq"], wl["config"]["dim"], wl["blobs"], wl["sigma"], seed, gen)
+        assert np.array_equal(Q2[: Q.shape[0]], Q), "query pool is not reproducible"
+        Q = Q2
+    return ipath, Q[: wl["nq"] * batches], meta
+
+
+class IndexMeta:
+    """What the byte model / launch count need from an index loaded by path."""
+
+    def __init__(self, dev):
+        self.config = dev.config
+        self.n = dev.n
+        self.pair_width = 1 if dev.config.pair_count <= 256 else 2
 
 
 def make_workload(name: str, seed: int, device: int, batches: int, shards: int | None = None):
@@ -300,28 +427,44 @@ def counters_ids(dev, dq, nq, k, step, d_ids, d_counts):
     return d_ids.cpu().numpy().view(np.uint32), d_counts.cpu().numpy().view(np.uint32)
 
 
-def measure_recall(name: str, seed: int, device: int, Q: np.ndarray, nq_pool: int, result):
-    """recall@R = fraction of queries whose exact nearest neighbour is within the first R
-    results (recall_fraction, bench.cpp:23-44); exact neighbours by the GPU brute force
-    (brute.cu, the reference's brute_force_knn) over the regenerated (deterministic) base set.
-    Identical for the CPU reference, whose ids are bit-identical."""
+def base_rows(name: str, seed: int, meta: dict | None, device):
+    """The workload's base rows again, chunk by chunk, on `device`: the reference-built
+    workloads' synth_stream (on the generator device their build used), else the GPU
+    builder's synth_clustered draw (make_workload)."""
     import torch
 
+    wl = WORKLOADS[name]
+    if meta is not None:
+        gen = torch.device(meta["generator_device"], 0) if meta["generator_device"] == "cuda" else torch.device("cpu")
+        for s, x in synth_stream(wl["n"], wl["config"]["dim"], wl["blobs"], wl["sigma"], seed, gen):
+            yield s, x.to(device)
+        return
     from paper_1702_05911_b200 import builder
+
+    X = builder.synth_clustered(wl["n"] + _GPU_POOL[0], wl["config"]["dim"], wl["blobs"], wl["sigma"], seed,
+                                device=device)[: wl["n"]]
+    yield 0, X
+
+
+_GPU_POOL = [0]  # query-pool size of the GPU-built draw (its queries are the draw's tail)
+
+
+def measure_recall(name: str, seed: int, device: int, Q: np.ndarray, meta, result):
+    """recall@R = fraction of queries whose exact nearest neighbour is within the first R
+    results (recall_fraction, bench.cpp:23-44); exact neighbours over the regenerated
+    (deterministic) base set. Identical for the CPU reference, whose ids are bit-identical."""
+    import torch
 
     wl = WORKLOADS[name]
     ids, counts = result
     dev = torch.device("cuda", device)
-    # regenerate exactly the build's draw (same generator sequence), keep the base rows
-    X = builder.synth_clustered(wl["n"] + nq_pool, wl["config"]["dim"], wl["blobs"], wl["sigma"], seed,
-                                device=dev)[: wl["n"]]
     q = torch.from_numpy(Q).to(dev)
-    if X.shape[0] <= 20_000_000:
+    if wl["n"] <= 20_000_000:
         # the exact nearest neighbour as the reference defines it (brute_force_knn, sequential fp32
         # l2_sq, (dist, id) order: search.cpp:276-299), on the GPU (pqtg_brute_force_knn_device)
         from paper_1702_05911_b200._abi import check, lib
 
-        X = X.contiguous()
+        X = torch.cat([x for _, x in base_rows(name, seed, meta, dev)]).contiguous()
         gt_i = torch.empty(q.shape[0], dtype=torch.int32, device=dev)
         gt_d = torch.empty(q.shape[0], dtype=torch.float32, device=dev)
         gt_c = torch.empty(q.shape[0], dtype=torch.int32, device=dev)
@@ -329,19 +472,23 @@ def measure_recall(name: str, seed: int, device: int, Q: np.ndarray, nq_pool: in
                                                 gt_i.data_ptr(), gt_d.data_ptr(), gt_c.data_ptr(),
                                                 torch.cuda.current_stream(dev).cuda_stream))
         truth = gt_i.cpu().numpy().view(np.uint32).astype(np.int64)
-    else:  # 100M+ rows: the torch matmul form (exact up to fp32 rounding of the expansion)
+        del X
+    else:  # 100M+ rows, streamed: the torch matmul form (exact up to fp32 rounding of the expansion)
+        old = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
         best_d = torch.full((q.shape[0],), float("inf"), device=dev)
         best_i = torch.zeros(q.shape[0], dtype=torch.int64, device=dev)
         qq = (q * q).sum(1, keepdim=True)
-        for s in range(0, X.shape[0], 1 << 18):
-            xb = X[s:s + (1 << 18)]
-            d = qq - 2.0 * (q @ xb.T) + (xb * xb).sum(1)[None, :]
-            v, i = d.min(1)
-            better = v < best_d
-            best_d = torch.where(better, v, best_d)
-            best_i = torch.where(better, i + s, best_i)
+        for s0, X in base_rows(name, seed, meta, dev):
+            for s in range(0, X.shape[0], 1 << 18):
+                xb = X[s:s + (1 << 18)]
+                d = qq - 2.0 * (q @ xb.T) + (xb * xb).sum(1)[None, :]
+                v, i = d.min(1)
+                better = v < best_d
+                best_d = torch.where(better, v, best_d)
+                best_i = torch.where(better, i + s0 + s, best_i)
+        torch.backends.cuda.matmul.allow_tf32 = old
         truth = best_i.cpu().numpy()
-    del X
     out = {}
     for R in (1, 10, 100):
         hit = [truth[i] in ids[i, : min(R, counts[i])] for i in range(len(truth))]
@@ -350,18 +497,50 @@ def measure_recall(name: str, seed: int, device: int, Q: np.ndarray, nq_pool: in
 
 
 # --------------------------------------------------------------------------- CPU legs
-def cpu_leg(hix, Q, k, min_seconds=10.0, max_reps=20, db=None):
-    """Time the reference (oracle/_ref) — else the C restatement — on this host's cores
-    (with the raw vectors attached when db is given: the exact re-rank stage)."""
+def same_results(a, b) -> bool:
+    """Bit-exact comparison of (ids, dists, counts, stats) batches: counts and stats equal, and
+    each query's first counts[q] ids and fp32 distance bit patterns equal."""
+    g_ids, g_d, g_c, g_s = a
+    r_ids, r_d, r_c, r_s = b
+    g_c = np.asarray(g_c).view(np.uint32)
+    if not (np.array_equal(g_c, np.asarray(r_c).astype(np.uint32))
+            and np.array_equal(np.asarray(g_s).astype(np.uint64), np.asarray(r_s).astype(np.uint64))):
+        return False
+    for q in range(len(g_c)):
+        c = g_c[q]
+        if not (np.array_equal(np.asarray(g_ids)[q, :c].view(np.uint32), np.asarray(r_ids)[q, :c].view(np.uint32))
+                and np.array_equal(np.asarray(g_d)[q, :c].view(np.uint32), np.asarray(r_d)[q, :c].view(np.uint32))):
+            return False
+    return True
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def load_reference(hix, path):
+    """The checker's copy of the index: the reference reads its own file (pqtref load_index,
+    index_io.cpp:148-229) when there is one, else it is built from the host arrays."""
     from oracle.bindings import Oracle, Ref
 
+    if Ref.available():
+        return (Ref.load(str(path)) if path is not None else Ref.from_host(hix)), "reference"
+    return Oracle(str(path) if path is not None else hix), "port"
+
+
+def cpu_leg(impl, kind, Q, k, min_seconds=10.0, max_reps=20, db=None):
+    """Time the reference (oracle/_ref) -- else the C restatement -- on this host's cores
+    (with the raw vectors attached when db is given: the exact re-rank stage): all host
+    threads, then one thread on a small sample."""
     if _ALL_CPUS:  # undo the GPU-side NUMA pinning: the reference gets every host core
         os.sched_setaffinity(0, _ALL_CPUS)
     threads = os.cpu_count() or 1
-    if Ref.available():
-        impl, kind = Ref.from_host(hix), "reference"
-    else:
-        impl, kind = Oracle(hix), "port"
     if db is not None:
         impl.attach_database(db)
     impl.knn(Q[: min(len(Q), 16)], k, threads=threads)  # warm-up (page-in)
@@ -372,54 +551,93 @@ def cpu_leg(hix, Q, k, min_seconds=10.0, max_reps=20, db=None):
         t_total += time.perf_counter() - t0
         out = out or res
         reps += 1
+    n1 = min(len(Q), 256)
+    t0 = time.perf_counter()
+    impl.knn(Q[:n1], k, threads=1)
+    one = n1 / (time.perf_counter() - t0)
     return {"value": reps * len(Q) / t_total, "unit": "queries/s", "cores": threads, "kind": kind,
-            "sample": f"{reps} x {len(Q)} queries of the timed batch (k={k}), all host threads"}, out
+            "sample": f"{reps} x {len(Q)} queries of the timed batch (k={k}), all host threads",
+            "threads1_value": one, "threads1_sample": f"{n1} queries, 1 thread", "cpu_model": cpu_model()}, out
 
 
 # --------------------------------------------------------------------------- reference arm
+def index_kind(wl, args) -> str:
+    if "shards" in wl:
+        return "gpu-built position shard (exact assign_bin/encode_line kernels, torch k-means)"
+    if args.index == "reference":
+        return "reference-built (pqtref IndexBuilder waves, keep_raw=false; PQTINDEX file)"
+    return "gpu-built (exact assign_bin/encode_line kernels, torch k-means)"
+
+
+def config_of(name: str, wl, args, world: int) -> dict:
+    """The config object both arms print (identical keys and values)."""
+    return {"workload": name, **wl["config"], "n": wl["n"], "queries_per_step": wl["nq"], "k": wl["k"],
+            "index": index_kind(wl, args), "exact_rerank": bool(args.exact),
+            "l2": "flushed between timed steps (256 MiB write)" if not args.no_flush else "not flushed",
+            "parallelism": (f"position shards x{world} (NCCL broadcast + all-gather + merge)"
+                            if args.shard else f"replicas x{world}")}
+
+
 def run_reference(args):
+    """The reference's own CPU path (oracle/_ref: the unmodified sources compiled in place) on
+    this host's cores: pqtref knn_query_batch over a bounded sample of the workload's batch.
+    This process never loads libpqtg.so: the index is built by pqtref itself (or read with
+    pqtref load_index from the file an earlier reference run wrote)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import torch
-
     wl = WORKLOADS[args.workload]
     if "shards" in wl:
-        print(json.dumps({"impl": "reference", "unavailable": f"{args.workload} is one shard of a "
-                          "larger-than-HBM index; the reference's CPU path has no shard build"}), flush=True)
+        print(json.dumps({"impl": "reference", "unavailable": f"{args.workload} is a {wl['n']:,}-vector index sharded "
+                          "over GPUs; the reference's CPU build of it takes hours and its CPU path has no shard "
+                          "view"}), flush=True)
         return
-    hix, Qpool = make_workload(args.workload, args.seed, 0, args.batches)
-    from oracle.bindings import Oracle, Ref
+    from oracle.bindings import Ref
 
     threads = os.cpu_count() or 1
-    impl, kind = (Ref.from_host(hix), "reference") if Ref.available() else (Oracle(hix), "port")
-    nq = wl["nq"]
-    Q = Qpool[:nq]
-    # bound each step to a few seconds of host work
+    if args.build_index_only:
+        build_reference_index(args.workload, args.seed, args.batches, threads)
+        return
+    ipath, qpath, mpath, rpath = ref_index_files(args.workload, args.seed)
+    if ipath.exists() and qpath.exists() and mpath.exists():
+        t0 = time.time()
+        ref = Ref.load(str(ipath))
+        log(f"[bench] pqtref load_index {ipath} in {time.time() - t0:.0f}s")
+    else:
+        ref = build_reference_index(args.workload, args.seed, args.batches, threads)
+    nq, k = wl["nq"], wl["k"]
+    Q = np.load(qpath)[:nq]
+    # the reference's answers for the whole first batch: the GPU arm's parity cross-check
     t0 = time.perf_counter()
-    impl.knn(Q[:64], wl["k"], threads=threads)
-    per_q = (time.perf_counter() - t0) / 64
+    ids, dists, counts, stats = ref.knn(Q, k, threads=threads)
+    per_q = (time.perf_counter() - t0) / nq
+    np.savez(rpath, ids=ids, dists=dists, counts=counts, stats=stats)
+    # bound each step to ~3 s of host work
     sample = int(max(16, min(nq, 3.0 / max(per_q, 1e-9))))
     Qs = Q[:sample]
     for _ in range(args.warmup):
-        impl.knn(Qs, wl["k"], threads=threads)
+        ref.knn(Qs, k, threads=threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        impl.knn(Qs, wl["k"], threads=threads)
+        ref.knn(Qs, k, threads=threads)
     dt = time.perf_counter() - t0
     v = args.steps * sample / dt
     line = {
-        "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (clustered blobs)",
-        "impl": "reference",
-        "config": {"workload": args.workload, **wl["config"], "n": wl["n"], "queries_per_step": sample, "k": wl["k"]},
-        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": threads, "kind": kind,
-                         "sample": f"{sample} queries per step of the {args.workload} batch"},
+        "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": DATA, "impl": "reference",
+        "config": config_of(args.workload, wl, args, world),
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": threads, "kind": "reference",
+                         "sample": f"{sample} of the {nq} queries of the {args.workload} batch per step, "
+                                   f"pqtref knn_query_batch, {threads} threads", "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-    del torch
+
+
+DATA = "synthetic clustered blobs (synth_clustered distribution)"
 
 
 # --------------------------------------------------------------------------- our arm
@@ -429,7 +647,12 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gist1m", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: deep100m (BASELINE configs[2]) at N=1; sift1b --shard (configs[3]) under torchrun")
+    ap.add_argument("--index", default="reference", choices=["reference", "gpu"],
+                    help="who builds an unsharded workload's index: the reference on the CPU (pqtref "
+                         "IndexBuilder, cached PQTINDEX file, default) or the GPU builder (quick runs)")
+    ap.add_argument("--build-index-only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--batches", type=int, default=4, help="distinct query batches cycled over steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -447,6 +670,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.workload is None:  # the north-star split under torchrun, the single-GPU config otherwise
+        multi = int(os.environ.get("WORLD_SIZE", "1")) > 1
+        args.workload = "sift1b" if multi else "deep100m"
+        args.shard = args.shard or multi
 
     if args.impl == "reference":
         run_reference(args)
@@ -473,33 +700,45 @@ def main():
     if args.shard and "shards" in wl and world == 1:
         raise SystemExit(f"--shard on {args.workload} splits the index over the ranks: run it under torchrun with "
                          f">= 2 ranks (without --shard one process serves shard 0 of {wl['shards']})")
+    ref_built = "shards" not in wl and args.index == "reference"
+    ipath = meta = None
+    pool = args.batches * max(world, 1)
     if "shards" in wl:  # every rank builds its shard at once (codebooks trained on rank 0)
-        hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * max(world, 1), shards)
+        hix, Qpool = make_workload(args.workload, args.seed, local, pool, shards)
     elif rank == 0:
-        hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * max(world, 1), shards)
+        if ref_built:
+            ipath, Qpool, meta = reference_index(args.workload, args.seed, pool)
+        else:
+            hix, Qpool = make_workload(args.workload, args.seed, local, pool, shards)
     if world > 1 and "shards" not in wl:
         dist.barrier()
         if rank != 0:
-            hix, Qpool = make_workload(args.workload, args.seed, local, args.batches * world, shards)
+            if ref_built:
+                ipath, Qpool, meta = reference_index(args.workload, args.seed, pool)
+            else:
+                hix, Qpool = make_workload(args.workload, args.seed, local, pool, shards)
+    _GPU_POOL[0] = len(Qpool)
     lib().pqtg_set_kernel_variant(args.variant)
+    t_load = time.time()
     if args.shard:
         from paper_1702_05911_b200.sharded import ShardedIndex
 
-        sh = ShardedIndex(hix, device=local, max_batch=nq)
+        sh = ShardedIndex(str(ipath) if ref_built else hix, device=local, max_batch=nq)
         dev = sh.local
         # every rank searches the same batches (rank 0's, broadcast inside the timed step)
         batches = [Qpool[b * nq:(b + 1) * nq] for b in range(args.batches)]
     else:
-        dev = DeviceIndex(hix, device=local, max_batch=nq)
+        dev = DeviceIndex(str(ipath) if ref_built else hix, device=local, max_batch=nq)
         batches = [Qpool[(rank * args.batches + b) * nq:(rank * args.batches + b + 1) * nq]
                    for b in range(args.batches)]
+    if ref_built:
+        log(f"[bench] pqtg_index_load of the reference-built file: {time.time() - t_load:.1f}s")
+        hix = IndexMeta(dev)
     dev.set_chunks(args.chunks)
     db_rows = None
-    if args.exact:  # the build's base rows, regenerated deterministically (make_workload's draw)
-        from paper_1702_05911_b200 import builder
-
-        db_rows = builder.synth_clustered(wl["n"] + len(Qpool), wl["config"]["dim"], wl["blobs"], wl["sigma"],
-                                          args.seed, device=torch.device("cuda", local))[: wl["n"]].cpu().numpy()
+    if args.exact:  # the build's base rows, regenerated deterministically
+        db_rows = torch.cat([x.cpu() for _, x in base_rows(args.workload, args.seed, meta,
+                                                              torch.device("cuda", local))]).numpy()
         dev.attach_database(db_rows)
     d_q = [torch.from_numpy(b).cuda() for b in batches]
     d_ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
@@ -658,29 +897,30 @@ def main():
         g_d = d_dists.cpu().numpy()
         g_c = d_counts.cpu().numpy().view(np.uint32)
         g_s = d_stats.cpu().numpy().astype(np.uint64)
-        cpu, (r_ids, r_d, r_c, r_s) = cpu_leg(hix, batches[0], k, db=db_rows)
-        same = np.array_equal(g_c, r_c) and np.array_equal(g_s, r_s)
-        for q in range(nq):
-            c = g_c[q]
-            same = same and np.array_equal(g_ids[q, :c], r_ids[q, :c]) and \
-                np.array_equal(g_d[q, :c].view(np.uint32), r_d[q, :c].view(np.uint32))
-        parity = {"queries": nq, "bit_exact_vs": cpu["kind"], "ok": bool(same)}
+        t0 = time.time()
+        impl, kind = load_reference(None if ref_built else hix, ipath if ref_built else None)
+        log(f"[bench] reference index for the CPU leg ready in {time.time() - t0:.0f}s ({kind})")
+        cpu, ref_out = cpu_leg(impl, kind, batches[0], k, db=db_rows)
+        del impl
+        parity = {"queries": nq, "bit_exact_vs": kind, "ok": same_results((g_ids, g_d, g_c, g_s), ref_out)}
+        if ref_built and rank == 0:  # the reference arm's own answers for this batch, if it ran on this box
+            rpath = ref_index_files(args.workload, args.seed)[3]
+            if rpath.exists() and not args.exact:
+                r = np.load(rpath)
+                parity["reference_arm_results"] = same_results((g_ids, g_d, g_c, g_s),
+                                                               (r["ids"], r["dists"], r["counts"], r["stats"]))
 
     recall = None
     if not args.no_recall and not sharded_wl:
-        recall = measure_recall(args.workload, args.seed, local, batches[0], nq * args.batches * max(world, 1),
+        recall = measure_recall(args.workload, args.seed, local, batches[0], meta,
                                 counters_ids(dev, d_q[0], nq, k, step, d_ids, d_counts))
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic clustered blobs (synth_clustered distribution), GPU-built PQT index",
-        "config": {"workload": args.workload, **wl["config"], "n": wl["n"], "queries_per_step": nq, "k": k,
-                   "exact_rerank": bool(args.exact),
-                   "l2": "flushed between timed steps (256 MiB write)" if not args.no_flush else "not flushed",
-                   "parallelism": (f"position shards x{world} (NCCL broadcast + all-gather + merge)"
-                                   if args.shard else f"replicas x{world}")},
+        "data": DATA,
+        "config": config_of(args.workload, wl, args, world),
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "link_gbs": link, "host_cpus": affinity,
                 "transfer_bound_qps": nq / (h2d / (link["h2d"] * 1e9) + d2h / (link["d2h"] * 1e9))},

@@ -3,11 +3,14 @@
 //
 // Same types, same signatures, same exceptions. Differences a caller can observe:
 //  * queries run on a CUDA device (device 0 unless PQTG_DEVICE is set); the first query on
-//    an index uploads it and caches the device copy in PqtIndex::gpu;
+//    an index uploads it and caches the device copy in PqtIndex::gpu, keyed by the config and
+//    the arrays' addresses/sizes (a changed config or re-assigned arrays re-upload; in-place
+//    element edits need index.gpu.reset());
 //  * exact re-ranking against attached raw vectors runs on the GPU (the database is copied to
 //    the device on the first query after attach_database); without one the calls warn once and
 //    disable it, exactly as the reference does (search.cpp:25-32);
-//  * QueryStats *_us are the batch's per-stage device times divided evenly over its queries.
+//  * QueryStats *_us are the batch call's wall time divided evenly over its queries, split over
+//    the stages in proportion to their device times.
 #pragma once
 
 #include <cstdint>

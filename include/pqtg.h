@@ -180,6 +180,11 @@ int pqtg_workspace_set_chunks(pqtg_workspace* ws, uint32_t chunks);
  * selection + gather, [2] re-rank + top-k, [3] whole search — of the call's first chunk (see
  * pqtg_workspace_set_chunks). Synchronises the last stream. */
 int pqtg_workspace_stage_ms(pqtg_workspace* ws, float* ms4);
+/* Synchronise the workspace's streams and report what the kernels of its last search call
+ * flagged: PQTG_ERR_UNSUPPORTED when a query's exact-order tuple heap outgrew shared memory
+ * (that query's candidate list is truncated). pqtg_search checks this itself; a caller of the
+ * asynchronous pqtg_search_device checks it here (pqtg_workspace_stage_ms reports it too). */
+int pqtg_workspace_status(pqtg_workspace* ws);
 /* Copy per-query intermediates of the LAST sub-batch searched with `ws` to host buffers
  * (any pointer may be NULL). Used by the per-stage parity tests.
  *   fine         nq × p_line × k1              traversal fine_dists (pqtree.cpp:84-97)

@@ -192,6 +192,9 @@ class Ref(_Lib):
         "ref_last_error": (C.c_char_p, []),
         "ref_synth_clustered": (C.c_int, [_u64, _u32, _u32, C.c_float, _u64, _vp]),
         "ref_build_index": (_vp, [_vp, _u64, _vp, _u64, C.POINTER(PqtgConfig), C.c_int, C.c_int]),
+        "ref_builder_new": (_vp, [_vp, _u64, _vp, C.c_int]),
+        "ref_builder_add": (C.c_int, [_vp, _vp, _u64, _u32]),
+        "ref_builder_finalize": (_vp, [_vp]),
         "ref_load_index": (_vp, [C.c_char_p]),
         "ref_save_index": (C.c_int, [_vp, C.c_char_p]),
         "ref_free": (None, [_vp]),
@@ -242,6 +245,26 @@ class Ref(_Lib):
         h = cls.so().ref_build_index(_p(train), train.shape[0], _p(db), db.shape[0], C.byref(c),
                                      threads, 1 if keep_raw else 0)
         return cls(h)
+
+    @classmethod
+    def build_streamed(cls, train: np.ndarray, chunks, cfg: PqtConfig, threads: int = 0) -> "Ref":
+        """pqt::IndexBuilder(train, cfg, threads, keep_raw=false), add(chunk) for every chunk of
+        the iterable, finalize() (search.cpp:52-117): the reference's wave build."""
+        train = np.ascontiguousarray(train, np.float32)
+        c = cfg.to_c()
+        so = cls.so()
+        b = so.ref_builder_new(_p(train), train.shape[0], C.byref(c), threads)
+        if not b:
+            raise RuntimeError("reference: " + so.ref_last_error().decode())
+        try:
+            for x in chunks:
+                x = np.ascontiguousarray(x, np.float32)
+                if so.ref_builder_add(b, _p(x), x.shape[0], cfg.dim) != 0:
+                    raise RuntimeError("reference: " + so.ref_last_error().decode())
+        except BaseException:
+            so.ref_builder_finalize(b)  # frees the builder
+            raise
+        return cls(so.ref_builder_finalize(b))
 
     @classmethod
     def load(cls, path: str) -> "Ref":

@@ -124,6 +124,44 @@ void* ref_build_index(const float* train, uint64_t ntrain, const float* db, uint
     }
 }
 
+// pqt::IndexBuilder streamed in waves (search.cpp:52-117): new(train) → add(chunk)* →
+// finalize. This is how the reference builds an index larger than one in-memory set
+// (DEEP100M / SIFT1B-shaped), keep_raw = false.
+void* ref_builder_new(const float* train, uint64_t ntrain, const pqtg_config* cfg, int threads) {
+    try {
+        pqt::PqtConfig c = to_cfg(cfg);
+        pqt::VectorSet tr = make_set(train, ntrain, c.dim);
+        return new pqt::IndexBuilder(tr, c, threads, false);
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+int ref_builder_add(void* builder, const float* rows, uint64_t n, uint32_t dim) {
+    try {
+        static_cast<pqt::IndexBuilder*>(builder)->add(make_set(rows, n, dim));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// finalize() consumes the builder (freed here) and returns an index handle
+void* ref_builder_finalize(void* builder) {
+    auto* b = static_cast<pqt::IndexBuilder*>(builder);
+    try {
+        auto* h = new Handle;
+        h->index = b->finalize();
+        delete b;
+        return h;
+    } catch (const std::exception& e) {
+        delete b;
+        fail(e);
+        return nullptr;
+    }
+}
+
 // pqt::load_index (index_io.cpp:148)
 void* ref_load_index(const char* path) {
     try {

@@ -43,6 +43,14 @@ Workspace::~Workspace() {
     for (void* p : allocations) cudaFree(p);
 }
 
+// throws the error the kernels flagged in the workspace's error word (the stream is synchronised)
+void check_ws_error(const Workspace& ws) {
+    uint32_t e = 0;
+    PQTG_CUDA_CHECK(cudaMemcpy(&e, ws.err, sizeof(e), cudaMemcpyDeviceToHost));
+    if (e & PQTG_WS_ERR_HEAP)
+        throw Error{PQTG_ERR_UNSUPPORTED, "exact bin order: the tuple heap outgrew shared memory"};
+}
+
 WsSlice Workspace::slice(uint64_t q0) const {
     const DevParams& p = index->prm;
     WsSlice s;
@@ -54,6 +62,7 @@ WsSlice Workspace::slice(uint64_t q0) const {
     s.nranges = nranges + q0;
     s.ncand = ncand + q0;
     s.ntuples = ntuples + q0;
+    s.err = err;
     s.hash = hash ? hash + q0 * hash_stride : nullptr;
     s.scr = scr ? scr + q0 * p.P * p.scr_nj : nullptr;
     return s;
@@ -342,7 +351,7 @@ int pqtg_index_attach_database(pqtg_index* index, const float* rows, uint64_t n,
         // search.cpp:44-49: the vector set must match the index
         if (n != d.n || dim != d.prm.D)
             throw Error{PQTG_ERR_BAD_DIM, "attach_database: vector set does not match index"};
-        if (d.prm.shard_hi > d.prm.shard_lo && (d.prm.shard_lo != 0 || d.prm.shard_hi != d.n))
+        if (d.prm.shard_lo != 0 || d.prm.shard_hi != d.n)
             unsupported("exact re-ranking on a sharded index");
         float* buf = nullptr;
         const uint32_t stride = (dim + 3) / 4 * 4;  // 16-byte rows for the exact stage's bulk copies
@@ -394,6 +403,8 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         ws->nranges = dev_alloc<uint32_t>(ws->allocations, B);
         ws->ncand = dev_alloc<uint32_t>(ws->allocations, B);
         ws->ntuples = dev_alloc<uint32_t>(ws->allocations, B);
+        ws->err = dev_alloc<uint32_t>(ws->allocations, 1);
+        PQTG_CUDA_CHECK(cudaMemset(ws->err, 0, sizeof(uint32_t)));
         ws->hash_words = binsel_fast_ok(p) ? binsel_hash_words(p, B) : 0;
         ws->hash_stride = ws->hash_words ? std::max(binsel_hash_stride(p), binsel_par_hash_stride(p)) : 0;
         ws->hash_words = ws->hash_stride * B;
@@ -426,6 +437,20 @@ int pqtg_workspace_stage_ms(pqtg_workspace* h, float* ms4) {
         PQTG_CUDA_CHECK(cudaEventSynchronize(ws.ev[3]));
         for (int i = 0; i < 3; ++i) PQTG_CUDA_CHECK(cudaEventElapsedTime(&ms4[i], ws.ev[i], ws.ev[i + 1]));
         PQTG_CUDA_CHECK(cudaEventElapsedTime(&ms4[3], ws.ev[0], ws.ev[3]));
+        check_ws_error(ws);
+        return PQTG_OK;
+    });
+}
+
+int pqtg_workspace_status(pqtg_workspace* h) {
+    return guarded([&] {
+        if (!h) throw Error{PQTG_ERR_ARG, "null argument"};
+        Workspace& ws = *h->ws;
+        std::lock_guard<std::mutex> lock(ws.mu);
+        PQTG_CUDA_CHECK(cudaSetDevice(ws.index->device));
+        if (ws.last_stream) PQTG_CUDA_CHECK(cudaStreamSynchronize(ws.last_stream));
+        PQTG_CUDA_CHECK(cudaStreamSynchronize(ws.aux_stream));
+        check_ws_error(ws);
         return PQTG_OK;
     });
 }
@@ -483,6 +508,7 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         // the workspace's aux stream may still run a previous call's chunks on these slices
         PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
         PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));
+        if (index->dev->prm.exact_order) PQTG_CUDA_CHECK(cudaMemsetAsync(ws.err, 0, sizeof(uint32_t), s));
         ws.last_stream = s;
         ws.last_nq = nq;
         // device-resident batches: two chunks on two streams, so the next chunk's traversal and bin
@@ -534,6 +560,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         cudaStream_t st[2] = {ws.own_stream, ws.aux_stream};
         ws.last_stream = ws.own_stream;
         auto enqueue = [&] {
+            if (d.prm.exact_order) PQTG_CUDA_CHECK(cudaMemsetAsync(ws.err, 0, sizeof(uint32_t), st[0]));
             // Sub-batches of <= max_batch queries; each is cut into chunks that alternate between
             // two streams, so chunk c's kernels overlap chunk c+1's H2D and chunk c-1's D2H.
             for (uint64_t q0 = 0; q0 < nq || (nq == 0 && q0 == 0); q0 += ws.max_batch) {
@@ -583,15 +610,10 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
             }
             return a.type == cudaMemoryTypeHost;
         };
-        // exact bin order: a query whose heap outgrew shared memory reports ntuples = ~0
-        // (kernels.cu exact_fill); checked on the last sub-batch
+        // exact bin order: a query whose heap outgrew shared memory sets the workspace's error
+        // word (kernels.cu binsel_kernel<EXACT>), whichever sub-batch it was in
         auto check_exact = [&] {
-            if (!d.prm.exact_order || ws.last_nq == 0) return;
-            std::vector<uint32_t> nt(ws.last_nq);
-            PQTG_CUDA_CHECK(cudaMemcpy(nt.data(), ws.ntuples, nt.size() * 4, cudaMemcpyDeviceToHost));
-            for (uint32_t v : nt)
-                if (v == 0xFFFFFFFFu)
-                    throw Error{PQTG_ERR_UNSUPPORTED, "exact bin order: the tuple heap outgrew shared memory"};
+            if (d.prm.exact_order) check_ws_error(ws);
         };
         if (no_graph || nq == 0 || !pinned(queries) || !pinned(ids) || !pinned(dists) || !pinned(counts) ||
             !pinned(stats)) {

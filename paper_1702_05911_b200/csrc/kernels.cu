@@ -334,7 +334,8 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                                                           uint32_t* __restrict__ ncand,
                                                           uint32_t* __restrict__ ntuples,
                                                           pqtg_query_stats* __restrict__ stats,
-                                                          uint32_t ts_log2, uint32_t heap_cap) {
+                                                          uint32_t ts_log2, uint32_t heap_cap,
+                                                          uint32_t* __restrict__ err) {
     using Sort = cub::BlockRadixSort<uint32_t, kThreads, ITEMS, uint32_t>;
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t PW_ = p.P * p.W;
@@ -560,7 +561,10 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         // tuples the reference's gather loop consumes: up to the one that filled the budget,
         // or the whole stream (search.cpp:166-217)
         ntuples[q] = C >= budget && budget > 0 ? s_maxord + 1 : (uint32_t)min(base, total);
-        if (EXACT && s_overflow) ntuples[q] = 0xFFFFFFFFu;  // the heap overflowed: reported by the host API
+        if (EXACT && s_overflow) {  // the heap overflowed: reported by the host API
+            ntuples[q] = 0xFFFFFFFFu;
+            atomicOr(err, PQTG_WS_ERR_HEAP);
+        }
         if (stats) {
             stats[q].bins_visited = R;
             stats[q].candidates = C;
@@ -614,16 +618,16 @@ void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_quer
         const size_t smx = fixed + (size_t)cap * 16;
         if (p.resort)
             binsel_kernel<16, true, true><<<(unsigned)nq, kThreads, smx, s>>>(
-                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap);
+                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap, ws.err);
         else
             binsel_kernel<4, false, true><<<(unsigned)nq, kThreads, smx, s>>>(
-                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap);
+                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap, ws.err);
     } else if (p.resort) {
         binsel_kernel<16, true, false><<<(unsigned)nq, kThreads, sm, s>>>(
-            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0);
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0, ws.err);
     } else {
         binsel_kernel<4, false, false><<<(unsigned)nq, kThreads, sm, s>>>(
-            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0);
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0, ws.err);
     }
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
@@ -751,7 +755,8 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     if (tid == 0) s_count = 0;
     __syncthreads();
 
-    const bool sharded = p.shard_hi > p.shard_lo;
+    // every index is a position range: [0, n) unsharded, possibly empty on a shard
+    constexpr bool sharded = true;
     uint32_t mine = 0;
     for (uint32_t j = tid; j < C; j += blockDim.x) {
         // range containing candidate j: last r with coff[r] <= j

@@ -244,6 +244,7 @@ struct DeviceCopy {
     pqtg_index* ix = nullptr;
     pqtg_workspace* ws = nullptr;
     const VectorSet* db = nullptr;  // raw vectors currently on the device (exact re-rank)
+    std::uint64_t fingerprint = 0;  // of the host index the copy was made from
     ~DeviceCopy() {
         pqtg_workspace_destroy(ws);
         pqtg_index_destroy(ix);
@@ -252,9 +253,52 @@ struct DeviceCopy {
 
 std::mutex g_upload_mu;
 
+// FNV-1a over the config and every array's (address, size) -- O(P·k1) per call:
+// the reference reads index.config and the arrays on every call (search.cpp:126-260), so a
+// changed config (budget, w, rerank_exact, ...), a copy with other arrays, or re-assigned lists
+// or codes rebuild the device copy instead of silently serving the old one. (In-place edits of
+// array elements behind unchanged vectors need index.gpu.reset().)
+struct Fnv {
+    std::uint64_t h = 1469598103934665603ull;
+    void bytes(const void* p, std::size_t n) {
+        const auto* b = static_cast<const unsigned char*>(p);
+        for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    }
+    template <class T>
+    void pod(const T& v) { bytes(&v, sizeof(T)); }
+    template <class T>
+    void where(const std::vector<T>& v) { pod(reinterpret_cast<std::uintptr_t>(v.data())); pod(v.size()); }
+};
+
+std::uint64_t fingerprint(const PqtIndex& index) {
+    Fnv f;
+    const PqtConfig& c = index.config;
+    f.pod(c.dim); f.pod(c.p_tree); f.pod(c.k1); f.pod(c.k2); f.pod(c.w); f.pod(c.p_line);
+    f.pod(c.hash_size); f.pod(c.candidate_budget); f.pod(c.rerank_exact); f.pod(c.resort_bins);
+    f.pod(c.train_iters); f.pod(c.seed);
+    for (const auto& b : index.tree.level1) f.where(b.centroids);
+    for (const auto& kids : index.tree.level2)
+        for (const auto& b : kids) f.where(b.centroids);
+    f.where(index.pair_table.d2);
+    for (const auto& t : index.tables) {
+        f.pod(t.slope);
+        f.where(t.entries);
+    }
+    f.where(index.lists.offsets);
+    f.where(index.lists.ids);
+    f.where(index.codes.lambda_q);
+    f.where(index.codes.pair_id);
+    return f.h;
+}
+
 DeviceCopy& device_copy(const PqtIndex& index) {
     std::lock_guard<std::mutex> lock(g_upload_mu);
-    if (index.gpu) return *static_cast<DeviceCopy*>(index.gpu.get());
+    const std::uint64_t fp = fingerprint(index);
+    if (index.gpu) {
+        auto* d = static_cast<DeviceCopy*>(index.gpu.get());
+        if (d->fingerprint == fp) return *d;
+        index.gpu.reset();  // stale: the index changed since its upload
+    }
     const PqtConfig& c = index.config;
     std::vector<float> l1, l2;
     for (const auto& b : index.tree.level1) l1.insert(l1.end(), b.centroids.begin(), b.centroids.end());
@@ -289,6 +333,7 @@ DeviceCopy& device_copy(const PqtIndex& index) {
     auto copy = std::make_shared<DeviceCopy>();
     check(pqtg_index_create(&v, device, &copy->ix));
     check(pqtg_workspace_create(copy->ix, 4096, &copy->ws));
+    copy->fingerprint = fp;
     index.gpu = copy;
     return *copy;
 }
@@ -323,11 +368,16 @@ std::vector<QueryResult> knn_query_batch(const PqtIndex& index, const VectorSet&
     std::vector<std::uint32_t> ids(nq * k), counts(nq);
     std::vector<float> dists(nq * k);
     std::vector<pqtg_query_stats> stats(nq);
+    const auto t0 = std::chrono::steady_clock::now();
     check(pqtg_search(d.ix, d.ws, queries.data.data(), nq, queries.dim, k, ids.data(), dists.data(), counts.data(),
                       stats.data()));
+    const double wall_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    // the reference times each query's stages (search.cpp:134-137,167-216,220,258); a batch on the
+    // GPU has one wall time: each query gets 1/nq of it, split by the stages' device-time shares
     float ms[4] = {0, 0, 0, 0};
-    pqtg_workspace_stage_ms(d.ws, ms);  // last sub-batch; a per-query share of device time
-    const double per = 1000.0 / static_cast<double>(std::min<std::size_t>(nq, 16384));
+    pqtg_workspace_stage_ms(d.ws, ms);
+    const double dev_ms = (double)ms[0] + ms[1] + ms[2];
+    const double per = wall_us / static_cast<double>(nq) / (dev_ms > 0 ? dev_ms : 1.0);
     for (std::size_t q = 0; q < nq; ++q) {
         QueryResult& r = results[q];
         r.ids.assign(ids.begin() + q * k, ids.begin() + q * k + counts[q]);

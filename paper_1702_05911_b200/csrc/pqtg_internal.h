@@ -111,7 +111,12 @@ struct WsSlice {
     uint32_t* ntuples = nullptr;
     uint32_t* hash = nullptr;     // [q][hash_stride] visited-slot table (binsel_fast.cu)
     float* scr = nullptr;         // [q][P][scr_nj] tensor-core dot products (screen.cu)
+    uint32_t* err = nullptr;      // the workspace's device error word (PQTG_WS_ERR_*), shared by all slices
 };
+
+// device error word bits (Workspace::err): set by kernels, cleared at the start of every search
+// call, reported by pqtg_search / pqtg_workspace_status / pqtg_workspace_stage_ms
+constexpr uint32_t PQTG_WS_ERR_HEAP = 1u;  // exact bin order: a query's tuple heap outgrew shared memory
 
 struct Workspace {
     const DevIndex* index = nullptr;
@@ -129,6 +134,7 @@ struct Workspace {
     uint32_t* nranges = nullptr;  // [B]
     uint32_t* ncand = nullptr;    // [B]
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
+    uint32_t* err = nullptr;      // [1] device error word (PQTG_WS_ERR_*)
     float* scr = nullptr;         // [B][P][scr_nj] (y - mu_p) . c'' on the tensor cores (screen.cu)
     uint32_t* hash = nullptr;     // [B << ts_log2] visited slots, cleared on use (binsel_fast.cu)
     uint64_t hash_words = 0;

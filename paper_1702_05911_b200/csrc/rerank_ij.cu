@@ -180,7 +180,9 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
         }
     }
     const uint2 rg0 = tid < R ? __ldg(qr + tid) : make_uint2(0, 0);
-    const bool sharded = p.shard_hi > p.shard_lo;
+    // every index is a position range [shard_lo, shard_hi): [0, n) unsharded, possibly empty
+    // on a shard (then every candidate is skipped and the query returns count 0)
+    constexpr bool sharded = true;
     const bool cached = R <= kRangeCache;
     // a position shard with cached ranges re-ranks only its own candidates: the ranges are
     // clipped to [shard_lo, shard_hi) and renumbered densely (thread r = range r), so the loop,

@@ -214,6 +214,23 @@ class HostIndex:
                 rec[:, 1:3] = self.pair_id.reshape(-1).astype("<u2").view(np.uint8).reshape(-1, 2)
             fp.write(rec.tobytes())
 
+    @staticmethod
+    def read_header(path: str) -> tuple["PqtConfig", int]:
+        """(config, n) from a PQTINDEX v1 file's fixed 73-byte header (index_io.cpp:94-106)."""
+        with open(path, "rb") as fp:
+            buf = fp.read(73)
+        if len(buf) < 73 or buf[:8] != MAGIC:
+            raise FormatError(f"{path}: bad index magic")
+        (version,) = struct.unpack("<I", buf[8:12])
+        if version != VERSION:
+            raise FormatError(f"{path}: unsupported index version {version}, expected {VERSION}")
+        f = struct.unpack("<IIIIIIQIIBIQ", buf[12:65])
+        cfg = PqtConfig(dim=f[0], p_tree=f[1], k1=f[2], k2=f[3], w=f[4], p_line=f[5], hash_size=f[6],
+                        candidate_budget=f[7], rerank_exact=f[8], resort_bins=bool(f[9]),
+                        train_iters=f[10], seed=f[11])
+        (n,) = struct.unpack("<Q", buf[65:73])
+        return cfg, n
+
     @classmethod
     def load(cls, path: str) -> "HostIndex":
         with open(path, "rb") as fp:

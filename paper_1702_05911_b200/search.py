@@ -166,6 +166,13 @@ class DeviceIndex:
         """Overlap stages across `chunks` pieces of each batch on two streams (0 = auto, 1 = off)."""
         check(lib().pqtg_workspace_set_chunks(self._ws, int(chunks)))
 
+    def status(self) -> None:
+        """Raise what the last search_device call's kernels flagged (pqtg_workspace_status)."""
+        try:
+            check(lib().pqtg_workspace_status(self._ws))
+        except PqtgError as e:
+            _raise(e)
+
     def stage_ms(self) -> list[float]:
         ms = (C.c_float * 4)()
         check(lib().pqtg_workspace_stage_ms(self._ws, ms))

@@ -30,6 +30,16 @@ class ShardedIndex:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = torch.cuda.current_device() if device is None else device
+        if isinstance(hix, str):  # a PQTINDEX file: this rank loads only its position range
+            cfg, n = HostIndex.read_header(hix)
+            lo, hi = shard_range(n, self.world, self.rank)
+            self.local = DeviceIndex(hix, device=self.device, shard=(lo, hi) if self.world > 1 else (0, 0),
+                                     max_batch=max_batch)
+            self.shard = (lo, hi)
+            self.n = n
+            self.dim = cfg.dim
+            self._bufs = {}
+            return
         if hasattr(hix, "shard_lo"):  # builder.ShardIndex: this rank's shard, built in place
             lo, hi = shard_range(hix.n, self.world, self.rank)
             if (lo, hi) != (hix.shard_lo, hix.shard_hi):
