@@ -560,6 +560,68 @@ def cpu_leg(impl, kind, Q, k, min_seconds=10.0, max_reps=20, db=None):
             "threads1_value": one, "threads1_sample": f"{n1} queries, 1 thread", "cpu_model": cpu_model()}, out
 
 
+def topk_merge_np(parts, k):
+    """Merge per-shard (ids, dists, counts) lists by (dist, id) (candidate_less,
+    search.cpp:39-41), in numpy: the checker's own merge."""
+    nq = parts[0][0].shape[0]
+    ids = np.zeros((nq, k), np.uint32)
+    dists = np.zeros((nq, k), np.float32)
+    counts = np.zeros(nq, np.uint32)
+    for q in range(nq):
+        i = np.concatenate([p[0][q, : p[2][q]] for p in parts]).astype(np.uint32)
+        d = np.concatenate([p[1][q, : p[2][q]] for p in parts]).astype(np.float32)
+        o = np.lexsort((i, d))[:k]
+        counts[q] = len(o)
+        ids[q, : len(o)], dists[q, : len(o)] = i[o], d[o]
+    return ids, dists, counts
+
+
+def shard_parity(args, six, Q, step, d_ids, d_dists, d_counts, d_stats, world, rank):
+    """Parity of a billion-scale position shard against the C restatement (oracle/, test
+    infrastructure) holding the same shard (pqto_from_shard_view: whole-index offsets, the
+    shard's ids and codes): bins_visited / candidates are global, the ids and distances this
+    rank's local top-k -- or, under --shard, every rank's oracle shard merged by (dist, id) on
+    rank 0 against the NCCL-merged GPU answer. Bounded to the first 1000 queries of the batch."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle.bindings import Oracle
+
+    k = WORKLOADS[args.workload]["k"]
+    nchk = min(len(Q), 1000)
+    step(0)
+    torch.cuda.synchronize()
+    g = (d_ids.cpu().numpy().view(np.uint32)[:nchk], d_dists.cpu().numpy()[:nchk],
+         d_counts.cpu().numpy().view(np.uint32)[:nchk], d_stats.cpu().numpy().astype(np.uint64)[:nchk])
+    if _ALL_CPUS:
+        os.sched_setaffinity(0, _ALL_CPUS)
+    threads = max(1, (os.cpu_count() or 1) // max(world, 1))
+    t0 = time.time()
+    orc = Oracle(six)
+    t_load = time.time() - t0
+    t0 = time.perf_counter()
+    r = orc.knn(Q[:nchk], k, threads=threads)
+    dt = time.perf_counter() - t0
+    del orc
+    merged = args.shard and world > 1
+    if merged:
+        box = [None] * world
+        dist.all_gather_object(box, r[:3])
+        want_ids, want_d, want_c = topk_merge_np(box, k)
+        want = (want_ids, want_d, want_c, r[3])
+    else:
+        want = r
+    ok = same_results(g, want)
+    cpu = {"value": nchk / dt, "unit": "queries/s", "cores": threads, "kind": "port",
+           "sample": f"{nchk} queries of the batch on this rank's position shard "
+                     f"[{six.shard_lo}, {six.shard_hi}) of {six.n:,} (the C restatement, oracle/pqt_oracle.c)",
+           "oracle_setup_s": t_load}
+    parity = {"queries": nchk, "bit_exact_vs": "port (C restatement, shard view)", "ok": bool(ok),
+              "what": "merged top-k of all shards (NCCL) vs the oracle shards merged by (dist, id)" if merged
+              else f"shard [{six.shard_lo}, {six.shard_hi}) local top-k + global bins_visited/candidates"}
+    return cpu, parity
+
+
 # --------------------------------------------------------------------------- reference arm
 def index_kind(wl, args) -> str:
     if "shards" in wl:
@@ -852,6 +914,11 @@ def main():
 
     e2e_value, h2d, d2h, link = run_e2e()
 
+    shard_cpu = shard_par = None
+    if "shards" in wl and not args.no_cpu_baseline:  # every rank checks its own shard
+        shard_cpu, shard_par = shard_parity(args, hix, batches[0], step, d_ids, d_dists, d_counts, d_stats, world,
+                                            rank)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -887,9 +954,7 @@ def main():
     parity = None
     sharded_wl = "shards" in wl
     if sharded_wl:
-        cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "port",
-               "sample": "none: the CPU restatement needs the whole index; shard parity is "
-                         "tests/test_gpu_topk.py::test_gpu_sharded_build_equals_full_build"}
+        cpu, parity = shard_cpu, shard_par
     if world == 1 and not args.no_cpu_baseline and not sharded_wl:
         step(0)
         torch.cuda.synchronize()

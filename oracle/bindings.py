@@ -78,11 +78,18 @@ class Oracle(_Lib):
         "pqto_candidates": (C.c_int64, [_vp, _vp, _vp, _u64, C.POINTER(_u64)]),
         "pqto_knn_batch": (C.c_int, [_vp, _vp, _u64, _u32, _u32, C.c_int, _u64, _u64, _vp, _vp, _vp, _vp]),
         "pqto_attach_database": (None, [_vp, _vp]),
+        "pqto_from_shard_view": (_vp, [_vp, _vp, _vp]),
     }
 
     def __init__(self, index: HostIndex | str):
         so = self.so()
-        if isinstance(index, (str, os.PathLike)):
+        if hasattr(index, "shard_lo"):  # builder.ShardIndex: one position shard, codes by position
+            v = index.view()
+            lam = np.ascontiguousarray(index.lambda_q, np.uint8)
+            pid = np.ascontiguousarray(index.pair_id).view(np.uint16)
+            self._keep = (index, lam, pid)  # borrowed by the oracle
+            h = so.pqto_from_shard_view(C.byref(v), _p(lam), _p(pid))
+        elif isinstance(index, (str, os.PathLike)):
             h = so.pqto_load(str(index).encode())
         else:
             v = index.view()

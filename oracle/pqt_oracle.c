@@ -44,6 +44,10 @@ struct pqto_index {
     uint16_t* pairs;        /* npairs × 2: PairDistanceTable::pairs (linequant.cpp:76-82) */
     uint32_t npairs;
     const float* db;        /* borrowed raw vectors n × dim (PqtIndex::database), or NULL */
+    /* a position shard (pqto_from_shard_view): ids and codes hold only positions
+     * [shard_lo, shard_hi), codes in POSITION order; offsets/ids/codes are borrowed */
+    int is_shard;
+    uint64_t shard_lo, shard_hi;
 };
 
 /* ---------------------------------------------------------------- small containers */
@@ -183,7 +187,7 @@ static int derive(pqto_index* ix) {
 void pqto_free(pqto_index* ix) {
     if (!ix) return;
     free(ix->level1); free(ix->level2); free(ix->d2); free(ix->slopes); free(ix->entries);
-    free(ix->offsets); free(ix->ids); free(ix->lambda_q); free(ix->pair_id);
+    if (!ix->is_shard) { free(ix->offsets); free(ix->ids); free(ix->lambda_q); free(ix->pair_id); }
     free(ix->fine); free(ix->pairs);
     free(ix);
 }
@@ -216,6 +220,43 @@ pqto_index* pqto_from_view(const pqtg_index_view* v) {
     ix->pair_id = (uint16_t*)dup_bytes(v->pair_id, (size_t)v->n * c->p_line * sizeof(uint16_t));
     if (!ix->level1 || !ix->level2 || !ix->d2 || !ix->slopes || !ix->entries || !ix->offsets ||
         !ix->ids || !ix->lambda_q || !ix->pair_id || derive(ix) != 0) {
+        set_err("out of memory");
+        pqto_free(ix);
+        return NULL;
+    }
+    return ix;
+}
+
+/* One position shard [v->shard_lo, v->shard_hi) of an n-vector index, as a sharded GPU
+ * deployment holds it (pqtg_index_create_shard): v->offsets covers the whole index, v->ids the
+ * shard's positions, and lambda_q / pair_id the shard's rows in position order. The big arrays
+ * are borrowed (they must outlive the oracle). knn on it re-ranks only the shard's candidates
+ * (search.cpp:221-227 restricted to the range) into that shard's local top-k. */
+pqto_index* pqto_from_shard_view(const pqtg_index_view* v, const uint8_t* lambda_q, const uint16_t* pair_id) {
+    if (!v || !lambda_q || !pair_id) { set_err("null view"); return NULL; }
+    if (validate_cfg(&v->config) != 0) return NULL;
+    if (v->shard_lo > v->shard_hi || v->shard_hi > v->n) { set_err("bad shard range"); return NULL; }
+    pqto_index* ix = (pqto_index*)calloc(1, sizeof *ix);
+    if (!ix) { set_err("out of memory"); return NULL; }
+    const pqtg_config* c = &v->config;
+    ix->cfg = *c;
+    ix->n = v->n;
+    ix->is_shard = 1;
+    ix->shard_lo = v->shard_lo;
+    ix->shard_hi = v->shard_hi;
+    uint32_t m = c->dim / c->p_tree;
+    ix->level1 = (float*)dup_bytes(v->level1, (size_t)c->p_tree * c->k1 * m * sizeof(float));
+    ix->level2 = (float*)dup_bytes(v->level2, (size_t)c->p_tree * c->k1 * c->k2 * m * sizeof(float));
+    ix->d2 = (float*)dup_bytes(v->d2, (size_t)c->p_line * c->k1 * c->k1 * sizeof(float));
+    ix->table_count = v->table_count;
+    ix->table_len = v->table_len;
+    ix->slopes = (double*)dup_bytes(v->table_slopes, (size_t)v->table_count * sizeof(double));
+    ix->entries = (uint32_t*)dup_bytes(v->table_entries, (size_t)v->table_count * v->table_len * 2 * sizeof(uint32_t));
+    ix->offsets = (uint64_t*)v->offsets;
+    ix->ids = (uint32_t*)v->ids;
+    ix->lambda_q = (uint8_t*)lambda_q;
+    ix->pair_id = (uint16_t*)pair_id;
+    if (!ix->level1 || !ix->level2 || !ix->d2 || !ix->slopes || !ix->entries || derive(ix) != 0) {
         set_err("out of memory");
         pqto_free(ix);
         return NULL;
@@ -806,18 +847,30 @@ static int knn_one(const pqto_index* ix, const float* y, uint32_t k, uint64_t lo
         return (int)C;
     }
     uint64_t nr = 0;
+    if (ix->is_shard) {  /* a shard holds (and re-ranks) only its own positions */
+        lo = ix->shard_lo;
+        hi = ix->shard_hi;
+    }
     for (int64_t i = 0; i < C; ++i) {  /* search.cpp:221-227 */
         uint64_t p = pos[i];
-        if (hi > lo && (p < lo || p >= hi)) continue;
-        uint32_t id = ix->ids[p];
+        if ((hi > lo || ix->is_shard) && (p < lo || p >= hi)) continue;
+        uint32_t id;
+        size_t row;
+        if (ix->is_shard) {  /* codes by position */
+            id = ix->ids[p - lo];
+            row = (size_t)(p - lo);
+        } else {
+            id = ix->ids[p];
+            row = id;
+        }
         ranked[nr].id = id;
-        ranked[nr].dist = pqto_line_distance(ix, ix->lambda_q + (size_t)id * c->p_line,
-                                             ix->pair_id + (size_t)id * c->p_line, fine);
+        ranked[nr].dist = pqto_line_distance(ix, ix->lambda_q + row * c->p_line,
+                                             ix->pair_id + row * c->p_line, fine);
         ++nr;
     }
     /* rerank = min(max(rerank_exact, k), C) with raw vectors attached (search.cpp:229-238) */
     uint64_t rerank = 0;
-    if (c->rerank_exact > 0 && ix->db && !(hi > lo)) {
+    if (c->rerank_exact > 0 && ix->db && !(hi > lo) && !ix->is_shard) {
         uint64_t r = c->rerank_exact > k ? c->rerank_exact : k;
         rerank = r < nr ? r : nr;
     }

@@ -26,6 +26,9 @@ const char* pqto_last_error(void);
 
 /* Deep copy of a view (src/index_io.cpp:186-190: fine slices derived from level1). */
 pqto_index* pqto_from_view(const pqtg_index_view* view);
+/* A position shard [v->shard_lo, v->shard_hi) of an n-vector index: whole-index offsets, the
+ * shard's ids, its line codes in position order (borrowed, not copied). */
+pqto_index* pqto_from_shard_view(const pqtg_index_view* v, const uint8_t* lambda_q, const uint16_t* pair_id);
 /* PQTINDEX v1 reader (src/index_io.cpp:148-229). NULL + pqto_last_error() on failure. */
 pqto_index* pqto_load(const char* path);
 /* PQTINDEX v1 writer (src/index_io.cpp:94-146). 0 on success. */
