@@ -63,6 +63,7 @@ WsSlice Workspace::slice(uint64_t q0) const {
     s.ncand = ncand + q0;
     s.ntuples = ntuples + q0;
     s.err = err;
+    s.keys = keys ? keys + q0 * std::max<uint64_t>(p.budget, 1) : nullptr;
     s.hash = hash ? hash + q0 * hash_stride : nullptr;
     s.scr = scr ? scr + q0 * p.P * p.scr_nj : nullptr;
     return s;
@@ -146,6 +147,15 @@ uint32_t exact_prefix(const DevParams& p, uint32_t k) {
 }
 
 // Buffers of the line-ranked prefix for the exact stage (only with raw vectors attached).
+// the re-rank's key buffer in HBM when a query's keys do not fit shared memory (large budgets)
+void ensure_keys(Workspace& ws, uint32_t k) {
+    const DevParams& p = ws.index->prm;
+    const uint32_t kk = (p.db && p.rerank_exact > 0 && k) ? exact_prefix(p, k) : k;
+    if (ws.keys || kk == 0 || !rerank_needs_gkeys(p, kk)) return;
+    ws.keys = dev_alloc<uint64_t>(ws.allocations, ws.max_batch * std::max<uint64_t>(p.budget, 1));
+    ++ws.gen;
+}
+
 void ensure_exact(Workspace& ws, uint32_t k) {
     const DevParams& p = ws.index->prm;
     if (!p.db || p.rerank_exact == 0 || k == 0) return;
@@ -504,6 +514,7 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         std::lock_guard<std::mutex> lock(ws.mu);  // the workspace's host state (buffers, chunking)
         PQTG_CUDA_CHECK(cudaSetDevice(index->dev->device));
         ensure_exact(ws, k);
+        ensure_keys(ws, k);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         // the workspace's aux stream may still run a previous call's chunks on these slices
         PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
@@ -556,6 +567,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         PQTG_CUDA_CHECK(cudaSetDevice(d.device));
         ensure_staging(ws, std::max<uint32_t>(k, 1));
         ensure_exact(ws, k);
+        ensure_keys(ws, k);
         const uint64_t D = d.prm.D;
         cudaStream_t st[2] = {ws.own_stream, ws.aux_stream};
         ws.last_stream = ws.own_stream;

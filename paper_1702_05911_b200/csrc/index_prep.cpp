@@ -211,7 +211,7 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     if (c.resort_bins && std::min<uint64_t>(c.candidate_budget, n) > 4096)
         unsupported("resort_bins with candidate budget > 4096");
     const uint64_t budget = std::min<uint64_t>(c.candidate_budget, n);
-    if (budget > 16384) unsupported("candidate budget > 16384");
+    if (budget > 65535) unsupported("candidate budget > 65535");
     if (shard_hi == 0 && shard_lo == 0) shard_hi = n;
     if (shard_lo > shard_hi || shard_hi > n) throw Error{PQTG_ERR_ARG, "bad shard range"};
 

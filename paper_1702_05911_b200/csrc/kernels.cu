@@ -602,6 +602,9 @@ void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_quer
     }
     const uint32_t lg = ts_log2_for(p);
     const size_t sm = binsel_smem(p);
+    if (sm + 2048 > (size_t)optin_bytes())
+        throw Error{PQTG_ERR_UNSUPPORTED, "bin selection's visited set does not fit shared memory at this budget "
+                                          "(resort_bins, exact bin order or the generic kernel)"};
     if (p.exact_order) {
         // the exact order's heap takes the rest of the opt-in shared memory (<= 64 Ki entries)
         const uint32_t ch = (p.resort ? 16u : 4u) * kThreads;
@@ -728,11 +731,13 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
                                                           const uint32_t* __restrict__ ncand,
                                                           uint32_t* __restrict__ out_ids,
                                                           float* __restrict__ out_dists,
-                                                          uint32_t* __restrict__ out_counts) {
+                                                          uint32_t* __restrict__ out_counts,
+                                                          uint64_t* __restrict__ gkeys) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t L = p.L, k1 = p.k1, npairs = p.npairs, budget = p.budget;
-    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);          // budget
-    uint64_t* sel = keys + budget;                                // sel_cap
+    // keys: shared memory, or this query's row of the workspace buffer for large budgets
+    uint64_t* keys = gkeys ? gkeys + blockIdx.x * (uint64_t)budget : reinterpret_cast<uint64_t*>(smem);
+    uint64_t* sel = gkeys ? reinterpret_cast<uint64_t*>(smem) : keys + budget;  // sel_cap
     float* fine = reinterpret_cast<float*>(sel + sel_cap);        // L*k1
     float* c2 = fine + L * k1;                                    // L*npairs
     uint32_t* pairs = reinterpret_cast<uint32_t*>(c2 + L * (p.code_ij ? 256u : npairs));  // npairs
@@ -810,9 +815,25 @@ void set_rerank_attr() {
 }
 }  // namespace
 
-size_t rerank_smem(const DevParams& p, uint32_t k) {
-    return 8ull * p.budget + 8ull * sel_cap_for(p, k) + 4ull * p.L * p.k1 +
+size_t rerank_smem(const DevParams& p, uint32_t k, bool gkeys) {
+    return (gkeys ? 0ull : 8ull * p.budget) + 8ull * sel_cap_for(p, k) + 4ull * p.L * p.k1 +
            4ull * p.L * (p.code_ij ? 256u : p.npairs) + 4ull * p.npairs + 4ull * p.budget;
+}
+
+int optin_bytes() {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return optin;
+}
+
+namespace {
+bool generic_gkeys(const DevParams& p, uint32_t k) { return rerank_smem(p, k) + 2048 > (size_t)optin_bytes(); }
+}  // namespace
+
+bool rerank_needs_gkeys(const DevParams& p, uint32_t k) {
+    if (kernel_variant() != 1 && rerank_ij_ok(p, k)) return rerank_ij_gkeys(p, k);
+    return generic_gkeys(p, k);
 }
 
 void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids,
@@ -821,11 +842,16 @@ void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& w
         launch_rerank_ij(p, nq, k, ws, ids, dists, counts, s);
         return;
     }
-    const size_t sm = rerank_smem(p, k);
+    const bool gk = generic_gkeys(p, k);
+    if (gk && !ws.keys) throw Error{PQTG_ERR_ARG, "workspace has no candidate-key buffer for this budget"};
+    const size_t sm = rerank_smem(p, k, gk);
+    if (sm + 2048 > (size_t)optin_bytes())
+        throw Error{PQTG_ERR_UNSUPPORTED, "re-rank tables and selection do not fit shared memory at this budget"};
     const uint32_t cap = sel_cap_for(p, k);
+    uint64_t* gkeys = gk ? ws.keys : nullptr;
 #define PQTG_RERANK(LT, PW)                                                                          \
     rerank_kernel<LT, PW><<<(unsigned)nq, kThreads, sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \
-                                                             ws.ncand, ids, dists, counts)
+                                                             ws.ncand, ids, dists, counts, gkeys)
     if (p.pw == 1) {
         switch (p.L) {
         case 16: PQTG_RERANK(16, 1); break;

@@ -112,6 +112,7 @@ struct WsSlice {
     uint32_t* hash = nullptr;     // [q][hash_stride] visited-slot table (binsel_fast.cu)
     float* scr = nullptr;         // [q][P][scr_nj] tensor-core dot products (screen.cu)
     uint32_t* err = nullptr;      // the workspace's device error word (PQTG_WS_ERR_*), shared by all slices
+    uint64_t* keys = nullptr;     // [q][budget] candidate keys when they do not fit shared memory, or null
 };
 
 // device error word bits (Workspace::err): set by kernels, cleared at the start of every search
@@ -135,6 +136,7 @@ struct Workspace {
     uint32_t* ncand = nullptr;    // [B]
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
     uint32_t* err = nullptr;      // [1] device error word (PQTG_WS_ERR_*)
+    uint64_t* keys = nullptr;     // [B][budget] re-rank keys for budgets too large for shared memory
     float* scr = nullptr;         // [B][P][scr_nj] (y - mu_p) . c'' on the tensor cores (screen.cu)
     uint32_t* hash = nullptr;     // [B << ts_log2] visited slots, cleared on use (binsel_fast.cu)
     uint64_t hash_words = 0;
@@ -243,7 +245,7 @@ void validate_config(const pqtg_config& c);
 // ---------------------------------------------------------------- kernels (kernels.cu)
 size_t traverse_smem(const DevParams& p);
 size_t binsel_smem(const DevParams& p);
-size_t rerank_smem(const DevParams& p, uint32_t k);
+size_t rerank_smem(const DevParams& p, uint32_t k, bool gkeys = false);
 void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                      cudaStream_t s);
 void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats,
@@ -256,6 +258,9 @@ void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids,
 void configure_kernels(const DevParams& p, uint32_t k);
 // rerank_ij.cu (1-byte (i, j) pair codes, k1 <= 16, p_line in {16, 32, 64})
 bool rerank_ij_ok(const DevParams& p, uint32_t k);
+bool rerank_ij_gkeys(const DevParams& p, uint32_t k);  // its keys go to the workspace (large budgets)
+bool rerank_needs_gkeys(const DevParams& p, uint32_t k);  // launch_rerank will use ws.keys
+int optin_bytes();  // the device's opt-in shared memory per block
 void configure_rerank_ij();
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids,
                       float* dists, uint32_t* counts, cudaStream_t s);

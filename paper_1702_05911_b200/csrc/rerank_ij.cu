@@ -20,6 +20,8 @@
 // per-pair table) and c2 = d2[f][pair] (read through L1), the same three roundings, and leaves
 // the shared memory small enough for two CTAs per SM.
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "pqtg_internal.h"
@@ -60,7 +62,7 @@ __host__ __device__ inline uint32_t ij_sel_cap(uint32_t kk) {
 __host__ __device__ constexpr uint32_t t_entries(int K1M) { return K1M == 16 ? 256u : 512u; }
 
 __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint32_t sel_cap, int K1M = 16,
-                                              bool direct = false) {
+                                              bool direct = false, bool gkeys = false) {
     IjLayout l{};
     size_t o = 0;
     l.t = o;  // T (DIRECT: the pairs' j, u16), fine, delta and rid sit at compile-time offsets
@@ -78,7 +80,7 @@ __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint3
     l.sel = o + ((size_t)4 << kSelBits);
     o += rid_bytes > sel_bytes ? rid_bytes : sel_bytes;
     l.keys = o;
-    o += al16((size_t)budget * 8);
+    if (!gkeys) o += al16((size_t)budget * 8);  // gkeys: the candidate keys live in the workspace (HBM/L2)
     l.total = o;
     return l;
 }
@@ -125,21 +127,26 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 
 }  // namespace
 
-template <int LT, int K1M, bool DIRECT>
+template <int LT, int K1M, bool DIRECT, bool PK = false>
 __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DIRECT)) ? 1 : 2)
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
-                     float* __restrict__ out_dists, uint32_t* __restrict__ out_counts) {
+                     float* __restrict__ out_dists, uint32_t* __restrict__ out_counts, uint64_t* __restrict__ gkeys) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k1 = p.k1, budget = p.budget;
     constexpr uint32_t TE = t_entries(K1M);
-    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT);
+    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr);
     const IjLayout fix = ij_layout(LT, 0, 0, K1M, DIRECT);
     float2* T = reinterpret_cast<float2*>(smem);
+    // PK (packed, K1M = 16): the same bytes as two float tables Et[f][t] and Ct[f][t]
+    float* Et = reinterpret_cast<float*>(smem);
+    float* Ct = reinterpret_cast<float*>(smem) + LT * TE;
     uint16_t* jt = reinterpret_cast<uint16_t*>(smem);  // DIRECT: j of pair id
     float* fine = reinterpret_cast<float*>(smem + fix.fine);
-    uint64_t* keys = reinterpret_cast<uint64_t*>(smem + lay.keys);
+    // candidate keys: shared memory, or this query's row of the workspace's key buffer when the
+    // budget is too large for shared memory (budget > ~8k)
+    uint64_t* keys = gkeys ? gkeys + blockIdx.x * (uint64_t)budget : reinterpret_cast<uint64_t*>(smem + lay.keys);
     uint64_t* sel = reinterpret_cast<uint64_t*>(smem + lay.sel);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + fix.rid);  // aliases rid
     uint16_t* rid = reinterpret_cast<uint16_t*>(smem + fix.rid);
@@ -251,7 +258,13 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
             const uint32_t f = f0 + u * kFLanes;
             if (f < LT) {
                 const float b2 = fine[f * K1M + pi_i], a2 = fine[f * K1M + pi_j];
-                T[f * TE + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
+                const float e = __fsub_rn(__fsub_rn(a2, b2), c2v[u]);
+                if constexpr (PK) {
+                    Et[f * TE + ij] = e;
+                    Ct[f * TE + ij] = c2v[u];
+                } else {
+                    T[f * TE + ij] = make_float2(e, c2v[u]);
+                }
             }
         }
     }
@@ -322,10 +335,71 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
         }
         keys[j] = key;
     };
+    // PK: two candidates per thread scored together in packed fp32 pairs (sm_100 FADD2/FMUL2,
+    // __fadd2_rn/__fmul2_rn: each lane rounds like __fadd_rn/__fmul_rn, so linequant.cpp:171-181's
+    // order holds for each candidate; no FFMA/FFMA2 may appear in this kernel's SASS). λ = fl(q · fl(1/255)) with q = (2^23 + q) − 2^23 built from
+    // the code byte by one byte permute (exact for q <= 255) instead of an I2F.
+    auto score2 = [&](uint32_t ja, const uint4* va, uint32_t ida, uint32_t jb, const uint4* vb, uint32_t idb) {
+        const uint32_t* wa = reinterpret_cast<const uint32_t*>(va);
+        const uint32_t* wb = reinterpret_cast<const uint32_t*>(vb);
+        float2 tot = make_float2(0.0f, 0.0f);
+        const float2 magic = make_float2(-8388608.0f, -8388608.0f);
+        const float2 inv2 = make_float2(inv255, inv255);
+#pragma unroll
+        for (int f = 0; f < LT; ++f) {
+            constexpr uint32_t kSel[2] = {0x7540u, 0x7542u};  // byte 0 / 2 -> low byte of 0x4B0000xx
+            const uint32_t xa = wa[f >> 1], xb = wb[f >> 1];
+            const uint32_t ta = (xa >> ((f & 1) * 16 + 8)) & 0xFFu, tb = (xb >> ((f & 1) * 16 + 8)) & 0xFFu;
+            const float2 b2 = make_float2(fine[f * K1M + (ta >> 4)], fine[f * K1M + (tb >> 4)]);
+            const float2 e = make_float2(Et[f * TE + ta], Et[f * TE + tb]);
+            const float2 c2 = make_float2(Ct[f * TE + ta], Ct[f * TE + tb]);
+            const float2 q = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(xa, 0x4B000000u, kSel[f & 1])),
+                                                    __uint_as_float(__byte_perm(xb, 0x4B000000u, kSel[f & 1]))),
+                                        magic);
+            const float2 lam = __fmul2_rn(q, inv2);
+            const float2 l2c = __fmul2_rn(__fmul2_rn(lam, lam), c2);
+            const float2 le = __fmul2_rn(lam, e);
+            // the two adds that take a product stay scalar: ptxas (12.9) contracts FMUL2 -> FADD2
+            // into FFMA2 even for explicit .rn and -fmad=false, which would change the rounding
+            const float2 part = make_float2(__fadd_rn(__fadd_rn(b2.x, l2c.x), le.x),
+                                            __fadd_rn(__fadd_rn(b2.y, l2c.y), le.y));
+            tot = __fadd2_rn(tot, part);
+        }
+        uint64_t key = kSentinel;
+        if (ida != kInvalid) {
+            const uint32_t od = orderable(tot.x);
+            key = ((uint64_t)od << 32) | ida;
+            kand &= od;
+            kor |= od;
+            ++mine;
+        }
+        keys[ja] = key;
+        if (jb < Cn) {
+            key = kSentinel;
+            if (idb != kInvalid) {
+                const uint32_t od = orderable(tot.y);
+                key = ((uint64_t)od << 32) | idb;
+                kand &= od;
+                kor |= od;
+                ++mine;
+            }
+            keys[jb] = key;
+        }
+    };
     // two row buffers in turn: the next candidate's row is in flight while this one is scored,
     // with no register copies between iterations
     const uint32_t step = blockDim.x;
-    if constexpr (DIRECT) {
+    if constexpr (PK) {
+        // candidates j and j + step of this thread together; both rows are loaded before scoring
+        uint4 va[kVec], vb[kVec];
+        for (uint32_t j = tid; j < Cn; j += 2 * step) {
+            const uint32_t j2 = j + step;
+            uint32_t ida = kInvalid, idb = kInvalid;
+            fetch(j, va, ida);
+            if (j2 < Cn) fetch(j2, vb, idb);
+            score2(j, va, ida, j2, vb, idb);
+        }
+    } else if constexpr (DIRECT) {
         // a shard's share of the candidates is about one per thread: one row buffer (the
         // 64-register budget of two CTAs per SM has no room for a second)
         uint4 va[kVec];
@@ -373,12 +447,21 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
 
 namespace {
 
-template <int LT, int K1M, bool DIRECT = false>
+template <int LT, int K1M, bool DIRECT = false, bool PK = false>
 void allow(int optin) {
     cudaFuncAttributes a{};
-    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, rerank_ij_kernel<LT, K1M, DIRECT>));
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_ij_kernel<LT, K1M, DIRECT>,
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, rerank_ij_kernel<LT, K1M, DIRECT, PK>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_ij_kernel<LT, K1M, DIRECT, PK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes));
+}
+
+// packed two-candidate scoring for K1M = 16 (PQTG_RERANK=scalar selects the one-candidate loop)
+bool ij_packed() {
+    static const bool packed = [] {
+        const char* e = std::getenv("PQTG_RERANK");
+        return !(e && std::strcmp(e, "scalar") == 0);
+    }();
+    return packed;
 }
 
 int code_k1m(const DevParams& p) { return p.code_ij ? 16 : (p.code_pi ? 32 : 0); }
@@ -389,10 +472,24 @@ bool ij_direct(const DevParams& p) {
     return code_k1m(p) == 32 && p.shard_hi > p.shard_lo && (p.shard_hi - p.shard_lo) * 4 <= p.n;
 }
 
-size_t ij_smem(const DevParams& p, uint32_t k) {
-    const uint32_t kk = k < p.budget ? k : p.budget;
-    return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16, ij_direct(p)).total;
+int optin_smem() {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return optin;
 }
+
+size_t ij_smem(const DevParams& p, uint32_t k, bool gkeys) {
+    const uint32_t kk = k < p.budget ? k : p.budget;
+    return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16, ij_direct(p), gkeys).total;
+}
+
+}  // namespace
+
+// keys go to the workspace when the shared-memory layout with them does not fit
+bool rerank_ij_gkeys(const DevParams& p, uint32_t k) { return ij_smem(p, k, false) + 4096 > (size_t)optin_smem(); }
+
+namespace {
 
 }  // namespace
 
@@ -403,7 +500,7 @@ bool rerank_ij_ok(const DevParams& p, uint32_t k) {
     const int k1m = code_k1m(p);
     const bool shape = k1m == 16 ? (p.L == 16 || p.L == 32 || p.L == 64) : (k1m == 32 && (p.L == 16 || p.L == 32));
     return shape && p.budget <= 65535 && p.npairs <= (k1m == 16 ? 128u : 512u) &&
-           ij_smem(p, k) + 4096 <= (size_t)optin;
+           ij_smem(p, k, true) + 4096 <= (size_t)optin;
 }
 
 void configure_rerank_ij() {
@@ -413,6 +510,9 @@ void configure_rerank_ij() {
     allow<16, 16>(optin);
     allow<32, 16>(optin);
     allow<64, 16>(optin);
+    allow<16, 16, false, true>(optin);
+    allow<32, 16, false, true>(optin);
+    allow<64, 16, false, true>(optin);
     allow<16, 32>(optin);
     allow<32, 32>(optin);
     allow<16, 32, true>(optin);
@@ -423,16 +523,25 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
                       uint32_t* counts, cudaStream_t s) {
     const uint32_t kk = k < p.budget ? k : p.budget;
     const uint32_t cap = ij_sel_cap(kk);
-    const size_t sm = ij_smem(p, k);
-#define PQTG_IJ(LT, K, D)                                                                                     \
-    rerank_ij_kernel<LT, K, D><<<(unsigned)nq, ij_threads(LT), sm, s>>>(p, k, cap, ws.fine, ws.ranges,         \
-                                                                      ws.nranges, ws.ncand, ids, dists, counts)
+    const bool gk = rerank_ij_gkeys(p, k);
+    if (gk && !ws.keys) throw Error{PQTG_ERR_ARG, "workspace has no candidate-key buffer for this budget"};
+    const size_t sm = ij_smem(p, k, gk);
+    uint64_t* gkeys = gk ? ws.keys : nullptr;
+#define PQTG_IJ(LT, K, D, ...)                                                                                \
+    rerank_ij_kernel<LT, K, D, ##__VA_ARGS__><<<(unsigned)nq, ij_threads(LT), sm, s>>>(                           \
+        p, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, ids, dists, counts, gkeys)
     if (code_k1m(p) == 32) {
         const bool direct = ij_direct(p);
         if (p.L == 16) {
             if (direct) PQTG_IJ(16, 32, true); else PQTG_IJ(16, 32, false);
         } else {
             if (direct) PQTG_IJ(32, 32, true); else PQTG_IJ(32, 32, false);
+        }
+    } else if (ij_packed()) {
+        switch (p.L) {
+        case 16: PQTG_IJ(16, 16, false, true); break;
+        case 32: PQTG_IJ(32, 16, false, true); break;
+        default: PQTG_IJ(64, 16, false, true); break;
         }
     } else {
         switch (p.L) {
