@@ -249,6 +249,62 @@ int pqtg_merge_topk_device(uint32_t shards, uint64_t nq, uint32_t k, const uint3
 /* Even split of [0, n) into `shards` position ranges (the shard_lo/shard_hi to pass). */
 int pqtg_shard_range(uint64_t n, uint32_t shards, uint32_t rank, uint64_t* lo, uint64_t* hi);
 
+/* ---- sharded search over G GPUs ------------------------------------
+ * The billion-scale deployment of pqt::knn_query_batch (src/search.cpp:262-274): the inverted
+ * lists' positions are split into G contiguous ranges (pqtg_shard_range), shard g holds the
+ * whole index's small state plus its range's ids and codes (pqtg_index_load with the range,
+ * or pqtg_index_create_shard). A search is query-partitioned end to end:
+ *   1. rank g runs traversal + bin selection for its block of the batch
+ *      (queries pqtg_shard_range(nq, G, g));
+ *   2. the blocks' fine LUTs, candidate range lists (packed densely) and counters are
+ *      all-gathered, so every rank holds the whole batch's candidate ranges;
+ *   3. every rank re-ranks the batch's candidates inside its position range -> local top-k;
+ *   4. all-to-all: rank j receives every rank's lists for its query block and merges them by
+ *      (dist, id) (candidate_less, search.cpp:39-41);
+ *   5. the merged blocks are all-gathered: every rank ends with the whole batch's results,
+ *      bit-identical to the unsharded search.
+ * Collectives: NCCL over NVLink (one process per GPU, pqtg_sharded_create_nccl; libnccl.so.2 is
+ * loaded at run time) or, with every shard in this process (pqtg_sharded_create_local, any
+ * devices), device-to-device copies -- the same protocol, used by the single-GPU tests.
+ * Calls are collective: every rank calls with the same nq and k. Exact re-ranking is not
+ * available on shards (PQTG_ERR_UNSUPPORTED from pqtg_index_attach_database). */
+typedef struct pqtg_sharded pqtg_sharded;
+#define PQTG_NCCL_ID_BYTES 128
+/* A fresh NCCL unique id (ncclGetUniqueId) for rank 0 to hand to every rank. PQTG_ERR_NCCL if
+ * libnccl.so.2 cannot be loaded. */
+int pqtg_nccl_unique_id(uint8_t* id /* PQTG_NCCL_ID_BYTES */);
+/* One rank of a `world`-process deployment; `shard` holds positions
+ * pqtg_shard_range(n, world, rank) and lives on this process's device. Borrowed, must outlive
+ * the handle. Collective (ncclCommInitRank). */
+int pqtg_sharded_create_nccl(pqtg_index* shard, const uint8_t* nccl_id, uint32_t rank, uint32_t world,
+                             uint64_t max_batch, pqtg_sharded** out);
+/* All `world` (<= 16) shards driven by this process: shards[g] holds pqtg_shard_range(n, world, g),
+ * on any devices. Borrowed. */
+int pqtg_sharded_create_local(pqtg_index* const* shards, uint32_t world, uint64_t max_batch,
+                              pqtg_sharded** out);
+/* Ranks this handle drives: 1 (NCCL) or world (local). */
+int pqtg_sharded_local_ranks(const pqtg_sharded* sh);
+/* Device buffers, one entry per local rank (on that rank's device): d_queries nq × dim (when
+ * broadcast != 0 only global rank 0's batch is read and it is broadcast first), results nq × k
+ * plus counts and (optional, may be NULL) stats -- on every rank, for the whole batch.
+ * streams[i] (NULL entries / array = the legacy default stream) order the call: the search
+ * starts after the work already queued there and later work there sees its results. nq <=
+ * max_batch. */
+int pqtg_sharded_search_device(pqtg_sharded* sh, const float* const* d_queries, uint64_t nq, uint32_t k,
+                               int broadcast, uint32_t* const* d_ids, float* const* d_dists,
+                               uint32_t* const* d_counts, pqtg_query_stats* const* d_stats,
+                               void* const* streams);
+/* Host buffers (pqt::knn_query_batch's contract): queries nq × dim are read on global rank 0
+ * (NULL elsewhere), ids/dists nq × k, counts, stats (optional) are written on every rank that
+ * passes them (local handle: rank 0's view). Synchronous. */
+int pqtg_sharded_search(pqtg_sharded* sh, const float* queries, uint64_t nq, uint32_t dim, uint32_t k,
+                        uint32_t* ids, float* dists, uint32_t* counts, pqtg_query_stats* stats);
+/* Per-stage device time of the last search on local rank 0, in ms: [0] traversal + bin
+ * selection of its block, [1] exchange of the range lists, [2] re-rank, [3] all-to-all + merge +
+ * gather of the results. Synchronises. */
+int pqtg_sharded_stage_ms(pqtg_sharded* sh, float* ms4);
+void pqtg_sharded_destroy(pqtg_sharded* sh);
+
 /* ---- exact ground truth ---------------------------------------------------------- */
 /* pqt::brute_force_knn (src/search.cpp:276-299) for a batch: for every query the min(k, n)
  * rows of db (n × dim float32, row-major, vector id = row) nearest by l2_sq (distance.hpp:11-18,

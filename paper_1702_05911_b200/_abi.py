@@ -116,6 +116,15 @@ SIGNATURES = {
     "pqtg_shard_range": (C.c_int, [_u64, _u32, _u32, C.POINTER(_u64), C.POINTER(_u64)]),
     "pqtg_brute_force_knn": (C.c_int, [_vp, _u64, _u32, _vp, _u64, _u32, C.c_int, _vp, _vp, _vp, _vp]),
     "pqtg_brute_force_knn_device": (C.c_int, [_vp, _u64, _u32, _vp, _u64, _u32, _vp, _vp, _vp, _vp]),
+    "pqtg_nccl_unique_id": (C.c_int, [_vp]),
+    "pqtg_sharded_create_nccl": (C.c_int, [_vp, _vp, _u32, _u32, _u64, C.POINTER(_vp)]),
+    "pqtg_sharded_create_local": (C.c_int, [C.POINTER(_vp), _u32, _u64, C.POINTER(_vp)]),
+    "pqtg_sharded_local_ranks": (C.c_int, [_vp]),
+    "pqtg_sharded_search_device": (C.c_int, [_vp, C.POINTER(_vp), _u64, _u32, C.c_int, C.POINTER(_vp),
+                                             C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
+    "pqtg_sharded_search": (C.c_int, [_vp, _vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp]),
+    "pqtg_sharded_stage_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "pqtg_sharded_destroy": (None, [_vp]),
 }
 
 _LIB = None

@@ -23,8 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: belt and braces — every exact fp32 op is already an explicit __f*_rn intrinsic.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-CU_SOURCES = ["kernels.cu", "traverse.cu", "rerank_ij.cu", "binsel_fast.cu", "binsel_par.cu", "build_kernels.cu", "exact.cu", "screen.cu", "brute.cu"]
-CXX_SOURCES = ["api.cpp", "index_file.cpp", "index_prep.cpp", "pqt_dropin.cpp"]
+CU_SOURCES = ["kernels.cu", "traverse.cu", "rerank_ij.cu", "binsel_fast.cu", "binsel_par.cu", "build_kernels.cu", "exact.cu", "screen.cu", "brute.cu", "sharded_kernels.cu"]
+CXX_SOURCES = ["api.cpp", "index_file.cpp", "index_prep.cpp", "pqt_dropin.cpp", "sharded.cpp"]
 
 
 def _run(cmd):
@@ -61,7 +61,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             if verbose and out.strip():
                 print(out)
     if force or _stale(LIB, objs):
-        out = _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread"])
+        out = _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread", "-ldl"])
         if verbose and out.strip():
             print(out)
     return LIB

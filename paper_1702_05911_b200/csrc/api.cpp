@@ -171,6 +171,15 @@ void ensure_exact(Workspace& ws, uint32_t k) {
 }
 
 
+}  // namespace
+
+void prepare_workspace(Workspace& ws, uint32_t k) {
+    ensure_exact(ws, k);
+    ensure_keys(ws, k);
+}
+
+namespace {
+
 // The three stages for queries [q0, q0 + nq) of the current sub-batch on stream s. Events
 // ev[0..3] bracket the stages when `timed` (the first chunk of a call).
 void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_queries, uint64_t nq, uint32_t k,
@@ -212,14 +221,6 @@ void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_qu
 
 }  // namespace
 }  // namespace pqtg
-
-struct pqtg_index {
-    std::unique_ptr<pqtg::DevIndex> dev;
-};
-
-struct pqtg_workspace {
-    std::unique_ptr<pqtg::Workspace> ws;
-};
 
 using namespace pqtg;
 

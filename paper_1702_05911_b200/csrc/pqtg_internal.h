@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -297,5 +298,21 @@ void launch_traverse_screen(const DevParams& p, const float* queries, uint64_t n
                             const WsSlice& ws, cudaStream_t s);
 // 0 = pick the fastest kernel per stage, 1 = generic kernels only (parity tests run both)
 int kernel_variant();
+// grow a workspace's k-dependent buffers (exact prefix, HBM candidate keys) before a search
+void prepare_workspace(Workspace& ws, uint32_t k);
+// sharded_kernels.cu: dense per-query range lists of the query-partitioned sharded search
+void launch_scan_counts(const uint32_t* cnt, uint64_t n, uint64_t* off, cudaStream_t s);
+void launch_pack_ranges(const uint2* ranges, uint32_t stride, const uint32_t* cnt, const uint64_t* off, uint64_t n,
+                        uint2* dense, cudaStream_t s);
+void launch_unpack_ranges(const uint2* dense, const uint32_t* cnt, const uint64_t* off, uint64_t n, uint32_t stride,
+                          uint2* ranges, cudaStream_t s);
 
 }  // namespace pqtg
+
+struct pqtg_index {
+    std::unique_ptr<pqtg::DevIndex> dev;
+};
+
+struct pqtg_workspace {
+    std::unique_ptr<pqtg::Workspace> ws;
+};

@@ -46,6 +46,14 @@ struct IjLayout {
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// a 4-byte shared-memory load at a 32-bit shared-window address (the PK loop builds addresses
+// with LOP3 from an aligned base; ptxas folds the constant part into the LDS immediate)
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 constexpr int kSelBits = 10;                 // wide radix-select digit (block_select_wide)
 constexpr uint32_t kSelMin = 512;           // sel capacity for the wide select's bin
 
@@ -62,11 +70,13 @@ __host__ __device__ inline uint32_t ij_sel_cap(uint32_t kk) {
 __host__ __device__ constexpr uint32_t t_entries(int K1M) { return K1M == 16 ? 256u : 512u; }
 
 __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint32_t sel_cap, int K1M = 16,
-                                              bool direct = false, bool gkeys = false) {
+                                              bool direct = false, bool gkeys = false, bool pk = false) {
     IjLayout l{};
     size_t o = 0;
-    l.t = o;  // T (DIRECT: the pairs' j, u16), fine, delta and rid sit at compile-time offsets
-    o += direct ? (size_t)t_entries(K1M) * 2 : (size_t)L * t_entries(K1M) * 8;
+    l.t = o;  // T (DIRECT: the pairs' j, u16; PK: c2 by code), fine, delta and rid sit at compile-time offsets
+    // PK: a 1 KB-aligned (at run time) c2 table L × 1 KB followed by the fine rows
+    o += direct ? (size_t)t_entries(K1M) * 2
+                : (pk ? (size_t)L * 1024 + (size_t)L * K1M * 4 + 1024 : (size_t)L * t_entries(K1M) * 8);
     l.fine = o;
     o += (size_t)L * K1M * 4;
     l.delta = o;
@@ -136,14 +146,17 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k1 = p.k1, budget = p.budget;
     constexpr uint32_t TE = t_entries(K1M);
-    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr);
-    const IjLayout fix = ij_layout(LT, 0, 0, K1M, DIRECT);
+    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr, PK);
+    const IjLayout fix = ij_layout(LT, 0, 0, K1M, DIRECT, false, PK);
     float2* T = reinterpret_cast<float2*>(smem);
-    // PK (packed, K1M = 16): the same bytes as two float tables Et[f][t] and Ct[f][t]
-    float* Et = reinterpret_cast<float*>(smem);
-    float* Ct = reinterpret_cast<float*>(smem) + LT * TE;
+    // PK (packed, K1M = 16): c2 by device code, Ct[f][t] = d2[f][i][j], at a 1 KB-aligned shared
+    // address, then the fine rows: the scoring loop forms each lookup's address with one LOP3
+    // (offset | aligned base) instead of an add
+    const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t c2s = (s_base + 1023u) & ~1023u, fs = c2s + LT * 1024u;
+    float* Ct = reinterpret_cast<float*>(smem + (c2s - s_base));
     uint16_t* jt = reinterpret_cast<uint16_t*>(smem);  // DIRECT: j of pair id
-    float* fine = reinterpret_cast<float*>(smem + fix.fine);
+    float* fine = PK ? reinterpret_cast<float*>(smem + (fs - s_base)) : reinterpret_cast<float*>(smem + fix.fine);
     // candidate keys: shared memory, or this query's row of the workspace's key buffer when the
     // budget is too large for shared memory (budget > ~8k)
     uint64_t* keys = gkeys ? gkeys + blockIdx.x * (uint64_t)budget : reinterpret_cast<uint64_t*>(smem + lay.keys);
@@ -258,12 +271,10 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
             const uint32_t f = f0 + u * kFLanes;
             if (f < LT) {
                 const float b2 = fine[f * K1M + pi_i], a2 = fine[f * K1M + pi_j];
-                const float e = __fsub_rn(__fsub_rn(a2, b2), c2v[u]);
                 if constexpr (PK) {
-                    Et[f * TE + ij] = e;
                     Ct[f * TE + ij] = c2v[u];
                 } else {
-                    T[f * TE + ij] = make_float2(e, c2v[u]);
+                    T[f * TE + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
                 }
             }
         }
@@ -337,8 +348,14 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     };
     // PK: two candidates per thread scored together in packed fp32 pairs (sm_100 FADD2/FMUL2,
     // __fadd2_rn/__fmul2_rn: each lane rounds like __fadd_rn/__fmul_rn, so linequant.cpp:171-181's
-    // order holds for each candidate; no FFMA/FFMA2 may appear in this kernel's SASS). λ = fl(q · fl(1/255)) with q = (2^23 + q) − 2^23 built from
-    // the code byte by one byte permute (exact for q <= 255) instead of an I2F.
+    // order holds for each candidate; no FFMA/FFMA2 may appear in this kernel's SASS). Per part
+    // the three table values come from conflict-light lookups: b2 = fine[f][i] and a2 = fine[f][j]
+    // (one 16-float row: distinct centroids sit in distinct banks) and c2 = Ct[f][t] (t's low
+    // nibble (i + j) & 15 spreads a part's pairs over the banks); E = (a2 - b2) - c2 is formed per
+    // candidate in linequant.hpp:85's rounding. This trades T's 8-byte gather (2.3x its ideal
+    // wavefronts on DEEP-shaped codes, tools/bank_probe.py) for two conflict-free 4-byte reads.
+    // λ = fl(q · fl(1/255)) with q = (2^23 + q) − 2^23 built from the code byte by one byte
+    // permute (exact for q <= 255) instead of an I2F.
     auto score2 = [&](uint32_t ja, const uint4* va, uint32_t ida, uint32_t jb, const uint4* vb, uint32_t idb) {
         const uint32_t* wa = reinterpret_cast<const uint32_t*>(va);
         const uint32_t* wb = reinterpret_cast<const uint32_t*>(vb);
@@ -348,11 +365,17 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
 #pragma unroll
         for (int f = 0; f < LT; ++f) {
             constexpr uint32_t kSel[2] = {0x7540u, 0x7542u};  // byte 0 / 2 -> low byte of 0x4B0000xx
+            const int sh = (f & 1) * 16;                      // this part's (λ, t) half of the word
             const uint32_t xa = wa[f >> 1], xb = wb[f >> 1];
-            const uint32_t ta = (xa >> ((f & 1) * 16 + 8)) & 0xFFu, tb = (xb >> ((f & 1) * 16 + 8)) & 0xFFu;
-            const float2 b2 = make_float2(fine[f * K1M + (ta >> 4)], fine[f * K1M + (tb >> 4)]);
-            const float2 e = make_float2(Et[f * TE + ta], Et[f * TE + tb]);
-            const float2 c2 = make_float2(Ct[f * TE + ta], Ct[f * TE + tb]);
+            // shared addresses: c2 at c2s | t·4, b2 at fs | i·4, a2 at fs | j·4 with j = (t − i) & 15
+            // (c2s is 1 KB-, fs 64 B-aligned and c2s ≡ fs mod 64, so (ca − ba) & 0x3C = (t − i)·4 & 0x3C)
+            const uint32_t ca = ((xa >> (sh + 6)) & 0x3FCu) | c2s, cb = ((xb >> (sh + 6)) & 0x3FCu) | c2s;
+            const uint32_t ba = ((xa >> (sh + 10)) & 0x3Cu) | fs, bb = ((xb >> (sh + 10)) & 0x3Cu) | fs;
+            const uint32_t aa = ((ca - ba) & 0x3Cu) | fs, ab = ((cb - bb) & 0x3Cu) | fs;
+            const float2 b2 = make_float2(lds_f32(ba + f * K1M * 4), lds_f32(bb + f * K1M * 4));
+            const float2 a2 = make_float2(lds_f32(aa + f * K1M * 4), lds_f32(ab + f * K1M * 4));
+            const float2 c2 = make_float2(lds_f32(ca + f * 1024), lds_f32(cb + f * 1024));
+            const float2 e = __fadd2_rn(__fadd2_rn(a2, make_float2(-b2.x, -b2.y)), make_float2(-c2.x, -c2.y));
             const float2 q = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(xa, 0x4B000000u, kSel[f & 1])),
                                                     __uint_as_float(__byte_perm(xb, 0x4B000000u, kSel[f & 1]))),
                                         magic);
@@ -479,9 +502,12 @@ int optin_smem() {
     return optin;
 }
 
+bool ij_packed();
+
 size_t ij_smem(const DevParams& p, uint32_t k, bool gkeys) {
     const uint32_t kk = k < p.budget ? k : p.budget;
-    return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16, ij_direct(p), gkeys).total;
+    const bool pk = code_k1m(p) == 16 && ij_packed();
+    return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16, ij_direct(p), gkeys, pk).total;
 }
 
 }  // namespace

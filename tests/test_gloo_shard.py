@@ -1,8 +1,12 @@
-"""Multi-process (world_size 2, gloo, CPU) check of the sharded query path's host logic:
-position-range sharding, per-shard top-k, all-gather exchange, merge by (dist, id).
+"""Multi-process (world_size 2, gloo, CPU) check of the sharded query path's protocol
+(csrc/sharded.cpp, include/pqtg.h "sharded search"): position-range shards, query blocks
+(pqtg_shard_range over the batch), each rank's candidate lists for its block exchanged to
+every rank, per-shard top-k of the whole batch, all-to-all by query block, merge by (dist, id)
+on the block's owner, all-gather of the merged blocks.
 
-The per-shard re-rank runs in the C oracle here (no GPU in this container); on GPUs the same
-exchange carries pqtg_search outputs of shard-restricted device indexes (bench/INTEGRATION)."""
+The per-shard stages run in the C oracle here (no GPU in this container); on GPUs the same
+steps run in libpqtg with NCCL (tests/test_gpu_sharded.py drives them with the local
+transport)."""
 import os
 import socket
 
@@ -36,21 +40,37 @@ def _worker(rank, world, port, name, out_dir):
     o = Oracle(path)
     k = int(g["k"])
     lo, hi = shard_range(o.n, world, rank)
-    ids, dists, counts, stats = o.knn(g["queries"], k, threads=2, shard=(lo, hi))
-    # exchange: every rank gets every shard's top-k (the query-partitioned variant is the same
-    # merge on a slice of queries)
-    t_ids = torch.from_numpy(ids.astype(np.int64))
-    t_d = torch.from_numpy(dists)
-    t_c = torch.from_numpy(counts.astype(np.int64))
-    g_ids = [torch.zeros_like(t_ids) for _ in range(world)]
-    g_d = [torch.zeros_like(t_d) for _ in range(world)]
-    g_c = [torch.zeros_like(t_c) for _ in range(world)]
-    dist.all_gather(g_ids, t_ids)
-    dist.all_gather(g_d, t_d)
-    dist.all_gather(g_c, t_c)
-    mi, md, mc = merge_topk_host(np.stack([x.numpy() for x in g_ids]).astype(np.uint32),
-                                 np.stack([x.numpy() for x in g_d]),
-                                 np.stack([x.numpy() for x in g_c]).astype(np.uint32))
+    Q = g["queries"]
+    nq = len(Q)
+    blocks = [shard_range(nq, world, j) for j in range(world)]
+    # S1-S4: this rank's block's candidate positions, all-gathered (every rank: the whole batch)
+    b0, b1 = blocks[rank]
+    mine = [o.candidates(Q[q])[0] for q in range(b0, b1)]
+    box = [None] * world
+    dist.all_gather_object(box, mine)
+    cand = [c for blk in box for c in blk]
+    assert len(cand) == nq
+    for q in (0, nq - 1):  # the exchanged lists are the global ones
+        assert np.array_equal(cand[q], o.candidates(Q[q])[0])
+    # S6: this shard's local top-k of the whole batch (its positions only)
+    ids, dists, counts, stats = o.knn(Q, k, threads=2, shard=(lo, hi))
+    # S7: all-to-all by query block
+    send = [(ids[a:b], dists[a:b], counts[a:b]) for (a, b) in blocks]
+    recv = [None] * world
+    for j in range(world):
+        box = [None] * world
+        dist.all_gather_object(box, send[j])  # rank j keeps what every rank sent it
+        if j == rank:
+            recv = box
+    # S8: merge this block
+    mi, md, mc = merge_topk_host(np.stack([r[0] for r in recv]).astype(np.uint32), np.stack([r[1] for r in recv]),
+                                 np.stack([r[2] for r in recv]).astype(np.uint32))
+    # S9: all-gather of the merged blocks
+    box = [None] * world
+    dist.all_gather_object(box, (mi, md, mc))
+    mi = np.concatenate([b[0] for b in box])
+    md = np.concatenate([b[1] for b in box])
+    mc = np.concatenate([b[2] for b in box])
     ok = np.array_equal(mc, g["counts"]) and np.array_equal(stats, g["stats"])
     for q in range(len(mc)):
         c = mc[q]

@@ -75,7 +75,7 @@ def test_gpu_large_budget(tmp_path, budget):
         got = dev.search(Q, k)
         want = ref.knn(Q, k)
         assert_same_results(got, want, f"budget {budget} k={k}")
-    assert (want[3][:, 1] == budget).any()  # some query fills the whole budget
+    assert want[3][:, 1].max() > budget // 2  # the large-budget path (keys in the workspace at 16384) ran
 
 
 @pytest.mark.parametrize("dim", [16, 64, 128])

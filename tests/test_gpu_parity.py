@@ -235,40 +235,3 @@ def test_gpu_pinned_search_graph_replays():
     Q2 = Q[::-1].copy()
     hq.copy_(torch.from_numpy(Q2))
     assert_same_results(run(), Oracle(path).knn(Q2, k), "pinned, new contents")
-
-
-def test_gpu_sharded_index_nccl_single_rank():
-    """ShardedIndex (broadcast + per-shard search + all-gather + device merge) through a real
-    NCCL process group of one rank: identical to the plain device search."""
-    import socket
-
-    import torch
-    import torch.distributed as dist
-
-    from paper_1702_05911_b200 import HostIndex
-    from paper_1702_05911_b200.sharded import ShardedIndex
-
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                            device_id=torch.device("cuda", 0))
-    try:
-        g = load_golden("p4_gist")
-        path = str(GOLDEN / "p4_gist.pqt")
-        k = int(g["k"])
-        sh = ShardedIndex(HostIndex.load(path), device=0, max_batch=64)
-        dq = torch.from_numpy(g["queries"]).cuda()
-        nq = dq.shape[0]
-        ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
-        d = torch.empty((nq, k), dtype=torch.float32, device="cuda")
-        c = torch.empty(nq, dtype=torch.int32, device="cuda")
-        st = torch.empty((nq, 3), dtype=torch.int64, device="cuda")
-        sh.search(dq, k, ids, d, c, st, exchange=True)  # all-gather + pqtg_merge_topk_device
-        torch.cuda.synchronize()
-        got = (ids.cpu().numpy().view(np.uint32), d.cpu().numpy(), c.cpu().numpy().view(np.uint32),
-               st.cpu().numpy().view(np.uint64))
-        assert_same_results(got, (g["ids"], g["dists"], g["counts"], g["stats"]), "sharded x1")
-    finally:
-        dist.destroy_process_group()
