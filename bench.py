@@ -347,14 +347,15 @@ def algorithmic_bytes(hix, counters, stats, k: int):
 
 
 def measured_traffic(workload: str, stage: str, nq: int):
-    """DRAM bytes per launch of `stage` from the committed ncu capture (profiles/traffic.json,
-    tools/ncu_traffic.py), scaled to this run's queries per launch; None if not captured."""
+    """DRAM bytes per launch of `stage` from the committed ncu capture of this workload
+    (profiles/traffic.json, tools/ncu_traffic.py), scaled to this run's queries per launch;
+    None if not captured."""
     p = REPO / "profiles" / "traffic.json"
     if not p.exists():
         return None, None
-    d = json.loads(p.read_text())
-    k = d.get("kernels", {}).get(stage)
-    if d.get("workload") != workload or not k:
+    d = json.loads(p.read_text()).get("workloads", {}).get(workload)
+    k = d.get("kernels", {}).get(stage) if d else None
+    if not k:
         return None, None
     return k["dram_bytes_per_launch"] * nq / d["queries_per_launch"], f"profiles/traffic.json ({d['report']})"
 

@@ -213,6 +213,8 @@ class Ref(_Lib):
         "ref_knn_batch": (C.c_int, [_vp, _vp, _u64, _u32, C.c_int, _vp, _vp, _vp, _vp, _vp]),
         "ref_traverse": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
         "ref_heuristic_order": (C.c_int64, [_vp, _vp, _u32, _u32, _u64, _vp]),
+        "ref_dijkstra_order": (C.c_int64, [_vp, _u32, _u32, _u64, _vp]),
+        "ref_decode_pairs": (C.c_int, [_u32, _u32, _vp]),
         "ref_pick_slope_table": (_u32, [_vp, _u64, _vp, _u64]),
         "ref_build_slope_tables": (C.c_int, [_u32, _vp, _vp]),
         "ref_encode_slot": (_u64, [_vp, _u32, _u32, _u32, _u64]),
@@ -359,6 +361,22 @@ class Ref(_Lib):
         a = np.ascontiguousarray(a, np.float32)
         b = np.ascontiguousarray(b, np.float32)
         return int(cls.so().ref_pick_slope_table(_p(a), a.size, _p(b), b.size))
+
+    @classmethod
+    def dijkstra_order(cls, lists: np.ndarray, max_bins: int):
+        lists = np.ascontiguousarray(lists, np.float32)
+        parts, ln = lists.shape
+        out = np.zeros((max(max_bins, 1), parts), np.uint32)
+        cnt = cls.so().ref_dijkstra_order(_p(lists), parts, ln, max_bins, _p(out))
+        if cnt < 0:
+            raise RuntimeError(cls.so().ref_last_error().decode())
+        return out[:cnt]
+
+    @classmethod
+    def decode_pairs(cls, k1: int, count: int):
+        out = np.zeros((max(count, 1), 2), np.uint16)
+        cls.so().ref_decode_pairs(k1, count, _p(out))
+        return out[:count]
 
     @classmethod
     def build_slope_tables(cls, length: int = 4096):

@@ -362,6 +362,30 @@ int ref_traverse(void* handle, const float* y, float* fine, uint32_t* l1_id, flo
     }
 }
 
+// pqt::dijkstra_order (binorder.cpp:114-167). lists: parts × len. Returns the tuple count.
+int64_t ref_dijkstra_order(const float* lists, uint32_t parts, uint32_t len, uint64_t max_bins, uint32_t* out) {
+    try {
+        std::vector<std::vector<float>> dl(parts);
+        for (uint32_t p = 0; p < parts; ++p) dl[p].assign(lists + (size_t)p * len, lists + (size_t)(p + 1) * len);
+        pqt::BinSequence s = pqt::dijkstra_order(dl, max_bins);
+        std::memcpy(out, s.ranks.data(), s.ranks.size() * sizeof(uint32_t));
+        return static_cast<int64_t>(s.size());
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
+}
+
+// pqt::decode_pair (linequant.cpp) for every pair id < count
+int ref_decode_pairs(uint32_t k1, uint32_t count, uint16_t* out) {
+    for (uint32_t q = 0; q < count; ++q) {
+        const auto ij = pqt::decode_pair(q, k1);
+        out[2 * q] = ij[0];
+        out[2 * q + 1] = ij[1];
+    }
+    return 0;
+}
+
 // pqt::heuristic_order over the index's tables (binorder.cpp:301-316). lists: parts × len.
 // Returns the number of tuples written to out (parts × count), or -1.
 int64_t ref_heuristic_order(void* handle, const float* lists, uint32_t parts, uint32_t len,

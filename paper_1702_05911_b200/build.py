@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 CU_SOURCES = ["kernels.cu", "traverse.cu", "rerank_ij.cu", "binsel_fast.cu", "binsel_par.cu", "build_kernels.cu", "exact.cu", "screen.cu", "brute.cu", "sharded_kernels.cu"]
-CXX_SOURCES = ["api.cpp", "index_file.cpp", "index_prep.cpp", "pqt_dropin.cpp", "sharded.cpp"]
+CXX_SOURCES = ["api.cpp", "index_file.cpp", "index_prep.cpp", "pqt_dropin.cpp", "pqt_stages.cpp", "sharded.cpp"]
 
 
 def _run(cmd):
@@ -54,8 +54,9 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         objs.append(obj)
         if force or _stale(obj, [path, *headers, Path(__file__)]):
             flags = list(NVCC_FLAGS)
-            if src == "pqt_dropin.cpp":  # the reference API is C++20 (std::span)
+            if src in ("pqt_dropin.cpp", "pqt_stages.cpp"):  # the reference API is C++20 (std::span)
                 flags[flags.index("-std=c++17")] = "-std=c++20"
+                flags[flags.index("-fPIC,-O2")] = "-fPIC,-O2,-ffp-contract=off"
             cmd = [NVCC, *ARCH, *flags, "-I", str(REPO / "include"), "-c", str(path), "-o", str(obj)]
             out = _run(cmd)
             if verbose and out.strip():

@@ -478,11 +478,15 @@ void allow(int optin) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes));
 }
 
-// packed two-candidate scoring for K1M = 16 (PQTG_RERANK=scalar selects the one-candidate loop)
+// The packed two-candidate loop (PK) is an opt-in variant (PQTG_RERANK=packed): bit-exact (the
+// GPU parity suite passes with it as the default), but slower on B200 -- DEEP100M 1438 vs 1402 us,
+// SIFT1M 1388 vs 1133 us, GIST1M 157 vs 130 us per batch (profiles/r02/rerank_packed_ab.md): it
+// cuts the L1 data-pipe wavefronts 20% (134 M -> 108 M per 5000 queries) but adds 20% more
+// instructions, and the scalar loop was co-limited by both.
 bool ij_packed() {
     static const bool packed = [] {
         const char* e = std::getenv("PQTG_RERANK");
-        return !(e && std::strcmp(e, "scalar") == 0);
+        return e && std::strcmp(e, "packed") == 0;
     }();
     return packed;
 }

@@ -4,6 +4,10 @@
 //   dropin_main io    <index.pqt> <copy.pqt>                         load + save (no GPU)
 //   dropin_main query <index.pqt> <queries.f32> <dim> <k> <out.bin> [db.f32]
 //                                                      load (+ attach_database) + knn_query_batch
+//   dropin_main stages <index.pqt> <queries.f32> <dim> <max_bins> <out.bin>
+//                                  per query: traverse, pick_slope_table, heuristic_order,
+//                                  dijkstra_order, line_distance of stored codes 0..7; then
+//                                  decode_pair of every pair id and build_slope_tables (no GPU)
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -12,8 +16,65 @@
 #include <string>
 #include <vector>
 
+#include "pqt/binorder.hpp"
 #include "pqt/index_io.hpp"
+#include "pqt/linequant.hpp"
+#include "pqt/pqtree.hpp"
 #include "pqt/search.hpp"
+
+template <class T>
+static void put(std::ofstream& o, const T* p, std::size_t n) {
+    o.write(reinterpret_cast<const char*>(p), static_cast<std::streamsize>(n * sizeof(T)));
+}
+
+static int stages(const pqt::PqtIndex& index, const pqt::VectorSet& q, std::size_t max_bins, const char* path) {
+    std::ofstream out(path, std::ios::binary);
+    const auto& c = index.config;
+    for (std::size_t i = 0; i < q.count(); ++i) {
+        const pqt::TraversalLists tl = pqt::traverse(index.tree, index.fine, q.row(i), c);
+        put(out, tl.fine_dists.data(), tl.fine_dists.size());
+        for (const auto& l : tl.level1)
+            for (const auto& e : l) {
+                put(out, &e.id, 1);
+                put(out, &e.dist, 1);
+            }
+        std::vector<std::vector<float>> lists;
+        for (const auto& l : tl.level2) {
+            lists.emplace_back();
+            for (const auto& e : l) {
+                put(out, &e.parent, 1);
+                put(out, &e.child, 1);
+                put(out, &e.dist, 1);
+                lists.back().push_back(e.dist);
+            }
+        }
+        const std::uint32_t slope = lists.size() >= 2 ? pqt::pick_slope_table(lists[0], lists[1]) : 5u;
+        put(out, &slope, 1);
+        for (const auto& seq : {pqt::heuristic_order(lists, index.tables, max_bins), pqt::dijkstra_order(lists, max_bins)}) {
+            const std::uint32_t cnt = static_cast<std::uint32_t>(seq.size());
+            put(out, &cnt, 1);
+            put(out, seq.ranks.data(), seq.ranks.size());
+        }
+        for (std::size_t v = 0; v < 8 && v < index.size(); ++v) {
+            const float d = pqt::line_distance(index.codes.lambda_row(v), index.codes.pair_row(v), tl.fine_dists.data(),
+                                               index.pair_table);
+            put(out, &d, 1);
+        }
+    }
+    for (std::uint32_t p = 0; p < index.pair_table.pair_count(); ++p) {
+        const auto ij = pqt::decode_pair(p, c.k1);
+        put(out, ij.data(), 2);
+    }
+    const auto tables = pqt::build_slope_tables(pqt::kDefaultOrderTableLen);
+    for (const auto& t : tables) {
+        put(out, &t.slope, 1);
+        for (const auto& [a, b] : t.entries) {
+            put(out, &a, 1);
+            put(out, &b, 1);
+        }
+    }
+    return 0;
+}
 
 int main(int argc, char** argv) {
     if (argc < 4) return 2;
@@ -34,6 +95,7 @@ int main(int argc, char** argv) {
         in.seekg(0);
         in.read(reinterpret_cast<char*>(q.data.data()), bytes);
     }
+    if (mode == "stages") return stages(index, q, k, argv[6]);
     // the reference's error behaviour: wrong dimension -> std::invalid_argument
     bool threw = false;
     try {
