@@ -823,7 +823,7 @@ def main():
     for b in range(args.batches):
         step(b)
         torch.cuda.synchronize()
-        counters.append(dev.counters(nq))
+        counters.append((sh if args.shard else dev).counters(nq))
         stats_all.append(d_stats.cpu().numpy().astype(np.uint64))
     for _ in range(args.warmup):
         for b in range(args.batches):
@@ -901,7 +901,9 @@ def main():
     ms_max = float(t.item())
     value = jobs * nq * args.steps / (ms_max / 1000.0)
 
-    # ---- per-kernel times (unchunked launches: one launch per stage per step)
+    # ---- per-kernel times (unchunked launches: one launch per stage per step). Sharded: the
+    # protocol's stages on this rank -- block traversal + bin selection, range exchange, re-rank,
+    # all-to-all + merge + result gather (pqtg_sharded_stage_ms)
     dev.set_chunks(1)
     stage_sum = np.zeros(4)
     kstep = min(args.steps, 50)
@@ -909,7 +911,7 @@ def main():
         if not args.no_flush:
             flush.fill_(s & 0xFF)
         step(s % args.batches)
-        stage_sum += np.array(dev.stage_ms())
+        stage_sum += np.array(sh.stage_ms() if args.shard else dev.stage_ms())
     stage_mean = stage_sum / kstep
     dev.set_chunks(args.chunks)
 
@@ -927,28 +929,48 @@ def main():
         return
 
     # ---- roofline of the dominant kernel
-    names = ["traverse", "binsel", "rerank"]
     abytes = [algorithmic_bytes(hix, counters[b], stats_all[b], k) for b in range(args.batches)]
     ab = {kk: float(np.mean([a[kk] for a in abytes])) for kk in abytes[0]}
-    dom = int(np.argmax(stage_mean[:3]))
     peak, peak_src = peaks()
-    traffic, traffic_src = measured_traffic(args.workload, names[dom], nq)
-    achieved = ab[names[dom]] / (stage_mean[dom] / 1000.0) / 1e9
-    roofline = {"bound": "hbm", "kernel": {"traverse": "traverse_kernel", "binsel": "binsel_kernel",
-                                           "rerank": "rerank_kernel"}[names[dom]],
+    limiter = {"traverse": "issue (IPC ~3.5, sequential fp32 chains + level-2 sort)",
+               "binsel": "latency / L2-probe throughput per pass (issue active ~22-60%)",
+               "rerank": "L1 data pipe (90% of peak: shared-memory table gathers at 2.3x their ideal wavefronts "
+                         "on DEEP) + issue (~15.5 SASS per part); profiles/r02/rerank_packed_ab.md"}
+    if args.shard:
+        # this rank's block is 1/world of the batch for traversal + bin selection (ntuples are
+        # counted on the block only; bins on the whole batch, so the block figure is an upper bound)
+        names = ["block_traverse_binsel", "exchange", "rerank", "merge"]
+        kb = {"block_traverse_binsel": ab["traverse"] / world + ab["binsel"], "rerank": ab["rerank"]}
+        dom = 2 if stage_mean[2] >= stage_mean[0] else 0
+        dname = names[dom]
+        traffic, traffic_src = None, None
+        achieved = kb[dname] / (stage_mean[dom] / 1000.0) / 1e9
+        stage_ms = {n: float(v) for n, v in zip(names, stage_mean)}
+        per_kernel = {n: kb[n] / (stage_mean[i] / 1000.0) / 1e9 for i, n in enumerate(names) if n in kb}
+        kernel = "rerank_kernel" if dom == 2 else "traverse+binsel_kernels"
+        abl = kb[dname]
+    else:
+        names = ["traverse", "binsel", "rerank"]
+        dom = int(np.argmax(stage_mean[:3]))
+        dname = names[dom]
+        traffic, traffic_src = measured_traffic(args.workload, dname, nq)
+        achieved = ab[dname] / (stage_mean[dom] / 1000.0) / 1e9
+        stage_ms = {n: float(v) for n, v in zip(names, stage_mean[:3])}
+        per_kernel = {n: ab[n] / (stage_mean[i] / 1000.0) / 1e9 for i, n in enumerate(names)}
+        kernel = {"traverse": "traverse_kernel", "binsel": "binsel_kernel", "rerank": "rerank_kernel"}[dname]
+        abl = ab[dname]
+    tot = sum(stage_ms.values())
+    roofline = {"bound": "hbm", "kernel": kernel,
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_src, "traffic": traffic, "traffic_source": traffic_src,
-                "algorithmic_bytes_per_launch": ab[names[dom]],
-                "stage_ms": {n: float(v) for n, v in zip(names, stage_mean[:3])},
-                "stage_share": {n: float(v / stage_mean[:3].sum()) for n, v in zip(names, stage_mean[:3])},
-                "per_kernel_gbs": {n: ab[n] / (stage_mean[i] / 1000.0) / 1e9 for i, n in enumerate(names)},
+                "algorithmic_bytes_per_launch": abl,
+                "stage_ms": stage_ms,
+                "stage_share": {n: v / tot for n, v in stage_ms.items()},
+                "per_kernel_gbs": per_kernel,
                 "T_q": ab["T_q"], "C_q": ab["C_q"], "bins_q": ab["bins_q"],
                 "survey_Bq_gbs": ab["survey_Bq_total"] / (ms_max / args.steps / 1000.0) / 1e9,
-                # what bounds each kernel instead of HBM (ncu, profiles/r01h/ncu_full_summary_*.txt)
-                "limiter": {"traverse": "issue (IPC ~3.5, sequential fp32 chains + level-2 sort)",
-                            "binsel": "latency / L2-probe throughput per pass (issue active ~22-60%)",
-                            "rerank": "issue + shared-memory pipe (~14 SASS and 2 LDS per part, issue "
-                                      "active ~64%; real DRAM traffic ~1/4 of the algorithmic bytes)"}}
+                # what bounds each kernel instead of HBM (ncu, profiles/r02/)
+                "limiter": limiter}
 
     # ---- CPU baseline (rank 0, N=1) + parity of the timed batch
     cpu = None
@@ -990,7 +1012,8 @@ def main():
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "link_gbs": link, "host_cpus": affinity,
                 "transfer_bound_qps": nq / (h2d / (link["h2d"] * 1e9) + d2h / (link["d2h"] * 1e9))},
-        "gpu_launches": gpu_launches(hix, nq, args.chunks) * args.steps * (4 if args.exact else 3) // 3,
+        "gpu_launches": (8 * args.steps if args.shard  # traverse, binsel, scan, pack, scan, unpack, rerank, merge
+                         else gpu_launches(hix, nq, args.chunks) * args.steps * (4 if args.exact else 3) // 3),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "parity": parity,

@@ -284,6 +284,10 @@ int pqtg_sharded_create_local(pqtg_index* const* shards, uint32_t world, uint64_
                               pqtg_sharded** out);
 /* Ranks this handle drives: 1 (NCCL) or world (local). */
 int pqtg_sharded_local_ranks(const pqtg_sharded* sh);
+/* The workspace a local rank searched its last batch in (borrowed; pqtg_workspace_read gives
+ * the whole batch's gathered candidate positions and counts; ntuples only for this rank's query
+ * block). NULL on a bad argument. */
+pqtg_workspace* pqtg_sharded_workspace(pqtg_sharded* sh, uint32_t local_rank);
 /* Device buffers, one entry per local rank (on that rank's device): d_queries nq × dim (when
  * broadcast != 0 only global rank 0's batch is read and it is broadcast first), results nq × k
  * plus counts and (optional, may be NULL) stats -- on every rank, for the whole batch.

@@ -414,6 +414,8 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             launch_unpack_ranges(r.all_packed, r.ws().nranges, r.all_off, nq, std::max<uint32_t>(budget, 1),
                                  r.ws().ranges, r.stream);
             launch_rerank(p, nq, k, r.ws().slice(0), r.l_ids, r.l_dists, r.l_counts, r.stream);
+            r.ws().last_nq = nq;  // pqtg_workspace_read of this rank's view (pqtg_sharded_workspace)
+            r.ws().last_stream = r.stream;
             if (i == 0) PQTG_CUDA_CHECK(cudaEventRecord(r.ev[3], r.stream));
         }
         // S7: all-to-all of the local lists by query block
@@ -582,6 +584,14 @@ int pqtg_sharded_create_local(pqtg_index* const* shards, uint32_t world, uint64_
 }
 
 int pqtg_sharded_local_ranks(const pqtg_sharded* sh) { return sh ? (int)sh->ranks.size() : 0; }
+
+pqtg_workspace* pqtg_sharded_workspace(pqtg_sharded* sh, uint32_t local_rank) {
+    if (!sh || local_rank >= sh->ranks.size()) {
+        set_error("bad sharded handle or local rank");
+        return nullptr;
+    }
+    return sh->ranks[local_rank]->wsh.get();
+}
 
 int pqtg_sharded_search_device(pqtg_sharded* sh, const float* const* d_queries, uint64_t nq, uint32_t k, int broadcast,
                                uint32_t* const* d_ids, float* const* d_dists, uint32_t* const* d_counts,

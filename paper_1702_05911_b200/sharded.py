@@ -64,6 +64,29 @@ class _Handle:
         check(lib().pqtg_sharded_stage_ms(self._sh, ms))
         return list(ms)
 
+    def counters(self, nq: int, local_rank: int = 0) -> dict:
+        """The last batch's per-query candidates (global), tuples consumed (this rank's query
+        block only; 0 elsewhere) and candidates inside the rank's position shard."""
+        ws = lib().pqtg_sharded_workspace(self._sh, local_rank)
+        if not ws:
+            raise RuntimeError(lib().pqtg_last_error().decode())
+        dev = self.shards[local_rank] if hasattr(self, "shards") else self.local
+        lo, hi = int(dev.info.shard_lo), int(dev.info.shard_hi)
+        budget = max(min(dev.config.candidate_budget, dev.n), 1)
+        pos = np.zeros((nq, budget), np.uint32)
+        nc = np.zeros(nq, np.uint32)
+        nt = np.zeros(nq, np.uint32)
+        check(lib().pqtg_workspace_read(ws, nq, None, None, None, None, pos.ctypes.data, nc.ctypes.data,
+                                        nt.ctypes.data))
+        valid = np.arange(budget)[None, :] < nc[:, None]
+        nl = np.count_nonzero(valid & (pos >= lo) & (pos < hi), axis=1).astype(np.uint32)
+        rank = getattr(self, "rank", local_rank)
+        world = self.world
+        b0, b1 = shard_range(nq, world, rank)
+        nt[:b0] = 0
+        nt[b1:] = 0
+        return dict(ncand=nc, ntuples=nt, nlocal=nl)
+
     def close(self):
         if getattr(self, "_sh", None):
             lib().pqtg_sharded_destroy(self._sh)
