@@ -18,6 +18,7 @@
 
 #include "../../include/pqt/index_io.hpp"
 #include "../../include/pqt/search.hpp"
+#include "../../include/pqt/sharded.hpp"
 #include "pqtg_internal.h"
 
 namespace pqt {
@@ -422,6 +423,68 @@ QueryResult brute_force_knn(const VectorSet& db, const float* y, std::uint32_t k
     result.stats.rerank_us =
         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     return result;
+}
+
+// ------------------------------------------------------------------ sharded (pqtg_sharded_*)
+ShardedIndex::UniqueId ShardedIndex::nccl_unique_id() {
+    UniqueId id{};
+    check(pqtg_nccl_unique_id(id.data()));
+    return id;
+}
+
+ShardedIndex::ShardedIndex(const std::string& path, std::uint32_t rank, std::uint32_t world, const UniqueId& id,
+                           int device, std::size_t max_batch)
+    : rank_(rank), max_batch_(max_batch) {
+    if (world == 0 || rank >= world) throw std::invalid_argument("ShardedIndex: rank must be < world");
+    {
+        std::ifstream in(path, std::ios::binary);  // n from the fixed header (index_io.cpp:94-106)
+        char hdr[73];
+        if (!in.read(hdr, sizeof hdr)) throw FormatError(path + ": truncated index file");
+        std::uint64_t n = 0;
+        std::uint32_t dim = 0;
+        std::memcpy(&dim, hdr + 12, 4);
+        std::memcpy(&n, hdr + 65, 8);
+        n_ = n;
+        dim_ = dim;
+    }
+    std::uint64_t lo = 0, hi = 0;
+    check(pqtg_shard_range(n_, world, rank, &lo, &hi));
+    if (world == 1) lo = hi = 0;
+    check(pqtg_index_load(path.c_str(), device, lo, hi, &shard_));
+    const int rc = pqtg_sharded_create_nccl(shard_, id.data(), rank, world, max_batch, &sh_);
+    if (rc != PQTG_OK) {
+        pqtg_index_destroy(shard_);
+        shard_ = nullptr;
+        rethrow(rc);
+    }
+}
+
+ShardedIndex::~ShardedIndex() {
+    pqtg_sharded_destroy(sh_);
+    pqtg_index_destroy(shard_);
+}
+
+std::vector<QueryResult> ShardedIndex::knn_query_batch(const VectorSet& queries, std::uint32_t k) {
+    if (queries.count() > 0 && queries.dim != dim_) throw std::invalid_argument("knn_query_batch: query dimension mismatch");
+    const std::size_t nq = queries.count();
+    std::vector<QueryResult> results(nq);
+    std::vector<std::uint32_t> ids(nq * std::max<std::uint32_t>(k, 1)), counts(nq);
+    std::vector<float> dists(nq * std::max<std::uint32_t>(k, 1));
+    std::vector<pqtg_query_stats> stats(nq);
+    for (std::size_t q0 = 0; q0 < nq; q0 += max_batch_) {  // sub-batches of max_batch (collective)
+        const std::size_t b = std::min(max_batch_, nq - q0);
+        check(pqtg_sharded_search(sh_, queries.data.data() + q0 * dim_, b, dim_, k, ids.data() + q0 * k,
+                                  dists.data() + q0 * k, counts.data() + q0, stats.data() + q0));
+    }
+    for (std::size_t q = 0; q < nq; ++q) {
+        QueryResult& r = results[q];
+        r.ids.assign(ids.begin() + q * k, ids.begin() + q * k + counts[q]);
+        r.dists.assign(dists.begin() + q * k, dists.begin() + q * k + counts[q]);
+        r.stats.bins_visited = stats[q].bins_visited;
+        r.stats.candidates = stats[q].candidates;
+        r.stats.exact_evals = stats[q].exact_evals;
+    }
+    return results;
 }
 
 }  // namespace pqt

@@ -4,6 +4,8 @@
 //   dropin_main io    <index.pqt> <copy.pqt>                         load + save (no GPU)
 //   dropin_main query <index.pqt> <queries.f32> <dim> <k> <out.bin> [db.f32]
 //                                                      load (+ attach_database) + knn_query_batch
+//   dropin_main sharded <index.pqt> <queries.f32> <dim> <k> <out.bin>
+//                                  pqt::ShardedIndex over a one-rank NCCL communicator
 //   dropin_main stages <index.pqt> <queries.f32> <dim> <max_bins> <out.bin>
 //                                  per query: traverse, pick_slope_table, heuristic_order,
 //                                  dijkstra_order, line_distance of stored codes 0..7; then
@@ -21,6 +23,7 @@
 #include "pqt/linequant.hpp"
 #include "pqt/pqtree.hpp"
 #include "pqt/search.hpp"
+#include "pqt/sharded.hpp"
 
 template <class T>
 static void put(std::ofstream& o, const T* p, std::size_t n) {
@@ -116,6 +119,20 @@ int main(int argc, char** argv) {
         in.seekg(0);
         in.read(reinterpret_cast<char*>(db->data.data()), bytes);
         index.attach_database(db);
+    }
+    if (mode == "sharded") {
+        pqt::ShardedIndex sh(argv[2], 0, 1, pqt::ShardedIndex::nccl_unique_id(), 0, 64);
+        const std::vector<pqt::QueryResult> res = sh.knn_query_batch(q, k);
+        std::ofstream out(argv[6], std::ios::binary);
+        for (const auto& r : res) {
+            const std::uint32_t c = static_cast<std::uint32_t>(r.ids.size());
+            const std::uint64_t st[3] = {r.stats.bins_visited, r.stats.candidates, r.stats.exact_evals};
+            out.write(reinterpret_cast<const char*>(&c), 4);
+            out.write(reinterpret_cast<const char*>(st), sizeof st);
+            out.write(reinterpret_cast<const char*>(r.ids.data()), 4 * c);
+            out.write(reinterpret_cast<const char*>(r.dists.data()), 4 * c);
+        }
+        return 0;
     }
     std::vector<pqt::QueryResult> res = pqt::knn_query_batch(index, q, k);
     pqt::QueryResult one = pqt::knn_query(index, q.row(0), k);

@@ -36,6 +36,7 @@ def main():
     wl = bench.WORKLOADS[a.workload]
     k = wl["k"]
     hix, Qpool = bench.make_workload(a.workload, 7, 0, 1)
+    # the sweep goes to 100k queries: tile the pool
     sizes = [int(x) for x in a.sizes.split(",")]
     dev = DeviceIndex(hix, max_batch=max(sizes))
     dim = hix.config.dim
@@ -63,6 +64,7 @@ def main():
             e1.record(st)
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
+        stage = dev.stage_ms()  # [traverse, bin selection, re-rank + top-k, whole] of the last call
         hq = torch.from_numpy(Q).pin_memory()
         h_ids = torch.empty((B, k), dtype=torch.int32).pin_memory()
         h_d = torch.empty((B, k), dtype=torch.float32).pin_memory()
@@ -84,7 +86,8 @@ def main():
         line = {"workload": a.workload, "batch": B, "k": k, "reps": reps,
                 "device_ms": dmed, "device_p90_ms": float(np.percentile(ms, 90)),
                 "device_qps": B / dmed * 1e3, "e2e_ms": hmed, "e2e_p90_ms": float(np.percentile(hs, 90) * 1e3),
-                "e2e_qps": B / hmed * 1e3}
+                "e2e_qps": B / hmed * 1e3,
+                "stage_ms_last_call": {"traverse": stage[0], "binsel": stage[1], "rerank": stage[2], "total": stage[3]}}
         if not a.no_cpu and B in (1, 1000):
             from oracle.bindings import Ref
 
