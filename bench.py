@@ -637,7 +637,10 @@ def config_of(name: str, wl, args, world: int) -> dict:
     return {"workload": name, **wl["config"], "n": wl["n"], "queries_per_step": wl["nq"], "k": wl["k"],
             "index": index_kind(wl, args), "exact_rerank": bool(args.exact),
             "l2": "flushed between timed steps (256 MiB write)" if not args.no_flush else "not flushed",
-            "parallelism": (f"position shards x{world} (NCCL broadcast + all-gather + merge)"
+            "parallelism": (f"rank 0 of {args.sim_ranks} position shards, peers simulated on this GPU "
+                            "(pqtg_sharded_create_sim)" if getattr(args, "sim_ranks", 0) else
+                            f"position shards x{world} (query-partitioned: block traversal + bin selection, "
+                            "range-list all-gather, shard re-rank, all-to-all merge; NCCL)"
                             if args.shard else f"replicas x{world}")}
 
 
@@ -716,6 +719,9 @@ def main():
                     help="who builds an unsharded workload's index: the reference on the CPU (pqtref "
                          "IndexBuilder, cached PQTINDEX file, default) or the GPU builder (quick runs)")
     ap.add_argument("--build-index-only", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--sim-ranks", type=int, default=0,
+                    help="sharded workloads on one GPU: time rank 0 of this many GPUs, the peers simulated "
+                         "(pqtg_sharded_create_sim; their transfers become device copies)")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--batches", type=int, default=4, help="distinct query batches cycled over steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -783,7 +789,16 @@ def main():
     _GPU_POOL[0] = len(Qpool)
     lib().pqtg_set_kernel_variant(args.variant)
     t_load = time.time()
-    if args.shard:
+    if args.sim_ranks:
+        from paper_1702_05911_b200.sharded import SimShardedIndex
+
+        if world != 1 or "shards" not in wl or args.sim_ranks != wl["shards"]:
+            raise SystemExit(f"--sim-ranks needs one process and a sharded workload built for that many shards")
+        args.shard = True  # the sharded step, on a simulated deployment
+        sh = SimShardedIndex(hix, 0, args.sim_ranks, device=local, max_batch=nq)
+        dev = sh.local
+        batches = [Qpool[b * nq:(b + 1) * nq] for b in range(args.batches)]
+    elif args.shard:
         from paper_1702_05911_b200.sharded import ShardedIndex
 
         sh = ShardedIndex(str(ipath) if ref_built else hix, device=local, max_batch=nq)
@@ -918,7 +933,7 @@ def main():
     e2e_value, h2d, d2h, link = run_e2e()
 
     shard_cpu = shard_par = None
-    if "shards" in wl and not args.no_cpu_baseline:  # every rank checks its own shard
+    if "shards" in wl and not args.no_cpu_baseline and not args.sim_ranks:  # every rank checks its own shard
         shard_cpu, shard_par = shard_parity(args, hix, batches[0], step, d_ids, d_dists, d_counts, d_stats, world,
                                             rank)
 
@@ -978,6 +993,9 @@ def main():
     sharded_wl = "shards" in wl
     if sharded_wl:
         cpu, parity = shard_cpu, shard_par
+        if args.sim_ranks:
+            parity = {"ok": None, "what": "simulated peers: outputs outside rank 0's query block are stand-ins "
+                                          "(the protocol's parity: tests/test_gpu_sharded.py)"}
     if world == 1 and not args.no_cpu_baseline and not sharded_wl:
         step(0)
         torch.cuda.synchronize()

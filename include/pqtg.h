@@ -282,6 +282,15 @@ int pqtg_sharded_create_nccl(pqtg_index* shard, const uint8_t* nccl_id, uint32_t
  * on any devices. Borrowed. */
 int pqtg_sharded_create_local(pqtg_index* const* shards, uint32_t world, uint64_t max_batch,
                               pqtg_sharded** out);
+/* Measurement harness: ONE real rank -- global rank `rank` of a `world`-GPU deployment, holding
+ * its shard -- whose peers are simulated: the first search of a batch computes every block's
+ * traversal + bin selection on this GPU (the peers' contributions), later searches of the same
+ * batch run this rank's real device work (its block, the re-rank of the whole batch over its
+ * shard, the merge of its block) with each transfer replaced by a device copy of the same bytes.
+ * Results are this rank's; the other blocks' outputs are stand-ins. Used by bench.py
+ * --sim-ranks to time a rank of the 8-GPU SIFT1B step on one GPU. */
+int pqtg_sharded_create_sim(pqtg_index* shard, uint32_t rank, uint32_t world, uint64_t max_batch,
+                            pqtg_sharded** out);
 /* Ranks this handle drives: 1 (NCCL) or world (local). */
 int pqtg_sharded_local_ranks(const pqtg_sharded* sh);
 /* The workspace a local rank searched its last batch in (borrowed; pqtg_workspace_read gives

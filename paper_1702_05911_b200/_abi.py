@@ -120,6 +120,7 @@ SIGNATURES = {
     "pqtg_sharded_create_nccl": (C.c_int, [_vp, _vp, _u32, _u32, _u64, C.POINTER(_vp)]),
     "pqtg_sharded_create_local": (C.c_int, [C.POINTER(_vp), _u32, _u64, C.POINTER(_vp)]),
     "pqtg_sharded_local_ranks": (C.c_int, [_vp]),
+    "pqtg_sharded_create_sim": (C.c_int, [_vp, _u32, _u32, _u64, C.POINTER(_vp)]),
     "pqtg_sharded_workspace": (_vp, [_vp, _u32]),
     "pqtg_sharded_search_device": (C.c_int, [_vp, C.POINTER(_vp), _u64, _u32, C.c_int, C.POINTER(_vp),
                                              C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),

@@ -64,6 +64,11 @@ WsSlice Workspace::slice(uint64_t q0) const {
     s.ntuples = ntuples + q0;
     s.err = err;
     s.keys = keys ? keys + q0 * std::max<uint64_t>(p.budget, 1) : nullptr;
+    s.split_ids = split_ids;
+    s.split_dists = split_dists;
+    s.split_counts = split_counts;
+    s.split_q = split_q;
+    s.split_k = split_k;
     s.hash = hash ? hash + q0 * hash_stride : nullptr;
     s.scr = scr ? scr + q0 * p.P * p.scr_nj : nullptr;
     return s;
@@ -151,6 +156,16 @@ uint32_t exact_prefix(const DevParams& p, uint32_t k) {
 void ensure_keys(Workspace& ws, uint32_t k) {
     const DevParams& p = ws.index->prm;
     const uint32_t kk = (p.db && p.rerank_exact > 0 && k) ? exact_prefix(p, k) : k;
+    // the split re-rank of small batches: per-(slice, query) lists
+    const uint64_t sq = std::min<uint64_t>(ws.max_batch, kSplitBelow);
+    if (kk && rerank_split(p, 1, kk) > 1 && (ws.split_k < kk || ws.split_q < sq)) {
+        ws.split_ids = dev_alloc<uint32_t>(ws.allocations, (uint64_t)kSplitMax * sq * kk);
+        ws.split_dists = dev_alloc<float>(ws.allocations, (uint64_t)kSplitMax * sq * kk);
+        ws.split_counts = dev_alloc<uint32_t>(ws.allocations, (uint64_t)kSplitMax * sq);
+        ws.split_q = sq;
+        ws.split_k = kk;
+        ++ws.gen;
+    }
     if (ws.keys || kk == 0 || !rerank_needs_gkeys(p, kk)) return;
     ws.keys = dev_alloc<uint64_t>(ws.allocations, ws.max_batch * std::max<uint64_t>(p.budget, 1));
     ++ws.gen;

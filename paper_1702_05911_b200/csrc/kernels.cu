@@ -940,12 +940,79 @@ __global__ void merge_topk_kernel(uint32_t G, uint64_t nq, uint32_t k, const uin
     out_counts[q] = out;
 }
 
+// Parallel merge of G sorted lists per query (one CTA per query): each element's output rank is
+// its index in its own list plus, per other list, the number of that list's keys below it (a
+// binary search; keys are (dist, id) with distinct ids, so ranks are distinct); elements of rank
+// < k are written at their rank. O(G k log k / threads) instead of the sequential k-step walk.
+constexpr int kMergeThreads = 256;
+
+__global__ void __launch_bounds__(kMergeThreads) merge_ranked_kernel(uint32_t G, uint64_t nq, uint32_t k,
+                                                                     const uint32_t* __restrict__ ids,
+                                                                     const float* __restrict__ dists,
+                                                                     const uint32_t* __restrict__ counts,
+                                                                     uint32_t* __restrict__ out_ids,
+                                                                     float* __restrict__ out_dists,
+                                                                     uint32_t* __restrict__ out_counts) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // [G][k]
+    __shared__ uint32_t cnt[16];
+    const uint64_t q = blockIdx.x;
+    if (threadIdx.x < G) cnt[threadIdx.x] = min(counts[(uint64_t)threadIdx.x * nq + q], k);
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < G * k; e += blockDim.x) {
+        const uint32_t g = e / k, i = e - g * k;
+        if (i < cnt[g]) {
+            const uint64_t off = ((uint64_t)g * nq + q) * k + i;
+            keys[e] = ((uint64_t)orderable(dists[off]) << 32) | ids[off];
+        }
+    }
+    __syncthreads();
+    uint32_t total = 0;
+    for (uint32_t g = 0; g < G; ++g) total += cnt[g];
+    const uint32_t kk = total < k ? total : k;
+    for (uint32_t e = threadIdx.x; e < G * k; e += blockDim.x) {
+        const uint32_t g = e / k, i = e - g * k;
+        if (i >= cnt[g] || i >= kk) continue;  // an element at index >= kk of its list ranks >= kk
+        const uint64_t key = keys[e];
+        uint32_t rank = i;
+        for (uint32_t h = 0; h < G && rank < kk; ++h) {
+            if (h == g) continue;
+            const uint64_t* l = keys + (uint64_t)h * k;
+            uint32_t lo = 0, hi = cnt[h];  // keys of list h below `key`
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (l[mid] < key) lo = mid + 1; else hi = mid;
+            }
+            rank += lo;
+        }
+        if (rank < kk) {
+            out_ids[q * k + rank] = (uint32_t)(key & 0xFFFFFFFFu);
+            out_dists[q * k + rank] = unorderable((uint32_t)(key >> 32));
+        }
+    }
+    for (uint32_t i = kk + threadIdx.x; i < k; i += blockDim.x) {
+        out_ids[q * k + i] = 0xFFFFFFFFu;
+        out_dists[q * k + i] = __uint_as_float(0x7F800000u);
+    }
+    if (threadIdx.x == 0) out_counts[q] = kk;
+}
+
 void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids, const float* dists,
                   const uint32_t* counts, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
                   cudaStream_t s) {
     if (nq == 0) return;
-    const unsigned blocks = (unsigned)((nq + 127) / 128);
-    merge_topk_kernel<<<blocks, 128, 0, s>>>(shards, nq, k, ids, dists, counts, out_ids, out_dists, out_counts);
+    const size_t sm = (size_t)shards * k * 8;
+    if (k > 0 && sm + 1024 <= (size_t)optin_bytes()) {
+        static std::once_flag once[64];
+        int dev = 0;
+        PQTG_CUDA_CHECK(cudaGetDevice(&dev));
+        std::call_once(once[dev & 63], [] { allow_max_smem(merge_ranked_kernel); });
+        merge_ranked_kernel<<<(unsigned)nq, kMergeThreads, sm, s>>>(shards, nq, k, ids, dists, counts, out_ids,
+                                                                    out_dists, out_counts);
+    } else {
+        const unsigned blocks = (unsigned)((nq + 127) / 128);
+        merge_topk_kernel<<<blocks, 128, 0, s>>>(shards, nq, k, ids, dists, counts, out_ids, out_dists, out_counts);
+    }
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
 

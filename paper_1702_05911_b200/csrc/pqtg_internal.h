@@ -114,7 +114,15 @@ struct WsSlice {
     float* scr = nullptr;         // [q][P][scr_nj] tensor-core dot products (screen.cu)
     uint32_t* err = nullptr;      // the workspace's device error word (PQTG_WS_ERR_*), shared by all slices
     uint64_t* keys = nullptr;     // [q][budget] candidate keys when they do not fit shared memory, or null
+    // small batches: per-(slice, query) top-k lists of the split re-rank [kSplitMax][split_q][split_k]
+    uint32_t* split_ids = nullptr;
+    float* split_dists = nullptr;
+    uint32_t* split_counts = nullptr;
+    uint64_t split_q = 0, split_k = 0;
 };
+
+constexpr uint32_t kSplitMax = 16;     // CTAs per query of the split re-rank
+constexpr uint64_t kSplitBelow = 148;  // batches below one query per SM spread each query over CTAs
 
 // device error word bits (Workspace::err): set by kernels, cleared at the start of every search
 // call, reported by pqtg_search / pqtg_workspace_status / pqtg_workspace_stage_ms
@@ -138,6 +146,10 @@ struct Workspace {
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
     uint32_t* err = nullptr;      // [1] device error word (PQTG_WS_ERR_*)
     uint64_t* keys = nullptr;     // [B][budget] re-rank keys for budgets too large for shared memory
+    uint32_t* split_ids = nullptr;    // small-batch split re-rank lists (see WsSlice)
+    float* split_dists = nullptr;
+    uint32_t* split_counts = nullptr;
+    uint64_t split_q = 0, split_k = 0;
     float* scr = nullptr;         // [B][P][scr_nj] (y - mu_p) . c'' on the tensor cores (screen.cu)
     uint32_t* hash = nullptr;     // [B << ts_log2] visited slots, cleared on use (binsel_fast.cu)
     uint64_t hash_words = 0;
@@ -260,6 +272,7 @@ void configure_kernels(const DevParams& p, uint32_t k);
 // rerank_ij.cu (1-byte (i, j) pair codes, k1 <= 16, p_line in {16, 32, 64})
 bool rerank_ij_ok(const DevParams& p, uint32_t k);
 bool rerank_ij_gkeys(const DevParams& p, uint32_t k);  // its keys go to the workspace (large budgets)
+uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k);  // CTAs per query (1 = no split)
 bool rerank_needs_gkeys(const DevParams& p, uint32_t k);  // launch_rerank will use ws.keys
 int optin_bytes();  // the device's opt-in shared memory per block
 void configure_rerank_ij();

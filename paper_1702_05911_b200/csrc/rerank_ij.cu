@@ -356,6 +356,10 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     // wavefronts on DEEP-shaped codes, tools/bank_probe.py) for two conflict-free 4-byte reads.
     // λ = fl(q · fl(1/255)) with q = (2^23 + q) − 2^23 built from the code byte by one byte
     // permute (exact for q <= 255) instead of an I2F.
+    // this CTA's slice of the query's candidates: all of them, or 1/gridDim.y of them when a small
+    // batch spreads each query over several CTAs (the slices' top-k lists are merged afterwards)
+    const uint32_t jlo = (uint32_t)((uint64_t)Cn * blockIdx.y / gridDim.y);
+    const uint32_t jhi = (uint32_t)((uint64_t)Cn * (blockIdx.y + 1) / gridDim.y);
     auto score2 = [&](uint32_t ja, const uint4* va, uint32_t ida, uint32_t jb, const uint4* vb, uint32_t idb) {
         const uint32_t* wa = reinterpret_cast<const uint32_t*>(va);
         const uint32_t* wb = reinterpret_cast<const uint32_t*>(vb);
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
             ++mine;
         }
         keys[ja] = key;
-        if (jb < Cn) {
+        if (jb < jhi) {
             key = kSentinel;
             if (idb != kInvalid) {
                 const uint32_t od = orderable(tot.y);
@@ -415,11 +419,11 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     if constexpr (PK) {
         // candidates j and j + step of this thread together; both rows are loaded before scoring
         uint4 va[kVec], vb[kVec];
-        for (uint32_t j = tid; j < Cn; j += 2 * step) {
+        for (uint32_t j = jlo + tid; j < jhi; j += 2 * step) {
             const uint32_t j2 = j + step;
             uint32_t ida = kInvalid, idb = kInvalid;
             fetch(j, va, ida);
-            if (j2 < Cn) fetch(j2, vb, idb);
+            if (j2 < jhi) fetch(j2, vb, idb);
             score2(j, va, ida, j2, vb, idb);
         }
     } else if constexpr (DIRECT) {
@@ -427,20 +431,20 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
         // 64-register budget of two CTAs per SM has no room for a second)
         uint4 va[kVec];
         uint32_t ida = kInvalid;
-        for (uint32_t j = tid; j < Cn; j += step) {
+        for (uint32_t j = jlo + tid; j < jhi; j += step) {
             fetch(j, va, ida);
             score(j, va, ida);
         }
     } else {
         uint4 va[kVec], vb[kVec];
         uint32_t ida = kInvalid, idb = kInvalid;
-        if (tid < Cn) fetch(tid, va, ida);
-        for (uint32_t j = tid; j < Cn; j += 2 * step) {
+        if (jlo + tid < jhi) fetch(jlo + tid, va, ida);
+        for (uint32_t j = jlo + tid; j < jhi; j += 2 * step) {
             const uint32_t j2 = j + step;
-            if (j2 < Cn) fetch(j2, vb, idb);
+            if (j2 < jhi) fetch(j2, vb, idb);
             score(j, va, ida);
-            if (j2 >= Cn) break;
-            if (j2 + step < Cn) fetch(j2 + step, va, ida);
+            if (j2 >= jhi) break;
+            if (j2 + step < jhi) fetch(j2 + step, va, ida);
             score(j2, vb, idb);
         }
     }
@@ -463,9 +467,11 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     if (kk) {
         for (uint32_t i = tid; i < (1u << kSelBits); i += blockDim.x) hist[i] = 0;
         __syncthreads();
-        m = block_select_wide<kSelBits, kIjThreads>(keys, Cn, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap, wmax, s_sel);
+        m = block_select_wide<kSelBits, kIjThreads>(keys + jlo, jhi - jlo, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap,
+                                                    wmax, s_sel);
     }
-    block_sort_write(sel, m, kk, k, q, out_ids, out_dists, out_counts);
+    // one list per (slice, query): [slice][query][k]
+    block_sort_write(sel, m, kk, k, (uint64_t)blockIdx.y * gridDim.x + q, out_ids, out_dists, out_counts);
 }
 
 namespace {
@@ -549,8 +555,26 @@ void configure_rerank_ij() {
     allow<32, 32, true>(optin);
 }
 
+// CTAs per query: a batch below one query per SM spreads each query's candidates over up to
+// kSplitMax CTAs (their top-k lists merged by launch_merge), so a single query's 4096-candidate
+// re-rank does not run on one SM (PQTG_SPLIT=0 disables)
+uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k) {
+    static const bool off = [] {
+        const char* e = std::getenv("PQTG_SPLIT");
+        return e && std::strcmp(e, "0") == 0;
+    }();
+    if (off || nq == 0 || nq >= kSplitBelow || p.budget < 1024 || !rerank_ij_ok(p, k)) return 1;
+    const uint64_t s = (2 * kSplitBelow) / nq;
+    return (uint32_t)std::min<uint64_t>(kSplitMax, std::max<uint64_t>(1, std::min<uint64_t>(s, p.budget / 256)));
+}
+
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids, float* dists,
                       uint32_t* counts, cudaStream_t s) {
+    const uint32_t S = rerank_split(p, nq, k);
+    if (S > 1 && (!ws.split_ids || ws.split_k < k || ws.split_q < nq)) throw Error{PQTG_ERR_ARG, "workspace has no split lists"};
+    uint32_t* o_ids = S > 1 ? ws.split_ids : ids;
+    float* o_dists = S > 1 ? ws.split_dists : dists;
+    uint32_t* o_counts = S > 1 ? ws.split_counts : counts;
     const uint32_t kk = k < p.budget ? k : p.budget;
     const uint32_t cap = ij_sel_cap(kk);
     const bool gk = rerank_ij_gkeys(p, k);
@@ -558,8 +582,8 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     const size_t sm = ij_smem(p, k, gk);
     uint64_t* gkeys = gk ? ws.keys : nullptr;
 #define PQTG_IJ(LT, K, D, ...)                                                                                \
-    rerank_ij_kernel<LT, K, D, ##__VA_ARGS__><<<(unsigned)nq, ij_threads(LT), sm, s>>>(                           \
-        p, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, ids, dists, counts, gkeys)
+    rerank_ij_kernel<LT, K, D, ##__VA_ARGS__><<<dim3((unsigned)nq, S), ij_threads(LT), sm, s>>>(                  \
+        p, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, o_ids, o_dists, o_counts, gkeys)
     if (code_k1m(p) == 32) {
         const bool direct = ij_direct(p);
         if (p.L == 16) {
@@ -582,6 +606,7 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     }
 #undef PQTG_IJ
     PQTG_CUDA_CHECK(cudaGetLastError());
+    if (S > 1) launch_merge(S, nq, k, o_ids, o_dists, o_counts, ids, dists, counts, s);
 }
 
 }  // namespace pqtg

@@ -151,6 +151,26 @@ struct Rank {
 struct pqtg_sharded {
     uint32_t world = 0;
     bool nccl = false;
+    // measurement harness (pqtg_sharded_create_sim): one real rank; the peers' pieces come from a
+    // one-time computation of the whole batch on this GPU, their transfers are device copies
+    bool sim = false;
+    struct SimCache {  // one per query batch seen (keyed by its device pointer and size)
+        const float* q = nullptr;
+        uint64_t nq = 0;
+        std::vector<void*> allocations;
+        float* fine = nullptr;
+        uint32_t* nranges = nullptr;
+        uint32_t* ncand = nullptr;
+        pqtg_query_stats* stats = nullptr;
+        uint2* packed = nullptr;
+        uint64_t* off = nullptr;
+        std::vector<uint64_t> total, toff;
+        ~SimCache() {
+            for (void* p : allocations) cudaFree(p);
+        }
+    };
+    std::vector<std::unique_ptr<SimCache>> simcs;
+    SimCache* simc = nullptr;  // the current batch's
     ncclComm_t comm = nullptr;
     uint64_t max_batch = 0, block_max = 0;
     uint64_t n = 0;
@@ -239,6 +259,50 @@ struct Piece {
     size_t bytes;
 };
 
+// the peers' inputs of a simulated step: traversal + bin selection of the WHOLE batch on this GPU,
+// each block's ranges packed as its owner would send them (done once per batch, outside timing)
+void sim_fill(pqtg_sharded& sh, Rank& r, const float* q, uint64_t nq, const std::vector<uint64_t>& blo,
+              const std::vector<uint64_t>& bn) {
+    for (auto& c : sh.simcs)
+        if (c->q == q && c->nq == nq) {
+            sh.simc = c.get();
+            return;
+        }
+    if (sh.simcs.size() >= 8) sh.simcs.erase(sh.simcs.begin());
+    sh.simcs.push_back(std::make_unique<pqtg_sharded::SimCache>());
+    auto& c = *sh.simcs.back();
+    const DevParams& p = r.ix->prm;
+    const uint32_t budget = std::max<uint32_t>(p.budget, 1);
+    PQTG_CUDA_CHECK(cudaSetDevice(r.ix->device));
+    c.fine = dev_alloc<float>(c.allocations, nq * p.L * p.k1);
+    c.nranges = dev_alloc<uint32_t>(c.allocations, nq);
+    c.ncand = dev_alloc<uint32_t>(c.allocations, nq);
+    c.stats = dev_alloc<pqtg_query_stats>(c.allocations, nq);
+    c.off = dev_alloc<uint64_t>(c.allocations, nq + 1);
+    const WsSlice sl = r.ws().slice(0);
+    launch_traverse(p, q, nq, sl, r.stream);
+    launch_binsel(p, nq, sl, c.stats, r.stream);
+    PQTG_CUDA_CHECK(cudaMemcpyAsync(c.fine, r.ws().fine, nq * p.L * p.k1 * sizeof(float), cudaMemcpyDeviceToDevice, r.stream));
+    PQTG_CUDA_CHECK(cudaMemcpyAsync(c.nranges, r.ws().nranges, nq * 4, cudaMemcpyDeviceToDevice, r.stream));
+    PQTG_CUDA_CHECK(cudaMemcpyAsync(c.ncand, r.ws().ncand, nq * 4, cudaMemcpyDeviceToDevice, r.stream));
+    launch_scan_counts(c.nranges, nq, c.off, r.stream);
+    std::vector<uint64_t> off(nq + 1);
+    PQTG_CUDA_CHECK(cudaMemcpyAsync(off.data(), c.off, (nq + 1) * 8, cudaMemcpyDeviceToHost, r.stream));
+    PQTG_CUDA_CHECK(cudaStreamSynchronize(r.stream));
+    c.packed = dev_alloc<uint2>(c.allocations, std::max<uint64_t>(off[nq], 1));
+    launch_pack_ranges(r.ws().ranges, budget, c.nranges, c.off, nq, c.packed, r.stream);
+    PQTG_CUDA_CHECK(cudaStreamSynchronize(r.stream));
+    c.total.assign(sh.world, 0);
+    c.toff.assign(sh.world + 1, 0);
+    for (uint32_t g = 0; g < sh.world; ++g) {
+        c.total[g] = off[blo[g] + bn[g]] - off[blo[g]];
+        c.toff[g] = off[blo[g]];
+    }
+    c.q = q;
+    c.nq = nq;
+    sh.simc = &c;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- the search
@@ -319,7 +383,7 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
     };
 
     // queries from global rank 0
-    if (bcast && G > 1) {
+    if (bcast && G > 1 && !sh.sim) {
         gather([&](Rank& self, uint32_t root) -> Piece {
             const uint32_t i = rank_index(self);
             float* q = const_cast<float*>(d_queries[i] ? d_queries[i] : self.q);
@@ -342,6 +406,15 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             }
         }
     } else {
+        if (sh.sim) {
+            std::vector<uint64_t> blo(G), bn(G);
+            for (uint32_t g = 0; g < G; ++g) {
+                blo[g] = blk[g].lo;
+                bn[g] = blk[g].n;
+            }
+            sim_fill(sh, *sh.ranks[0], qptr(0), nq, blo, bn);
+            PQTG_CUDA_CHECK(cudaEventRecord(sh.ranks[0]->ev[0], sh.ranks[0]->stream));
+        }
         // S1 + S2: this block's traversal, bin selection and packed ranges
         for (uint32_t i = 0; i < R; ++i) {
             Rank& r = *sh.ranks[i];
@@ -360,7 +433,13 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
         }
         // S3: packed sizes (host round trip)
         std::vector<uint64_t> total(G, 0);
-        if (nc) {
+        if (sh.sim) {
+            Rank& r = *sh.ranks[0];
+            PQTG_CUDA_CHECK(cudaMemcpyAsync(r.h_totals, r.blk_off + blk[r.g].n, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                            r.stream));
+            PQTG_CUDA_CHECK(cudaStreamSynchronize(r.stream));
+            for (uint32_t g = 0; g < G; ++g) total[g] = g == r.g ? r.h_totals[0] : sh.simc->total[g];
+        } else if (nc) {
             Rank& r = *sh.ranks[0];
             on(r);
             const Block b = blk[r.g];
@@ -384,6 +463,27 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
         std::vector<uint64_t> toff(G + 1, 0);
         for (uint32_t g = 0; g < G; ++g) toff[g + 1] = toff[g] + total[g];
         for (auto& rp : sh.ranks) ensure_all_packed(*rp, toff[G]);
+        if (sh.sim) {  // S4 simulated: every peer's piece arrives as a device copy of its bytes
+            Rank& r = *sh.ranks[0];
+            auto& c = *sh.simc;
+            const cudaStream_t st = r.stream;
+            for (uint32_t g = 0; g < G; ++g) {
+                const Block b = blk[g];
+                if (g == r.g) {
+                    PQTG_CUDA_CHECK(cudaMemcpyAsync(r.all_packed + toff[g], r.packed, total[g] * sizeof(uint2),
+                                                    cudaMemcpyDeviceToDevice, st));
+                    continue;
+                }
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.ws().fine + b.lo * L * k1, c.fine + b.lo * L * k1,
+                                                b.n * L * k1 * sizeof(float), cudaMemcpyDeviceToDevice, st));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.ws().nranges + b.lo, c.nranges + b.lo, b.n * 4, cudaMemcpyDeviceToDevice, st));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.ws().ncand + b.lo, c.ncand + b.lo, b.n * 4, cudaMemcpyDeviceToDevice, st));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(stats_of(0) + b.lo, c.stats + b.lo, b.n * sizeof(pqtg_query_stats),
+                                                cudaMemcpyDeviceToDevice, st));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.all_packed + toff[g], c.packed + c.toff[g], total[g] * sizeof(uint2),
+                                                cudaMemcpyDeviceToDevice, st));
+            }
+        } else {
         // S4: the blocks' fine LUTs, counters, stats and packed ranges to every rank
         gather([&](Rank& self, uint32_t root) -> Piece {
             const Block b = blk[root];
@@ -404,6 +504,7 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
         gather([&](Rank& self, uint32_t root) -> Piece {
             return Piece{self.g == root ? self.packed : nullptr, self.all_packed + toff[root], total[root] * sizeof(uint2)};
         });
+        }
         // S5 + S6: the whole batch's ranges, then the re-rank of this shard's candidates
         for (uint32_t i = 0; i < R; ++i) {
             Rank& r = *sh.ranks[i];
@@ -419,7 +520,18 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             if (i == 0) PQTG_CUDA_CHECK(cudaEventRecord(r.ev[3], r.stream));
         }
         // S7: all-to-all of the local lists by query block
-        if (nc) {
+        if (sh.sim) {  // the peers' lists of this block: stand-ins of the same size (this rank's own)
+            Rank& r = *sh.ranks[0];
+            const Block mine = blk[r.g];
+            for (uint32_t j = 0; j < G && mine.n; ++j) {
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.r_ids + (uint64_t)j * mine.n * k, r.l_ids + mine.lo * k,
+                                                mine.n * k * sizeof(uint32_t), cudaMemcpyDeviceToDevice, r.stream));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.r_dists + (uint64_t)j * mine.n * k, r.l_dists + mine.lo * k,
+                                                mine.n * k * sizeof(float), cudaMemcpyDeviceToDevice, r.stream));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.r_counts + (uint64_t)j * mine.n, r.l_counts + mine.lo,
+                                                mine.n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, r.stream));
+            }
+        } else if (nc) {
             Rank& r = *sh.ranks[0];
             on(r);
             const Block mine = blk[r.g];
@@ -467,6 +579,18 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
                              d_counts[i] + b.lo, r.stream);
         }
         // S9: the merged blocks to every rank
+        if (sh.sim) {  // the peers' merged blocks arrive: stand-in copies of the same bytes
+            Rank& r = *sh.ranks[0];
+            const Block mine = blk[r.g];
+            for (uint32_t g = 0; g < G; ++g) {
+                const Block b = blk[g];
+                if (g == r.g || !b.n || !mine.n) continue;
+                const uint64_t n = std::min(b.n, mine.n);
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(d_ids[0] + b.lo * k, d_ids[0] + mine.lo * k, n * k * 4, cudaMemcpyDeviceToDevice, r.stream));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(d_dists[0] + b.lo * k, d_dists[0] + mine.lo * k, n * k * 4, cudaMemcpyDeviceToDevice, r.stream));
+                PQTG_CUDA_CHECK(cudaMemcpyAsync(d_counts[0] + b.lo, d_counts[0] + mine.lo, n * 4, cudaMemcpyDeviceToDevice, r.stream));
+            }
+        } else {
         gather([&](Rank& self, uint32_t root) -> Piece {
             const Block b = blk[root];
             return Piece{nullptr, d_ids[rank_index(self)] + b.lo * k, b.n * k * sizeof(uint32_t)};
@@ -479,6 +603,7 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             const Block b = blk[root];
             return Piece{nullptr, d_counts[rank_index(self)] + b.lo, b.n * sizeof(uint32_t)};
         });
+        }
     }
     // the caller's streams continue after the search
     for (uint32_t i = 0; i < R; ++i) {
@@ -578,6 +703,33 @@ int pqtg_sharded_create_local(pqtg_index* const* shards, uint32_t world, uint64_
             setup_rank(*sh, *r);
             sh->ranks.push_back(std::move(r));
         }
+        *out = sh.release();
+        return PQTG_OK;
+    });
+}
+
+int pqtg_sharded_create_sim(pqtg_index* shard, uint32_t rank, uint32_t world, uint64_t max_batch, pqtg_sharded** out) {
+    return guarded_sh([&] {
+        if (!shard || !out || world == 0 || world > 16 || rank >= world || max_batch == 0)
+            throw Error{PQTG_ERR_ARG, "bad sharded arguments"};
+        *out = nullptr;
+        DevIndex& ix = *shard->dev;
+        check_shard(ix, world, rank);
+        auto sh = std::make_unique<pqtg_sharded>();
+        sh->world = world;
+        sh->sim = true;
+        sh->max_batch = max_batch;
+        sh->block_max = (max_batch + world - 1) / world;
+        sh->n = ix.n;
+        sh->D = ix.prm.D;
+        sh->L = ix.prm.L;
+        sh->k1 = ix.prm.k1;
+        sh->budget = ix.prm.budget;
+        auto r = std::make_unique<Rank>();
+        r->g = rank;
+        r->ix = &ix;
+        setup_rank(*sh, *r);
+        sh->ranks.push_back(std::move(r));
         *out = sh.release();
         return PQTG_OK;
     });

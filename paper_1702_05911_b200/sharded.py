@@ -180,3 +180,26 @@ class LocalShardedIndex(_Handle):
         except PqtgError as e:
             _raise(e)
         return ids[:, :k], dists[:, :k], counts, stats
+
+
+class SimShardedIndex(_Handle):
+    """Measurement harness (pqtg_sharded_create_sim): global rank `rank` of a `world`-GPU
+    deployment on this one GPU, its peers simulated (their traversal + bin selection computed
+    once per batch here, their transfers replaced by device copies of the same bytes). Only this
+    rank's device work is timed; results outside its query block are stand-ins."""
+
+    def __init__(self, source, rank: int, world: int, device: int = 0, max_batch: int = 4096):
+        self.world, self.rank, self.device = world, rank, device
+        self.local = load_shard(source, world, rank, device, 1)
+        sh = _vp()
+        try:
+            check(lib().pqtg_sharded_create_sim(self.local.handle, rank, world, max_batch, C.byref(sh)))
+        except PqtgError as e:
+            _raise(e)
+        self._sh = sh
+
+    def search(self, d_queries, k, out_ids, out_dists, out_counts, d_stats=None, broadcast=False) -> None:
+        self._nq = int(d_queries.shape[0])
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._search([d_queries.data_ptr()], k, [out_ids.data_ptr()], [out_dists.data_ptr()],
+                     [out_counts.data_ptr()], [d_stats.data_ptr() if d_stats is not None else None], [stream], False)
