@@ -313,7 +313,21 @@ void launch_traverse_screen(const DevParams& p, const float* queries, uint64_t n
 int kernel_variant();
 // grow a workspace's k-dependent buffers (exact prefix, HBM candidate keys) before a search
 void prepare_workspace(Workspace& ws, uint32_t k);
-// sharded_kernels.cu: dense per-query range lists of the query-partitioned sharded search
+// sharded_kernels.cu: dense per-query range lists of the query-partitioned sharded search, and
+// the batch's fine LUTs recomputed on every rank
+void launch_fine_lut(const DevParams& p, const float* queries, uint64_t nq, float* fine, cudaStream_t s);
+struct CopySegment {
+    void* dst;
+    const void* src;
+    uint64_t bytes;  // multiple of 4, 4-byte aligned pointers
+};
+constexpr uint32_t kCopySegmentsMax = 64;
+struct CopySegments {
+    uint32_t n;
+    CopySegment s[kCopySegmentsMax];
+};
+// device-to-device copies of one device's buffers in one launch per 64 segments
+void launch_copy_segments(const std::vector<CopySegment>& segs, cudaStream_t s);
 void launch_scan_counts(const uint32_t* cnt, uint64_t n, uint64_t* off, cudaStream_t s);
 void launch_pack_ranges(const uint2* ranges, uint32_t stride, const uint32_t* cnt, const uint64_t* off, uint64_t n,
                         uint2* dense, cudaStream_t s);

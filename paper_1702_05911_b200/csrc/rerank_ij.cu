@@ -555,13 +555,14 @@ void configure_rerank_ij() {
     allow<32, 32, true>(optin);
 }
 
-// CTAs per query: a batch below one query per SM spreads each query's candidates over up to
-// kSplitMax CTAs (their top-k lists merged by launch_merge), so a single query's 4096-candidate
-// re-rank does not run on one SM (PQTG_SPLIT=0 disables)
+// CTAs per query: a batch below one query per SM can spread each query's candidates over up to
+// kSplitMax CTAs (their top-k lists merged by launch_merge) -- opt-in (PQTG_SPLIT=1): at batch 1
+// the re-rank is bound by its serial prologue / selection, not its candidate loop, and the split
+// measured slower (SIFT1M batch 1: 33.9 vs 25.6 us, profiles/r02/latency.md)
 uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k) {
     static const bool off = [] {
         const char* e = std::getenv("PQTG_SPLIT");
-        return e && std::strcmp(e, "0") == 0;
+        return !(e && std::strcmp(e, "1") == 0);
     }();
     if (off || nq == 0 || nq >= kSplitBelow || p.budget < 1024 || !rerank_ij_ok(p, k)) return 1;
     const uint64_t s = (2 * kSplitBelow) / nq;

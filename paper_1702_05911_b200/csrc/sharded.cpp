@@ -13,8 +13,9 @@
 //   S1  rank g: traversal + bin selection of block g (its workspace rows [lo_g, hi_g));
 //   S2  rank g: its block's range lists packed densely (scan of nranges, gather);
 //   S3  the packed sizes are all-gathered (the only host round trip of the call);
-//   S4  all-gather-v of the blocks' fine LUTs, nranges, ncand, stats and packed ranges;
-//   S5  every rank unpacks the whole batch's ranges into its workspace;
+//   S4  all-gather-v of the blocks' nranges, ncand, stats and packed ranges;
+//   S5  every rank recomputes the batch's fine LUTs (L·k1·fd multiply-adds per query: cheaper
+//       than moving 4·L·k1 bytes per query) and unpacks the whole batch's ranges;
 //   S6  every rank re-ranks the batch's candidates inside its position range (local top-k);
 //   S7  all-to-all: rank j receives every rank's lists of block j;
 //   S8  rank j merges them by (dist, id) (candidate_less, search.cpp:39-41);
@@ -158,7 +159,6 @@ struct pqtg_sharded {
         const float* q = nullptr;
         uint64_t nq = 0;
         std::vector<void*> allocations;
-        float* fine = nullptr;
         uint32_t* nranges = nullptr;
         uint32_t* ncand = nullptr;
         pqtg_query_stats* stats = nullptr;
@@ -274,7 +274,6 @@ void sim_fill(pqtg_sharded& sh, Rank& r, const float* q, uint64_t nq, const std:
     const DevParams& p = r.ix->prm;
     const uint32_t budget = std::max<uint32_t>(p.budget, 1);
     PQTG_CUDA_CHECK(cudaSetDevice(r.ix->device));
-    c.fine = dev_alloc<float>(c.allocations, nq * p.L * p.k1);
     c.nranges = dev_alloc<uint32_t>(c.allocations, nq);
     c.ncand = dev_alloc<uint32_t>(c.allocations, nq);
     c.stats = dev_alloc<pqtg_query_stats>(c.allocations, nq);
@@ -282,7 +281,6 @@ void sim_fill(pqtg_sharded& sh, Rank& r, const float* q, uint64_t nq, const std:
     const WsSlice sl = r.ws().slice(0);
     launch_traverse(p, q, nq, sl, r.stream);
     launch_binsel(p, nq, sl, c.stats, r.stream);
-    PQTG_CUDA_CHECK(cudaMemcpyAsync(c.fine, r.ws().fine, nq * p.L * p.k1 * sizeof(float), cudaMemcpyDeviceToDevice, r.stream));
     PQTG_CUDA_CHECK(cudaMemcpyAsync(c.nranges, r.ws().nranges, nq * 4, cudaMemcpyDeviceToDevice, r.stream));
     PQTG_CUDA_CHECK(cudaMemcpyAsync(c.ncand, r.ws().ncand, nq * 4, cudaMemcpyDeviceToDevice, r.stream));
     launch_scan_counts(c.nranges, nq, c.off, r.stream);
@@ -318,7 +316,7 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             throw Error{PQTG_ERR_ARG, "null argument"};
     if (nq == 0) return;
     const std::vector<Block> blk = blocks_of(nq, G);
-    const uint32_t D = sh.D, L = sh.L, k1 = sh.k1, budget = sh.budget;
+    const uint32_t D = sh.D, budget = sh.budget;
     const uint64_t kk = std::max<uint32_t>(k, 1);
     Nccl* nc = sh.nccl ? &Nccl::get() : nullptr;
     auto caller = [&](uint32_t i) -> cudaStream_t {
@@ -350,6 +348,17 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             if (o.get() != &dst) PQTG_CUDA_CHECK(cudaStreamWaitEvent(dst.stream, o->done, 0));
     };
     auto mark = [&](Rank& r) { PQTG_CUDA_CHECK(cudaEventRecord(r.done, r.stream)); };
+    // local transport: one copy kernel when every rank lives on one device, else peer memcpys
+    bool one_device = true;
+    for (auto& rp : sh.ranks) one_device = one_device && rp->ix->device == sh.ranks[0]->ix->device;
+    auto copies = [&](Rank& dst, const std::vector<CopySegment>& cs) {
+        if (one_device) {
+            launch_copy_segments(cs, dst.stream);
+            return;
+        }
+        for (const auto& c : cs)
+            PQTG_CUDA_CHECK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, dst.stream));
+    };
     // all-gather-v of per-root pieces
     auto gather = [&](auto piece_of /* (Rank& self, uint32_t root) -> Piece */) {
         if (nc) {
@@ -370,14 +379,16 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             Rank& dst = *rp;
             on(dst);
             wait_all(dst);
+            std::vector<CopySegment> cs;
             for (auto& sp : sh.ranks) {
                 Rank& src = *sp;
                 const Piece mine = piece_of(src, src.g);  // the root's own view of its piece
                 const Piece there = piece_of(dst, src.g);
                 const void* from = mine.src ? mine.src : mine.dst;
                 if (from == there.dst || there.bytes == 0) continue;
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(there.dst, from, there.bytes, cudaMemcpyDefault, dst.stream));
+                cs.push_back({there.dst, from, there.bytes});
             }
+            copies(dst, cs);
         }
         for (auto& rp : sh.ranks) mark(*rp);
     };
@@ -466,29 +477,21 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
         if (sh.sim) {  // S4 simulated: every peer's piece arrives as a device copy of its bytes
             Rank& r = *sh.ranks[0];
             auto& c = *sh.simc;
-            const cudaStream_t st = r.stream;
+            std::vector<CopySegment> cs;
             for (uint32_t g = 0; g < G; ++g) {
                 const Block b = blk[g];
                 if (g == r.g) {
-                    PQTG_CUDA_CHECK(cudaMemcpyAsync(r.all_packed + toff[g], r.packed, total[g] * sizeof(uint2),
-                                                    cudaMemcpyDeviceToDevice, st));
+                    cs.push_back({r.all_packed + toff[g], r.packed, total[g] * sizeof(uint2)});
                     continue;
                 }
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.ws().fine + b.lo * L * k1, c.fine + b.lo * L * k1,
-                                                b.n * L * k1 * sizeof(float), cudaMemcpyDeviceToDevice, st));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.ws().nranges + b.lo, c.nranges + b.lo, b.n * 4, cudaMemcpyDeviceToDevice, st));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.ws().ncand + b.lo, c.ncand + b.lo, b.n * 4, cudaMemcpyDeviceToDevice, st));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(stats_of(0) + b.lo, c.stats + b.lo, b.n * sizeof(pqtg_query_stats),
-                                                cudaMemcpyDeviceToDevice, st));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.all_packed + toff[g], c.packed + c.toff[g], total[g] * sizeof(uint2),
-                                                cudaMemcpyDeviceToDevice, st));
+                cs.push_back({r.ws().nranges + b.lo, c.nranges + b.lo, b.n * 4});
+                cs.push_back({r.ws().ncand + b.lo, c.ncand + b.lo, b.n * 4});
+                cs.push_back({stats_of(0) + b.lo, c.stats + b.lo, b.n * sizeof(pqtg_query_stats)});
+                cs.push_back({r.all_packed + toff[g], c.packed + c.toff[g], total[g] * sizeof(uint2)});
             }
+            launch_copy_segments(cs, r.stream);
         } else {
         // S4: the blocks' fine LUTs, counters, stats and packed ranges to every rank
-        gather([&](Rank& self, uint32_t root) -> Piece {
-            const Block b = blk[root];
-            return Piece{nullptr, self.ws().fine + b.lo * L * k1, b.n * L * k1 * sizeof(float)};
-        });
         gather([&](Rank& self, uint32_t root) -> Piece {
             const Block b = blk[root];
             return Piece{nullptr, self.ws().nranges + b.lo, b.n * sizeof(uint32_t)};
@@ -511,6 +514,7 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             on(r);
             if (i == 0) PQTG_CUDA_CHECK(cudaEventRecord(r.ev[2], r.stream));
             const DevParams& p = r.ix->prm;
+            launch_fine_lut(p, qptr(i), nq, r.ws().fine, r.stream);  // cheaper than exchanging the LUTs
             launch_scan_counts(r.ws().nranges, nq, r.all_off, r.stream);
             launch_unpack_ranges(r.all_packed, r.ws().nranges, r.all_off, nq, std::max<uint32_t>(budget, 1),
                                  r.ws().ranges, r.stream);
@@ -523,14 +527,13 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
         if (sh.sim) {  // the peers' lists of this block: stand-ins of the same size (this rank's own)
             Rank& r = *sh.ranks[0];
             const Block mine = blk[r.g];
+            std::vector<CopySegment> cs;
             for (uint32_t j = 0; j < G && mine.n; ++j) {
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.r_ids + (uint64_t)j * mine.n * k, r.l_ids + mine.lo * k,
-                                                mine.n * k * sizeof(uint32_t), cudaMemcpyDeviceToDevice, r.stream));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.r_dists + (uint64_t)j * mine.n * k, r.l_dists + mine.lo * k,
-                                                mine.n * k * sizeof(float), cudaMemcpyDeviceToDevice, r.stream));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(r.r_counts + (uint64_t)j * mine.n, r.l_counts + mine.lo,
-                                                mine.n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, r.stream));
+                cs.push_back({r.r_ids + (uint64_t)j * mine.n * k, r.l_ids + mine.lo * k, mine.n * k * sizeof(uint32_t)});
+                cs.push_back({r.r_dists + (uint64_t)j * mine.n * k, r.l_dists + mine.lo * k, mine.n * k * sizeof(float)});
+                cs.push_back({r.r_counts + (uint64_t)j * mine.n, r.l_counts + mine.lo, mine.n * sizeof(uint32_t)});
             }
+            launch_copy_segments(cs, r.stream);
         } else if (nc) {
             Rank& r = *sh.ranks[0];
             on(r);
@@ -557,16 +560,15 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
                 wait_all(dst);
                 const Block mine = blk[dst.g];
                 if (!mine.n) continue;
+                std::vector<CopySegment> cs;
                 for (auto& sp : sh.ranks) {
                     Rank& src = *sp;
                     const uint64_t j = src.g;
-                    PQTG_CUDA_CHECK(cudaMemcpyAsync(dst.r_ids + j * mine.n * k, src.l_ids + mine.lo * k,
-                                                    mine.n * k * sizeof(uint32_t), cudaMemcpyDefault, dst.stream));
-                    PQTG_CUDA_CHECK(cudaMemcpyAsync(dst.r_dists + j * mine.n * k, src.l_dists + mine.lo * k,
-                                                    mine.n * k * sizeof(float), cudaMemcpyDefault, dst.stream));
-                    PQTG_CUDA_CHECK(cudaMemcpyAsync(dst.r_counts + j * mine.n, src.l_counts + mine.lo,
-                                                    mine.n * sizeof(uint32_t), cudaMemcpyDefault, dst.stream));
+                    cs.push_back({dst.r_ids + j * mine.n * k, src.l_ids + mine.lo * k, mine.n * k * sizeof(uint32_t)});
+                    cs.push_back({dst.r_dists + j * mine.n * k, src.l_dists + mine.lo * k, mine.n * k * sizeof(float)});
+                    cs.push_back({dst.r_counts + j * mine.n, src.l_counts + mine.lo, mine.n * sizeof(uint32_t)});
                 }
+                copies(dst, cs);
             }
         }
         // S8: merge of this block
@@ -582,14 +584,16 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
         if (sh.sim) {  // the peers' merged blocks arrive: stand-in copies of the same bytes
             Rank& r = *sh.ranks[0];
             const Block mine = blk[r.g];
+            std::vector<CopySegment> cs;
             for (uint32_t g = 0; g < G; ++g) {
                 const Block b = blk[g];
                 if (g == r.g || !b.n || !mine.n) continue;
                 const uint64_t n = std::min(b.n, mine.n);
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(d_ids[0] + b.lo * k, d_ids[0] + mine.lo * k, n * k * 4, cudaMemcpyDeviceToDevice, r.stream));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(d_dists[0] + b.lo * k, d_dists[0] + mine.lo * k, n * k * 4, cudaMemcpyDeviceToDevice, r.stream));
-                PQTG_CUDA_CHECK(cudaMemcpyAsync(d_counts[0] + b.lo, d_counts[0] + mine.lo, n * 4, cudaMemcpyDeviceToDevice, r.stream));
+                cs.push_back({d_ids[0] + b.lo * k, d_ids[0] + mine.lo * k, n * k * 4});
+                cs.push_back({d_dists[0] + b.lo * k, d_dists[0] + mine.lo * k, n * k * 4});
+                cs.push_back({d_counts[0] + b.lo, d_counts[0] + mine.lo, n * 4});
             }
+            launch_copy_segments(cs, r.stream);
         } else {
         gather([&](Rank& self, uint32_t root) -> Piece {
             const Block b = blk[root];

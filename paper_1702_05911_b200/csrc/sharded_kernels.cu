@@ -7,9 +7,12 @@
 
 #include <cstdint>
 
+#include "common.cuh"
 #include "pqtg_internal.h"
 
 namespace pqtg {
+
+using dev::sq_step;
 
 namespace {
 
@@ -52,7 +55,60 @@ __global__ void __launch_bounds__(256) move_ranges_kernel(uint2* __restrict__ ro
     }
 }
 
+// fine_dists[q][f][i] = l2_sq(y_f, slice(f, i), fd) in the traversal's (and the reference's,
+// pqtree.cpp:90-93) sequential fp32 order: the sharded search recomputes the batch's fine LUTs on
+// every rank (L·k1·fd multiply-adds per query) instead of all-gathering them (4·L·k1 bytes per
+// query, 4 KB on the SIFT1B tree)
+__global__ void __launch_bounds__(256) fine_lut_kernel(DevParams p, const float* __restrict__ Q, float* __restrict__ fine) {
+    const uint64_t q = blockIdx.x;
+    const uint32_t L = p.L, k1 = p.k1, fd = p.fd;
+    const float* y = Q + q * p.D;
+    for (uint32_t idx = threadIdx.x; idx < L * k1; idx += blockDim.x) {
+        const uint32_t f = idx / k1, i = idx - f * k1;
+        const float* c = p.fine_t + (size_t)f * fd * k1 + i;
+        const float* yf = y + f * fd;
+        float acc = 0.0f;
+        for (uint32_t t = 0; t < fd; ++t, c += k1) acc = sq_step(acc, __ldg(yf + t), __ldg(c));
+        fine[q * L * k1 + idx] = acc;
+    }
+}
+
+// many small device-to-device copies in one launch (the local / simulated transports' stand-in
+// for one NCCL group): blockIdx.y = segment, 4-byte words, grid-stride over the segment
+__global__ void __launch_bounds__(256) copy_segments_kernel(CopySegments segs) {
+    const CopySegment sg = segs.s[blockIdx.y];
+    const uint32_t* src = static_cast<const uint32_t*>(sg.src);
+    uint32_t* dst = static_cast<uint32_t*>(sg.dst);
+    const uint64_t words = sg.bytes / 4;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = __ldg(src + i);
+}
+
 }  // namespace
+
+void launch_copy_segments(const std::vector<CopySegment>& segs, cudaStream_t s) {
+    for (size_t b = 0; b < segs.size(); b += kCopySegmentsMax) {
+        CopySegments batch{};
+        uint64_t most = 0;
+        for (size_t i = b; i < segs.size() && i < b + kCopySegmentsMax; ++i) {
+            const CopySegment& c = segs[i];
+            if ((c.bytes & 3) || (reinterpret_cast<uintptr_t>(c.src) & 3) || (reinterpret_cast<uintptr_t>(c.dst) & 3))
+                throw Error{PQTG_ERR_ARG, "copy segment not 4-byte aligned"};
+            batch.s[batch.n++] = c;
+            most = c.bytes > most ? c.bytes : most;
+        }
+        if (!batch.n || !most) continue;
+        const uint64_t blocks = (most / 4 + 1023) / 1024;
+        copy_segments_kernel<<<dim3((unsigned)(blocks < 64 ? (blocks ? blocks : 1) : 64), batch.n), 256, 0, s>>>(batch);
+        PQTG_CUDA_CHECK(cudaGetLastError());
+    }
+}
+
+void launch_fine_lut(const DevParams& p, const float* queries, uint64_t nq, float* fine, cudaStream_t s) {
+    if (nq == 0) return;
+    fine_lut_kernel<<<(unsigned)nq, 256, 0, s>>>(p, queries, fine);
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
 
 void launch_scan_counts(const uint32_t* cnt, uint64_t n, uint64_t* off, cudaStream_t s) {
     scan_counts_kernel<<<1, kScanThreads, 0, s>>>(cnt, n, off);

@@ -92,3 +92,30 @@ def test_local_sharded_sift1b_tree():
     lsi = LocalShardedIndex(hix, 8, max_batch=64)
     for r, got in enumerate(run_local(lsi, Q, 100, True)):
         assert_same_results(got, want, f"sift1b tree G=8 rank {r}")
+
+
+def test_gpu_split_rerank_opt_in():
+    """The small-batch split re-rank (PQTG_SPLIT=1: each query's candidates over up to 16 CTAs,
+    their lists merged by the parallel ranked merge) against the golden fixtures, in a fresh
+    process (the switch is read once)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np\n"
+        "from conftest import GOLDEN, load_golden\n"
+        "from test_gpu_parity import assert_same_results\n"
+        "from paper_1702_05911_b200 import DeviceIndex\n"
+        "for name in ['p2_sift', 'p4_gist', 'p2_wide']:\n"
+        "    g = load_golden(name)\n"
+        "    dev = DeviceIndex(str(GOLDEN / f'{name}.pqt'))\n"
+        "    for nq in (1, 5, len(g['queries'])):\n"
+        "        got = dev.search(g['queries'][:nq], int(g['k']))\n"
+        "        assert_same_results(got, tuple(x[:nq] for x in (g['ids'], g['dists'], g['counts'], g['stats'])), name)\n"
+        "print('ok')\n")
+    import os
+    from conftest import REPO
+
+    env = dict(os.environ, PQTG_SPLIT="1", PYTHONPATH=f"{REPO}:{REPO / 'tests'}")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=str(REPO / "tests"))
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

@@ -299,3 +299,4 @@ def test_gpu_sift1b_tree_small():
     mi, md, mc = merge_topk_host(np.stack([x[0] for x in parts]), np.stack([x[1] for x in parts]),
                                  np.stack([x[2] for x in parts]))
     assert_same_results((mi, md, mc, want[3]), want, "sift1b tree, 8 shards")
+
