@@ -384,6 +384,7 @@ __device__ __forceinline__ void binsel_fast_body(const DevParams& p, uint64_t q,
                 nvis = st.nvis;
                 spilled = st.spilled;
                 const uint32_t c = st.c, r = st.r, maxord = st.maxord;
+                __syncwarp();  // every lane read s_C / s_R / s_maxord above before lane 0 updates them
                 if (lane == 0) {
                     s_C = c;
                     s_R = r;

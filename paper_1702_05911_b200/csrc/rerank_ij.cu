@@ -137,17 +137,21 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 
 }  // namespace
 
-template <int LT, int K1M, bool DIRECT, bool PK = false>
+// MODE (K1M = 16): 0 = per-query table T[f][t] = (E, c2) (default); 1 = packed two-candidate loop
+// (PK); 2 = the scalar loop reading c2 by code and a2 = fine[f][j], E formed per candidate (C3).
+// Modes 1 and 2 use the c2-table layout (CT).
+template <int LT, int K1M, bool DIRECT, int MODE = 0>
 __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DIRECT)) ? 1 : 2)
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
                      float* __restrict__ out_dists, uint32_t* __restrict__ out_counts, uint64_t* __restrict__ gkeys) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE != 0;
     const uint32_t k1 = p.k1, budget = p.budget;
     constexpr uint32_t TE = t_entries(K1M);
-    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr, PK);
-    const IjLayout fix = ij_layout(LT, 0, 0, K1M, DIRECT, false, PK);
+    const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr, CT);
+    const IjLayout fix = ij_layout(LT, 0, 0, K1M, DIRECT, false, CT);
     float2* T = reinterpret_cast<float2*>(smem);
     // PK (packed, K1M = 16): c2 by device code, Ct[f][t] = d2[f][i][j], at a 1 KB-aligned shared
     // address, then the fine rows: the scoring loop forms each lookup's address with one LOP3
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     const uint32_t c2s = (s_base + 1023u) & ~1023u, fs = c2s + LT * 1024u;
     float* Ct = reinterpret_cast<float*>(smem + (c2s - s_base));
     uint16_t* jt = reinterpret_cast<uint16_t*>(smem);  // DIRECT: j of pair id
-    float* fine = PK ? reinterpret_cast<float*>(smem + (fs - s_base)) : reinterpret_cast<float*>(smem + fix.fine);
+    float* fine = CT ? reinterpret_cast<float*>(smem + (fs - s_base)) : reinterpret_cast<float*>(smem + fix.fine);
     // candidate keys: shared memory, or this query's row of the workspace's key buffer when the
     // budget is too large for shared memory (budget > ~8k)
     uint64_t* keys = gkeys ? gkeys + blockIdx.x * (uint64_t)budget : reinterpret_cast<uint64_t*>(smem + lay.keys);
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
             const uint32_t f = f0 + u * kFLanes;
             if (f < LT) {
                 const float b2 = fine[f * K1M + pi_i], a2 = fine[f * K1M + pi_j];
-                if constexpr (PK) {
+                if constexpr (CT) {
                     Ct[f * TE + ij] = c2v[u];
                 } else {
                     T[f * TE + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
@@ -330,6 +334,10 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
                 if constexpr (DIRECT) {  // E and c2 of this part, in T's roundings
                     const float a2 = fine[f * K1M + jt[ti]];
                     ec.y = __ldg(p.c2p + f * 512 + ti);
+                    ec.x = __fsub_rn(__fsub_rn(a2, b2), ec.y);
+                } else if constexpr (C3) {  // c2 by code, a2 = fine[f][j] with j = (t − i) & 15
+                    const float a2 = fine[f * K1M + ((ti - fi) & 15u)];
+                    ec.y = Ct[f * TE + ti];
                     ec.x = __fsub_rn(__fsub_rn(a2, b2), ec.y);
                 } else {
                     ec = T[f * TE + ti];
@@ -476,11 +484,11 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
 
 namespace {
 
-template <int LT, int K1M, bool DIRECT = false, bool PK = false>
+template <int LT, int K1M, bool DIRECT = false, int MODE = 0>
 void allow(int optin) {
     cudaFuncAttributes a{};
-    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, rerank_ij_kernel<LT, K1M, DIRECT, PK>));
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_ij_kernel<LT, K1M, DIRECT, PK>,
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, rerank_ij_kernel<LT, K1M, DIRECT, MODE>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(rerank_ij_kernel<LT, K1M, DIRECT, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes));
 }
 
@@ -489,12 +497,14 @@ void allow(int optin) {
 // SIFT1M 1388 vs 1133 us, GIST1M 157 vs 130 us per batch (profiles/r02/rerank_packed_ab.md): it
 // cuts the L1 data-pipe wavefronts 20% (134 M -> 108 M per 5000 queries) but adds 20% more
 // instructions, and the scalar loop was co-limited by both.
-bool ij_packed() {
-    static const bool packed = [] {
+int ij_mode() {
+    static const int mode = [] {
         const char* e = std::getenv("PQTG_RERANK");
-        return e && std::strcmp(e, "packed") == 0;
+        if (e && std::strcmp(e, "packed") == 0) return 1;
+        if (e && std::strcmp(e, "c3") == 0) return 2;
+        return 0;
     }();
-    return packed;
+    return mode;
 }
 
 int code_k1m(const DevParams& p) { return p.code_ij ? 16 : (p.code_pi ? 32 : 0); }
@@ -512,11 +522,11 @@ int optin_smem() {
     return optin;
 }
 
-bool ij_packed();
+int ij_mode();
 
 size_t ij_smem(const DevParams& p, uint32_t k, bool gkeys) {
     const uint32_t kk = k < p.budget ? k : p.budget;
-    const bool pk = code_k1m(p) == 16 && ij_packed();
+    const bool pk = code_k1m(p) == 16 && ij_mode() != 0;
     return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16, ij_direct(p), gkeys, pk).total;
 }
 
@@ -546,9 +556,12 @@ void configure_rerank_ij() {
     allow<16, 16>(optin);
     allow<32, 16>(optin);
     allow<64, 16>(optin);
-    allow<16, 16, false, true>(optin);
-    allow<32, 16, false, true>(optin);
-    allow<64, 16, false, true>(optin);
+    allow<16, 16, false, 1>(optin);
+    allow<32, 16, false, 1>(optin);
+    allow<64, 16, false, 1>(optin);
+    allow<16, 16, false, 2>(optin);
+    allow<32, 16, false, 2>(optin);
+    allow<64, 16, false, 2>(optin);
     allow<16, 32>(optin);
     allow<32, 32>(optin);
     allow<16, 32, true>(optin);
@@ -592,11 +605,17 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
         } else {
             if (direct) PQTG_IJ(32, 32, true); else PQTG_IJ(32, 32, false);
         }
-    } else if (ij_packed()) {
+    } else if (ij_mode() == 1) {
         switch (p.L) {
-        case 16: PQTG_IJ(16, 16, false, true); break;
-        case 32: PQTG_IJ(32, 16, false, true); break;
-        default: PQTG_IJ(64, 16, false, true); break;
+        case 16: PQTG_IJ(16, 16, false, 1); break;
+        case 32: PQTG_IJ(32, 16, false, 1); break;
+        default: PQTG_IJ(64, 16, false, 1); break;
+        }
+    } else if (ij_mode() == 2) {
+        switch (p.L) {
+        case 16: PQTG_IJ(16, 16, false, 2); break;
+        case 32: PQTG_IJ(32, 16, false, 2); break;
+        default: PQTG_IJ(64, 16, false, 2); break;
         }
     } else {
         switch (p.L) {
