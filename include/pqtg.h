@@ -15,6 +15,9 @@
  *                              src/search.cpp:44-49 (enables the exact re-rank, :229-249)
  *   pqtg_merge_topk_host     ← no reference counterpart: merges per-shard top-k lists by the
  *                              reference's (dist, id) order (candidate_less, src/search.cpp:39-41)
+ *   pqtg_sharded_*           ← pqt::knn_query_batch (src/search.cpp:262-274) over G position shards,
+ *                              one process per GPU, query-partitioned, NCCL (no reference counterpart)
+ *   pqtg_brute_force_knn     ← pqt::brute_force_knn        include/pqt/search.hpp:86, src/search.cpp:276-299
  *
  * Errors: every int-returning call returns PQTG_OK (0) or a negative pqtg_status; the message
  * is available from pqtg_last_error() (thread-local). The C++ drop-in (include/pqt/) maps
