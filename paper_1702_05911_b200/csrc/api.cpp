@@ -64,9 +64,9 @@ WsSlice Workspace::slice(uint64_t q0) const {
     s.ntuples = ntuples + q0;
     s.err = err;
     s.keys = keys ? keys + q0 * std::max<uint64_t>(p.budget, 1) : nullptr;
-    s.split_ids = split_ids;
-    s.split_dists = split_dists;
-    s.split_counts = split_counts;
+    s.split_keys = split_keys;
+    s.split_cnt = split_cnt;
+    s.split_ctr = split_ctr;
     s.split_q = split_q;
     s.split_k = split_k;
     s.hash = hash ? hash + q0 * hash_stride : nullptr;
@@ -159,9 +159,10 @@ void ensure_keys(Workspace& ws, uint32_t k) {
     // the split re-rank of small batches: per-(slice, query) lists
     const uint64_t sq = std::min<uint64_t>(ws.max_batch, kSplitBelow);
     if (kk && rerank_split(p, 1, kk) > 1 && (ws.split_k < kk || ws.split_q < sq)) {
-        ws.split_ids = dev_alloc<uint32_t>(ws.allocations, (uint64_t)kSplitMax * sq * kk);
-        ws.split_dists = dev_alloc<float>(ws.allocations, (uint64_t)kSplitMax * sq * kk);
-        ws.split_counts = dev_alloc<uint32_t>(ws.allocations, (uint64_t)kSplitMax * sq);
+        ws.split_keys = dev_alloc<uint64_t>(ws.allocations, (uint64_t)kSplitMax * sq * kk);
+        ws.split_cnt = dev_alloc<uint32_t>(ws.allocations, (uint64_t)kSplitMax * sq);
+        ws.split_ctr = dev_alloc<uint32_t>(ws.allocations, sq);
+        PQTG_CUDA_CHECK(cudaMemset(ws.split_ctr, 0, sq * sizeof(uint32_t)));
         ws.split_q = sq;
         ws.split_k = kk;
         ++ws.gen;

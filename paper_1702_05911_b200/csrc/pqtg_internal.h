@@ -114,10 +114,11 @@ struct WsSlice {
     float* scr = nullptr;         // [q][P][scr_nj] tensor-core dot products (screen.cu)
     uint32_t* err = nullptr;      // the workspace's device error word (PQTG_WS_ERR_*), shared by all slices
     uint64_t* keys = nullptr;     // [q][budget] candidate keys when they do not fit shared memory, or null
-    // small batches: per-(slice, query) top-k lists of the split re-rank [kSplitMax][split_q][split_k]
-    uint32_t* split_ids = nullptr;
-    float* split_dists = nullptr;
-    uint32_t* split_counts = nullptr;
+    // small batches: the split re-rank's per-(query, slice) top-k keys [q][kSplitMax][split_k], their
+    // counts [q][kSplitMax] and per-query arrival counters [q] (zero between calls)
+    uint64_t* split_keys = nullptr;
+    uint32_t* split_cnt = nullptr;
+    uint32_t* split_ctr = nullptr;
     uint64_t split_q = 0, split_k = 0;
 };
 
@@ -146,9 +147,9 @@ struct Workspace {
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
     uint32_t* err = nullptr;      // [1] device error word (PQTG_WS_ERR_*)
     uint64_t* keys = nullptr;     // [B][budget] re-rank keys for budgets too large for shared memory
-    uint32_t* split_ids = nullptr;    // small-batch split re-rank lists (see WsSlice)
-    float* split_dists = nullptr;
-    uint32_t* split_counts = nullptr;
+    uint64_t* split_keys = nullptr;   // small-batch split re-rank lists (see WsSlice)
+    uint32_t* split_cnt = nullptr;
+    uint32_t* split_ctr = nullptr;
     uint64_t split_q = 0, split_k = 0;
     float* scr = nullptr;         // [B][P][scr_nj] (y - mu_p) . c'' on the tensor cores (screen.cu)
     uint32_t* hash = nullptr;     // [B << ts_log2] visited slots, cleared on use (binsel_fast.cu)

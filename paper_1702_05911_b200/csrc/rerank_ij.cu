@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
-                     float* __restrict__ out_dists, uint32_t* __restrict__ out_counts, uint64_t* __restrict__ gkeys) {
+                     float* __restrict__ out_dists, uint32_t* __restrict__ out_counts, uint64_t* __restrict__ gkeys,
+                     uint64_t* __restrict__ split_keys, uint32_t* __restrict__ split_cnt,
+                     uint32_t* __restrict__ split_ctr) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE != 0;
     const uint32_t k1 = p.k1, budget = p.budget;
@@ -478,8 +480,62 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
         m = block_select_wide<kSelBits, kIjThreads>(keys + jlo, jhi - jlo, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap,
                                                     wmax, s_sel);
     }
-    // one list per (slice, query): [slice][query][k]
-    block_sort_write(sel, m, kk, k, (uint64_t)blockIdx.y * gridDim.x + q, out_ids, out_dists, out_counts);
+    if (gridDim.y == 1) {
+        block_sort_write(sel, m, kk, k, q, out_ids, out_dists, out_counts);
+        return;
+    }
+    // split: this slice's top-kk keys to its list, then the query's last-arriving slice selects the
+    // top-k of all S lists (threadfence-reduction pattern: no second launch)
+    const uint32_t S = gridDim.y;
+    uint64_t* lst = split_keys + ((uint64_t)q * kSplitMax + blockIdx.y) * k;
+    block_rank_keys(sel, m, kk, lst);
+    if (tid == 0) split_cnt[q * kSplitMax + blockIdx.y] = kk;
+    __threadfence();
+    __syncthreads();
+    __shared__ uint32_t s_last;
+    if (tid == 0) s_last = atomicAdd(&split_ctr[q], 1u) == S - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // the S lists into keys[0 ..) (they fit: S·k <= budget, rerank_split), then select + sort
+    uint32_t tot = 0;
+    for (uint32_t g = 0; g < S; ++g) {
+        const uint32_t c = __ldcg(split_cnt + q * kSplitMax + g);
+        const uint64_t* src = split_keys + ((uint64_t)q * kSplitMax + g) * k;
+        for (uint32_t i = tid; i < c; i += blockDim.x) keys[tot + i] = __ldcg(src + i);
+        tot += c;
+    }
+    if (tid == 0) {
+        split_ctr[q] = 0;  // ready for the next call
+        s_sel.kand = ~0ull;
+        s_sel.kor = 0ull;
+    }
+    __syncthreads();
+    {
+        uint64_t a = ~0ull, o = 0ull;
+        for (uint32_t j = tid; j < tot; j += blockDim.x) {
+            a &= keys[j];
+            o |= keys[j];
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            a &= __shfl_xor_sync(0xffffffffu, a, d);
+            o |= __shfl_xor_sync(0xffffffffu, o, d);
+        }
+        if ((tid & 31) == 0) {
+            atomicAnd(&s_sel.kand, (unsigned long long)a);
+            atomicOr(&s_sel.kor, (unsigned long long)o);
+        }
+    }
+    const uint32_t k2 = tot < k ? tot : k;
+    uint32_t m2 = 0;
+    if (k2) {
+        for (uint32_t i = tid; i < (1u << kSelBits); i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        m2 = block_select_wide<kSelBits, kIjThreads>(keys, tot, k2, s_sel.kand, s_sel.kor, hist, sel, sel_cap, wmax,
+                                                     s_sel);
+    }
+    block_sort_write(sel, m2, k2, k, q, out_ids, out_dists, out_counts);
 }
 
 namespace {
@@ -569,15 +625,15 @@ void configure_rerank_ij() {
 }
 
 // CTAs per query: a batch below one query per SM can spread each query's candidates over up to
-// kSplitMax CTAs (their top-k lists merged by launch_merge) -- opt-in (PQTG_SPLIT=1): at batch 1
-// the re-rank is bound by its serial prologue / selection, not its candidate loop, and the split
-// measured slower (SIFT1M batch 1: 33.9 vs 25.6 us, profiles/r02/latency.md)
+// kSplitMax CTAs; each slice ranks its top-k keys into a list and the query's last-arriving
+// slice selects the top-k of all lists (PQTG_SPLIT=1 enables; 0 / unset keeps one CTA per query)
 uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k) {
     static const bool off = [] {
         const char* e = std::getenv("PQTG_SPLIT");
         return !(e && std::strcmp(e, "1") == 0);
     }();
     if (off || nq == 0 || nq >= kSplitBelow || p.budget < 1024 || !rerank_ij_ok(p, k)) return 1;
+    if ((uint64_t)kSplitMax * k > p.budget) return 1;  // the last slice gathers every list into its key array
     const uint64_t s = (2 * kSplitBelow) / nq;
     return (uint32_t)std::min<uint64_t>(kSplitMax, std::max<uint64_t>(1, std::min<uint64_t>(s, p.budget / 256)));
 }
@@ -585,10 +641,7 @@ uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k) {
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids, float* dists,
                       uint32_t* counts, cudaStream_t s) {
     const uint32_t S = rerank_split(p, nq, k);
-    if (S > 1 && (!ws.split_ids || ws.split_k < k || ws.split_q < nq)) throw Error{PQTG_ERR_ARG, "workspace has no split lists"};
-    uint32_t* o_ids = S > 1 ? ws.split_ids : ids;
-    float* o_dists = S > 1 ? ws.split_dists : dists;
-    uint32_t* o_counts = S > 1 ? ws.split_counts : counts;
+    if (S > 1 && (!ws.split_keys || ws.split_k < k || ws.split_q < nq)) throw Error{PQTG_ERR_ARG, "workspace has no split lists"};
     const uint32_t kk = k < p.budget ? k : p.budget;
     const uint32_t cap = ij_sel_cap(kk);
     const bool gk = rerank_ij_gkeys(p, k);
@@ -597,7 +650,8 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     uint64_t* gkeys = gk ? ws.keys : nullptr;
 #define PQTG_IJ(LT, K, D, ...)                                                                                \
     rerank_ij_kernel<LT, K, D, ##__VA_ARGS__><<<dim3((unsigned)nq, S), ij_threads(LT), sm, s>>>(                  \
-        p, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, o_ids, o_dists, o_counts, gkeys)
+        p, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, ids, dists, counts, gkeys, ws.split_keys,          \
+        ws.split_cnt, ws.split_ctr)
     if (code_k1m(p) == 32) {
         const bool direct = ij_direct(p);
         if (p.L == 16) {
@@ -626,7 +680,6 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     }
 #undef PQTG_IJ
     PQTG_CUDA_CHECK(cudaGetLastError());
-    if (S > 1) launch_merge(S, nq, k, o_ids, o_dists, o_counts, ids, dists, counts, s);
 }
 
 }  // namespace pqtg

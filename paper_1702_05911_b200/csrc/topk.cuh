@@ -271,6 +271,29 @@ __device__ inline void block_sort_write(uint64_t* sel, uint32_t m, uint32_t kk, 
     if (tid == 0) out_counts[q] = kk;
 }
 
+// The kk smallest of the m >= kk distinct keys sel[0..m) to out[0..kk) in ascending order (the
+// rank count of block_sort_write, storing keys).
+__device__ inline void block_rank_keys(uint64_t* sel, uint32_t m, uint32_t kk, uint64_t* out) {
+    const uint32_t tid = threadIdx.x;
+    uint32_t n2 = 1;
+    while (n2 < m) n2 <<= 1;
+    if (n2 <= blockDim.x) {
+        uint32_t g = blockDim.x / n2;
+        g = g > 32 ? 32 : g;
+        const uint32_t e = tid / g, sub = tid - e * g;
+        const bool own = e < m;
+        const uint64_t me = own ? sel[e] : 0ull;
+        uint32_t rank = 0;
+        if (own)
+            for (uint32_t j = sub; j < m; j += g) rank += sel[j] < me;
+        for (uint32_t o = 1; o < g; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+        if (own && sub == 0 && rank < kk) out[rank] = me;
+    } else {
+        block_bitonic(sel, m);
+        for (uint32_t i = tid; i < kk; i += blockDim.x) out[i] = sel[i];
+    }
+}
+
 // Write the sorted top-kk (padded to k with (UINT32_MAX, +inf)) and the count.
 __device__ inline void write_topk(const uint64_t* sel, uint32_t kk, uint32_t k, uint64_t q,
                                   uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {

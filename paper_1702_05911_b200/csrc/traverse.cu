@@ -463,6 +463,119 @@ __global__ void __launch_bounds__(128) traverse_warp_wide_kernel(DevParams p, co
     }
 }
 
+
+// Small batches (fewer queries than SMs): latency, not throughput. One CTA per (query, part)
+// stages the part's WHOLE level-2 codebook (k1 × m × k2 floats) and its fine parts' codebook
+// slice with two TMA bulk copies issued at kernel start, in parallel with the query load, so the
+// chain of dependent memory round trips is [query ‖ codebooks] → compute, instead of the
+// per-parent block loads that follow the level-1 order. Same arithmetic and orders as
+// traverse_part_kernel (pqtree.cpp:74-120).
+struct TsLayout {
+    size_t cb, ft, y, fine, l1d, l1o, keys, total;
+};
+
+__host__ __device__ inline TsLayout ts_layout(const DevParams& p) {
+    TsLayout l{};
+    size_t o = 0;
+    l.cb = o;
+    o += (size_t)p.k1 * p.m * p.k2 * 4;
+    l.ft = o;
+    o += (size_t)p.per_part * p.fd * p.k1 * 4;
+    l.y = o;
+    o += ((size_t)p.m * 4 + 15) & ~size_t(15);
+    l.fine = o;
+    o += (size_t)p.per_part * p.k1 * 4;
+    l.l1d = o;
+    o += (size_t)p.k1 * 4;
+    l.l1o = o;
+    o += (size_t)p.k1 * 4;
+    l.keys = (o + 7) & ~size_t(7);
+    uint32_t n2 = 1;
+    while (n2 < p.W) n2 <<= 1;
+    o = l.keys + (size_t)n2 * 8;
+    l.total = (o + 15) & ~size_t(15);
+    return l;
+}
+
+__global__ void __launch_bounds__(kTpThreads) traverse_small_kernel(DevParams p, const float* __restrict__ Q,
+                                                                    float* __restrict__ fine_out,
+                                                                    float* __restrict__ l2d_out,
+                                                                    uint32_t* __restrict__ l2c_out, const TsLayout lay) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) uint64_t mbar;
+    const uint32_t k1 = p.k1, k2 = p.k2, P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W;
+    float* cb = reinterpret_cast<float*>(smem + lay.cb);
+    float* ft = reinterpret_cast<float*>(smem + lay.ft);
+    float* y = reinterpret_cast<float*>(smem + lay.y);
+    float* fine = reinterpret_cast<float*>(smem + lay.fine);
+    float* l1d = reinterpret_cast<float*>(smem + lay.l1d);
+    uint32_t* l1o = reinterpret_cast<uint32_t*>(smem + lay.l1o);
+    const uint64_t q = blockIdx.x / P;
+    const uint32_t part = blockIdx.x - (uint32_t)q * P;
+    const uint32_t tid = threadIdx.x, f0 = part * pp;
+    const uint32_t cb_bytes = k1 * m * k2 * 4, ft_bytes = pp * fd * k1 * 4;
+    if (tid == 0) {
+        mbar_init(&mbar, 1);
+        mbar_expect_tx(&mbar, cb_bytes + ft_bytes);
+        bulk_g2s(cb, p.l2_t + (size_t)part * k1 * m * k2, cb_bytes, &mbar);
+        bulk_g2s(ft, p.fine_t + (size_t)f0 * fd * k1, ft_bytes, &mbar);
+    }
+    const float* yq = Q + q * p.D + (uint64_t)part * m;
+    for (uint32_t t = tid; t < m; t += blockDim.x) y[t] = __ldg(yq + t);
+    __syncthreads();
+    mbar_wait(&mbar, 0);
+    // fine_dists[f][i] = l2_sq(y_f, slice(f, i), fd), sequential (pqtree.cpp:90-93)
+    for (uint32_t idx = tid; idx < pp * k1; idx += blockDim.x) {
+        const uint32_t lf = idx / k1, i = idx - lf * k1;
+        const float* c = ft + (size_t)lf * fd * k1 + i;
+        const float* yf = y + lf * fd;
+        float acc = 0.0f;
+        for (uint32_t t = 0; t < fd; ++t) acc = sq_step(acc, yf[t], c[t * k1]);
+        fine[idx] = acc;
+        fine_out[(q * p.L + f0 + lf) * k1 + i] = acc;
+    }
+    __syncthreads();
+    // level-1 totals in f order (pqtree.cpp:88-96), ranked by (dist, id) (:98-100)
+    for (uint32_t i = tid; i < k1; i += blockDim.x) {
+        float tot = 0.0f;
+        for (uint32_t lf = 0; lf < pp; ++lf) tot = __fadd_rn(tot, fine[lf * k1 + i]);
+        l1d[i] = tot;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < k1; i += blockDim.x) {
+        const float d = l1d[i];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < k1; ++j) {
+            const float dj = l1d[j];
+            rank += (dj < d) || (dj == d && j < i);
+        }
+        l1o[rank] = i;
+    }
+    __syncthreads();
+    // level-2 chains of the w best parents' children from the staged codebook (pqtree.cpp:102-111)
+    const uint32_t j = tid, r = j / k2, c = j - r * k2;
+    float acc = 0.0f;
+    if (j < W) {
+        const float* bp = cb + (size_t)l1o[r] * m * k2 + c;
+        for (uint32_t t = 0; t < m; ++t) acc = sq_step(acc, y[t], bp[t * k2]);
+    }
+    uint64_t key = ~0ull;
+    if (j < W) key = ((uint64_t)orderable(acc) << 32) | ((l1o[r] << 16) | c);
+    uint64_t* kbuf = reinterpret_cast<uint64_t*>(smem + lay.keys);
+    if (W <= 32) {
+        if (tid < 32) key = bitonic_block<32>(key, tid, kbuf);
+    } else if (W <= 64) {
+        key = bitonic_block<64>(key, tid, kbuf);
+    } else {
+        key = bitonic_block<128>(key, tid, kbuf);
+    }
+    if (j < W) {
+        const size_t out = (q * P + part) * W + j;
+        l2d_out[out] = unorderable((uint32_t)(key >> 32));
+        l2c_out[out] = (uint32_t)key;
+    }
+}
+
 namespace {
 
 template <int A, int B, int FB>
@@ -490,6 +603,12 @@ void configure_traverse_part() {
     int dev = 0, optin = 0;
     PQTG_CUDA_CHECK(cudaGetDevice(&dev));
     PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    {
+        cudaFuncAttributes a{};
+        PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, traverse_small_kernel));
+        PQTG_CUDA_CHECK(cudaFuncSetAttribute(traverse_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             optin - (int)a.sharedSizeBytes));
+    }
     tp_allow<16, 8>(optin);
     tp_allow<32, 16>(optin);
     tp_allow<16, 16>(optin);
@@ -513,8 +632,25 @@ bool traverse_warp_wide_ok(const DevParams& p) {
            (reinterpret_cast<uintptr_t>(p.l2_t) & 15) == 0;
 }
 
+// the whole-codebook staging pays when the batch leaves SMs idle and the part's level-2 codebook
+// fits shared memory (SIFT1M / DEEP: 32 / 24 KB); PQTG_NO_TRAVERSE_SMALL=1 disables
+bool traverse_small_ok(const DevParams& p, uint64_t nq) {
+    static const bool off = std::getenv("PQTG_NO_TRAVERSE_SMALL") != nullptr;
+    const uint64_t cb = (uint64_t)p.k1 * p.m * p.k2 * 4, ft = (uint64_t)p.per_part * p.fd * p.k1 * 4;
+    return !off && nq * p.P <= 2 * 148 && p.W <= (uint32_t)kTpThreads && cb % 16 == 0 && ft % 16 == 0 &&
+           ((uint64_t)p.k1 * p.m * p.k2 * 4) % 16 == 0 && ts_layout(p).total <= 96 * 1024 &&
+           (reinterpret_cast<uintptr_t>(p.l2_t) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.fine_t) & 15) == 0;
+}
+
 void launch_traverse_part(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                           cudaStream_t s) {
+    if (traverse_small_ok(p, nq)) {
+        const TsLayout lay = ts_layout(p);
+        traverse_small_kernel<<<(unsigned)(nq * p.P), kTpThreads, lay.total, s>>>(p, queries, ws.fine, ws.l2_dist,
+                                                                                ws.l2_code, lay);
+        PQTG_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     if (traverse_warp_wide_ok(p)) {
         traverse_warp_wide_kernel<32, 16, 4><<<(unsigned)nq, 32 * p.P, tw_smem(p), s>>>(p, queries, ws.fine,
                                                                                       ws.l2_dist, ws.l2_code);
