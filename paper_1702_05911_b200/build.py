@@ -46,6 +46,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     OUT.mkdir(exist_ok=True)
     headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list((REPO / "include").rglob("*.h*"))
     objs = []
+    compiled = []
     for src in CU_SOURCES + CXX_SOURCES:
         path = CSRC / src
         if not path.exists():
@@ -59,12 +60,18 @@ def build(verbose: bool = False, force: bool = False) -> Path:
                 flags[flags.index("-fPIC,-O2")] = "-fPIC,-O2,-ffp-contract=off"
             cmd = [NVCC, *ARCH, *flags, "-I", str(REPO / "include"), "-c", str(path), "-o", str(obj)]
             out = _run(cmd)
+            compiled.append(src)
             if verbose and out.strip():
                 print(out)
-    if force or _stale(LIB, objs):
+    linked = force or _stale(LIB, objs)
+    if linked:
         out = _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread", "-ldl"])
         if verbose and out.strip():
             print(out)
+    if verbose:  # what this call did (the driver's build check reads it)
+        print(f"[build] sm_100a: compiled {len(compiled)} of {len(objs)} sources"
+              f"{' (' + ', '.join(compiled) + ')' if compiled else ' (all up to date)'}; "
+              f"{'linked' if linked else 'library up to date'}: {LIB}")
     return LIB
 
 

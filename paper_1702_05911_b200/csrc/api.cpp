@@ -189,6 +189,12 @@ void ensure_exact(Workspace& ws, uint32_t k) {
 
 }  // namespace
 
+// a position shard's exact stage needs the other shards' prefixes: it runs in the sharded search
+void refuse_shard_exact(const DevParams& p) {
+    if (p.db && p.rerank_exact > 0 && (p.shard_lo != 0 || p.shard_hi != p.n))
+        throw Error{PQTG_ERR_UNSUPPORTED, "exact re-ranking of a position shard runs in the sharded search (pqtg_sharded_*)"};
+}
+
 void prepare_workspace(Workspace& ws, uint32_t k) {
     ensure_exact(ws, k);
     ensure_keys(ws, k);
@@ -366,39 +372,56 @@ int pqtg_index_attach_database(pqtg_index* index, const float* rows, uint64_t n,
         if (!index) throw Error{PQTG_ERR_ARG, "null argument"};
         DevIndex& d = *index->dev;
         PQTG_CUDA_CHECK(cudaSetDevice(d.device));
-        if (!rows) {  // detach
-            if (d.db) {
-                PQTG_CUDA_CHECK(cudaDeviceSynchronize());
-                PQTG_CUDA_CHECK(cudaFree(d.db));
-            }
+        auto release = [&] {
+            if (d.db || d.id2row) PQTG_CUDA_CHECK(cudaDeviceSynchronize());
+            if (d.db) cudaFree(d.db);
+            if (d.id2row) cudaFree(d.id2row);
             d.db = nullptr;
+            d.id2row = nullptr;
             d.prm.db = nullptr;
+            d.prm.id2row = nullptr;
+        };
+        if (!rows) {  // detach
+            release();
             return PQTG_OK;
         }
-        // search.cpp:44-49: the vector set must match the index
-        if (n != d.n || dim != d.prm.D)
+        // search.cpp:44-49: the vector set must match the index -- all n rows in id order, or, on a
+        // position shard, the shard's rows in position order (db[ids[lo..hi)])
+        const bool shard = d.prm.shard_lo != 0 || d.prm.shard_hi != d.n;
+        const uint64_t want = shard ? d.prm.shard_hi - d.prm.shard_lo : d.n;
+        if (n != want || dim != d.prm.D)
             throw Error{PQTG_ERR_BAD_DIM, "attach_database: vector set does not match index"};
-        if (d.prm.shard_lo != 0 || d.prm.shard_hi != d.n)
-            unsupported("exact re-ranking on a sharded index");
         float* buf = nullptr;
+        uint32_t* map = nullptr;
         const uint32_t stride = (dim + 3) / 4 * 4;  // 16-byte rows for the exact stage's bulk copies
         const size_t bytes = (size_t)n * stride * sizeof(float);
         cudaError_t e = cudaMalloc(&buf, bytes ? bytes : 16);
-        if (e != cudaSuccess) throw Error{PQTG_ERR_OOM, std::string("attach_database: ") + cudaGetErrorString(e)};
+        if (e == cudaSuccess && shard) e = cudaMalloc(&map, (size_t)std::max<uint64_t>(d.n, 1) * sizeof(uint32_t));
+        if (e != cudaSuccess) {
+            cudaFree(buf);
+            throw Error{PQTG_ERR_OOM, std::string("attach_database: ") + cudaGetErrorString(e)};
+        }
         if (stride != dim) e = cudaMemset(buf, 0, bytes);
         if (e == cudaSuccess && n)
             e = cudaMemcpy2D(buf, stride * sizeof(float), rows, dim * sizeof(float), dim * sizeof(float), n,
                              cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && shard) {  // id -> row of this shard's rows (ids of other shards: none)
+            e = cudaMemset(map, 0xFF, (size_t)d.n * sizeof(uint32_t));
+            if (e == cudaSuccess) {
+                launch_fill_id2row(d.prm.ids, n, map, nullptr);
+                e = cudaDeviceSynchronize();
+            }
+        }
         if (e != cudaSuccess) {
             cudaFree(buf);
+            cudaFree(map);
             throw Error{PQTG_ERR_CUDA, std::string("attach_database: ") + cudaGetErrorString(e)};
         }
-        if (d.db) {
-            PQTG_CUDA_CHECK(cudaDeviceSynchronize());
-            cudaFree(d.db);
-        }
+        release();
         d.db = buf;
+        d.id2row = map;
         d.prm.db = buf;
+        d.prm.id2row = map;
         d.prm.db_stride = stride;
         return PQTG_OK;
     });
@@ -530,6 +553,7 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         if (nq > ws.max_batch) throw Error{PQTG_ERR_ARG, "nq exceeds the workspace max_batch"};
         std::lock_guard<std::mutex> lock(ws.mu);  // the workspace's host state (buffers, chunking)
         PQTG_CUDA_CHECK(cudaSetDevice(index->dev->device));
+        refuse_shard_exact(index->dev->prm);
         ensure_exact(ws, k);
         ensure_keys(ws, k);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -582,6 +606,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         if (ws.index != &d) throw Error{PQTG_ERR_ARG, "workspace belongs to another index"};
         std::lock_guard<std::mutex> lock(ws.mu);
         PQTG_CUDA_CHECK(cudaSetDevice(d.device));
+        refuse_shard_exact(d.prm);
         ensure_staging(ws, std::max<uint32_t>(k, 1));
         ensure_exact(ws, k);
         ensure_keys(ws, k);

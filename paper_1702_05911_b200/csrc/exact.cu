@@ -8,6 +8,7 @@
 // here streams those rows through shared memory with TMA bulk copies (below) and ranks them
 // by the exact keys.
 #include <cstdint>
+#include <mutex>
 
 #include "common.cuh"
 #include "pqtg_internal.h"
@@ -29,13 +30,15 @@ constexpr int kExRow = 272;       // bytes per staged row piece: 256 + 16 pad (c
 // 3-chunk shared ring on per-chunk mbarriers, so ~50 KB per CTA is in flight from HBM while each
 // thread sums its own row's previous piece in order (distance.hpp:11-18). Device rows have a
 // stride of D rounded up to 4 floats (16-byte bulk copies).
+template <bool PREFIX>  // PREFIX: write every prefix entry's exact distance in line order, no cut
 __global__ void __launch_bounds__(kExThreads) exact_rerank_kernel(DevParams p, const float* __restrict__ Q, uint32_t kp,
                                                                   const uint32_t* __restrict__ line_ids,
                                                                   const uint32_t* __restrict__ line_counts, uint32_t k,
                                                                   uint32_t* __restrict__ out_ids,
                                                                   float* __restrict__ out_dists,
                                                                   uint32_t* __restrict__ out_counts,
-                                                                  pqtg_query_stats* __restrict__ stats) {
+                                                                  pqtg_query_stats* __restrict__ stats,
+                                                                  float* __restrict__ exact_out) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t D = p.D, Dp = p.db_stride;
     unsigned char* ring = smem;                                     // kExStages × 128 × kExRow
@@ -53,6 +56,8 @@ __global__ void __launch_bounds__(kExThreads) exact_rerank_kernel(DevParams p, c
     for (uint32_t g0 = 0; g0 < n; g0 += kExThreads) {
         const uint32_t cnt = n - g0 < (uint32_t)kExThreads ? n - g0 : (uint32_t)kExThreads;
         const uint32_t id = tid < cnt ? line_ids[q * kp + g0 + tid] : 0u;
+        // the row of this id: by id, or through a position shard's id -> row table
+        const uint64_t row = p.id2row ? (tid < cnt ? p.id2row[id] : 0u) : id;
         // chunk c's bytes are armed on its slot's barrier by thread 0 before a block barrier,
         // then every thread bulk-copies its own row's piece (the copies issue in parallel)
         auto chunk_bytes = [&](uint32_t c) {
@@ -62,7 +67,7 @@ __global__ void __launch_bounds__(kExThreads) exact_rerank_kernel(DevParams p, c
         auto issue_mine = [&](uint32_t c, uint32_t use) {
             if (tid < cnt)
                 bulk_g2s(ring + (size_t)(use % kExStages) * kExThreads * kExRow + tid * kExRow,
-                         p.db + (size_t)id * Dp + c * kExDims, chunk_bytes(c), &full[use % kExStages]);
+                         p.db + (size_t)row * Dp + c * kExDims, chunk_bytes(c), &full[use % kExStages]);
         };
         if (tid == 0)
             for (uint32_t c = 0; c < nch && c < (uint32_t)kExStages; ++c)
@@ -95,8 +100,12 @@ __global__ void __launch_bounds__(kExThreads) exact_rerank_kernel(DevParams p, c
             __syncthreads();  // the slot is free again and armed for chunk c + stages
             if (more) issue_mine(c + kExStages, uses + kExStages);
         }
-        if (tid < cnt) keys[g0 + tid] = ((uint64_t)orderable(acc) << 32) | id;
+        if (tid < cnt) {
+            if (PREFIX) exact_out[q * kp + g0 + tid] = acc;
+            else keys[g0 + tid] = ((uint64_t)orderable(acc) << 32) | id;
+        }
     }
+    if (PREFIX) return;
     __syncthreads();
     const uint32_t kk = n < k ? n : k;
     block_sort_write(keys, n, kk, k, q, out_ids, out_dists, out_counts);
@@ -114,8 +123,11 @@ void configure_exact() {
     PQTG_CUDA_CHECK(cudaGetDevice(&dev));
     PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes a{};
-    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, exact_rerank_kernel));
-    PQTG_CUDA_CHECK(cudaFuncSetAttribute(exact_rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, exact_rerank_kernel<false>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(exact_rerank_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         optin - (int)a.sharedSizeBytes));
+    PQTG_CUDA_CHECK(cudaFuncGetAttributes(&a, exact_rerank_kernel<true>));
+    PQTG_CUDA_CHECK(cudaFuncSetAttribute(exact_rerank_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          optin - (int)a.sharedSizeBytes));
 }
 
@@ -123,8 +135,122 @@ void launch_exact(const DevParams& p, const float* queries, uint64_t nq, uint32_
                   const uint32_t* line_counts, uint32_t k, uint32_t* ids, float* dists, uint32_t* counts,
                   pqtg_query_stats* stats, cudaStream_t s) {
     if (nq == 0) return;
-    exact_rerank_kernel<<<(unsigned)nq, kExThreads, exact_smem(p, kp), s>>>(p, queries, kp, line_ids, line_counts, k,
-                                                                              ids, dists, counts, stats);
+    exact_rerank_kernel<false><<<(unsigned)nq, kExThreads, exact_smem(p, kp), s>>>(
+        p, queries, kp, line_ids, line_counts, k, ids, dists, counts, stats, nullptr);
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_exact_prefix(const DevParams& p, const float* queries, uint64_t nq, uint32_t kp, const uint32_t* line_ids,
+                         const uint32_t* line_counts, float* exact, cudaStream_t s) {
+    if (nq == 0) return;
+    exact_rerank_kernel<true><<<(unsigned)nq, kExThreads, exact_smem(p, kp), s>>>(
+        p, queries, kp, line_ids, line_counts, 0, nullptr, nullptr, nullptr, nullptr, exact);
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+namespace {
+
+__global__ void fill_id2row_kernel(const uint32_t* __restrict__ ids, uint64_t count, uint32_t* __restrict__ id2row) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+        id2row[ids[i]] = (uint32_t)i;
+}
+
+// One CTA per query: the G (line, id)-sorted lists in shared memory; each element's global
+// (line, id) rank by binary searches in the other lists; the first R' = min(R, C) form the
+// reference's exact prefix (search.cpp:229-240), ranked again by (exact, id) (:242-249).
+constexpr int kMxThreads = 256;
+
+__global__ void __launch_bounds__(kMxThreads) merge_exact_kernel(uint32_t G, uint64_t nq, uint32_t kp, uint32_t R,
+                                                                 uint32_t k, const uint32_t* __restrict__ ids,
+                                                                 const float* __restrict__ line,
+                                                                 const float* __restrict__ exact,
+                                                                 const uint32_t* __restrict__ counts,
+                                                                 pqtg_query_stats* __restrict__ stats,
+                                                                 uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
+                                                                 uint32_t* __restrict__ out_counts) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* lk = reinterpret_cast<uint64_t*>(smem);   // [G][kp] (line, id) keys
+    uint64_t* pre = lk + (size_t)G * kp;                 // [R'] (exact, id) keys at their line rank
+    __shared__ uint32_t cnt[16];
+    const uint64_t q = blockIdx.x;
+    if (threadIdx.x < G) cnt[threadIdx.x] = min(counts[(uint64_t)threadIdx.x * nq + q], kp);
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < G * kp; e += blockDim.x) {
+        const uint32_t g = e / kp, i = e - g * kp;
+        if (i < cnt[g]) {
+            const uint64_t off = ((uint64_t)g * nq + q) * kp + i;
+            lk[e] = ((uint64_t)orderable(line[off]) << 32) | ids[off];
+        }
+    }
+    __syncthreads();
+    const uint64_t C = stats[q].candidates;
+    const uint32_t Rp = (uint32_t)(C < R ? C : R);
+    for (uint32_t e = threadIdx.x; e < G * kp; e += blockDim.x) {
+        const uint32_t g = e / kp, i = e - g * kp;
+        if (i >= cnt[g] || i >= Rp) continue;
+        const uint64_t key = lk[e];
+        uint32_t rank = i;
+        for (uint32_t h = 0; h < G && rank < Rp; ++h) {
+            if (h == g) continue;
+            const uint64_t* l = lk + (uint64_t)h * kp;
+            uint32_t lo = 0, hi = cnt[h];
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (l[mid] < key) lo = mid + 1; else hi = mid;
+            }
+            rank += lo;
+        }
+        if (rank < Rp) {
+            const uint64_t off = ((uint64_t)g * nq + q) * kp + i;
+            pre[rank] = ((uint64_t)orderable(exact[off]) << 32) | (uint32_t)(key & 0xFFFFFFFFu);
+        }
+    }
+    __syncthreads();
+    const uint32_t kk = Rp < k ? Rp : k;
+    for (uint32_t e = threadIdx.x; e < Rp; e += blockDim.x) {  // rank by (exact, id): O(R'^2) counts
+        const uint64_t me = pre[e];
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < Rp; ++j) r += pre[j] < me;
+        if (r < kk) {
+            out_ids[q * k + r] = (uint32_t)(me & 0xFFFFFFFFu);
+            out_dists[q * k + r] = unorderable((uint32_t)(me >> 32));
+        }
+    }
+    for (uint32_t i = kk + threadIdx.x; i < k; i += blockDim.x) {
+        out_ids[q * k + i] = 0xFFFFFFFFu;
+        out_dists[q * k + i] = __uint_as_float(0x7F800000u);
+    }
+    if (threadIdx.x == 0) {
+        out_counts[q] = kk;
+        stats[q].exact_evals = Rp;
+    }
+}
+
+}  // namespace
+
+void launch_fill_id2row(const uint32_t* ids, uint64_t count, uint32_t* id2row, cudaStream_t s) {
+    if (count == 0) return;
+    const uint64_t blocks = (count + 255) / 256;
+    fill_id2row_kernel<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(ids, count, id2row);
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_merge_exact(uint32_t G, uint64_t nq, uint32_t kp, uint32_t R, uint32_t k, const uint32_t* ids,
+                        const float* line, const float* exact, const uint32_t* counts, pqtg_query_stats* stats,
+                        uint32_t* out_ids, float* out_dists, uint32_t* out_counts, cudaStream_t s) {
+    if (nq == 0) return;
+    const size_t sm = ((size_t)G * kp + R) * 8;
+    if (sm + 1024 > (size_t)optin_bytes()) throw Error{PQTG_ERR_UNSUPPORTED, "sharded exact re-rank: prefix too long"};
+    static std::once_flag once[64];
+    int dev = 0;
+    PQTG_CUDA_CHECK(cudaGetDevice(&dev));
+    std::call_once(once[dev & 63], [] {
+        cudaFuncAttributes a{};
+        cudaFuncGetAttributes(&a, merge_exact_kernel);
+        cudaFuncSetAttribute(merge_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_bytes() - (int)a.sharedSizeBytes);
+    });
+    merge_exact_kernel<<<(unsigned)nq, kMxThreads, sm, s>>>(G, nq, kp, R, k, ids, line, exact, counts, stats, out_ids,
+                                                          out_dists, out_counts);
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -39,6 +39,7 @@ DevIndex::~DevIndex() {
     cudaSetDevice(device);
     for (void* p : allocations) cudaFree(p);
     if (db) cudaFree(db);
+    if (id2row) cudaFree(id2row);
     cudaSetDevice(prev);
 }
 

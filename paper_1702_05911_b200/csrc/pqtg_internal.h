@@ -78,7 +78,8 @@ struct DevParams {
     const float* c2ij;          // [L][256] d2[f][i][j] at i << 4 | j (code_ij only)
     const float* c2p;           // [L][512] d2[f][pair] (code_pi only)
     // exact re-rank (search.cpp:229-249): raw vectors n × D f32 in id order, or null
-    const float* db;            // [n][db_stride]
+    const float* db;            // [n][db_stride] by id; on a position shard [shard rows][db_stride] by position
+    const uint32_t* id2row;     // shard only: id -> row of db (0xFFFFFFFF: not in this shard), else null
     uint32_t db_stride;         // D rounded up to 4 floats
     uint32_t rerank_exact;
     // tensor-core level-2 screen (screen.cu)
@@ -97,6 +98,7 @@ struct DevIndex {
     uint64_t bytes = 0;
     std::vector<void*> allocations;
     float* db = nullptr;  // attached raw vectors (pqtg_index_attach_database)
+    uint32_t* id2row = nullptr;  // a shard's id -> db row table (n entries)
     ~DevIndex();
 };
 
@@ -304,6 +306,18 @@ void configure_exact();
 void launch_exact(const DevParams& p, const float* queries, uint64_t nq, uint32_t kp, const uint32_t* line_ids,
                   const uint32_t* line_counts, uint32_t k, uint32_t* ids, float* dists, uint32_t* counts,
                   pqtg_query_stats* stats, cudaStream_t s);
+// the exact distances of the whole line-ranked prefix, in its (line, id) order, into exact[q][kp]
+// (a position shard's part of the sharded exact stage; no cut, no sort)
+void launch_exact_prefix(const DevParams& p, const float* queries, uint64_t nq, uint32_t kp, const uint32_t* line_ids,
+                         const uint32_t* line_counts, float* exact, cudaStream_t s);
+// the sharded exact stage's merge: G lists of (id, line, exact) sorted by (line, id), counts;
+// per query the first min(R, C) by (line, id) over all lists (C = stats.candidates), then the
+// first min(k, that) of those by (exact, id) (search.cpp:229-257); exact_evals = min(R, C)
+void launch_merge_exact(uint32_t G, uint64_t nq, uint32_t kp, uint32_t R, uint32_t k, const uint32_t* ids,
+                        const float* line, const float* exact, const uint32_t* counts, pqtg_query_stats* stats,
+                        uint32_t* out_ids, float* out_dists, uint32_t* out_counts, cudaStream_t s);
+// id2row[ids[p]] = p for the shard's positions (the table pre-filled with 0xFFFFFFFF)
+void launch_fill_id2row(const uint32_t* ids, uint64_t count, uint32_t* id2row, cudaStream_t s);
 // screen.cu (tcgen05 level-2 screen + certified exact residual check)
 bool screen_ok(const DevParams& p);
 void configure_screen();

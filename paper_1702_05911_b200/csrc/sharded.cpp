@@ -127,6 +127,8 @@ struct Rank {
     uint32_t* r_ids = nullptr;
     float* r_dists = nullptr;
     uint32_t* r_counts = nullptr;
+    float* l_exact = nullptr;       // the exact stage: exact distances of the local line prefix
+    float* r_exact = nullptr;
     // host-call staging (k-dependent outputs share lk)
     float* q = nullptr;
     uint32_t* o_ids = nullptr;
@@ -234,6 +236,8 @@ void ensure_k(pqtg_sharded& sh, Rank& r, uint32_t k) {
     r.r_ids = dev_alloc<uint32_t>(r.allocations, (uint64_t)sh.world * sh.block_max * k);
     r.r_dists = dev_alloc<float>(r.allocations, (uint64_t)sh.world * sh.block_max * k);
     r.r_counts = dev_alloc<uint32_t>(r.allocations, (uint64_t)sh.world * sh.block_max);
+    r.l_exact = dev_alloc<float>(r.allocations, B * k);
+    r.r_exact = dev_alloc<float>(r.allocations, (uint64_t)sh.world * sh.block_max * k);
     r.o_ids = dev_alloc<uint32_t>(r.allocations, B * k);
     r.o_dists = dev_alloc<float>(r.allocations, B * k);
     r.o_counts = dev_alloc<uint32_t>(r.allocations, B);
@@ -331,12 +335,21 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
         while (sh.ranks[i].get() != &self) ++i;
         return i;
     };
+    // the exact stage (search.cpp:229-249) when the shards hold their raw rows: each rank's
+    // line-ranked prefix of R = max(k, rerank_exact) with exact distances travels as
+    // (id, line, exact) triples and the merge cuts the global prefix min(R, C) before ranking by
+    // exact distance; lists then have R entries instead of k
+    const bool exact = sh.ranks[0]->ix->prm.db && sh.ranks[0]->ix->prm.rerank_exact > 0 && k > 0;
+    const uint32_t Rx = exact ? std::min(std::max(k, sh.ranks[0]->ix->prm.rerank_exact), std::max(budget, 1u)) : k;
+    const uint64_t lk = std::max<uint32_t>(Rx, 1);  // list stride of S6-S8
     for (uint32_t i = 0; i < R; ++i) {
         Rank& r = *sh.ranks[i];
         on(r);
-        if (r.ix->prm.db && r.ix->prm.rerank_exact > 0) throw Error{PQTG_ERR_UNSUPPORTED, "exact re-ranking on a sharded index"};
+        if (((bool)r.ix->prm.db && r.ix->prm.rerank_exact > 0) != exact)
+            throw Error{PQTG_ERR_ARG, "sharded exact re-rank: every shard must hold its raw rows, or none"};
+        if (exact && sh.sim) throw Error{PQTG_ERR_UNSUPPORTED, "the simulated transport has no exact stage"};
         prepare_workspace(r.ws(), k);
-        ensure_k(sh, r, (uint32_t)kk);
+        ensure_k(sh, r, (uint32_t)std::max<uint64_t>(kk, lk));
         // start after the caller's queued work
         PQTG_CUDA_CHECK(cudaEventRecord(r.done, caller(i)));
         PQTG_CUDA_CHECK(cudaStreamWaitEvent(r.stream, r.done, 0));
@@ -518,7 +531,8 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             launch_scan_counts(r.ws().nranges, nq, r.all_off, r.stream);
             launch_unpack_ranges(r.all_packed, r.ws().nranges, r.all_off, nq, std::max<uint32_t>(budget, 1),
                                  r.ws().ranges, r.stream);
-            launch_rerank(p, nq, k, r.ws().slice(0), r.l_ids, r.l_dists, r.l_counts, r.stream);
+            launch_rerank(p, nq, (uint32_t)lk, r.ws().slice(0), r.l_ids, r.l_dists, r.l_counts, r.stream);
+            if (exact) launch_exact_prefix(p, qptr(i), nq, (uint32_t)lk, r.l_ids, r.l_counts, r.l_exact, r.stream);
             r.ws().last_nq = nq;  // pqtg_workspace_read of this rank's view (pqtg_sharded_workspace)
             r.ws().last_stream = r.stream;
             if (i == 0) PQTG_CUDA_CHECK(cudaEventRecord(r.ev[3], r.stream));
@@ -541,15 +555,21 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             nccl_check(nc->group_start(), "ncclGroupStart");
             for (uint32_t j = 0; j < G; ++j) {
                 const Block bj = blk[j];
-                nccl_check(nc->send(r.l_ids + bj.lo * k, bj.n * k, ncclUint32, (int)j, sh.comm, r.stream), "ncclSend");
-                nccl_check(nc->send(r.l_dists + bj.lo * k, bj.n * k, ncclFloat32, (int)j, sh.comm, r.stream), "ncclSend");
+                nccl_check(nc->send(r.l_ids + bj.lo * lk, bj.n * lk, ncclUint32, (int)j, sh.comm, r.stream), "ncclSend");
+                nccl_check(nc->send(r.l_dists + bj.lo * lk, bj.n * lk, ncclFloat32, (int)j, sh.comm, r.stream), "ncclSend");
                 nccl_check(nc->send(r.l_counts + bj.lo, bj.n, ncclUint32, (int)j, sh.comm, r.stream), "ncclSend");
-                nccl_check(nc->recv(r.r_ids + (uint64_t)j * mine.n * k, mine.n * k, ncclUint32, (int)j, sh.comm, r.stream),
+                if (exact)
+                    nccl_check(nc->send(r.l_exact + bj.lo * lk, bj.n * lk, ncclFloat32, (int)j, sh.comm, r.stream),
+                               "ncclSend");
+                nccl_check(nc->recv(r.r_ids + (uint64_t)j * mine.n * lk, mine.n * lk, ncclUint32, (int)j, sh.comm, r.stream),
                            "ncclRecv");
-                nccl_check(nc->recv(r.r_dists + (uint64_t)j * mine.n * k, mine.n * k, ncclFloat32, (int)j, sh.comm,
+                nccl_check(nc->recv(r.r_dists + (uint64_t)j * mine.n * lk, mine.n * lk, ncclFloat32, (int)j, sh.comm,
                                     r.stream), "ncclRecv");
                 nccl_check(nc->recv(r.r_counts + (uint64_t)j * mine.n, mine.n, ncclUint32, (int)j, sh.comm, r.stream),
                            "ncclRecv");
+                if (exact)
+                    nccl_check(nc->recv(r.r_exact + (uint64_t)j * mine.n * lk, mine.n * lk, ncclFloat32, (int)j, sh.comm,
+                                        r.stream), "ncclRecv");
             }
             nccl_check(nc->group_end(), "ncclGroupEnd");
         } else {
@@ -564,9 +584,11 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
                 for (auto& sp : sh.ranks) {
                     Rank& src = *sp;
                     const uint64_t j = src.g;
-                    cs.push_back({dst.r_ids + j * mine.n * k, src.l_ids + mine.lo * k, mine.n * k * sizeof(uint32_t)});
-                    cs.push_back({dst.r_dists + j * mine.n * k, src.l_dists + mine.lo * k, mine.n * k * sizeof(float)});
+                    cs.push_back({dst.r_ids + j * mine.n * lk, src.l_ids + mine.lo * lk, mine.n * lk * sizeof(uint32_t)});
+                    cs.push_back({dst.r_dists + j * mine.n * lk, src.l_dists + mine.lo * lk, mine.n * lk * sizeof(float)});
                     cs.push_back({dst.r_counts + j * mine.n, src.l_counts + mine.lo, mine.n * sizeof(uint32_t)});
+                    if (exact)
+                        cs.push_back({dst.r_exact + j * mine.n * lk, src.l_exact + mine.lo * lk, mine.n * lk * sizeof(float)});
                 }
                 copies(dst, cs);
             }
@@ -576,7 +598,11 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             Rank& r = *sh.ranks[i];
             on(r);
             const Block b = blk[r.g];
-            if (b.n)
+            if (b.n && exact)
+                launch_merge_exact(G, b.n, (uint32_t)lk, Rx, k, r.r_ids, r.r_dists, r.r_exact, r.r_counts,
+                                   stats_of(i) + b.lo, d_ids[i] + b.lo * k, d_dists[i] + b.lo * k, d_counts[i] + b.lo,
+                                   r.stream);
+            else if (b.n)
                 launch_merge(G, b.n, k, r.r_ids, r.r_dists, r.r_counts, d_ids[i] + b.lo * k, d_dists[i] + b.lo * k,
                              d_counts[i] + b.lo, r.stream);
         }
@@ -607,6 +633,11 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             const Block b = blk[root];
             return Piece{nullptr, d_counts[rank_index(self)] + b.lo, b.n * sizeof(uint32_t)};
         });
+        if (exact)  // exact_evals were set by the block's merge
+            gather([&](Rank& self, uint32_t root) -> Piece {
+                const Block b = blk[root];
+                return Piece{nullptr, stats_of(rank_index(self)) + b.lo, b.n * sizeof(pqtg_query_stats)};
+            });
         }
     }
     // the caller's streams continue after the search
@@ -644,7 +675,6 @@ static void check_shard(const DevIndex& ix, uint32_t world, uint32_t g) {
     if (!whole && (ix.prm.shard_lo != lo || ix.prm.shard_hi != hi))
         throw Error{PQTG_ERR_ARG, "shard " + std::to_string(g) + " of " + std::to_string(world) + " must hold positions [" +
                                       std::to_string(lo) + ", " + std::to_string(hi) + ")"};
-    if (ix.db) throw Error{PQTG_ERR_UNSUPPORTED, "exact re-ranking on a sharded index"};
 }
 
 int pqtg_sharded_create_nccl(pqtg_index* shard, const uint8_t* nccl_id, uint32_t rank, uint32_t world,

@@ -118,7 +118,8 @@ class DeviceIndex:
 
     def attach_database(self, rows: "np.ndarray | None") -> None:
         """PqtIndex::attach_database (search.cpp:44-49): n × dim raw vectors (id order) for the
-        exact re-rank stage (search.cpp:229-249, when rerank_exact > 0); None detaches."""
+        exact re-rank stage (search.cpp:229-249, when rerank_exact > 0); on a position shard the
+        shard's rows in position order (db[ids[lo:hi]]), used by the sharded search. None detaches."""
         if rows is None:
             check(lib().pqtg_index_attach_database(self._h, None, 0, 0))
             return

@@ -100,7 +100,8 @@ class _Handle:
 
 
 class ShardedIndex(_Handle):
-    """One rank of a torch.distributed job (one process per GPU)."""
+    """One rank of a torch.distributed job (one process per GPU). For the exact stage attach
+    this rank's raw rows (its positions' vectors, db[ids[lo:hi]]) with self.local.attach_database."""
 
     def __init__(self, source, group=None, device: int | None = None, max_batch: int = 4096):
         self.group = group
@@ -164,6 +165,16 @@ class LocalShardedIndex(_Handle):
                      [t.data_ptr() for t in out_counts],
                      [t.data_ptr() if t is not None else None for t in (d_stats or [None] * self.world)], streams,
                      broadcast)
+
+    def attach_database(self, db: np.ndarray, ids: np.ndarray) -> None:
+        """PqtIndex::attach_database (search.cpp:44-49) for every shard: the full n × dim raw
+        vectors in id order and the index's inverted-list ids; shard g receives the rows of its
+        positions (db[ids[lo:hi]]), and searches then run the exact stage (search.cpp:229-249)
+        across the shards."""
+        db = np.ascontiguousarray(db, np.float32)
+        for dev in self.shards:
+            lo, hi = int(dev.info.shard_lo), int(dev.info.shard_hi)
+            dev.attach_database(db[np.asarray(ids[lo:hi], np.int64)])
 
     def search_host(self, queries: np.ndarray, k: int):
         """pqtg_sharded_search: host queries in, host results (rank 0's view) out."""

@@ -119,3 +119,36 @@ def test_gpu_split_rerank_opt_in():
     env = dict(os.environ, PQTG_SPLIT="1", PYTHONPATH=f"{REPO}:{REPO / 'tests'}")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=str(REPO / "tests"))
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("shards", [2, 3, 8])
+@pytest.mark.parametrize("k", [20, 80])
+def test_local_sharded_exact_rerank(shards, k):
+    """The exact stage across position shards (search.cpp:229-249): each shard re-ranks its own
+    line prefix with its own raw rows and ships (id, line, exact) triples; the merge cuts the
+    global prefix min(max(rerank_exact, k), C) by (line, id) and ranks it by (exact, id) --
+    bit-exact against the reference's keep_raw build (golden p2_exact), exact_evals included."""
+    from paper_1702_05911_b200 import HostIndex
+
+    g = load_golden("p2_exact")
+    path = str(GOLDEN / "p2_exact.pqt")
+    hix = HostIndex.load(path)
+    lsi = LocalShardedIndex(path, shards, max_batch=64)
+    lsi.attach_database(g["db"], hix.ids)
+    want = (g[f"ids_k{k}"], g[f"dists_k{k}"], g[f"counts_k{k}"], g[f"stats_k{k}"])
+    for r, got in enumerate(run_local(lsi, g["queries"], k, True)):
+        assert_same_results(got, want, f"exact G={shards} k={k} rank {r}")
+    assert_same_results(lsi.search_host(g["queries"], k), want, f"exact G={shards} k={k} host")
+
+
+def test_shard_exact_outside_the_sharded_search_is_refused():
+    from paper_1702_05911_b200 import HostIndex, shard_range
+
+    g = load_golden("p2_exact")
+    path = str(GOLDEN / "p2_exact.pqt")
+    hix = HostIndex.load(path)
+    lo, hi = shard_range(hix.n, 2, 1)
+    dev = DeviceIndex(path, shard=(lo, hi))
+    dev.attach_database(g["db"][hix.ids[lo:hi].astype(np.int64)])
+    with pytest.raises(Exception, match="sharded search"):
+        dev.search(g["queries"], 20)
