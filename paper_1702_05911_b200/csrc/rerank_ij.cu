@@ -35,7 +35,9 @@ namespace {
 
 // threads per CTA: 512, two CTAs (queries) per SM. (1024-thread CTAs, one query per SM, cut the
 // last wave's idle time but measured 20% slower on B200: MIO-queue stalls.)
-__host__ __device__ constexpr int ij_threads(int L) { return L >= 64 ? 512 : 512; }
+// DIRECT (a shard's ~1 candidate per thread): 256-thread CTAs, four per SM, so an SM overlaps four
+// queries' serial prologue / selection chains instead of two
+__host__ __device__ constexpr int ij_threads(int L, bool direct = false) { return direct ? 256 : (L >= 64 ? 512 : 512); }
 constexpr int kScanItems = 8;  // rid entries per thread per scan tile
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // no id: the candidate belongs to another shard
 constexpr uint32_t kRangeCache = 512;       // ranges whose (start − offset) is kept in smem
@@ -84,7 +86,7 @@ __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint3
     // rid: u16 range index per candidate, padded to whole 4096-candidate scan tiles; after
     // the candidate loop the same bytes hold the select histogram and sel
     l.rid = o;
-    const size_t tile = (size_t)kScanItems * ij_threads((int)L);
+    const size_t tile = (size_t)kScanItems * ij_threads((int)L, direct);
     const size_t rid_bytes = al16((budget + tile - 1) / tile * tile * 2);
     const size_t sel_bytes = ((size_t)4 << kSelBits) + (size_t)sel_cap * 8;
     l.sel = o + ((size_t)4 << kSelBits);
@@ -141,7 +143,7 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 // (PK); 2 = the scalar loop reading c2 by code and a2 = fine[f][j], E formed per candidate (C3).
 // Modes 1 and 2 use the c2-table layout (CT).
 template <int LT, int K1M, bool DIRECT, int MODE = 0>
-__global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DIRECT)) ? 1 : 2)
+__global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 64 || K1M == 32) ? 1 : 2))
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + fix.rid);  // aliases rid
     uint16_t* rid = reinterpret_cast<uint16_t*>(smem + fix.rid);
     uint32_t* delta = reinterpret_cast<uint32_t*>(smem + fix.delta);
-    constexpr int kIjThreads = ij_threads(LT);
+    constexpr int kIjThreads = ij_threads(LT, DIRECT);
     __shared__ uint32_t wmax[kIjThreads / 32];
     __shared__ uint32_t s_count;
     __shared__ TopkShared s_sel;
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     // every global load of the prologue is issued before the first barrier: the query's fine
     // LUT, the first kIjThreads ranges and this thread's column of d2 (T build below)
     constexpr uint32_t kPairLanes = K1M == 16 ? 128 : 512;  // >= the pair count
-    constexpr uint32_t kFLanes = kIjThreads / kPairLanes;
+    constexpr uint32_t kFLanes = kIjThreads >= (int)kPairLanes ? kIjThreads / kPairLanes : 1;
     constexpr uint32_t kFPer = (LT + kFLanes - 1) / kFLanes;
     const uint32_t pi = tid & (kPairLanes - 1), f0 = tid / kPairLanes;
     const bool pair_lane = pi < p.npairs;
@@ -195,6 +197,8 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
         pi_j = pr >> 16;
         if constexpr (DIRECT) {
             if (f0 == 0) jt[pi] = (uint16_t)pi_j;
+            for (uint32_t o = pi + blockDim.x; o < p.npairs && f0 == 0; o += blockDim.x)  // more pairs than threads
+                jt[o] = (uint16_t)(__ldg(p.pairs + o) >> 16);
         } else
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(ij_threads(LT), (LT >= 64 || (K1M == 32 && !DI
     // every index is a position range [shard_lo, shard_hi): [0, n) unsharded, possibly empty
     // on a shard (then every candidate is skipped and the query returns count 0)
     constexpr bool sharded = true;
-    const bool cached = R <= kRangeCache;
+    const bool cached = R <= (kRangeCache < (uint32_t)kIjThreads ? kRangeCache : (uint32_t)kIjThreads);
     // a position shard with cached ranges re-ranks only its own candidates: the ranges are
     // clipped to [shard_lo, shard_hi) and renumbered densely (thread r = range r), so the loop,
     // the scan and the select run over this shard's candidates only
@@ -649,7 +653,7 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     const size_t sm = ij_smem(p, k, gk);
     uint64_t* gkeys = gk ? ws.keys : nullptr;
 #define PQTG_IJ(LT, K, D, ...)                                                                                \
-    rerank_ij_kernel<LT, K, D, ##__VA_ARGS__><<<dim3((unsigned)nq, S), ij_threads(LT), sm, s>>>(                  \
+    rerank_ij_kernel<LT, K, D, ##__VA_ARGS__><<<dim3((unsigned)nq, S), ij_threads(LT, D), sm, s>>>(                  \
         p, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, ids, dists, counts, gkeys, ws.split_keys,          \
         ws.split_cnt, ws.split_ctr)
     if (code_k1m(p) == 32) {
