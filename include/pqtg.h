@@ -165,7 +165,9 @@ int pqtg_index_create_shard(const pqtg_index_view* view, const uint8_t* shard_la
  * stage when config.rerank_exact > 0 (src/search.cpp:229-249): the min(max(rerank_exact, k), C)
  * best candidates by line distance get l2_sq(row, y) distances in the reference's fp32 order
  * and are re-sorted by (dist, id). rows == NULL detaches. A mismatched n or dim returns
- * PQTG_ERR_BAD_DIM (std::invalid_argument in the reference); a sharded index returns
+ * PQTG_ERR_BAD_DIM (std::invalid_argument in the reference). A position shard takes its own
+ * rows, n = shard_hi - shard_lo in position order (db[ids[shard_lo..shard_hi)]); its exact stage
+ * then runs in the sharded search (pqtg_sharded_*), and pqtg_search on it returns
  * PQTG_ERR_UNSUPPORTED. Not safe to call concurrently with a search on the same index. */
 int pqtg_index_attach_database(pqtg_index* index, const float* rows, uint64_t n, uint32_t dim);
 void pqtg_index_destroy(pqtg_index* index);
@@ -269,8 +271,9 @@ int pqtg_shard_range(uint64_t n, uint32_t shards, uint32_t rank, uint64_t* lo, u
  * Collectives: NCCL over NVLink (one process per GPU, pqtg_sharded_create_nccl; libnccl.so.2 is
  * loaded at run time) or, with every shard in this process (pqtg_sharded_create_local, any
  * devices), device-to-device copies -- the same protocol, used by the single-GPU tests.
- * Calls are collective: every rank calls with the same nq and k. Exact re-ranking is not
- * available on shards (PQTG_ERR_UNSUPPORTED from pqtg_index_attach_database). */
+ * Calls are collective: every rank calls with the same nq and k. With raw rows attached to every
+ * shard (pqtg_index_attach_database of its positions) the exact stage runs across the shards: each
+ * ships its line prefix with exact distances, the merge reproduces the reference's prefix cut. */
 typedef struct pqtg_sharded pqtg_sharded;
 #define PQTG_NCCL_ID_BYTES 128
 /* A fresh NCCL unique id (ncclGetUniqueId) for rank 0 to hand to every rank. PQTG_ERR_NCCL if
