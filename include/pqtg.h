@@ -178,8 +178,9 @@ void pqtg_workspace_destroy(pqtg_workspace* ws);
 /* Split each (sub-)batch into `chunks` pieces that alternate between two streams so one
  * piece's re-rank overlaps the next piece's traversal / bin selection (and, in pqtg_search, the
  * copies). 0 = automatic (2 from 256 queries; 4 for host batches from 4096), 1 = no overlap.
- * Results are identical. Calls on one workspace serialise on its lock; use one workspace per
- * concurrent caller. */
+ * Results are identical. Calls on one workspace serialise on its lock (host) and on the device:
+ * each call's work starts after the previous call's (any stream, either entry point). Use one
+ * workspace per concurrent caller. */
 int pqtg_workspace_set_chunks(pqtg_workspace* ws, uint32_t chunks);
 /* Device milliseconds of the last pqtg_search* call per stage: [0] traversal, [1] bin
  * selection + gather, [2] re-rank + top-k, [3] whole search — of the call's first chunk (see

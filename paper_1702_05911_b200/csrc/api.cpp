@@ -37,6 +37,7 @@ Workspace::~Workspace() {
         if (e) cudaEventDestroy(e);
     if (join) cudaEventDestroy(join);
     if (fork) cudaEventDestroy(fork);
+    if (done) cudaEventDestroy(done);
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (aux_stream) cudaStreamDestroy(aux_stream);
@@ -443,6 +444,8 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         PQTG_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->aux_stream, cudaStreamNonBlocking));
         PQTG_CUDA_CHECK(cudaEventCreateWithFlags(&ws->join, cudaEventDisableTiming));
         PQTG_CUDA_CHECK(cudaEventCreateWithFlags(&ws->fork, cudaEventDisableTiming));
+        PQTG_CUDA_CHECK(cudaEventCreateWithFlags(&ws->done, cudaEventDisableTiming));
+        PQTG_CUDA_CHECK(cudaEventRecord(ws->done, ws->own_stream));
         for (auto& e : ws->ev) PQTG_CUDA_CHECK(cudaEventCreate(&e));
         const uint64_t B = max_batch;
         ws->fine = dev_alloc<float>(ws->allocations, B * p.L * p.k1);
@@ -557,9 +560,11 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         ensure_exact(ws, k);
         ensure_keys(ws, k);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        // the workspace's aux stream may still run a previous call's chunks on these slices
+        // the workspace's aux stream may still run a previous call's chunks on these slices, and
+        // the previous call may have run on another stream (or through pqtg_search)
         PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
         PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));
+        PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.done, 0));
         if (index->dev->prm.exact_order) PQTG_CUDA_CHECK(cudaMemsetAsync(ws.err, 0, sizeof(uint32_t), s));
         ws.last_stream = s;
         ws.last_nq = nq;
@@ -573,6 +578,7 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         const uint64_t nch = ws.chunks ? ws.chunks : (nq >= 256 && (nq < 4096 || !shard) ? 2 : 1);
         if (nch <= 1 || nq < nch) {
             run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, s, true);
+            PQTG_CUDA_CHECK(cudaEventRecord(ws.done, s));
             return PQTG_OK;
         }
         // chunks alternate between the caller's stream and the workspace's aux stream (forked
@@ -590,6 +596,7 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         }
         PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
         PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));
+        PQTG_CUDA_CHECK(cudaEventRecord(ws.done, s));
         return PQTG_OK;
     });
 }
@@ -607,6 +614,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         std::lock_guard<std::mutex> lock(ws.mu);
         PQTG_CUDA_CHECK(cudaSetDevice(d.device));
         refuse_shard_exact(d.prm);
+        PQTG_CUDA_CHECK(cudaStreamWaitEvent(ws.own_stream, ws.done, 0));  // a previous pqtg_search_device call
         ensure_staging(ws, std::max<uint32_t>(k, 1));
         ensure_exact(ws, k);
         ensure_keys(ws, k);
@@ -674,6 +682,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
             enqueue();
             PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
             PQTG_CUDA_CHECK(cudaStreamSynchronize(st[1]));
+            PQTG_CUDA_CHECK(cudaEventRecord(ws.done, st[0]));
             check_exact();
             return PQTG_OK;
         }
@@ -722,6 +731,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         hit->used = ++ws.graph_clock;
         PQTG_CUDA_CHECK(cudaGraphLaunch(hit->exec, st[0]));
         PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
+        PQTG_CUDA_CHECK(cudaEventRecord(ws.done, st[0]));
         check_exact();
         return PQTG_OK;
     });

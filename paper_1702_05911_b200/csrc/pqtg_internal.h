@@ -161,6 +161,8 @@ struct Workspace {
     uint32_t chunks = 0;                // sub-batch chunks per search (0 = automatic)
     cudaEvent_t join = nullptr;
     cudaEvent_t fork = nullptr;         // graph capture: brings aux_stream into the capture
+    cudaEvent_t done = nullptr;         // the end of the last call's work on its stream: the next call
+                                        // (any stream, either entry point) starts after it
     // pqtg_search replays: CUDA graphs of whole host-buffer searches, keyed by their arguments
     struct GraphEntry {
         uint64_t key[12];
