@@ -153,17 +153,18 @@ def test_gpu_line_counts(p_line):
     assert_same_results(got, want, f"L={p_line}")
 
 
-def test_gpu_sharded_index_refuses_raw_vectors():
-    """Exact re-rank needs every candidate's row: a position shard refuses attach_database."""
+def test_gpu_sharded_index_raw_vectors_are_the_shards_rows():
+    """A position shard's attach_database takes its own rows (db[ids[lo:hi]], position order):
+    the full set is refused like a mismatched set in the reference (search.cpp:46-48)."""
     from paper_1702_05911_b200 import HostIndex
-    from paper_1702_05911_b200._abi import PqtgError
 
     path = str(GOLDEN / "p2_exact.pqt")
     g = load_golden("p2_exact")
     hix = HostIndex.load(path)
     shard = DeviceIndex(hix, shard=(0, hix.n // 2))
-    with pytest.raises(PqtgError):
+    with pytest.raises(ValueError):
         shard.attach_database(g["db"])
+    shard.attach_database(g["db"][hix.ids[: hix.n // 2].astype(np.int64)])
 
 
 def test_gpu_sharded_build_equals_full_build():
