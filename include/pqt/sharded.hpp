@@ -8,6 +8,7 @@
 #include <array>
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "pqt/search.hpp"
@@ -36,6 +37,12 @@ public:
     // rank 0 only and broadcast); every rank gets all results.
     std::vector<QueryResult> knn_query_batch(const VectorSet& queries, std::uint32_t k);
 
+    // PqtIndex::attach_database (search.cpp:44-49) for this rank: its positions' raw rows in
+    // position order (db rows ids[lo..hi)); with rows on every rank and rerank_exact > 0 the
+    // exact stage runs across the shards. nullptr detaches. Not concurrent with a search.
+    void attach_database(const VectorSet* shard_rows);
+    std::pair<std::uint64_t, std::uint64_t> positions() const { return {lo_, hi_}; }
+
     std::size_t size() const { return n_; }
     std::uint32_t rank() const { return rank_; }
 
@@ -43,6 +50,7 @@ private:
     pqtg_index* shard_ = nullptr;
     pqtg_sharded* sh_ = nullptr;
     std::size_t n_ = 0;
+    std::uint64_t lo_ = 0, hi_ = 0;
     std::uint32_t dim_ = 0, rank_ = 0;
     std::size_t max_batch_ = 0;
 };

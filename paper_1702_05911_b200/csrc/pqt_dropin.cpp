@@ -449,6 +449,8 @@ ShardedIndex::ShardedIndex(const std::string& path, std::uint32_t rank, std::uin
     }
     std::uint64_t lo = 0, hi = 0;
     check(pqtg_shard_range(n_, world, rank, &lo, &hi));
+    lo_ = lo;
+    hi_ = hi;
     if (world == 1) lo = hi = 0;
     check(pqtg_index_load(path.c_str(), device, lo, hi, &shard_));
     const int rc = pqtg_sharded_create_nccl(shard_, id.data(), rank, world, max_batch, &sh_);
@@ -457,6 +459,14 @@ ShardedIndex::ShardedIndex(const std::string& path, std::uint32_t rank, std::uin
         shard_ = nullptr;
         rethrow(rc);
     }
+}
+
+void ShardedIndex::attach_database(const VectorSet* shard_rows) {
+    if (!shard_rows) {
+        check(pqtg_index_attach_database(shard_, nullptr, 0, 0));
+        return;
+    }
+    check(pqtg_index_attach_database(shard_, shard_rows->data.data(), shard_rows->count(), shard_rows->dim));
 }
 
 ShardedIndex::~ShardedIndex() {
