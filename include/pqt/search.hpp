@@ -9,8 +9,9 @@
 //  * exact re-ranking against attached raw vectors runs on the GPU (the database is copied to
 //    the device on the first query after attach_database); without one the calls warn once and
 //    disable it, exactly as the reference does (search.cpp:25-32);
-//  * QueryStats *_us are the batch call's wall time divided evenly over its queries, split over
-//    the stages in proportion to their device times.
+//  * QueryStats *_us are each query's per-stage device wall times (its stage kernels' CTAs, with
+//    the batch's other queries running beside them); bin selection and candidate gathering are one
+//    kernel, reported as bin_selection_us (vector_proposal_us = 0).
 #pragma once
 
 #include <cstdint>

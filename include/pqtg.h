@@ -191,6 +191,16 @@ int pqtg_workspace_stage_ms(pqtg_workspace* ws, float* ms4);
  * (that query's candidate list is truncated). pqtg_search checks this itself; a caller of the
  * asynchronous pqtg_search_device checks it here (pqtg_workspace_stage_ms reports it too). */
 int pqtg_workspace_status(pqtg_workspace* ws);
+/* Per-query stage clocks -- the GPU counterpart of the reference's per-query timers
+ * (QueryStats::traversal_us / bin_selection_us / vector_proposal_us / rerank_us,
+ * src/search.cpp:134-137,167-216,220,258): with them enabled, each query's traversal, bin
+ * selection + gather and re-rank (+ exact) kernels record the first start and the last end of
+ * their CTAs for that query (globaltimer). pqtg_workspace_read_query_times gives, for the last
+ * call's queries (pqtg_search: all sub-batches; pqtg_search_device: its batch), nq × 3 stage
+ * durations in microseconds. A query's stage duration is its CTAs' wall time on the device, with
+ * the batch's other queries running beside it. */
+int pqtg_workspace_query_times(pqtg_workspace* ws, int enable);
+int pqtg_workspace_read_query_times(pqtg_workspace* ws, uint64_t nq, float* us3);
 /* Copy per-query intermediates of the LAST sub-batch searched with `ws` to host buffers
  * (any pointer may be NULL). Used by the per-stage parity tests.
  *   fine         nq × p_line × k1              traversal fine_dists (pqtree.cpp:84-97)

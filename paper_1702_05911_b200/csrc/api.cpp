@@ -38,6 +38,7 @@ Workspace::~Workspace() {
     if (join) cudaEventDestroy(join);
     if (fork) cudaEventDestroy(fork);
     if (done) cudaEventDestroy(done);
+    if (h_qtime) cudaFreeHost(h_qtime);
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (aux_stream) cudaStreamDestroy(aux_stream);
@@ -207,8 +208,12 @@ namespace {
 // ev[0..3] bracket the stages when `timed` (the first chunk of a call).
 void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_queries, uint64_t nq, uint32_t k,
                uint32_t* d_ids, float* d_dists, uint32_t* d_counts, pqtg_query_stats* d_stats, cudaStream_t s,
-               bool timed) {
-    const DevParams& p = ix.prm;
+               bool timed, unsigned long long* h_qt = nullptr) {
+    DevParams p = ix.prm;
+    if (ws.qtime_on && nq) {  // per-query stage clocks of this chunk (pqtg_workspace_query_times)
+        p.qtime = ws.qtime + q0 * 6;
+        PQTG_CUDA_CHECK(cudaMemsetAsync(p.qtime, 0, nq * 6 * sizeof(unsigned long long), s));
+    }
     if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[0], s));
     if (nq == 0 || k == 0 || ix.n == 0) {  // search.cpp:130-132: empty results, zero stats
         if (nq) {
@@ -221,6 +226,8 @@ void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_qu
         }
         if (timed)
             for (int i = 1; i < 4; ++i) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[i], s));
+        if (h_qt && p.qtime && nq)
+            PQTG_CUDA_CHECK(cudaMemcpyAsync(h_qt, p.qtime, nq * 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         return;
     }
     const WsSlice sl = ws.slice(q0);
@@ -240,6 +247,8 @@ void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_qu
         launch_rerank(p, nq, k, sl, d_ids, d_dists, d_counts, s);
     }
     if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[3], s));
+    if (h_qt && p.qtime)
+        PQTG_CUDA_CHECK(cudaMemcpyAsync(h_qt, p.qtime, nq * 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
 }
 
 }  // namespace
@@ -495,6 +504,48 @@ int pqtg_workspace_stage_ms(pqtg_workspace* h, float* ms4) {
     });
 }
 
+int pqtg_workspace_query_times(pqtg_workspace* h, int enable) {
+    return guarded([&] {
+        if (!h) throw Error{PQTG_ERR_ARG, "null argument"};
+        Workspace& ws = *h->ws;
+        std::lock_guard<std::mutex> lock(ws.mu);
+        PQTG_CUDA_CHECK(cudaSetDevice(ws.index->device));
+        if (enable && !ws.qtime) ws.qtime = dev_alloc<unsigned long long>(ws.allocations, ws.max_batch * 6);
+        ws.qtime_on = enable != 0;
+        ++ws.gen;
+        return PQTG_OK;
+    });
+}
+
+int pqtg_workspace_read_query_times(pqtg_workspace* h, uint64_t nq, float* us) {
+    return guarded([&] {
+        if (!h || (nq && !us)) throw Error{PQTG_ERR_ARG, "null argument"};
+        Workspace& ws = *h->ws;
+        std::lock_guard<std::mutex> lock(ws.mu);
+        if (!ws.qtime_on) throw Error{PQTG_ERR_ARG, "per-query times are not enabled on this workspace"};
+        PQTG_CUDA_CHECK(cudaSetDevice(ws.index->device));
+        std::vector<unsigned long long> raw;
+        const unsigned long long* src = nullptr;
+        if (ws.qtime_host) {
+            if (nq > ws.qtime_cap) throw Error{PQTG_ERR_ARG, "nq exceeds the last search"};
+            PQTG_CUDA_CHECK(cudaStreamSynchronize(ws.own_stream));
+            src = ws.h_qtime;
+        } else {
+            if (nq > ws.last_nq) throw Error{PQTG_ERR_ARG, "nq exceeds the last searched batch"};
+            if (ws.last_stream) PQTG_CUDA_CHECK(cudaStreamSynchronize(ws.last_stream));
+            PQTG_CUDA_CHECK(cudaStreamSynchronize(ws.aux_stream));
+            raw.resize(nq * 6);
+            PQTG_CUDA_CHECK(cudaMemcpy(raw.data(), ws.qtime, nq * 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            src = raw.data();
+        }
+        for (uint64_t q = 0; q < nq * 3; ++q) {
+            const unsigned long long start = ~src[2 * q], end = src[2 * q + 1];
+            us[q] = (src[2 * q] && end >= start) ? (float)((double)(end - start) * 1e-3) : 0.0f;
+        }
+        return PQTG_OK;
+    });
+}
+
 int pqtg_workspace_status(pqtg_workspace* h) {
     return guarded([&] {
         if (!h) throw Error{PQTG_ERR_ARG, "null argument"};
@@ -567,6 +618,7 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.done, 0));
         if (index->dev->prm.exact_order) PQTG_CUDA_CHECK(cudaMemsetAsync(ws.err, 0, sizeof(uint32_t), s));
         ws.last_stream = s;
+        ws.qtime_host = false;
         ws.last_nq = nq;
         // device-resident batches: two chunks on two streams, so the next chunk's traversal and bin
         // selection fill the SMs the re-rank's last wave leaves idle (tools/e2e_probe.py on B200,
@@ -616,6 +668,15 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         refuse_shard_exact(d.prm);
         PQTG_CUDA_CHECK(cudaStreamWaitEvent(ws.own_stream, ws.done, 0));  // a previous pqtg_search_device call
         ensure_staging(ws, std::max<uint32_t>(k, 1));
+        if (ws.qtime_on && ws.qtime_cap < nq) {  // the per-query clocks of the whole call (pinned)
+            PQTG_CUDA_CHECK(cudaStreamSynchronize(ws.own_stream));
+            if (ws.h_qtime) cudaFreeHost(ws.h_qtime);
+            ws.h_qtime = nullptr;
+            PQTG_CUDA_CHECK(cudaMallocHost(&ws.h_qtime, nq * 6 * sizeof(unsigned long long)));
+            ws.qtime_cap = nq;
+            ++ws.gen;
+        }
+        ws.qtime_host = true;
         ensure_exact(ws, k);
         ensure_keys(ws, k);
         const uint64_t D = d.prm.D;
@@ -644,7 +705,8 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
                     PQTG_CUDA_CHECK(cudaMemcpyAsync(ws.d_queries + c0 * D, queries + (q0 + c0) * D, cn * D * sizeof(float),
                                                     cudaMemcpyHostToDevice, s));
                     run_chunk(d, ws, c0, ws.d_queries + c0 * D, cn, k, ws.d_ids + c0 * std::max<uint32_t>(k, 1),
-                              ws.d_dists + c0 * std::max<uint32_t>(k, 1), ws.d_counts + c0, ws.d_stats + c0, s, c == 0);
+                              ws.d_dists + c0 * std::max<uint32_t>(k, 1), ws.d_counts + c0, ws.d_stats + c0, s, c == 0,
+                              ws.qtime_on ? ws.h_qtime + (q0 + c0) * 6 : nullptr);
                     if (k) {
                         PQTG_CUDA_CHECK(cudaMemcpyAsync(ids + (q0 + c0) * k, ws.d_ids + c0 * k, cn * k * sizeof(uint32_t),
                                                         cudaMemcpyDeviceToHost, s));

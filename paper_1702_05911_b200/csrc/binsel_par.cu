@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t q = blockIdx.x;
+    qt_begin(p, q, 1);
     const uint32_t W = p.W, PW = P * W;
     const uint32_t H = (uint32_t)p.H;
     const Layout lay = layout(PW, W2ab, HASH);
@@ -421,6 +422,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
             stats[q].exact_evals = 0;
         }
     }
+    qt_end(p, q, 1);
 }
 
 namespace {

@@ -11,6 +11,24 @@ namespace dev {
 constexpr int kThreads = 256;
 constexpr uint64_t kSentinel = ~0ull;
 
+// Per-query stage clock (pqtg_workspace_query_times): thread 0 of a query's CTA stores its start
+// complemented (so one atomicMax from a zeroed record keeps the earliest start) and every warp's
+// lane 0 its end (the latest end wins); p.qtime is [query][3 stages][start, end] in
+// globaltimer nanoseconds, or null when the workspace does not collect them.
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+template <class PR>
+__device__ __forceinline__ void qt_begin(const PR& p, uint64_t q, int stage) {
+    if (p.qtime && threadIdx.x == 0) atomicMax(p.qtime + (q * 3 + stage) * 2, ~gtimer_ns());
+}
+template <class PR>
+__device__ __forceinline__ void qt_end(const PR& p, uint64_t q, int stage) {
+    if (p.qtime && (threadIdx.x & 31) == 0) atomicMax(p.qtime + (q * 3 + stage) * 2 + 1, gtimer_ns());
+}
+
 __device__ __forceinline__ float sq_step(float acc, float a, float b) {
     const float d = __fsub_rn(a, b);
     return __fadd_rn(acc, __fmul_rn(d, d));

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(kExThreads) exact_rerank_kernel(DevParams p, c
     uint64_t* keys = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(y) + ((size_t)D * 4 + 15) / 16 * 16);
     __shared__ __align__(8) uint64_t full[kExStages];
     const uint64_t q = blockIdx.x;
+    qt_begin(p, q, 2);
     const uint32_t tid = threadIdx.x;
     const uint32_t n = line_counts[q];  // = rerank: min(max(k, rerank_exact), C) line-ranked candidates
     for (uint32_t t = tid; t < D; t += blockDim.x) y[t] = Q[q * D + t];
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(kExThreads) exact_rerank_kernel(DevParams p, c
     const uint32_t kk = n < k ? n : k;
     block_sort_write(keys, n, kk, k, q, out_ids, out_dists, out_counts);
     if (tid == 0 && stats) stats[q].exact_evals = n;
+    qt_end(p, q, 2);
 }
 
 size_t exact_smem(const DevParams& p, uint32_t kp) {

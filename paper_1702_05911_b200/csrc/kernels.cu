@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
     float* l2d = reinterpret_cast<float*>(l1o + P * k1);
     uint32_t* l2c = reinterpret_cast<uint32_t*>(l2d + P * W);
     const uint64_t q = blockIdx.x;
+    qt_begin(p, q, 0);
     const int tid = threadIdx.x;
 
     for (uint32_t i = tid; i < D; i += blockDim.x) y[i] = Q[q * D + i];
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
         l2d_out[o] = d;
         l2c_out[o] = code;
     }
+    qt_end(p, q, 0);
 }
 
 size_t traverse_smem(const DevParams& p) {
@@ -355,6 +357,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
     __shared__ typename Sort::TempStorage sort_tmp;
 
     const uint64_t q = blockIdx.x;
+    qt_begin(p, q, 1);
     const int tid = threadIdx.x;
 
     for (uint32_t idx = tid; idx < PW_; idx += blockDim.x) {
@@ -571,6 +574,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
             stats[q].exact_evals = 0;
         }
     }
+    qt_end(p, q, 1);
 }
 
 namespace {
@@ -747,6 +751,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     __shared__ TopkShared s_sel;
 
     const uint64_t q = blockIdx.x;
+    qt_begin(p, q, 2);
     const int tid = threadIdx.x;
     const uint32_t R = nranges[q], C = ncand[q];
     const uint2* qr = ranges + q * (uint64_t)budget;
@@ -789,6 +794,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
 
     block_topk(keys, C, kk, sel, sel_cap, hist, s_sel);
     write_topk(sel, kk, k, q, out_ids, out_dists, out_counts);
+    qt_end(p, q, 2);
 }
 
 namespace {

@@ -334,6 +334,7 @@ DeviceCopy& device_copy(const PqtIndex& index) {
     auto copy = std::make_shared<DeviceCopy>();
     check(pqtg_index_create(&v, device, &copy->ix));
     check(pqtg_workspace_create(copy->ix, 4096, &copy->ws));
+    check(pqtg_workspace_query_times(copy->ws, 1));  // QueryStats *_us per query (device clocks)
     copy->fingerprint = fp;
     index.gpu = copy;
     return *copy;
@@ -369,16 +370,13 @@ std::vector<QueryResult> knn_query_batch(const PqtIndex& index, const VectorSet&
     std::vector<std::uint32_t> ids(nq * k), counts(nq);
     std::vector<float> dists(nq * k);
     std::vector<pqtg_query_stats> stats(nq);
-    const auto t0 = std::chrono::steady_clock::now();
     check(pqtg_search(d.ix, d.ws, queries.data.data(), nq, queries.dim, k, ids.data(), dists.data(), counts.data(),
                       stats.data()));
-    const double wall_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-    // the reference times each query's stages (search.cpp:134-137,167-216,220,258); a batch on the
-    // GPU has one wall time: each query gets 1/nq of it, split by the stages' device-time shares
-    float ms[4] = {0, 0, 0, 0};
-    pqtg_workspace_stage_ms(d.ws, ms);
-    const double dev_ms = (double)ms[0] + ms[1] + ms[2];
-    const double per = wall_us / static_cast<double>(nq) / (dev_ms > 0 ? dev_ms : 1.0);
+    // the reference times each query's stages (search.cpp:134-137,167-216,220,258); here each
+    // query's stage kernels record their CTAs' device wall time (pqtg_workspace_query_times).
+    // Bin selection and candidate gathering are one kernel: its time is bin_selection_us.
+    std::vector<float> us(nq * 3);
+    check(pqtg_workspace_read_query_times(d.ws, nq, us.data()));
     for (std::size_t q = 0; q < nq; ++q) {
         QueryResult& r = results[q];
         r.ids.assign(ids.begin() + q * k, ids.begin() + q * k + counts[q]);
@@ -386,10 +384,10 @@ std::vector<QueryResult> knn_query_batch(const PqtIndex& index, const VectorSet&
         r.stats.bins_visited = stats[q].bins_visited;
         r.stats.candidates = stats[q].candidates;
         r.stats.exact_evals = stats[q].exact_evals;
-        r.stats.traversal_us = ms[0] * per;
-        r.stats.bin_selection_us = 0.5 * ms[1] * per;
-        r.stats.vector_proposal_us = 0.5 * ms[1] * per;
-        r.stats.rerank_us = ms[2] * per;
+        r.stats.traversal_us = us[q * 3];
+        r.stats.bin_selection_us = us[q * 3 + 1];
+        r.stats.vector_proposal_us = 0.0;
+        r.stats.rerank_us = us[q * 3 + 2];
     }
     return results;
 }

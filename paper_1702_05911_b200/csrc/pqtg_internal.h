@@ -88,6 +88,8 @@ struct DevParams {
     const float* scr_cn;        // [P][scr_nj] |c''|^2
     const float* scr_kc;        // [P][scr_nj] (mu_i - mu_p) . c''
     uint32_t scr_nj, scr_kpad;  // k1·k2 padded to the N tile; m padded to 16
+    // per-query stage clock of the current chunk ([q][3][~start, end] ns), null when not collected
+    unsigned long long* qtime;
 };
 
 struct DevIndex {
@@ -149,6 +151,11 @@ struct Workspace {
     uint32_t* ntuples = nullptr;  // [B] stream tuples consumed by the gather
     uint32_t* err = nullptr;      // [1] device error word (PQTG_WS_ERR_*)
     uint64_t* keys = nullptr;     // [B][budget] re-rank keys for budgets too large for shared memory
+    unsigned long long* qtime = nullptr;  // [B][3][2] per-query stage clock (pqtg_workspace_query_times)
+    unsigned long long* h_qtime = nullptr;  // pinned [qtime_cap][6]: the last pqtg_search call's clocks
+    uint64_t qtime_cap = 0;
+    bool qtime_on = false;
+    bool qtime_host = false;              // the last call was pqtg_search (clocks in h_qtime)
     uint64_t* split_keys = nullptr;   // small-batch split re-rank lists (see WsSlice)
     uint32_t* split_cnt = nullptr;
     uint32_t* split_ctr = nullptr;

@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
 
     const uint64_t q = blockIdx.x;
     const uint32_t tid = threadIdx.x;
+    qt_begin(p, q, 2);
     const uint32_t R = nranges[q], C = ncand[q];
     const uint2* qr = ranges + q * (uint64_t)budget;
 
@@ -486,6 +487,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     }
     if (gridDim.y == 1) {
         block_sort_write(sel, m, kk, k, q, out_ids, out_dists, out_counts);
+        qt_end(p, q, 2);
         return;
     }
     // split: this slice's top-kk keys to its list, then the query's last-arriving slice selects the
@@ -540,6 +542,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                                                      s_sel);
     }
     block_sort_write(sel, m2, k2, k, q, out_ids, out_dists, out_counts);
+    qt_end(p, q, 2);
 }
 
 namespace {

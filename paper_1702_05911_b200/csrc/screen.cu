@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
     __shared__ float s_yn[4];
 
     const uint64_t q = blockIdx.x / P;
+    qt_begin(p, q, 0);
     const uint32_t part = blockIdx.x - (uint32_t)q * P;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t jobs = pp * k1, f0 = part * pp;
@@ -469,6 +470,7 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
         l2d_out[out] = d;
         l2c_out[out] = code[j];
     }
+    qt_end(p, q, 0);
 }
 
 namespace {

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
 
     const uint64_t q = blockIdx.x / P;
     const uint32_t part = blockIdx.x - (uint32_t)q * P;
+    qt_begin(p, q, 0);
     const uint32_t tid = threadIdx.x;
     const uint32_t jobs = pp * k1;  // this part's fine LUT entries (f, i)
     const uint32_t f0 = part * pp;
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
         l2d_out[out] = unorderable((uint32_t)(key >> 32));
         l2c_out[out] = (uint32_t)key;
     }
+    qt_end(p, q, 0);
 }
 
 // Small trees (W = w·k2 <= 32, k1 <= 32, P <= 4): one CTA per query, one warp per part, no
@@ -266,6 +268,7 @@ __global__ void __launch_bounds__(128) traverse_warp_kernel(DevParams p, const f
     const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W;
     const uint64_t q = blockIdx.x;
     const uint32_t tid = threadIdx.x, lane = tid & 31, part = tid >> 5;
+    qt_begin(p, q, 0);
     float* y = reinterpret_cast<float*>(smem);                        // [D]
     float* fine = y + ((p.D + 3) & ~3u) + part * pp * 32;             // [P][pp][<= 32]
     float* l1d = y + ((p.D + 3) & ~3u) + P * pp * 32 + part * 32;     // [P][32]
@@ -333,6 +336,7 @@ __global__ void __launch_bounds__(128) traverse_warp_kernel(DevParams p, const f
         l2d_out[out] = unorderable((uint32_t)(key >> 32));
         l2c_out[out] = (uint32_t)key;
     }
+    qt_end(p, q, 0);
 }
 
 // Ascending bitonic sort of 32·EPT u64 keys held by one warp in registers, lane l holding keys
@@ -380,6 +384,7 @@ __global__ void __launch_bounds__(128) traverse_warp_wide_kernel(DevParams p, co
     constexpr uint32_t k1 = K1T, k2 = K2T;
     const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W;
     const uint64_t q = blockIdx.x;
+    qt_begin(p, q, 0);
     const uint32_t tid = threadIdx.x, lane = tid & 31, part = tid >> 5;
     float* y = reinterpret_cast<float*>(smem);
     float* fine = y + ((p.D + 3) & ~3u) + part * pp * 32;
@@ -461,6 +466,7 @@ __global__ void __launch_bounds__(128) traverse_warp_wide_kernel(DevParams p, co
             l2c_out[(q * P + part) * W + o] = (uint32_t)key[e];
         }
     }
+    qt_end(p, q, 0);
 }
 
 
@@ -512,6 +518,7 @@ __global__ void __launch_bounds__(kTpThreads) traverse_small_kernel(DevParams p,
     uint32_t* l1o = reinterpret_cast<uint32_t*>(smem + lay.l1o);
     const uint64_t q = blockIdx.x / P;
     const uint32_t part = blockIdx.x - (uint32_t)q * P;
+    qt_begin(p, q, 0);
     const uint32_t tid = threadIdx.x, f0 = part * pp;
     const uint32_t cb_bytes = k1 * m * k2 * 4, ft_bytes = pp * fd * k1 * 4;
     if (tid == 0) {
@@ -574,6 +581,7 @@ __global__ void __launch_bounds__(kTpThreads) traverse_small_kernel(DevParams p,
         l2d_out[out] = unorderable((uint32_t)(key >> 32));
         l2c_out[out] = (uint32_t)key;
     }
+    qt_end(p, q, 0);
 }
 
 namespace {

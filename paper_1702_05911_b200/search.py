@@ -25,7 +25,7 @@ from .index import FormatError, HostIndex, PqtConfig
 
 @dataclass
 class QueryStats:
-    """pqt::QueryStats (search.hpp:15-23); *_us are per-query shares of the batch's stage times."""
+    """pqt::QueryStats (search.hpp:15-23); *_us are the query's per-stage device times."""
 
     bins_visited: int = 0
     candidates: int = 0
@@ -92,6 +92,8 @@ class DeviceIndex:
         ws = C.c_void_p()
         check(L.pqtg_workspace_create(h, self.max_batch, C.byref(ws)))
         self._ws = ws
+        self._query_times = False
+        self.has_database = False
 
     def close(self):
         L = _abi._LIB
@@ -122,6 +124,7 @@ class DeviceIndex:
         shard's rows in position order (db[ids[lo:hi]]), used by the sharded search. None detaches."""
         if rows is None:
             check(lib().pqtg_index_attach_database(self._h, None, 0, 0))
+            self.has_database = False
             return
         r = np.ascontiguousarray(rows, np.float32)
         if r.ndim != 2:
@@ -132,6 +135,7 @@ class DeviceIndex:
             if e.status == -1:  # BAD_DIM: std::invalid_argument in the reference
                 raise ValueError(str(e)) from None
             raise
+        self.has_database = True
 
     @property
     def workspace(self):
@@ -173,6 +177,17 @@ class DeviceIndex:
             check(lib().pqtg_workspace_status(self._ws))
         except PqtgError as e:
             _raise(e)
+
+    def enable_query_times(self, on: bool = True) -> None:
+        """Collect per-query stage clocks (pqtg_workspace_query_times)."""
+        check(lib().pqtg_workspace_query_times(self._ws, 1 if on else 0))
+
+    def query_times(self, nq: int) -> np.ndarray:
+        """nq × 3 per-query stage device times of the last search, µs: traversal, bin
+        selection + gather, re-rank (+ exact) -- QueryStats' *_us (search.cpp:134-137)."""
+        us = np.zeros((nq, 3), np.float32)
+        check(lib().pqtg_workspace_read_query_times(self._ws, nq, us.ctypes.data))
+        return us
 
     def stage_ms(self) -> list[float]:
         ms = (C.c_float * 4)()
@@ -248,16 +263,20 @@ def knn_query_batch(index: DeviceIndex, queries: np.ndarray, k: int, threads: in
         q = q.reshape(1, -1)
     if q.shape[0] > 0 and q.shape[1] != index.config.dim:
         raise ValueError("knn_query_batch: query dimension mismatch")
-    if index.config.rerank_exact > 0 and k > 0 and index.n > 0 and q.shape[0] > 0:
+    if index.config.rerank_exact > 0 and k > 0 and index.n > 0 and q.shape[0] > 0 and not index.has_database:
         _warn_missing_database()
+    if not index._query_times:
+        index.enable_query_times()
+        index._query_times = True
     ids, dists, counts, stats = index.search(q, k)
-    ms = index.stage_ms() if q.shape[0] else [0.0] * 4
-    per = 1000.0 / max(q.shape[0], 1)
+    # each query's stage device times (search.cpp:134-137,167-216,220,258); bin selection and
+    # gathering are one kernel, reported as bin_selection_us
+    us = index.query_times(q.shape[0]) if q.shape[0] else np.zeros((0, 3), np.float32)
     out = []
     for i in range(q.shape[0]):
         c = int(counts[i])
         st = QueryStats(int(stats[i, 0]), int(stats[i, 1]), int(stats[i, 2]),
-                        ms[0] * per, ms[1] * per * 0.5, ms[1] * per * 0.5, ms[2] * per)
+                        float(us[i, 0]), float(us[i, 1]), 0.0, float(us[i, 2]))
         out.append(QueryResult(ids[i, :c].copy(), dists[i, :c].copy(), st))
     return out
 
