@@ -128,7 +128,10 @@ std::vector<uint64_t> host_chunks(const Workspace& ws, uint64_t b) {
             c = *end ? end + 1 : end;
         }
     } else if (b >= 4096) {
-        w = {1, 1, 1, 1};  // SIFT1M 10k queries: e2e 6.66 (2 chunks) -> 6.95 M q/s
+        // small first / last chunks: only they expose their copies (the first H2D, the last D2H);
+        // DEEP100M 10k queries, host-call median: 1,1,1,1 1.75 ms, 1,2,2,1 1.64, 1,3,3,3,1 1.65,
+        // 1,4,4,1 1.60 ms (profiles/r02/e2e_chunk_plans.md)
+        w = {1, 4, 4, 1};
     } else if (b >= 256) {
         w = {1, 1};
     }
