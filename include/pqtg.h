@@ -200,6 +200,10 @@ int pqtg_workspace_status(pqtg_workspace* ws);
  * durations in microseconds. A query's stage duration is its CTAs' wall time on the device, with
  * the batch's other queries running beside it. */
 int pqtg_workspace_query_times(pqtg_workspace* ws, int enable);
+/* Diagnostic: phase clocks (ns) of the re-rank's first CTA in its last launch -- start, prologue,
+ * range map, candidates scored, selected, written, merged (split) -- when the process started with
+ * PQTG_PHASES=1 (tools/phase_probe.py); PQTG_ERR_ARG otherwise. */
+int pqtg_debug_rerank_phases(uint64_t* out7);
 int pqtg_workspace_read_query_times(pqtg_workspace* ws, uint64_t nq, float* us3);
 /* Copy per-query intermediates of the LAST sub-batch searched with `ws` to host buffers
  * (any pointer may be NULL). Used by the per-stage parity tests.

@@ -507,6 +507,17 @@ int pqtg_workspace_stage_ms(pqtg_workspace* h, float* ms4) {
     });
 }
 
+// diagnostic: the re-rank's phase clocks of CTA (0, 0) of its last launch (PQTG_PHASES=1), ns
+int pqtg_debug_rerank_phases(uint64_t* out7) {
+    return guarded([&] {
+        unsigned long long* b = phase_buffer();
+        if (!b || !out7) throw Error{PQTG_ERR_ARG, "phase clocks are off (PQTG_PHASES=1 enables them)"};
+        PQTG_CUDA_CHECK(cudaDeviceSynchronize());
+        for (int i = 0; i < 7; ++i) out7[i] = b[i];
+        return PQTG_OK;
+    });
+}
+
 int pqtg_workspace_query_times(pqtg_workspace* h, int enable) {
     return guarded([&] {
         if (!h) throw Error{PQTG_ERR_ARG, "null argument"};

@@ -288,6 +288,7 @@ uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k);  // CTAs per
 bool rerank_needs_gkeys(const DevParams& p, uint32_t k);  // launch_rerank will use ws.keys
 int optin_bytes();  // the device's opt-in shared memory per block
 void configure_rerank_ij();
+unsigned long long* phase_buffer();  // PQTG_PHASES=1: the re-rank's phase clocks (managed memory), else null
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids,
                       float* dists, uint32_t* counts, cudaStream_t s);
 // binsel_fast.cu (no resort, 32-bit slot arithmetic)

@@ -31,6 +31,15 @@ namespace pqtg {
 
 using namespace dev;
 
+// phase clocks of CTA (0, 0) of the last re-rank launch (PQTG_PHASES=1: tools/phase_probe.py);
+// null otherwise. [0] start, [1] prologue done, [2] range map done, [3] candidates scored,
+// [4] selected, [5] written (split: the slice's list), [6] merged (split's last slice)
+__device__ unsigned long long* g_phase = nullptr;
+#define PQTG_PHASE(i)                                                                                  \
+    do {                                                                                               \
+        if (g_phase && blockIdx.x == 0 && threadIdx.x == 0 && (blockIdx.y == 0 || (i) == 6)) g_phase[i] = gtimer_ns(); \
+    } while (0)
+
 namespace {
 
 // threads per CTA: 512, two CTAs (queries) per SM. (1024-thread CTAs, one query per SM, cut the
@@ -180,6 +189,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     const uint64_t q = blockIdx.x;
     const uint32_t tid = threadIdx.x;
     qt_begin(p, q, 2);
+    PQTG_PHASE(0);
     const uint32_t R = nranges[q], C = ncand[q];
     const uint2* qr = ranges + q * (uint64_t)budget;
 
@@ -291,7 +301,9 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         }
     }
     __syncthreads();
+    PQTG_PHASE(1);
     range_index_scan<kIjThreads>(rid, Cn, wmax);
+    PQTG_PHASE(2);
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     constexpr int kVec = ((K1M == 16 ? 2 : 3) * LT + 15) / 16;
@@ -476,6 +488,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         atomicOr(&s_sel.kor, ((unsigned long long)kor << 32) | 0xFFFFFFFFull);
     }
     __syncthreads();
+    PQTG_PHASE(3);
     const uint32_t nvalid = s_count;
     const uint32_t kk = nvalid < k ? nvalid : k;
     uint32_t m = 0;
@@ -485,8 +498,10 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         m = block_select_wide<kSelBits, kIjThreads>(keys + jlo, jhi - jlo, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap,
                                                     wmax, s_sel);
     }
+    PQTG_PHASE(4);
     if (gridDim.y == 1) {
         block_sort_write(sel, m, kk, k, q, out_ids, out_dists, out_counts);
+        PQTG_PHASE(5);
         qt_end(p, q, 2);
         return;
     }
@@ -495,6 +510,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     const uint32_t S = gridDim.y;
     uint64_t* lst = split_keys + ((uint64_t)q * kSplitMax + blockIdx.y) * k;
     block_rank_keys(sel, m, kk, lst);
+    PQTG_PHASE(5);
     if (tid == 0) split_cnt[q * kSplitMax + blockIdx.y] = kk;
     __threadfence();
     __syncthreads();
@@ -542,6 +558,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                                                      s_sel);
     }
     block_sort_write(sel, m2, k2, k, q, out_ids, out_dists, out_counts);
+    PQTG_PHASE(6);
     qt_end(p, q, 2);
 }
 
@@ -612,7 +629,21 @@ bool rerank_ij_ok(const DevParams& p, uint32_t k) {
            ij_smem(p, k, true) + 4096 <= (size_t)optin;
 }
 
+unsigned long long* phase_buffer() {
+    static unsigned long long* buf = [] {
+        unsigned long long* b = nullptr;
+        const char* e = std::getenv("PQTG_PHASES");
+        if (e && std::strcmp(e, "1") == 0 && cudaMallocManaged(&b, 8 * sizeof(unsigned long long)) == cudaSuccess) {
+            std::memset(b, 0, 8 * sizeof(unsigned long long));
+            cudaMemcpyToSymbol(g_phase, &b, sizeof(b));
+        }
+        return b;
+    }();
+    return buf;
+}
+
 void configure_rerank_ij() {
+    phase_buffer();
     int dev = 0, optin = 0;
     PQTG_CUDA_CHECK(cudaGetDevice(&dev));
     PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
