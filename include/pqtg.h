@@ -203,7 +203,10 @@ int pqtg_workspace_query_times(pqtg_workspace* ws, int enable);
 /* Diagnostic: phase clocks (ns) of the re-rank's first CTA in its last launch -- start, prologue,
  * range map, candidates scored, selected, written, merged (split) -- when the process started with
  * PQTG_PHASES=1 (tools/phase_probe.py); PQTG_ERR_ARG otherwise. */
-int pqtg_debug_rerank_phases(uint64_t* out7);
+int pqtg_debug_rerank_phases(uint64_t* out16);
+/* Diagnostic: the raw per-query stage clocks of the last pqtg_search_device call (globaltimer
+ * ns, nq x 3 stages x [start, end]) when per-query times are on. */
+int pqtg_debug_query_clocks(pqtg_workspace* ws, uint64_t nq, uint64_t* out);
 int pqtg_workspace_read_query_times(pqtg_workspace* ws, uint64_t nq, float* us3);
 /* Copy per-query intermediates of the LAST sub-batch searched with `ws` to host buffers
  * (any pointer may be NULL). Used by the per-stage parity tests.

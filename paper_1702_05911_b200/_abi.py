@@ -108,6 +108,7 @@ SIGNATURES = {
     "pqtg_workspace_status": (C.c_int, [_vp]),
     "pqtg_workspace_query_times": (C.c_int, [_vp, C.c_int]),
     "pqtg_debug_rerank_phases": (C.c_int, [_vp]),
+    "pqtg_debug_query_clocks": (C.c_int, [_vp, C.c_uint64, _vp]),
     "pqtg_workspace_read_query_times": (C.c_int, [_vp, _u64, _vp]),
     "pqtg_workspace_read": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pqtg_search": (C.c_int, [_vp, _vp, _vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp]),

@@ -67,7 +67,6 @@ WsSlice Workspace::slice(uint64_t q0) const {
     s.err = err;
     s.keys = keys ? keys + q0 * std::max<uint64_t>(p.budget, 1) : nullptr;
     s.split_keys = split_keys;
-    s.split_cnt = split_cnt;
     s.split_ctr = split_ctr;
     s.split_q = split_q;
     s.split_k = split_k;
@@ -165,7 +164,6 @@ void ensure_keys(Workspace& ws, uint32_t k) {
     const uint64_t sq = std::min<uint64_t>(ws.max_batch, kSplitBelow);
     if (kk && rerank_split(p, 1, kk) > 1 && (ws.split_k < kk || ws.split_q < sq)) {
         ws.split_keys = dev_alloc<uint64_t>(ws.allocations, (uint64_t)kSplitMax * sq * kk);
-        ws.split_cnt = dev_alloc<uint32_t>(ws.allocations, (uint64_t)kSplitMax * sq);
         ws.split_ctr = dev_alloc<uint32_t>(ws.allocations, sq);
         PQTG_CUDA_CHECK(cudaMemset(ws.split_ctr, 0, sq * sizeof(uint32_t)));
         ws.split_q = sq;
@@ -207,17 +205,37 @@ void prepare_workspace(Workspace& ws, uint32_t k) {
 
 namespace {
 
+// A stage event: an external event node when s is being captured (a plain record there only
+// orders the capture and is never timed), a plain record otherwise.
+void record_stage(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    PQTG_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+    PQTG_CUDA_CHECK(cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                                        : cudaEventRecord(e, s));
+}
+
 // The three stages for queries [q0, q0 + nq) of the current sub-batch on stream s. Events
-// ev[0..3] bracket the stages when `timed` (the first chunk of a call).
+// ev[0..3] bracket the stages when `timed` (the first chunk of a call); recorded as external
+// events, so a captured search (CUDA graph) records them when it replays.
 void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_queries, uint64_t nq, uint32_t k,
                uint32_t* d_ids, float* d_dists, uint32_t* d_counts, pqtg_query_stats* d_stats, cudaStream_t s,
                bool timed, unsigned long long* h_qt = nullptr) {
     DevParams p = ix.prm;
+    // small chunks are launch-latency bound: their stages run as one PDL chain, without the stage
+    // events between the kernels (pqtg_workspace_stage_ms then reports the whole search only;
+    // pqtg_workspace_query_times has the per-stage clocks). PQTG_CHAIN=0 disables, =all chains
+    // every chunk.
+    static const int chain_mode = [] {
+        const char* e = std::getenv("PQTG_CHAIN");
+        return !e ? 1 : std::strcmp(e, "0") == 0 ? 0 : std::strcmp(e, "all") == 0 ? 2 : 1;
+    }();
+    p.chain = chain_mode == 2 || (chain_mode == 1 && nq < kChainBelow) ? 1u : 0u;
+    if (timed) ws.stages_timed = !p.chain;
     if (ws.qtime_on && nq) {  // per-query stage clocks of this chunk (pqtg_workspace_query_times)
         p.qtime = ws.qtime + q0 * 6;
         PQTG_CUDA_CHECK(cudaMemsetAsync(p.qtime, 0, nq * 6 * sizeof(unsigned long long), s));
     }
-    if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[0], s));
+    if (timed) record_stage(ws.ev[0], s);
     if (nq == 0 || k == 0 || ix.n == 0) {  // search.cpp:130-132: empty results, zero stats
         if (nq) {
             PQTG_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, nq * sizeof(uint32_t), s));
@@ -228,16 +246,16 @@ void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_qu
             }
         }
         if (timed)
-            for (int i = 1; i < 4; ++i) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[i], s));
+            for (int i = 1; i < 4; ++i) record_stage(ws.ev[i], s);
         if (h_qt && p.qtime && nq)
             PQTG_CUDA_CHECK(cudaMemcpyAsync(h_qt, p.qtime, nq * 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         return;
     }
     const WsSlice sl = ws.slice(q0);
     launch_traverse(p, d_queries, nq, sl, s);
-    if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[1], s));
+    if (timed && !p.chain) record_stage(ws.ev[1], s);
     launch_binsel(p, nq, sl, d_stats, s);
-    if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[2], s));
+    if (timed && !p.chain) record_stage(ws.ev[2], s);
     if (p.db && p.rerank_exact > 0) {
         // exact re-rank (search.cpp:229-249): K5 keeps the k' = max(k, rerank_exact) best by
         // line distance (the reference's partial_sort prefix, :239-240), K6 replaces their
@@ -249,9 +267,53 @@ void run_chunk(const DevIndex& ix, Workspace& ws, uint64_t q0, const float* d_qu
     } else {
         launch_rerank(p, nq, k, sl, d_ids, d_dists, d_counts, s);
     }
-    if (timed) PQTG_CUDA_CHECK(cudaEventRecord(ws.ev[3], s));
+    if (timed) record_stage(ws.ev[3], s);
     if (h_qt && p.qtime)
         PQTG_CUDA_CHECK(cudaMemcpyAsync(h_qt, p.qtime, nq * 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+}
+
+// The cached CUDA graph of `enqueue` (work captured on stream cs, which forks to and joins
+// back from the workspace's aux stream) for these arguments, captured on a miss; least
+// recently used of at most 8 evicted.
+template <class F>
+cudaGraphExec_t cached_graph(Workspace& ws, const uint64_t (&key)[12], cudaStream_t cs, F&& enqueue) {
+    Workspace::GraphEntry* hit = nullptr;
+    for (auto& g : ws.graphs)
+        if (std::memcmp(g.key, key, sizeof(key)) == 0) hit = &g;
+    if (!hit) {
+        cudaGraph_t graph = nullptr;
+        PQTG_CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        try {
+            PQTG_CUDA_CHECK(cudaEventRecord(ws.fork, cs));
+            PQTG_CUDA_CHECK(cudaStreamWaitEvent(ws.aux_stream, ws.fork, 0));
+            enqueue();
+            PQTG_CUDA_CHECK(cudaEventRecord(ws.fork, ws.aux_stream));
+            PQTG_CUDA_CHECK(cudaStreamWaitEvent(cs, ws.fork, 0));
+        } catch (...) {
+            cudaStreamEndCapture(cs, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            throw;
+        }
+        PQTG_CUDA_CHECK(cudaStreamEndCapture(cs, &graph));
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        PQTG_CUDA_CHECK(e);
+        if (ws.graphs.size() >= 8) {  // evict the least recently used
+            auto lru = std::min_element(ws.graphs.begin(), ws.graphs.end(),
+                                        [](const auto& x, const auto& y) { return x.used < y.used; });
+            cudaGraphExecDestroy(lru->exec);
+            ws.graphs.erase(lru);
+        }
+        Workspace::GraphEntry g{};
+        std::memcpy(g.key, key, sizeof(key));
+        g.exec = exec;
+        ws.graphs.push_back(g);
+        hit = &ws.graphs.back();
+    }
+    hit->used = ++ws.graph_clock;
+    return hit->exec;
 }
 
 }  // namespace
@@ -500,7 +562,10 @@ int pqtg_workspace_stage_ms(pqtg_workspace* h, float* ms4) {
         if (!h || !ms4) throw Error{PQTG_ERR_ARG, "null argument"};
         Workspace& ws = *h->ws;
         PQTG_CUDA_CHECK(cudaEventSynchronize(ws.ev[3]));
-        for (int i = 0; i < 3; ++i) PQTG_CUDA_CHECK(cudaEventElapsedTime(&ms4[i], ws.ev[i], ws.ev[i + 1]));
+        for (int i = 0; i < 3; ++i) {
+            ms4[i] = -1.0f;  // a chained search has no events between its stages
+            if (ws.stages_timed) PQTG_CUDA_CHECK(cudaEventElapsedTime(&ms4[i], ws.ev[i], ws.ev[i + 1]));
+        }
         PQTG_CUDA_CHECK(cudaEventElapsedTime(&ms4[3], ws.ev[0], ws.ev[3]));
         check_ws_error(ws);
         return PQTG_OK;
@@ -508,12 +573,12 @@ int pqtg_workspace_stage_ms(pqtg_workspace* h, float* ms4) {
 }
 
 // diagnostic: the re-rank's phase clocks of CTA (0, 0) of its last launch (PQTG_PHASES=1), ns
-int pqtg_debug_rerank_phases(uint64_t* out7) {
+int pqtg_debug_rerank_phases(uint64_t* out16) {
     return guarded([&] {
         unsigned long long* b = phase_buffer();
-        if (!b || !out7) throw Error{PQTG_ERR_ARG, "phase clocks are off (PQTG_PHASES=1 enables them)"};
+        if (!b || !out16) throw Error{PQTG_ERR_ARG, "phase clocks are off (PQTG_PHASES=1 enables them)"};
         PQTG_CUDA_CHECK(cudaDeviceSynchronize());
-        for (int i = 0; i < 7; ++i) out7[i] = b[i];
+        PQTG_CUDA_CHECK(cudaMemcpy(out16, b, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
         return PQTG_OK;
     });
 }
@@ -556,6 +621,22 @@ int pqtg_workspace_read_query_times(pqtg_workspace* h, uint64_t nq, float* us) {
             const unsigned long long start = ~src[2 * q], end = src[2 * q + 1];
             us[q] = (src[2 * q] && end >= start) ? (float)((double)(end - start) * 1e-3) : 0.0f;
         }
+        return PQTG_OK;
+    });
+}
+
+// diagnostic: the raw per-query stage clocks (globaltimer ns: [q][stage][start, end]) of the last
+// pqtg_search_device call with per-query times on
+int pqtg_debug_query_clocks(pqtg_workspace* h, uint64_t nq, uint64_t* out) {
+    return guarded([&] {
+        if (!h || (nq && !out)) throw Error{PQTG_ERR_ARG, "null argument"};
+        Workspace& ws = *h->ws;
+        std::lock_guard<std::mutex> lock(ws.mu);
+        if (!ws.qtime_on || ws.qtime_host || nq > ws.last_nq)
+            throw Error{PQTG_ERR_ARG, "no per-query clocks of a device-entry search of this size"};
+        if (ws.last_stream) PQTG_CUDA_CHECK(cudaStreamSynchronize(ws.last_stream));
+        PQTG_CUDA_CHECK(cudaMemcpy(out, ws.qtime, nq * 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < nq * 3; ++i) out[2 * i] = ~out[2 * i];
         return PQTG_OK;
     });
 }
@@ -643,7 +724,26 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         const bool shard = pp.shard_hi > pp.shard_lo && (pp.shard_lo > 0 || pp.shard_hi < pp.n);
         const uint64_t nch = ws.chunks ? ws.chunks : (nq >= 256 && (nq < 4096 || !shard) ? 2 : 1);
         if (nch <= 1 || nq < nch) {
-            run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, s, true);
+            // Small batches are launch-bound (batch 1: ~3 µs in each kernel, ~7 µs of host API time
+            // between them): the second call in a row with the same arguments captures the stages
+            // as a CUDA graph and every later one replays it (PQTG_NO_GRAPH=1 disables).
+            static const bool no_graph = std::getenv("PQTG_NO_GRAPH") != nullptr;
+            const uint64_t key[12] = {(uint64_t)(uintptr_t)d_queries, nq, k, (uint64_t)(uintptr_t)d_ids,
+                                      (uint64_t)(uintptr_t)d_dists, (uint64_t)(uintptr_t)d_counts,
+                                      (uint64_t)(uintptr_t)d_stats, ws.gen, (uint64_t)kernel_variant(),
+                                      (uint64_t)(uintptr_t)index->dev->db, pp.rerank_exact,
+                                      0x9d5ea7c4f1e2b3a1ull};  // device-path tag
+            const bool repeat = std::memcmp(ws.dev_last_key, key, sizeof(key)) == 0;
+            std::memcpy(ws.dev_last_key, key, sizeof(key));
+            if (no_graph || nq == 0 || nq >= 256 || !repeat) {
+                run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, s, true);
+            } else {
+                const cudaGraphExec_t exec = cached_graph(ws, key, ws.own_stream, [&] {
+                    run_chunk(*index->dev, ws, 0, d_queries, nq, k, d_ids, d_dists, d_counts, d_stats, ws.own_stream,
+                              true);
+                });
+                PQTG_CUDA_CHECK(cudaGraphLaunch(exec, s));
+            }
             PQTG_CUDA_CHECK(cudaEventRecord(ws.done, s));
             return PQTG_OK;
         }
@@ -762,50 +862,52 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
             check_exact();
             return PQTG_OK;
         }
+        // Small batches write their results straight into the caller's page-locked buffers
+        // (mapped into the device's address space): the replayed graph is the query copy and the
+        // three kernels, with no result copies behind them (PQTG_ZERO_COPY=0 disables).
+        static const bool zero_copy = [] {
+            const char* e = std::getenv("PQTG_ZERO_COPY");
+            return !(e && std::strcmp(e, "0") == 0);
+        }();
+        auto mapped = [](void* ptr) -> void* {
+            if (!ptr) return nullptr;
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+            return a.devicePointer;
+        };
+        void* zc_out[4] = {mapped(ids), mapped(dists), mapped(counts), mapped(stats)};
+        const bool zc = zero_copy && nq <= 64 && nq <= ws.max_batch && (zc_out[0] || !ids) && (zc_out[1] || !dists) &&
+                        zc_out[2] && (zc_out[3] || !stats);
+        auto enqueue_zc = [&] {
+            if (d.prm.exact_order) PQTG_CUDA_CHECK(cudaMemsetAsync(ws.err, 0, sizeof(uint32_t), st[0]));
+            PQTG_CUDA_CHECK(cudaMemcpyAsync(ws.d_queries, queries, nq * D * sizeof(float), cudaMemcpyHostToDevice, st[0]));
+            run_chunk(d, ws, 0, ws.d_queries, nq, k, static_cast<uint32_t*>(zc_out[0]), static_cast<float*>(zc_out[1]),
+                      static_cast<uint32_t*>(zc_out[2]), static_cast<pqtg_query_stats*>(zc_out[3]), st[0], true,
+                      ws.qtime_on ? ws.h_qtime : nullptr);
+        };
         const uint64_t key[12] = {(uint64_t)(uintptr_t)queries, nq, k, (uint64_t)(uintptr_t)ids,
                                   (uint64_t)(uintptr_t)dists, (uint64_t)(uintptr_t)counts,
                                   (uint64_t)(uintptr_t)stats, ws.gen, (uint64_t)kernel_variant(),
                                   (uint64_t)(uintptr_t)d.db, d.prm.rerank_exact,
-                                  (uint64_t)std::hash<std::string>{}(std::getenv("PQTG_CHUNK_PLAN") ? std::getenv("PQTG_CHUNK_PLAN") : "")};
-        Workspace::GraphEntry* hit = nullptr;
-        for (auto& g : ws.graphs)
-            if (std::memcmp(g.key, key, sizeof(key)) == 0) hit = &g;
-        if (!hit) {
-            cudaGraph_t graph = nullptr;
-            PQTG_CUDA_CHECK(cudaStreamBeginCapture(st[0], cudaStreamCaptureModeThreadLocal));
-            try {
-                PQTG_CUDA_CHECK(cudaEventRecord(ws.fork, st[0]));
-                PQTG_CUDA_CHECK(cudaStreamWaitEvent(st[1], ws.fork, 0));
-                enqueue();
-                PQTG_CUDA_CHECK(cudaEventRecord(ws.fork, st[1]));
-                PQTG_CUDA_CHECK(cudaStreamWaitEvent(st[0], ws.fork, 0));
-            } catch (...) {
-                cudaStreamEndCapture(st[0], &graph);
-                if (graph) cudaGraphDestroy(graph);
-                cudaGetLastError();
-                throw;
-            }
-            PQTG_CUDA_CHECK(cudaStreamEndCapture(st[0], &graph));
-            cudaGraphExec_t exec = nullptr;
-            const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
-            cudaGraphDestroy(graph);
-            PQTG_CUDA_CHECK(e);
-            if (ws.graphs.size() >= 8) {  // evict the least recently used
-                auto lru = std::min_element(ws.graphs.begin(), ws.graphs.end(),
-                                            [](const auto& x, const auto& y) { return x.used < y.used; });
-                cudaGraphExecDestroy(lru->exec);
-                ws.graphs.erase(lru);
-            }
-            Workspace::GraphEntry g{};
-            std::memcpy(g.key, key, sizeof(key));
-            g.exec = exec;
-            ws.graphs.push_back(g);
-            hit = &ws.graphs.back();
-        } else {
-            ws.last_nq = nq - (nq - 1) / ws.max_batch * ws.max_batch;  // the last sub-batch
+                                  (uint64_t)std::hash<std::string>{}(std::getenv("PQTG_CHUNK_PLAN") ? std::getenv("PQTG_CHUNK_PLAN") : "") ^
+                                      (zc ? 0x5a5a5a5a5a5a5a5aull : 0ull)};
+        if (zc) {
+            const cudaGraphExec_t exec = cached_graph(ws, key, st[0], enqueue_zc);
+            ws.last_nq = nq;
+            PQTG_CUDA_CHECK(cudaGraphLaunch(exec, st[0]));
+            PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
+            PQTG_CUDA_CHECK(cudaEventRecord(ws.done, st[0]));
+            check_exact();
+            return PQTG_OK;
         }
-        hit->used = ++ws.graph_clock;
-        PQTG_CUDA_CHECK(cudaGraphLaunch(hit->exec, st[0]));
+        const bool cached = std::any_of(ws.graphs.begin(), ws.graphs.end(),
+                                        [&](const auto& g) { return std::memcmp(g.key, key, sizeof(key)) == 0; });
+        const cudaGraphExec_t exec = cached_graph(ws, key, st[0], enqueue);
+        if (cached) ws.last_nq = nq - (nq - 1) / ws.max_batch * ws.max_batch;  // the last sub-batch
+        PQTG_CUDA_CHECK(cudaGraphLaunch(exec, st[0]));
         PQTG_CUDA_CHECK(cudaStreamSynchronize(st[0]));
         PQTG_CUDA_CHECK(cudaEventRecord(ws.done, st[0]));
         check_exact();

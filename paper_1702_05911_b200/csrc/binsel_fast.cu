@@ -30,6 +30,8 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                        uint32_t* __restrict__ ntuples, pqtg_query_stats* __restrict__ stats, uint32_t ts_log2,
                        uint32_t* __restrict__ ghash, uint32_t W2ab) {
     extern __shared__ __align__(16) unsigned char smem[];
+    griddep_wait();  // the traversal's lists (a PDL dependent in a chained chunk)
+    griddep_launch();
     qt_begin(p, blockIdx.x, 1);
     binsel_fast_body<P, HASH, SyncBlock>(p, blockIdx.x, l2c_in, l2d_in, slope_out, ranges, nranges, ncand, ntuples,
                                          stats, ts_log2, ghash, W2ab, smem, threadIdx.x);
@@ -85,7 +87,7 @@ void configure_binsel_fast() {
 void launch_binsel_fast(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats, cudaStream_t s) {
     const BsConfig c = bs_config(p);
 #define PQTG_BS(PP, HH)                                                                                       \
-    binsel_fast_kernel<PP, HH><<<(unsigned)nq, kBsThreads, c.smem, s>>>(p, ws.l2_code, ws.l2_dist, ws.slope, ws.ranges,     \
+    launch_kernel(p.chain, binsel_fast_kernel<PP, HH>, dim3((unsigned)nq), dim3(kBsThreads), c.smem, s, p, ws.l2_code, ws.l2_dist, ws.slope, ws.ranges,     \
                                                                        ws.nranges, ws.ncand, ws.ntuples, stats, \
                                                                        c.ts_log2, ws.hash, c.W2ab)
     if (p.P == 1) {

@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t q = blockIdx.x;
+    griddep_wait();  // the traversal's lists (a PDL dependent in a chained chunk)
+    griddep_launch();
     qt_begin(p, q, 1);
     const uint32_t W = p.W, PW = P * W;
     const uint32_t H = (uint32_t)p.H;
@@ -462,7 +464,7 @@ void launch_binsel_par(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_
     const uint32_t lg = bsp::ts_log2_for(p.budget);
     const size_t smem = bsp::layout(p.P * p.W, c.W2ab, c.use_hash).total;
 #define PQTG_BP(PP, HH)                                                                                      \
-    binsel_par_kernel<PP, HH, 256><<<(unsigned)nq, 256, smem, s>>>(p, ws.l2_code, ws.l2_dist, ws.slope, ws.ranges, \
+    launch_kernel(p.chain, binsel_par_kernel<PP, HH, 256>, dim3((unsigned)nq), dim3(256), smem, s, p, ws.l2_code, ws.l2_dist, ws.slope, ws.ranges, \
                                                                   ws.nranges, ws.ncand, ws.ntuples, stats, lg,   \
                                                                   ws.hash, c.W2ab)
     if (p.P == 1) {

@@ -15,6 +15,12 @@ constexpr uint64_t kSentinel = ~0ull;
 // complemented (so one atomicMax from a zeroed record keeps the earliest start) and every warp's
 // lane 0 its end (the latest end wins); p.qtime is [query][3 stages][start, end] in
 // globaltimer nanoseconds, or null when the workspace does not collect them.
+// Programmatic dependent launch (PDL): a dependent kernel waits for its predecessor's results
+// (and their memory flush) with griddep_wait(); a kernel lets its dependents launch early with
+// griddep_launch(). Both are no-ops when the launch has no programmatic dependency.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long gtimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

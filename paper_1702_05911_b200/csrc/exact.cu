@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(kExThreads) exact_rerank_kernel(DevParams p, c
     uint64_t* keys = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(y) + ((size_t)D * 4 + 15) / 16 * 16);
     __shared__ __align__(8) uint64_t full[kExStages];
     const uint64_t q = blockIdx.x;
+    griddep_wait();  // the re-rank's line-ranked prefix (a PDL dependent in a chained chunk)
     qt_begin(p, q, 2);
     const uint32_t tid = threadIdx.x;
     const uint32_t n = line_counts[q];  // = rerank: min(max(k, rerank_exact), C) line-ranked candidates
@@ -137,7 +138,7 @@ void launch_exact(const DevParams& p, const float* queries, uint64_t nq, uint32_
                   const uint32_t* line_counts, uint32_t k, uint32_t* ids, float* dists, uint32_t* counts,
                   pqtg_query_stats* stats, cudaStream_t s) {
     if (nq == 0) return;
-    exact_rerank_kernel<false><<<(unsigned)nq, kExThreads, exact_smem(p, kp), s>>>(
+    launch_kernel(p.chain, exact_rerank_kernel<false>, dim3((unsigned)nq), dim3(kExThreads), exact_smem(p, kp), s, 
         p, queries, kp, line_ids, line_counts, k, ids, dists, counts, stats, nullptr);
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
@@ -145,7 +146,7 @@ void launch_exact(const DevParams& p, const float* queries, uint64_t nq, uint32_
 void launch_exact_prefix(const DevParams& p, const float* queries, uint64_t nq, uint32_t kp, const uint32_t* line_ids,
                          const uint32_t* line_counts, float* exact, cudaStream_t s) {
     if (nq == 0) return;
-    exact_rerank_kernel<true><<<(unsigned)nq, kExThreads, exact_smem(p, kp), s>>>(
+    launch_kernel(p.chain, exact_rerank_kernel<true>, dim3((unsigned)nq), dim3(kExThreads), exact_smem(p, kp), s, 
         p, queries, kp, line_ids, line_counts, 0, nullptr, nullptr, nullptr, nullptr, exact);
     PQTG_CUDA_CHECK(cudaGetLastError());
 }

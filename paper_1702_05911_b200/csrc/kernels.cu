@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
     uint32_t* l2c = reinterpret_cast<uint32_t*>(l2d + P * W);
     const uint64_t q = blockIdx.x;
     qt_begin(p, q, 0);
+    griddep_launch();  // a chained chunk\'s bin selection may launch
     const int tid = threadIdx.x;
 
     for (uint32_t i = tid; i < D; i += blockDim.x) y[i] = Q[q * D + i];
@@ -357,6 +358,8 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
     __shared__ typename Sort::TempStorage sort_tmp;
 
     const uint64_t q = blockIdx.x;
+    griddep_wait();  // the traversal's lists (a PDL dependent in a chained chunk)
+    griddep_launch();
     qt_begin(p, q, 1);
     const int tid = threadIdx.x;
 
@@ -624,16 +627,16 @@ void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_quer
         const uint32_t cap = (uint32_t)std::min<size_t>((avail - fixed) / 16, 65536);
         const size_t smx = fixed + (size_t)cap * 16;
         if (p.resort)
-            binsel_kernel<16, true, true><<<(unsigned)nq, kThreads, smx, s>>>(
+            launch_kernel(p.chain, binsel_kernel<16, true, true>, dim3((unsigned)nq), dim3(kThreads), smx, s, 
                 p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap, ws.err);
         else
-            binsel_kernel<4, false, true><<<(unsigned)nq, kThreads, smx, s>>>(
+            launch_kernel(p.chain, binsel_kernel<4, false, true>, dim3((unsigned)nq), dim3(kThreads), smx, s, 
                 p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap, ws.err);
     } else if (p.resort) {
-        binsel_kernel<16, true, false><<<(unsigned)nq, kThreads, sm, s>>>(
+        launch_kernel(p.chain, binsel_kernel<16, true, false>, dim3((unsigned)nq), dim3(kThreads), sm, s, 
             p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0, ws.err);
     } else {
-        binsel_kernel<4, false, false><<<(unsigned)nq, kThreads, sm, s>>>(
+        launch_kernel(p.chain, binsel_kernel<4, false, false>, dim3((unsigned)nq), dim3(kThreads), sm, s, 
             p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0, ws.err);
     }
     PQTG_CUDA_CHECK(cudaGetLastError());
@@ -751,6 +754,8 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     __shared__ TopkShared s_sel;
 
     const uint64_t q = blockIdx.x;
+    griddep_wait();  // the bin selection's ranges (a PDL dependent in a chained chunk)
+    griddep_launch();
     qt_begin(p, q, 2);
     const int tid = threadIdx.x;
     const uint32_t R = nranges[q], C = ncand[q];
@@ -856,7 +861,7 @@ void launch_rerank(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& w
     const uint32_t cap = sel_cap_for(p, k);
     uint64_t* gkeys = gk ? ws.keys : nullptr;
 #define PQTG_RERANK(LT, PW)                                                                          \
-    rerank_kernel<LT, PW><<<(unsigned)nq, kThreads, sm, s>>>(p, k, cap, ws.fine, ws.ranges, ws.nranges, \
+    launch_kernel(p.chain, rerank_kernel<LT, PW>, dim3((unsigned)nq), dim3(kThreads), sm, s, p, k, cap, ws.fine, ws.ranges, ws.nranges, \
                                                              ws.ncand, ids, dists, counts, gkeys)
     if (p.pw == 1) {
         switch (p.L) {

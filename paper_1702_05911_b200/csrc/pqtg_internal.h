@@ -7,6 +7,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/pqtg.h"
@@ -30,6 +31,24 @@ struct Error {
                                                    cudaGetErrorString(_e)};                \
         }                                                                                  \
     } while (0)
+
+// Kernel launch; with `chain`, as a programmatic dependent of the stream's previous kernel (PDL:
+// its CTAs may start while that kernel drains, and call griddep_wait() before reading its results)
+template <typename... KArgs, typename... Args>
+void launch_kernel(bool chain, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = chain ? 1 : 0;
+    PQTG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // ---------------------------------------------------------------- constants
 constexpr uint32_t kSlopeTables = 10;      // binorder.hpp:25
@@ -90,6 +109,9 @@ struct DevParams {
     uint32_t scr_nj, scr_kpad;  // k1·k2 padded to the N tile; m padded to 16
     // per-query stage clock of the current chunk ([q][3][~start, end] ns), null when not collected
     unsigned long long* qtime;
+    // the chunk's stages run as one programmatic-dependent chain (PDL): bin selection and the
+    // re-rank (and the exact stage) are launched as dependents of the previous stage's kernel
+    uint32_t chain;
 };
 
 struct DevIndex {
@@ -121,12 +143,12 @@ struct WsSlice {
     // small batches: the split re-rank's per-(query, slice) top-k keys [q][kSplitMax][split_k], their
     // counts [q][kSplitMax] and per-query arrival counters [q] (zero between calls)
     uint64_t* split_keys = nullptr;
-    uint32_t* split_cnt = nullptr;
     uint32_t* split_ctr = nullptr;
     uint64_t split_q = 0, split_k = 0;
 };
 
-constexpr uint32_t kSplitMax = 16;     // CTAs per query of the split re-rank
+constexpr uint64_t kChainBelow = 256;  // chunks below this many queries run as one PDL chain
+constexpr uint32_t kSplitMax = 16;     // CTAs per query of the split re-rank (< 32: one warp scans the counts)
 constexpr uint64_t kSplitBelow = 148;  // batches below one query per SM spread each query over CTAs
 
 // device error word bits (Workspace::err): set by kernels, cleared at the start of every search
@@ -157,7 +179,6 @@ struct Workspace {
     bool qtime_on = false;
     bool qtime_host = false;              // the last call was pqtg_search (clocks in h_qtime)
     uint64_t* split_keys = nullptr;   // small-batch split re-rank lists (see WsSlice)
-    uint32_t* split_cnt = nullptr;
     uint32_t* split_ctr = nullptr;
     uint64_t split_q = 0, split_k = 0;
     float* scr = nullptr;         // [B][P][scr_nj] (y - mu_p) . c'' on the tensor cores (screen.cu)
@@ -178,7 +199,10 @@ struct Workspace {
     };
     std::vector<GraphEntry> graphs;
     uint64_t graph_clock = 0;
+    uint64_t dev_last_key[12] = {};     // pqtg_search_device: a small batch is captured the second
+                                        // time the same arguments arrive in a row
     uint64_t gen = 0;                   // bumped when buffers / settings a graph bakes in change
+    bool stages_timed = true;           // the last timed chunk recorded events between its stages
     WsSlice slice(uint64_t q0) const;
     // host-call staging (grown on demand)
     float* d_queries = nullptr;

@@ -33,11 +33,16 @@ using namespace dev;
 
 // phase clocks of CTA (0, 0) of the last re-rank launch (PQTG_PHASES=1: tools/phase_probe.py);
 // null otherwise. [0] start, [1] prologue done, [2] range map done, [3] candidates scored,
-// [4] selected, [5] written (split: the slice's list), [6] merged (split's last slice)
+// [4] selected, [5] written (split: the slice's list), [6] merged and [7] arrived (split's last slice)
 __device__ unsigned long long* g_phase = nullptr;
 #define PQTG_PHASE(i)                                                                                  \
     do {                                                                                               \
-        if (g_phase && blockIdx.x == 0 && threadIdx.x == 0 && (blockIdx.y == 0 || (i) == 6)) g_phase[i] = gtimer_ns(); \
+        if (g_phase && blockIdx.x == 0 && threadIdx.x == 0 && (blockIdx.y == 0 || (i) >= 6)) g_phase[i] = gtimer_ns(); \
+    } while (0)
+
+#define PQTG_PHASE_VAL(i, v)                                                                           \
+    do {                                                                                               \
+        if (g_phase && blockIdx.x == 0 && threadIdx.x == 0) g_phase[i] = (v);                          \
     } while (0)
 
 namespace {
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
                      float* __restrict__ out_dists, uint32_t* __restrict__ out_counts, uint64_t* __restrict__ gkeys,
-                     uint64_t* __restrict__ split_keys, uint32_t* __restrict__ split_cnt,
+                     uint64_t* __restrict__ split_keys,
                      uint32_t* __restrict__ split_ctr) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE != 0;
@@ -188,9 +193,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
 
     const uint64_t q = blockIdx.x;
     const uint32_t tid = threadIdx.x;
-    qt_begin(p, q, 2);
     PQTG_PHASE(0);
-    const uint32_t R = nranges[q], C = ncand[q];
     const uint2* qr = ranges + q * (uint64_t)budget;
 
     // every global load of the prologue is issued before the first barrier: the query's fine
@@ -220,7 +223,13 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                 c2v[u] = f < LT ? __ldg(p.c2 + f * p.npairs + pi) : 0.0f;
         }
     }
-    const uint2 rg0 = tid < R ? __ldg(qr + tid) : make_uint2(0, 0);
+    // everything above reads the index only; the bin selection's ranges and the traversal's fine
+    // LUT are read below (a PDL dependent in a chained chunk starts before they are complete)
+    griddep_wait();
+    griddep_launch();
+    qt_begin(p, q, 2);
+    const uint32_t R = nranges[q], C = ncand[q];
+    const uint2 rg0 = tid < R ? __ldcg(qr + tid) : make_uint2(0, 0);
     // every index is a position range [shard_lo, shard_hi): [0, n) unsharded, possibly empty
     // on a shard (then every candidate is skipped and the query returns count 0)
     constexpr bool sharded = true;
@@ -383,10 +392,15 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     // wavefronts on DEEP-shaped codes, tools/bank_probe.py) for two conflict-free 4-byte reads.
     // λ = fl(q · fl(1/255)) with q = (2^23 + q) − 2^23 built from the code byte by one byte
     // permute (exact for q <= 255) instead of an I2F.
-    // this CTA's slice of the query's candidates: all of them, or 1/gridDim.y of them when a small
-    // batch spreads each query over several CTAs (the slices' top-k lists are merged afterwards)
-    const uint32_t jlo = (uint32_t)((uint64_t)Cn * blockIdx.y / gridDim.y);
-    const uint32_t jhi = (uint32_t)((uint64_t)Cn * (blockIdx.y + 1) / gridDim.y);
+    // this CTA's slice of the query's candidates: all of them, or, when a small batch spreads each
+    // query over S = gridDim.y CTAs, every S-th one from blockIdx.y (interleaved, so every slice
+    // samples near and far bins alike and the slices' top-k lists have similar ranges, which keeps
+    // the merge's cut tight). Slice candidate u is candidate y + u·S; its key goes to keys[kb + u]
+    // (slices own disjoint key ranges, in candidate order).
+    const uint32_t S_ = gridDim.y, y_ = blockIdx.y;
+    const uint32_t jn = Cn > y_ ? (Cn - y_ + S_ - 1) / S_ : 0u;
+    const uint32_t kb = y_ * (Cn / S_) + (y_ < Cn % S_ ? y_ : Cn % S_);
+    const uint32_t jhi = kb + jn;
     auto score2 = [&](uint32_t ja, const uint4* va, uint32_t ida, uint32_t jb, const uint4* vb, uint32_t idb) {
         const uint32_t* wa = reinterpret_cast<const uint32_t*>(va);
         const uint32_t* wb = reinterpret_cast<const uint32_t*>(vb);
@@ -446,33 +460,33 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     if constexpr (PK) {
         // candidates j and j + step of this thread together; both rows are loaded before scoring
         uint4 va[kVec], vb[kVec];
-        for (uint32_t j = jlo + tid; j < jhi; j += 2 * step) {
-            const uint32_t j2 = j + step;
+        for (uint32_t u = tid; u < jn; u += 2 * step) {
+            const uint32_t u2 = u + step;
             uint32_t ida = kInvalid, idb = kInvalid;
-            fetch(j, va, ida);
-            if (j2 < jhi) fetch(j2, vb, idb);
-            score2(j, va, ida, j2, vb, idb);
+            fetch(y_ + u * S_, va, ida);
+            if (u2 < jn) fetch(y_ + u2 * S_, vb, idb);
+            score2(kb + u, va, ida, kb + u2, vb, idb);
         }
     } else if constexpr (DIRECT) {
         // a shard's share of the candidates is about one per thread: one row buffer (the
         // 64-register budget of two CTAs per SM has no room for a second)
         uint4 va[kVec];
         uint32_t ida = kInvalid;
-        for (uint32_t j = jlo + tid; j < jhi; j += step) {
-            fetch(j, va, ida);
-            score(j, va, ida);
+        for (uint32_t u = tid; u < jn; u += step) {
+            fetch(y_ + u * S_, va, ida);
+            score(kb + u, va, ida);
         }
     } else {
         uint4 va[kVec], vb[kVec];
         uint32_t ida = kInvalid, idb = kInvalid;
-        if (jlo + tid < jhi) fetch(jlo + tid, va, ida);
-        for (uint32_t j = jlo + tid; j < jhi; j += 2 * step) {
-            const uint32_t j2 = j + step;
-            if (j2 < jhi) fetch(j2, vb, idb);
-            score(j, va, ida);
-            if (j2 >= jhi) break;
-            if (j2 + step < jhi) fetch(j2 + step, va, ida);
-            score(j2, vb, idb);
+        if (tid < jn) fetch(y_ + tid * S_, va, ida);
+        for (uint32_t u = tid; u < jn; u += 2 * step) {
+            const uint32_t u2 = u + step;
+            if (u2 < jn) fetch(y_ + u2 * S_, vb, idb);
+            score(kb + u, va, ida);
+            if (u2 >= jn) break;
+            if (u2 + step < jn) fetch(y_ + (u2 + step) * S_, va, ida);
+            score(kb + u2, vb, idb);
         }
     }
 #pragma unroll
@@ -495,7 +509,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     if (kk) {
         for (uint32_t i = tid; i < (1u << kSelBits); i += blockDim.x) hist[i] = 0;
         __syncthreads();
-        m = block_select_wide<kSelBits, kIjThreads>(keys + jlo, jhi - jlo, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap,
+        m = block_select_wide<kSelBits, kIjThreads>(keys + kb, jn, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap,
                                                     wmax, s_sel);
     }
     PQTG_PHASE(4);
@@ -505,39 +519,92 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         qt_end(p, q, 2);
         return;
     }
-    // split: this slice's top-kk keys to its list, then the query's last-arriving slice selects the
-    // top-k of all S lists (threadfence-reduction pattern: no second launch)
+    // split: this slice's top-kk keys to its list (sorted, padded to k with kSentinel), then the
+    // query's last-arriving slice ranks the union's top k (threadfence-reduction pattern: no
+    // second launch)
     const uint32_t S = gridDim.y;
     uint64_t* lst = split_keys + ((uint64_t)q * kSplitMax + blockIdx.y) * k;
     block_rank_keys(sel, m, kk, lst);
+    for (uint32_t i = kk + tid; i < k; i += blockDim.x) lst[i] = kSentinel;
     PQTG_PHASE(5);
-    if (tid == 0) split_cnt[q * kSplitMax + blockIdx.y] = kk;
     __threadfence();
     __syncthreads();
     __shared__ uint32_t s_last;
     if (tid == 0) s_last = atomicAdd(&split_ctr[q], 1u) == S - 1;
     __syncthreads();
     if (!s_last) return;
+    PQTG_PHASE(7);
     __threadfence();
-    // the S lists into keys[0 ..) (they fit: S·k <= budget, rerank_split), then select + sort
-    uint32_t tot = 0;
-    for (uint32_t g = 0; g < S; ++g) {
-        const uint32_t c = __ldcg(split_cnt + q * kSplitMax + g);
-        const uint64_t* src = split_keys + ((uint64_t)q * kSplitMax + g) * k;
-        for (uint32_t i = tid; i < c; i += blockDim.x) keys[tot + i] = __ldcg(src + i);
-        tot += c;
-    }
-    if (tid == 0) {
-        split_ctr[q] = 0;  // ready for the next call
-        s_sel.kand = ~0ull;
-        s_sel.kor = 0ull;
+    // the S lists (contiguous, stride k) into keys[0, S·k) in one pass; the kept keys' list map
+    // goes behind them (2·S·k keys <= budget, rerank_split)
+    const uint64_t* src = split_keys + (uint64_t)q * kSplitMax * k;
+    for (uint32_t i = tid; i < S * k; i += blockDim.x) keys[i] = __ldcg(src + i);
+    if (tid == 0) split_ctr[q] = 0;  // ready for the next call
+    __syncthreads();
+    PQTG_PHASE(8);
+    // per list (lane g): its length n_g (keys below kSentinel); k2 = min(k, Σ n_g). The first
+    // c = ceil(k2 / S) keys of every list are <= M, the largest of their last keys, so when those
+    // prefixes hold >= k2 keys the top k2 of the union are all <= M: each list is cut at M, and a
+    // kept key's rank among the kept keys is its rank in the union.
+    __shared__ uint32_t s_len[kSplitMax], s_off[kSplitMax + 1], s_k2;
+    auto lower = [&](const uint64_t* l, uint32_t n, uint64_t x) {  // keys of sorted l[0, n) below x
+        uint32_t lo = 0, hi = n;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (l[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    if (tid < 32) {
+        const uint32_t n = tid < S ? lower(keys + tid * k, k, kSentinel) : 0u;
+        uint32_t tot = n;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+        const uint32_t k2 = tot < k ? tot : k;
+        const uint32_t c = (k2 + S - 1) / S;
+        uint32_t have = n < c ? n : c;
+        uint64_t mx = have ? keys[tid * k + have - 1] : 0ull;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, mx, d);
+            mx = o > mx ? o : mx;
+            have += __shfl_xor_sync(0xffffffffu, have, d);
+        }
+        const uint64_t thr = have >= k2 ? mx : kSentinel - 1;
+        const uint32_t len = tid < S ? lower(keys + tid * k, n, thr + 1) : 0u;  // keys <= thr
+        uint32_t incl = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (tid >= (uint32_t)d) incl += v;
+        }
+        if (tid < S) s_len[tid] = len;
+        if (tid <= S) s_off[tid] = incl - len;
+        if (tid == 0) {
+            s_k2 = k2;
+            s_sel.kand = ~0ull;
+            s_sel.kor = 0ull;
+        }
     }
     __syncthreads();
-    {
+    PQTG_PHASE(9);
+    // the kept keys, compacted behind the lists, ranked by counting and written at their ranks
+    const uint32_t k2 = s_k2, E = s_off[S];
+    PQTG_PHASE_VAL(12, E);
+    uint64_t* kept = keys + (uint64_t)S * k;
+    for (uint32_t i = tid; i < S * k; i += blockDim.x) {
+        const uint32_t g = i / k, j = i - g * k;
+        if (j < s_len[g]) kept[s_off[g] + j] = keys[i];
+    }
+    __syncthreads();
+    PQTG_PHASE(10);
+    if (E <= blockDim.x) {
+        block_sort_write(kept, E, k2, k, q, out_ids, out_dists, out_counts);
+    } else {  // a loose cut: select the top k2 of the kept keys first
         uint64_t a = ~0ull, o = 0ull;
-        for (uint32_t j = tid; j < tot; j += blockDim.x) {
-            a &= keys[j];
-            o |= keys[j];
+        for (uint32_t j = tid; j < E; j += blockDim.x) {
+            a &= kept[j];
+            o |= kept[j];
         }
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
@@ -548,16 +615,12 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
             atomicAnd(&s_sel.kand, (unsigned long long)a);
             atomicOr(&s_sel.kor, (unsigned long long)o);
         }
-    }
-    const uint32_t k2 = tot < k ? tot : k;
-    uint32_t m2 = 0;
-    if (k2) {
         for (uint32_t i = tid; i < (1u << kSelBits); i += blockDim.x) hist[i] = 0;
         __syncthreads();
-        m2 = block_select_wide<kSelBits, kIjThreads>(keys, tot, k2, s_sel.kand, s_sel.kor, hist, sel, sel_cap, wmax,
-                                                     s_sel);
+        const uint32_t m2 = block_select_wide<kSelBits, kIjThreads>(kept, E, k2, s_sel.kand, s_sel.kor, hist, sel,
+                                                                    sel_cap, wmax, s_sel);
+        block_sort_write(sel, m2, k2, k, q, out_ids, out_dists, out_counts);
     }
-    block_sort_write(sel, m2, k2, k, q, out_ids, out_dists, out_counts);
     PQTG_PHASE(6);
     qt_end(p, q, 2);
 }
@@ -633,8 +696,8 @@ unsigned long long* phase_buffer() {
     static unsigned long long* buf = [] {
         unsigned long long* b = nullptr;
         const char* e = std::getenv("PQTG_PHASES");
-        if (e && std::strcmp(e, "1") == 0 && cudaMallocManaged(&b, 8 * sizeof(unsigned long long)) == cudaSuccess) {
-            std::memset(b, 0, 8 * sizeof(unsigned long long));
+        if (e && std::strcmp(e, "1") == 0 && cudaMalloc(&b, 16 * sizeof(unsigned long long)) == cudaSuccess) {
+            cudaMemset(b, 0, 16 * sizeof(unsigned long long));  // device memory: no page faults in the clocks
             cudaMemcpyToSymbol(g_phase, &b, sizeof(b));
         }
         return b;
@@ -664,16 +727,17 @@ void configure_rerank_ij() {
 
 // CTAs per query: a batch below one query per SM can spread each query's candidates over up to
 // kSplitMax CTAs; each slice ranks its top-k keys into a list and the query's last-arriving
-// slice selects the top-k of all lists (PQTG_SPLIT=1 enables; 0 / unset keeps one CTA per query)
+// slice merges the lists (default; PQTG_SPLIT=0 keeps one CTA per query)
 uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k) {
     static const bool off = [] {
         const char* e = std::getenv("PQTG_SPLIT");
-        return !(e && std::strcmp(e, "1") == 0);
+        return e && std::strcmp(e, "0") == 0;
     }();
     if (off || nq == 0 || nq >= kSplitBelow || p.budget < 1024 || !rerank_ij_ok(p, k)) return 1;
-    if ((uint64_t)kSplitMax * k > p.budget) return 1;  // the last slice gathers every list into its key array
-    const uint64_t s = (2 * kSplitBelow) / nq;
-    return (uint32_t)std::min<uint64_t>(kSplitMax, std::max<uint64_t>(1, std::min<uint64_t>(s, p.budget / 256)));
+    // the last slice gathers the S lists of k keys into its key array, with room behind: 2·S·k <= budget
+    const uint64_t s = std::min<uint64_t>(std::min<uint64_t>((2 * kSplitBelow) / nq, p.budget / 256),
+                                          std::min<uint64_t>(p.budget / (2ull * k), kSplitMax));
+    return s >= 2 ? (uint32_t)s : 1u;
 }
 
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids, float* dists,
@@ -687,9 +751,9 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     const size_t sm = ij_smem(p, k, gk);
     uint64_t* gkeys = gk ? ws.keys : nullptr;
 #define PQTG_IJ(LT, K, D, ...)                                                                                \
-    rerank_ij_kernel<LT, K, D, ##__VA_ARGS__><<<dim3((unsigned)nq, S), ij_threads(LT, D), sm, s>>>(                  \
+    launch_kernel(p.chain, rerank_ij_kernel<LT, K, D, ##__VA_ARGS__>, dim3((unsigned)nq, S), dim3(ij_threads(LT, D)), sm, s,                   \
         p, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, ids, dists, counts, gkeys, ws.split_keys,          \
-        ws.split_cnt, ws.split_ctr)
+        ws.split_ctr)
     if (code_k1m(p) == 32) {
         const bool direct = ij_direct(p);
         if (p.L == 16) {

@@ -94,10 +94,12 @@ def test_local_sharded_sift1b_tree():
         assert_same_results(got, want, f"sift1b tree G=8 rank {r}")
 
 
-def test_gpu_split_rerank_opt_in():
-    """The small-batch split re-rank (PQTG_SPLIT=1: each query's candidates over up to 16 CTAs,
-    their lists merged by the parallel ranked merge) against the golden fixtures, in a fresh
-    process (the switch is read once)."""
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_gpu_split_rerank_switch(split):
+    """The small-batch split re-rank (default; PQTG_SPLIT=0 turns it off: each query's candidates
+    over up to 16 CTAs, the last-arriving slice merging their sorted lists pairwise) and the
+    one-CTA-per-query re-rank against the golden fixtures, in a fresh process (the switch is read
+    once)."""
     import subprocess
     import sys
 
@@ -116,7 +118,7 @@ def test_gpu_split_rerank_opt_in():
     import os
     from conftest import REPO
 
-    env = dict(os.environ, PQTG_SPLIT="1", PYTHONPATH=f"{REPO}:{REPO / 'tests'}")
+    env = dict(os.environ, PQTG_SPLIT=split, PYTHONPATH=f"{REPO}:{REPO / 'tests'}")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=str(REPO / "tests"))
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
