@@ -337,7 +337,7 @@ int pqtg_sharded_search_device(pqtg_sharded* sh, const float* const* d_queries, 
 int pqtg_sharded_search(pqtg_sharded* sh, const float* queries, uint64_t nq, uint32_t dim, uint32_t k,
                         uint32_t* ids, float* dists, uint32_t* counts, pqtg_query_stats* stats);
 /* Per-stage device time of the last search on local rank 0, in ms: [0] traversal + bin
- * selection of its block, [1] exchange of the range lists, [2] re-rank, [3] all-to-all + merge +
+ * selection of its block, [1] exchange of the range lists (with the batch's fine LUTs, computed while the host reads the sizes), [2] re-rank, [3] all-to-all + merge +
  * gather of the results. Synchronises. */
 int pqtg_sharded_stage_ms(pqtg_sharded* sh, float* ms4);
 void pqtg_sharded_destroy(pqtg_sharded* sh);

@@ -951,11 +951,15 @@ __global__ void merge_topk_kernel(uint32_t G, uint64_t nq, uint32_t k, const uin
     out_counts[q] = out;
 }
 
-// Parallel merge of G sorted lists per query (one CTA per query): each element's output rank is
-// its index in its own list plus, per other list, the number of that list's keys below it (a
-// binary search; keys are (dist, id) with distinct ids, so ranks are distinct); elements of rank
-// < k are written at their rank. O(G k log k / threads) instead of the sequential k-step walk.
+// Parallel merge of G sorted lists per query (one CTA per query). For G <= 32: every list is cut
+// at M, the largest of the lists' ceil(kk/G)-th keys (the lists' first ceil(kk/G) keys, >= kk in
+// all, lie at or below M, so the top kk of the union do too), the kept keys are compacted and
+// each is written at its rank among them -- its rank in the union -- found by counting (keys are
+// (dist, id) with distinct ids, so ranks are distinct). Otherwise each element's rank is its index
+// in its own list plus, per other list, a binary search. Elements of rank < kk are written at
+// their rank.
 constexpr int kMergeThreads = 256;
+constexpr uint32_t kMergeMaxLists = 64;
 
 __global__ void __launch_bounds__(kMergeThreads) merge_ranked_kernel(uint32_t G, uint64_t nq, uint32_t k,
                                                                      const uint32_t* __restrict__ ids,
@@ -965,12 +969,13 @@ __global__ void __launch_bounds__(kMergeThreads) merge_ranked_kernel(uint32_t G,
                                                                      float* __restrict__ out_dists,
                                                                      uint32_t* __restrict__ out_counts) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // [G][k]
-    __shared__ uint32_t cnt[16];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // [G][k], then the kept keys (G <= 32)
+    __shared__ uint32_t cnt[kMergeMaxLists], s_len[32], s_off[33];
     const uint64_t q = blockIdx.x;
-    if (threadIdx.x < G) cnt[threadIdx.x] = min(counts[(uint64_t)threadIdx.x * nq + q], k);
+    const uint32_t tid = threadIdx.x;
+    if (tid < G) cnt[tid] = min(counts[(uint64_t)tid * nq + q], k);
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < G * k; e += blockDim.x) {
+    for (uint32_t e = tid; e < G * k; e += blockDim.x) {
         const uint32_t g = e / k, i = e - g * k;
         if (i < cnt[g]) {
             const uint64_t off = ((uint64_t)g * nq + q) * k + i;
@@ -981,39 +986,93 @@ __global__ void __launch_bounds__(kMergeThreads) merge_ranked_kernel(uint32_t G,
     uint32_t total = 0;
     for (uint32_t g = 0; g < G; ++g) total += cnt[g];
     const uint32_t kk = total < k ? total : k;
-    for (uint32_t e = threadIdx.x; e < G * k; e += blockDim.x) {
-        const uint32_t g = e / k, i = e - g * k;
-        if (i >= cnt[g] || i >= kk) continue;  // an element at index >= kk of its list ranks >= kk
-        const uint64_t key = keys[e];
-        uint32_t rank = i;
-        for (uint32_t h = 0; h < G && rank < kk; ++h) {
-            if (h == g) continue;
-            const uint64_t* l = keys + (uint64_t)h * k;
-            uint32_t lo = 0, hi = cnt[h];  // keys of list h below `key`
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (l[mid] < key) lo = mid + 1; else hi = mid;
+    if (G <= 32) {
+        if (tid < 32) {
+            const uint32_t n = tid < G ? cnt[tid] : 0u;
+            const uint32_t c = (kk + G - 1) / G;
+            uint32_t have = n < c ? n : c;
+            uint64_t mx = have ? keys[tid * k + have - 1] : 0ull;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, mx, d);
+                mx = o > mx ? o : mx;
+                have += __shfl_xor_sync(0xffffffffu, have, d);
             }
-            rank += lo;
+            const uint64_t thr = have >= kk ? mx : ~0ull;
+            uint32_t len = 0;  // list keys <= thr
+            if (tid < G) {
+                const uint64_t* l = keys + tid * k;
+                uint32_t lo = 0, hi = n;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (l[mid] <= thr) lo = mid + 1; else hi = mid;
+                }
+                len = lo;
+            }
+            uint32_t incl = len;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (tid >= (uint32_t)d) incl += v;
+            }
+            if (tid < G) s_len[tid] = len;
+            if (tid <= G) s_off[tid] = incl - len;
         }
-        if (rank < kk) {
-            out_ids[q * k + rank] = (uint32_t)(key & 0xFFFFFFFFu);
-            out_dists[q * k + rank] = unorderable((uint32_t)(key >> 32));
+        __syncthreads();
+        const uint32_t E = s_off[G];
+        uint64_t* kept = keys + (uint64_t)G * k;
+        for (uint32_t e = tid; e < G * k; e += blockDim.x) {
+            const uint32_t g = e / k, i = e - g * k;
+            if (i < s_len[g]) kept[s_off[g] + i] = keys[e];
+        }
+        __syncthreads();
+        for (uint32_t e = tid; e < E; e += blockDim.x) {
+            const uint64_t key = kept[e];
+            uint32_t rank = 0, j = 0;
+            for (; j + 4 <= E; j += 4)  // broadcast reads, four in flight
+                rank += (uint32_t)(kept[j] < key) + (uint32_t)(kept[j + 1] < key) + (uint32_t)(kept[j + 2] < key) +
+                        (uint32_t)(kept[j + 3] < key);
+            for (; j < E; ++j) rank += kept[j] < key;
+            if (rank < kk) {
+                out_ids[q * k + rank] = (uint32_t)(key & 0xFFFFFFFFu);
+                out_dists[q * k + rank] = unorderable((uint32_t)(key >> 32));
+            }
+        }
+    } else {
+        for (uint32_t e = tid; e < G * k; e += blockDim.x) {
+            const uint32_t g = e / k, i = e - g * k;
+            if (i >= cnt[g] || i >= kk) continue;  // an element at index >= kk of its list ranks >= kk
+            const uint64_t key = keys[e];
+            uint32_t rank = i;
+            for (uint32_t h = 0; h < G && rank < kk; ++h) {
+                if (h == g) continue;
+                const uint64_t* l = keys + (uint64_t)h * k;
+                uint32_t lo = 0, hi = cnt[h];  // keys of list h below `key`
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (l[mid] < key) lo = mid + 1; else hi = mid;
+                }
+                rank += lo;
+            }
+            if (rank < kk) {
+                out_ids[q * k + rank] = (uint32_t)(key & 0xFFFFFFFFu);
+                out_dists[q * k + rank] = unorderable((uint32_t)(key >> 32));
+            }
         }
     }
-    for (uint32_t i = kk + threadIdx.x; i < k; i += blockDim.x) {
+    for (uint32_t i = kk + tid; i < k; i += blockDim.x) {
         out_ids[q * k + i] = 0xFFFFFFFFu;
         out_dists[q * k + i] = __uint_as_float(0x7F800000u);
     }
-    if (threadIdx.x == 0) out_counts[q] = kk;
+    if (tid == 0) out_counts[q] = kk;
 }
 
 void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids, const float* dists,
                   const uint32_t* counts, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
                   cudaStream_t s) {
     if (nq == 0) return;
-    const size_t sm = (size_t)shards * k * 8;
-    if (k > 0 && sm + 1024 <= (size_t)optin_bytes()) {
+    const size_t sm = (size_t)shards * k * 8 * (shards <= 32 ? 2 : 1);  // lists (+ kept keys)
+    if (k > 0 && shards <= kMergeMaxLists && sm + 1024 <= (size_t)optin_bytes()) {
         static std::once_flag once[64];
         int dev = 0;
         PQTG_CUDA_CHECK(cudaGetDevice(&dev));

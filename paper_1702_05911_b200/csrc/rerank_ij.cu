@@ -154,8 +154,10 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 }  // namespace
 
 // MODE (K1M = 16): 0 = per-query table T[f][t] = (E, c2) (default); 1 = packed two-candidate loop
-// (PK); 2 = the scalar loop reading c2 by code and a2 = fine[f][j], E formed per candidate (C3).
-// Modes 1 and 2 use the c2-table layout (CT).
+// (PK); 2 = the scalar loop reading c2 by code and a2 = fine[f][j], E formed per candidate (C3);
+// 3 = E[f][t] and c2[f][t] as two 4-byte tables in T's bytes (S2: a 4-byte gather spreads a warp's
+// distinct pairs over 32 banks instead of the 16 bank pairs of an 8-byte one). Modes 1 and 2 use
+// the c2-table layout (CT).
 template <int LT, int K1M, bool DIRECT, int MODE = 0>
 __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 64 || K1M == 32) ? 1 : 2))
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                      uint64_t* __restrict__ split_keys,
                      uint32_t* __restrict__ split_ctr) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE != 0;
+    constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE == 1 || MODE == 2, S2 = MODE == 3;
     const uint32_t k1 = p.k1, budget = p.budget;
     constexpr uint32_t TE = t_entries(K1M);
     const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr, CT);
@@ -303,6 +305,10 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                 const float b2 = fine[f * K1M + pi_i], a2 = fine[f * K1M + pi_j];
                 if constexpr (CT) {
                     Ct[f * TE + ij] = c2v[u];
+                } else if constexpr (S2) {
+                    float* Et = reinterpret_cast<float*>(smem);
+                    Et[f * TE + ij] = __fsub_rn(__fsub_rn(a2, b2), c2v[u]);
+                    Et[LT * TE + f * TE + ij] = c2v[u];
                 } else {
                     T[f * TE + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
                 }
@@ -367,6 +373,10 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                     const float a2 = fine[f * K1M + ((ti - fi) & 15u)];
                     ec.y = Ct[f * TE + ti];
                     ec.x = __fsub_rn(__fsub_rn(a2, b2), ec.y);
+                } else if constexpr (S2) {  // E and c2 from two 4-byte tables (32 banks each)
+                    const float* Et = reinterpret_cast<const float*>(smem);
+                    ec.x = Et[f * TE + ti];
+                    ec.y = Et[LT * TE + f * TE + ti];
                 } else {
                     ec = T[f * TE + ti];
                 }
@@ -645,6 +655,7 @@ int ij_mode() {
         const char* e = std::getenv("PQTG_RERANK");
         if (e && std::strcmp(e, "packed") == 0) return 1;
         if (e && std::strcmp(e, "c3") == 0) return 2;
+        if (e && std::strcmp(e, "split") == 0) return 3;
         return 0;
     }();
     return mode;
@@ -669,7 +680,7 @@ int ij_mode();
 
 size_t ij_smem(const DevParams& p, uint32_t k, bool gkeys) {
     const uint32_t kk = k < p.budget ? k : p.budget;
-    const bool pk = code_k1m(p) == 16 && ij_mode() != 0;
+    const bool pk = code_k1m(p) == 16 && (ij_mode() == 1 || ij_mode() == 2);
     return ij_layout(p.L, p.budget, ij_sel_cap(kk), code_k1m(p) ? code_k1m(p) : 16, ij_direct(p), gkeys, pk).total;
 }
 
@@ -717,6 +728,9 @@ void configure_rerank_ij() {
     allow<32, 16, false, 1>(optin);
     allow<64, 16, false, 1>(optin);
     allow<16, 16, false, 2>(optin);
+    allow<16, 16, false, 3>(optin);
+    allow<32, 16, false, 3>(optin);
+    allow<64, 16, false, 3>(optin);
     allow<32, 16, false, 2>(optin);
     allow<64, 16, false, 2>(optin);
     allow<16, 32>(optin);
@@ -772,6 +786,12 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
         case 16: PQTG_IJ(16, 16, false, 2); break;
         case 32: PQTG_IJ(32, 16, false, 2); break;
         default: PQTG_IJ(64, 16, false, 2); break;
+        }
+    } else if (ij_mode() == 3) {
+        switch (p.L) {
+        case 16: PQTG_IJ(16, 16, false, 3); break;
+        case 32: PQTG_IJ(32, 16, false, 3); break;
+        default: PQTG_IJ(64, 16, false, 3); break;
         }
     } else {
         switch (p.L) {

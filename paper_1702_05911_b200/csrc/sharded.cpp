@@ -110,6 +110,7 @@ struct Rank {
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;     // this rank's last queued step
     cudaEvent_t ev[5] = {};         // stage timing (local rank 0)
+    cudaEvent_t sized = nullptr;    // the packed sizes are on the host (S3)
     std::vector<void*> allocations;
     uint64_t* blk_off = nullptr;    // [max_batch + 1] scan of this block's nranges
     uint64_t* all_off = nullptr;    // [max_batch + 1] scan of the batch's nranges
@@ -144,6 +145,7 @@ struct Rank {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (done) cudaEventDestroy(done);
+        if (sized) cudaEventDestroy(sized);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -216,6 +218,7 @@ void setup_rank(pqtg_sharded& sh, Rank& r) {
     PQTG_CUDA_CHECK(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
     PQTG_CUDA_CHECK(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
     for (auto& e : r.ev) PQTG_CUDA_CHECK(cudaEventCreate(&e));
+    PQTG_CUDA_CHECK(cudaEventCreateWithFlags(&r.sized, cudaEventDisableTiming));
     r.blk_off = dev_alloc<uint64_t>(r.allocations, sh.max_batch + 1);
     r.all_off = dev_alloc<uint64_t>(r.allocations, sh.max_batch + 1);
     r.d_totals = dev_alloc<uint64_t>(r.allocations, sh.world);
@@ -455,13 +458,23 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
                                r.ws().nranges + b.lo, r.blk_off, b.n, r.packed, r.stream);
             if (i == 0) PQTG_CUDA_CHECK(cudaEventRecord(r.ev[1], r.stream));
         }
-        // S3: packed sizes (host round trip)
+        // S3: packed sizes (host round trip). The batch's fine LUTs (S5) are queued behind the
+        // size copy, so the GPU computes them while the host waits for the sizes.
+        auto fine_luts = [&] {
+            for (uint32_t i = 0; i < R; ++i) {
+                Rank& r = *sh.ranks[i];
+                on(r);
+                launch_fine_lut(r.ix->prm, qptr(i), nq, r.ws().fine, r.stream);  // cheaper than exchanging the LUTs
+            }
+        };
         std::vector<uint64_t> total(G, 0);
         if (sh.sim) {
             Rank& r = *sh.ranks[0];
             PQTG_CUDA_CHECK(cudaMemcpyAsync(r.h_totals, r.blk_off + blk[r.g].n, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                             r.stream));
-            PQTG_CUDA_CHECK(cudaStreamSynchronize(r.stream));
+            PQTG_CUDA_CHECK(cudaEventRecord(r.sized, r.stream));
+            fine_luts();
+            PQTG_CUDA_CHECK(cudaEventSynchronize(r.sized));
             for (uint32_t g = 0; g < G; ++g) total[g] = g == r.g ? r.h_totals[0] : sh.simc->total[g];
         } else if (nc) {
             Rank& r = *sh.ranks[0];
@@ -469,7 +482,9 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             const Block b = blk[r.g];
             nccl_check(nc->all_gather(r.blk_off + b.n, r.d_totals, 1, ncclUint64, sh.comm, r.stream), "ncclAllGather");
             PQTG_CUDA_CHECK(cudaMemcpyAsync(r.h_totals, r.d_totals, G * sizeof(uint64_t), cudaMemcpyDeviceToHost, r.stream));
-            PQTG_CUDA_CHECK(cudaStreamSynchronize(r.stream));
+            PQTG_CUDA_CHECK(cudaEventRecord(r.sized, r.stream));
+            fine_luts();
+            PQTG_CUDA_CHECK(cudaEventSynchronize(r.sized));
             for (uint32_t g = 0; g < G; ++g) total[g] = r.h_totals[g];
         } else {
             for (auto& rp : sh.ranks) {
@@ -477,10 +492,12 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
                 on(r);
                 PQTG_CUDA_CHECK(cudaMemcpyAsync(r.h_totals, r.blk_off + blk[r.g].n, sizeof(uint64_t),
                                                 cudaMemcpyDeviceToHost, r.stream));
+                PQTG_CUDA_CHECK(cudaEventRecord(r.sized, r.stream));
             }
+            fine_luts();
             for (auto& rp : sh.ranks) {
                 on(*rp);
-                PQTG_CUDA_CHECK(cudaStreamSynchronize(rp->stream));
+                PQTG_CUDA_CHECK(cudaEventSynchronize(rp->sized));
                 total[rp->g] = rp->h_totals[0];
             }
         }
@@ -527,7 +544,6 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             on(r);
             if (i == 0) PQTG_CUDA_CHECK(cudaEventRecord(r.ev[2], r.stream));
             const DevParams& p = r.ix->prm;
-            launch_fine_lut(p, qptr(i), nq, r.ws().fine, r.stream);  // cheaper than exchanging the LUTs
             launch_scan_counts(r.ws().nranges, nq, r.all_off, r.stream);
             launch_unpack_ranges(r.all_packed, r.ws().nranges, r.all_off, nq, std::max<uint32_t>(budget, 1),
                                  r.ws().ranges, r.stream);

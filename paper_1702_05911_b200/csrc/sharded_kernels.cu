@@ -3,9 +3,12 @@
 // every query's (start position, candidate offset) ranges densely, the packed blocks are
 // all-gathered, and every rank unpacks the whole batch's ranges into its workspace before
 // re-ranking its position shard.
+#include <cub/block/block_load.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/block/block_store.cuh>
 
 #include <cstdint>
+#include <mutex>
 
 #include "common.cuh"
 #include "pqtg_internal.h"
@@ -17,24 +20,41 @@ using dev::sq_step;
 namespace {
 
 constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
 
-// off[i] = sum of cnt[0..i) for i <= n (off[n] = the total), one block: each thread sums a
-// contiguous chunk, one block scan of the chunk sums, each thread writes its chunk's offsets
+// off[i] = sum of cnt[0..i) for i <= n (off[n] = the total), one block over tiles of
+// kScanThreads·kScanItems counts: each tile is loaded coalesced (all loads in flight), scanned
+// and stored, the running total carried to the next tile
 __global__ void __launch_bounds__(kScanThreads) scan_counts_kernel(const uint32_t* __restrict__ cnt, uint64_t n,
                                                                    uint64_t* __restrict__ off) {
+    using Load = cub::BlockLoad<uint32_t, kScanThreads, kScanItems, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
+    using Store = cub::BlockStore<uint64_t, kScanThreads, kScanItems, cub::BLOCK_STORE_WARP_TRANSPOSE>;
     using Scan = cub::BlockScan<uint64_t, kScanThreads>;
-    __shared__ typename Scan::TempStorage tmp;
-    const uint64_t per = (n + kScanThreads - 1) / kScanThreads;
-    const uint64_t b = threadIdx.x * per, e = b + per < n ? b + per : n;
-    uint64_t sum = 0;
-    for (uint64_t i = b; i < e; ++i) sum += cnt[i];
-    uint64_t excl, tot;
-    Scan(tmp).ExclusiveSum(sum, excl, tot);
-    for (uint64_t i = b; i < e; ++i) {
-        off[i] = excl;
-        excl += cnt[i];
+    __shared__ union {
+        typename Load::TempStorage load;
+        typename Store::TempStorage store;
+        typename Scan::TempStorage scan;
+    } tmp;
+    constexpr uint64_t kTile = (uint64_t)kScanThreads * kScanItems;
+    uint64_t carry = 0;
+    for (uint64_t base = 0; base < n; base += kTile) {
+        const int valid = (int)(n - base < kTile ? n - base : kTile);
+        uint32_t v[kScanItems];
+        Load(tmp.load).Load(cnt + base, v, valid, 0u);
+        __syncthreads();
+        uint64_t w[kScanItems];
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) w[i] = v[i];
+        uint64_t tot;
+        Scan(tmp.scan).ExclusiveSum(w, w, tot);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) w[i] += carry;
+        Store(tmp.store).Store(off + base, w, valid);
+        carry += tot;
+        __syncthreads();
     }
-    if (threadIdx.x == 0) off[n] = tot;
+    if (threadIdx.x == 0) off[n] = carry;
 }
 
 // dense <- per-query rows (pack) or per-query rows <- dense (unpack); one warp per query
@@ -58,22 +78,34 @@ __global__ void __launch_bounds__(256) move_ranges_kernel(uint2* __restrict__ ro
 // pqtree.cpp:90-93) sequential fp32 order: the sharded search recomputes the batch's fine LUTs on
 // every rank (L·k1·fd multiply-adds per query) instead of all-gathering them (4·L·k1 bytes per
 // query, 4 KB on the SIFT1B tree)
-__global__ void __launch_bounds__(256) fine_lut_kernel(DevParams p, const float* __restrict__ Q, uint64_t nq,
-                                                       float* __restrict__ fine) {
-    extern __shared__ float y[];  // the current query
-    const uint32_t L = p.L, k1 = p.k1, fd = p.fd, D = p.D;
-    for (uint64_t q = blockIdx.x; q < nq; q += gridDim.x) {  // a few resident CTAs loop over the batch
-        for (uint32_t t = threadIdx.x; t < D; t += blockDim.x) y[t] = Q[q * D + t];
-        __syncthreads();
-        for (uint32_t idx = threadIdx.x; idx < L * k1; idx += blockDim.x) {
-            const uint32_t f = idx / k1, i = idx - f * k1;
-            const float* c = p.fine_t + (size_t)f * fd * k1 + i;
-            const float* yf = y + f * fd;
+// One warp per query (eight per CTA, no block barriers): the warp stages its query in shared
+// memory, then walks the parts, lane l computing centroids l, l + 32, ... of each (k1 = 32: the
+// centroid loads and the LUT stores are 128-byte coalesced rows; no index division).
+constexpr uint32_t kLutWarps = 8;
+// FD, K1: compile-time part width and centroid count (0: read from p), so the inner loop's loads
+// sit at immediate offsets from one base
+template <int FD, int K1>
+__global__ void __launch_bounds__(kLutWarps * 32) fine_lut_kernel(DevParams p, const float* __restrict__ Q, uint64_t nq,
+                                                                   float* __restrict__ fine) {
+    extern __shared__ float ys[];  // [kLutWarps][D]
+    const uint32_t L = p.L, k1 = K1 ? (uint32_t)K1 : p.k1, fd = FD ? (uint32_t)FD : p.fd, D = p.D;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t q = (uint64_t)blockIdx.x * kLutWarps + warp;
+    if (q >= nq) return;
+    float* y = ys + (size_t)warp * D;
+    for (uint32_t t = lane; t < D; t += 32) y[t] = __ldg(Q + q * D + t);
+    __syncwarp();
+    float* out = fine + q * L * k1;
+    const float* cf = p.fine_t;
+    for (uint32_t f = 0; f < L; ++f, cf += fd * k1, out += k1) {
+        const float* yf = y + f * fd;
+        for (uint32_t i = lane; i < k1; i += 32) {
+            const float* c = cf + i;
             float acc = 0.0f;
-            for (uint32_t t = 0; t < fd; ++t, c += k1) acc = sq_step(acc, yf[t], __ldg(c));
-            fine[q * L * k1 + idx] = acc;
+#pragma unroll
+            for (uint32_t t = 0; t < (FD ? (uint32_t)FD : fd); ++t) acc = sq_step(acc, yf[t], __ldg(c + t * k1));
+            out[i] = acc;
         }
-        __syncthreads();
     }
 }
 
@@ -110,8 +142,21 @@ void launch_copy_segments(const std::vector<CopySegment>& segs, cudaStream_t s) 
 
 void launch_fine_lut(const DevParams& p, const float* queries, uint64_t nq, float* fine, cudaStream_t s) {
     if (nq == 0) return;
-    const uint64_t grid = nq < 148 * 8 ? nq : 148 * 8;
-    fine_lut_kernel<<<(unsigned)grid, 256, p.D * sizeof(float), s>>>(p, queries, nq, fine);
+    const uint64_t grid = (nq + kLutWarps - 1) / kLutWarps;
+    const size_t sm = (size_t)kLutWarps * p.D * sizeof(float);
+    auto run = [&](auto kernel) {
+        if (sm > 48 * 1024) {
+            int d = 0, optin = 0;
+            PQTG_CUDA_CHECK(cudaGetDevice(&d));
+            PQTG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d));
+            if (sm > (size_t)optin) throw Error{PQTG_ERR_UNSUPPORTED, "fine LUT: query does not fit shared memory"};
+            PQTG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        }
+        kernel<<<(unsigned)grid, kLutWarps * 32, sm, s>>>(p, queries, nq, fine);
+    };
+    if (p.fd == 4 && p.k1 == 32) run(fine_lut_kernel<4, 32>);
+    else if (p.fd == 4 && p.k1 == 16) run(fine_lut_kernel<4, 16>);
+    else run(fine_lut_kernel<0, 0>);
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
 
