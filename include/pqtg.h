@@ -184,7 +184,9 @@ void pqtg_workspace_destroy(pqtg_workspace* ws);
 int pqtg_workspace_set_chunks(pqtg_workspace* ws, uint32_t chunks);
 /* Device milliseconds of the last pqtg_search* call per stage: [0] traversal, [1] bin
  * selection + gather, [2] re-rank + top-k, [3] whole search — of the call's first chunk (see
- * pqtg_workspace_set_chunks). Synchronises the last stream. */
+ * pqtg_workspace_set_chunks). A chunk below 256 queries runs its stages as one programmatic-
+ * dependent (PDL) chain with no events between them: [0..2] are then -1 and [3] is the whole
+ * search (pqtg_workspace_query_times has per-stage clocks). Synchronises the last stream. */
 int pqtg_workspace_stage_ms(pqtg_workspace* ws, float* ms4);
 /* Synchronise the workspace's streams and report what the kernels of its last search call
  * flagged: PQTG_ERR_UNSUPPORTED when a query's exact-order tuple heap outgrew shared memory
