@@ -706,11 +706,10 @@ int pqtg_search_device(pqtg_index* index, pqtg_workspace* wsh, const float* d_qu
         ensure_exact(ws, k);
         ensure_keys(ws, k);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        // the workspace's aux stream may still run a previous call's chunks on these slices, and
-        // the previous call may have run on another stream (or through pqtg_search)
-        PQTG_CUDA_CHECK(cudaEventRecord(ws.join, ws.aux_stream));
-        PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join, 0));
-        PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.done, 0));
+        // every previous call's work on these slices, its aux-stream chunks included (they are
+        // joined back before it records ws.done), is behind ws.done; a call on the same stream as
+        // the last one is ordered after it already (one API call less on the latency path)
+        if (s != ws.last_stream) PQTG_CUDA_CHECK(cudaStreamWaitEvent(s, ws.done, 0));
         if (index->dev->prm.exact_order) PQTG_CUDA_CHECK(cudaMemsetAsync(ws.err, 0, sizeof(uint32_t), s));
         ws.last_stream = s;
         ws.qtime_host = false;
@@ -869,14 +868,14 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
             const char* e = std::getenv("PQTG_ZERO_COPY");
             return !(e && std::strcmp(e, "0") == 0);
         }();
-        auto mapped = [](void* ptr) -> void* {
+        auto mapped = [&](void* ptr) -> void* {  // the device view of a page-locked buffer of this device
             if (!ptr) return nullptr;
             cudaPointerAttributes a{};
             if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
                 cudaGetLastError();
                 return nullptr;
             }
-            return a.devicePointer;
+            return a.type == cudaMemoryTypeHost && a.device == d.device ? a.devicePointer : nullptr;
         };
         void* zc_out[4] = {mapped(ids), mapped(dists), mapped(counts), mapped(stats)};
         const bool zc = zero_copy && nq <= 64 && nq <= ws.max_batch && (zc_out[0] || !ids) && (zc_out[1] || !dists) &&

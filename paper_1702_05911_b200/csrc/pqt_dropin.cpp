@@ -5,6 +5,8 @@
 //   pqt::save_index        ← index_io.cpp:94-146    (byte-identical container)
 //   pqt::knn_query_batch   ← search.cpp:262-274     → pqtg_search on the cached device index
 //   pqt::knn_query         ← search.cpp:126-260     → a batch of one
+#include <cuda_runtime.h>
+
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -241,12 +243,54 @@ void save_index(const PqtIndex& ix, const std::string& path) {
 // ------------------------------------------------------------------ queries
 namespace {
 
+// page-locked staging for small batches (<= kStageMax queries): the search then replays a CUDA
+// graph that writes the results straight into these buffers (pqtg_search's zero-copy path), and
+// a serving loop of knn_query calls keeps hitting the same graph
+constexpr std::size_t kStageMax = 64;
+
 struct DeviceCopy {
     pqtg_index* ix = nullptr;
     pqtg_workspace* ws = nullptr;
     const VectorSet* db = nullptr;  // raw vectors currently on the device (exact re-rank)
     std::uint64_t fingerprint = 0;  // of the host index the copy was made from
+    std::mutex stage_mu;
+    std::uint32_t stage_k = 0, stage_dim = 0;
+    float* h_q = nullptr;
+    std::uint32_t* h_ids = nullptr;
+    float* h_dists = nullptr;
+    std::uint32_t* h_counts = nullptr;
+    pqtg_query_stats* h_stats = nullptr;
+    void free_stage() {
+        for (void* p : {static_cast<void*>(h_q), static_cast<void*>(h_ids), static_cast<void*>(h_dists),
+                        static_cast<void*>(h_counts), static_cast<void*>(h_stats)})
+            if (p) cudaFreeHost(p);
+        h_q = nullptr;
+        h_ids = nullptr;
+        h_dists = nullptr;
+        h_counts = nullptr;
+        h_stats = nullptr;
+        stage_k = stage_dim = 0;
+    }
+    // staging for kStageMax queries of `dim` floats and k results; false when it cannot be had
+    bool stage(std::uint32_t dim, std::uint32_t k) {
+        if (h_q && stage_dim == dim && stage_k >= k) return true;
+        free_stage();
+        const bool ok = cudaMallocHost(reinterpret_cast<void**>(&h_q), kStageMax * dim * sizeof(float)) == cudaSuccess &&
+                        cudaMallocHost(reinterpret_cast<void**>(&h_ids), kStageMax * k * sizeof(std::uint32_t)) == cudaSuccess &&
+                        cudaMallocHost(reinterpret_cast<void**>(&h_dists), kStageMax * k * sizeof(float)) == cudaSuccess &&
+                        cudaMallocHost(reinterpret_cast<void**>(&h_counts), kStageMax * sizeof(std::uint32_t)) == cudaSuccess &&
+                        cudaMallocHost(reinterpret_cast<void**>(&h_stats), kStageMax * sizeof(pqtg_query_stats)) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();
+            free_stage();
+            return false;
+        }
+        stage_dim = dim;
+        stage_k = k;
+        return true;
+    }
     ~DeviceCopy() {
+        free_stage();
         pqtg_workspace_destroy(ws);
         pqtg_index_destroy(ix);
     }
@@ -370,8 +414,22 @@ std::vector<QueryResult> knn_query_batch(const PqtIndex& index, const VectorSet&
     std::vector<std::uint32_t> ids(nq * k), counts(nq);
     std::vector<float> dists(nq * k);
     std::vector<pqtg_query_stats> stats(nq);
-    check(pqtg_search(d.ix, d.ws, queries.data.data(), nq, queries.dim, k, ids.data(), dists.data(), counts.data(),
-                      stats.data()));
+    {
+        std::unique_lock<std::mutex> stage_lock(d.stage_mu, std::defer_lock);
+        if (nq <= kStageMax) stage_lock.lock();
+        if (nq <= kStageMax && d.stage(queries.dim, k)) {
+            // the latency path: page-locked staging, a replayed graph, zero-copy results
+            std::memcpy(d.h_q, queries.data.data(), nq * queries.dim * sizeof(float));
+            check(pqtg_search(d.ix, d.ws, d.h_q, nq, queries.dim, k, d.h_ids, d.h_dists, d.h_counts, d.h_stats));
+            std::memcpy(ids.data(), d.h_ids, nq * k * sizeof(std::uint32_t));
+            std::memcpy(dists.data(), d.h_dists, nq * k * sizeof(float));
+            std::memcpy(counts.data(), d.h_counts, nq * sizeof(std::uint32_t));
+            std::memcpy(stats.data(), d.h_stats, nq * sizeof(pqtg_query_stats));
+        } else {
+            check(pqtg_search(d.ix, d.ws, queries.data.data(), nq, queries.dim, k, ids.data(), dists.data(),
+                              counts.data(), stats.data()));
+        }
+    }
     // the reference times each query's stages (search.cpp:134-137,167-216,220,258); here each
     // query's stage kernels record their CTAs' device wall time (pqtg_workspace_query_times).
     // Bin selection and candidate gathering are one kernel: its time is bin_selection_us.

@@ -56,6 +56,8 @@ def main():
                               st.cuda_stream)
         torch.cuda.synchronize()
         ms = []
+        sampler = bench.ClockSampler(0, period=0.001)
+        sampler.__enter__()
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
@@ -64,6 +66,7 @@ def main():
             e1.record(st)
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
+        sampler.__exit__(None, None, None)
         stage = dev.stage_ms()  # [traverse, bin selection, re-rank + top-k, whole] of the last call
         hq = torch.from_numpy(Q).pin_memory()
         h_ids = torch.empty((B, k), dtype=torch.int32).pin_memory()
@@ -87,7 +90,8 @@ def main():
                 "device_ms": dmed, "device_p90_ms": float(np.percentile(ms, 90)),
                 "device_qps": B / dmed * 1e3, "e2e_ms": hmed, "e2e_p90_ms": float(np.percentile(hs, 90) * 1e3),
                 "e2e_qps": B / hmed * 1e3,
-                "stage_ms_last_call": {"traverse": stage[0], "binsel": stage[1], "rerank": stage[2], "total": stage[3]}}
+                "stage_ms_last_call": {"traverse": stage[0], "binsel": stage[1], "rerank": stage[2], "total": stage[3]},
+                "clocks": sampler.summary()}
         if not a.no_cpu and B in (1, 1000):
             from oracle.bindings import Ref
 
