@@ -284,8 +284,14 @@ __device__ inline void block_rank_keys(uint64_t* sel, uint32_t m, uint32_t kk, u
         const bool own = e < m;
         const uint64_t me = own ? sel[e] : 0ull;
         uint32_t rank = 0;
-        if (own)
-            for (uint32_t j = sub; j < m; j += g) rank += sel[j] < me;
+        if (own) {
+            uint32_t j = sub;
+            for (; j + 3 * g < m; j += 4 * g) {  // four loads in flight
+                const uint64_t a = sel[j], b = sel[j + g], c = sel[j + 2 * g], d = sel[j + 3 * g];
+                rank += (uint32_t)(a < me) + (uint32_t)(b < me) + (uint32_t)(c < me) + (uint32_t)(d < me);
+            }
+            for (; j < m; j += g) rank += sel[j] < me;
+        }
         for (uint32_t o = 1; o < g; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
         if (own && sub == 0 && rank < kk) out[rank] = me;
     } else {

@@ -58,7 +58,7 @@ def test_workspace_calls_on_two_streams_and_both_entry_points():
         assert_same_results(got, want, "device call")
 
 
-@pytest.mark.parametrize("name", ["p2_sift", "p4_gist", "p2_wide"])
+@pytest.mark.parametrize("name", ["p2_sift", "p4_gist", "p2_wide", "p2_exact"])
 @pytest.mark.parametrize("nq", [1, 5, 37])
 def test_small_batch_replays(name, nq):
     """Small batches: the device entry point captures its chained stages (PDL) as a CUDA graph on
@@ -68,10 +68,14 @@ def test_small_batch_replays(name, nq):
     from paper_1702_05911_b200._abi import check, lib
 
     g = load_golden(name)
-    k = int(g["k"])
     Q = g["queries"]
     nq = min(nq, Q.shape[0])
     dev = DeviceIndex(str(GOLDEN / f"{name}.pqt"), max_batch=64)
+    if name == "p2_exact":  # the exact stage behind the chain (search.cpp:229-249), k = 20
+        dev.attach_database(g["db"])
+        g = {"ids": g["ids_k20"], "dists": g["dists_k20"], "counts": g["counts_k20"], "stats": g["stats_k20"],
+             "k": 20}
+    k = int(g["k"])
     dq = torch.empty((nq, Q.shape[1]), dtype=torch.float32, device="cuda")
     ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
     d = torch.empty((nq, k), dtype=torch.float32, device="cuda")
