@@ -22,4 +22,7 @@ timeout 1500 python bench.py --workload sift1b --steps 20 --warmup 5 --no-recall
 timeout 1500 python bench.py --workload sift1b --sim-ranks 8 --steps 20 --warmup 5 --no-recall > $O/${T}_sift1b_sim8.json 2> $O/${T}_sift1b_sim8.err
 timeout 900 python tools/latency_sweep.py > $O/${T}_latency_sweep.json 2> $O/${T}_latency_sweep.err
 timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_sharded.py tests/test_gpu_api.py -x -q -k "exact or times or p2_small" > $O/${T}_san_memcheck.log 2>&1; echo "rc=$?" >> $O/${T}_san_memcheck.log
-echo done
+
+timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_api.py -x -q -k "small_batch and p2_sift" > $O/${T}_san_racecheck.log 2>&1; echo "rc=$?" >> $O/${T}_san_racecheck.log
+timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_api.py -x -q -k "small_batch and p2_sift" > $O/${T}_san_synccheck.log 2>&1; echo "rc=$?" >> $O/${T}_san_synccheck.log
+echo done2
