@@ -299,7 +299,7 @@ typedef struct pqtg_sharded pqtg_sharded;
 /* A fresh NCCL unique id (ncclGetUniqueId) for rank 0 to hand to every rank. PQTG_ERR_NCCL if
  * libnccl.so.2 cannot be loaded. */
 int pqtg_nccl_unique_id(uint8_t* id /* PQTG_NCCL_ID_BYTES */);
-/* One rank of a `world`-process deployment; `shard` holds positions
+/* One rank of a `world`-process (world <= 64) deployment; `shard` holds positions
  * pqtg_shard_range(n, world, rank) and lives on this process's device. Borrowed, must outlive
  * the handle. Collective (ncclCommInitRank). */
 int pqtg_sharded_create_nccl(pqtg_index* shard, const uint8_t* nccl_id, uint32_t rank, uint32_t world,

@@ -30,8 +30,10 @@ __global__ void __launch_bounds__(kBsThreads, 4)
                        uint32_t* __restrict__ ntuples, pqtg_query_stats* __restrict__ stats, uint32_t ts_log2,
                        uint32_t* __restrict__ ghash, uint32_t W2ab) {
     extern __shared__ __align__(16) unsigned char smem[];
-    griddep_wait();  // the traversal's lists (a PDL dependent in a chained chunk)
-    griddep_launch();
+    if (p.chain) {  // the traversal's lists (a PDL dependent in a chained chunk)
+        griddep_wait();
+        griddep_launch();
+    }
     qt_begin(p, blockIdx.x, 1);
     binsel_fast_body<P, HASH, SyncBlock>(p, blockIdx.x, l2c_in, l2d_in, slope_out, ranges, nranges, ncand, ntuples,
                                          stats, ts_log2, ghash, W2ab, smem, threadIdx.x);

@@ -217,8 +217,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t q = blockIdx.x;
-    griddep_wait();  // the traversal's lists (a PDL dependent in a chained chunk)
-    griddep_launch();
+    if (p.chain) {  // the traversal's lists (a PDL dependent in a chained chunk)
+        griddep_wait();
+        griddep_launch();
+    }
     qt_begin(p, q, 1);
     const uint32_t W = p.W, PW = P * W;
     const uint32_t H = (uint32_t)p.H;

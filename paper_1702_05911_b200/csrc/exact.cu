@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kExThreads) exact_rerank_kernel(DevParams p, c
     uint64_t* keys = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(y) + ((size_t)D * 4 + 15) / 16 * 16);
     __shared__ __align__(8) uint64_t full[kExStages];
     const uint64_t q = blockIdx.x;
-    griddep_wait();  // the re-rank's line-ranked prefix (a PDL dependent in a chained chunk)
+    if (p.chain) griddep_wait();  // the re-rank's line-ranked prefix (a PDL dependent in a chained chunk)
     qt_begin(p, q, 2);
     const uint32_t tid = threadIdx.x;
     const uint32_t n = line_counts[q];  // = rerank: min(max(k, rerank_exact), C) line-ranked candidates

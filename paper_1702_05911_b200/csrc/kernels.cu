@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kThreads) traverse_kernel(DevParams p, const f
     uint32_t* l2c = reinterpret_cast<uint32_t*>(l2d + P * W);
     const uint64_t q = blockIdx.x;
     qt_begin(p, q, 0);
-    griddep_launch();  // a chained chunk\'s bin selection may launch
+    if (p.chain) griddep_launch();  // a chained chunk's bin selection may launch
     const int tid = threadIdx.x;
 
     for (uint32_t i = tid; i < D; i += blockDim.x) y[i] = Q[q * D + i];
@@ -358,8 +358,10 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
     __shared__ typename Sort::TempStorage sort_tmp;
 
     const uint64_t q = blockIdx.x;
-    griddep_wait();  // the traversal's lists (a PDL dependent in a chained chunk)
-    griddep_launch();
+    if (p.chain) {  // the traversal's lists (a PDL dependent in a chained chunk)
+        griddep_wait();
+        griddep_launch();
+    }
     qt_begin(p, q, 1);
     const int tid = threadIdx.x;
 
@@ -754,8 +756,10 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
     __shared__ TopkShared s_sel;
 
     const uint64_t q = blockIdx.x;
-    griddep_wait();  // the bin selection's ranges (a PDL dependent in a chained chunk)
-    griddep_launch();
+    if (p.chain) {  // the bin selection's ranges (a PDL dependent in a chained chunk)
+        griddep_wait();
+        griddep_launch();
+    }
     qt_begin(p, q, 2);
     const int tid = threadIdx.x;
     const uint32_t R = nranges[q], C = ncand[q];

@@ -380,6 +380,21 @@ void launch_copy_segments(const std::vector<CopySegment>& segs, cudaStream_t s);
 void launch_scan_counts(const uint32_t* cnt, uint64_t n, uint64_t* off, cudaStream_t s);
 void launch_pack_ranges(const uint2* ranges, uint32_t stride, const uint32_t* cnt, const uint64_t* off, uint64_t n,
                         uint2* dense, cudaStream_t s);
+// The sharded exchange's query blocks (sharded.cpp): queries [lo[g], lo[g+1]) belong to block g;
+// v[q] is the gathered offset of q's ranges in its block's packed array, so q's ranges start at
+// base[g] + v[q] in the batch's packed array and end at base[g] + v[q + 1] (vend[g] for a block's
+// last query)
+constexpr uint32_t kMaxBlocks = 64;
+struct BlockMap {
+    uint32_t G;
+    uint64_t lo[kMaxBlocks + 1];
+    uint64_t base[kMaxBlocks];
+    uint64_t vend[kMaxBlocks];
+};
+// per-query rows + counts <- the batch's packed ranges, offsets from the blocks' own scans (no
+// scan over the batch)
+void launch_unpack_blocks(const uint2* dense, const uint64_t* v, const BlockMap& m, uint64_t n, uint32_t stride,
+                          uint2* rows, uint32_t* cnt, cudaStream_t s);
 void launch_unpack_ranges(const uint2* dense, const uint32_t* cnt, const uint64_t* off, uint64_t n, uint32_t stride,
                           uint2* ranges, cudaStream_t s);
 

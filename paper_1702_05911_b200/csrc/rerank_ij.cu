@@ -37,12 +37,12 @@ using namespace dev;
 __device__ unsigned long long* g_phase = nullptr;
 #define PQTG_PHASE(i)                                                                                  \
     do {                                                                                               \
-        if (g_phase && blockIdx.x == 0 && threadIdx.x == 0 && (blockIdx.y == 0 || (i) >= 6)) g_phase[i] = gtimer_ns(); \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (blockIdx.y == 0 || (i) >= 6) && g_phase) g_phase[i] = gtimer_ns(); \
     } while (0)
 
 #define PQTG_PHASE_VAL(i, v)                                                                           \
     do {                                                                                               \
-        if (g_phase && blockIdx.x == 0 && threadIdx.x == 0) g_phase[i] = (v);                          \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && g_phase) g_phase[i] = (v);                          \
     } while (0)
 
 namespace {
@@ -227,11 +227,13 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     }
     // everything above reads the index only; the bin selection's ranges and the traversal's fine
     // LUT are read below (a PDL dependent in a chained chunk starts before they are complete)
-    griddep_wait();
-    griddep_launch();
+    if (p.chain) {
+        griddep_wait();
+        griddep_launch();
+    }
     qt_begin(p, q, 2);
     const uint32_t R = nranges[q], C = ncand[q];
-    const uint2 rg0 = tid < R ? __ldcg(qr + tid) : make_uint2(0, 0);
+    const uint2 rg0 = tid < R ? (p.chain ? __ldcg(qr + tid) : __ldg(qr + tid)) : make_uint2(0, 0);
     // every index is a position range [shard_lo, shard_hi): [0, n) unsharded, possibly empty
     // on a shard (then every candidate is skipped and the query returns count 0)
     constexpr bool sharded = true;
@@ -485,6 +487,18 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         for (uint32_t u = tid; u < jn; u += step) {
             fetch(y_ + u * S_, va, ida);
             score(kb + u, va, ida);
+        }
+    } else if (S_ == 1) {  // one CTA per query (the throughput path): candidate u is candidate u
+        uint4 va[kVec], vb[kVec];
+        uint32_t ida = kInvalid, idb = kInvalid;
+        if (tid < jn) fetch(tid, va, ida);
+        for (uint32_t j = tid; j < jn; j += 2 * step) {
+            const uint32_t j2 = j + step;
+            if (j2 < jn) fetch(j2, vb, idb);
+            score(j, va, ida);
+            if (j2 >= jn) break;
+            if (j2 + step < jn) fetch(j2 + step, va, ida);
+            score(j2, vb, idb);
         }
     } else {
         uint4 va[kVec], vb[kVec];

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(128) traverse_screen_kernel(DevParams p, const
 
     const uint64_t q = blockIdx.x / P;
     qt_begin(p, q, 0);
-    griddep_launch();  // a chained chunk\'s bin selection may launch
+    if (p.chain) griddep_launch();  // a chained chunk's bin selection may launch
     const uint32_t part = blockIdx.x - (uint32_t)q * P;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t jobs = pp * k1, f0 = part * pp;

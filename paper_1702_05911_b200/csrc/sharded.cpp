@@ -512,9 +512,12 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
                 const Block b = blk[g];
                 if (g == r.g) {
                     cs.push_back({r.all_packed + toff[g], r.packed, total[g] * sizeof(uint2)});
+                    if (b.n) cs.push_back({r.all_off + b.lo, r.blk_off, b.n * sizeof(uint64_t)});
                     continue;
                 }
-                cs.push_back({r.ws().nranges + b.lo, c.nranges + b.lo, b.n * 4});
+                // the cache's offsets are over its whole packed batch (= this batch's toff[g] + the
+                // block's own offsets): base 0 for these blocks below
+                cs.push_back({r.all_off + b.lo, c.off + b.lo, b.n * sizeof(uint64_t)});
                 cs.push_back({r.ws().ncand + b.lo, c.ncand + b.lo, b.n * 4});
                 cs.push_back({stats_of(0) + b.lo, c.stats + b.lo, b.n * sizeof(pqtg_query_stats)});
                 cs.push_back({r.all_packed + toff[g], c.packed + c.toff[g], total[g] * sizeof(uint2)});
@@ -522,9 +525,9 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             launch_copy_segments(cs, r.stream);
         } else {
         // S4: the blocks' fine LUTs, counters, stats and packed ranges to every rank
-        gather([&](Rank& self, uint32_t root) -> Piece {
+        gather([&](Rank& self, uint32_t root) -> Piece {  // the blocks' own range offsets (counts follow)
             const Block b = blk[root];
-            return Piece{nullptr, self.ws().nranges + b.lo, b.n * sizeof(uint32_t)};
+            return Piece{self.g == root ? self.blk_off : nullptr, self.all_off + b.lo, b.n * sizeof(uint64_t)};
         });
         gather([&](Rank& self, uint32_t root) -> Piece {
             const Block b = blk[root];
@@ -544,9 +547,17 @@ static void sharded_search(pqtg_sharded& sh, const float* const* d_queries, uint
             on(r);
             if (i == 0) PQTG_CUDA_CHECK(cudaEventRecord(r.ev[2], r.stream));
             const DevParams& p = r.ix->prm;
-            launch_scan_counts(r.ws().nranges, nq, r.all_off, r.stream);
-            launch_unpack_ranges(r.all_packed, r.ws().nranges, r.all_off, nq, std::max<uint32_t>(budget, 1),
-                                 r.ws().ranges, r.stream);
+            BlockMap m{};
+            m.G = G;
+            for (uint32_t g = 0; g < G; ++g) {
+                const bool cached = sh.sim && g != r.g;  // offsets over the simulation cache's batch
+                m.lo[g] = blk[g].lo;
+                m.base[g] = cached ? 0 : toff[g];
+                m.vend[g] = cached ? toff[g] + total[g] : total[g];
+            }
+            m.lo[G] = nq;
+            launch_unpack_blocks(r.all_packed, r.all_off, m, nq, std::max<uint32_t>(budget, 1), r.ws().ranges,
+                                 r.ws().nranges, r.stream);
             launch_rerank(p, nq, (uint32_t)lk, r.ws().slice(0), r.l_ids, r.l_dists, r.l_counts, r.stream);
             if (exact) launch_exact_prefix(p, qptr(i), nq, (uint32_t)lk, r.l_ids, r.l_counts, r.l_exact, r.stream);
             r.ws().last_nq = nq;  // pqtg_workspace_read of this rank's view (pqtg_sharded_workspace)
@@ -696,7 +707,7 @@ static void check_shard(const DevIndex& ix, uint32_t world, uint32_t g) {
 int pqtg_sharded_create_nccl(pqtg_index* shard, const uint8_t* nccl_id, uint32_t rank, uint32_t world,
                              uint64_t max_batch, pqtg_sharded** out) {
     return guarded_sh([&] {
-        if (!shard || !nccl_id || !out || world == 0 || rank >= world || max_batch == 0)
+        if (!shard || !nccl_id || !out || world == 0 || world > kMaxBlocks || rank >= world || max_batch == 0)
             throw Error{PQTG_ERR_ARG, "bad sharded arguments"};
         *out = nullptr;
         DevIndex& ix = *shard->dev;

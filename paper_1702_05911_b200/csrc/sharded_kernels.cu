@@ -78,6 +78,24 @@ __global__ void __launch_bounds__(256) move_ranges_kernel(uint2* __restrict__ ro
 // pqtree.cpp:90-93) sequential fp32 order: the sharded search recomputes the batch's fine LUTs on
 // every rank (L·k1·fd multiply-adds per query) instead of all-gathering them (4·L·k1 bytes per
 // query, 4 KB on the SIFT1B tree)
+// one warp per query: its block by a search of m.lo, its offset and count from the gathered
+// block-relative offsets, then the row copy
+__global__ void __launch_bounds__(256) unpack_blocks_kernel(const uint2* __restrict__ dense,
+                                                            const uint64_t* __restrict__ v, const BlockMap m,
+                                                            uint64_t n, uint32_t stride, uint2* __restrict__ rows,
+                                                            uint32_t* __restrict__ cnt) {
+    const uint64_t q = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (q >= n) return;
+    uint32_t g = 0;
+    while (g + 1 < m.G && m.lo[g + 1] <= q) ++g;
+    const uint64_t a = v[q], b = q + 1 < m.lo[g + 1] ? v[q + 1] : m.vend[g];
+    const uint32_t c = (uint32_t)(b - a);
+    const uint2* d = dense + m.base[g] + a;
+    uint2* row = rows + q * (uint64_t)stride;
+    for (uint32_t i = threadIdx.x & 31; i < c; i += 32) row[i] = d[i];
+    if ((threadIdx.x & 31) == 0) cnt[q] = c;
+}
+
 // One warp per query (eight per CTA, no block barriers): the warp stages its query in shared
 // memory, then walks the parts, lane l computing centroids l, l + 32, ... of each (k1 = 32: the
 // centroid loads and the LUT stores are 128-byte coalesced rows; no index division).
@@ -169,6 +187,13 @@ void launch_pack_ranges(const uint2* ranges, uint32_t stride, const uint32_t* cn
                         uint2* dense, cudaStream_t s) {
     if (n == 0) return;
     move_ranges_kernel<true><<<(unsigned)((n + 7) / 8), 256, 0, s>>>(const_cast<uint2*>(ranges), stride, cnt, off, dense, n);
+    PQTG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_unpack_blocks(const uint2* dense, const uint64_t* v, const BlockMap& m, uint64_t n, uint32_t stride,
+                          uint2* rows, uint32_t* cnt, cudaStream_t s) {
+    if (n == 0) return;
+    unpack_blocks_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(dense, v, m, n, stride, rows, cnt);
     PQTG_CUDA_CHECK(cudaGetLastError());
 }
 

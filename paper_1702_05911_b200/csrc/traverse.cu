@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kTpThreads) traverse_part_kernel(DevParams p, 
     const uint64_t q = blockIdx.x / P;
     const uint32_t part = blockIdx.x - (uint32_t)q * P;
     qt_begin(p, q, 0);
-    griddep_launch();  // a chained chunk\'s bin selection may launch
+    if (p.chain) griddep_launch();  // a chained chunk's bin selection may launch
     const uint32_t tid = threadIdx.x;
     const uint32_t jobs = pp * k1;  // this part's fine LUT entries (f, i)
     const uint32_t f0 = part * pp;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(128) traverse_warp_kernel(DevParams p, const f
     const uint64_t q = blockIdx.x;
     const uint32_t tid = threadIdx.x, lane = tid & 31, part = tid >> 5;
     qt_begin(p, q, 0);
-    griddep_launch();  // a chained chunk\'s bin selection may launch
+    if (p.chain) griddep_launch();  // a chained chunk's bin selection may launch
     float* y = reinterpret_cast<float*>(smem);                        // [D]
     float* fine = y + ((p.D + 3) & ~3u) + part * pp * 32;             // [P][pp][<= 32]
     float* l1d = y + ((p.D + 3) & ~3u) + P * pp * 32 + part * 32;     // [P][32]
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(128) traverse_warp_wide_kernel(DevParams p, co
     const uint32_t P = p.P, m = p.m, fd = p.fd, pp = p.per_part, W = p.W;
     const uint64_t q = blockIdx.x;
     qt_begin(p, q, 0);
-    griddep_launch();  // a chained chunk\'s bin selection may launch
+    if (p.chain) griddep_launch();  // a chained chunk's bin selection may launch
     const uint32_t tid = threadIdx.x, lane = tid & 31, part = tid >> 5;
     float* y = reinterpret_cast<float*>(smem);
     float* fine = y + ((p.D + 3) & ~3u) + part * pp * 32;
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kTpThreads) traverse_small_kernel(DevParams p,
     const uint64_t q = blockIdx.x / P;
     const uint32_t part = blockIdx.x - (uint32_t)q * P;
     qt_begin(p, q, 0);
-    griddep_launch();  // a chained chunk\'s bin selection may launch
+    if (p.chain) griddep_launch();  // a chained chunk's bin selection may launch
     const uint32_t tid = threadIdx.x, f0 = part * pp;
     const uint32_t cb_bytes = k1 * m * k2 * 4, ft_bytes = pp * fd * k1 * 4;
     if (tid == 0) {
