@@ -83,6 +83,111 @@ std::vector<uint32_t> pair_stream(const uint32_t* entries, uint32_t tlen, uint32
     return out;
 }
 
+// Per-part bank map of the 1-byte line codes (k1 <= 16). The re-rank reads its per-query table
+// T[f][t] = (E, c2) with 8-byte gathers, 16 lanes at a time, and entries whose slots t share the
+// low nibble share a bank pair. The 16 lanes hold 16 consecutive candidates -- consecutive
+// positions of an inverted list -- so which pairs meet there is a property of the index: sample
+// groups of 16 consecutive positions, count per part how often two pairs meet, and give every
+// pair (i, j) a nibble n (slot t = i << 4 | n; the pairs of one i need distinct nibbles) so that
+// pairs that meet often sit in different bank pairs: greedy by how often a pair meets others,
+// then passes of moves / swaps within an i while they lower the count. Returns t per [f][pair];
+// empty when there are too few positions to sample.
+std::vector<uint8_t> bank_map(uint32_t L, const std::vector<uint32_t>& pairs, uint64_t npos,
+                              const std::function<uint32_t(uint64_t, uint32_t)>& pid_at) {
+    const uint32_t np = (uint32_t)pairs.size();
+    const uint64_t ng = std::min<uint64_t>(16384, npos / 16);
+    if (np < 2 || ng < 256) return {};
+    std::vector<uint8_t> out((size_t)L * np);
+    auto one_part = [&](uint32_t f) {
+        std::vector<uint32_t> w((size_t)np * np, 0);
+        for (uint64_t g = 0; g < ng; ++g) {
+            const uint64_t start = (npos - 16) * g / ng;
+            uint32_t u[16];
+            uint32_t m = 0;
+            for (uint32_t r = 0; r < 16; ++r) {
+                const uint32_t pid = pid_at(start + r, f);
+                if (pid >= np) continue;
+                bool seen = false;
+                for (uint32_t x = 0; x < m && !seen; ++x) seen = u[x] == pid;
+                if (!seen) u[m++] = pid;
+            }
+            for (uint32_t a = 0; a < m; ++a)
+                for (uint32_t b = a + 1; b < m; ++b) {
+                    ++w[(size_t)u[a] * np + u[b]];
+                    ++w[(size_t)u[b] * np + u[a]];
+                }
+        }
+        std::vector<uint32_t> nib(np, 16), first(np);
+        std::vector<uint64_t> meets(np, 0);
+        for (uint32_t a = 0; a < np; ++a) {
+            first[a] = pairs[a] & 0xFFFFu;
+            for (uint32_t b = 0; b < np; ++b) meets[a] += w[(size_t)a * np + b];
+        }
+        // cost of pair a in nibble n: how often it meets the pairs of other i holding n
+        auto cost = [&](uint32_t a, uint32_t n) {
+            uint64_t c = 0;
+            for (uint32_t b = 0; b < np; ++b)
+                if (b != a && nib[b] == n && first[b] != first[a]) c += w[(size_t)a * np + b];
+            return c;
+        };
+        std::vector<uint32_t> order(np);
+        for (uint32_t a = 0; a < np; ++a) order[a] = a;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return meets[x] > meets[y]; });
+        std::vector<uint32_t> used(16, 0);  // per i: nibbles taken (bitmask)
+        for (uint32_t a : order) {
+            const uint32_t i = first[a], j = pairs[a] >> 16, pref = (i + j) & 15u;
+            uint32_t best = 16;
+            uint64_t bc = ~0ull;
+            for (uint32_t k = 0; k < 16; ++k) {
+                const uint32_t n = (pref + k) & 15u;  // ties keep the fixed slot's nibble first
+                if (used[i] >> n & 1u) continue;
+                const uint64_t c = cost(a, n);
+                if (c < bc) {
+                    bc = c;
+                    best = n;
+                }
+            }
+            nib[a] = best;
+            used[i] |= 1u << best;
+        }
+        for (int pass = 0; pass < 4; ++pass) {
+            bool moved = false;
+            for (uint32_t a = 0; a < np; ++a) {
+                const uint32_t i = first[a], na = nib[a];
+                for (uint32_t n = 0; n < 16; ++n) {
+                    if (n == na) continue;
+                    uint32_t r = np;  // the pair of the same i holding n, if any
+                    if (used[i] >> n & 1u)
+                        for (uint32_t b = 0; b < np && r == np; ++b)
+                            if (first[b] == i && nib[b] == n) r = b;
+                    const int64_t before = (int64_t)cost(a, na) + (r < np ? (int64_t)cost(r, n) : 0);
+                    nib[a] = n;
+                    if (r < np) nib[r] = na;
+                    const int64_t after = (int64_t)cost(a, n) + (r < np ? (int64_t)cost(r, na) : 0);
+                    if (after < before) {
+                        if (r == np) used[i] = (used[i] & ~(1u << na)) | (1u << n);
+                        moved = true;
+                        break;
+                    }
+                    nib[a] = na;
+                    if (r < np) nib[r] = n;
+                }
+            }
+            if (!moved) break;
+        }
+        for (uint32_t a = 0; a < np; ++a) out[(size_t)f * np + a] = (uint8_t)(first[a] << 4 | nib[a]);
+    };
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    std::atomic<uint32_t> next{0};
+    for (unsigned t = 0; t < std::min<unsigned>(hw, L); ++t)
+        th.emplace_back([&] {
+            for (uint32_t f; (f = next.fetch_add(1)) < L;) one_part(f);
+        });
+    for (auto& t : th) t.join();
+    return out;
+}
+
 void parallel_rows(uint64_t n, const std::function<void(uint64_t, uint64_t)>& fn) {
     unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
     if (n < 65536 || hw == 1) {
@@ -438,22 +543,61 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     }
     std::vector<uint8_t> ij_of(npairs, 0);
     auto tcode = [](uint32_t i, uint32_t j) { return (uint8_t)((i << 4) | ((i + j) & 15u)); };
-    if (p.code_ij) {
-        std::vector<float> c2ij((size_t)L * 256, 0.0f);
-        uint32_t q = 0;
-        if (k1 > 1) {
-            for (uint32_t i = 0; i < k1; ++i)
-                for (uint32_t j = i + 1; j < k1; ++j) ij_of[q++] = tcode(i, j);
-        }
-        for (uint32_t f = 0; f < L; ++f)
-            for (uint32_t i = 0; i < k1; ++i)
-                for (uint32_t j = 0; j < k1; ++j) c2ij[(size_t)f * 256 + tcode(i, j)] = src.d2[((size_t)f * k1 + i) * k1 + j];
-        p.c2ij = upload(*ix, c2ij.data(), c2ij.size());
-    }
 
     // --- this shard's ids and line codes in slot order
     const uint64_t npos = shard_hi - shard_lo;
     const uint32_t* shard_ids = src.pos_lambda_q ? src.ids : src.ids + shard_lo;  // shard-only ids: from 0
+    // a position's stored pair id in part f (the staging loop below reads the same sources)
+    auto pid_at = [&](uint64_t pos, uint32_t f) -> uint32_t {
+        if (src.pos_lambda_q) return src.pos_pair_id[pos * L + f];
+        const uint64_t id = shard_ids[pos];
+        if (id >= n) return npairs;
+        if (src.records) {
+            const uint8_t* rec = src.records + (id * L + f) * (1 + src.record_pw);
+            return src.record_pw == 1 ? rec[1] : (uint32_t)rec[1] | ((uint32_t)rec[2] << 8);
+        }
+        return src.pair_id[id * L + f];
+    };
+    std::vector<uint8_t> tmap;  // [L][npairs] slot per part (the bank map), empty: fixed slots
+    if (p.code_ij) {
+        std::vector<uint32_t> pr;
+        if (k1 > 1) {
+            uint32_t q = 0;
+            for (uint32_t i = 0; i < k1; ++i)
+                for (uint32_t j = i + 1; j < k1; ++j, ++q) {
+                    ij_of[q] = tcode(i, j);
+                    pr.push_back(i | (j << 16));
+                }
+        }
+        static const bool no_map = [] {
+            const char* e = std::getenv("PQTG_BANK_MAP");
+            return e && std::strcmp(e, "0") == 0;
+        }();
+        if (!no_map && !rerank_needs_fixed_slots()) tmap = bank_map(L, pr, npos, pid_at);
+        std::vector<float> c2ij((size_t)L * 256, 0.0f);
+        if (tmap.empty()) {
+            for (uint32_t f = 0; f < L; ++f)
+                for (uint32_t i = 0; i < k1; ++i)
+                    for (uint32_t j = 0; j < k1; ++j)
+                        c2ij[(size_t)f * 256 + tcode(i, j)] = src.d2[((size_t)f * k1 + i) * k1 + j];
+        } else {
+            std::vector<uint2> c2slot((size_t)L * npairs);
+            std::vector<uint8_t> jt((size_t)L * 256, 0);
+            for (uint32_t f = 0; f < L; ++f)
+                for (uint32_t q = 0; q < npairs; ++q) {
+                    const uint32_t i = pr[q] & 0xFFFFu, j = pr[q] >> 16, t = tmap[(size_t)f * npairs + q];
+                    const float d = src.d2[((size_t)f * k1 + i) * k1 + j];
+                    c2ij[(size_t)f * 256 + t] = d;
+                    uint32_t bits;
+                    std::memcpy(&bits, &d, 4);
+                    c2slot[(size_t)f * npairs + q] = make_uint2(bits, t);
+                    jt[(size_t)f * 256 + t] = (uint8_t)j;
+                }
+            p.c2slot = upload(*ix, c2slot.data(), c2slot.size());
+            p.jt_ij = upload(*ix, jt.data(), jt.size());
+        }
+        p.c2ij = upload(*ix, c2ij.data(), c2ij.size());
+    }
     p.ids = upload(*ix, shard_ids, npos);
     {
         uint8_t* dcodes = dev_alloc<uint8_t>(ix->allocations, npos * p.row_bytes + 16, &ix->bytes);
@@ -490,7 +634,9 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
                             row[2 * f] = (uint8_t)lq;
                             // k1 <= 16: store the pair as its centroids (i << 4 | j), so the
                             // re-rank indexes the fine row and c2[f][i][j] directly
-                            row[2 * f + 1] = (uint8_t)(p.code_ij && pid < npairs ? ij_of[pid] : pid);
+                            row[2 * f + 1] = (uint8_t)(p.code_ij && pid < npairs
+                                                           ? (tmap.empty() ? ij_of[pid] : tmap[(size_t)f * npairs + pid])
+                                                           : pid);
                         } else {        // lambda block, then little-endian u16 pair ids (| i << 9)
                             const uint32_t v = p.code_pi && pid < npairs ? pi_of[pid] : pid;
                             row[f] = (uint8_t)lq;

@@ -656,10 +656,10 @@ namespace {
 // for (i, j) codes, [f][256].
 __device__ __forceinline__ void pair_terms(uint32_t b, uint32_t f, bool ij, const float* fine, const float* c2,
                                            const uint32_t* pairs, uint32_t k1, uint32_t npairs, float& b2,
-                                           float& a2, float& cc) {
-    if (ij) {  // b = i << 4 | ((i + j) & 15) (index_prep.cpp)
+                                           float& a2, float& cc, const uint8_t* __restrict__ jt) {
+    if (ij) {  // b = i << 4 | n: n = (i + j) & 15, or the per-part bank map's (jt: j of b)
         b2 = fine[f * k1 + (b >> 4)];
-        a2 = fine[f * k1 + (((b & 15u) - (b >> 4)) & 15u)];
+        a2 = fine[f * k1 + (jt ? (uint32_t)__ldg(jt + f * 256 + b) : (((b & 15u) - (b >> 4)) & 15u))];
         cc = c2[f * 256 + b];
     } else {
         const uint32_t pr = pairs[b];
@@ -672,7 +672,8 @@ __device__ __forceinline__ void pair_terms(uint32_t b, uint32_t f, bool ij, cons
 template <int LT, int PW>
 __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ row, const float* fine,
                                                    const float* c2, const uint32_t* pairs, uint32_t L,
-                                                   uint32_t k1, uint32_t npairs, bool ij, uint32_t pid_mask) {
+                                                   uint32_t k1, uint32_t npairs, bool ij, uint32_t pid_mask,
+                                                   const uint8_t* __restrict__ jt) {
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     float total = 0.0f;
     if constexpr (LT > 0) {
@@ -697,7 +698,7 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
                 pid &= pid_mask;  // code_pi rows carry the first centroid in bits 9..13
             }
             float b2, a2, cc;
-            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc);
+            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc, jt);
             const float lam = __fmul_rn((float)lq, inv255);
             const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
                                          __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
@@ -714,7 +715,7 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
                 pid = ((uint32_t)__ldg(row + L + 2 * f) | ((uint32_t)__ldg(row + L + 2 * f + 1) << 8)) & pid_mask;
             }
             float b2, a2, cc;
-            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc);
+            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc, jt);
             const float lam = __fmul_rn((float)lq, inv255);
             const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
                                          __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
@@ -790,7 +791,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
             const uint64_t lp = pos - p.shard_lo;
             const uint32_t id = __ldg(p.ids + lp);
             const float d = line_distance_row<LT, PW>(p.codes + lp * p.row_bytes, fine, c2, pairs, L, k1, npairs, ij,
-                                                      p.code_pi ? 0x1FFu : 0xFFFFu);
+                                                      p.code_pi ? 0x1FFu : 0xFFFFu, p.jt_ij);
             key = ((uint64_t)orderable(d) << 32) | id;
             ++mine;
         }

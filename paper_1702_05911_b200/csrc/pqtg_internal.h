@@ -94,7 +94,12 @@ struct DevParams {
     const uint8_t* codes;       // [shard positions][row_bytes]
     uint32_t code_ij;           // 1-byte codes hold i << 4 | ((i + j) & 15) instead of the pair id (k1 <= 16)
     uint32_t code_pi;           // 2-byte codes hold pid | i << 9 (16 < k1 <= 32)
-    const float* c2ij;          // [L][256] d2[f][i][j] at i << 4 | j (code_ij only)
+    const float* c2ij;          // [L][256] d2[f][i][j] at the pair's slot t (code_ij only)
+    // code_ij with a per-part bank map (index_prep.cpp bank_map): slot t = i << 4 | n_f(pair) and
+    // [L][npairs] (c2 bits, t) for the re-rank's table build, [L][256] j of slot t for the generic
+    // kernel; null: the fixed slot i << 4 | ((i + j) & 15)
+    const uint2* c2slot;
+    const uint8_t* jt_ij;
     const float* c2p;           // [L][512] d2[f][pair] (code_pi only)
     // exact re-rank (search.cpp:229-249): raw vectors n × D f32 in id order, or null
     const float* db;            // [n][db_stride] by id; on a position shard [shard rows][db_stride] by position
@@ -307,6 +312,9 @@ void launch_merge(uint32_t shards, uint64_t nq, uint32_t k, const uint32_t* ids,
 void configure_kernels(const DevParams& p, uint32_t k);
 // rerank_ij.cu (1-byte (i, j) pair codes, k1 <= 16, p_line in {16, 32, 64})
 bool rerank_ij_ok(const DevParams& p, uint32_t k);
+// the opt-in re-rank loops that derive j from the fixed slot i << 4 | ((i + j) & 15) (PQTG_RERANK=
+// packed / c3): indexes uploaded under them keep the fixed slots (no per-part bank map)
+bool rerank_needs_fixed_slots();
 bool rerank_ij_gkeys(const DevParams& p, uint32_t k);  // its keys go to the workspace (large budgets)
 uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k);  // CTAs per query (1 = no split)
 bool rerank_needs_gkeys(const DevParams& p, uint32_t k);  // launch_rerank will use ws.keys

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     const bool pair_lane = pi < p.npairs;
     uint32_t pi_i = 0, pi_j = 0;
     float c2v[kFPer];
+    uint32_t slot[kFPer];  // K1M = 16: the pair's T slot per part (the per-part bank map, or fixed)
     if (pair_lane) {
         const uint32_t pr = __ldg(p.pairs + pi);
         pi_i = pr & 0xFFFFu;
@@ -219,9 +220,16 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
             const uint32_t f = f0 + u * kFLanes;
-            if constexpr (K1M == 16)
-                c2v[u] = f < LT ? __ldg(p.c2ij + f * 256 + (pi_i << 4 | ((pi_i + pi_j) & 15u))) : 0.0f;
-            else
+            if constexpr (K1M == 16) {
+                if (!CT && p.c2slot) {
+                    const uint2 cs = f < LT ? __ldg(p.c2slot + f * p.npairs + pi) : make_uint2(0, 0);
+                    c2v[u] = __uint_as_float(cs.x);
+                    slot[u] = cs.y;
+                } else {
+                    slot[u] = pi_i << 4 | ((pi_i + pi_j) & 15u);
+                    c2v[u] = f < LT ? __ldg(p.c2ij + f * 256 + slot[u]) : 0.0f;
+                }
+            } else
                 c2v[u] = f < LT ? __ldg(p.c2 + f * p.npairs + pi) : 0.0f;
         }
     }
@@ -298,11 +306,11 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     // T[f][t(i, j)] = (E, c2) for every pair i < j (linequant.cpp:76-82); other entries
     // are never referenced. Thread: one pair, every (blockDim / 128)-th part.
     if (!DIRECT && pair_lane) {
-        // the pair's T slot: its device code (K1M = 16) or its pair id (K1M = 32)
-        const uint32_t ij = K1M == 16 ? (pi_i << 4 | ((pi_i + pi_j) & 15u)) : pi;
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
             const uint32_t f = f0 + u * kFLanes;
+            // the pair's T slot: its device code in part f (K1M = 16) or its pair id (K1M = 32)
+            const uint32_t ij = K1M == 16 ? slot[u] : pi;
             if (f < LT) {
                 const float b2 = fine[f * K1M + pi_i], a2 = fine[f * K1M + pi_j];
                 if constexpr (CT) {
@@ -702,6 +710,8 @@ size_t ij_smem(const DevParams& p, uint32_t k, bool gkeys) {
 }
 
 }  // namespace
+
+bool rerank_needs_fixed_slots() { return ij_mode() == 1 || ij_mode() == 2; }
 
 // keys go to the workspace when the shared-memory layout with them does not fit
 bool rerank_ij_gkeys(const DevParams& p, uint32_t k) { return ij_smem(p, k, false) + 4096 > (size_t)optin_smem(); }
