@@ -154,3 +154,29 @@ def test_shard_exact_outside_the_sharded_search_is_refused():
     dev.attach_database(g["db"][hix.ids[lo:hi].astype(np.int64)])
     with pytest.raises(Exception, match="sharded search"):
         dev.search(g["queries"], 20)
+
+
+def test_gpu_fixed_slots_without_bank_map():
+    """PQTG_BANK_MAP=0: the 1-byte line codes keep the fixed slots t = i << 4 | ((i + j) & 15)
+    instead of the per-part bank map learned at upload; same results (fresh process: the switch
+    is read once)."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    code = (
+        "from conftest import GOLDEN, load_golden\n"
+        "from test_gpu_parity import assert_same_results\n"
+        "from paper_1702_05911_b200 import DeviceIndex\n"
+        "for name in ['p2_sift', 'p4_gist', 'p2_wide', 'p2_small']:\n"
+        "    g = load_golden(name)\n"
+        "    dev = DeviceIndex(str(GOLDEN / f'{name}.pqt'))\n"
+        "    for nq in (1, len(g['queries'])):\n"
+        "        got = dev.search(g['queries'][:nq], int(g['k']))\n"
+        "        assert_same_results(got, tuple(x[:nq] for x in (g['ids'], g['dists'], g['counts'], g['stats'])), name)\n"
+        "print('ok')\n")
+    env = dict(os.environ, PQTG_BANK_MAP="0", PYTHONPATH=f"{REPO}:{REPO / 'tests'}")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=str(REPO / "tests"))
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
