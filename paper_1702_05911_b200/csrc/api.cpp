@@ -878,6 +878,9 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
             return a.type == cudaMemoryTypeHost && a.device == d.device ? a.devicePointer : nullptr;
         };
         void* zc_out[4] = {mapped(ids), mapped(dists), mapped(counts), mapped(stats)};
+        // (Zero-copy for larger batches -- queries read by the traversal and results written by the
+        // re-rank straight over the link -- measured far slower: DEEP100M e2e 6.35 -> 4.25 M q/s,
+        // the re-rank's scattered 4-byte result stores do not suit the link.)
         const bool zc = zero_copy && nq <= 64 && nq <= ws.max_batch && (zc_out[0] || !ids) && (zc_out[1] || !dists) &&
                         zc_out[2] && (zc_out[3] || !stats);
         auto enqueue_zc = [&] {
