@@ -87,8 +87,8 @@ __device__ __forceinline__ uint64_t bitonic_block(uint64_t key, uint32_t tid, ui
             } else {
                 other = __shfl_xor_sync(0xffffffffu, key, jj);
             }
-            const bool take_min = ((tid & kk) == 0) == ((tid & jj) == 0);
-            key = (take_min ? (other < key) : (other > key)) ? other : key;
+            const uint32_t take_min = ((tid & kk) == 0) == ((tid & jj) == 0), lt = other < key, gt = other > key;
+            key = ((take_min & lt) | (~take_min & 1u & gt)) ? other : key;  // branch-free
         }
     }
     return key;
@@ -357,7 +357,10 @@ __device__ __forceinline__ void warp_sort_regs(uint64_t (&e)[EPT], uint32_t lane
                     if (i & jj) continue;
                     const uint32_t n = lane * EPT + i;
                     const uint64_t a = e[i], b = e[i ^ jj];
-                    const bool sw = ((n & kk) == 0) ? (b < a) : (a < b);
+                    // branch-free (the direction is lane-dependent: a ternary here compiled to
+                    // divergent branches with reconvergence around every exchange)
+                    const uint32_t up = (n & kk) == 0, lt = b < a, gt = a < b;
+                    const bool sw = (up & lt) | (~up & 1u & gt);
                     e[i] = sw ? b : a;
                     e[i ^ jj] = sw ? a : b;
                 }
@@ -366,8 +369,8 @@ __device__ __forceinline__ void warp_sort_regs(uint64_t (&e)[EPT], uint32_t lane
                 for (uint32_t i = 0; i < (uint32_t)EPT; ++i) {
                     const uint32_t n = lane * EPT + i;
                     const uint64_t o = __shfl_xor_sync(0xffffffffu, e[i], jj / EPT);
-                    const bool take_min = ((n & kk) == 0) == ((n & jj) == 0);
-                    e[i] = (take_min ? (o < e[i]) : (o > e[i])) ? o : e[i];
+                    const uint32_t take_min = ((n & kk) == 0) == ((n & jj) == 0), lt = o < e[i], gt = o > e[i];
+                    e[i] = ((take_min & lt) | (~take_min & 1u & gt)) ? o : e[i];
                 }
             }
         }
