@@ -527,9 +527,22 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     // first centroid, v = pid | i << 9, so the re-rank reads fine[f][i] without the pair table
     p.code_pi = (pw == 2 && k1 <= 32 && npairs <= 512) ? 1u : 0u;
     std::vector<uint16_t> pi_of(p.code_pi ? npairs : 0);
-    if (p.code_pi) {
+    // DIRECT shards (rerank_ij.cu: ~budget/8 candidates per query at 8 shards, no per-query table)
+    p.code_j = p.code_pi && shard_hi > shard_lo && (shard_hi - shard_lo) * 4 <= n ? 1u : 0u;
+    if (p.code_j) {
+        std::vector<float> c2v((size_t)L * 1024, 0.0f);
         uint32_t q = 0;
         for (uint32_t i = 0; i < k1; ++i)
+            for (uint32_t j = i + 1; j < k1; ++j, ++q) pi_of[q] = (uint16_t)(i | (j << 5));
+        for (uint32_t f = 0; f < L; ++f)
+            for (uint32_t i = 0; i < k1; ++i)
+                for (uint32_t j = i + 1; j < k1; ++j)
+                    c2v[(size_t)f * 1024 + (i | (j << 5))] = src.d2[((size_t)f * k1 + i) * k1 + j];
+        p.c2v = upload(*ix, c2v.data(), c2v.size());
+    }
+    if (p.code_pi) {
+        uint32_t q = 0;
+        for (uint32_t i = 0; i < k1 && !p.code_j; ++i)
             for (uint32_t j = i + 1; j < k1; ++j, ++q) pi_of[q] = (uint16_t)(q | (i << 9));
         // c2 rows padded to 512 pairs: the DIRECT re-rank's loads use compile-time row offsets
         std::vector<float> c2p((size_t)L * 512, 0.0f);
@@ -539,7 +552,7 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
                 for (uint32_t j = i + 1; j < k1; ++j, ++pq)
                     c2p[(size_t)f * 512 + pq] = src.d2[((size_t)f * k1 + i) * k1 + j];
         }
-        p.c2p = upload(*ix, c2p.data(), c2p.size());
+        if (!p.code_j) p.c2p = upload(*ix, c2p.data(), c2p.size());
     }
     std::vector<uint8_t> ij_of(npairs, 0);
     auto tcode = [](uint32_t i, uint32_t j) { return (uint8_t)((i << 4) | ((i + j) & 15u)); };

@@ -656,11 +656,16 @@ namespace {
 // for (i, j) codes, [f][256].
 __device__ __forceinline__ void pair_terms(uint32_t b, uint32_t f, bool ij, const float* fine, const float* c2,
                                            const uint32_t* pairs, uint32_t k1, uint32_t npairs, float& b2,
-                                           float& a2, float& cc, const uint8_t* __restrict__ jt) {
+                                           float& a2, float& cc, const uint8_t* __restrict__ jt,
+                                           const float* __restrict__ c2v) {
     if (ij) {  // b = i << 4 | n: n = (i + j) & 15, or the per-part bank map's (jt: j of b)
         b2 = fine[f * k1 + (b >> 4)];
         a2 = fine[f * k1 + (jt ? (uint32_t)__ldg(jt + f * 256 + b) : (((b & 15u) - (b >> 4)) & 15u))];
         cc = c2[f * 256 + b];
+    } else if (c2v) {  // code_j: b = i | j << 5 (index_prep.cpp, DIRECT shards)
+        b2 = fine[f * k1 + (b & 31u)];
+        a2 = fine[f * k1 + ((b >> 5) & 31u)];
+        cc = __ldg(c2v + f * 1024 + (b & 0x3FFu));
     } else {
         const uint32_t pr = pairs[b];
         b2 = fine[f * k1 + (pr & 0xFFFFu)];
@@ -673,7 +678,7 @@ template <int LT, int PW>
 __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ row, const float* fine,
                                                    const float* c2, const uint32_t* pairs, uint32_t L,
                                                    uint32_t k1, uint32_t npairs, bool ij, uint32_t pid_mask,
-                                                   const uint8_t* __restrict__ jt) {
+                                                   const uint8_t* __restrict__ jt, const float* __restrict__ c2v) {
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     float total = 0.0f;
     if constexpr (LT > 0) {
@@ -695,10 +700,10 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
                 lq = (wds[f >> 2] >> ((f & 3) * 8)) & 0xFFu;
                 const int b0 = LT + 2 * f, b1 = b0 + 1;
                 pid = ((wds[b0 >> 2] >> ((b0 & 3) * 8)) & 0xFFu) | (((wds[b1 >> 2] >> ((b1 & 3) * 8)) & 0xFFu) << 8);
-                pid &= pid_mask;  // code_pi rows carry the first centroid in bits 9..13
+                pid &= pid_mask;  // code_pi rows carry the first centroid in bits 9..13 (code_j: i | j << 5)
             }
             float b2, a2, cc;
-            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc, jt);
+            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc, jt, c2v);
             const float lam = __fmul_rn((float)lq, inv255);
             const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
                                          __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
@@ -715,7 +720,7 @@ __device__ __forceinline__ float line_distance_row(const uint8_t* __restrict__ r
                 pid = ((uint32_t)__ldg(row + L + 2 * f) | ((uint32_t)__ldg(row + L + 2 * f + 1) << 8)) & pid_mask;
             }
             float b2, a2, cc;
-            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc, jt);
+            pair_terms(pid, f, ij, fine, c2, pairs, k1, npairs, b2, a2, cc, jt, c2v);
             const float lam = __fmul_rn((float)lq, inv255);
             const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), cc)),
                                          __fmul_rn(lam, __fsub_rn(__fsub_rn(a2, b2), cc)));
@@ -791,7 +796,8 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(DevParams p, uint32_t 
             const uint64_t lp = pos - p.shard_lo;
             const uint32_t id = __ldg(p.ids + lp);
             const float d = line_distance_row<LT, PW>(p.codes + lp * p.row_bytes, fine, c2, pairs, L, k1, npairs, ij,
-                                                      p.code_pi ? 0x1FFu : 0xFFFFu, p.jt_ij);
+                                                      p.code_j ? 0x3FFu : p.code_pi ? 0x1FFu : 0xFFFFu, p.jt_ij,
+                                                      p.code_j ? p.c2v : nullptr);
             key = ((uint64_t)orderable(d) << 32) | id;
             ++mine;
         }

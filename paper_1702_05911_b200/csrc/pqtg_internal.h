@@ -94,6 +94,11 @@ struct DevParams {
     const uint8_t* codes;       // [shard positions][row_bytes]
     uint32_t code_ij;           // 1-byte codes hold i << 4 | ((i + j) & 15) instead of the pair id (k1 <= 16)
     uint32_t code_pi;           // 2-byte codes hold pid | i << 9 (16 < k1 <= 32)
+    // code_pi on a position shard holding <= 1/4 of the lists (the re-rank's DIRECT mode): the
+    // 2-byte codes hold v = i | j << 5 instead, so the re-rank reads fine[f][j] and c2 by v
+    // without a pair-table lookup
+    uint32_t code_j;
+    const float* c2v;           // [L][1024] d2[f][i][j] at i | j << 5 (code_j only)
     const float* c2ij;          // [L][256] d2[f][i][j] at the pair's slot t (code_ij only)
     // code_ij with a per-part bank map (index_prep.cpp bank_map): slot t = i << 4 | n_f(pair) and
     // [L][npairs] (c2 bits, t) for the re-rank's table build, [L][256] j of slot t for the generic

@@ -91,7 +91,7 @@ __host__ __device__ inline IjLayout ij_layout(uint32_t L, uint32_t budget, uint3
     size_t o = 0;
     l.t = o;  // T (DIRECT: the pairs' j, u16; PK: c2 by code), fine, delta and rid sit at compile-time offsets
     // PK: a 1 KB-aligned (at run time) c2 table L × 1 KB followed by the fine rows
-    o += direct ? (size_t)t_entries(K1M) * 2
+    o += direct ? (size_t)0
                 : (pk ? (size_t)L * 1024 + (size_t)L * K1M * 4 + 1024 : (size_t)L * t_entries(K1M) * 8);
     l.fine = o;
     o += (size_t)L * K1M * 4;
@@ -179,7 +179,6 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem);
     const uint32_t c2s = (s_base + 1023u) & ~1023u, fs = c2s + LT * 1024u;
     float* Ct = reinterpret_cast<float*>(smem + (c2s - s_base));
-    uint16_t* jt = reinterpret_cast<uint16_t*>(smem);  // DIRECT: j of pair id
     float* fine = CT ? reinterpret_cast<float*>(smem + (fs - s_base)) : reinterpret_cast<float*>(smem + fix.fine);
     // candidate keys: shared memory, or this query's row of the workspace's key buffer when the
     // budget is too large for shared memory (budget > ~8k)
@@ -213,9 +212,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         pi_i = pr & 0xFFFFu;
         pi_j = pr >> 16;
         if constexpr (DIRECT) {
-            if (f0 == 0) jt[pi] = (uint16_t)pi_j;
-            for (uint32_t o = pi + blockDim.x; o < p.npairs && f0 == 0; o += blockDim.x)  // more pairs than threads
-                jt[o] = (uint16_t)(__ldg(p.pairs + o) >> 16);
+            // (the codes carry j: nothing to stage)
         } else
 #pragma unroll
         for (uint32_t u = 0; u < kFPer; ++u) {
@@ -367,6 +364,10 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                     ti = (half >> 8) & 0xFFu;
                     fi = ti >> 4;
                     lq = half & 0xFFu;
+                } else if constexpr (DIRECT) {
+                    lq = (w[f >> 2] >> ((f & 3) * 8)) & 0xFFu;                 // λ block
+                    ti = (w[LT / 4 + (f >> 1)] >> ((f & 1) * 16)) & 0x3FFu;   // i | j << 5
+                    fi = ti & 31u;
                 } else {
                     lq = (w[f >> 2] >> ((f & 3) * 8)) & 0xFFu;                 // λ block
                     const uint32_t v2 = (w[LT / 4 + (f >> 1)] >> ((f & 1) * 16)) & 0xFFFFu;  // pid | i << 9
@@ -376,8 +377,8 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                 const float b2 = fine[f * K1M + fi];
                 float2 ec;
                 if constexpr (DIRECT) {  // E and c2 of this part, in T's roundings
-                    const float a2 = fine[f * K1M + jt[ti]];
-                    ec.y = __ldg(p.c2p + f * 512 + ti);
+                    const float a2 = fine[f * K1M + (ti >> 5)];
+                    ec.y = __ldg(p.c2v + f * 1024 + ti);
                     ec.x = __fsub_rn(__fsub_rn(a2, b2), ec.y);
                 } else if constexpr (C3) {  // c2 by code, a2 = fine[f][j] with j = (t − i) & 15
                     const float a2 = fine[f * K1M + ((ti - fi) & 15u)];
@@ -690,9 +691,7 @@ int code_k1m(const DevParams& p) { return p.code_ij ? 16 : (p.code_pi ? 32 : 0);
 
 // DIRECT when this index re-ranks a small share of each query's candidates: a position shard
 // holding at most a quarter of the lists (about budget / 4 candidates per query)
-bool ij_direct(const DevParams& p) {
-    return code_k1m(p) == 32 && p.shard_hi > p.shard_lo && (p.shard_hi - p.shard_lo) * 4 <= p.n;
-}
+bool ij_direct(const DevParams& p) { return code_k1m(p) == 32 && p.code_j; }  // decided at upload
 
 int optin_smem() {
     int dev = 0, optin = 0;
