@@ -180,3 +180,19 @@ def test_gpu_fixed_slots_without_bank_map():
     env = dict(os.environ, PQTG_BANK_MAP="0", PYTHONPATH=f"{REPO}:{REPO / 'tests'}")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=str(REPO / "tests"))
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+def test_local_sharded_bank_mapped_codes():
+    """k1 = 16 shards large enough for the per-part bank map (index_prep.cpp bank_map, learned
+    from each shard's own positions) against the unsharded index, bit for bit."""
+    dev = torch.device("cuda", 0)
+    cfg = PqtConfig(dim=96, p_tree=2, k1=16, k2=8, w=4, p_line=32, train_iters=4, seed=5, candidate_budget=2048,
+                    rerank_exact=0)
+    X = builder.synth_clustered(60_000 + 64, cfg.dim, 60, 20.0, 5, device=dev)
+    db, Q = X[:60_000], X[60_000:].cpu().numpy()
+    hix = builder.build_index(db, db[:20_000], cfg)
+    want = DeviceIndex(hix).search(Q, 50)
+    assert_same_results(want, Oracle(hix).knn(Q, 50), "unsharded vs oracle")
+    lsi = LocalShardedIndex(hix, 2, max_batch=64)
+    for r, got in enumerate(run_local(lsi, Q, 50, True)):
+        assert_same_results(got, want, f"bank-mapped shards rank {r}")
