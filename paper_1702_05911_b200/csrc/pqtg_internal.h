@@ -33,21 +33,40 @@ struct Error {
     } while (0)
 
 // Kernel launch; with `chain`, as a programmatic dependent of the stream's previous kernel (PDL:
-// its CTAs may start while that kernel drains, and call griddep_wait() before reading its results)
+// its CTAs may start while that kernel drains, and call griddep_wait() before reading its
+// results); with a cluster shape other than 1x1x1, as thread-block clusters of that shape
 template <typename... KArgs, typename... Args>
-void launch_kernel(bool chain, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                   Args&&... args) {
+void launch_kernel_cluster(bool chain, dim3 cluster, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                           cudaStream_t s, Args&&... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    unsigned n = 0;
+    if (chain) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (cluster.x * cluster.y * cluster.z > 1) {
+        at[n].id = cudaLaunchAttributeClusterDimension;
+        at[n].val.clusterDim.x = cluster.x;
+        at[n].val.clusterDim.y = cluster.y;
+        at[n].val.clusterDim.z = cluster.z;
+        ++n;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = chain ? 1 : 0;
+    cfg.numAttrs = n;
     PQTG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+
+template <typename... KArgs, typename... Args>
+void launch_kernel(bool chain, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args&&... args) {
+    launch_kernel_cluster(chain, dim3(1, 1, 1), kernel, grid, block, smem, s, std::forward<Args>(args)...);
 }
 
 // ---------------------------------------------------------------- constants
@@ -122,6 +141,9 @@ struct DevParams {
     // the chunk's stages run as one programmatic-dependent chain (PDL): bin selection and the
     // re-rank (and the exact stage) are launched as dependents of the previous stage's kernel
     uint32_t chain;
+    // the split re-rank's slices of a query form one thread-block cluster: the lists meet in
+    // distributed shared memory instead of global memory (set per launch, rerank_ij.cu)
+    uint32_t split_cluster;
 };
 
 struct DevIndex {

@@ -20,8 +20,13 @@
 // per-pair table) and c2 = d2[f][pair] (read through L1), the same three roundings, and leaves
 // the shared memory small enough for two CTAs per SM.
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdlib>
 #include <cstring>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "pqtg_internal.h"
@@ -30,6 +35,7 @@
 namespace pqtg {
 
 using namespace dev;
+namespace cg = cooperative_groups;
 
 // phase clocks of CTA (0, 0) of the last re-rank launch (PQTG_PHASES=1: tools/phase_probe.py);
 // null otherwise. [0] start, [1] prologue done, [2] range map done, [3] candidates scored,
@@ -559,24 +565,42 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     // query's last-arriving slice ranks the union's top k (threadfence-reduction pattern: no
     // second launch)
     const uint32_t S = gridDim.y;
-    uint64_t* lst = split_keys + ((uint64_t)q * kSplitMax + blockIdx.y) * k;
-    block_rank_keys(sel, m, kk, lst);
-    for (uint32_t i = kk + tid; i < k; i += blockDim.x) lst[i] = kSentinel;
-    PQTG_PHASE(5);
-    __threadfence();
-    __syncthreads();
-    __shared__ uint32_t s_last;
-    if (tid == 0) s_last = atomicAdd(&split_ctr[q], 1u) == S - 1;
-    __syncthreads();
-    if (!s_last) return;
-    PQTG_PHASE(7);
-    __threadfence();
-    // the S lists (contiguous, stride k) into keys[0, S·k) in one pass; the kept keys' list map
-    // goes behind them (2·S·k keys <= budget, rerank_split)
-    const uint64_t* src = split_keys + (uint64_t)q * kSplitMax * k;
-    for (uint32_t i = tid; i < S * k; i += blockDim.x) keys[i] = __ldcg(src + i);
-    if (tid == 0) split_ctr[q] = 0;  // ready for the next call
-    __syncthreads();
+    if (p.split_cluster) {
+        // the query's slices are one cluster: each ranks its list into its own shared key array,
+        // slice 0 reads the others' through distributed shared memory, then all may exit
+        block_rank_keys(sel, m, kk, keys);
+        for (uint32_t i = kk + tid; i < k; i += blockDim.x) keys[i] = kSentinel;
+        PQTG_PHASE(5);
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();
+        PQTG_PHASE(7);
+        if (blockIdx.y == 0)
+            for (uint32_t i = tid; i < (S - 1) * k; i += blockDim.x) {
+                const uint32_t r = 1 + i / k, j = i - (r - 1) * k;
+                keys[r * k + j] = cl.map_shared_rank(keys, r)[j];
+            }
+        cl.sync();  // the other slices' shared memory stays until slice 0 has read it
+        if (blockIdx.y != 0) return;
+    } else {
+        uint64_t* lst = split_keys + ((uint64_t)q * kSplitMax + blockIdx.y) * k;
+        block_rank_keys(sel, m, kk, lst);
+        for (uint32_t i = kk + tid; i < k; i += blockDim.x) lst[i] = kSentinel;
+        PQTG_PHASE(5);
+        __threadfence();
+        __syncthreads();
+        __shared__ uint32_t s_last;
+        if (tid == 0) s_last = atomicAdd(&split_ctr[q], 1u) == S - 1;
+        __syncthreads();
+        if (!s_last) return;
+        PQTG_PHASE(7);
+        __threadfence();
+        // the S lists (contiguous, stride k) into keys[0, S·k) in one pass; the kept keys' list
+        // map goes behind them (2·S·k keys <= budget, rerank_split)
+        const uint64_t* src = split_keys + (uint64_t)q * kSplitMax * k;
+        for (uint32_t i = tid; i < S * k; i += blockDim.x) keys[i] = __ldcg(src + i);
+        if (tid == 0) split_ctr[q] = 0;  // ready for the next call
+        __syncthreads();
+    }
     PQTG_PHASE(8);
     // per list (lane g): its length n_g (keys below kSentinel); k2 = min(k, Σ n_g). The first
     // c = ceil(k2 / S) keys of every list are <= M, the largest of their last keys, so when those
@@ -780,6 +804,45 @@ uint32_t rerank_split(const DevParams& p, uint64_t nq, uint32_t k) {
     return s >= 2 ? (uint32_t)s : 1u;
 }
 
+// Whether S-CTA clusters of this re-rank variant (threads, sm bytes) can be resident
+// (cudaOccupancyMaxActiveClusters; clusters above 8 CTAs need the non-portable opt-in), per device;
+// PQTG_SPLIT_CLUSTER=0 keeps the global-memory merge
+template <class Kernel>
+bool split_cluster_ok(Kernel kernel, uint32_t S, int threads, size_t sm) {
+    static const bool off = [] {
+        const char* e = std::getenv("PQTG_SPLIT_CLUSTER");
+        return e && std::strcmp(e, "0") == 0;
+    }();
+    if (off || S < 2 || S > kSplitMax) return false;
+    int dev = 0;
+    PQTG_CUDA_CHECK(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, uint32_t, int, size_t, int>, bool> known;
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), S, threads, sm, dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto it = known.find(key);
+    if (it != known.end()) return it->second;
+    bool ok = S <= 8 || cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    if (ok) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(1, S, 1);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = sm;
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = 1;
+        at.val.clusterDim.y = S;
+        at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        ok = cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) == cudaSuccess && n > 0;
+    }
+    cudaGetLastError();
+    known[key] = ok;
+    return ok;
+}
+
 void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice& ws, uint32_t* ids, float* dists,
                       uint32_t* counts, cudaStream_t s) {
     const uint32_t S = rerank_split(p, nq, k);
@@ -790,10 +853,15 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
     if (gk && !ws.keys) throw Error{PQTG_ERR_ARG, "workspace has no candidate-key buffer for this budget"};
     const size_t sm = ij_smem(p, k, gk);
     uint64_t* gkeys = gk ? ws.keys : nullptr;
-#define PQTG_IJ(LT, K, D, ...)                                                                                \
-    launch_kernel(p.chain, rerank_ij_kernel<LT, K, D, ##__VA_ARGS__>, dim3((unsigned)nq, S), dim3(ij_threads(LT, D)), sm, s,                   \
-        p, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, ids, dists, counts, gkeys, ws.split_keys,          \
-        ws.split_ctr)
+    // a split query's S slices as one cluster (lists through DSMEM) when its shape can be resident
+    auto launch_ij = [&](auto kernel, int threads) {
+        DevParams pl = p;
+        pl.split_cluster = (S > 1 && !gk && split_cluster_ok(kernel, S, threads, sm)) ? 1u : 0u;
+        launch_kernel_cluster(p.chain, dim3(1, pl.split_cluster ? S : 1, 1), kernel, dim3((unsigned)nq, S),
+                              dim3(threads), sm, s, pl, k, cap, ws.fine, ws.ranges, ws.nranges, ws.ncand, ids, dists,
+                              counts, gkeys, ws.split_keys, ws.split_ctr);
+    };
+#define PQTG_IJ(LT, K, D, ...) launch_ij(rerank_ij_kernel<LT, K, D, ##__VA_ARGS__>, ij_threads(LT, D))
     if (code_k1m(p) == 32) {
         const bool direct = ij_direct(p);
         if (p.L == 16) {

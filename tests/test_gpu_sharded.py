@@ -94,12 +94,13 @@ def test_local_sharded_sift1b_tree():
         assert_same_results(got, want, f"sift1b tree G=8 rank {r}")
 
 
-@pytest.mark.parametrize("split", ["0", "1"])
-def test_gpu_split_rerank_switch(split):
+@pytest.mark.parametrize("split,cluster", [("0", "1"), ("1", "1"), ("1", "0")])
+def test_gpu_split_rerank_switch(split, cluster):
     """The small-batch split re-rank (default; PQTG_SPLIT=0 turns it off: each query's candidates
-    over up to 16 CTAs, the last-arriving slice merging their sorted lists pairwise) and the
-    one-CTA-per-query re-rank against the golden fixtures, in a fresh process (the switch is read
-    once)."""
+    over up to 16 CTAs whose sorted lists meet in one slice -- through distributed shared memory
+    when the slices form a cluster, through global memory and an arrival counter with
+    PQTG_SPLIT_CLUSTER=0) and the one-CTA-per-query re-rank against the golden fixtures, in a fresh
+    process (the switches are read once)."""
     import subprocess
     import sys
 
@@ -118,7 +119,7 @@ def test_gpu_split_rerank_switch(split):
     import os
     from conftest import REPO
 
-    env = dict(os.environ, PQTG_SPLIT=split, PYTHONPATH=f"{REPO}:{REPO / 'tests'}")
+    env = dict(os.environ, PQTG_SPLIT=split, PQTG_SPLIT_CLUSTER=cluster, PYTHONPATH=f"{REPO}:{REPO / 'tests'}")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=str(REPO / "tests"))
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
