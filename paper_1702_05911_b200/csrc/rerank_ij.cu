@@ -566,21 +566,22 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     // second launch)
     const uint32_t S = gridDim.y;
     if (p.split_cluster) {
-        // the query's slices are one cluster: each ranks its list into its own shared key array,
-        // slice 0 reads the others' through distributed shared memory, then all may exit
-        block_rank_keys(sel, m, kk, keys);
-        for (uint32_t i = kk + tid; i < k; i += blockDim.x) keys[i] = kSentinel;
+        // the query's slices are one cluster: slice y ranks its list into keys[y·k ..) of its own
+        // shared memory, every slice reads the others' lists through distributed shared memory,
+        // and after a second barrier (no slice's memory is read any more) each one cuts the lists
+        // the same way and ranks 1/S of the kept keys (below)
+        const uint32_t y = blockIdx.y;
+        block_rank_keys(sel, m, kk, keys + y * k);
+        for (uint32_t i = kk + tid; i < k; i += blockDim.x) keys[y * k + i] = kSentinel;
         PQTG_PHASE(5);
         cg::cluster_group cl = cg::this_cluster();
         cl.sync();
         PQTG_PHASE(7);
-        if (blockIdx.y == 0)
-            for (uint32_t i = tid; i < (S - 1) * k; i += blockDim.x) {
-                const uint32_t r = 1 + i / k, j = i - (r - 1) * k;
-                keys[r * k + j] = cl.map_shared_rank(keys, r)[j];
-            }
-        cl.sync();  // the other slices' shared memory stays until slice 0 has read it
-        if (blockIdx.y != 0) return;
+        for (uint32_t i = tid; i < (S - 1) * k; i += blockDim.x) {
+            const uint32_t rr = i / k, r = rr + (rr >= y), j = i - rr * k;
+            keys[r * k + j] = cl.map_shared_rank(keys, r)[r * k + j];
+        }
+        cl.sync();
     } else {
         uint64_t* lst = split_keys + ((uint64_t)q * kSplitMax + blockIdx.y) * k;
         block_rank_keys(sel, m, kk, lst);
@@ -658,7 +659,39 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     }
     __syncthreads();
     PQTG_PHASE(10);
-    if (E <= blockDim.x) {
+    if (p.split_cluster) {
+        // this slice's share of the kept keys, each counted against all of them by g threads
+        const uint32_t y = blockIdx.y, lo = E * y / S, nm = E * (y + 1) / S - lo;
+        uint32_t n2 = 1;
+        while (n2 < nm) n2 <<= 1;
+        uint32_t g = blockDim.x / n2;
+        g = g > 32 ? 32 : (g ? g : 1);
+        for (uint32_t base = 0; base < nm; base += blockDim.x / g) {
+            const uint32_t e = base + tid / g, sub = tid % g;
+            const bool own = e < nm;
+            const uint64_t me = own ? kept[lo + e] : 0ull;
+            uint32_t cnt = 0;
+            if (own) {
+                uint32_t j = sub;
+                for (; j + 3 * g < E; j += 4 * g)  // four loads in flight
+                    cnt += (uint32_t)(kept[j] < me) + (uint32_t)(kept[j + g] < me) + (uint32_t)(kept[j + 2 * g] < me) +
+                           (uint32_t)(kept[j + 3 * g] < me);
+                for (; j < E; j += g) cnt += kept[j] < me;
+            }
+            for (uint32_t o = 1; o < g; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if (own && sub == 0 && cnt < k2) {
+                out_ids[q * k + cnt] = (uint32_t)(me & 0xFFFFFFFFu);
+                out_dists[q * k + cnt] = unorderable((uint32_t)(me >> 32));
+            }
+        }
+        if (y == 0) {
+            for (uint32_t i = k2 + tid; i < k; i += blockDim.x) {
+                out_ids[q * k + i] = 0xFFFFFFFFu;
+                out_dists[q * k + i] = __uint_as_float(0x7F800000u);
+            }
+            if (tid == 0) out_counts[q] = k2;
+        }
+    } else if (E <= blockDim.x) {
         block_sort_write(kept, E, k2, k, q, out_ids, out_dists, out_counts);
     } else {  // a loose cut: select the top k2 of the kept keys first
         uint64_t a = ~0ull, o = 0ull;
