@@ -236,9 +236,47 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                 c2v[u] = f < LT ? __ldg(p.c2 + f * p.npairs + pi) : 0.0f;
         }
     }
-    // everything above reads the index only; the bin selection's ranges and the traversal's fine
-    // LUT are read below (a PDL dependent in a chained chunk starts before they are complete)
+    // the query's fine LUT (the traversal's) into shared memory, and T[f][t(i, j)] = (E, c2) for
+    // every pair i < j (linequant.cpp:76-82; other entries are never referenced; thread: one pair,
+    // every (blockDim / 128)-th part)
+    auto copy_fine = [&](bool l2_only) {
+        for (uint32_t i = tid; i < LT * K1M; i += blockDim.x) {
+            const uint32_t f = i / K1M, c = i % K1M;
+            const float* src = fine_in + q * LT * k1 + f * k1 + c;
+            fine[i] = c < k1 ? (l2_only ? __ldcg(src) : *src) : 0.0f;
+        }
+    };
+    auto build_T = [&] {
+        if (!DIRECT && pair_lane) {
+#pragma unroll
+            for (uint32_t u = 0; u < kFPer; ++u) {
+                const uint32_t f = f0 + u * kFLanes;
+                // the pair's T slot: its device code in part f (K1M = 16) or its pair id (K1M = 32)
+                const uint32_t ij = K1M == 16 ? slot[u] : pi;
+                if (f < LT) {
+                    const float b2 = fine[f * K1M + pi_i], a2 = fine[f * K1M + pi_j];
+                    if constexpr (CT) {
+                        Ct[f * TE + ij] = c2v[u];
+                    } else if constexpr (S2) {
+                        float* Et = reinterpret_cast<float*>(smem);
+                        Et[f * TE + ij] = __fsub_rn(__fsub_rn(a2, b2), c2v[u]);
+                        Et[LT * TE + f * TE + ij] = c2v[u];
+                    } else {
+                        T[f * TE + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
+                    }
+                }
+            }
+        }
+    };
+    // Everything above reads the index only; the bin selection's ranges are read below, after the
+    // wait of a PDL dependent (a chained chunk). The traversal's fine LUT is complete already: the
+    // bin selection's CTAs passed their own wait on it before this grid could launch, so a chained
+    // re-rank stages the LUT and builds T while the bin selection still runs (from L2: no L1 line
+    // of an earlier search's LUT).
     if (p.chain) {
+        copy_fine(true);
+        __syncthreads();
+        build_T();
         griddep_wait();
         griddep_launch();
     }
@@ -254,10 +292,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     // the scan and the select run over this shard's candidates only
     const bool clip = sharded && cached;
     const uint32_t y1 = clip && tid < R ? (tid + 1 < R ? __ldg(&qr[tid + 1].y) : C) : 0u;
-    for (uint32_t i = tid; i < LT * K1M; i += blockDim.x) {
-        const uint32_t f = i / K1M, c = i % K1M;
-        fine[i] = c < k1 ? fine_in[q * LT * k1 + f * k1 + c] : 0.0f;
-    }
+    if (!p.chain) copy_fine(false);
     const uint32_t Cpad = (C + kScanItems * kIjThreads - 1) / (kScanItems * kIjThreads) * (kScanItems * kIjThreads);
     for (uint32_t i = tid; i < Cpad / 2; i += blockDim.x) reinterpret_cast<uint32_t*>(rid)[i] = 0;
     if (tid == 0) {
@@ -306,28 +341,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
             if (cached) delta[r] = rg.x - rg.y;
         }
     }
-    // T[f][t(i, j)] = (E, c2) for every pair i < j (linequant.cpp:76-82); other entries
-    // are never referenced. Thread: one pair, every (blockDim / 128)-th part.
-    if (!DIRECT && pair_lane) {
-#pragma unroll
-        for (uint32_t u = 0; u < kFPer; ++u) {
-            const uint32_t f = f0 + u * kFLanes;
-            // the pair's T slot: its device code in part f (K1M = 16) or its pair id (K1M = 32)
-            const uint32_t ij = K1M == 16 ? slot[u] : pi;
-            if (f < LT) {
-                const float b2 = fine[f * K1M + pi_i], a2 = fine[f * K1M + pi_j];
-                if constexpr (CT) {
-                    Ct[f * TE + ij] = c2v[u];
-                } else if constexpr (S2) {
-                    float* Et = reinterpret_cast<float*>(smem);
-                    Et[f * TE + ij] = __fsub_rn(__fsub_rn(a2, b2), c2v[u]);
-                    Et[LT * TE + f * TE + ij] = c2v[u];
-                } else {
-                    T[f * TE + ij] = make_float2(__fsub_rn(__fsub_rn(a2, b2), c2v[u]), c2v[u]);
-                }
-            }
-        }
-    }
+    if (!p.chain) build_T();
     __syncthreads();
     PQTG_PHASE(1);
     range_index_scan<kIjThreads>(rid, Cn, wmax);
