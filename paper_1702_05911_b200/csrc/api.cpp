@@ -861,7 +861,7 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
             check_exact();
             return PQTG_OK;
         }
-        // Small batches write their results straight into the caller's page-locked buffers
+        // Small batches (<= zc_max) write their results straight into the caller's page-locked buffers
         // (mapped into the device's address space): the replayed graph is the query copy and the
         // three kernels, with no result copies behind them (PQTG_ZERO_COPY=0 disables).
         static const bool zero_copy = [] {
@@ -881,7 +881,13 @@ int pqtg_search(pqtg_index* index, pqtg_workspace* wsh, const float* queries, ui
         // (Zero-copy for larger batches -- queries read by the traversal and results written by the
         // re-rank straight over the link -- measured far slower: DEEP100M e2e 6.35 -> 4.25 M q/s,
         // the re-rank's scattered 4-byte result stores do not suit the link.)
-        const bool zc = zero_copy && nq <= 64 && nq <= ws.max_batch && (zc_out[0] || !ids) && (zc_out[1] || !dists) &&
+        // up to 128 queries (SIFT1M e2e, zero-copy vs copies: batch 100 78.4 vs 88.2 µs, batch 200
+        // 104.6 vs 94.0, batch 1000 232 vs 215); PQTG_ZC_MAX overrides for experiments
+        static const uint64_t zc_max = [] {
+            const char* e = std::getenv("PQTG_ZC_MAX");
+            return e ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)128;
+        }();
+        const bool zc = zero_copy && nq <= zc_max && nq <= ws.max_batch && (zc_out[0] || !ids) && (zc_out[1] || !dists) &&
                         zc_out[2] && (zc_out[3] || !stats);
         auto enqueue_zc = [&] {
             if (d.prm.exact_order) PQTG_CUDA_CHECK(cudaMemsetAsync(ws.err, 0, sizeof(uint32_t), st[0]));

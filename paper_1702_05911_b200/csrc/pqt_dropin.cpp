@@ -246,7 +246,7 @@ namespace {
 // page-locked staging for small batches (<= kStageMax queries): the search then replays a CUDA
 // graph that writes the results straight into these buffers (pqtg_search's zero-copy path), and
 // a serving loop of knn_query calls keeps hitting the same graph
-constexpr std::size_t kStageMax = 64;
+constexpr std::size_t kStageMax = 128;
 
 struct DeviceCopy {
     pqtg_index* ix = nullptr;

@@ -59,7 +59,7 @@ def test_workspace_calls_on_two_streams_and_both_entry_points():
 
 
 @pytest.mark.parametrize("name", ["p2_sift", "p4_gist", "p2_wide", "p2_exact"])
-@pytest.mark.parametrize("nq", [1, 5, 37, 300])
+@pytest.mark.parametrize("nq", [1, 5, 37, 100, 300])
 def test_small_batch_replays(name, nq):
     """Small batches: the device entry point captures its chained stages (PDL) as a CUDA graph on
     the second call with the same buffers and replays it after that; the host entry point replays
