@@ -71,6 +71,7 @@ WsSlice Workspace::slice(uint64_t q0) const {
     s.split_q = split_q;
     s.split_k = split_k;
     s.hash = hash ? hash + q0 * hash_stride : nullptr;
+    s.bscr = bscr ? bscr + q0 * bscr_stride : nullptr;
     s.scr = scr ? scr + q0 * p.P * p.scr_nj : nullptr;
     return s;
 }
@@ -536,6 +537,8 @@ int pqtg_workspace_create(const pqtg_index* index, uint64_t max_batch, pqtg_work
         ws->hash_stride = ws->hash_words ? std::max(binsel_hash_stride(p), binsel_par_hash_stride(p)) : 0;
         ws->hash_words = ws->hash_stride * B;
         if (ws->hash_words) ws->hash = dev_alloc<uint32_t>(ws->allocations, ws->hash_words);
+        ws->bscr_stride = binsel_scratch_stride(p);
+        if (ws->bscr_stride) ws->bscr = dev_alloc<uint64_t>(ws->allocations, B * ws->bscr_stride);
         if (screen_ok(p)) {
             ws->scr = dev_alloc<float>(ws->allocations, B * p.P * p.scr_nj);
         }

@@ -314,8 +314,6 @@ DevIndex* build_device_index(const Source& src, int device, uint64_t shard_lo, u
     const uint32_t npairs = k1 <= 1 ? 1u : k1 * (k1 - 1) / 2;
     const uint32_t pw = npairs <= 256 ? 1u : 2u;  // index_io.cpp:132
     if (npairs > 65536) unsupported("k1 too large for 16-bit pair ids");
-    if (c.resort_bins && std::min<uint64_t>(c.candidate_budget, n) > 4096)
-        unsupported("resort_bins with candidate budget > 4096");
     const uint64_t budget = std::min<uint64_t>(c.candidate_budget, n);
     if (budget > 65535) unsupported("candidate budget > 65535");
     if (shard_hi == 0 && shard_lo == 0) shard_hi = n;

@@ -338,26 +338,31 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                                                           uint32_t* __restrict__ ntuples,
                                                           pqtg_query_stats* __restrict__ stats,
                                                           uint32_t ts_log2, uint32_t heap_cap,
-                                                          uint32_t* __restrict__ err) {
+                                                          uint32_t* __restrict__ err,
+                                                          uint64_t* __restrict__ gscr, uint64_t gscr_stride) {
     using Sort = cub::BlockRadixSort<uint32_t, kThreads, ITEMS, uint32_t>;
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t PW_ = p.P * p.W;
     const uint32_t TS = 1u << ts_log2;
     const uint32_t shift = 32 - ts_log2;
+    const uint64_t q = blockIdx.x;
+    // gscr (large budgets): this query's scratch in the workspace -- the visited set [TS] (u32
+    // keys, u32 first positions) and, for resort batches longer than one chunk, two sort buffers
+    // and the exact order's batch of tuples, [budget] u64 each
+    uint64_t* gq = gscr ? gscr + q * gscr_stride : nullptr;
     uint64_t* terms = reinterpret_cast<uint64_t*>(smem);
     uint64_t* warp_sums = terms + PW_;
     float* dl = reinterpret_cast<float*>(warp_sums + 32);
-    uint32_t* hkeys = reinterpret_cast<uint32_t*>(dl + PW_);
+    uint32_t* hkeys = gq ? reinterpret_cast<uint32_t*>(gq) : reinterpret_cast<uint32_t*>(dl + PW_);
     uint32_t* hvals = hkeys + TS;
     // EXACT: this chunk's tuples, then the heap (8-byte aligned after the u32 tables)
-    uint64_t* tbuf = reinterpret_cast<uint64_t*>(
-        smem + (((size_t)(reinterpret_cast<unsigned char*>(hvals + TS) - smem) + 7) & ~size_t(7)));
+    unsigned char* after = reinterpret_cast<unsigned char*>(gq ? reinterpret_cast<uint32_t*>(dl + PW_) : hvals + TS);
+    uint64_t* tbuf = reinterpret_cast<uint64_t*>(smem + (((size_t)(after - smem) + 7) & ~size_t(7)));
     ExactHeap heap{reinterpret_cast<double*>(tbuf + kThreads * ITEMS), nullptr, heap_cap};
     heap.tup = reinterpret_cast<uint64_t*>(heap.sum + heap_cap);
     __shared__ uint32_t s_emitted, s_maxord, s_got, s_overflow, s_heap_n;
     __shared__ typename Sort::TempStorage sort_tmp;
 
-    const uint64_t q = blockIdx.x;
     if (p.chain) {  // the traversal's lists (a PDL dependent in a chained chunk)
         griddep_wait();
         griddep_launch();
@@ -404,6 +409,11 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         s_heap_n = n0;
     }
 
+    // a resort batch longer than one chunk sorts through the workspace (RESORT implies gq then)
+    uint64_t* srt_a = gq ? gq + TS : nullptr;
+    uint64_t* srt_b = srt_a ? srt_a + budget : nullptr;
+    uint64_t* tup = tbuf;  // the exact order's tuples of this chunk / batch
+    if (EXACT && RESORT && gq && budget > CH) tup = srt_b + budget;
     while (C < budget && base < total) {
         if constexpr (EXACT) {
             // this chunk's (or resort batch's) tuples, in order, from the heap
@@ -411,7 +421,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
             __syncthreads();
             if (tid == 0) {
                 uint32_t n = s_heap_n;
-                s_got = exact_fill(p, heap, n, dl, tbuf, want, &s_overflow);
+                s_got = exact_fill(p, heap, n, dl, tup, want, &s_overflow);
                 s_heap_n = n;
             }
             __syncthreads();
@@ -421,14 +431,19 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         uint64_t spos[ITEMS];
         bool inb[ITEMS];
         uint64_t step;
+        uint32_t nsub = 1;             // chunks of CH tuples this batch is processed in
+        const uint64_t* srt = nullptr;  // a long resort batch in order: (key << 32 | batch index)
+        uint64_t bs = 0;
         if (RESORT) {
             // one batch = the next `budget` tuples (search.cpp:153), stable-sorted by the
             // fp32 sum of their part distances (search.cpp:179-190)
-            const uint64_t bs = min((uint64_t)budget, total - base);
+            bs = min((uint64_t)budget, total - base);
+            if (bs > CH) nsub = (uint32_t)((bs + CH - 1) / CH);
+            for (uint32_t sc = 0; sc < nsub; ++sc) {
             uint32_t keys[ITEMS], vals[ITEMS];
 #pragma unroll
             for (int it = 0; it < ITEMS; ++it) {
-                const uint32_t o = tid * ITEMS + it;
+                const uint32_t o = sc * CH + tid * ITEMS + it;
                 vals[it] = o;
                 keys[it] = 0xFFFFFFFFu;
                 if (o < bs) {
@@ -436,7 +451,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                     // ranks of tuple s (recomputed; resort batches are budget-sized)
                     uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                     if (EXACT) {
-                        exact_ranks(p, tbuf[o], r);
+                        exact_ranks(p, tup[o], r);
                     } else if (p.P == 1) {
                         r[0] = (uint32_t)s;
                     } else if (p.P == 2) {
@@ -467,11 +482,46 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
             }
             Sort(sort_tmp).Sort(keys, vals);  // stable LSD radix sort, blocked arrangement
             __syncthreads();
+            if (nsub == 1) {
 #pragma unroll
-            for (int it = 0; it < ITEMS; ++it) {
-                const uint32_t o = tid * ITEMS + it;
-                inb[it] = o < bs;
-                spos[it] = base + vals[it];
+                for (int it = 0; it < ITEMS; ++it) {
+                    const uint32_t o = tid * ITEMS + it;
+                    inb[it] = o < bs;
+                    spos[it] = base + vals[it];
+                }
+            } else {  // the chunk's sorted run (its valid keys first: sentinels sort last, stably)
+#pragma unroll
+                for (int it = 0; it < ITEMS; ++it) {
+                    const uint32_t o = sc * CH + tid * ITEMS + it;
+                    if (o < bs) srt_a[o] = (uint64_t)keys[it] << 32 | vals[it];
+                }
+            }
+            }
+            if (nsub > 1) {
+                // merge the sorted runs pairwise: (key, batch index) pairs are distinct, so an
+                // element's place is its index in its run plus the count of smaller elements in
+                // the partner run (the stable sort's order)
+                __syncthreads();
+                uint64_t* src = srt_a;
+                uint64_t* dst = srt_b;
+                for (uint64_t w = CH; w < bs; w *= 2) {
+                    for (uint32_t e = tid; e < bs; e += kThreads) {
+                        const uint64_t key = src[e];
+                        const uint64_t r = e / w, lo = e - r * w, pb = (r ^ 1) * w;
+                        uint64_t a = pb, b = pb < bs ? min(pb + w, bs) : pb;
+                        while (a < b) {
+                            const uint64_t m = (a + b) >> 1;
+                            if (src[m] < key) a = m + 1;
+                            else b = m;
+                        }
+                        dst[(r & ~1ull) * w + lo + (a - pb)] = key;
+                    }
+                    __syncthreads();
+                    uint64_t* t = src;
+                    src = dst;
+                    dst = t;
+                }
+                srt = src;
             }
             step = bs;
         } else {
@@ -483,6 +533,16 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
             step = CH;
         }
 
+        for (uint32_t sc = 0; sc < nsub && C < budget; ++sc) {
+        const uint64_t obase = base + (uint64_t)sc * CH;  // processing-order position of the chunk
+        if (srt) {
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) {
+                const uint64_t o = (uint64_t)sc * CH + tid * ITEMS + it;
+                inb[it] = o < bs;
+                spos[it] = base + (inb[it] ? (uint32_t)srt[o] : 0u);
+            }
+        }
         // slot, emptiness and first-occurrence bookkeeping
         uint32_t slot[ITEMS], hidx[ITEMS];
         bool ne[ITEMS];
@@ -495,7 +555,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                 uint64_t sl;
                 if constexpr (EXACT) {
                     uint32_t r[8];
-                    exact_ranks(p, tbuf[spos[it] - base], r);
+                    exact_ranks(p, tup[spos[it] - base], r);
                     sl = slot_of_ranks(p, r, terms);
                 } else {
                     sl = tuple_slot(p, spos[it], ta, tb, terms);
@@ -505,7 +565,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
             }
             if (ne[it]) {
                 // Empty slots need no dedup: a repeat of an empty slot is empty again.
-                const uint32_t ord = (uint32_t)(base + tid * ITEMS + it);
+                const uint32_t ord = (uint32_t)(obase + tid * ITEMS + it);
                 uint32_t h = hash_slot(slot[it], shift);
                 for (;;) {
                     const uint32_t prev = atomicCAS(hkeys + h, kEmptyKey, slot[it]);
@@ -527,8 +587,9 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
             cnt[it] = 0;
             start[it] = 0;
             if (ne[it]) {
-                const uint32_t ord = (uint32_t)(base + tid * ITEMS + it);
-                if (hvals[hidx[it]] == ord) {  // first occurrence in processing order
+                const uint32_t ord = (uint32_t)(obase + tid * ITEMS + it);
+                const uint32_t first = gq ? __ldcg(hvals + hidx[it]) : hvals[hidx[it]];  // global: its atomics live in L2
+                if (first == ord) {  // first occurrence in processing order
                     start[it] = __ldg(p.offsets + slot[it]);
                     cnt[it] = __ldg(p.offsets + slot[it] + 1) - start[it];
                 }
@@ -547,7 +608,7 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
                     const uint32_t r = R + (uint32_t)(excl & 0xFFFFFFFFu);
                     qranges[r] = make_uint2(start[it], (uint32_t)before_c);
                     ++emitted;
-                    maxord = max(maxord, (uint32_t)(base + tid * ITEMS + it));
+                    maxord = max(maxord, (uint32_t)(obase + tid * ITEMS + it));
                 }
                 excl += ((uint64_t)cnt[it] << 32) | 1u;
             }
@@ -560,8 +621,9 @@ __global__ void __launch_bounds__(kThreads) binsel_kernel(DevParams p, const flo
         R += s_emitted;
         const uint64_t newc = (uint64_t)C + (tot >> 32);
         C = newc < budget ? (uint32_t)newc : budget;
-        base += step;
         __syncthreads();
+        }
+        base += step;
     }
     if (tid == 0) {
         nranges[q] = R;
@@ -592,9 +654,19 @@ uint32_t ts_log2_for(const DevParams& p) {
 }
 }  // namespace
 
-size_t binsel_smem(const DevParams& p) {
-    const uint64_t TS = 1ull << ts_log2_for(p);
+size_t binsel_smem(const DevParams& p, bool global_visited) {
+    const uint64_t TS = global_visited ? 0 : 1ull << ts_log2_for(p);
     return (size_t)p.P * p.W * (8 + 4) + TS * 8 + 32 * 8;
+}
+
+// u64 words of workspace scratch per query for the generic bin selection (0: none): the visited
+// set when it does not fit shared memory, plus the sort buffers of resort batches longer than
+// one chunk (budget > 4096) -- see binsel_kernel
+uint64_t binsel_scratch_stride(const DevParams& p) {
+    if (binsel_fast_ok(p)) return 0;
+    const bool big_resort = p.resort && p.budget > 16u * kThreads;
+    if (!big_resort && binsel_smem(p, false) + 2048 <= (size_t)optin_bytes()) return 0;
+    return (1ull << ts_log2_for(p)) + (big_resort ? 3ull * p.budget : 0ull);
 }
 
 void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_query_stats* stats,
@@ -610,10 +682,10 @@ void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_quer
         return;
     }
     const uint32_t lg = ts_log2_for(p);
-    const size_t sm = binsel_smem(p);
-    if (sm + 2048 > (size_t)optin_bytes())
-        throw Error{PQTG_ERR_UNSUPPORTED, "bin selection's visited set does not fit shared memory at this budget "
-                                          "(resort_bins, exact bin order or the generic kernel)"};
+    const uint64_t gstride = binsel_scratch_stride(p);
+    if (gstride && !ws.bscr) throw Error{PQTG_ERR_ARG, "bin selection scratch missing from the workspace"};
+    uint64_t* gscr = gstride ? ws.bscr : nullptr;
+    const size_t sm = binsel_smem(p, gstride != 0);
     if (p.exact_order) {
         // the exact order's heap takes the rest of the opt-in shared memory (<= 64 Ki entries)
         const uint32_t ch = (p.resort ? 16u : 4u) * kThreads;
@@ -630,16 +702,16 @@ void launch_binsel(const DevParams& p, uint64_t nq, const WsSlice& ws, pqtg_quer
         const size_t smx = fixed + (size_t)cap * 16;
         if (p.resort)
             launch_kernel(p.chain, binsel_kernel<16, true, true>, dim3((unsigned)nq), dim3(kThreads), smx, s, 
-                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap, ws.err);
+                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap, ws.err, gscr, gstride);
         else
             launch_kernel(p.chain, binsel_kernel<4, false, true>, dim3((unsigned)nq), dim3(kThreads), smx, s, 
-                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap, ws.err);
+                p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, cap, ws.err, gscr, gstride);
     } else if (p.resort) {
         launch_kernel(p.chain, binsel_kernel<16, true, false>, dim3((unsigned)nq), dim3(kThreads), sm, s, 
-            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0, ws.err);
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0, ws.err, gscr, gstride);
     } else {
         launch_kernel(p.chain, binsel_kernel<4, false, false>, dim3((unsigned)nq), dim3(kThreads), sm, s, 
-            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0, ws.err);
+            p, ws.l2_dist, ws.l2_code, ws.slope, ws.ranges, ws.nranges, ws.ncand, ws.ntuples, stats, lg, 0, ws.err, gscr, gstride);
     }
     PQTG_CUDA_CHECK(cudaGetLastError());
 }

@@ -172,6 +172,7 @@ struct WsSlice {
     float* scr = nullptr;         // [q][P][scr_nj] tensor-core dot products (screen.cu)
     uint32_t* err = nullptr;      // the workspace's device error word (PQTG_WS_ERR_*), shared by all slices
     uint64_t* keys = nullptr;     // [q][budget] candidate keys when they do not fit shared memory, or null
+    uint64_t* bscr = nullptr;     // [q][binsel_scratch_stride] generic bin selection scratch, or null
     // small batches: the split re-rank's per-(query, slice) top-k keys [q][kSplitMax][split_k], their
     // counts [q][kSplitMax] and per-query arrival counters [q] (zero between calls)
     uint64_t* split_keys = nullptr;
@@ -217,6 +218,8 @@ struct Workspace {
     uint32_t* hash = nullptr;     // [B << ts_log2] visited slots, cleared on use (binsel_fast.cu)
     uint64_t hash_words = 0;
     uint64_t hash_stride = 0;     // words per query
+    uint64_t* bscr = nullptr;     // [B][bscr_stride] (binsel_scratch_stride), or null
+    uint64_t bscr_stride = 0;
     cudaStream_t aux_stream = nullptr;  // second stream of the pipelined searches
     uint32_t chunks = 0;                // sub-batch chunks per search (0 = automatic)
     cudaEvent_t join = nullptr;
@@ -325,7 +328,8 @@ void validate_config(const pqtg_config& c);
 
 // ---------------------------------------------------------------- kernels (kernels.cu)
 size_t traverse_smem(const DevParams& p);
-size_t binsel_smem(const DevParams& p);
+size_t binsel_smem(const DevParams& p, bool global_visited = false);
+uint64_t binsel_scratch_stride(const DevParams& p);  // u64 words per query of ws.bscr (0: none)
 size_t rerank_smem(const DevParams& p, uint32_t k, bool gkeys = false);
 void launch_traverse(const DevParams& p, const float* queries, uint64_t nq, const WsSlice& ws,
                      cudaStream_t s);

@@ -5,7 +5,9 @@ indexes the reference builds (pqtref IndexBuilder, search.cpp:52-117) and writes
 * k1 = 1: the single pair (0, 0) and lambda = 0 (linequant.cpp:72-74, 96-100);
 * W = w·k2 = 1 (one child per part list);
 * an empty index, n = 0 (search.cpp:130-132);
-* candidate budgets above 4096 (8192, 16384; search.cpp:153, 166-217);
+* candidate budgets above 4096 (8192, 16384; search.cpp:153, 166-217), also with resort_bins,
+  whose budget-sized batches (search.cpp:153, 179-190) are then longer than one 4096-tuple chunk
+  (heuristic P = 2 and the exact order at P = 3);
 * SPEC.md acceptance criterion 2, "full-coverage degeneracy": w = k1, budget >= n,
   rerank_exact >= k  =>  knn_query equals brute_force_knn id for id (n = 5000, D in {16, 64, 128});
 * a 1M-vector SIFT-shaped index built by the reference.
@@ -76,6 +78,25 @@ def test_gpu_large_budget(tmp_path, budget):
         want = ref.knn(Q, k)
         assert_same_results(got, want, f"budget {budget} k={k}")
     assert want[3][:, 1].max() > budget // 2  # the large-budget path (keys in the workspace at 16384) ran
+
+
+@pytest.mark.parametrize("p_tree,k2,w,budget", [(2, 16, 8, 8192), (2, 16, 8, 16384), (3, 8, 4, 8192)])
+def test_gpu_resort_large_budget(tmp_path, p_tree, k2, w, budget):
+    """resort_bins with a batch of `budget` tuples (W^P > budget > 4096): the batch is sorted
+    through the workspace (binsel_kernel's merge of 4096-tuple runs) and gathered chunk by chunk."""
+    dim = 96 if p_tree == 3 else 128
+    cfg = PqtConfig(dim=dim, p_tree=p_tree, k1=16, k2=k2, w=w, p_line=dim // 4, train_iters=6, seed=budget + p_tree,
+                    candidate_budget=budget, resort_bins=True, rerank_exact=0)
+    db = clustered(60_000, dim, 128, 21)
+    Q = clustered(48, dim, 128, 22)
+    path, ref = ref_index(tmp_path, f"rs{p_tree}_{budget}", cfg, db, 20_000)
+    dev = DeviceIndex(path)
+    assert (w * k2) ** p_tree > budget
+    for k in (10, 300):
+        got = dev.search(Q, k)
+        want = ref.knn(Q, k)
+        assert_same_results(got, want, f"resort P={p_tree} budget {budget} k={k}")
+    assert want[3][:, 1].max() > 4096  # candidates beyond the first chunk
 
 
 @pytest.mark.parametrize("dim", [16, 64, 128])
