@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                      uint64_t* __restrict__ split_keys,
                      uint32_t* __restrict__ split_ctr) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE == 1 || MODE == 2, S2 = MODE == 3;
+    constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE == 1 || MODE == 2, S2 = MODE == 3, COOP = MODE == 4;
     const uint32_t k1 = p.k1, budget = p.budget;
     constexpr uint32_t TE = t_entries(K1M);
     const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr, CT);
@@ -370,6 +370,58 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
             for (int i = 0; i < kVec; ++i) v[i] = __ldg(r4 + i);
         }
     };
+    // COOP: a warp's 32 code rows are read kVec lanes per row (each row's kVec 16-byte pieces in
+    // one load instruction, 32 / kVec rows per instruction: 32 / kVec lines per load instead of
+    // 32), then transposed by shuffles so every lane holds its own candidate's row. Lane
+    // l = kVec·g + u loads, in round r, piece (u − r) mod kVec of the warp's candidate
+    // (32 / kVec)·r + g; in shuffle round s every lane m receives piece s of its candidate from
+    // lane kVec·(m mod 32/kVec) + (s + m / (32/kVec)) mod kVec, which sends its round (u − s) mod
+    // kVec value (the sources of one shuffle round are distinct). issue() starts the loads,
+    // finish() runs the shuffles one candidate later, so the loads stay in flight over a score.
+    constexpr uint32_t kRowsPer = 32 / kVec;  // rows per load round
+    auto issue = [&](uint32_t j, uint32_t jlim, uint4* x, uint32_t& id) {
+        uint32_t lp = kInvalid;
+        id = kInvalid;
+        if (j < jlim) {
+            const uint32_t r = rid[j];
+            uint64_t pos;
+            if (cached) {
+                pos = (uint32_t)(delta[r] + j);
+            } else {
+                const uint2 rl = __ldg(qr + r);
+                pos = (uint64_t)rl.x + (j - rl.y);
+            }
+            if (clip || (pos >= p.shard_lo && pos < p.shard_hi)) {
+                lp = (uint32_t)(pos - p.shard_lo);
+                id = __ldg(p.ids + lp);
+            }
+        }
+        const uint32_t lane = tid & 31, g = lane / kVec, u = lane % kVec;
+#pragma unroll
+        for (uint32_t r = 0; r < kVec; ++r) {
+            const uint32_t slp = __shfl_sync(0xffffffffu, lp, kRowsPer * r + g);
+            x[r] = slp != kInvalid ? __ldg(reinterpret_cast<const uint4*>(p.codes + (uint64_t)slp * p.row_bytes) +
+                                           ((u + kVec - r) % kVec))
+                                   : make_uint4(0, 0, 0, 0);
+        }
+    };
+    auto finish = [&](const uint4* x, uint4* v) {
+        const uint32_t lane = tid & 31, u = lane % kVec;
+        const uint32_t src0 = kVec * (lane % kRowsPer), rr = lane / kRowsPer;
+#pragma unroll
+        for (uint32_t s = 0; s < kVec; ++s) {
+            const uint32_t want = (u + kVec - s) % kVec;
+            uint4 snd = x[0];
+#pragma unroll
+            for (uint32_t r = 1; r < kVec; ++r)
+                if (want == r) snd = x[r];
+            const uint32_t src = src0 + (s + rr) % kVec;
+            v[s].x = __shfl_sync(0xffffffffu, snd.x, src);
+            v[s].y = __shfl_sync(0xffffffffu, snd.y, src);
+            v[s].z = __shfl_sync(0xffffffffu, snd.z, src);
+            v[s].w = __shfl_sync(0xffffffffu, snd.w, src);
+        }
+    };
     // one candidate's line distance -> its (dist, id) key
     auto score = [&](uint32_t j, const uint4* v, uint32_t id) {
         uint64_t key = kSentinel;
@@ -516,6 +568,19 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         for (uint32_t u = tid; u < jn; u += step) {
             fetch(y_ + u * S_, va, ida);
             score(kb + u, va, ida);
+        }
+    } else if (COOP && S_ == 1) {
+        // warp-uniform trip count (every lane takes part in the shuffles); a lane past the end
+        // scores nothing
+        uint4 x[kVec], v[kVec];
+        uint32_t idn = kInvalid, id = kInvalid;
+        const uint32_t lane = tid & 31;
+        if (tid - lane < jn) issue(tid, jn, x, idn);
+        for (uint32_t j = tid; j - lane < jn; j += step) {
+            finish(x, v);
+            id = idn;
+            if (j + step - lane < jn) issue(j + step, jn, x, idn);
+            if (j < jn) score(j, v, id);
         }
     } else if (S_ == 1) {  // one CTA per query (the throughput path): candidate u is candidate u
         uint4 va[kVec], vb[kVec];
@@ -753,6 +818,7 @@ int ij_mode() {
         if (e && std::strcmp(e, "packed") == 0) return 1;
         if (e && std::strcmp(e, "c3") == 0) return 2;
         if (e && std::strcmp(e, "split") == 0) return 3;
+        if (e && std::strcmp(e, "coop") == 0) return 4;
         return 0;
     }();
     return mode;
@@ -829,6 +895,9 @@ void configure_rerank_ij() {
     allow<32, 16, false, 3>(optin);
     allow<64, 16, false, 3>(optin);
     allow<32, 16, false, 2>(optin);
+    allow<16, 16, false, 4>(optin);
+    allow<32, 16, false, 4>(optin);
+    allow<64, 16, false, 4>(optin);
     allow<64, 16, false, 2>(optin);
     allow<16, 32>(optin);
     allow<32, 32>(optin);
@@ -935,6 +1004,12 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
         case 16: PQTG_IJ(16, 16, false, 2); break;
         case 32: PQTG_IJ(32, 16, false, 2); break;
         default: PQTG_IJ(64, 16, false, 2); break;
+        }
+    } else if (ij_mode() == 4) {
+        switch (p.L) {
+        case 16: PQTG_IJ(16, 16, false, 4); break;
+        case 32: PQTG_IJ(32, 16, false, 4); break;
+        default: PQTG_IJ(64, 16, false, 4); break;
         }
     } else if (ij_mode() == 3) {
         switch (p.L) {
