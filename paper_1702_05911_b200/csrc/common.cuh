@@ -41,6 +41,13 @@ __device__ __forceinline__ float sq_step(float acc, float a, float b) {
 }
 
 // fp32 -> u32 preserving order (with -0.0 folded onto +0.0 so it ties like operator<).
+// one 256-bit read-only global load (sm_100: LDG.E.ENL2.256), p 32-byte aligned
+__device__ __forceinline__ void ldg256(const void* p, uint4& a, uint4& b) {
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(p));
+}
+
 __device__ __forceinline__ uint32_t orderable(float x) {
     uint32_t u = __float_as_uint(x);
     if (u == 0x80000000u) u = 0u;

@@ -349,6 +349,8 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     constexpr int kVec = ((K1M == 16 ? 2 : 3) * LT + 15) / 16;
+    // 256-bit row loads (MODE 5, PQTG_RERANK=narrow, keeps the 16-byte ones for comparison)
+    constexpr bool kWide = MODE != 5;
     uint32_t mine = 0;
     uint32_t kand = ~0u, kor = 0u;  // AND / OR of this thread's orderable distances
     // candidate j's code row and id, fetched one iteration ahead (software pipelining)
@@ -366,8 +368,15 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
             const uint64_t lp = pos - p.shard_lo;
             id = __ldg(p.ids + lp);
             const uint4* r4 = reinterpret_cast<const uint4*>(p.codes + lp * p.row_bytes);
+            if constexpr (kVec % 2 == 0 && kWide) {
+                // rows of a multiple of 32 bytes: 32-byte loads, half the load instructions (and
+                // L1 wavefronts) of 16-byte ones
 #pragma unroll
-            for (int i = 0; i < kVec; ++i) v[i] = __ldg(r4 + i);
+                for (int i = 0; i < kVec; i += 2) ldg256(r4 + i, v[i], v[i + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kVec; ++i) v[i] = __ldg(r4 + i);
+            }
         }
     };
     // COOP: a warp's 32 code rows are read kVec lanes per row (each row's kVec 16-byte pieces in
@@ -819,6 +828,7 @@ int ij_mode() {
         if (e && std::strcmp(e, "c3") == 0) return 2;
         if (e && std::strcmp(e, "split") == 0) return 3;
         if (e && std::strcmp(e, "coop") == 0) return 4;
+        if (e && std::strcmp(e, "narrow") == 0) return 5;
         return 0;
     }();
     return mode;
@@ -898,6 +908,9 @@ void configure_rerank_ij() {
     allow<16, 16, false, 4>(optin);
     allow<32, 16, false, 4>(optin);
     allow<64, 16, false, 4>(optin);
+    allow<16, 16, false, 5>(optin);
+    allow<32, 16, false, 5>(optin);
+    allow<64, 16, false, 5>(optin);
     allow<64, 16, false, 2>(optin);
     allow<16, 32>(optin);
     allow<32, 32>(optin);
@@ -1004,6 +1017,12 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
         case 16: PQTG_IJ(16, 16, false, 2); break;
         case 32: PQTG_IJ(32, 16, false, 2); break;
         default: PQTG_IJ(64, 16, false, 2); break;
+        }
+    } else if (ij_mode() == 5) {
+        switch (p.L) {
+        case 16: PQTG_IJ(16, 16, false, 5); break;
+        case 32: PQTG_IJ(32, 16, false, 5); break;
+        default: PQTG_IJ(64, 16, false, 5); break;
         }
     } else if (ij_mode() == 4) {
         switch (p.L) {
