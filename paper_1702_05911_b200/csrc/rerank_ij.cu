@@ -349,8 +349,10 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
 
     const float inv255 = __uint_as_float(0x3B808081u);  // 1.0f / 255.0f (linequant.cpp:175)
     constexpr int kVec = ((K1M == 16 ? 2 : 3) * LT + 15) / 16;
-    // 256-bit row loads (MODE 5, PQTG_RERANK=narrow, keeps the 16-byte ones for comparison)
+    // 256-bit row loads (MODE 5, PQTG_RERANK=narrow, keeps the 16-byte loads and the I2F of
+    // round 2's measurements for comparison)
     constexpr bool kWide = MODE != 5;
+    constexpr bool I2F = MODE == 5 || MODE == 6;  // MODE 6 (PQTG_RERANK=i2f): 256-bit loads, λ by I2F
     uint32_t mine = 0;
     uint32_t kand = ~0u, kor = 0u;  // AND / OR of this thread's orderable distances
     // candidate j's code row and id, fetched one iteration ahead (software pipelining)
@@ -472,7 +474,17 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                 } else {
                     ec = T[f * TE + ti];
                 }
-                const float lam = __fmul_rn(__uint2float_rn(lq), inv255);
+                float qf;  // λq as a float: exact either way (q <= 255)
+                if constexpr (I2F) {
+                    qf = __uint2float_rn(lq);
+                } else {
+                    // one byte permute builds 2^23 + q (0x4B0000qq) from the code word, one FADD
+                    // removes 2^23: no I2F on the quarter-rate conversion pipe
+                    const uint32_t bsel = K1M == 16 ? (0x7540u | ((f & 1) * 2)) : (0x7540u | (f & 3));
+                    const uint32_t src = K1M == 16 ? w[f >> 1] : w[f >> 2];
+                    qf = __fsub_rn(__uint_as_float(__byte_perm(src, 0x4B000000u, bsel)), 8388608.0f);
+                }
+                const float lam = __fmul_rn(qf, inv255);
                 const float part = __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), ec.y)), __fmul_rn(lam, ec.x));
                 total = __fadd_rn(total, part);
             }
@@ -829,6 +841,7 @@ int ij_mode() {
         if (e && std::strcmp(e, "split") == 0) return 3;
         if (e && std::strcmp(e, "coop") == 0) return 4;
         if (e && std::strcmp(e, "narrow") == 0) return 5;
+        if (e && std::strcmp(e, "i2f") == 0) return 6;
         return 0;
     }();
     return mode;
@@ -911,6 +924,9 @@ void configure_rerank_ij() {
     allow<16, 16, false, 5>(optin);
     allow<32, 16, false, 5>(optin);
     allow<64, 16, false, 5>(optin);
+    allow<16, 16, false, 6>(optin);
+    allow<32, 16, false, 6>(optin);
+    allow<64, 16, false, 6>(optin);
     allow<64, 16, false, 2>(optin);
     allow<16, 32>(optin);
     allow<32, 32>(optin);
@@ -1017,6 +1033,12 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
         case 16: PQTG_IJ(16, 16, false, 2); break;
         case 32: PQTG_IJ(32, 16, false, 2); break;
         default: PQTG_IJ(64, 16, false, 2); break;
+        }
+    } else if (ij_mode() == 6) {
+        switch (p.L) {
+        case 16: PQTG_IJ(16, 16, false, 6); break;
+        case 32: PQTG_IJ(32, 16, false, 6); break;
+        default: PQTG_IJ(64, 16, false, 6); break;
         }
     } else if (ij_mode() == 5) {
         switch (p.L) {
