@@ -949,8 +949,9 @@ def main():
     peak, peak_src = peaks()
     limiter = {"traverse": "issue (IPC ~3.5, sequential fp32 chains + level-2 sort)",
                "binsel": "latency / L2-probe throughput per pass (issue active ~22-60%)",
-               "rerank": "L1 data pipe (90% of peak: shared-memory table gathers at 2.3x their ideal wavefronts "
-                         "on DEEP) + issue (~15.5 SASS per part); profiles/r02/rerank_packed_ab.md"}
+               "rerank": "L1 data pipe (~76% of peak with 256-bit row loads; 3/4 of its wavefronts are the "
+                         "shared-memory table gathers) + issue (~76% active, ~15.5 SASS per part); "
+                         "profiles/r02/wide/, profiles/r02/rerank_packed_ab.md"}
     if args.shard:
         # this rank's block is 1/world of the batch for traversal + bin selection (ntuples are
         # counted on the block only; bins on the whole batch, so the block figure is an upper bound)
