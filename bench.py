@@ -1,16 +1,16 @@
 #!/usr/bin/env python
 """bench.py — PQT online-query throughput on B200 (queries/s), one JSON line on rank 0.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload gist1m|sift1m|deep10m]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload deep100m|sift1m|gist1m|sift1b|...]
     python bench.py --impl reference ...      # the reference's own CPU path (oracle/_ref)
 
 A step = one pass of the hot path (traverse → bin selection/gather → line-quantized re-rank →
-top-k) over one query batch of the workload. Default workload = BASELINE.json configs[1]
-(GIST1M-shaped: 1M × 960-D, P=4, 1k queries, top-100). Data are synthetic clustered vectors
-(the reference's synth_clustered distribution) and an index trained/encoded on the GPU by
-paper_1702_05911_b200.builder (the reference's exact assign_bin / encode_line / inverted-list
-layout); the same index feeds every arm. The index (≈ 85 MB of HBM for gist1m) fits in L2,
-so L2 is flushed (256 MiB write) between timed steps, outside the timed intervals.
+top-k) over one query batch of the workload. Default workload at N=1 = BASELINE.json configs[2]
+(DEEP100M-shaped: 100M × 96-D, P=2, 10k queries, top-100): synthetic clustered vectors (the
+reference's synth_clustered distribution) and an index BUILT BY THE REFERENCE (pqtref
+IndexBuilder, keep_raw=false) and written as a PQTINDEX file, which the GPU reads through
+pqtg_index_load. The index (7.3 GB) is far larger than L2; L2 is still flushed (256 MiB write)
+between timed steps, outside the timed intervals.
 
   value        device-resident: queries already in HBM, pqtg_search_device on the current
                stream, CUDA events around each step, summed over K steps, max over ranks.
@@ -20,8 +20,10 @@ so L2 is flushed (256 MiB write) between timed steps, outside the timed interval
                 ÷ its mean launch time, against MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline the reference compiled in place (oracle/_ref; else the C restatement) on this
                host's cores over the same batch, with a parity check of the GPU results.
-Multi-GPU (torchrun): every rank holds a replica and processes its own batches (no data-path
-collective): "scaling": "weak".
+Multi-GPU (torchrun, N > 1): the default is SIFT1B (configs[3]) over N inverted-list position
+shards with the query-partitioned NCCL protocol (csrc/sharded.cpp): "scaling":
+"strong" (the 1B index and the batch are fixed; each rank holds 1/N of the positions and runs
+1/N of the traversal / bin selection).
 """
 from __future__ import annotations
 
@@ -734,8 +736,8 @@ def main():
     ap.add_argument("--exact", action="store_true",
                     help="attach the raw base vectors: the exact re-rank stage runs (rerank_exact = 64)")
     ap.add_argument("--shard", action="store_true",
-                    help="shard the index's positions over the ranks (NCCL broadcast + all-gather + "
-                         "merge; sharded.py) instead of one replica per rank")
+                    help="shard the index's positions over the ranks (query-partitioned protocol over "
+                         "NCCL, csrc/sharded.cpp) instead of one replica per rank")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
