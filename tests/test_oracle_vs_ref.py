@@ -19,6 +19,7 @@ CONFIGS = [
     dict(dim=60, p_tree=2, k1=30, k2=4, w=5, p_line=20, candidate_budget=800),   # pair width 2
     dict(dim=32, p_tree=2, k1=1, k2=4, w=1, p_line=8, candidate_budget=100),    # k1 == 1
     dict(dim=32, p_tree=2, k1=4, k2=1, w=1, p_line=8, candidate_budget=100),    # W == 1
+    dict(dim=64, p_tree=2, k1=16, k2=16, w=8, p_line=16, candidate_budget=6000, resort_bins=True),  # resort batch > 4096
 ]
 
 
