@@ -352,7 +352,9 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     // 256-bit row loads (MODE 5, PQTG_RERANK=narrow, keeps the 16-byte loads and the I2F of
     // round 2's measurements for comparison)
     constexpr bool kWide = MODE != 5;
-    constexpr bool I2F = MODE == 5 || MODE == 6;  // MODE 6 (PQTG_RERANK=i2f): 256-bit loads, λ by I2F
+    // λq by I2F; MODE 6 (PQTG_RERANK=prmt) builds 2^23 + q with a byte permute and removes 2^23
+    // with an FADD instead (measured slower: DEEP100M 1223 -> 1231 us, SIFT1M 1074 -> 1105 us)
+    constexpr bool I2F = MODE != 6;
     uint32_t mine = 0;
     uint32_t kand = ~0u, kor = 0u;  // AND / OR of this thread's orderable distances
     // candidate j's code row and id, fetched one iteration ahead (software pipelining)
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                     qf = __uint2float_rn(lq);
                 } else {
                     // one byte permute builds 2^23 + q (0x4B0000qq) from the code word, one FADD
-                    // removes 2^23: no I2F on the quarter-rate conversion pipe
+                    // removes 2^23: no I2F (one more instruction per part than I2F.U8)
                     const uint32_t bsel = K1M == 16 ? (0x7540u | ((f & 1) * 2)) : (0x7540u | (f & 3));
                     const uint32_t src = K1M == 16 ? w[f >> 1] : w[f >> 2];
                     qf = __fsub_rn(__uint_as_float(__byte_perm(src, 0x4B000000u, bsel)), 8388608.0f);
@@ -841,7 +843,7 @@ int ij_mode() {
         if (e && std::strcmp(e, "split") == 0) return 3;
         if (e && std::strcmp(e, "coop") == 0) return 4;
         if (e && std::strcmp(e, "narrow") == 0) return 5;
-        if (e && std::strcmp(e, "i2f") == 0) return 6;
+        if (e && std::strcmp(e, "prmt") == 0) return 6;
         return 0;
     }();
     return mode;
