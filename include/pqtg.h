@@ -28,7 +28,8 @@
  * There is no CPU fallback: configurations the GPU path does not implement (p_tree > 8; an
  * exact-order tuple wider than 64 bits; an exact Dijkstra-order frontier larger than the
  * shared-memory heap -- src/binorder.cpp:114-167, used for p_tree not in {1,2,4} or without
- * slope tables) return PQTG_ERR_UNSUPPORTED.
+ * slope tables; a candidate budget above 65535) return PQTG_ERR_UNSUPPORTED. resort_bins runs at
+ * every budget up to that (batches longer than 4096 tuples are sorted through the workspace).
  */
 #ifndef PQTG_H
 #define PQTG_H
