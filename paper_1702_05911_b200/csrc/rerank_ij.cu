@@ -165,7 +165,7 @@ __device__ inline void range_index_scan(uint16_t* rid, uint32_t C, uint32_t* wma
 // distinct pairs over 32 banks instead of the 16 bank pairs of an 8-byte one). Modes 1 and 2 use
 // the c2-table layout (CT).
 template <int LT, int K1M, bool DIRECT, int MODE = 0>
-__global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 64 || K1M == 32) ? 1 : 2))
+__global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 64 || K1M == 32 || MODE == 7) ? 1 : 2))
     rerank_ij_kernel(DevParams p, uint32_t k, uint32_t sel_cap, const float* __restrict__ fine_in,
                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ nranges,
                      const uint32_t* __restrict__ ncand, uint32_t* __restrict__ out_ids,
@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
                      uint64_t* __restrict__ split_keys,
                      uint32_t* __restrict__ split_ctr) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE == 1 || MODE == 2, S2 = MODE == 3, COOP = MODE == 4;
+    constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE == 1 || MODE == 2, S2 = MODE == 3, COOP = MODE == 4,
+                   HALF = MODE == 8 && K1M == 16 && LT == 32 && !DIRECT;
     const uint32_t k1 = p.k1, budget = p.budget;
     constexpr uint32_t TE = t_entries(K1M);
     const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr, CT);
@@ -592,6 +593,87 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
             fetch(y_ + u * S_, va, ida);
             score(kb + u, va, ida);
         }
+    } else if (HALF && S_ == 1) {
+        // HALF (MODE 8, K1M = 16, L = 32): each 64-byte row in two 32-byte halves with three
+        // half-row buffers in rotation: the next row's first half loads before this row's first
+        // 16 parts, its second half (into the buffer just consumed) before the last 16 -- 24
+        // registers of row buffers instead of 32, left to the scheduler for shared-memory loads
+        auto rowptr = [&](uint32_t j, uint32_t& id) -> const uint4* {
+            const uint32_t r = rid[j];
+            uint64_t pos;
+            if (cached) {
+                pos = (uint32_t)(delta[r] + j);
+            } else {
+                const uint2 rl = __ldg(qr + r);
+                pos = (uint64_t)rl.x + (j - rl.y);
+            }
+            id = kInvalid;
+            if (clip || (pos >= p.shard_lo && pos < p.shard_hi)) {
+                const uint64_t lp = pos - p.shard_lo;
+                id = __ldg(p.ids + lp);
+                return reinterpret_cast<const uint4*>(p.codes + lp * p.row_bytes);
+            }
+            return nullptr;
+        };
+        auto acc16 = [&](const uint4* h, float total, const int fbase) -> float {
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(h);
+#pragma unroll
+            for (int ff = 0; ff < 16; ++ff) {
+                const int f = fbase + ff;
+                const uint32_t half = w[ff >> 1] >> ((ff & 1) * 16);
+                const uint32_t ti = (half >> 8) & 0xFFu, fi = ti >> 4, lq = half & 0xFFu;
+                const float b2 = fine[f * K1M + fi];
+                const float2 ec = T[f * TE + ti];
+                const float lam = __fmul_rn(__uint2float_rn(lq), inv255);
+                total = __fadd_rn(total, __fadd_rn(__fadd_rn(b2, __fmul_rn(__fmul_rn(lam, lam), ec.y)), __fmul_rn(lam, ec.x)));
+            }
+            return total;
+        };
+        // one candidate: F / S its row halves, N the next row's first half; the next row's second
+        // half goes to F once F is scored. Returns whether there is a next candidate.
+        auto iter = [&](uint32_t j, uint4* F, uint4* S, uint4* N, uint32_t id, uint32_t& idn) -> bool {
+            const bool more = j + step < jn;
+            const uint4* nrow = nullptr;
+            idn = kInvalid;
+            if (more) {
+                nrow = rowptr(j + step, idn);
+                if (nrow) ldg256(nrow, N[0], N[1]);
+            }
+            float total = 0.0f;
+            if (id != kInvalid) total = acc16(F, total, 0);
+            if (nrow) ldg256(nrow + 2, F[0], F[1]);
+            uint64_t key = kSentinel;
+            if (id != kInvalid) {
+                total = acc16(S, total, 16);
+                const uint32_t od = orderable(total);
+                key = ((uint64_t)od << 32) | id;
+                kand &= od;
+                kor |= od;
+                ++mine;
+            }
+            keys[j] = key;
+            return more;
+        };
+        uint4 A[2], B[2], Cb[2];
+        uint32_t id = kInvalid, idn = kInvalid;
+        if (tid < jn) {
+            const uint4* row = rowptr(tid, id);
+            if (row) {
+                ldg256(row, A[0], A[1]);
+                ldg256(row + 2, B[0], B[1]);
+            }
+            for (uint32_t j = tid;;) {
+                if (!iter(j, A, B, Cb, id, idn)) break;
+                j += step;
+                id = idn;
+                if (!iter(j, Cb, A, B, id, idn)) break;
+                j += step;
+                id = idn;
+                if (!iter(j, B, Cb, A, id, idn)) break;
+                j += step;
+                id = idn;
+            }
+        }
     } else if (COOP && S_ == 1) {
         // warp-uniform trip count (every lane takes part in the shuffles); a lane past the end
         // scores nothing
@@ -844,6 +926,8 @@ int ij_mode() {
         if (e && std::strcmp(e, "coop") == 0) return 4;
         if (e && std::strcmp(e, "narrow") == 0) return 5;
         if (e && std::strcmp(e, "prmt") == 0) return 6;
+        if (e && std::strcmp(e, "onecta") == 0) return 7;  // one CTA per SM, up to 128 registers
+        if (e && std::strcmp(e, "half") == 0) return 8;    // half-row buffers in rotation
         return 0;
     }();
     return mode;
@@ -929,6 +1013,8 @@ void configure_rerank_ij() {
     allow<16, 16, false, 6>(optin);
     allow<32, 16, false, 6>(optin);
     allow<64, 16, false, 6>(optin);
+    allow<32, 16, false, 7>(optin);
+    allow<32, 16, false, 8>(optin);
     allow<64, 16, false, 2>(optin);
     allow<16, 32>(optin);
     allow<32, 32>(optin);
@@ -1036,6 +1122,10 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
         case 32: PQTG_IJ(32, 16, false, 2); break;
         default: PQTG_IJ(64, 16, false, 2); break;
         }
+    } else if (ij_mode() == 8 && p.L == 32) {
+        PQTG_IJ(32, 16, false, 8);
+    } else if (ij_mode() == 7 && p.L == 32) {
+        PQTG_IJ(32, 16, false, 7);
     } else if (ij_mode() == 6) {
         switch (p.L) {
         case 16: PQTG_IJ(16, 16, false, 6); break;
