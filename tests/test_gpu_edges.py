@@ -81,7 +81,8 @@ def test_gpu_large_budget(tmp_path, budget):
 
 
 @pytest.mark.parametrize("p_tree,k2,w,budget,resort", [(2, 16, 8, 8192, True), (2, 16, 8, 16384, True),
-                                                      (3, 8, 4, 8192, True), (3, 8, 4, 16384, False)])
+                                                      (3, 8, 4, 8192, True), (3, 8, 4, 16384, False),
+                                                      (2, 32, 8, 65535, True)])
 def test_gpu_resort_large_budget(tmp_path, p_tree, k2, w, budget, resort):
     """resort_bins with a batch of `budget` tuples (W^P > budget > 4096): the batch is sorted
     through the workspace (binsel_kernel's merge of 4096-tuple runs) and gathered chunk by chunk.
@@ -89,7 +90,7 @@ def test_gpu_resort_large_budget(tmp_path, p_tree, k2, w, budget, resort):
     dim = 96 if p_tree == 3 else 128
     cfg = PqtConfig(dim=dim, p_tree=p_tree, k1=16, k2=k2, w=w, p_line=dim // 4, train_iters=6, seed=budget + p_tree,
                     candidate_budget=budget, resort_bins=resort, rerank_exact=0)
-    db = clustered(60_000, dim, 128, 21)
+    db = clustered(max(60_000, budget + 20_000), dim, 128, 21)
     Q = clustered(48, dim, 128, 22)
     path, ref = ref_index(tmp_path, f"rs{p_tree}_{budget}_{resort}", cfg, db, 20_000)
     dev = DeviceIndex(path)
