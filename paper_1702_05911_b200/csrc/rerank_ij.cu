@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool PK = MODE == 1, C3 = MODE == 2, CT = MODE == 1 || MODE == 2, S2 = MODE == 3, COOP = MODE == 4,
                    HALF = MODE == 8 && K1M == 16 && LT == 32 && !DIRECT;
+    // GRP: the final top-k ranks each kept key within its radix bin only (MODE 9, PQTG_RERANK=grouped)
+    constexpr bool GRP = MODE == 9;
     const uint32_t k1 = p.k1, budget = p.budget;
     constexpr uint32_t TE = t_entries(K1M);
     const IjLayout lay = ij_layout(LT, budget, sel_cap, K1M, DIRECT, gkeys != nullptr, CT);
@@ -735,12 +737,19 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     if (kk) {
         for (uint32_t i = tid; i < (1u << kSelBits); i += blockDim.x) hist[i] = 0;
         __syncthreads();
-        m = block_select_wide<kSelBits, kIjThreads>(keys + kb, jn, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap,
-                                                    wmax, s_sel);
+        if (GRP && gridDim.y == 1)
+            m = block_select_wide<kSelBits, kIjThreads, true>(keys + kb, jn, kk, s_sel.kand, s_sel.kor, hist, sel,
+                                                              sel_cap, wmax, s_sel);
+        else
+            m = block_select_wide<kSelBits, kIjThreads>(keys + kb, jn, kk, s_sel.kand, s_sel.kor, hist, sel, sel_cap,
+                                                        wmax, s_sel);
     }
     PQTG_PHASE(4);
     if (gridDim.y == 1) {
-        block_sort_write(sel, m, kk, k, q, out_ids, out_dists, out_counts);
+        if (GRP && kk && s_sel.grouped)
+            block_sort_write_grouped<kSelBits>(sel, m, kk, k, q, hist, s_sel.shift, out_ids, out_dists, out_counts);
+        else
+            block_sort_write(sel, m, kk, k, q, out_ids, out_dists, out_counts);
         PQTG_PHASE(5);
         qt_end(p, q, 2);
         return;
@@ -928,6 +937,7 @@ int ij_mode() {
         if (e && std::strcmp(e, "prmt") == 0) return 6;
         if (e && std::strcmp(e, "onecta") == 0) return 7;  // one CTA per SM, up to 128 registers
         if (e && std::strcmp(e, "half") == 0) return 8;    // half-row buffers in rotation
+        if (e && std::strcmp(e, "grouped") == 0) return 9;  // top-k ranked within radix bins
         return 0;
     }();
     return mode;
@@ -1015,6 +1025,7 @@ void configure_rerank_ij() {
     allow<64, 16, false, 6>(optin);
     allow<32, 16, false, 7>(optin);
     allow<32, 16, false, 8>(optin);
+    allow<32, 16, false, 9>(optin);
     allow<64, 16, false, 2>(optin);
     allow<16, 32>(optin);
     allow<32, 32>(optin);
@@ -1122,6 +1133,8 @@ void launch_rerank_ij(const DevParams& p, uint64_t nq, uint32_t k, const WsSlice
         case 32: PQTG_IJ(32, 16, false, 2); break;
         default: PQTG_IJ(64, 16, false, 2); break;
         }
+    } else if (ij_mode() == 9 && p.L == 32) {
+        PQTG_IJ(32, 16, false, 9);
     } else if (ij_mode() == 8 && p.L == 32) {
         PQTG_IJ(32, 16, false, 8);
     } else if (ij_mode() == 7 && p.L == 32) {

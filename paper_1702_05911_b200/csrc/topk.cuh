@@ -13,6 +13,7 @@ namespace dev {
 struct TopkShared {
     uint32_t nsel, digit, before, bucket;
     unsigned long long kand, kor;
+    uint32_t grouped, shift;  // block_select_wide<GROUP>: sel is grouped by digit, hist[b] = end of digit b
 };
 
 // Radix select over keys[0..C) given the AND / OR of its valid keys (bits shared by every
@@ -87,7 +88,7 @@ __device__ inline void block_select(const uint64_t* keys, uint32_t C, uint32_t k
 // bin holding the kk-th smallest key; every key in that bin or below — m >= kk keys, usually
 // only a few more than kk — is collected into sel[0..m). When m would exceed sel_cap, it falls
 // back to the exact 8-bit select (m = kk). Returns m; all threads call it.
-template <int BITS, int THREADS>
+template <int BITS, int THREADS, bool GROUP = false>
 __device__ inline uint32_t block_select_wide(const uint64_t* keys, uint32_t C, uint32_t kk, uint64_t kand,
                                              uint64_t kor, uint32_t* hist, uint64_t* sel, uint32_t sel_cap,
                                              uint32_t* wsum, TopkShared& sh) {
@@ -149,9 +150,25 @@ __device__ inline uint32_t block_select_wide(const uint64_t* keys, uint32_t C, u
     const uint32_t m = sh.before + sh.bucket;
     if (m > sel_cap) {  // a crowded bin: exact select instead
         const uint32_t kk2 = kk;
+        if (GROUP && tid == 0) sh.grouped = 0;
         __syncthreads();
         block_select(keys, C, kk2, kand, kor, sel, sel_cap, hist, sh);
         return kk2;
+    }
+    if constexpr (GROUP) {
+        // the kept keys are placed grouped by digit: each bin's counter becomes its start (the
+        // exclusive scan), and a key's slot is its bin's counter, post-incremented
+        uint32_t acc = excl;
+#pragma unroll
+        for (uint32_t b = 0; b < per; ++b) {
+            hist[tid * per + b] = acc;
+            acc += h[b];
+        }
+        if (tid == 0) {
+            sh.grouped = 1;
+            sh.shift = (uint32_t)shift;
+        }
+        __syncthreads();
     }
     const uint64_t top = ((kand & (hb >= 63 ? 0ull : (~0ull << (hb + 1)))) >> shift) | sh.digit;
     for (uint32_t j0 = tid; j0 < C; j0 += 4 * blockDim.x) {
@@ -163,10 +180,40 @@ __device__ inline uint32_t block_select_wide(const uint64_t* keys, uint32_t C, u
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (kv[u] != kSentinel && (kv[u] >> shift) <= top) sel[atomicAdd(&sh.nsel, 1u)] = kv[u];
+            if (kv[u] != kSentinel && (kv[u] >> shift) <= top) {
+                if constexpr (GROUP) sel[atomicAdd(&hist[(kv[u] >> shift) & (NB - 1)], 1u)] = kv[u];
+                else sel[atomicAdd(&sh.nsel, 1u)] = kv[u];
+            }
     }
     __syncthreads();
     return m;
+}
+
+// block_sort_write for a selection grouped by digit (block_select_wide<GROUP>, sh.grouped): after
+// the placement hist[b] is the end of bin b's keys in sel and hist[b - 1] its start, and every key
+// of a lower bin is smaller, so a key's rank is its bin's start plus the count of smaller keys in
+// its own bin -- a few compares instead of a count over all m keys.
+template <int BITS>
+__device__ inline void block_sort_write_grouped(const uint64_t* sel, uint32_t m, uint32_t kk, uint32_t k, uint64_t q,
+                                                const uint32_t* hist, uint32_t shift, uint32_t* out_ids,
+                                                float* out_dists, uint32_t* out_counts) {
+    constexpr uint32_t NB = 1u << BITS;
+    for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
+        const uint64_t me = sel[p];
+        const uint32_t b = (uint32_t)(me >> shift) & (NB - 1);
+        const uint32_t s = b ? hist[b - 1] : 0u, e = hist[b];
+        uint32_t rank = s;
+        for (uint32_t j = s; j < e; ++j) rank += sel[j] < me;
+        if (rank < kk) {
+            out_ids[q * k + rank] = (uint32_t)(me & 0xFFFFFFFFu);
+            out_dists[q * k + rank] = unorderable((uint32_t)(me >> 32));
+        }
+    }
+    for (uint32_t i = kk + threadIdx.x; i < k; i += blockDim.x) {
+        out_ids[q * k + i] = 0xFFFFFFFFu;
+        out_dists[q * k + i] = __uint_as_float(0x7F800000u);
+    }
+    if (threadIdx.x == 0) out_counts[q] = kk;
 }
 
 // Bitonic sort of sel[0..kk) (padded with kSentinel to a power of two <= sel_cap).
