@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
     if (kk) {
         for (uint32_t i = tid; i < (1u << kSelBits); i += blockDim.x) hist[i] = 0;
         __syncthreads();
-        if (GRP && gridDim.y == 1)
+        if (GRP)
             m = block_select_wide<kSelBits, kIjThreads, true>(keys + kb, jn, kk, s_sel.kand, s_sel.kor, hist, sel,
                                                               sel_cap, wmax, s_sel);
         else
@@ -766,7 +766,8 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         // and after a second barrier (no slice's memory is read any more) each one cuts the lists
         // the same way and ranks 1/S of the kept keys (below)
         const uint32_t y = blockIdx.y;
-        block_rank_keys(sel, m, kk, keys + y * k);
+        if (GRP && kk && s_sel.grouped) block_rank_keys_grouped<kSelBits>(sel, m, kk, hist, s_sel.shift, keys + y * k);
+        else block_rank_keys(sel, m, kk, keys + y * k);
         for (uint32_t i = kk + tid; i < k; i += blockDim.x) keys[y * k + i] = kSentinel;
         PQTG_PHASE(5);
         cg::cluster_group cl = cg::this_cluster();
@@ -779,7 +780,8 @@ __global__ void __launch_bounds__(ij_threads(LT, DIRECT), DIRECT ? 4 : ((LT >= 6
         cl.sync();
     } else {
         uint64_t* lst = split_keys + ((uint64_t)q * kSplitMax + blockIdx.y) * k;
-        block_rank_keys(sel, m, kk, lst);
+        if (GRP && kk && s_sel.grouped) block_rank_keys_grouped<kSelBits>(sel, m, kk, hist, s_sel.shift, lst);
+        else block_rank_keys(sel, m, kk, lst);
         for (uint32_t i = kk + tid; i < k; i += blockDim.x) lst[i] = kSentinel;
         PQTG_PHASE(5);
         __threadfence();

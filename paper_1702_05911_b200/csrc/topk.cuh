@@ -193,6 +193,21 @@ __device__ inline uint32_t block_select_wide(const uint64_t* keys, uint32_t C, u
 // the placement hist[b] is the end of bin b's keys in sel and hist[b - 1] its start, and every key
 // of a lower bin is smaller, so a key's rank is its bin's start plus the count of smaller keys in
 // its own bin -- a few compares instead of a count over all m keys.
+// block_rank_keys for a selection grouped by digit: the kk smallest keys to out[0..kk) in order
+template <int BITS>
+__device__ inline void block_rank_keys_grouped(const uint64_t* sel, uint32_t m, uint32_t kk, const uint32_t* hist,
+                                               uint32_t shift, uint64_t* out) {
+    constexpr uint32_t NB = 1u << BITS;
+    for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
+        const uint64_t me = sel[p];
+        const uint32_t b = (uint32_t)(me >> shift) & (NB - 1);
+        const uint32_t s = b ? hist[b - 1] : 0u, e = hist[b];
+        uint32_t rank = s;
+        for (uint32_t j = s; j < e; ++j) rank += sel[j] < me;
+        if (rank < kk) out[rank] = me;
+    }
+}
+
 template <int BITS>
 __device__ inline void block_sort_write_grouped(const uint64_t* sel, uint32_t m, uint32_t kk, uint32_t k, uint64_t q,
                                                 const uint32_t* hist, uint32_t shift, uint32_t* out_ids,
